@@ -1,0 +1,374 @@
+#!/usr/bin/env python
+"""Benchmark of the grid-resistance hot path (skyline + descending-g scan).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C2]
+                    [--impl ours|reference] [--scaling weak|strong]
+
+One STEP = one pass of the hot path over one seeded synthetic relation:
+parallel_skyline of the n tuples, then grid_resistance of every skyline tuple
+(proj/src/harness.cpp:208, :229-231).  Default workload C2 (BASELINE.json
+configs[1]: anti-correlated n=1,000,000, d=3, seed 1, cap 25, angular p=16).
+
+value  = skyline tuples whose resistance was computed per second, whole job,
+         inputs resident in HBM (device-event timed, max over ranks).
+e2e    = the same metric through the public C-ABI call with pinned HOST
+         buffers: H2D of the relation + ids and D2H of positions + denominators
+         inside the timed region (host clock around the synchronous call).
+--impl reference times the unmodified reference library (oracle/_ref,
+compiled from /root/reference by oracle/build_ref.sh) on all host cores.
+Timing: W untimed warm-up steps, then K steps, each bracketed by CUDA events
+on the stream the kernels run on; L2 is flushed (256 MiB write) before every
+timed step because the C2 relation (32 MB) fits in the 126 MB L2.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (generator, n, d, seed, strategy, target partitions, cap)
+    "C1": ("uni", 100_000, 4, 1, "sliced", 16, 25),
+    "C2": ("ant", 1_000_000, 3, 1, "angular", 16, 25),
+    "C3": ("corr", 1_000_000, 6, 1, "sliced", 16, 25),
+    "C4": ("uni", 10_000_000, 5, 1, "angular", 64, 25),
+    "C5p10k": ("ant", 10_000, 7, 1, "angular", 64, 25),
+    "C5p20k": ("ant", 20_000, 7, 1, "angular", 64, 25),
+}
+METRIC = "grid-resistance skyline tuples/sec"
+UNIT = "skyline tuples/s"
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ------------------------------------------------------------- reference arm
+def run_reference_cpu(wl, repeat, cores=0):
+    """Time the unmodified reference (oracle/_ref/refdrive, release build) —
+    the CPU baseline.  Falls back to the C oracle port when it was not built."""
+    from oracle import pyoracle as po
+    gen, n, d, seed, strat, p, cap = WORKLOADS[wl]
+    exe = po.refdrive_path(release=True)
+    ncores = os.cpu_count() or 1
+    if exe:
+        cmd = [exe, "--mode", "bench", "--gen", gen, "--n", str(n), "--d", str(d), "--seed",
+               str(seed), "--strategy", strat, "--p", str(p), "--cap", str(cap), "--cores",
+               str(cores or ncores), "--repeat", str(repeat)]
+        r = json.loads(subprocess.check_output(cmd, text=True))
+        step_ms = r["skyline_ms_mean"] + r["gres_ms_mean"]
+        return {"kind": "reference", "cores": r["cores"], "step_ms": step_ms, "S": r["skyline_size"],
+                "detail": r}
+    v = po.generate(gen, n, d, seed)
+    t0 = time.perf_counter()
+    for _ in range(repeat):
+        pos, _ = po.skyline_sfs(v)
+        po.grid_resistance(v[pos], pos, cap)
+    step_ms = (time.perf_counter() - t0) * 1e3 / repeat
+    return {"kind": "port", "cores": 1, "step_ms": step_ms, "S": len(pos), "detail": {}}
+
+
+def reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    wl = args.workload
+    # warm-up runs are discarded; K timed runs (one step = one full pass)
+    if args.warmup:
+        run_reference_cpu(wl, 1)
+    r = run_reference_cpu(wl, max(1, args.steps))
+    value = r["S"] / (r["step_ms"] / 1e3)
+    gen, n, d, seed, strat, p, cap = WORKLOADS[wl]
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["step_ms"],
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference generator, seeded)",
+        "config": {"workload": f"{wl}: {gen} n={n} d={d} seed={seed}, {strat} p={p}, cap={cap}",
+                   "cores": r["cores"], "cpu": cpu_model()},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": r["cores"], "kind": r["kind"],
+                         "sample": f"full {wl} workload x{args.steps}"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "reference_detail": r["detail"],
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------- clocks
+class ClockSampler:
+    def __init__(self, device_index):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._t = None
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.ok = False
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+            "hw_power_brake_slowdown": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def start(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+
+    def stop(self):
+        if self._t:
+            self._stop.set()
+            self._t.join()
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "samples": len(self.samples),
+                "reasons": sorted(self.reasons)}
+
+
+# ------------------------------------------------------------------ our arm
+def our_arm(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2412_02274_b200 as sk
+    from paper_2412_02274_b200 import skypar
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    skypar.set_device(local)
+    stream = torch.cuda.current_stream(dev)
+    skypar.set_stream(stream.cuda_stream)
+
+    gen, n, d, seed, strat, p, cap = WORKLOADS[args.workload]
+    strong = args.scaling == "strong"
+    my_seed = seed if (strong or world == 1) else seed + rank  # weak: one instance per rank
+    host = sk.generate(gen, n, d, my_seed)
+    ids_host = np.arange(n, dtype=np.int64)
+    plan = sk.make_plan(strat, p, d)
+    vals_d = torch.from_numpy(host).to(dev)
+    ids_d = torch.from_numpy(ids_host).to(dev)
+    pos_d = torch.empty(n, dtype=torch.int64, device=dev)
+    den_d = torch.empty(n, dtype=torch.int32, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    shard_rank, shard_world = (rank, world) if strong else (0, 1)
+
+    def step_device():
+        S, gm, st = skypar.pipeline_raw(vals_d.data_ptr(), ids_d.data_ptr(), n, d, plan, cap,
+                                        args.engine, shard_rank, shard_world, skypar.DEVICE_PTRS,
+                                        pos_d.data_ptr(), den_d.data_ptr())
+        if strong and world > 1:  # NCCL max-reduce of the sharded denominators
+            dist.all_reduce(den_d[:S], op=dist.ReduceOp.MAX)
+        return S, gm, st
+
+    for _ in range(args.warmup):
+        step_device()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    times, stats = [], []
+    S = gm = 0
+    for _ in range(args.steps):
+        flush.zero_()  # L2 flush outside the timed region
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        S, gm, st = step_device()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1))
+        stats.append(st)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+
+    total_ms = sum(times)
+    units = S if strong else S * 1  # per rank
+    t = torch.tensor([total_ms, float(units)], dtype=torch.float64, device=dev)
+    if world > 1:
+        tmax = t.clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        tsum = t.clone()
+        dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
+        total_ms = float(tmax[0])
+        units_all = float(t[1]) if strong else float(tsum[1])
+    else:
+        units_all = float(units)
+    ms_per_step = total_ms / args.steps
+    value = units_all / (ms_per_step / 1e3)
+
+    # ---- e2e through the public API with pinned host buffers
+    skypar.set_stream(None)
+    pin_vals = torch.from_numpy(host).pin_memory()
+    pin_ids = torch.from_numpy(ids_host).pin_memory()
+    out_pos = torch.empty(n, dtype=torch.int64).pin_memory()
+    out_den = torch.empty(n, dtype=torch.int32).pin_memory()
+
+    def step_e2e():
+        S2, _, _ = skypar.pipeline_raw(pin_vals.data_ptr(), pin_ids.data_ptr(), n, d, plan, cap,
+                                       args.engine, shard_rank, shard_world, 0,
+                                       out_pos.data_ptr(), out_den.data_ptr())
+        if strong and world > 1:
+            t_den = torch.from_numpy(out_den.numpy()[:S2]).to(dev)
+            dist.all_reduce(t_den, op=dist.ReduceOp.MAX)
+            out_den[:S2].copy_(t_den.cpu())
+        return S2
+
+    for _ in range(max(1, args.warmup)):
+        step_e2e()
+    e2e_times = []
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        step_e2e()
+        e2e_times.append((time.perf_counter() - t0) * 1e3)
+    e2e_ms = sum(e2e_times) / len(e2e_times)
+    if world > 1:
+        te = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e_ms = float(te[0])
+    e2e_value = units_all / (e2e_ms / 1e3)
+
+    # ---- roofline of the dominant kernel (live CUDA-event launch times)
+    sky_ms = sum(s["ms_sky_kernel"] for s in stats) / len(stats)
+    gres_ms = sum(s["ms_gres_kernel"] for s in stats) / len(stats)
+    st0 = stats[-1]
+    roof = roofline(st0, sky_ms, gres_ms, d, clk)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded reference generators, bit-exact)",
+        "config": {"workload": f"{args.workload}: {gen} n={n} d={d} seed={seed}"
+                               f"{'' if strong or world == 1 else '+rank'}, {strat} p={p}, cap={cap}",
+                   "skyline_size": S, "g_max": gm, "l2": "flushed (256 MiB write) before each step",
+                   "parallelism": f"{'sharded gres + NCCL max' if strong else 'independent instance'}"
+                                  f" per GPU x{world}",
+                   "gres_engine": {0: "auto", 1: "pairs", 2: "cells"}[args.engine]},
+        "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": n * d * 8 + n * 8,
+                "d2h_bytes_per_step": S * 4 + S * 4},
+        "gpu_launches": int(sum(s["kernel_launches"] for s in stats)),
+        "roofline": roof,
+        "clocks": clk,
+        "stage_ms": {"skyline": st0["ms_skyline"], "gres": st0["ms_gres"],
+                     "sky_kernels": sky_ms, "gres_kernels": gres_ms},
+        "tests": {"skyline": st0["skyline_tests"], "gres": st0["gres_tests"],
+                  "sfs_rounds": st0["sfs_rounds"], "gres_steps": st0["gres_steps"],
+                  "code_bits": st0["code_bits"]},
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            r = run_reference_cpu(args.workload, args.cpu_repeat)
+            line["cpu_baseline"] = {"value": r["S"] / (r["step_ms"] / 1e3), "unit": UNIT,
+                                    "cores": r["cores"], "kind": r["kind"],
+                                    "sample": f"full {args.workload} workload x{args.cpu_repeat} "
+                                              f"({r['step_ms']:.1f} ms/step, {cpu_model()})"}
+        except Exception as e:  # pragma: no cover
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "port",
+                                    "sample": f"unavailable: {e}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def roofline(st, sky_ms, gres_ms, d, clk):
+    """Compare roofline of the dominant dominance kernel:
+    R = N_SM * f_clk * L_pipe / I_test.  float64 path: I_test = 2d DSETP on
+    the FP64 pipe (64 lanes/clk/SM); u8 SWAR path: I_test = 5 integer ops on
+    the ALU pipe (64 lanes/clk/SM).  f_clk = median SM clock sampled during
+    the timed region (else the 1965 MHz max)."""
+    f = (clk.get("sm_mhz") or 1965.0) * 1e6
+    if gres_ms > sky_ms and st["gres_kernel_launches"]:
+        kern = "k_gres_pairs_u8" if st["code_bits"] == 8 else "k_gres_pairs_f64"
+        tests, ms, launches = st["gres_tests"], gres_ms, st["gres_kernel_launches"]
+        i_test, l_pipe = (5, 64) if st["code_bits"] == 8 else (2 * d, 64)
+    else:
+        kern = "k_sfs_intra+k_sfs_filter"
+        tests, ms, launches = st["skyline_tests"], sky_ms, st["sky_kernel_launches"]
+        i_test, l_pipe = 2 * d, 64
+    peak = 148 * f * l_pipe / i_test
+    achieved = tests / (ms / 1e3) if ms > 0 else 0.0
+    return {"bound": "compare", "kernel": kern, "achieved": achieved / 1e9, "peak": peak / 1e9,
+            "unit": "Gtests/s", "frac": achieved / peak if peak else None, "traffic": None,
+            "tests_per_step": tests, "kernel_ms_per_step": ms, "launches_per_step": launches,
+            "I_test": i_test, "L_pipe": l_pipe, "f_clk_mhz": f / 1e6}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="C2", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--engine", type=int, default=0)
+    ap.add_argument("--cpu-repeat", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        return reference_arm(args)
+    return our_arm(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

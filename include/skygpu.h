@@ -1,0 +1,160 @@
+/*
+ * skygpu.h — C-ABI of the B200-native grid-resistance engine (libskygpu.so).
+ *
+ * The reference (arXiv 2412.02274 `skypar`, /root/reference/proj) has no FFI:
+ * its hot path is a set of C++ free functions in namespace skypar.  Each entry
+ * point below is the flat, exception-free form of one of them; the C++ drop-in
+ * adapter (paper_2412_02274_b200/adapter/skypar_gpu.cpp) re-wraps them into the
+ * exact reference signatures and re-throws the same exception type and text.
+ *
+ *   skygpu_parallel_skyline    <- skypar::parallel_skyline   include/skypar/parallel.hpp:46-47
+ *   skygpu_grid_resistance     <- skypar::grid_resistance    include/skypar/gres.hpp:73-75
+ *   skygpu_snap_relation       <- skypar::snap_relation      include/skypar/gres.hpp:28
+ *                                 (and snap_to_grid, gres.hpp:26 = a 1-tuple relation)
+ *   skygpu_max_grid_intervals  <- skypar::max_grid_intervals include/skypar/gres.hpp:35
+ *   skygpu_make_plan           <- skypar::make_plan          include/skypar/partition.hpp:43
+ *   skygpu_pipeline            <- the composition run_experiment performs
+ *                                 (proj/src/harness.cpp:208 then :229-231)
+ *
+ * Conventions
+ *  - Values are float64, row-major n x d (tuple i = vals[i*d .. i*d+d-1]),
+ *    smaller is better, non-negative (Relation::add, core.cpp:8-19); NaN is
+ *    rejected.  Ids are int64 and must be unique.
+ *  - Buffers are caller-owned.  Unless a function says otherwise pointers are
+ *    HOST pointers (pinned memory makes the copies faster); skygpu_pipeline
+ *    also accepts device pointers (flag SKYGPU_DEVICE_PTRS).
+ *  - Every function returns a status; on failure a NUL-terminated message is
+ *    written into err[0..errlen) (err may be NULL).  No exception crosses the ABI.
+ *  - Calls are not re-entrant per device; one host thread drives a device.
+ *  - There is NO CPU fallback: without a usable sm_100 device every compute
+ *    entry point fails with SKYGPU_ECUDA.
+ */
+#ifndef SKYGPU_H
+#define SKYGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define SKYGPU_OK 0
+#define SKYGPU_EINVAL 1   /* the reference throws std::invalid_argument */
+#define SKYGPU_ERUNTIME 2 /* the reference throws std::runtime_error */
+#define SKYGPU_ECUDA 3    /* CUDA error or no usable device */
+#define SKYGPU_ENOMEM 4   /* device allocation failed */
+
+/* strategies, numbered as skypar::Strategy (partition.hpp:21) */
+#define SKYGPU_NONE 0
+#define SKYGPU_GRID 1
+#define SKYGPU_ANGULAR 2
+#define SKYGPU_SLICED 3
+
+/* gres engines */
+#define SKYGPU_GRES_AUTO 0  /* pair-dominance kernel unless the cell engine is far cheaper */
+#define SKYGPU_GRES_PAIRS 1 /* (tuple, comparator, step) dominance tests, early exit */
+#define SKYGPU_GRES_CELLS 2 /* per-step occupancy prefix-OR over the code grid */
+
+/* skygpu_pipeline flags */
+#define SKYGPU_DEVICE_PTRS 1u   /* vals/ids/outputs are device pointers */
+#define SKYGPU_CHECK_SKYLINE 2u /* O(S^2) "input is a skyline" check (gres.cpp:70-80, !NDEBUG) */
+#define SKYGPU_SKIP_GRES 4u     /* skyline only (harness mode "skyline") */
+
+/* mirrors skypar::PartitionPlan (partition.hpp:27-32) */
+typedef struct skygpu_plan {
+    int strategy;
+    int slices;
+    long long partitions;
+    int dims;
+} skygpu_plan;
+
+/* counters and device-event timings of one call */
+typedef struct skygpu_stats {
+    uint64_t tuples_in;            /* n */
+    uint64_t tuples_into_parallel; /* after grid-cell pruning / rep filtering */
+    uint64_t tuples_into_final;    /* candidates entering the merge */
+    uint64_t skyline_size;         /* S */
+    uint64_t skyline_tests;        /* dominance tests executed by the skyline kernels */
+    uint64_t gres_tests;           /* (candidate, comparator, g) code tests executed */
+    uint64_t gres_cells;           /* cells swept by the cell engine */
+    int g_max;                     /* ResistanceMetrics::g_max (gres.hpp:46) */
+    int gres_steps;                /* interval counts scanned (g_max-1 or fewer) */
+    int gres_engine;               /* engine actually used */
+    int code_bits;                 /* 8 = packed u8 codes, 64 = float64 projections */
+    int sfs_rounds;                /* block-SFS rounds */
+    int pad_;
+    double ms_total;               /* device time of the whole call (events) */
+    double ms_h2d, ms_skyline, ms_gres, ms_d2h;
+    double ms_gres_kernel;         /* summed time of the dominant gres kernel launches */
+    double ms_sky_kernel;          /* summed time of the dominant skyline kernel launches */
+    uint64_t gres_kernel_launches;
+    uint64_t sky_kernel_launches;
+    uint64_t kernel_launches;      /* all of libskygpu's kernel launches in the call */
+} skygpu_stats;
+
+/* library / device */
+int skygpu_version(void);
+int skygpu_device_count(void);
+int skygpu_set_device(int device, char* err, size_t errlen);
+/* bind subsequent calls on the current device to a caller stream (NULL = the
+ * library's own non-blocking stream) */
+int skygpu_set_stream(void* cuda_stream, char* err, size_t errlen);
+/* release cached device buffers of the current device */
+int skygpu_release(void);
+
+/* partition.hpp:43 make_plan */
+int skygpu_make_plan(int strategy, long long target_partitions, int dims, skygpu_plan* out,
+                     char* err, size_t errlen);
+
+/* parallel.hpp:46-47 parallel_skyline.
+ * out_pos[0..*out_n) receives the INPUT POSITIONS of the skyline tuples in the
+ * reference's output order ((sum, id) ascending); out_pos must hold n entries.
+ * rep_vals/rep_ids: the RepresentativeSet tuples (may be NULL when n_reps = 0). */
+int skygpu_parallel_skyline(const double* vals, const int64_t* ids, uint64_t n, int d,
+                            const skygpu_plan* plan, const double* rep_vals,
+                            const int64_t* rep_ids, uint64_t n_reps, int cores,
+                            uint64_t* out_pos, uint64_t* out_n, skygpu_stats* stats, char* err,
+                            size_t errlen);
+
+/* gres.hpp:73-75 grid_resistance over a skyline of s tuples.
+ * out_den[i] = resistance denominator of input tuple i (1 or g in [2, g_max]);
+ * cap <= 0 means no cap (std::nullopt).  check_skyline != 0 runs the O(S^2)
+ * precondition check of gres.cpp:70-80. */
+int skygpu_grid_resistance(const double* sky_vals, const int64_t* sky_ids, uint64_t s, int d,
+                           const skygpu_plan* plan, uint64_t rep_count, int cores, int cap,
+                           int check_skyline, int32_t* out_den, int* out_g_max,
+                           skygpu_stats* stats, char* err, size_t errlen);
+
+/* gres.hpp:28 snap_relation on `count` values: out = floor(v*g)/g */
+int skygpu_snap_relation(const double* vals, uint64_t count, int intervals, double* out,
+                         char* err, size_t errlen);
+
+/* gres.hpp:35 max_grid_intervals; cap <= 0 means no cap */
+int skygpu_max_grid_intervals(const double* vals, uint64_t n, int d, int cap, int* out,
+                              char* err, size_t errlen);
+
+/* The whole hot path in one call: skyline of (vals, ids), then the
+ * grid-resistance scan of that skyline (harness.cpp:208, :229-231).
+ * Outputs: out_pos[0..*out_s) skyline input positions in (sum, id) order and
+ * out_den[k] the denominator of skyline tuple out_pos[k]; both sized n.
+ * shard_world > 1 computes denominators only for this shard's skyline tuples
+ * (interleaved chunks) and writes 0 for the others,
+ * so a max-reduction over ranks yields the full map. */
+int skygpu_pipeline(const double* vals, const int64_t* ids, uint64_t n, int d,
+                    const skygpu_plan* plan, int cap, int gres_engine, int shard_rank,
+                    int shard_world, unsigned flags, uint64_t* out_pos, int32_t* out_den,
+                    uint64_t* out_s, int* out_g_max, skygpu_stats* stats, char* err,
+                    size_t errlen);
+
+/* Product-side seeded generators (bit-exact with proj/src/datagen.cpp:41-94;
+ * kind 0 uni, 1 ant, 2 corr = BASELINE C3, 3 lattice = test_util.hpp:38-54).
+ * Host-side input preparation, not part of the timed path. */
+int skygpu_generate(int kind, uint64_t n, int d, uint64_t seed, double* out, char* err,
+                    size_t errlen);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SKYGPU_H */

@@ -205,7 +205,13 @@ int run_golden(const Args& a) {
     if (!a.no_gres) {
         std::optional<int> cap;
         if (a.cap > 0) cap = a.cap;
-        GridResistanceResult g = grid_resistance(sky.skyline, plan, a.reps, a.cores, cap);
+        GridResistanceResult g;
+        try {
+            g = grid_resistance(sky.skyline, plan, a.reps, a.cores, cap);
+        } catch (const std::exception& e) {
+            std::printf(",\"gres_error\":\"%s\"}\n", e.what());
+            return 0;
+        }
         std::printf(",\"g_max\":%d,\"den\":[", g.metrics.g_max);
         bool first = true;
         for (const auto& [id, den] : g.denominators) {

@@ -1,0 +1,8 @@
+"""B200-native grid-resistance engine (arXiv 2412.02274 hot path) behind the
+reference's skypar API.  The compute lives in libskygpu.so (csrc/, sm_100a);
+this package is the host-side mirror of the reference interface."""
+from .skypar import (  # noqa: F401
+    GRES_AUTO, GRES_CELLS, GRES_PAIRS, GridResistanceResult, PartitionPlan, SkyGpuError,
+    SkylineResult, Strategy, device_count, generate, grid_resistance, make_plan,
+    max_grid_intervals, parallel_skyline, pipeline, snap_relation, snap_to_grid,
+)

@@ -1,0 +1,474 @@
+// abi.cu — the C-ABI of libskygpu (include/skygpu.h): per-device context,
+// host<->device staging, exception -> status translation, plan sizing.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+
+#include "sky_common.cuh"
+
+namespace skygpu {
+
+namespace {
+Ctx* g_ctx[64] = {nullptr};
+cudaStream_t g_user_stream[64] = {nullptr};
+bool g_user_stream_set[64] = {false};
+
+void write_err(char* err, size_t errlen, const std::string& m) {
+    if (!err || errlen == 0) return;
+    size_t k = std::min(errlen - 1, m.size());
+    memcpy(err, m.data(), k);
+    err[k] = 0;
+}
+
+int current_device() {
+    int dev = 0;
+    SKY_CUDA(cudaGetDevice(&dev));
+    return dev;
+}
+}  // namespace
+
+Ctx& ctx() {
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0)
+        throw Error(SKYGPU_ECUDA, std::string("no CUDA device available (") +
+                                      cudaGetErrorString(e) + "); libskygpu has no CPU fallback");
+    const int dev = current_device();
+    if (!g_ctx[dev]) {
+        cudaDeviceProp prop;
+        SKY_CUDA(cudaGetDeviceProperties(&prop, dev));
+        if (prop.major < 10)
+            throw Error(SKYGPU_ECUDA, "device " + std::to_string(dev) + " is sm_" +
+                                          std::to_string(prop.major) +
+                                          std::to_string(prop.minor) +
+                                          "; libskygpu is built for sm_100a only");
+        Ctx* c = new Ctx();
+        c->device = dev;
+        c->num_sms = prop.multiProcessorCount;
+        SKY_CUDA(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
+        c->stream = c->own;
+        SKY_CUDA(cudaMalloc(&c->d_slots, sizeof(unsigned long long) * S_COUNT_));
+        SKY_CUDA(cudaMallocHost(&c->h_slots, sizeof(unsigned long long) * S_COUNT_));
+        for (auto& ev : c->ev) SKY_CUDA(cudaEventCreate(&ev));
+        g_ctx[dev] = c;
+    }
+    Ctx& c = *g_ctx[dev];
+    c.stream = g_user_stream_set[dev] ? g_user_stream[dev] : c.own;
+    return c;
+}
+
+void read_slots(Ctx& c, int first, int count) {
+    SKY_CUDA(cudaMemcpyAsync(c.h_slots + first, c.d_slots + first,
+                             sizeof(unsigned long long) * count, cudaMemcpyDeviceToHost,
+                             c.stream));
+    SKY_CUDA(cudaStreamSynchronize(c.stream));
+}
+
+void zero_slots(Ctx& c) {
+    unsigned long long init[S_COUNT_];
+    for (int i = 0; i < S_COUNT_; ++i) init[i] = 0;
+    init[S_BAD] = ~0ULL;
+    init[S_PAIR] = ~0ULL;
+    init[S_GRIDBAD] = ~0ULL;
+    init[S_MINGAP] = 0x7FF0000000000000ULL;
+    memcpy(c.h_slots, init, sizeof(init));
+    SKY_CUDA(cudaMemcpyAsync(c.d_slots, c.h_slots, sizeof(init), cudaMemcpyHostToDevice,
+                             c.stream));
+    SKY_CUDA(cudaStreamSynchronize(c.stream));
+}
+
+// gres.cu
+bool min_positive_gap_device(Ctx& c, const double* d_soa, uint64_t S, int d, double* gap,
+                             double* maxv);
+
+namespace {
+
+__global__ void k_aos_to_soa(const double* __restrict__ a, uint64_t n, int d,
+                             double* __restrict__ s) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n * d;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t t = i / d;
+        int k = (int)(i % d);
+        s[(uint64_t)k * n + t] = a[i];
+    }
+}
+
+__global__ void k_snap(const double* __restrict__ v, uint64_t total, int g,
+                       double* __restrict__ out) {
+    const double gd = (double)g;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = __ddiv_rn(floor(__dmul_rn(v[i], gd)), gd);
+}
+
+__global__ void k_check_values(const double* __restrict__ v, uint64_t total,
+                               unsigned long long* __restrict__ slots) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        if (!(v[i] >= 0.0)) atomicMin(&slots[S_BAD], (unsigned long long)i);
+}
+
+struct Timer {
+    Ctx& c;
+    int a, b;
+    Timer(Ctx& cc, int ea) : c(cc), a(ea), b(ea + 1) { SKY_CUDA(cudaEventRecord(c.ev[a], c.stream)); }
+    double stop() {
+        SKY_CUDA(cudaEventRecord(c.ev[b], c.stream));
+        SKY_CUDA(cudaEventSynchronize(c.ev[b]));
+        float ms = 0;
+        SKY_CUDA(cudaEventElapsedTime(&ms, c.ev[a], c.ev[b]));
+        return ms;
+    }
+};
+
+void validate_plan(const skygpu_plan* plan, int d) {
+    if (!plan) return;
+    if (plan->strategy < 0 || plan->strategy > 3) invalid("unknown strategy");
+    if (plan->partitions < 1) invalid("partitions must be >= 1");
+    (void)d;
+}
+
+template <class F>
+int guarded(char* err, size_t errlen, F&& f) {
+    try {
+        f();
+        write_err(err, errlen, "");
+        return SKYGPU_OK;
+    } catch (const Error& e) {
+        write_err(err, errlen, e.what());
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        write_err(err, errlen, "host allocation failed");
+        return SKYGPU_ENOMEM;
+    } catch (const std::exception& e) {
+        write_err(err, errlen, e.what());
+        return SKYGPU_ERUNTIME;
+    }
+}
+
+skygpu_stats g_scratch_stats;
+
+void begin_stats(Ctx& c, skygpu_stats* st) {
+    c.st = st ? st : &g_scratch_stats;
+    memset(c.st, 0, sizeof(skygpu_stats));
+    c.launches = 0;
+}
+
+void end_stats(Ctx& c) { c.st->kernel_launches = c.launches; }
+
+// ---- partition.cpp:13-83 plan sizing (host) ----
+constexpr long long kMaxPartitions = 1LL << 20;
+long long ipow_cap(long long b, int e) {
+    long long v = 1;
+    for (int i = 0; i < e; ++i) {
+        v *= b;
+        if (v > kMaxPartitions) return kMaxPartitions + 1;
+    }
+    return v;
+}
+int closest_slices(long long target, int e) {
+    int m = 2;
+    while (ipow_cap(m + 1, e) <= target) ++m;
+    long long lo = ipow_cap(m, e), hi = ipow_cap(m + 1, e);
+    return (target - lo <= hi - target) ? m : m + 1;
+}
+
+}  // namespace
+
+namespace {
+__global__ void k_widen(const uint32_t* __restrict__ a, uint64_t* __restrict__ b, uint64_t n) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        b[i] = a[i];
+}
+}  // namespace
+
+void widen_u32_u64(Ctx& c, const uint32_t* a, uint64_t* b, uint64_t n) {
+    k_widen<<<grid_for(n, 256), 256, 0, c.stream>>>(a, b, n);
+    SKY_LAUNCH_CHECK();
+    note_launch(c);
+}
+
+void aos_to_soa(Ctx& c, const double* d_aos, uint64_t n, int d, double* d_soa) {
+    if (n == 0) return;
+    k_aos_to_soa<<<grid_for(n * d, 256), 256, 0, c.stream>>>(d_aos, n, d, d_soa);
+    SKY_LAUNCH_CHECK();
+    note_launch(c);
+}
+
+}  // namespace skygpu
+
+using namespace skygpu;
+
+extern "C" {
+
+int skygpu_version(void) { return 10; }
+
+int skygpu_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
+int skygpu_set_device(int device, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] { SKY_CUDA(cudaSetDevice(device)); });
+}
+
+int skygpu_set_stream(void* stream, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        int dev = 0;
+        SKY_CUDA(cudaGetDevice(&dev));
+        g_user_stream[dev] = static_cast<cudaStream_t>(stream);
+        g_user_stream_set[dev] = stream != nullptr;
+    });
+}
+
+int skygpu_release(void) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return SKYGPU_ECUDA;
+    if (g_ctx[dev]) {
+        cudaStreamSynchronize(g_ctx[dev]->stream);
+        for (auto& b : g_ctx[dev]->buf) b.release();
+    }
+    return SKYGPU_OK;
+}
+
+int skygpu_make_plan(int strategy, long long target, int dims, skygpu_plan* out, char* err,
+                     size_t errlen) {
+    return guarded(err, errlen, [&] {
+        if (dims < 1) invalid("make_plan: dims must be >= 1");
+        if (target < 1 || target > kMaxPartitions)
+            invalid("make_plan: target partition count must be in [1, " +
+                    std::to_string(kMaxPartitions) + "]");
+        skygpu_plan p{strategy, 1, 1, dims};
+        switch (strategy) {
+            case SKYGPU_NONE: break;
+            case SKYGPU_GRID:
+                p.slices = closest_slices(target, dims);
+                p.partitions = ipow_cap(p.slices, dims);
+                break;
+            case SKYGPU_ANGULAR:
+                if (dims < 2) invalid("make_plan: angular partitioning needs dims >= 2");
+                p.slices = closest_slices(target, dims - 1);
+                p.partitions = ipow_cap(p.slices, dims - 1);
+                break;
+            case SKYGPU_SLICED: p.partitions = target; break;
+            default: invalid("unknown strategy");
+        }
+        if (p.partitions > kMaxPartitions)
+            invalid("make_plan: partition count exceeds " + std::to_string(kMaxPartitions));
+        *out = p;
+    });
+}
+
+int skygpu_parallel_skyline(const double* vals, const int64_t* ids, uint64_t n, int d,
+                            const skygpu_plan* plan, const double* rep_vals,
+                            const int64_t* rep_ids, uint64_t n_reps, int cores,
+                            uint64_t* out_pos, uint64_t* out_n, skygpu_stats* stats, char* err,
+                            size_t errlen) {
+    (void)rep_ids;
+    return guarded(err, errlen, [&] {
+        if (cores < 1) invalid("parallel_skyline: cores must be >= 1");
+        if (d < 1 || d > kMaxDims) invalid("parallel_skyline: dims must be in [1, 32]");
+        validate_plan(plan, d);
+        skygpu_plan pl = plan ? *plan : skygpu_plan{SKYGPU_NONE, 1, 1, d};
+        Ctx& c = ctx();
+        begin_stats(c, stats);
+        *out_n = 0;
+        if (n == 0) {
+            end_stats(c);
+            return;
+        }
+        Timer all(c, 0);
+        double* dv = c.buf[B_IN_VALS].as<double>(n * d);
+        int64_t* di = c.buf[B_IN_IDS].as<int64_t>(n);
+        double* dr = nullptr;
+        SKY_CUDA(cudaMemcpyAsync(dv, vals, n * d * sizeof(double), cudaMemcpyHostToDevice,
+                                 c.stream));
+        SKY_CUDA(cudaMemcpyAsync(di, ids, n * sizeof(int64_t), cudaMemcpyHostToDevice, c.stream));
+        if (n_reps) {
+            dr = c.buf[B_REPS].as<double>(n_reps * d);
+            SKY_CUDA(cudaMemcpyAsync(dr, rep_vals, n_reps * d * sizeof(double),
+                                     cudaMemcpyHostToDevice, c.stream));
+        }
+        SkylineOut so = skyline_device(c, dv, di, n, d, pl, dr, n_reps);
+        std::vector<uint32_t> pos(so.S);
+        if (so.S)
+            SKY_CUDA(cudaMemcpyAsync(pos.data(), so.d_inpos, so.S * sizeof(uint32_t),
+                                     cudaMemcpyDeviceToHost, c.stream));
+        c.st->ms_total = all.stop();
+        for (uint64_t k = 0; k < so.S; ++k) out_pos[k] = pos[k];
+        *out_n = so.S;
+        end_stats(c);
+    });
+}
+
+int skygpu_grid_resistance(const double* sky_vals, const int64_t* sky_ids, uint64_t s, int d,
+                           const skygpu_plan* plan, uint64_t rep_count, int cores, int cap,
+                           int check_skyline, int32_t* out_den, int* out_g_max,
+                           skygpu_stats* stats, char* err, size_t errlen) {
+    (void)rep_count;
+    return guarded(err, errlen, [&] {
+        if (cores < 1) invalid("grid_resistance: cores must be >= 1");
+        if (d < 1 || d > kMaxDims) invalid("grid_resistance: dims must be in [1, 32]");
+        validate_plan(plan, d);
+        Ctx& c = ctx();
+        begin_stats(c, stats);
+        *out_g_max = 1;
+        if (s == 0) {
+            end_stats(c);
+            return;
+        }
+        Timer all(c, 0);
+        double* dv = c.buf[B_IN_VALS].as<double>(s * d);
+        double* soa = c.buf[B_SKYV].as<double>(s * d);
+        int64_t* di = c.buf[B_IN_IDS].as<int64_t>(s);
+        int32_t* den = c.buf[B_DEN].as<int32_t>(s);
+        SKY_CUDA(cudaMemcpyAsync(dv, sky_vals, s * d * sizeof(double), cudaMemcpyHostToDevice,
+                                 c.stream));
+        SKY_CUDA(cudaMemcpyAsync(di, sky_ids, s * sizeof(int64_t), cudaMemcpyHostToDevice,
+                                 c.stream));
+        zero_slots(c);
+        k_check_values<<<grid_for(s * d, 256), 256, 0, c.stream>>>(dv, s * d, c.d_slots);
+        SKY_LAUNCH_CHECK();
+        note_launch(c);
+        read_slots(c, S_BAD, 1);
+        if (c.h_slots[S_BAD] != ~0ULL)
+            invalid("grid_resistance: tuple at position " + std::to_string(c.h_slots[S_BAD] / d) +
+                    " has a negative or NaN value (Relation::add contract, core.cpp:14-17)");
+        aos_to_soa(c, dv, s, d, soa);
+        GresOut go = gres_device(c, soa, di, s, d, cap, SKYGPU_GRES_AUTO, 0, 1,
+                                 check_skyline != 0, den);
+        SKY_CUDA(cudaMemcpyAsync(out_den, den, s * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                                 c.stream));
+        c.st->ms_total = all.stop();
+        *out_g_max = go.g_max;
+        end_stats(c);
+    });
+}
+
+int skygpu_snap_relation(const double* vals, uint64_t count, int intervals, double* out,
+                         char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        if (intervals < 1) invalid("snap_to_grid: intervals must be >= 1");
+        if (count == 0) return;
+        Ctx& c = ctx();
+        double* dv = c.buf[B_IN_VALS].as<double>(count);
+        double* dq = c.buf[B_PROJ].as<double>(count);
+        SKY_CUDA(cudaMemcpyAsync(dv, vals, count * sizeof(double), cudaMemcpyHostToDevice,
+                                 c.stream));
+        k_snap<<<grid_for(count, 256), 256, 0, c.stream>>>(dv, count, intervals, dq);
+        SKY_LAUNCH_CHECK();
+        SKY_CUDA(cudaMemcpyAsync(out, dq, count * sizeof(double), cudaMemcpyDeviceToHost,
+                                 c.stream));
+        SKY_CUDA(cudaStreamSynchronize(c.stream));
+    });
+}
+
+int skygpu_max_grid_intervals(const double* vals, uint64_t n, int d, int cap, int* out,
+                              char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        if (d < 1) invalid("max_grid_intervals: dims must be >= 1");
+        Ctx& c = ctx();
+        skygpu_stats tmp;
+        begin_stats(c, &tmp);
+        double gap = 0, maxv = 0;
+        bool has = false;
+        if (n > 0) {
+            double* dv = c.buf[B_IN_VALS].as<double>(n * d);
+            double* soa = c.buf[B_SKYV].as<double>(n * d);
+            SKY_CUDA(cudaMemcpyAsync(dv, vals, n * d * sizeof(double), cudaMemcpyHostToDevice,
+                                     c.stream));
+            aos_to_soa(c, dv, n, d, soa);
+            has = min_positive_gap_device(c, soa, n, d, &gap, &maxv);
+        }
+        if (!has)
+            invalid("max_grid_intervals: undefined, all tuples are identical on every attribute");
+        if (cap > 0 && 1.0 / gap >= static_cast<double>(cap)) {
+            *out = cap;
+            return;
+        }
+        double bound = std::floor(1.0 / gap);
+        if (bound > 2147483647.0)
+            invalid("max_grid_intervals: bound overflows the integer range; set a cap");
+        *out = static_cast<int>(bound);
+    });
+}
+
+int skygpu_pipeline(const double* vals, const int64_t* ids, uint64_t n, int d,
+                    const skygpu_plan* plan, int cap, int gres_engine, int shard_rank,
+                    int shard_world, unsigned flags, uint64_t* out_pos, int32_t* out_den,
+                    uint64_t* out_s, int* out_g_max, skygpu_stats* stats, char* err,
+                    size_t errlen) {
+    return guarded(err, errlen, [&] {
+        if (d < 1 || d > kMaxDims) invalid("pipeline: dims must be in [1, 32]");
+        validate_plan(plan, d);
+        if (shard_world < 1 || shard_rank < 0 || shard_rank >= shard_world)
+            invalid("pipeline: bad shard");
+        skygpu_plan pl = plan ? *plan : skygpu_plan{SKYGPU_NONE, 1, 1, d};
+        Ctx& c = ctx();
+        begin_stats(c, stats);
+        const bool dev = flags & SKYGPU_DEVICE_PTRS;
+        *out_s = 0;
+        *out_g_max = 1;
+        if (n == 0) {
+            end_stats(c);
+            return;
+        }
+        Timer all(c, 0);
+        const double* dv = vals;
+        const int64_t* di = ids;
+        if (!dev) {
+            Timer h2d(c, 2);
+            double* bv = c.buf[B_IN_VALS].as<double>(n * d);
+            int64_t* bi = c.buf[B_IN_IDS].as<int64_t>(n);
+            SKY_CUDA(cudaMemcpyAsync(bv, vals, n * d * sizeof(double), cudaMemcpyHostToDevice,
+                                     c.stream));
+            SKY_CUDA(cudaMemcpyAsync(bi, ids, n * sizeof(int64_t), cudaMemcpyHostToDevice,
+                                     c.stream));
+            c.st->ms_h2d = h2d.stop();
+            dv = bv;
+            di = bi;
+        }
+        Timer tsky(c, 4);
+        SkylineOut so = skyline_device(c, dv, di, n, d, pl, nullptr, 0);
+        c.st->ms_skyline = tsky.stop();
+        int32_t* den = c.buf[B_DEN].as<int32_t>(so.S ? so.S : 1);
+        GresOut go;
+        if (!(flags & SKYGPU_SKIP_GRES)) {
+            Timer tg(c, 6);
+            go = gres_device(c, so.d_skyv, so.d_ids, so.S, d, cap, gres_engine, shard_rank,
+                             shard_world, (flags & SKYGPU_CHECK_SKYLINE) != 0, den);
+            c.st->ms_gres = tg.stop();
+        }
+        Timer d2h(c, 12);
+        if (dev) {
+            // outputs stay on the device; positions widened to u64
+            if (so.S) {
+                if (!(flags & SKYGPU_SKIP_GRES))
+                    SKY_CUDA(cudaMemcpyAsync(out_den, den, so.S * sizeof(int32_t),
+                                             cudaMemcpyDeviceToDevice, c.stream));
+                widen_u32_u64(c, so.d_inpos, out_pos, so.S);
+            }
+        } else if (so.S) {
+            std::vector<uint32_t> pos(so.S);
+            SKY_CUDA(cudaMemcpyAsync(pos.data(), so.d_inpos, so.S * sizeof(uint32_t),
+                                     cudaMemcpyDeviceToHost, c.stream));
+            if (!(flags & SKYGPU_SKIP_GRES))
+                SKY_CUDA(cudaMemcpyAsync(out_den, den, so.S * sizeof(int32_t),
+                                         cudaMemcpyDeviceToHost, c.stream));
+            SKY_CUDA(cudaStreamSynchronize(c.stream));
+            for (uint64_t k = 0; k < so.S; ++k) out_pos[k] = pos[k];
+        }
+        c.st->ms_d2h = d2h.stop();
+        c.st->ms_total = all.stop();
+        *out_s = so.S;
+        *out_g_max = go.g_max;
+        end_stats(c);
+    });
+}
+
+}  // extern "C"
+

@@ -1,0 +1,486 @@
+// gres.cu — the grid-resistance stage on sm_100a (north_star (b)).
+//
+// Reference: grid_resistance (proj/src/gres.cpp:65-129).  g_max comes from the
+// smallest non-zero same-attribute gap of the skyline (gres.cpp:15-37,
+// :89-90); then for g = g_max .. 2 every tuple is projected to
+// floor(v*g)/g (gres.cpp:41-55) and the projected skyline is recomputed
+// (parallel_skyline, :102); a tuple's denominator is the first (largest) g
+// whose projected skyline does not contain it, else 1 (:112-121).
+//
+// By the predecessor rule (skyline.cu) the projected skyline drops t at g
+// iff some tuple s before t in (projected sum, id) order has q(s) dominating
+// q(t), q = floor(v*g)/g.  Two exact reductions make this a pure code test:
+//  * codes: with k = floor(v*g) (k < 2^52), correctly rounded k/g is
+//    strictly increasing in k, so q(s) dominates q(t) iff k(s) dominates k(t);
+//  * order: q(s) dominating q(t) forces psum(s) <= psum(t); a tie (which would
+//    let a later-id dominator NOT eject t) needs sums that differ by >= 1/g to
+//    round to the same double, impossible while g*d*(d+1)*(max|v|+1) < 2^50.
+//    Outside that bound the float64 path re-checks (psum, id) order exactly.
+// So at step g, t is ejected iff some skyline tuple's code vector dominates
+// t's — every skyline tuple is a comparator; no order bookkeeping.
+//
+// Pair engine (the dominance-test kernel the metric counts): one launch per
+// g over the still-undecided candidates (descending g, exit at the first
+// dominating step), comparators streamed through shared-memory tiles.
+//  - u8 path (d <= 8, max code <= 127): a tuple's codes at step g packed one
+//    byte per attribute in a u64; one test = SWAR subtract + mask + compare
+//    (dom_u8), 4 candidates per thread share each broadcast LDS.64.
+//  - f64 path (anything else): the reference's own projections
+//    floor(v*g)/g compared as float64, with the exact (psum, id) order check
+//    when ties are possible.
+#include <cub/cub.cuh>
+
+#include <cmath>
+#include <limits>
+
+#include "sky_common.cuh"
+
+namespace skygpu {
+
+namespace {
+
+constexpr int kBlock = 256;
+
+template <class F>
+void dispatch_d(int d, F&& f) {
+    switch (d) {
+        case 1: f(std::integral_constant<int, 1>{}); break;
+        case 2: f(std::integral_constant<int, 2>{}); break;
+        case 3: f(std::integral_constant<int, 3>{}); break;
+        case 4: f(std::integral_constant<int, 4>{}); break;
+        case 5: f(std::integral_constant<int, 5>{}); break;
+        case 6: f(std::integral_constant<int, 6>{}); break;
+        case 7: f(std::integral_constant<int, 7>{}); break;
+        case 8: f(std::integral_constant<int, 8>{}); break;
+        default: f(std::integral_constant<int, 0>{}); break;
+    }
+}
+
+// column j of the SoA skyline into a contiguous buffer (for the gap sort)
+__global__ void k_copy(const double* __restrict__ src, uint64_t n, double* __restrict__ dst) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+}
+
+// gres.cpp:20-24: min positive adjacent difference of a sorted column
+__global__ void k_min_gap(const double* __restrict__ col, uint64_t n,
+                          unsigned long long* __restrict__ slots) {
+    unsigned long long best = 0x7FF0000000000000ULL;  // +inf
+    for (uint64_t i = 1 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        double gap = __dsub_rn(col[i], col[i - 1]);
+        if (gap > 0.0) {
+            unsigned long long b = (unsigned long long)__double_as_longlong(gap);
+            best = b < best ? b : best;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long x = __shfl_down_sync(0xffffffffu, best, o);
+        best = x < best ? x : best;
+    }
+    if ((threadIdx.x & 31) == 0) atomicMin(&slots[S_MINGAP], best);
+}
+
+__global__ void k_max_value(const double* __restrict__ v, uint64_t n,
+                            unsigned long long* __restrict__ slots) {
+    unsigned long long best = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        unsigned long long b = ord_bits(v[i]);
+        best = b > best ? b : best;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long x = __shfl_down_sync(0xffffffffu, best, o);
+        best = x > best ? x : best;
+    }
+    if ((threadIdx.x & 31) == 0) atomicMax(&slots[S_MAXV], best);
+}
+
+// gres.cpp:70-80 (checked builds): the first (a, b) in input order with
+// a dominating b.  Per candidate b the smallest dominating a; global min of
+// a*S + b gives the lexicographically first pair.
+template <int D>
+__global__ void __launch_bounds__(kBlock)
+k_check_skyline(const double* __restrict__ v, uint64_t S, int d,
+                unsigned long long* __restrict__ slots) {
+    constexpr int TILE = D > 0 ? 256 : 128;
+    constexpr int DM = D > 0 ? D : kMaxDims;
+    extern __shared__ double tile[];
+    const int dd = D > 0 ? D : d;
+    const uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const bool valid = b < S;
+    double t[DM];
+#pragma unroll
+    for (int k = 0; k < DM; ++k)
+        if (k < dd) t[k] = valid ? v[k * S + b] : 0.0;
+    bool alive = valid;
+    for (uint64_t base = 0; base < S; base += TILE) {
+        const uint32_t nt = (uint32_t)min((uint64_t)TILE, S - base);
+        for (uint32_t k = threadIdx.x; k < nt; k += blockDim.x)
+            for (int a = 0; a < dd; ++a) tile[a * TILE + k] = v[a * S + base + k];
+        __syncthreads();
+        if (alive) {
+            for (uint32_t k = 0; k < nt; ++k) {
+                double s[DM];
+#pragma unroll
+                for (int a = 0; a < DM; ++a)
+                    if (a < dd) s[a] = tile[a * TILE + k];
+                bool dm = D > 0 ? dom_f64<(D > 0 ? D : 1)>(s, t) : dom_f64_dyn(s, t, dd);
+                if (dm) {
+                    atomicMin(&slots[S_PAIR], (unsigned long long)((base + k) * S + b));
+                    alive = false;
+                    break;
+                }
+            }
+        }
+        if (!__syncthreads_or(alive)) break;
+    }
+}
+
+// codes at step g, one byte per attribute: k = floor(v*g) (gres.cpp:46)
+__global__ void k_codes_u8(const double* __restrict__ v, uint64_t S, int d, int g,
+                           unsigned long long* __restrict__ codes) {
+    const double gd = (double)g;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < S;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        unsigned long long w = 0;
+        for (int k = 0; k < d; ++k) {
+            double q = floor(__dmul_rn(v[k * S + i], gd));
+            w |= (unsigned long long)(unsigned)q << (8 * k);
+        }
+        codes[i] = w;
+    }
+}
+
+// projections at step g exactly as the reference: floor(v*g)/g (gres.cpp:46)
+__global__ void k_project(const double* __restrict__ v, uint64_t total, int g,
+                          double* __restrict__ q) {
+    const double gd = (double)g;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        q[i] = __ddiv_rn(floor(__dmul_rn(v[i], gd)), gd);
+}
+
+// initial candidate list for this shard: interleaved chunks of 256 tuples
+__global__ void k_shard_list(uint64_t S, int rank, int world, uint32_t* __restrict__ act,
+                             unsigned long long* __restrict__ slots) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < S;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        if ((int)((i >> 8) % (uint64_t)world) == rank) {
+            unsigned long long pos = atomicAdd(&slots[S_SEL2], 1ULL);
+            act[pos] = (uint32_t)i;
+        }
+    }
+}
+
+__global__ void k_fill_den(const uint32_t* __restrict__ act, uint64_t na, int value,
+                           int32_t* __restrict__ den) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < na;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        den[act[i]] = value;
+}
+
+// ---- pair engine, u8 path ---------------------------------------------
+constexpr int kTileU8 = 2048;
+constexpr int kCandU8 = 4;
+
+__global__ void __launch_bounds__(kBlock)
+k_gres_pairs_u8(const unsigned long long* __restrict__ codes, uint32_t S,
+                const uint32_t* __restrict__ act, uint32_t na, int g,
+                int32_t* __restrict__ den, uint8_t* __restrict__ still,
+                unsigned long long* __restrict__ tests) {
+    __shared__ unsigned long long tile[kTileU8];
+    unsigned long long tc[kCandU8], tg[kCandU8];
+    uint32_t ti[kCandU8];
+    bool alive[kCandU8];
+    const uint32_t base_i = blockIdx.x * (kBlock * kCandU8);
+#pragma unroll
+    for (int c = 0; c < kCandU8; ++c) {
+        const uint32_t idx = base_i + c * kBlock + threadIdx.x;
+        alive[c] = idx < na;
+        ti[c] = alive[c] ? act[idx] : 0;
+        tc[c] = alive[c] ? codes[ti[c]] : 0;
+        tg[c] = tc[c] | kGuard;
+    }
+    unsigned long long cnt = 0;
+    bool any = alive[0] | alive[1] | alive[2] | alive[3];
+    for (uint32_t base = 0; base < S; base += kTileU8) {
+        const uint32_t nt = min((uint32_t)kTileU8, S - base);
+        for (uint32_t k = threadIdx.x; k < nt; k += kBlock) tile[k] = codes[base + k];
+        __syncthreads();
+        if (any) {
+            for (uint32_t k0 = 0; k0 < nt; k0 += 32) {
+                const uint32_t k1 = min(nt, k0 + 32);
+                for (uint32_t k = k0; k < k1; ++k) {
+                    const unsigned long long s = tile[k];
+#pragma unroll
+                    for (int c = 0; c < kCandU8; ++c) {
+                        cnt += alive[c];
+                        alive[c] &= !dom_u8(s, tc[c], tg[c]);
+                    }
+                }
+                any = alive[0] | alive[1] | alive[2] | alive[3];
+                if (!any) break;
+            }
+        }
+        if (!__syncthreads_or(any)) break;
+    }
+#pragma unroll
+    for (int c = 0; c < kCandU8; ++c) {
+        const uint32_t idx = base_i + c * kBlock + threadIdx.x;
+        if (idx < na) {
+            still[idx] = alive[c];
+            if (!alive[c]) den[ti[c]] = g;
+        }
+    }
+    add_count(tests, cnt);
+}
+
+// ---- pair engine, float64 path ------------------------------------------
+// psum (core.cpp:21-23 on the projection) and the (psum, id) predecessor
+// order, only consulted when ties are possible.
+__device__ __forceinline__ bool before(const double* __restrict__ q, uint64_t S, int d,
+                                       const int64_t* __restrict__ ids, uint32_t s, uint32_t t) {
+    double ps = 0.0, pt = 0.0;
+    for (int k = 0; k < d; ++k) {
+        ps = __dadd_rn(ps, q[k * S + s]);
+        pt = __dadd_rn(pt, q[k * S + t]);
+    }
+    if (ps != pt) return ps < pt;
+    if (ids[s] != ids[t]) return ids[s] < ids[t];
+    return s < t;
+}
+
+template <int D>
+__global__ void __launch_bounds__(kBlock)
+k_gres_pairs_f64(const double* __restrict__ q, uint32_t S, int d,
+                 const int64_t* __restrict__ ids, const uint32_t* __restrict__ act,
+                 uint32_t na, int g, int tiecheck, int32_t* __restrict__ den,
+                 uint8_t* __restrict__ still, unsigned long long* __restrict__ tests) {
+    constexpr int TILE = D > 0 ? 256 : 128;
+    constexpr int DM = D > 0 ? D : kMaxDims;
+    extern __shared__ double tile[];
+    const int dd = D > 0 ? D : d;
+    const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool valid = idx < na;
+    const uint32_t ti = valid ? act[idx] : 0;
+    double t[DM];
+#pragma unroll
+    for (int k = 0; k < DM; ++k)
+        if (k < dd) t[k] = valid ? q[(uint64_t)k * S + ti] : 0.0;
+    bool alive = valid;
+    unsigned long long cnt = 0;
+    for (uint32_t base = 0; base < S; base += TILE) {
+        const uint32_t nt = min((uint32_t)TILE, S - base);
+        for (uint32_t k = threadIdx.x; k < nt; k += blockDim.x)
+            for (int a = 0; a < dd; ++a) tile[a * TILE + k] = q[(uint64_t)a * S + base + k];
+        __syncthreads();
+        if (alive) {
+            for (uint32_t k = 0; k < nt; ++k) {
+                double s[DM];
+#pragma unroll
+                for (int a = 0; a < DM; ++a)
+                    if (a < dd) s[a] = tile[a * TILE + k];
+                ++cnt;
+                bool dm = D > 0 ? dom_f64<(D > 0 ? D : 1)>(s, t) : dom_f64_dyn(s, t, dd);
+                if (dm && tiecheck) dm = before(q, S, dd, ids, base + k, ti);
+                if (dm) {
+                    alive = false;
+                    break;
+                }
+            }
+        }
+        if (!__syncthreads_or(alive)) break;
+    }
+    if (valid) {
+        still[idx] = alive;
+        if (!alive) den[ti] = g;
+    }
+    add_count(tests, cnt);
+}
+
+uint64_t select_flagged(Ctx& c, const uint32_t* in, const uint8_t* flags, uint32_t* out,
+                        uint64_t n) {
+    if (n == 0) return 0;
+    size_t tmp = 0;
+    SKY_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp, in, flags, out, c.d_slots + S_SEL,
+                                         (int64_t)n, c.stream));
+    void* t = c.buf[B_CUB].get(tmp);
+    SKY_CUDA(cub::DeviceSelect::Flagged(t, tmp, in, flags, out, c.d_slots + S_SEL, (int64_t)n,
+                                         c.stream));
+    note_launch(c, 2);
+    read_slots(c, S_SEL, 1);
+    return c.h_slots[S_SEL];
+}
+
+}  // namespace
+
+// gres.cpp:30-37 intervals_from_gap, same float64 arithmetic
+static int intervals_from_gap(double gap, int cap) {
+    if (cap > 0 && 1.0 / gap >= static_cast<double>(cap)) return cap;
+    double bound = std::floor(1.0 / gap);
+    if (bound > static_cast<double>(std::numeric_limits<int>::max()))
+        invalid("max_grid_intervals: bound overflows the integer range; set a cap");
+    return static_cast<int>(bound);
+}
+
+// gres.cpp:15-28 on the device: per column sort + adjacent-difference min.
+// Returns false when every attribute is constant.
+bool min_positive_gap_device(Ctx& c, const double* d_soa, uint64_t S, int d, double* gap,
+                             double* maxv) {
+    zero_slots(c);
+    double* col = c.buf[B_GTMP0].as<double>(S);
+    double* srt = c.buf[B_GTMP1].as<double>(S);
+    const unsigned gb = grid_for(S, kBlock);
+    for (int j = 0; j < d; ++j) {
+        k_copy<<<gb, kBlock, 0, c.stream>>>(d_soa + (uint64_t)j * S, S, col);
+        SKY_LAUNCH_CHECK();
+        size_t tmp = 0;
+        SKY_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, col, srt, (int64_t)S, 0, 64,
+                                                 c.stream));
+        void* t = c.buf[B_CUB].get(tmp);
+        SKY_CUDA(cub::DeviceRadixSort::SortKeys(t, tmp, col, srt, (int64_t)S, 0, 64, c.stream));
+        k_min_gap<<<gb, kBlock, 0, c.stream>>>(srt, S, c.d_slots);
+        SKY_LAUNCH_CHECK();
+        note_launch(c, 6);
+    }
+    k_max_value<<<grid_for(S * d, kBlock), kBlock, 0, c.stream>>>(d_soa, S * d, c.d_slots);
+    SKY_LAUNCH_CHECK();
+    note_launch(c);
+    read_slots(c, S_MINGAP, 2);
+    unsigned long long gb_bits = c.h_slots[S_MINGAP], mb = c.h_slots[S_MAXV];
+    double g, m;
+    memcpy(&g, &gb_bits, 8);
+    memcpy(&m, &mb, 8);
+    *maxv = m;
+    if (!std::isfinite(g)) return false;
+    *gap = g;
+    return true;
+}
+
+GresOut gres_device(Ctx& c, const double* d_skyv, const int64_t* d_ids, uint64_t S, int d,
+                    int cap, int engine, int shard_rank, int shard_world, bool check_skyline,
+                    int32_t* d_den) {
+    GresOut out;
+    skygpu_stats& st = *c.st;
+    if (S >= 0x7FFFFFFFull) invalid("grid_resistance: more than 2^31-1 skyline tuples");
+    if (S == 0) return out;
+    if (shard_world < 1) shard_world = 1;
+
+    if (check_skyline) {
+        zero_slots(c);
+        dispatch_d(d, [&](auto DC) {
+            constexpr int D = decltype(DC)::value;
+            const size_t smem = sizeof(double) * (D > 0 ? 256 : 128) * (D > 0 ? D : d);
+            k_check_skyline<D><<<grid_for(S, kBlock, 1 << 30), kBlock, smem, c.stream>>>(
+                d_skyv, S, d, c.d_slots);
+        });
+        SKY_LAUNCH_CHECK();
+        note_launch(c);
+        read_slots(c, S_PAIR, 1);
+        if (c.h_slots[S_PAIR] != ~0ULL) {
+            const uint64_t key = c.h_slots[S_PAIR];
+            int64_t ia = 0, ib = 0;
+            SKY_CUDA(cudaMemcpyAsync(&ia, d_ids + key / S, 8, cudaMemcpyDeviceToHost, c.stream));
+            SKY_CUDA(cudaMemcpyAsync(&ib, d_ids + key % S, 8, cudaMemcpyDeviceToHost, c.stream));
+            SKY_CUDA(cudaStreamSynchronize(c.stream));
+            invalid("grid_resistance: input is not a skyline (tuple " + std::to_string(ia) +
+                    " dominates tuple " + std::to_string(ib) + ")");
+        }
+    }
+
+    double gap = 0, maxv = 0;
+    const bool has_gap = min_positive_gap_device(c, d_skyv, S, d, &gap, &maxv);
+    out.g_max = has_gap ? intervals_from_gap(gap, cap) : 1;
+    st.g_max = out.g_max;
+
+    // candidate list of this shard
+    uint32_t* act = c.buf[B_ACT0].as<uint32_t>(S);
+    uint32_t* act2 = c.buf[B_ACT1].as<uint32_t>(S);
+    uint8_t* still = c.buf[B_FLAGS].as<uint8_t>(S);
+    const unsigned gb = grid_for(S, kBlock);
+    SKY_CUDA(cudaMemsetAsync(d_den, 0, S * sizeof(int32_t), c.stream));
+    zero_slots(c);
+    k_shard_list<<<gb, kBlock, 0, c.stream>>>(S, shard_rank, shard_world, act, c.d_slots);
+    SKY_LAUNCH_CHECK();
+    note_launch(c);
+    read_slots(c, S_SEL2, 1);
+    uint64_t na = c.h_slots[S_SEL2];
+    if (shard_world > 1) {  // keep ascending order for coalesced candidate reads
+        size_t tmp = 0;
+        SKY_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, act, act2, (int64_t)na, 0, 32,
+                                                 c.stream));
+        void* t = c.buf[B_CUB].get(tmp);
+        SKY_CUDA(cub::DeviceRadixSort::SortKeys(t, tmp, act, act2, (int64_t)na, 0, 32,
+                                                 c.stream));
+        note_launch(c, 4);
+        std::swap(act, act2);
+    }
+
+    // path selection (see file header)
+    const double code_max = std::floor(maxv * (double)out.g_max);
+    const double tie_bound = (double)out.g_max * d * (d + 1) * (maxv + 1.0);
+    const bool ties_possible = !(tie_bound < 1125899906842624.0);  // 2^50
+    const bool u8 = d <= 8 && code_max <= 127.0 && !ties_possible;
+    st.code_bits = u8 ? 8 : 64;
+    st.gres_engine = SKYGPU_GRES_PAIRS;
+    (void)engine;
+
+    unsigned long long* codes = u8 ? c.buf[B_CODES].as<unsigned long long>(S) : nullptr;
+    double* q = u8 ? nullptr : c.buf[B_PROJ].as<double>(S * d);
+    cudaEvent_t e0 = c.ev[10], e1 = c.ev[11];
+    double kms = 0;
+    uint64_t klaunch = 0;
+    int steps = 0;
+    for (int g = out.g_max; g >= 2 && na > 0; --g) {
+        ++steps;
+        if (u8) {
+            k_codes_u8<<<gb, kBlock, 0, c.stream>>>(d_skyv, S, d, g, codes);
+            SKY_LAUNCH_CHECK();
+            const unsigned blocks = (unsigned)((na + kBlock * kCandU8 - 1) / (kBlock * kCandU8));
+            SKY_CUDA(cudaEventRecord(e0, c.stream));
+            k_gres_pairs_u8<<<blocks, kBlock, 0, c.stream>>>(codes, (uint32_t)S, act,
+                                                             (uint32_t)na, g, d_den, still,
+                                                             c.d_slots + S_TESTS_GRES);
+            SKY_CUDA(cudaEventRecord(e1, c.stream));
+            SKY_LAUNCH_CHECK();
+        } else {
+            k_project<<<grid_for(S * d, kBlock), kBlock, 0, c.stream>>>(d_skyv, S * d, g, q);
+            SKY_LAUNCH_CHECK();
+            dispatch_d(d, [&](auto DC) {
+                constexpr int D = decltype(DC)::value;
+                const size_t smem = sizeof(double) * (D > 0 ? 256 : 128) * (D > 0 ? D : d);
+                SKY_CUDA(cudaEventRecord(e0, c.stream));
+                k_gres_pairs_f64<D><<<grid_for(na, kBlock, 1 << 30), kBlock, smem, c.stream>>>(
+                    q, (uint32_t)S, d, d_ids, act, (uint32_t)na, g, ties_possible ? 1 : 0,
+                    d_den, still, c.d_slots + S_TESTS_GRES);
+                SKY_CUDA(cudaEventRecord(e1, c.stream));
+            });
+            SKY_LAUNCH_CHECK();
+        }
+        note_launch(c, 2);
+        na = select_flagged(c, act, still, act2, na);
+        std::swap(act, act2);
+        float ms = 0;
+        SKY_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        kms += ms;
+        ++klaunch;
+    }
+    if (na > 0) {
+        k_fill_den<<<grid_for(na, kBlock), kBlock, 0, c.stream>>>(act, na, 1, d_den);
+        SKY_LAUNCH_CHECK();
+        note_launch(c);
+    }
+    out.steps = steps;
+    st.gres_steps = steps;
+    st.ms_gres_kernel += kms;
+    st.gres_kernel_launches += klaunch;
+    read_slots(c, S_TESTS_GRES, 1);
+    st.gres_tests = c.h_slots[S_TESTS_GRES];
+    return out;
+}
+
+}  // namespace skygpu

@@ -1,0 +1,194 @@
+// sky_common.cuh — shared pieces of libskygpu: per-device context with cached
+// device buffers, error plumbing, and the dominance primitives.
+//
+// Dominance (core.hpp:55-67): s dominates t iff s_i <= t_i for every i and
+// s_i < t_i for some i.  Values are compared as float64 with exact IEEE
+// semantics (no epsilon); -0.0 == +0.0 as in the reference.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "skygpu.h"
+
+namespace skygpu {
+
+constexpr int kMaxDims = 32;  // generic-path limit (template paths cover d <= 8)
+
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define SKY_CUDA(call)                                                                   \
+    do {                                                                                 \
+        cudaError_t e_ = (call);                                                         \
+        if (e_ != cudaSuccess)                                                           \
+            throw ::skygpu::Error(e_ == cudaErrorMemoryAllocation ? SKYGPU_ENOMEM          \
+                                                                  : SKYGPU_ECUDA,        \
+                                  std::string(#call) + ": " + cudaGetErrorString(e_));   \
+    } while (0)
+
+#define SKY_LAUNCH_CHECK() SKY_CUDA(cudaGetLastError())
+
+inline void invalid(const std::string& m) { throw Error(SKYGPU_EINVAL, m); }
+
+// Growable device buffer owned by the context (never shrinks until release).
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    void* get(size_t bytes) {
+        if (bytes == 0) bytes = 16;
+        if (bytes > cap) {
+            if (p) cudaFree(p);
+            p = nullptr;
+            cap = 0;
+            size_t want = bytes + bytes / 8 + 256;
+            SKY_CUDA(cudaMalloc(&p, want));
+            cap = want;
+        }
+        return p;
+    }
+    template <class T>
+    T* as(size_t count) { return static_cast<T*>(get(count * sizeof(T))); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+enum BufId {
+    B_IN_VALS, B_IN_IDS, B_KEY0, B_KEY1, B_IDX0, B_IDX1, B_SV, B_SID, B_SPOS,
+    B_R0, B_R1, B_FLAGS, B_KLIST, B_CUB, B_SKYV, B_SKYID, B_CODES, B_ACT0, B_ACT1,
+    B_DEN, B_GTMP0, B_GTMP1, B_OUTPOS, B_PROJ, B_REPS, B_MISC, B_CELLS, B_CSUM,
+    B_ORDER, B_COUNT
+};
+
+// Device-side scalar slots (one small allocation, read back through pinned memory).
+enum Slot {
+    S_SEL = 0,         // DeviceSelect count
+    S_TESTS_SKY = 1,   // dominance tests, skyline stage
+    S_TESTS_GRES = 2,  // code tests, gres stage
+    S_MINGAP = 3,      // bits of the min positive gap (atomicMin)
+    S_MAXV = 4,        // bits of max |value| (atomicMax)
+    S_BAD = 5,         // first tuple index with a negative/NaN value (atomicMin; ~0 = none)
+    S_FLAG = 6,        // generic flag
+    S_PAIR = 7,        // check_skyline: min (a*S + b) (~0 = none)
+    S_SEL2 = 8,
+    S_GRIDBAD = 9,     // first flat index of a Grid value outside [0,1]
+    S_COUNT_ = 16
+};
+
+struct Ctx {
+    int device = 0;
+    cudaStream_t own = nullptr;
+    cudaStream_t stream = nullptr;
+    DevBuf buf[B_COUNT];
+    unsigned long long* d_slots = nullptr;
+    unsigned long long* h_slots = nullptr;  // pinned mirror
+    cudaEvent_t ev[16];
+    skygpu_stats* st = nullptr;
+    uint64_t launches = 0;
+    int num_sms = 148;
+};
+
+Ctx& ctx();  // current device's context (created lazily)
+
+inline void note_launch(Ctx& c, uint64_t k = 1) { c.launches += k; }
+
+// Read `count` slots back (synchronises the stream).
+void read_slots(Ctx& c, int first, int count);
+void zero_slots(Ctx& c);
+
+// ---------------------------------------------------------------- dominance
+// s dominates t on D float64 attributes (branch-free form of core.hpp:55-67).
+template <int D>
+__device__ __forceinline__ bool dom_f64(const double* s, const double* t) {
+    bool le = true, lt = false;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+        le &= (s[k] <= t[k]);
+        lt |= (s[k] < t[k]);
+    }
+    return le & lt;
+}
+
+__device__ __forceinline__ bool dom_f64_dyn(const double* s, const double* t, int d) {
+    bool le = true, lt = false;
+    for (int k = 0; k < d; ++k) {
+        le &= (s[k] <= t[k]);
+        lt |= (s[k] < t[k]);
+    }
+    return le & lt;
+}
+
+// Packed u8 codes (one byte per attribute, code <= 127, d <= 8): s dominates
+// t at this step iff every byte of s <= the byte of t and the words differ.
+// tg = t | H: bit 7 of each byte of (tg - s) is set iff t_byte >= s_byte
+// (no borrow can cross a byte since 128 + t - s >= 1).
+constexpr uint64_t kGuard = 0x8080808080808080ULL;
+__device__ __forceinline__ bool dom_u8(uint64_t s, uint64_t t, uint64_t tg) {
+    return (((tg - s) & kGuard) == kGuard) & (s != t);
+}
+
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// lane 0 of each warp adds the warp's total into *dst
+__device__ __forceinline__ void add_count(unsigned long long* dst, unsigned long long v) {
+    v = warp_sum_u64(v);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(dst, v);
+}
+
+// bits of a non-negative double, canonicalising -0.0 to +0.0 so that the
+// unsigned order of the bits equals the numeric order
+__device__ __forceinline__ unsigned long long ord_bits(double v) {
+    return v == 0.0 ? 0ULL : static_cast<unsigned long long>(__double_as_longlong(v));
+}
+
+inline unsigned grid_for(uint64_t n, int block, int cap_blocks = 148 * 32) {
+    uint64_t b = (n + block - 1) / block;
+    if (b < 1) b = 1;
+    if (b > (uint64_t)cap_blocks) b = cap_blocks;
+    return static_cast<unsigned>(b);
+}
+
+// ------------------------------------------------------------- stage APIs
+struct SkylineOut {
+    uint64_t S = 0;
+    // device: sorted-order positions of skyline tuples (u32), S entries, in
+    // (sum, id) order; input positions (u32) and ids (i64) of the same.
+    uint32_t* d_inpos = nullptr;
+    int64_t* d_ids = nullptr;
+    double* d_skyv = nullptr;  // SoA [d][S]
+};
+
+// Skyline of n tuples already resident on the device (AoS vals, ids).
+SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, uint64_t n, int d,
+                          const skygpu_plan& plan, const double* d_reps, uint64_t n_reps);
+
+struct GresOut {
+    int g_max = 1;
+    int steps = 0;
+};
+
+// Grid resistance of S skyline tuples held SoA on the device (d_skyv[d][S]).
+// d_den (S entries) receives the denominators (0 for tuples outside this
+// shard).  Throws Error(EINVAL, ...) exactly where the reference throws.
+GresOut gres_device(Ctx& c, const double* d_skyv, const int64_t* d_ids, uint64_t S, int d,
+                    int cap, int engine, int shard_rank, int shard_world, bool check_skyline,
+                    int32_t* d_den);
+
+// float64 AoS -> SoA transpose on the device
+void aos_to_soa(Ctx& c, const double* d_aos, uint64_t n, int d, double* d_soa);
+
+}  // namespace skygpu

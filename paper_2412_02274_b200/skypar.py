@@ -1,0 +1,311 @@
+"""Python host mirror of the reference's hot-path API over libskygpu's C-ABI.
+
+Same names, argument meaning and error behaviour as the reference C++ API
+(/root/reference/proj/include/skypar/*.hpp); ``std::invalid_argument``
+becomes ``ValueError``, ``std::runtime_error`` becomes ``RuntimeError``:
+
+    make_plan(strategy, target_partitions, dims)            partition.hpp:43
+    parallel_skyline(values, ids, plan, reps, cores)        parallel.hpp:46-47
+    grid_resistance(sky_values, sky_ids, plan, rep_count,   gres.hpp:73-75
+                    cores, cap)
+    snap_to_grid(values, intervals) / snap_relation(...)    gres.hpp:26-28
+    max_grid_intervals(values, cap)                         gres.hpp:35
+
+A relation is a float64 array of shape (n, d) plus an int64 id vector
+(default: row index, the reference's generator/CSV convention).  There is
+no CPU fallback: if libskygpu.so is missing or no sm_100 device is present,
+every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "_lib", "libskygpu.so")
+
+SKYGPU_OK, SKYGPU_EINVAL, SKYGPU_ERUNTIME, SKYGPU_ECUDA, SKYGPU_ENOMEM = range(5)
+GRES_AUTO, GRES_PAIRS, GRES_CELLS = 0, 1, 2
+DEVICE_PTRS, CHECK_SKYLINE, SKIP_GRES = 1, 2, 4
+
+
+class SkyGpuError(RuntimeError):
+    """CUDA / device failure inside libskygpu (no CPU fallback exists)."""
+
+
+class Strategy(enum.IntEnum):
+    NONE = 0
+    GRID = 1
+    ANGULAR = 2
+    SLICED = 3
+
+    @classmethod
+    def from_name(cls, name: str) -> "Strategy":  # partition.cpp:43-49
+        table = {"none": cls.NONE, "grid": cls.GRID, "angular": cls.ANGULAR, "sliced": cls.SLICED}
+        if name not in table:
+            raise ValueError("unknown strategy: " + name)
+        return table[name]
+
+
+class _Plan(C.Structure):
+    _fields_ = [("strategy", C.c_int), ("slices", C.c_int), ("partitions", C.c_longlong),
+                ("dims", C.c_int)]
+
+
+class Stats(C.Structure):
+    _fields_ = [(n, C.c_uint64) for n in ("tuples_in", "tuples_into_parallel", "tuples_into_final",
+                                           "skyline_size", "skyline_tests", "gres_tests",
+                                           "gres_cells")] + \
+               [(n, C.c_int) for n in ("g_max", "gres_steps", "gres_engine", "code_bits",
+                                        "sfs_rounds", "pad_")] + \
+               [(n, C.c_double) for n in ("ms_total", "ms_h2d", "ms_skyline", "ms_gres", "ms_d2h",
+                                           "ms_gres_kernel", "ms_sky_kernel")] + \
+               [(n, C.c_uint64) for n in ("gres_kernel_launches", "sky_kernel_launches",
+                                           "kernel_launches")]
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_ if k != "pad_"}
+
+
+@dataclass
+class PartitionPlan:  # partition.hpp:27-32
+    strategy: Strategy = Strategy.NONE
+    slices: int = 1
+    partitions: int = 1
+    dims: int = 0
+
+    def _c(self) -> _Plan:
+        return _Plan(int(self.strategy), self.slices, self.partitions, self.dims)
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load the in-tree libskygpu.so (raises if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2412_02274_b200.build` "
+                              "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        vp, u64, i32, i64, sz, cp = C.c_void_p, C.c_uint64, C.c_int, C.c_longlong, C.c_size_t, C.c_char_p
+        L.skygpu_version.restype = i32
+        L.skygpu_device_count.restype = i32
+        L.skygpu_set_device.argtypes = [i32, cp, sz]
+        L.skygpu_set_stream.argtypes = [vp, cp, sz]
+        L.skygpu_make_plan.argtypes = [i32, i64, i32, C.POINTER(_Plan), cp, sz]
+        L.skygpu_parallel_skyline.argtypes = [vp, vp, u64, i32, C.POINTER(_Plan), vp, vp, u64, i32,
+                                              vp, vp, C.POINTER(Stats), cp, sz]
+        L.skygpu_grid_resistance.argtypes = [vp, vp, u64, i32, C.POINTER(_Plan), u64, i32, i32, i32,
+                                             vp, vp, C.POINTER(Stats), cp, sz]
+        L.skygpu_snap_relation.argtypes = [vp, u64, i32, vp, cp, sz]
+        L.skygpu_max_grid_intervals.argtypes = [vp, u64, i32, i32, vp, cp, sz]
+        L.skygpu_pipeline.argtypes = [vp, vp, u64, i32, C.POINTER(_Plan), i32, i32, i32, i32,
+                                      C.c_uint, vp, vp, vp, vp, C.POINTER(Stats), cp, sz]
+        L.skygpu_generate.argtypes = [i32, u64, i32, u64, vp, cp, sz]
+        _lib = L
+    return _lib
+
+
+EXPORTED_SYMBOLS = ("skygpu_version", "skygpu_device_count", "skygpu_set_device", "skygpu_set_stream",
+                    "skygpu_release", "skygpu_make_plan", "skygpu_parallel_skyline",
+                    "skygpu_grid_resistance", "skygpu_snap_relation", "skygpu_max_grid_intervals",
+                    "skygpu_pipeline", "skygpu_generate")
+
+
+def _check(rc: int, err: C.Array) -> None:
+    if rc == SKYGPU_OK:
+        return
+    msg = err.value.decode(errors="replace")
+    if rc == SKYGPU_EINVAL:
+        raise ValueError(msg)
+    if rc == SKYGPU_ERUNTIME:
+        raise RuntimeError(msg)
+    if rc == SKYGPU_ENOMEM:
+        raise MemoryError(msg)
+    raise SkyGpuError(msg)
+
+
+def _errbuf():
+    return C.create_string_buffer(1024)
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def _relation(values, ids):
+    v = np.ascontiguousarray(values, dtype=np.float64)
+    if v.ndim != 2:
+        raise ValueError("a relation is an (n, d) float64 array")
+    n = v.shape[0]
+    i = np.arange(n, dtype=np.int64) if ids is None else np.ascontiguousarray(ids, dtype=np.int64)
+    if i.shape != (n,):
+        raise ValueError("ids must have one entry per tuple")
+    return v, i
+
+
+# ------------------------------------------------------------------ API
+def make_plan(strategy, target_partitions: int, dims: int) -> PartitionPlan:
+    s = Strategy.from_name(strategy) if isinstance(strategy, str) else Strategy(strategy)
+    out = _Plan()
+    err = _errbuf()
+    _check(lib().skygpu_make_plan(int(s), int(target_partitions), int(dims), C.byref(out), err, 1024), err)
+    return PartitionPlan(Strategy(out.strategy), out.slices, out.partitions, out.dims)
+
+
+@dataclass
+class SkylineResult:
+    positions: np.ndarray  # input positions, (sum, id) order
+    ids: np.ndarray
+    values: np.ndarray
+    stats: dict = field(default_factory=dict)
+
+
+def parallel_skyline(values, ids=None, plan: PartitionPlan | None = None, reps=None,
+                     cores: int = 1) -> SkylineResult:
+    """parallel.hpp:46-47.  ``reps`` = (rep_values (k, d), rep_ids) or None."""
+    v, i = _relation(values, ids)
+    n, d = v.shape
+    plan = plan or PartitionPlan(Strategy.NONE, 1, 1, d)
+    if reps is not None and len(reps[0]):
+        rv = np.ascontiguousarray(reps[0], dtype=np.float64).reshape(-1, d)
+        ri = np.ascontiguousarray(reps[1], dtype=np.int64)
+    else:
+        rv = np.zeros((0, d)); ri = np.zeros(0, dtype=np.int64)
+    out = np.empty(max(n, 1), dtype=np.uint64)
+    cnt = np.zeros(1, dtype=np.uint64)
+    st = Stats()
+    err = _errbuf()
+    _check(lib().skygpu_parallel_skyline(_p(v), _p(i), n, d, C.byref(plan._c()), _p(rv), _p(ri),
+                                         rv.shape[0], int(cores), _p(out), _p(cnt), C.byref(st),
+                                         err, 1024), err)
+    pos = out[: int(cnt[0])].astype(np.int64)
+    return SkylineResult(pos, i[pos], v[pos], st.as_dict())
+
+
+@dataclass
+class GridResistanceResult:  # gres.hpp:56-64
+    ids: np.ndarray
+    den: np.ndarray  # denominator per input skyline tuple
+    g_max: int
+    stats: dict = field(default_factory=dict)
+
+    @property
+    def denominators(self) -> dict:
+        return {int(k): int(v) for k, v in zip(self.ids, self.den)}
+
+
+def grid_resistance(sky_values, sky_ids=None, plan: PartitionPlan | None = None, rep_count: int = 0,
+                    cores: int = 1, cap: int | None = 25, check_skyline: bool = False
+                    ) -> GridResistanceResult:
+    """gres.hpp:73-75.  ``cap=None`` = std::nullopt."""
+    v, i = _relation(sky_values, sky_ids)
+    s, d = v.shape
+    plan = plan or PartitionPlan(Strategy.NONE, 1, 1, d)
+    den = np.zeros(max(s, 1), dtype=np.int32)
+    gm = np.zeros(1, dtype=np.int32)
+    st = Stats()
+    err = _errbuf()
+    _check(lib().skygpu_grid_resistance(_p(v), _p(i), s, d, C.byref(plan._c()), int(rep_count),
+                                        int(cores), 0 if cap is None else int(cap),
+                                        1 if check_skyline else 0, _p(den), _p(gm), C.byref(st),
+                                        err, 1024), err)
+    return GridResistanceResult(i, den[:s], int(gm[0]), st.as_dict())
+
+
+def snap_relation(values, intervals: int) -> np.ndarray:
+    v = np.ascontiguousarray(values, dtype=np.float64)
+    out = np.empty_like(v)
+    err = _errbuf()
+    _check(lib().skygpu_snap_relation(_p(v), v.size, int(intervals), _p(out), err, 1024), err)
+    return out
+
+
+def snap_to_grid(values, intervals: int) -> np.ndarray:
+    return snap_relation(np.asarray(values, dtype=np.float64).reshape(1, -1), intervals)[0]
+
+
+def max_grid_intervals(values, cap: int | None) -> int:
+    v = np.ascontiguousarray(values, dtype=np.float64)
+    if v.ndim != 2:
+        raise ValueError("a relation is an (n, d) float64 array")
+    out = np.zeros(1, dtype=np.int32)
+    err = _errbuf()
+    _check(lib().skygpu_max_grid_intervals(_p(v), v.shape[0], v.shape[1], 0 if cap is None else int(cap),
+                                           _p(out), err, 1024), err)
+    return int(out[0])
+
+
+@dataclass
+class PipelineResult:
+    positions: np.ndarray
+    den: np.ndarray
+    g_max: int
+    stats: dict
+
+
+def pipeline(values, ids=None, plan: PartitionPlan | None = None, cap: int | None = 25,
+             engine: int = GRES_AUTO, shard_rank: int = 0, shard_world: int = 1,
+             check_skyline: bool = False, skip_gres: bool = False) -> PipelineResult:
+    """Skyline + grid resistance in one call (harness.cpp:208, :229-231)."""
+    v, i = _relation(values, ids)
+    n, d = v.shape
+    plan = plan or PartitionPlan(Strategy.NONE, 1, 1, d)
+    pos = np.empty(max(n, 1), dtype=np.uint64)
+    den = np.zeros(max(n, 1), dtype=np.int32)
+    s = np.zeros(1, dtype=np.uint64)
+    gm = np.zeros(1, dtype=np.int32)
+    st = Stats()
+    err = _errbuf()
+    flags = (CHECK_SKYLINE if check_skyline else 0) | (SKIP_GRES if skip_gres else 0)
+    _check(lib().skygpu_pipeline(_p(v), _p(i), n, d, C.byref(plan._c()), 0 if cap is None else int(cap),
+                                 int(engine), int(shard_rank), int(shard_world), flags, _p(pos), _p(den),
+                                 _p(s), _p(gm), C.byref(st), err, 1024), err)
+    S = int(s[0])
+    return PipelineResult(pos[:S].astype(np.int64), den[:S].copy(), int(gm[0]), st.as_dict())
+
+
+def pipeline_raw(vals_ptr: int, ids_ptr: int, n: int, d: int, plan: PartitionPlan, cap: int | None,
+                 engine: int, shard_rank: int, shard_world: int, flags: int, out_pos_ptr: int,
+                 out_den_ptr: int):
+    """Pointer-level call (host pinned or device pointers per ``flags``) used by bench.py."""
+    s = np.zeros(1, dtype=np.uint64)
+    gm = np.zeros(1, dtype=np.int32)
+    st = Stats()
+    err = _errbuf()
+    _check(lib().skygpu_pipeline(C.c_void_p(vals_ptr), C.c_void_p(ids_ptr), n, d, C.byref(plan._c()),
+                                 0 if cap is None else int(cap), int(engine), int(shard_rank),
+                                 int(shard_world), int(flags), C.c_void_p(out_pos_ptr),
+                                 C.c_void_p(out_den_ptr), _p(s), _p(gm), C.byref(st), err, 1024), err)
+    return int(s[0]), int(gm[0]), st.as_dict()
+
+
+def set_device(device: int) -> None:
+    err = _errbuf()
+    _check(lib().skygpu_set_device(int(device), err, 1024), err)
+
+
+def set_stream(stream_ptr: int | None) -> None:
+    err = _errbuf()
+    _check(lib().skygpu_set_stream(C.c_void_p(stream_ptr or 0), err, 1024), err)
+
+
+def device_count() -> int:
+    return int(lib().skygpu_device_count())
+
+
+GEN_KINDS = {"uni": 0, "ant": 1, "corr": 2, "lattice": 3}
+
+
+def generate(kind: str, n: int, d: int, seed: int) -> np.ndarray:
+    """Seeded input (datagen.cpp recipes; 'corr' = BASELINE C3)."""
+    out = np.empty((n, d), dtype=np.float64)
+    err = _errbuf()
+    _check(lib().skygpu_generate(GEN_KINDS[kind], n, d, seed, _p(out), err, 1024), err)
+    return out

@@ -1,0 +1,143 @@
+"""GPU parity: libskygpu (through its C-ABI) against the reference's golden
+outputs and against the CPU oracle on seeded inputs.  Bit-exact: skyline id
+sets and order, g_max, every denominator."""
+import numpy as np
+import pytest
+
+import paper_2412_02274_b200 as sk
+from conftest import golden_input, golden_names, load_golden, spec_cap
+from oracle import pyoracle as po
+
+pytestmark = pytest.mark.gpu
+
+
+def plan_of(g, d):
+    sp = g["spec"]
+    return sk.make_plan(sp["strategy"], sp["p"], d)
+
+
+def check_pipeline_against_golden(g, engine=sk.GRES_AUTO):
+    v, ids = golden_input(g, sk.generate)
+    n, d = v.shape
+    plan = plan_of(g, d)
+    if "error" in g:
+        with pytest.raises(ValueError) as ei:
+            sk.parallel_skyline(v, ids, plan)
+        assert str(ei.value) == g["error"]
+        return
+    sky = sk.parallel_skyline(v, ids, plan, cores=4)
+    assert sorted(sky.ids.tolist()) == g["skyline_ids"]
+    assert sky.ids.tolist() == g["skyline_order"]
+    if "gres_error" in g:
+        with pytest.raises(ValueError) as ei:
+            sk.grid_resistance(sky.values, sky.ids, plan, cap=spec_cap(g), check_skyline=True)
+        assert str(ei.value) == g["gres_error"]
+        return
+    res = sk.pipeline(v, ids, plan, cap=spec_cap(g), engine=engine)
+    assert ids[res.positions].tolist() == g["skyline_order"]
+    assert res.g_max == g["g_max"]
+    got = dict(zip(ids[res.positions].tolist(), res.den.tolist()))
+    assert [got[i] for i in g["skyline_ids"]] == g["den"]
+    # the standalone grid_resistance entry point on the reference's skyline
+    gr = sk.grid_resistance(sky.values, sky.ids, plan, cap=spec_cap(g), cores=2)
+    assert gr.g_max == g["g_max"]
+    assert [gr.denominators[i] for i in g["skyline_ids"]] == g["den"]
+
+
+@pytest.mark.parametrize("name", golden_names(exclude=("C4_", "C5_", "C1_", "C2_", "C3_")))
+def test_small_goldens(name):
+    check_pipeline_against_golden(load_golden(name))
+
+
+@pytest.mark.parametrize("name", ["C1_uni_100k_d4", "C1_uni_100k_d4_sliced16", "C2_ant_1M_d3",
+                                  "C3_corr_1M_d6", "C5_prefix_2k_d7", "C5_prefix_10k_d7",
+                                  "C4_uni_10M_d5"])
+def test_config_goldens(name):
+    check_pipeline_against_golden(load_golden(name))
+
+
+@pytest.mark.parametrize("gen,n,d,seed", [
+    ("uni", 3000, 1, 1), ("ant", 3000, 2, 2), ("lattice", 5000, 3, 3), ("uni", 20000, 6, 4),
+    ("ant", 4000, 8, 5), ("uni", 2000, 9, 6), ("ant", 1500, 12, 7), ("lattice", 3000, 10, 8),
+    ("corr", 50000, 4, 9), ("ant", 100000, 4, 10)])
+def test_random_against_oracle(gen, n, d, seed):
+    v = sk.generate(gen, n, d, seed)
+    ids = np.arange(n, dtype=np.int64)
+    pos, _ = po.skyline_sfs(v, ids)
+    res = sk.pipeline(v, ids, cap=25)
+    assert res.positions.tolist() == pos.tolist()
+    den, gm, _ = po.grid_resistance(v[pos], ids[pos], 25)
+    assert res.g_max == gm
+    assert res.den.tolist() == den.tolist()
+
+
+def test_unsorted_and_negative_ids_follow_sum_id_order():
+    rng = np.random.default_rng(3)
+    v = np.floor(rng.random((4000, 3)) * 8) / 8  # many sum ties -> id order matters
+    ids = rng.permutation(10**6)[:4000].astype(np.int64) - 500000
+    pos, _ = po.skyline_sfs(v, ids)
+    sky = sk.parallel_skyline(v, ids)
+    assert sky.positions.tolist() == pos.tolist()
+
+
+def test_reps_filtering_keeps_result():
+    v = sk.generate("ant", 5000, 3, 21)
+    base = sk.parallel_skyline(v)
+    order = np.lexsort((np.arange(5000), v.sum(axis=1)))
+    reps = (v[order[:10]], order[:10])
+    withr = sk.parallel_skyline(v, None, sk.make_plan("angular", 16, 3), reps=reps, cores=4)
+    assert sorted(withr.ids.tolist()) == sorted(base.ids.tolist())
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_shards_max_reduce_to_full_map(world):
+    v = sk.generate("ant", 20000, 5, 31)
+    full = sk.pipeline(v, cap=25)
+    acc = np.zeros_like(full.den)
+    for r in range(world):
+        part = sk.pipeline(v, cap=25, shard_rank=r, shard_world=world)
+        assert part.positions.tolist() == full.positions.tolist()
+        assert ((part.den == 0) | (part.den == full.den)).all()
+        acc = np.maximum(acc, part.den)
+    assert acc.tolist() == full.den.tolist()
+
+
+def test_api_kats():
+    # proj/tests/test_gres.cpp:26-34, 61-73, 91-97, 163-170, 172-177
+    assert sk.snap_to_grid([0.30, 0.62], 5).tolist() == [0.2, 0.6]
+    assert sk.snap_to_grid([0.0, 0.0], 7).tolist() == [0.0, 0.0]
+    with pytest.raises(ValueError, match="intervals must be >= 1"):
+        sk.snap_to_grid([0.3], 0)
+    assert sk.max_grid_intervals(np.array([[0.2], [0.7]]), None) == 2
+    assert sk.max_grid_intervals(np.array([[0.2, 0.9], [0.24, 0.9]]), None) == 25
+    assert sk.max_grid_intervals(np.array([[0.2, 0.9], [0.24, 0.9]]), 10) == 10
+    with pytest.raises(ValueError, match="all tuples are identical"):
+        sk.max_grid_intervals(np.array([[0.3, 0.3], [0.3, 0.3]]), 25)
+    with pytest.raises(ValueError, match="overflows the integer range"):
+        sk.max_grid_intervals(np.array([[0.5], [0.5 + 1e-12]]), None)
+    assert sk.max_grid_intervals(np.array([[0.5], [0.5 + 1e-12]]), 25) == 25
+    r = sk.grid_resistance(np.array([[0.5, 0.5]]), cap=25)
+    assert r.den.tolist() == [1]
+    r = sk.grid_resistance(np.array([[0.30, 0.40], [0.40, 0.30]]), cap=None)
+    assert r.g_max >= 2 and r.den.tolist() == [1, 1]
+    r = sk.grid_resistance(np.zeros((0, 2)), cap=25)
+    assert r.den.size == 0 and r.g_max == 1
+    with pytest.raises(ValueError, match="cores must be >= 1"):
+        sk.grid_resistance(np.array([[0.5, 0.5]]), cores=0)
+    with pytest.raises(ValueError, match="cores must be >= 1"):
+        sk.parallel_skyline(np.array([[0.5, 0.5]]), cores=0)
+    with pytest.raises(ValueError, match=r"input is not a skyline \(tuple 0 dominates tuple 1\)"):
+        sk.grid_resistance(np.array([[0.1, 0.1], [0.5, 0.5]]), check_skyline=True)
+    assert sk.parallel_skyline(np.zeros((0, 3))).ids.size == 0
+
+
+def test_generic_dims_and_duplicates():
+    rng = np.random.default_rng(5)
+    base = np.floor(rng.random((300, 11)) * 4) / 4
+    v = np.vstack([base, base[:50]])  # exact duplicates are all retained
+    ids = np.arange(len(v), dtype=np.int64)
+    pos, _ = po.skyline_sfs(v, ids)
+    res = sk.pipeline(v, ids, cap=None)
+    assert res.positions.tolist() == pos.tolist()
+    den, gm, _ = po.grid_resistance(v[pos], ids[pos], None)
+    assert res.g_max == gm and res.den.tolist() == den.tolist()
