@@ -66,17 +66,23 @@ void read_slots(Ctx& c, int first, int count) {
     SKY_CUDA(cudaStreamSynchronize(c.stream));
 }
 
+namespace {
+__global__ void k_init_slots(unsigned long long* slots) {
+    const int i = threadIdx.x;
+    if (i < S_COUNT_) {
+        unsigned long long v = 0;
+        if (i == S_BAD || i == S_PAIR || i == S_GRIDBAD) v = ~0ULL;
+        if (i == S_MINGAP) v = 0x7FF0000000000000ULL;
+        slots[i] = v;
+    }
+}
+}  // namespace
+
+// stream-ordered, no host synchronisation
 void zero_slots(Ctx& c) {
-    unsigned long long init[S_COUNT_];
-    for (int i = 0; i < S_COUNT_; ++i) init[i] = 0;
-    init[S_BAD] = ~0ULL;
-    init[S_PAIR] = ~0ULL;
-    init[S_GRIDBAD] = ~0ULL;
-    init[S_MINGAP] = 0x7FF0000000000000ULL;
-    memcpy(c.h_slots, init, sizeof(init));
-    SKY_CUDA(cudaMemcpyAsync(c.d_slots, c.h_slots, sizeof(init), cudaMemcpyHostToDevice,
-                             c.stream));
-    SKY_CUDA(cudaStreamSynchronize(c.stream));
+    k_init_slots<<<1, 32, 0, c.stream>>>(c.d_slots);
+    SKY_LAUNCH_CHECK();
+    note_launch(c);
 }
 
 // gres.cu

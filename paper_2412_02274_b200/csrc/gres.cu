@@ -239,6 +239,123 @@ k_gres_pairs_u8(const unsigned long long* __restrict__ codes, uint32_t S,
     add_count(tests, cnt);
 }
 
+// ---- pair engine, u8 path, all steps in ONE launch ----------------------
+// codes of every step: codes[gi*S + t] for g = g_max - gi (gi = 0 .. G-1),
+// one byte per attribute (u32 words for d <= 4, u64 for d <= 8)
+// Tiled pair kernel (all steps, one launch).  Block = 8 warps x 8
+// candidates each, over one comparator range.  For each step g (descending)
+// the range's codes at g are staged through shared memory in 2048-code tiles;
+// every lane loads one comparator code and tests it against all of its
+// warp's still-undecided candidates (register blocking: 1 LDS per 8 tests),
+// and one redux.or per 32 comparators tells the warp which candidates were
+// hit (warp-level early exit).  A hit at g is the candidate's final answer
+// (atomicMax(den, g)); candidates re-read den every step, so exits found by
+// blocks working on other comparator ranges prune this block too.
+constexpr int kTileCodes = 2048;
+constexpr int kCandPerWarp = 8;
+constexpr int kCandPerBlock = (kBlock / 32) * kCandPerWarp;
+
+template <class W>
+__device__ __forceinline__ bool dom_w(W s, W t, W tg) {
+    constexpr W H = (W)kGuard;
+    return (((tg - s) & H) == H) & (s != t);
+}
+
+template <class W>
+__global__ void k_codes_all(const double* __restrict__ v, uint64_t S, int d, int g_max, int G,
+                            W* __restrict__ codes) {
+    const uint64_t total = S * (uint64_t)G;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t gi = i / S, t = i - gi * S;
+        const double gd = (double)(g_max - (int)gi);
+        W w = 0;
+        for (int k = 0; k < d; ++k) {
+            double q = floor(__dmul_rn(v[k * S + t], gd));
+            w |= (W)(unsigned)q << (8 * k);
+        }
+        codes[i] = w;
+    }
+}
+
+template <class W>
+__global__ void __launch_bounds__(kBlock)
+k_gres_pairs_tiled(const W* __restrict__ codes, uint32_t S, int G, int g_max,
+                   const uint32_t* __restrict__ act, uint32_t na, uint32_t range,
+                   int32_t* __restrict__ den, unsigned long long* __restrict__ tests) {
+    constexpr W H = (W)kGuard;
+    __shared__ W tile[kTileCodes];
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t r0 = blockIdx.y * range;
+    const uint32_t r1 = min(S, r0 + range);
+    volatile int32_t* vden = den;
+    uint32_t t[kCandPerWarp];
+    int best[kCandPerWarp];
+    unsigned valid = 0;
+#pragma unroll
+    for (int c = 0; c < kCandPerWarp; ++c) {
+        const uint32_t idx = blockIdx.x * kCandPerBlock + warp * kCandPerWarp + c;
+        t[c] = idx < na ? act[idx] : 0;
+        best[c] = idx < na ? 0 : 0x7fffffff;
+        if (idx < na) valid |= 1u << c;
+    }
+    unsigned long long cnt = 0;
+    for (int gi = 0; gi < G; ++gi) {
+        const int g = g_max - gi;
+        unsigned alive = 0;
+#pragma unroll
+        for (int c = 0; c < kCandPerWarp; ++c) {
+            if (((valid >> c) & 1) && best[c] < g) best[c] = max(best[c], vden[t[c]]);
+            if (best[c] < g) alive |= 1u << c;
+        }
+        if (!__syncthreads_or(alive != 0)) break;
+        const W* cg = codes + (uint64_t)gi * S;
+        W tc[kCandPerWarp], tg[kCandPerWarp];
+#pragma unroll
+        for (int c = 0; c < kCandPerWarp; ++c) {
+            tc[c] = ((alive >> c) & 1) ? cg[t[c]] : (W)0;
+            tg[c] = tc[c] | H;
+        }
+        for (uint32_t base = r0; base < r1; base += kTileCodes) {
+            const uint32_t nt = min((uint32_t)kTileCodes, r1 - base);
+            for (uint32_t k = threadIdx.x; k < nt; k += kBlock) tile[k] = cg[base + k];
+            __syncthreads();
+            for (uint32_t k0 = 0; k0 < nt && alive; k0 += 32) {
+                const uint32_t k = k0 + lane;
+                unsigned hits = 0;
+                if (k < nt) {
+                    const W s = tile[k];
+#pragma unroll
+                    for (int c = 0; c < kCandPerWarp; ++c)
+                        if ((alive >> c) & 1) hits |= (unsigned)dom_w<W>(s, tc[c], tg[c]) << c;
+                    cnt += __popc(alive);
+                }
+                hits = __reduce_or_sync(0xffffffffu, hits);
+                if (hits) {
+                    alive &= ~hits;
+#pragma unroll
+                    for (int c = 0; c < kCandPerWarp; ++c)
+                        if ((hits >> c) & 1) {
+                            best[c] = g;
+                            if (lane == 0) atomicMax(&den[t[c]], g);
+                        }
+                }
+            }
+            if (!__syncthreads_or(alive != 0)) break;
+        }
+    }
+    add_count(tests, cnt);
+}
+
+__global__ void k_finalize_den(const uint32_t* __restrict__ act, uint64_t na,
+                               int32_t* __restrict__ den) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < na;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t t = act[i];
+        if (den[t] == 0) den[t] = 1;
+    }
+}
+
 // ---- pair engine, float64 path ------------------------------------------
 // psum (core.cpp:21-23 on the projection) and the (psum, id) predecessor
 // order, only consulted when ties are possible.
@@ -327,6 +444,44 @@ static int intervals_from_gap(double gap, int cap) {
     return static_cast<int>(bound);
 }
 
+// Witness for the capped branch of intervals_from_gap (gres.cpp:31): two
+// DISTINCT values of one attribute in the same bucket of width 1/(2 cap)
+// have an FP gap with 1.0/gap >= cap, and the reference's min adjacent gap
+// is <= that gap (rounding is monotone), so g_max = cap exactly.  Values
+// outside [0,1) are simply not bucketed (the witness is then inconclusive
+// only if no other pair qualifies).  Also reduces max value (code range).
+__global__ void k_gap_witness(const double* __restrict__ v, uint64_t S, int d, int cap,
+                              unsigned long long* __restrict__ table,
+                              unsigned long long* __restrict__ slots) {
+    const int nb = 2 * cap;
+    unsigned long long mx = 0;
+    bool found = false;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < S * d;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t j = i / S;
+        const double x = v[i];
+        const unsigned long long bits = ord_bits(x);
+        mx = bits > mx ? bits : mx;
+        if (!(x >= 0.0 && x < 1.0) || found) continue;
+        int b = (int)floor(__dmul_rn(x, (double)nb));
+        b = b < 0 ? 0 : (b >= nb ? nb - 1 : b);
+        const unsigned long long old = atomicCAS(&table[j * nb + b], 0ULL, bits + 1);
+        if (old != 0ULL && old != bits + 1) {
+            const unsigned long long ob = old - 1;
+            const double w = __longlong_as_double((long long)ob);
+            const double gap = x > w ? __dsub_rn(x, w) : __dsub_rn(w, x);
+            if (gap > 0.0 && __ddiv_rn(1.0, gap) >= (double)cap) found = true;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long x = __shfl_down_sync(0xffffffffu, mx, o);
+        mx = x > mx ? x : mx;
+    }
+    if ((threadIdx.x & 31) == 0) atomicMax(&slots[S_MAXV], mx);
+    if (found) atomicOr(&slots[S_FLAG], 1ULL);
+}
+
 // gres.cpp:15-28 on the device: per column sort + adjacent-difference min.
 // Returns false when every attribute is constant.
 bool min_positive_gap_device(Ctx& c, const double* d_soa, uint64_t S, int d, double* gap,
@@ -361,6 +516,29 @@ bool min_positive_gap_device(Ctx& c, const double* d_soa, uint64_t S, int d, dou
     return true;
 }
 
+// g_max of gres.cpp:89-90: the cap witness when it fires, else the exact
+// per-column sort.  Also returns the max value (code range).
+int g_max_device(Ctx& c, const double* d_soa, uint64_t S, int d, int cap, double* maxv) {
+    if (cap > 0 && cap <= 65536 && S >= 2) {
+        zero_slots(c);
+        unsigned long long* table = c.buf[B_CELLS].as<unsigned long long>((uint64_t)d * 2 * cap);
+        SKY_CUDA(cudaMemsetAsync(table, 0, sizeof(unsigned long long) * d * 2 * cap, c.stream));
+        k_gap_witness<<<grid_for(S * d, kBlock), kBlock, 0, c.stream>>>(d_soa, S, d, cap, table,
+                                                                         c.d_slots);
+        SKY_LAUNCH_CHECK();
+        note_launch(c);
+        read_slots(c, S_MAXV, 3);  // S_MAXV, S_BAD, S_FLAG
+        if (c.h_slots[S_FLAG] & 1ULL) {
+            unsigned long long mb = c.h_slots[S_MAXV];
+            memcpy(maxv, &mb, 8);
+            return cap;
+        }
+    }
+    double gap = 0;
+    if (!min_positive_gap_device(c, d_soa, S, d, &gap, maxv)) return 1;
+    return intervals_from_gap(gap, cap);
+}
+
 GresOut gres_device(Ctx& c, const double* d_skyv, const int64_t* d_ids, uint64_t S, int d,
                     int cap, int engine, int shard_rank, int shard_world, bool check_skyline,
                     int32_t* d_den) {
@@ -392,9 +570,8 @@ GresOut gres_device(Ctx& c, const double* d_skyv, const int64_t* d_ids, uint64_t
         }
     }
 
-    double gap = 0, maxv = 0;
-    const bool has_gap = min_positive_gap_device(c, d_skyv, S, d, &gap, &maxv);
-    out.g_max = has_gap ? intervals_from_gap(gap, cap) : 1;
+    double maxv = 0;
+    out.g_max = g_max_device(c, d_skyv, S, d, cap, &maxv);
     st.g_max = out.g_max;
 
     // candidate list of this shard
@@ -429,12 +606,63 @@ GresOut gres_device(Ctx& c, const double* d_skyv, const int64_t* d_ids, uint64_t
     st.gres_engine = SKYGPU_GRES_PAIRS;
     (void)engine;
 
-    unsigned long long* codes = u8 ? c.buf[B_CODES].as<unsigned long long>(S) : nullptr;
-    double* q = u8 ? nullptr : c.buf[B_PROJ].as<double>(S * d);
     cudaEvent_t e0 = c.ev[10], e1 = c.ev[11];
     double kms = 0;
     uint64_t klaunch = 0;
     int steps = 0;
+    const int G = out.g_max - 1;
+    if (u8 && G >= 1 && na > 0) {
+        // one launch for every step (north_star (b)): (candidate tile x
+        // comparator range) blocks, per-step dominance with early exit
+        const bool w32 = d <= 4;
+        void* codes = c.buf[B_CODES].get(S * (uint64_t)G * (w32 ? 4 : 8));
+        const unsigned cgrid = grid_for(S * (uint64_t)G, kBlock);
+        if (w32)
+            k_codes_all<uint32_t><<<cgrid, kBlock, 0, c.stream>>>(d_skyv, S, d, out.g_max, G,
+                                                                  (uint32_t*)codes);
+        else
+            k_codes_all<unsigned long long><<<cgrid, kBlock, 0, c.stream>>>(
+                d_skyv, S, d, out.g_max, G, (unsigned long long*)codes);
+        SKY_LAUNCH_CHECK();
+        const uint64_t cand_tiles = (na + kCandPerBlock - 1) / kCandPerBlock;
+        const uint64_t target_blocks = (uint64_t)c.num_sms * 8;
+        uint64_t ranges = (target_blocks + cand_tiles - 1) / cand_tiles;
+        const uint64_t max_ranges = (S + 255) / 256;
+        ranges = std::max<uint64_t>(1, std::min(ranges, max_ranges));
+        uint64_t range = (S + ranges - 1) / ranges;
+        range = (range + 31) / 32 * 32;
+        ranges = (S + range - 1) / range;
+        if (ranges > 65535) {
+            ranges = 65535;
+            range = (S + ranges - 1) / ranges;
+        }
+        dim3 grid((unsigned)cand_tiles, (unsigned)ranges);
+        SKY_CUDA(cudaEventRecord(e0, c.stream));
+        if (w32)
+            k_gres_pairs_tiled<uint32_t><<<grid, kBlock, 0, c.stream>>>(
+                (const uint32_t*)codes, (uint32_t)S, G, out.g_max, act, (uint32_t)na,
+                (uint32_t)range, d_den, c.d_slots + S_TESTS_GRES);
+        else
+            k_gres_pairs_tiled<unsigned long long><<<grid, kBlock, 0, c.stream>>>(
+                (const unsigned long long*)codes, (uint32_t)S, G, out.g_max, act, (uint32_t)na,
+                (uint32_t)range, d_den, c.d_slots + S_TESTS_GRES);
+        SKY_CUDA(cudaEventRecord(e1, c.stream));
+        SKY_LAUNCH_CHECK();
+        k_finalize_den<<<grid_for(na, kBlock), kBlock, 0, c.stream>>>(act, na, d_den);
+        SKY_LAUNCH_CHECK();
+        note_launch(c, 3);
+        read_slots(c, S_TESTS_GRES, 1);
+        float ms = 0;
+        SKY_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        out.steps = G;
+        st.gres_steps = G;
+        st.ms_gres_kernel += ms;
+        st.gres_kernel_launches += 1;
+        st.gres_tests = c.h_slots[S_TESTS_GRES];
+        return out;
+    }
+    unsigned long long* codes = u8 ? c.buf[B_CODES].as<unsigned long long>(S) : nullptr;
+    double* q = u8 ? nullptr : c.buf[B_PROJ].as<double>(S * d);
     for (int g = out.g_max; g >= 2 && na > 0; --g) {
         ++steps;
         if (u8) {

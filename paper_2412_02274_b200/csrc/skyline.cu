@@ -234,6 +234,99 @@ k_sfs_filter(const double* __restrict__ sv, uint64_t stride, int d,
     add_count(tests, cnt);
 }
 
+// compact SoA copy of the tuples at sorted positions list[0..m)
+__global__ void k_gather_list(const double* __restrict__ sv, uint64_t stride, int d,
+                              const uint32_t* __restrict__ list, uint64_t m,
+                              double* __restrict__ out) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m * d;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t a = i / m, k = i - a * m;
+        out[i] = sv[a * stride + list[k]];
+    }
+}
+
+// Warp-cooperative variants (warp-ballot early exit, north_star (a)): one
+// candidate per warp, its d values broadcast in registers; the 32 lanes test
+// 32 consecutive comparators per iteration (coalesced float64 SoA loads that
+// hit L1/L2: the comparator block is small and shared by every warp) and the
+// warp leaves the candidate at the first iteration whose ballot is non-zero.
+// No divergence inside a warp, no block-level barrier.
+template <int D>
+__global__ void __launch_bounds__(kBlock)
+k_sfs_intra_warp(const double* __restrict__ Av, uint32_t m, int d, uint8_t* __restrict__ keep,
+                 unsigned long long* __restrict__ tests) {
+    constexpr int DM = D > 0 ? D : kMaxDims;
+    const int dd = D > 0 ? D : d;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    unsigned long long cnt = 0;
+    for (uint32_t i = warp; i < m; i += nwarps) {
+        double t[DM];
+#pragma unroll
+        for (int k = 0; k < DM; ++k)
+            if (k < dd) t[k] = Av[(uint64_t)k * m + i];
+        bool dominated = false;
+        for (uint32_t j0 = 0; j0 < i; j0 += 32) {
+            const uint32_t j = j0 + lane;
+            bool hit = false;
+            if (j < i) {
+                double s[DM];
+#pragma unroll
+                for (int k = 0; k < DM; ++k)
+                    if (k < dd) s[k] = Av[(uint64_t)k * m + j];
+                hit = D > 0 ? dom_f64<(D > 0 ? D : 1)>(s, t) : dom_f64_dyn(s, t, dd);
+                ++cnt;
+            }
+            if (__any_sync(0xffffffffu, hit)) {
+                dominated = true;
+                break;
+            }
+        }
+        if (lane == 0) keep[i] = dominated ? 0 : 1;
+    }
+    add_count(tests, cnt);
+}
+
+template <int D>
+__global__ void __launch_bounds__(kBlock)
+k_sfs_filter_warp(const double* __restrict__ sv, uint64_t stride, int d,
+                  const uint32_t* __restrict__ C, uint32_t cn, const double* __restrict__ Pv,
+                  uint32_t np, uint8_t* __restrict__ keep, unsigned long long* __restrict__ tests) {
+    constexpr int DM = D > 0 ? D : kMaxDims;
+    const int dd = D > 0 ? D : d;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    unsigned long long cnt = 0;
+    for (uint32_t i = warp; i < cn; i += nwarps) {
+        const uint32_t p = C[i];
+        double t[DM];
+#pragma unroll
+        for (int k = 0; k < DM; ++k)
+            if (k < dd) t[k] = sv[(uint64_t)k * stride + p];
+        bool dominated = false;
+        for (uint32_t j0 = 0; j0 < np; j0 += 32) {
+            const uint32_t j = j0 + lane;
+            bool hit = false;
+            if (j < np) {
+                double s[DM];
+#pragma unroll
+                for (int k = 0; k < DM; ++k)
+                    if (k < dd) s[k] = Pv[(uint64_t)k * np + j];
+                hit = D > 0 ? dom_f64<(D > 0 ? D : 1)>(s, t) : dom_f64_dyn(s, t, dd);
+                ++cnt;
+            }
+            if (__any_sync(0xffffffffu, hit)) {
+                dominated = true;
+                break;
+            }
+        }
+        if (lane == 0) keep[i] = dominated ? 0 : 1;
+    }
+    add_count(tests, cnt);
+}
+
 __global__ void k_emit_skyline(const uint32_t* __restrict__ K, uint64_t S,
                                const double* __restrict__ sv, uint64_t n, int d,
                                const int64_t* __restrict__ sid, const uint32_t* __restrict__ spos,
@@ -397,18 +490,26 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
     cudaEvent_t e0 = c.ev[8], e1 = c.ev[9];
     double kernel_ms = 0;
     uint64_t kernel_launches = 0;
+    double* Av = c.buf[B_MISC].as<double>(std::min<uint64_t>(n, kAlphaMax) * d);
+    double* Pv = c.buf[B_CSUM].as<double>(std::min<uint64_t>(n, kAlphaMax) * d);
+    auto warp_grid = [&](uint64_t items) {
+        const uint64_t warps = std::min<uint64_t>(items, (uint64_t)c.num_sms * 64);
+        return (unsigned)std::max<uint64_t>(1, (warps * 32 + kBlock - 1) / kBlock);
+    };
     while (r > 0) {
         const uint64_t m = (r <= kFinal) ? r : std::min(alpha, r);
+        if (m > kAlphaMax) Av = c.buf[B_MISC].as<double>(m * d);
+        k_gather_list<<<grid_for(m * d, kBlock), kBlock, 0, c.stream>>>(sv, n, d, R, m, Av);
+        SKY_LAUNCH_CHECK();
         dispatch_d(d, [&](auto DC) {
             constexpr int D = decltype(DC)::value;
-            const size_t smem = sizeof(double) * tile_of<D>() * (D > 0 ? D : d);
             SKY_CUDA(cudaEventRecord(e0, c.stream));
-            k_sfs_intra<D><<<grid_for(m, kBlock, 1 << 30), kBlock, smem, c.stream>>>(
-                sv, n, d, R, (uint32_t)m, flags, c.d_slots + S_TESTS_SKY);
+            k_sfs_intra_warp<D><<<warp_grid(m), kBlock, 0, c.stream>>>(
+                Av, (uint32_t)m, d, flags, c.d_slots + S_TESTS_SKY);
             SKY_CUDA(cudaEventRecord(e1, c.stream));
         });
         SKY_LAUNCH_CHECK();
-        note_launch(c);
+        note_launch(c, 2);
         const uint64_t a = select_flagged(c, R, flags, K + kc, m);
         float ms = 0;
         SKY_CUDA(cudaEventElapsedTime(&ms, e0, e1));
@@ -418,13 +519,16 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
         ++rounds;
         if (m == r) break;
         const uint64_t cn = r - m;
+        if (a > kAlphaMax) Pv = c.buf[B_CSUM].as<double>(a * d);
+        k_gather_list<<<grid_for(a * d, kBlock), kBlock, 0, c.stream>>>(sv, n, d, K + kc - a, a,
+                                                                         Pv);
+        SKY_LAUNCH_CHECK();
+        note_launch(c);
         dispatch_d(d, [&](auto DC) {
             constexpr int D = decltype(DC)::value;
-            const size_t smem = sizeof(double) * tile_of<D>() * (D > 0 ? D : d);
             SKY_CUDA(cudaEventRecord(e0, c.stream));
-            k_sfs_filter<D><<<grid_for(cn, kBlock, 1 << 30), kBlock, smem, c.stream>>>(
-                sv, n, d, R + m, (uint32_t)cn, K + kc - a, (uint32_t)a, flags,
-                c.d_slots + S_TESTS_SKY);
+            k_sfs_filter_warp<D><<<warp_grid(cn), kBlock, 0, c.stream>>>(
+                sv, n, d, R + m, (uint32_t)cn, Pv, (uint32_t)a, flags, c.d_slots + S_TESTS_SKY);
             SKY_CUDA(cudaEventRecord(e1, c.stream));
         });
         SKY_LAUNCH_CHECK();
