@@ -67,20 +67,50 @@ void read_slots(Ctx& c, int first, int count) {
 }
 
 namespace {
-__global__ void k_init_slots(unsigned long long* slots) {
+__global__ void k_init_slots(unsigned long long* slots, int mode) {
     const int i = threadIdx.x;
-    if (i < S_COUNT_) {
-        unsigned long long v = 0;
-        if (i == S_BAD || i == S_PAIR || i == S_GRIDBAD) v = ~0ULL;
-        if (i == S_MINGAP) v = 0x7FF0000000000000ULL;
-        slots[i] = v;
+    if (i >= S_COUNT_) return;
+    if (mode == 1) {  // test counters only
+        if (i == S_TESTS_SKY || i == S_TESTS_GRES) slots[i] = 0;
+        return;
     }
+    if (mode == 2) {  // round counters only
+        if (i == S_C1 || i == S_C2 || i == S_C3) slots[i] = 0;
+        return;
+    }
+    if (mode == 3) {  // sum range only
+        if (i == S_SMIN) slots[i] = ~0ULL;
+        if (i == S_SMAX) slots[i] = 0;
+        return;
+    }
+    if (i == S_TESTS_SKY || i == S_TESTS_GRES) return;
+    unsigned long long v = 0;
+    if (i == S_BAD || i == S_PAIR || i == S_GRIDBAD || i == S_SMIN) v = ~0ULL;
+    if (i == S_MINGAP) v = 0x7FF0000000000000ULL;
+    slots[i] = v;
 }
 }  // namespace
 
-// stream-ordered, no host synchronisation
 void zero_slots(Ctx& c) {
-    k_init_slots<<<1, 32, 0, c.stream>>>(c.d_slots);
+    k_init_slots<<<1, 32, 0, c.stream>>>(c.d_slots, 0);
+    SKY_LAUNCH_CHECK();
+    note_launch(c);
+}
+
+void reset_tests(Ctx& c) {
+    k_init_slots<<<1, 32, 0, c.stream>>>(c.d_slots, 1);
+    SKY_LAUNCH_CHECK();
+    note_launch(c);
+}
+
+void reset_counts(Ctx& c) {
+    k_init_slots<<<1, 32, 0, c.stream>>>(c.d_slots, 2);
+    SKY_LAUNCH_CHECK();
+    note_launch(c);
+}
+
+void reset_range(Ctx& c) {
+    k_init_slots<<<1, 32, 0, c.stream>>>(c.d_slots, 3);
     SKY_LAUNCH_CHECK();
     note_launch(c);
 }
@@ -116,16 +146,22 @@ __global__ void k_check_values(const double* __restrict__ v, uint64_t total,
         if (!(v[i] >= 0.0)) atomicMin(&slots[S_BAD], (unsigned long long)i);
 }
 
+// Event span on the call's stream; stop() only records — the elapsed time
+// is resolved by end_stats after the call's single final synchronisation.
+struct PendingSpan {
+    int a;
+    double* dst;
+};
+PendingSpan g_spans[8];
+int g_nspans = 0;
+
 struct Timer {
     Ctx& c;
-    int a, b;
-    Timer(Ctx& cc, int ea) : c(cc), a(ea), b(ea + 1) { SKY_CUDA(cudaEventRecord(c.ev[a], c.stream)); }
-    double stop() {
-        SKY_CUDA(cudaEventRecord(c.ev[b], c.stream));
-        SKY_CUDA(cudaEventSynchronize(c.ev[b]));
-        float ms = 0;
-        SKY_CUDA(cudaEventElapsedTime(&ms, c.ev[a], c.ev[b]));
-        return ms;
+    int a;
+    Timer(Ctx& cc, int ea) : c(cc), a(ea) { SKY_CUDA(cudaEventRecord(c.ev[a], c.stream)); }
+    void stop(double* dst) {
+        SKY_CUDA(cudaEventRecord(c.ev[a + 1], c.stream));
+        if (g_nspans < 8) g_spans[g_nspans++] = PendingSpan{a, dst};
     }
 };
 
@@ -160,9 +196,30 @@ void begin_stats(Ctx& c, skygpu_stats* st) {
     c.st = st ? st : &g_scratch_stats;
     memset(c.st, 0, sizeof(skygpu_stats));
     c.launches = 0;
+    c.gres_timing_pending = false;
+    g_nspans = 0;
+    reset_tests(c);
 }
 
-void end_stats(Ctx& c) { c.st->kernel_launches = c.launches; }
+// the call's final synchronisation: test counters and event spans
+void end_stats(Ctx& c) {
+    read_slots(c, S_TESTS_SKY, 2);
+    c.st->skyline_tests = c.h_slots[S_TESTS_SKY];
+    c.st->gres_tests = c.h_slots[S_TESTS_GRES];
+    for (int i = 0; i < g_nspans; ++i) {
+        float ms = 0;
+        SKY_CUDA(cudaEventElapsedTime(&ms, c.ev[g_spans[i].a], c.ev[g_spans[i].a + 1]));
+        *g_spans[i].dst = ms;
+    }
+    g_nspans = 0;
+    if (c.gres_timing_pending) {
+        float ms = 0;
+        SKY_CUDA(cudaEventElapsedTime(&ms, c.ev[10], c.ev[11]));
+        c.st->ms_gres_kernel += ms;
+        c.gres_timing_pending = false;
+    }
+    c.st->kernel_launches = c.launches;
+}
 
 // ---- partition.cpp:13-83 plan sizing (host) ----
 constexpr long long kMaxPartitions = 1LL << 20;
@@ -304,10 +361,10 @@ int skygpu_parallel_skyline(const double* vals, const int64_t* ids, uint64_t n, 
         if (so.S)
             SKY_CUDA(cudaMemcpyAsync(pos.data(), so.d_inpos, so.S * sizeof(uint32_t),
                                      cudaMemcpyDeviceToHost, c.stream));
-        c.st->ms_total = all.stop();
+        all.stop(&c.st->ms_total);
+        end_stats(c);  // final synchronisation
         for (uint64_t k = 0; k < so.S; ++k) out_pos[k] = pos[k];
         *out_n = so.S;
-        end_stats(c);
     });
 }
 
@@ -349,7 +406,7 @@ int skygpu_grid_resistance(const double* sky_vals, const int64_t* sky_ids, uint6
                                  check_skyline != 0, den);
         SKY_CUDA(cudaMemcpyAsync(out_den, den, s * sizeof(int32_t), cudaMemcpyDeviceToHost,
                                  c.stream));
-        c.st->ms_total = all.stop();
+        all.stop(&c.st->ms_total);
         *out_g_max = go.g_max;
         end_stats(c);
     });
@@ -434,20 +491,20 @@ int skygpu_pipeline(const double* vals, const int64_t* ids, uint64_t n, int d,
                                      c.stream));
             SKY_CUDA(cudaMemcpyAsync(bi, ids, n * sizeof(int64_t), cudaMemcpyHostToDevice,
                                      c.stream));
-            c.st->ms_h2d = h2d.stop();
+            h2d.stop(&c.st->ms_h2d);
             dv = bv;
             di = bi;
         }
         Timer tsky(c, 4);
         SkylineOut so = skyline_device(c, dv, di, n, d, pl, nullptr, 0);
-        c.st->ms_skyline = tsky.stop();
+        tsky.stop(&c.st->ms_skyline);
         int32_t* den = c.buf[B_DEN].as<int32_t>(so.S ? so.S : 1);
         GresOut go;
         if (!(flags & SKYGPU_SKIP_GRES)) {
             Timer tg(c, 6);
             go = gres_device(c, so.d_skyv, so.d_ids, so.S, d, cap, gres_engine, shard_rank,
                              shard_world, (flags & SKYGPU_CHECK_SKYLINE) != 0, den);
-            c.st->ms_gres = tg.stop();
+            tg.stop(&c.st->ms_gres);
         }
         Timer d2h(c, 12);
         if (dev) {
@@ -468,8 +525,8 @@ int skygpu_pipeline(const double* vals, const int64_t* ids, uint64_t n, int d,
             SKY_CUDA(cudaStreamSynchronize(c.stream));
             for (uint64_t k = 0; k < so.S; ++k) out_pos[k] = pos[k];
         }
-        c.st->ms_d2h = d2h.stop();
-        c.st->ms_total = all.stop();
+        d2h.stop(&c.st->ms_d2h);
+        all.stop(&c.st->ms_total);
         *out_s = so.S;
         *out_g_max = go.g_max;
         end_stats(c);

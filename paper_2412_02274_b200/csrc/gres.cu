@@ -164,15 +164,13 @@ __global__ void k_project(const double* __restrict__ v, uint64_t total, int g,
         q[i] = __ddiv_rn(floor(__dmul_rn(v[i], gd)), gd);
 }
 
-// initial candidate list for this shard: interleaved chunks of 256 tuples
-__global__ void k_shard_list(uint64_t S, int rank, int world, uint32_t* __restrict__ act,
-                             unsigned long long* __restrict__ slots) {
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < S;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        if ((int)((i >> 8) % (uint64_t)world) == rank) {
-            unsigned long long pos = atomicAdd(&slots[S_SEL2], 1ULL);
-            act[pos] = (uint32_t)i;
-        }
+// candidate list of this shard, ascending: the k-th owned tuple of the
+// interleaved 256-tuple chunks rank, rank + world, rank + 2*world, ...
+__global__ void k_shard_iota(uint64_t na, int rank, int world, uint32_t* __restrict__ act) {
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < na;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t chunk = (uint64_t)rank + (uint64_t)world * (k >> 8);
+        act[k] = (uint32_t)(chunk * 256 + (k & 255));
     }
 }
 
@@ -580,22 +578,13 @@ GresOut gres_device(Ctx& c, const double* d_skyv, const int64_t* d_ids, uint64_t
     uint8_t* still = c.buf[B_FLAGS].as<uint8_t>(S);
     const unsigned gb = grid_for(S, kBlock);
     SKY_CUDA(cudaMemsetAsync(d_den, 0, S * sizeof(int32_t), c.stream));
-    zero_slots(c);
-    k_shard_list<<<gb, kBlock, 0, c.stream>>>(S, shard_rank, shard_world, act, c.d_slots);
+    uint64_t na = 0;  // owned tuples: interleaved 256-tuple chunks (load balance)
+    for (uint64_t ch = shard_rank; ch * 256 < S; ch += shard_world)
+        na += std::min<uint64_t>(256, S - ch * 256);
+    k_shard_iota<<<grid_for(na ? na : 1, kBlock), kBlock, 0, c.stream>>>(na, shard_rank,
+                                                                           shard_world, act);
     SKY_LAUNCH_CHECK();
     note_launch(c);
-    read_slots(c, S_SEL2, 1);
-    uint64_t na = c.h_slots[S_SEL2];
-    if (shard_world > 1) {  // keep ascending order for coalesced candidate reads
-        size_t tmp = 0;
-        SKY_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, act, act2, (int64_t)na, 0, 32,
-                                                 c.stream));
-        void* t = c.buf[B_CUB].get(tmp);
-        SKY_CUDA(cub::DeviceRadixSort::SortKeys(t, tmp, act, act2, (int64_t)na, 0, 32,
-                                                 c.stream));
-        note_launch(c, 4);
-        std::swap(act, act2);
-    }
 
     // path selection (see file header)
     const double code_max = std::floor(maxv * (double)out.g_max);
@@ -651,14 +640,10 @@ GresOut gres_device(Ctx& c, const double* d_skyv, const int64_t* d_ids, uint64_t
         k_finalize_den<<<grid_for(na, kBlock), kBlock, 0, c.stream>>>(act, na, d_den);
         SKY_LAUNCH_CHECK();
         note_launch(c, 3);
-        read_slots(c, S_TESTS_GRES, 1);
-        float ms = 0;
-        SKY_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        c.gres_timing_pending = true;  // resolved after the call's final sync
         out.steps = G;
         st.gres_steps = G;
-        st.ms_gres_kernel += ms;
         st.gres_kernel_launches += 1;
-        st.gres_tests = c.h_slots[S_TESTS_GRES];
         return out;
     }
     unsigned long long* codes = u8 ? c.buf[B_CODES].as<unsigned long long>(S) : nullptr;
@@ -706,8 +691,6 @@ GresOut gres_device(Ctx& c, const double* d_skyv, const int64_t* d_ids, uint64_t
     st.gres_steps = steps;
     st.ms_gres_kernel += kms;
     st.gres_kernel_launches += klaunch;
-    read_slots(c, S_TESTS_GRES, 1);
-    st.gres_tests = c.h_slots[S_TESTS_GRES];
     return out;
 }
 

@@ -82,6 +82,12 @@ enum Slot {
     S_PAIR = 7,        // check_skyline: min (a*S + b) (~0 = none)
     S_SEL2 = 8,
     S_GRIDBAD = 9,     // first flat index of a Grid value outside [0,1]
+    S_SMIN = 10,       // ord bits of the min / max tuple sum (skyline rounds)
+    S_SMAX = 11,
+    S_THR = 12,        // bits of the prefix threshold T (double)
+    S_C1 = 13,         // prefix size
+    S_C2 = 14,         // new skyline tuples of the round
+    S_C3 = 15,         // survivors of the round
     S_COUNT_ = 16
 };
 
@@ -96,6 +102,7 @@ struct Ctx {
     skygpu_stats* st = nullptr;
     uint64_t launches = 0;
     int num_sms = 148;
+    bool gres_timing_pending = false;  // ev[10]/ev[11] span awaiting the final sync
 };
 
 Ctx& ctx();  // current device's context (created lazily)
@@ -104,7 +111,13 @@ inline void note_launch(Ctx& c, uint64_t k = 1) { c.launches += k; }
 
 // Read `count` slots back (synchronises the stream).
 void read_slots(Ctx& c, int first, int count);
+// Stream-ordered (re)initialisation of the scalar slots, no host sync.
+// zero_slots keeps the two test counters; reset_tests clears them;
+// reset_counts clears only the round counters S_C1..S_C3.
 void zero_slots(Ctx& c);
+void reset_tests(Ctx& c);
+void reset_counts(Ctx& c);
+void reset_range(Ctx& c);  // S_SMIN / S_SMAX
 
 // ---------------------------------------------------------------- dominance
 // s dominates t on D float64 attributes (branch-free form of core.hpp:55-67).
