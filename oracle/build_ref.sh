@@ -44,3 +44,25 @@ build_variant rel -O3 -DNDEBUG
 $CXX $COMMON -O2 -I"$REF/include" "$HERE/refdrive.cpp" "$OUT/libskypar_chk.a" -o "$OUT/refdrive_chk"
 $CXX $COMMON -O3 -DNDEBUG -I"$REF/include" "$HERE/refdrive.cpp" "$OUT/libskypar_rel.a" -o "$OUT/refdrive"
 echo "build_ref: ok -> $OUT"
+
+# ---- drop-in link test: the reference's acceptance suite and library objects
+# with parallel.o and gres.o REPLACED by the GPU adapter
+ROOT="$(cd "$HERE/.." && pwd)"
+LIBDIR="$ROOT/paper_2412_02274_b200/_lib"
+if [ -f "$LIBDIR/libskygpu.so" ]; then
+  for v in chk rel; do
+    if [ "$v" = chk ]; then VF="-O2 -g"; else VF="-O3 -DNDEBUG"; fi
+    $CXX $COMMON $VF -I"$ROOT/include" -c "$ROOT/paper_2412_02274_b200/adapter/skypar_gpu.cpp" \
+        -o "$OUT/$v/skypar_gpu.o"
+    rm -f "$OUT/libskypar_gpu_$v.a"
+    ar rcs "$OUT/libskypar_gpu_$v.a" "$OUT/$v/core.o" "$OUT/$v/oracle.o" "$OUT/$v/partition.o" \
+        "$OUT/$v/datagen.o" "$OUT/$v/metrics.o" "$OUT/$v/harness.o" "$OUT/$v/skypar_gpu.o"
+  done
+  RPATH="-Wl,-rpath,\$ORIGIN/../../paper_2412_02274_b200/_lib"
+  $CXX $COMMON -O2 "$REF/tests/acceptance_main.cpp" "$OUT/libskypar_gpu_chk.a" -L"$LIBDIR" -lskygpu \
+      $RPATH -o "$OUT/acceptance_gpu"
+  $CXX $COMMON -O2 "$REF/tests/acceptance_main.cpp" "$OUT/libskypar_chk.a" -o "$OUT/acceptance_ref"
+  $CXX $COMMON -O3 -DNDEBUG -I"$REF/include" "$HERE/refdrive.cpp" "$OUT/libskypar_gpu_rel.a" \
+      -L"$LIBDIR" -lskygpu $RPATH -o "$OUT/refdrive_gpu"
+  echo "build_ref: drop-in binaries ok (acceptance_gpu, refdrive_gpu)"
+fi

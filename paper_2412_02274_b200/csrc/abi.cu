@@ -404,6 +404,8 @@ int skygpu_grid_resistance(const double* sky_vals, const int64_t* sky_ids, uint6
         aos_to_soa(c, dv, s, d, soa);
         GresOut go = gres_device(c, soa, di, s, d, cap, SKYGPU_GRES_AUTO, 0, 1,
                                  check_skyline != 0, den);
+        if (plan && plan->strategy == SKYGPU_GRID && go.g_max >= 2)
+            check_grid_projection(c, soa, s, d, go.g_max);
         SKY_CUDA(cudaMemcpyAsync(out_den, den, s * sizeof(int32_t), cudaMemcpyDeviceToHost,
                                  c.stream));
         all.stop(&c.st->ms_total);

@@ -695,3 +695,43 @@ GresOut gres_device(Ctx& c, const double* d_skyv, const int64_t* d_ids, uint64_t
 }
 
 }  // namespace skygpu
+
+namespace skygpu {
+
+namespace {
+// Grid plan inside the scan (gres.cpp:94-102 -> partition.cpp:88-95): the
+// first projection floor(v*g)/g outside [0,1], in input (tuple, attribute)
+// order, at the first step g = g_max.
+__global__ void k_grid_projection_range(const double* __restrict__ v, uint64_t S, int d, int g,
+                                        unsigned long long* __restrict__ slots) {
+    const double gd = (double)g;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < S * d;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t a = i / S, t = i - a * S;
+        const double q = __ddiv_rn(floor(__dmul_rn(v[i], gd)), gd);
+        if (q < 0.0 || q > 1.0) atomicMin(&slots[S_GRIDBAD], t * d + a);
+    }
+}
+}  // namespace
+
+void check_grid_projection(Ctx& c, const double* d_skyv, uint64_t S, int d, int g) {
+    zero_slots(c);
+    k_grid_projection_range<<<grid_for(S * d, 256), 256, 0, c.stream>>>(d_skyv, S, d, g,
+                                                                         c.d_slots);
+    SKY_LAUNCH_CHECK();
+    note_launch(c);
+    read_slots(c, S_GRIDBAD, 1);
+    if (c.h_slots[S_GRIDBAD] != ~0ULL) {
+        const uint64_t flat = c.h_slots[S_GRIDBAD];
+        const uint64_t t = flat / d, a = flat % d;
+        double v = 0;
+        SKY_CUDA(cudaMemcpyAsync(&v, d_skyv + a * S + t, sizeof(double), cudaMemcpyDeviceToHost,
+                                 c.stream));
+        SKY_CUDA(cudaStreamSynchronize(c.stream));
+        const double q = std::floor(v * g) / g;
+        invalid("grid_cell: value " + std::to_string(q) + " in attribute " +
+                std::to_string(a + 1) + " outside [0,1]; normalize the data first");
+    }
+}
+
+}  // namespace skygpu

@@ -201,6 +201,10 @@ GresOut gres_device(Ctx& c, const double* d_skyv, const int64_t* d_ids, uint64_t
                     int cap, int engine, int shard_rank, int shard_world, bool check_skyline,
                     int32_t* d_den);
 
+// Grid plan inside the scan: throw the reference's grid_cell error when a
+// projection at step g leaves [0,1]
+void check_grid_projection(Ctx& c, const double* d_skyv, uint64_t S, int d, int g);
+
 // float64 AoS -> SoA transpose on the device
 void aos_to_soa(Ctx& c, const double* d_aos, uint64_t n, int d, double* d_soa);
 
