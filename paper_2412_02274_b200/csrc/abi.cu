@@ -52,11 +52,21 @@ Ctx& ctx() {
         SKY_CUDA(cudaMalloc(&c->d_slots, sizeof(unsigned long long) * S_COUNT_));
         SKY_CUDA(cudaMallocHost(&c->h_slots, sizeof(unsigned long long) * S_COUNT_));
         for (auto& ev : c->ev) SKY_CUDA(cudaEventCreate(&ev));
+        const char* tr = getenv("SKYGPU_TRACE");
+        c->trace = tr && tr[0] == '1';
+        if (c->trace)
+            for (auto& ev : c->tev) SKY_CUDA(cudaEventCreate(&ev));
         g_ctx[dev] = c;
     }
     Ctx& c = *g_ctx[dev];
     c.stream = g_user_stream_set[dev] ? g_user_stream[dev] : c.own;
     return c;
+}
+
+void trace_mark(Ctx& c, const char* label) {
+    if (!c.trace || c.ntrace >= 96) return;
+    c.tlabel[c.ntrace] = label;
+    SKY_CUDA(cudaEventRecord(c.tev[c.ntrace++], c.stream));
 }
 
 void read_slots(Ctx& c, int first, int count) {
@@ -198,6 +208,8 @@ void begin_stats(Ctx& c, skygpu_stats* st) {
     c.launches = 0;
     c.gres_timing_pending = false;
     g_nspans = 0;
+    c.ntrace = 0;
+    trace_mark(c, "begin");
     reset_tests(c);
 }
 
@@ -219,6 +231,18 @@ void end_stats(Ctx& c) {
         c.gres_timing_pending = false;
     }
     c.st->kernel_launches = c.launches;
+    if (c.trace && c.ntrace > 1) {
+        for (int i = 1; i < c.ntrace; ++i) {
+            float ms = 0;
+            SKY_CUDA(cudaEventElapsedTime(&ms, c.tev[i - 1], c.tev[i]));
+            fprintf(stderr, "[skygpu trace] %8.1f us  %s\n", ms * 1e3, c.tlabel[i]);
+        }
+        float tot = 0;
+        SKY_CUDA(cudaEventElapsedTime(&tot, c.tev[0], c.tev[c.ntrace - 1]));
+        fprintf(stderr, "[skygpu trace] %8.1f us  TOTAL (%llu launches)\n", tot * 1e3,
+                (unsigned long long)c.launches);
+    }
+    c.ntrace = 0;
 }
 
 // ---- partition.cpp:13-83 plan sizing (host) ----
@@ -508,6 +532,7 @@ int skygpu_pipeline(const double* vals, const int64_t* ids, uint64_t n, int d,
                              shard_world, (flags & SKYGPU_CHECK_SKYLINE) != 0, den);
             tg.stop(&c.st->ms_gres);
         }
+        trace_mark(c, "gres: finalize");
         Timer d2h(c, 12);
         if (dev) {
             // outputs stay on the device; positions widened to u64

@@ -569,7 +569,9 @@ GresOut gres_device(Ctx& c, const double* d_skyv, const int64_t* d_ids, uint64_t
     }
 
     double maxv = 0;
+    trace_mark(c, "gres: start");
     out.g_max = g_max_device(c, d_skyv, S, d, cap, &maxv);
+    trace_mark(c, "gres: g_max (witness/sort + sync)");
     st.g_max = out.g_max;
 
     // candidate list of this shard
@@ -626,6 +628,7 @@ GresOut gres_device(Ctx& c, const double* d_skyv, const int64_t* d_ids, uint64_t
             range = (S + ranges - 1) / ranges;
         }
         dim3 grid((unsigned)cand_tiles, (unsigned)ranges);
+        trace_mark(c, "gres: shard list + codes");
         SKY_CUDA(cudaEventRecord(e0, c.stream));
         if (w32)
             k_gres_pairs_tiled<uint32_t><<<grid, kBlock, 0, c.stream>>>(
@@ -637,6 +640,7 @@ GresOut gres_device(Ctx& c, const double* d_skyv, const int64_t* d_ids, uint64_t
                 (uint32_t)range, d_den, c.d_slots + S_TESTS_GRES);
         SKY_CUDA(cudaEventRecord(e1, c.stream));
         SKY_LAUNCH_CHECK();
+        trace_mark(c, "gres: tiled pair kernel");
         k_finalize_den<<<grid_for(na, kBlock), kBlock, 0, c.stream>>>(act, na, d_den);
         SKY_LAUNCH_CHECK();
         note_launch(c, 3);

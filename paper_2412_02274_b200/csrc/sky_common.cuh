@@ -103,7 +103,16 @@ struct Ctx {
     uint64_t launches = 0;
     int num_sms = 148;
     bool gres_timing_pending = false;  // ev[10]/ev[11] span awaiting the final sync
+    // SKYGPU_TRACE=1: device timestamps between phases (events only, no sync),
+    // printed to stderr at the end of the call
+    bool trace = false;
+    int ntrace = 0;
+    cudaEvent_t tev[96];
+    const char* tlabel[96];
 };
+
+// record a labelled device timestamp when tracing is on
+void trace_mark(Ctx& c, const char* label);
 
 Ctx& ctx();  // current device's context (created lazily)
 

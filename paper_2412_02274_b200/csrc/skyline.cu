@@ -554,6 +554,7 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
 
     zero_slots(c);
     auto* keys = c.buf[B_KEY0].as<unsigned long long>(n);
+    trace_mark(c, "sky: start");
     k_score<<<gb, kBlock, 0, c.stream>>>(d_vals, n, d, keys, c.d_slots);
     SKY_LAUNCH_CHECK();
     k_ids_check<<<gb, kBlock, 0, c.stream>>>(d_ids, n, c.d_slots);
@@ -617,7 +618,9 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
         reset_counts(c);
         uint32_t* Pfull = c.buf[B_IDX0].as<uint32_t>(r);
         unsigned long long* Pkey = c.buf[B_KEY1].as<unsigned long long>(r);
+        trace_mark(c, "sky: range/hist/threshold");
         select_if(c, R, r, BelowThreshold{keys, c.d_slots + S_THR}, Pfull, c.d_slots + S_C1);
+        trace_mark(c, "sky: select prefix");
         note_launch(c, 2);
         read_slots(c, S_BAD, 11);
         if (!checked) {
@@ -667,6 +670,7 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
 
         // ---- K4: SFS inside the prefix
         double* Av = c.buf[B_MISC].as<double>(m * d);
+        trace_mark(c, "sky: (sync) + sort prefix");
         k_gather_aos<<<grid_for(m * d, kBlock), kBlock, 0, c.stream>>>(d_vals, d, order, m,
                                                                         nullptr, Av);
         SKY_LAUNCH_CHECK();
@@ -675,6 +679,7 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
         SKY_CUDA(cudaEventRecord(e0, c.stream));
         dispatch_d(d, [&](auto DC) {
             constexpr int D = decltype(DC)::value;
+            trace_mark(c, "sky: gather prefix");
             k_sfs_intra_warp<D><<<(unsigned)((wi * 32 + kBlock - 1) / kBlock), kBlock, 0,
                                   c.stream>>>(Av, (uint32_t)m, d, keep, c.d_slots + S_TESTS_SKY);
         });
@@ -747,6 +752,7 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
         SKY_CUDA(cudaEventRecord(e2, c.stream));
         dispatch_d(d, [&](auto DC) {
             constexpr int D = decltype(DC)::value;
+            trace_mark(c, "sky: select A' + cells + gather Pv");
             k_sfs_filter_cells<D><<<(unsigned)((wf * 32 + kBlock - 1) / kBlock), kBlock, 0,
                                     c.stream>>>(d_vals, d, keys, R, (uint32_t)r, Pv, (uint32_t)m,
                                                 seg, mcell, c.d_slots, fkeep,
@@ -755,7 +761,9 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
         SKY_CUDA(cudaEventRecord(e3, c.stream));
         SKY_LAUNCH_CHECK();
         note_launch(c, 2);
+        trace_mark(c, "sky: K5 filter kernel");
         select_flags(c, R, r, fkeep, Rnext, c.d_slots + S_C3);
+        trace_mark(c, "sky: select survivors");
         kernel_launches += 1;
         read_slots(c, S_C2, 2);  // S_C2 (A'), S_C3 (survivors)
         float ms = 0;
@@ -780,6 +788,7 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
     out.d_ids = c.buf[B_SKYID].as<int64_t>(kc);
     out.d_skyv = c.buf[B_SKYV].as<double>(kc * d);
     if (kc) {
+        trace_mark(c, "sky: rounds done (sync)");
         k_emit_skyline<<<grid_for(kc, kBlock), kBlock, 0, c.stream>>>(K, kc, d_vals, d, d_ids,
                                                                       out.d_ids, out.d_skyv);
         SKY_LAUNCH_CHECK();
