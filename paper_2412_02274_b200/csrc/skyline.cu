@@ -10,22 +10,27 @@
 // This equals the skyline except in the FP-tie case of SURVEY.md §7.4 item 1,
 // where it reproduces parallel_skyline (not skyline_bruteforce) exactly.
 //
-// GPU algorithm — prefix rounds (no full sort of the relation):
-//   K1 score     left-to-right __dadd_rn sum -> key bits, min/max sum, contract
-//                checks (one HBM pass over the relation)
-//   K2 histogram of the undecided tuples' sums -> threshold T such that about
-//                k tuples have sum < T.  {sum < T} is a PREFIX of the (sum, id)
-//                order, so it can be decided on its own:
-//   K3 select    the prefix (warp-aggregated compaction)
-//   -- CUB radix sort of the prefix by (sum, id)  (k items, not n)
-//   K4 intra     warp-per-candidate SFS inside the prefix (warp-ballot exit)
-//                -> new skyline tuples A' (appended to the output in order)
-//   K5 filter    every other undecided tuple against A' (warp-per-candidate,
-//                coalesced float64 SoA comparator loads, ballot exit); the
-//                survivors become the next round's undecided set.
-// Because the lowest-sum tuples are the strongest dominators, one round of
-// k = 16384 leaves ~10^3 survivors out of 10^6 on the benchmark data; large
-// skylines (ANT d=7) grow k up to 65536 per round.
+// GPU algorithm — prefix rounds, no sort of the relation:
+//   K1 score     left-to-right __dadd_rn sum -> order-preserving key bits,
+//                contract checks (one HBM pass over the relation)
+//   K2 sample    one CTA sorts a strided sample of the undecided keys ->
+//                threshold T with about k keys below it.  {key < T} is a
+//                PREFIX of the (sum, id) order: every predecessor of a prefix
+//                member is in the prefix, so the prefix can be decided alone.
+//   K3 select    the prefix (order-preserving compaction)
+//   K3b sort     the prefix by (sum, id): one-launch rank sort (k <= 16384)
+//   K4 intra     warp-per-candidate: each prefix member against its
+//                predecessors in sum order (strongest first), warp-ballot
+//                exit at the first dominator -> new skyline tuples A', already
+//                in the reference's output order
+//   K5 filter    every other undecided tuple against A' regrouped by
+//                direction cell (own cell first, coalesced float64 SoA loads,
+//                ballot exit); survivors are the next round's undecided set.
+// The lowest-sum tuples are the strongest dominators: one round of k ~ 12k
+// leaves ~10^3 survivors out of 10^6 on the benchmark data; large skylines
+// (ANT d=7) grow k up to 65536 per round.  The direction cells are the GPU
+// recast of the paper's angular partitioning: they only decide the SCAN
+// ORDER (how fast a dominator is met), never the result.
 #include <cub/cub.cuh>
 
 #include "sky_common.cuh"
@@ -35,7 +40,9 @@ namespace skygpu {
 namespace {
 
 constexpr int kBlock = 256;
-constexpr int kHistBins = 4096;
+constexpr int kCTAItems = 16;
+constexpr uint32_t kCTACap = 1024 * kCTAItems;  // single-CTA helpers up to 16384 items
+constexpr uint32_t kMaxCells = 4096;
 
 template <class F>
 void dispatch_d(int d, F&& f) {
@@ -52,16 +59,11 @@ void dispatch_d(int d, F&& f) {
     }
 }
 
-__device__ __forceinline__ double slot_double(const unsigned long long* slots, int i) {
-    return __longlong_as_double((long long)slots[i]);
-}
-
 // K1 (core.cpp:21-23): sum with __dadd_rn from +0.0, key = ord bits (sums
-// are never -0.0: 0.0 + -0.0 = +0.0), min/max of the sums, value contract.
+// are never -0.0: 0.0 + -0.0 = +0.0), value contract (Relation::add).
 __global__ void k_score(const double* __restrict__ v, uint64_t n, int d,
                         unsigned long long* __restrict__ key,
                         unsigned long long* __restrict__ slots) {
-    unsigned long long mn = ~0ULL, mx = 0;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x) {
         double s = 0.0;
@@ -71,22 +73,8 @@ __global__ void k_score(const double* __restrict__ v, uint64_t n, int d,
             bad |= !(x >= 0.0);  // negative or NaN
             s = __dadd_rn(s, x);
         }
-        const unsigned long long b = ord_bits(s);
-        key[i] = b;
-        mn = b < mn ? b : mn;
-        mx = b > mx ? b : mx;
+        key[i] = ord_bits(s);
         if (bad) atomicMin(&slots[S_BAD], static_cast<unsigned long long>(i));
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        unsigned long long a = __shfl_down_sync(0xffffffffu, mn, o);
-        unsigned long long b = __shfl_down_sync(0xffffffffu, mx, o);
-        mn = a < mn ? a : mn;
-        mx = b > mx ? b : mx;
-    }
-    if ((threadIdx.x & 31) == 0) {
-        atomicMin(&slots[S_SMIN], mn);
-        atomicMax(&slots[S_SMAX], mx);
     }
 }
 
@@ -108,138 +96,169 @@ __global__ void k_grid_range(const double* __restrict__ v, uint64_t total,
     }
 }
 
-// min / max sum of the undecided set (rounds >= 2)
-__global__ void k_range(const unsigned long long* __restrict__ key, const uint32_t* __restrict__ R,
-                        uint64_t r, unsigned long long* __restrict__ slots) {
-    unsigned long long mn = ~0ULL, mx = 0;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < r;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        const unsigned long long b = key[R[i]];
-        mn = b < mn ? b : mn;
-        mx = b > mx ? b : mx;
+// K2: threshold key T with about `want` undecided keys below it.  One block
+// sorts a strided sample of 4096 keys; T = (q-th sample) + 1 for
+// q = want * 4096 / r, so at least that sample is selected (progress).  The
+// keys are order-preserving bits of the sums, so {key < T} is a prefix of
+// the (sum, id) order.  want >= r takes everything.
+constexpr int kSampleItems = 4;
+__global__ void __launch_bounds__(1024)
+k_sample_threshold(const unsigned long long* __restrict__ key, const uint32_t* __restrict__ R,
+                   uint64_t r, uint64_t want, unsigned long long* __restrict__ slots) {
+    using Sort = cub::BlockRadixSort<unsigned long long, 1024, kSampleItems>;
+    __shared__ typename Sort::TempStorage tmp;
+    constexpr uint64_t NS = 1024 * kSampleItems;
+    if (want >= r) {
+        if (threadIdx.x == 0) slots[S_THR] = ~0ULL;
+        return;
     }
+    unsigned long long items[kSampleItems];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        unsigned long long a = __shfl_down_sync(0xffffffffu, mn, o);
-        unsigned long long b = __shfl_down_sync(0xffffffffu, mx, o);
-        mn = a < mn ? a : mn;
-        mx = b > mx ? b : mx;
+    for (int j = 0; j < kSampleItems; ++j) {
+        const uint64_t s = threadIdx.x * kSampleItems + j;
+        const uint64_t pos = s * r / NS;
+        const uint32_t t = R ? R[pos] : (uint32_t)pos;
+        items[j] = key[t];
     }
-    if ((threadIdx.x & 31) == 0) {
-        atomicMin(&slots[S_SMIN], mn);
-        atomicMax(&slots[S_SMAX], mx);
-    }
-}
-
-// K2a: histogram of the undecided tuples' sums over [min, max]
-__global__ void k_hist(const unsigned long long* __restrict__ key, const uint32_t* __restrict__ R,
-                       uint64_t r, const unsigned long long* __restrict__ slots,
-                       unsigned* __restrict__ hist) {
-    __shared__ unsigned h[kHistBins];
-    for (int b = threadIdx.x; b < kHistBins; b += blockDim.x) h[b] = 0;
-    __syncthreads();
-    const double lo = slot_double(slots, S_SMIN), hi = slot_double(slots, S_SMAX);
-    const double scale = hi > lo ? (double)kHistBins / (hi - lo) : 0.0;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < r;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t t = R ? R[i] : (uint32_t)i;
-        const double s = __longlong_as_double((long long)key[t]);
-        int b = (int)((s - lo) * scale);
-        b = b < 0 ? 0 : (b >= kHistBins ? kHistBins - 1 : b);
-        atomicAdd(&h[b], 1u);
-    }
-    __syncthreads();
-    for (int b = threadIdx.x; b < kHistBins; b += blockDim.x)
-        if (h[b]) atomicAdd(&hist[b], h[b]);
-}
-
-// K2b: threshold T with about `want` undecided sums below it (one block).
-// Progress is guaranteed: T > min sum.  want >= r selects everything.
-__global__ void k_threshold(const unsigned* __restrict__ hist, uint64_t r, uint64_t want,
-                            unsigned long long* __restrict__ slots) {
-    __shared__ unsigned long long part[1024];
-    const int per = kHistBins / 1024;
-    unsigned long long local = 0;
-    for (int k = 0; k < per; ++k) local += hist[threadIdx.x * per + k];
-    part[threadIdx.x] = local;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const double lo = slot_double(slots, S_SMIN), hi = slot_double(slots, S_SMAX);
-        double T = __longlong_as_double(0x7FF0000000000000LL);  // +inf: take all
-        if (want < r && hi > lo) {
-            unsigned long long cum = 0;
-            int bin = kHistBins - 1;
-            for (int t = 0; t < 1024; ++t) {
-                if (cum + part[t] >= want) {
-                    for (int k = 0; k < per; ++k) {
-                        cum += hist[t * per + k];
-                        if (cum >= want) {
-                            bin = t * per + k;
-                            break;
-                        }
-                    }
-                    break;
-                }
-                cum += part[t];
-            }
-            T = lo + (double)(bin + 1) * ((hi - lo) / (double)kHistBins);
-            const double nxt = __longlong_as_double((long long)(slots[S_SMIN] + 1));
-            if (T < nxt) T = nxt;  // at least the minimum is selected
-            if (bin == kHistBins - 1) T = __longlong_as_double(0x7FF0000000000000LL);
-        }
-        slots[S_THR] = (unsigned long long)__double_as_longlong(T);
+    Sort(tmp).Sort(items);
+    uint64_t q = want * NS / r;
+    if (q >= NS) q = NS - 1;
+    if (threadIdx.x == q / kSampleItems) {
+#pragma unroll
+        for (int j = 0; j < kSampleItems; ++j)
+            if (j == (int)(q % kSampleItems)) slots[S_THR] = items[j] + 1;
     }
 }
 
-// warp-aggregated append of `pred` items; returns this lane's slot
-__device__ __forceinline__ uint32_t warp_append(bool pred, unsigned long long* counter) {
-    const unsigned mask = __ballot_sync(0xffffffffu, pred);
-    const uint32_t lane = threadIdx.x & 31;
-    unsigned long long base = 0;
-    if (mask) {
-        const int leader = __ffs(mask) - 1;
-        if ((int)lane == leader) base = atomicAdd(counter, (unsigned long long)__popc(mask));
-        base = __shfl_sync(0xffffffffu, base, leader);
-    }
-    return (uint32_t)(base + __popc(mask & ((1u << lane) - 1)));
-}
-
-// K3 predicate: the prefix {sum < T} of the undecided set (selected with an
-// order-preserving CUB DeviceSelect so ties in the sum keep index order)
+// K3 predicate: the prefix {key < T} of the undecided set
 struct BelowThreshold {
     const unsigned long long* key;
     const unsigned long long* thr;
-    __device__ __forceinline__ bool operator()(uint32_t t) const {
-        return __longlong_as_double((long long)key[t]) < __longlong_as_double((long long)*thr);
-    }
+    __device__ __forceinline__ bool operator()(uint32_t t) const { return key[t] < *thr; }
 };
 
-__global__ void k_id_keys(const int64_t* __restrict__ ids, const uint32_t* __restrict__ list,
-                          uint64_t m, unsigned long long* __restrict__ out) {
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
-         i += (uint64_t)gridDim.x * blockDim.x)
-        out[i] = static_cast<unsigned long long>(ids[list[i]]) ^ 0x8000000000000000ULL;
+// Direction cell of a tuple: a grid over its first d-1 normalised
+// coordinates u_j = t_j / sum(t) (a cheap stand-in for the paper's angular
+// coordinates, partition.cpp:139-174).  A dominator s of t lies in the
+// orthant below t; on large-skyline data (tuples near a hyperplane) that
+// means a nearby direction, so scanning t's own cell first finds it early.
+template <int DM>
+__device__ __forceinline__ uint32_t direction_cell(const double* t, int dd, int m) {
+    if (dd < 2 || m <= 1) return 0;
+    double s = 0.0;
+    for (int k = 0; k < DM; ++k)
+        if (k < dd) s += t[k];
+    if (!(s > 0.0)) return 0;
+    const double inv = (double)m / s;
+    uint32_t cell = 0;
+    for (int k = DM - 2; k >= 0; --k) {
+        if (k >= dd - 1) continue;
+        int b = (int)(t[k] * inv);
+        b = b < 0 ? 0 : (b >= m ? m - 1 : b);
+        cell = cell * (uint32_t)m + (uint32_t)b;
+    }
+    return cell;
 }
 
-__global__ void k_keys_of(const unsigned long long* __restrict__ key,
-                          const uint32_t* __restrict__ list, uint64_t m,
-                          unsigned long long* __restrict__ out) {
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
-         i += (uint64_t)gridDim.x * blockDim.x)
-        out[i] = key[list[i]];
+// K3b: cell of every prefix member, then a one-CTA counting sort by cell
+// (m <= 16384): cell-ordered list + cell keys.  Order inside a cell is free.
+template <int D>
+__global__ void __launch_bounds__(1024)
+k_cell_order(const double* __restrict__ v, int d, const uint32_t* __restrict__ in, uint32_t mcap,
+             const unsigned long long* __restrict__ count, int mcell, uint32_t ncells,
+             uint32_t* __restrict__ out, uint32_t* __restrict__ out_cell) {
+    constexpr int DM = D > 0 ? D : kMaxDims;
+    const int dd = D > 0 ? D : d;
+    const uint32_t m = count ? (uint32_t)*count : mcap;
+    __shared__ uint32_t cnt[kMaxCells];
+    for (uint32_t c = threadIdx.x; c < ncells; c += 1024) cnt[c] = 0;
+    __syncthreads();
+    uint32_t cl[kCTAItems];
+#pragma unroll
+    for (int j = 0; j < kCTAItems; ++j) {
+        const uint32_t i = threadIdx.x + j * 1024;
+        cl[j] = 0;
+        if (i < m) {
+            double t[DM];
+            const uint64_t p = in[i];
+#pragma unroll
+            for (int k = 0; k < DM; ++k)
+                if (k < dd) t[k] = v[p * dd + k];
+            cl[j] = direction_cell<DM>(t, dd, mcell);
+            atomicAdd(&cnt[cl[j]], 1u);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {  // exclusive scan of the cell counts by one warp
+        uint32_t carry = 0;
+        for (uint32_t base = 0; base < ncells; base += 32) {
+            const uint32_t c = base + threadIdx.x;
+            const uint32_t x = c < ncells ? cnt[c] : 0;
+            uint32_t incl = x;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if ((int)threadIdx.x >= o) incl += y;
+            }
+            if (c < ncells) cnt[c] = carry + incl - x;
+            carry += __shfl_sync(0xffffffffu, incl, 31);
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kCTAItems; ++j) {
+        const uint32_t i = threadIdx.x + j * 1024;
+        if (i < m) {
+            const uint32_t pos = atomicAdd(&cnt[cl[j]], 1u);
+            out[pos] = in[i];
+            out_cell[pos] = cl[j];
+        }
+    }
 }
 
-// compact SoA copy [d][m] of the tuples list[0..m) from the AoS input; the
+template <int D>
+__global__ void k_cells_of(const double* __restrict__ v, int d, const uint32_t* __restrict__ in,
+                           uint32_t m, int mcell, uint32_t* __restrict__ cell) {
+    constexpr int DM = D > 0 ? D : kMaxDims;
+    const int dd = D > 0 ? D : d;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+        double t[DM];
+        const uint64_t p = in[i];
+#pragma unroll
+        for (int k = 0; k < DM; ++k)
+            if (k < dd) t[k] = v[p * dd + k];
+        cell[i] = direction_cell<DM>(t, dd, mcell);
+    }
+}
+
+// seg[c] = first position of cell >= c in a cell-sorted list of *count items
+__global__ void k_cell_segments(const uint32_t* __restrict__ ckey,
+                                const unsigned long long* __restrict__ count, uint32_t ncells,
+                                uint32_t* __restrict__ seg) {
+    const uint32_t mcount = (uint32_t)*count;
+    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c <= ncells;
+         c += gridDim.x * blockDim.x) {
+        uint32_t lo = 0, hi = mcount;
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (ckey[mid] < c) lo = mid + 1;
+            else hi = mid;
+        }
+        seg[c] = lo;
+    }
+}
+
+// compact SoA copy [d][cap] of the tuples list[0..m) from the AoS input; the
 // count is read from device memory when `count` is given (no host sync)
 __global__ void k_gather_aos(const double* __restrict__ v, int d, const uint32_t* __restrict__ list,
-                             uint64_t m, const unsigned long long* __restrict__ count,
+                             uint64_t cap, const unsigned long long* __restrict__ count,
                              double* __restrict__ out) {
-    const uint64_t mm = count ? *count : m;
+    const uint64_t mm = count ? *count : cap;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < mm * d;
          i += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t k = i / d;
         const int a = (int)(i - k * d);
-        out[(uint64_t)a * m + k] = v[(uint64_t)list[k] * d + a];
+        out[(uint64_t)a * cap + k] = v[(uint64_t)list[k] * d + a];
     }
 }
 
@@ -268,13 +287,59 @@ __global__ void k_rep_filter(const double* __restrict__ v, uint64_t n, int d,
     add_count(tests, cnt);
 }
 
-// K4: warp-per-candidate SFS inside the sorted prefix Av[d][m]: candidate i
-// tests its predecessors 0..i-1, 32 per iteration, leaving at the first
-// non-zero ballot (north_star (a): warp-ballot early exit).
+// (key, id) order of the predecessor rule; ids are unique
+__device__ __forceinline__ bool precedes(unsigned long long ka, int64_t ia,
+                                         unsigned long long kb, int64_t ib) {
+    return ka < kb || (ka == kb && ia < ib);
+}
+
+// Rank sort of a small list (m <= 16384) by (key, id, position): element i
+// counts the elements that precede it (O(m^2) compares, split over a 2-D
+// grid of 256-element x 1024-comparator blocks staged in shared memory,
+// partial ranks combined with atomics), then scatters itself to its rank:
+// two short launches instead of a multi-pass device radix sort.
+__global__ void __launch_bounds__(256)
+k_rank_count(const uint32_t* __restrict__ in, uint32_t m, const unsigned long long* __restrict__ key,
+             const int64_t* __restrict__ ids, uint32_t* __restrict__ rank) {
+    __shared__ unsigned long long tk[1024];
+    __shared__ long long ti[1024];
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t base = blockIdx.y * 1024;
+    const uint32_t nt = min(1024u, m - base);
+    for (uint32_t k = threadIdx.x; k < nt; k += blockDim.x) {
+        const uint32_t q = in[base + k];
+        tk[k] = key[q];
+        ti[k] = ids[q];
+    }
+    __syncthreads();
+    if (i >= m) return;
+    const uint32_t p = in[i];
+    const unsigned long long kp = key[p];
+    const long long ip = ids[p];
+    uint32_t r = 0;
+#pragma unroll 4
+    for (uint32_t k = 0; k < nt; ++k) {
+        const unsigned long long kq = tk[k];
+        const long long iq = ti[k];
+        r += (kq < kp) | ((kq == kp) & ((iq < ip) | ((iq == ip) & (base + k < i))));
+    }
+    atomicAdd(&rank[i], r);
+}
+
+__global__ void k_rank_scatter(const uint32_t* __restrict__ in, uint32_t m,
+                               const uint32_t* __restrict__ rank, uint32_t* __restrict__ out) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
+        out[rank[i]] = in[i];
+}
+
+// K4: warp-per-candidate SFS inside the (sum, id)-sorted prefix Av[d][m]:
+// candidate i tests its predecessors 0..i-1 in sum order (strongest
+// dominators first), 32 per iteration, leaving at the first non-zero ballot
+// (north_star (a): warp-ballot early exit).
 template <int D>
 __global__ void __launch_bounds__(kBlock)
-k_sfs_intra_warp(const double* __restrict__ Av, uint32_t m, int d, uint8_t* __restrict__ keep,
-                 unsigned long long* __restrict__ tests) {
+k_sfs_intra_sorted(const double* __restrict__ Av, uint32_t m, int d, uint8_t* __restrict__ keep,
+                   unsigned long long* __restrict__ tests) {
     constexpr int DM = D > 0 ? D : kMaxDims;
     const int dd = D > 0 ? D : d;
     const uint32_t lane = threadIdx.x & 31;
@@ -308,139 +373,107 @@ k_sfs_intra_warp(const double* __restrict__ Av, uint32_t m, int d, uint8_t* __re
     add_count(tests, cnt);
 }
 
-// K5: every undecided tuple outside the prefix against the new skyline
-// tuples Pv[d][cap] (np = *np_dev, all of which precede it in (sum, id)
-// order); keep[i] = 1 for survivors (compacted in order by the caller).
+// K4: warp-per-candidate decision of the prefix.  The prefix is in cell
+// order (list P, SoA values Av[d][m], cell keys); candidate i scans all
+// members starting in its own cell and wrapping around; a dominance hit
+// counts only when the dominator precedes it (dominance already implies
+// key_j <= key_i, so only exact sum ties need the id check).
 template <int D>
 __global__ void __launch_bounds__(kBlock)
-k_sfs_filter_warp(const double* __restrict__ v, int d, const unsigned long long* __restrict__ key,
-                  const uint32_t* __restrict__ R, uint64_t r, const double* __restrict__ Pv,
-                  uint64_t pcap, unsigned long long* __restrict__ slots,
-                  uint8_t* __restrict__ keep, unsigned long long* __restrict__ tests) {
+k_sfs_intra_cells(const double* __restrict__ Av, const uint32_t* __restrict__ P, uint32_t m,
+                  int d, const unsigned long long* __restrict__ key,
+                  const int64_t* __restrict__ ids, const uint32_t* __restrict__ cellof,
+                  const uint32_t* __restrict__ seg, uint8_t* __restrict__ keep,
+                  unsigned long long* __restrict__ tests, uint32_t bs) {
     constexpr int DM = D > 0 ? D : kMaxDims;
     const int dd = D > 0 ? D : d;
     const uint32_t lane = threadIdx.x & 31;
-    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    const double T = slot_double(slots, S_THR);
-    const uint32_t np = (uint32_t)slots[S_C2];
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
     unsigned long long cnt = 0;
-    for (uint64_t i = warp; i < r; i += nwarps) {
-        const uint32_t p = R ? R[i] : (uint32_t)i;
-        if (__longlong_as_double((long long)key[p]) < T) {  // in the prefix: decided
-            if (lane == 0) keep[i] = 0;
-            continue;
-        }
+    for (uint32_t base = warp * bs; base < m; base += nwarps * bs) {
+        const uint32_t idx = base + lane;
+        const bool valid = lane < bs && idx < m;
         double t[DM];
 #pragma unroll
         for (int k = 0; k < DM; ++k)
-            if (k < dd) t[k] = v[(uint64_t)p * dd + k];
-        bool dominated = false;
-        for (uint32_t j0 = 0; j0 < np; j0 += 32) {
-            const uint32_t j = j0 + lane;
-            bool hit = false;
-            if (j < np) {
-                double s[DM];
+            if (k < dd) t[k] = valid ? Av[(uint64_t)k * m + idx] : 0.0;
+        const uint32_t p = valid ? P[idx] : 0;
+        const unsigned long long kt = valid ? key[p] : 0;
+        const int64_t it = valid ? ids[p] : 0;
+        const uint32_t start = (valid && seg) ? seg[cellof[idx]] : 0;
+        bool mykeep = valid;
+        unsigned todo = __ballot_sync(0xffffffffu, valid);
+        while (todo) {
+            const int j = __ffs(todo) - 1;
+            todo &= todo - 1;
+            double tj[DM];
 #pragma unroll
-                for (int k = 0; k < DM; ++k)
-                    if (k < dd) s[k] = Pv[(uint64_t)k * pcap + j];
-                hit = D > 0 ? dom_f64<(D > 0 ? D : 1)>(s, t) : dom_f64_dyn(s, t, dd);
-                ++cnt;
+            for (int k = 0; k < DM; ++k)
+                if (k < dd) tj[k] = __shfl_sync(0xffffffffu, t[k], j);
+            const unsigned long long ktj = __shfl_sync(0xffffffffu, kt, j);
+            const int64_t itj = __shfl_sync(0xffffffffu, it, j);
+            uint32_t q = __shfl_sync(0xffffffffu, start, j) + lane;
+            if (q >= m) q -= m;
+            bool dominated = false;
+            for (uint32_t done = 0; done < m; done += 32) {
+                bool hit = false;
+                if (done + lane < m) {
+                    double s[DM];
+#pragma unroll
+                    for (int k = 0; k < DM; ++k)
+                        if (k < dd) s[k] = Av[(uint64_t)k * m + q];
+                    hit = D > 0 ? dom_f64<(D > 0 ? D : 1)>(s, tj) : dom_f64_dyn(s, tj, dd);
+                    if (hit) {
+                        const uint32_t pq = P[q];
+                        hit = precedes(key[pq], ids[pq], ktj, itj);
+                    }
+                    ++cnt;
+                }
+                if (__any_sync(0xffffffffu, hit)) {
+                    dominated = true;
+                    break;
+                }
+                q += 32;
+                if (q >= m) q -= m;
             }
-            if (__any_sync(0xffffffffu, hit)) {
-                dominated = true;
-                break;
-            }
+            if ((int)lane == j) mykeep = !dominated;
         }
-        if (lane == 0) keep[i] = dominated ? 0 : 1;
+        if (valid) keep[idx] = mykeep ? 1 : 0;
     }
     add_count(tests, cnt);
 }
 
-// Direction cell of a tuple: a grid over its first d-1 normalised
-// coordinates u_j = t_j / sum(t) (a cheap stand-in for the paper's angular
-// coordinates, partition.cpp:139-174).  A dominator s of t lies in the
-// orthant below t; on large-skyline data (tuples near a hyperplane) that
-// means a nearby direction, so scanning t's own cell first finds it early.
-// Only the scan ORDER depends on cells — results never do.
-template <int DM>
-__device__ __forceinline__ uint32_t direction_cell(const double* t, int dd, int m) {
-    if (dd < 2 || m <= 1) return 0;
-    double s = 0.0;
-    for (int k = 0; k < DM; ++k)
-        if (k < dd) s += t[k];
-    if (!(s > 0.0)) return 0;
-    const double inv = (double)m / s;
-    uint32_t cell = 0;
-    for (int k = DM - 2; k >= 0; --k) {
-        if (k >= dd - 1) continue;
-        int b = (int)(t[k] * inv);
-        b = b < 0 ? 0 : (b >= m ? m - 1 : b);
-        cell = cell * (uint32_t)m + (uint32_t)b;
-    }
-    return cell;
-}
-
-// cell keys of the prefix in sorted order; non-skyline entries sort last
-template <int D>
-__global__ void k_prefix_cells(const double* __restrict__ Av, uint32_t mcount, int d,
-                               const uint8_t* __restrict__ keep, int m,
-                               uint32_t* __restrict__ ckey) {
-    constexpr int DM = D > 0 ? D : kMaxDims;
-    const int dd = D > 0 ? D : d;
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < mcount;
-         i += gridDim.x * blockDim.x) {
-        double t[DM];
-#pragma unroll
-        for (int k = 0; k < DM; ++k)
-            if (k < dd) t[k] = Av[(uint64_t)k * mcount + i];
-        ckey[i] = keep[i] ? direction_cell<DM>(t, dd, m) : 0xFFFFFFFFu;
-    }
-}
-
-// seg[c] = first position of cell >= c in the cell-sorted comparator list
-__global__ void k_cell_segments(const uint32_t* __restrict__ ckey, uint32_t mcount,
-                                uint32_t ncells, uint32_t* __restrict__ seg) {
-    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c <= ncells;
-         c += gridDim.x * blockDim.x) {
-        uint32_t lo = 0, hi = mcount;
-        while (lo < hi) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (ckey[mid] < c) lo = mid + 1;
-            else hi = mid;
-        }
-        seg[c] = lo;
-    }
-}
-
-// K5 (v2): 32 candidates are loaded per warp at once (lane-parallel,
-// coalesced), then decided one after another with the whole warp scanning
-// the comparators 32 at a time, starting in the candidate's own direction
-// cell and wrapping around; ballot exit at the first dominator.
+// K5: 32 candidates are loaded per warp at once (lane-parallel, coalesced),
+// then decided one after another with the whole warp scanning the new
+// skyline tuples Pv[d][pcap] (np = slots[S_C2], all preceding the candidate
+// in (sum, id) order) 32 at a time, starting in the candidate's own cell and
+// wrapping around; ballot exit at the first dominator.  keep[i] = 1 marks
+// survivors (compacted in order by the caller).
 template <int D>
 __global__ void __launch_bounds__(kBlock)
 k_sfs_filter_cells(const double* __restrict__ v, int d, const unsigned long long* __restrict__ key,
                    const uint32_t* __restrict__ R, uint32_t r, const double* __restrict__ Pv,
                    uint32_t pcap, const uint32_t* __restrict__ seg, int m,
                    const unsigned long long* __restrict__ slots, uint8_t* __restrict__ keep,
-                   unsigned long long* __restrict__ tests) {
+                   unsigned long long* __restrict__ tests, uint32_t bs) {
     constexpr int DM = D > 0 ? D : kMaxDims;
     const int dd = D > 0 ? D : d;
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-    const double T = slot_double(slots, S_THR);
+    const unsigned long long T = slots[S_THR];
     const uint32_t np = (uint32_t)slots[S_C2];
     unsigned long long cnt = 0;
-    for (uint32_t base = warp * 32; base < r; base += nwarps * 32) {
+    for (uint32_t base = warp * bs; base < r; base += nwarps * bs) {
         const uint32_t idx = base + lane;
-        const bool valid = idx < r;
+        const bool valid = lane < bs && idx < r;
         const uint32_t p = valid ? (R ? R[idx] : idx) : 0;
         double t[DM];
 #pragma unroll
         for (int k = 0; k < DM; ++k)
             if (k < dd) t[k] = valid ? v[(uint64_t)p * dd + k] : 0.0;
-        const bool need = valid && !(__longlong_as_double((long long)key[p]) < T);
+        const bool need = valid && !(key[p] < T);  // not in the (decided) prefix
         const uint32_t start = (need && seg) ? seg[direction_cell<DM>(t, dd, m)] : 0;
         bool mykeep = need;
         unsigned todo = __ballot_sync(0xffffffffu, need);
@@ -478,6 +511,51 @@ k_sfs_filter_cells(const double* __restrict__ v, int d, const unsigned long long
     add_count(tests, cnt);
 }
 
+// One-CTA order-preserving compaction of up to 16384 flagged items (and
+// their cell keys); the count lands in *count.
+__global__ void __launch_bounds__(1024)
+k_cta_select(const uint32_t* __restrict__ in, const uint32_t* __restrict__ in_cell,
+             const uint8_t* __restrict__ flags, uint32_t m, uint32_t* __restrict__ out,
+             uint32_t* __restrict__ out_cell, unsigned long long* __restrict__ count) {
+    using Scan = cub::BlockScan<uint32_t, 1024>;
+    __shared__ typename Scan::TempStorage tmp;
+    uint32_t f[kCTAItems];
+    uint32_t local = 0;
+#pragma unroll
+    for (int j = 0; j < kCTAItems; ++j) {
+        const uint32_t i = threadIdx.x * kCTAItems + j;
+        f[j] = (i < m && flags[i]) ? 1u : 0u;
+        local += f[j];
+    }
+    uint32_t offset = 0, total = 0;
+    Scan(tmp).ExclusiveSum(local, offset, total);
+#pragma unroll
+    for (int j = 0; j < kCTAItems; ++j) {
+        const uint32_t i = threadIdx.x * kCTAItems + j;
+        if (f[j]) {
+            out[offset] = in[i];
+            if (out_cell) out_cell[offset] = in_cell[i];
+            ++offset;
+        }
+    }
+    if (threadIdx.x == 0) *count = total;
+}
+
+__global__ void k_keys_of(const unsigned long long* __restrict__ key,
+                          const uint32_t* __restrict__ list, uint64_t m,
+                          unsigned long long* __restrict__ out) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = key[list[i]];
+}
+
+__global__ void k_id_keys(const int64_t* __restrict__ ids, const uint32_t* __restrict__ list,
+                          uint64_t m, unsigned long long* __restrict__ out) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = static_cast<unsigned long long>(ids[list[i]]) ^ 0x8000000000000000ULL;
+}
+
 __global__ void k_emit_skyline(const uint32_t* __restrict__ K, uint64_t S,
                                const double* __restrict__ v, int d,
                                const int64_t* __restrict__ ids, int64_t* __restrict__ oid,
@@ -490,14 +568,16 @@ __global__ void k_emit_skyline(const uint32_t* __restrict__ K, uint64_t S,
     }
 }
 
-void sort_pairs(Ctx& c, unsigned long long* k0, unsigned long long* k1, uint32_t* v0,
-                uint32_t* v1, uint64_t n, unsigned long long** kout, uint32_t** vout) {
-    cub::DoubleBuffer<unsigned long long> kb(k0, k1);
+template <class KT>
+void sort_pairs(Ctx& c, KT* k0, KT* k1, uint32_t* v0, uint32_t* v1, uint64_t n, int end_bit,
+                KT** kout, uint32_t** vout) {
+    cub::DoubleBuffer<KT> kb(k0, k1);
     cub::DoubleBuffer<uint32_t> vb(v0, v1);
     size_t tmp = 0;
-    SKY_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kb, vb, (int64_t)n, 0, 64, c.stream));
+    SKY_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kb, vb, (int64_t)n, 0, end_bit,
+                                             c.stream));
     void* t = c.buf[B_CUB].get(tmp);
-    SKY_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, kb, vb, (int64_t)n, 0, 64, c.stream));
+    SKY_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, kb, vb, (int64_t)n, 0, end_bit, c.stream));
     note_launch(c, 4);
     *kout = kb.Current();
     *vout = vb.Current();
@@ -521,7 +601,8 @@ void select_if(Ctx& c, const uint32_t* R, uint64_t r, Op op, uint32_t* out,
     note_launch(c, 2);
 }
 
-void select_flags(Ctx& c, const uint32_t* R, uint64_t r, const uint8_t* flags, uint32_t* out,
+template <class T>
+void select_flags(Ctx& c, const T* R, uint64_t r, const uint8_t* flags, T* out,
                   unsigned long long* d_count) {
     size_t tmp = 0;
     if (R) {
@@ -531,7 +612,7 @@ void select_flags(Ctx& c, const uint32_t* R, uint64_t r, const uint8_t* flags, u
         SKY_CUDA(cub::DeviceSelect::Flagged(t, tmp, R, flags, out, d_count, (int64_t)r,
                                              c.stream));
     } else {
-        cub::CountingInputIterator<uint32_t> it(0);
+        cub::CountingInputIterator<T> it(0);
         SKY_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp, it, flags, out, d_count, (int64_t)r,
                                              c.stream));
         void* t = c.buf[B_CUB].get(tmp);
@@ -539,6 +620,29 @@ void select_flags(Ctx& c, const uint32_t* R, uint64_t r, const uint8_t* flags, u
                                              c.stream));
     }
     note_launch(c, 2);
+}
+
+// candidates per warp batch: 32 (one coalesced load per lane) when there
+// are enough candidates to keep ~48 warps per SM busy, fewer otherwise
+uint32_t batch_size(const Ctx& c, uint64_t count) {
+    const uint64_t target_warps = (uint64_t)c.num_sms * 48;
+    uint64_t bs = (count + target_warps - 1) / target_warps;
+    return (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(32, bs));
+}
+
+// bins per normalised coordinate so that the cells hold ~128 tuples each
+int cells_per_dim(uint64_t m, int d, uint32_t* ncells) {
+    int mcell = 1;
+    if (d >= 2) {
+        const double target = std::max(1.0, (double)m / 128.0);
+        mcell = (int)std::floor(std::pow(target, 1.0 / (d - 1)) + 1e-9);
+        mcell = std::max(1, std::min(mcell, 64));
+    }
+    uint32_t nc = 1;
+    for (int k = 0; k < d - 1; ++k) nc *= (uint32_t)mcell;
+    if (nc > kMaxCells) mcell = 1, nc = 1;
+    *ncells = nc;
+    return mcell;
 }
 
 }  // namespace
@@ -571,8 +675,7 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
     uint32_t* Rbuf0 = c.buf[B_R0].as<uint32_t>(n);
     uint32_t* Rbuf1 = c.buf[B_R1].as<uint32_t>(n);
     uint32_t* K = c.buf[B_KLIST].as<uint32_t>(n);
-    // histogram bins + direction-cell segment table (ncells <= m/128 + 1 <= 4096)
-    unsigned* hist = c.buf[B_ORDER].as<unsigned>(kHistBins + 4096 + 1);
+    uint32_t* seg_table = c.buf[B_ORDER].as<uint32_t>(kMaxCells + 1);
     bool checked = false;
     if (n_reps > 0) {
         uint8_t* rflags = c.buf[B_FLAGS].as<uint8_t>(n);
@@ -583,45 +686,33 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
         });
         SKY_LAUNCH_CHECK();
         note_launch(c);
-        select_flags(c, nullptr, n, rflags, Rbuf0, c.d_slots + S_C3);
+        select_flags<uint32_t>(c, nullptr, n, rflags, Rbuf0, c.d_slots + S_C3);
         read_slots(c, S_BAD, 11);  // S_BAD .. S_C3 (checks + survivors)
-        checked = true;
         R = Rbuf0;
         r = c.h_slots[S_C3];
     }
     st.tuples_into_parallel = r;
 
     uint64_t kc = 0;
-    uint64_t want = 16384;
-    const uint64_t kMaxPrefix = 65536, kFinal = 32768;
+    uint64_t want = 12000;  // stays below the one-CTA capacity despite sampling noise
+    const uint64_t kMaxPrefix = 65536, kFinal = kCTACap;
     int rounds = 0;
     cudaEvent_t e0 = c.ev[8], e1 = c.ev[9], e2 = c.ev[14], e3 = c.ev[15];
     double kernel_ms = 0;
     uint64_t kernel_launches = 0;
     uint32_t* Rnext = Rbuf1;
+    bool ids_sorted = true;
     while (r > 0) {
-        // ---- K2: threshold, K3: prefix selection
-        SKY_CUDA(cudaMemsetAsync(hist, 0, sizeof(unsigned) * kHistBins, c.stream));
+        // ---- K2: sampled threshold, K3: ordered prefix selection
         const uint64_t w = r <= kFinal ? r : want;
-        if (R) {  // sum range of the undecided set
-            reset_range(c);
-            k_range<<<grid_for(r, kBlock, c.num_sms * 4), kBlock, 0, c.stream>>>(keys, R, r,
-                                                                                 c.d_slots);
-            SKY_LAUNCH_CHECK();
-            note_launch(c);
-        }
-        k_hist<<<grid_for(r, kBlock, c.num_sms * 4), kBlock, 0, c.stream>>>(keys, R, r, c.d_slots,
-                                                                            hist);
-        SKY_LAUNCH_CHECK();
-        k_threshold<<<1, 1024, 0, c.stream>>>(hist, r, w, c.d_slots);
+        k_sample_threshold<<<1, 1024, 0, c.stream>>>(keys, R, r, w, c.d_slots);
         SKY_LAUNCH_CHECK();
         reset_counts(c);
         uint32_t* Pfull = c.buf[B_IDX0].as<uint32_t>(r);
-        unsigned long long* Pkey = c.buf[B_KEY1].as<unsigned long long>(r);
-        trace_mark(c, "sky: range/hist/threshold");
+        trace_mark(c, "sky: score + sample threshold");
         select_if(c, R, r, BelowThreshold{keys, c.d_slots + S_THR}, Pfull, c.d_slots + S_C1);
+        note_launch(c, 1);
         trace_mark(c, "sky: select prefix");
-        note_launch(c, 2);
         read_slots(c, S_BAD, 11);
         if (!checked) {
             checked = true;
@@ -639,62 +730,72 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
                         " outside [0,1]; normalize the data first");
             }
         }
-        const bool ids_sorted = (c.h_slots[S_FLAG] & 1ULL) == 0;
+        ids_sorted = (c.h_slots[S_FLAG] & 1ULL) == 0;
         const uint64_t m = c.h_slots[S_C1];
-        k_keys_of<<<grid_for(m, kBlock), kBlock, 0, c.stream>>>(keys, Pfull, m, Pkey);
-        SKY_LAUNCH_CHECK();
-        note_launch(c);
+        if (m == 0) throw Error(SKYGPU_ERUNTIME, "skyline: empty prefix (internal)");
 
         // ---- sort the prefix by (sum, id)
-        uint32_t* P2 = c.buf[B_IDX1].as<uint32_t>(m);
-        unsigned long long* Pkey2 = c.buf[B_GTMP0].as<unsigned long long>(m);
-        unsigned long long* kcur;
-        uint32_t* order;
-        if (ids_sorted) {
-            sort_pairs(c, Pkey, Pkey2, Pfull, P2, m, &kcur, &order);
-        } else {
-            // stable LSD: by id first, then by sum
-            unsigned long long* ik0 = c.buf[B_GTMP1].as<unsigned long long>(m);
-            k_id_keys<<<grid_for(m, kBlock), kBlock, 0, c.stream>>>(d_ids, Pfull, m, ik0);
+        uint32_t* Ps = c.buf[B_IDX1].as<uint32_t>(m);
+        uint32_t* order = Ps;
+        if (m <= kCTACap) {
+            uint32_t* rk = c.buf[B_GTMP1].as<uint32_t>(m);
+            SKY_CUDA(cudaMemsetAsync(rk, 0, m * sizeof(uint32_t), c.stream));
+            dim3 rg((unsigned)((m + 255) / 256), (unsigned)((m + 1023) / 1024));
+            k_rank_count<<<rg, 256, 0, c.stream>>>(Pfull, (uint32_t)m, keys, d_ids, rk);
             SKY_LAUNCH_CHECK();
-            unsigned long long* ikc;
-            uint32_t* by_id;
-            sort_pairs(c, ik0, Pkey2, Pfull, P2, m, &ikc, &by_id);
-            uint32_t* other = by_id == Pfull ? P2 : Pfull;
-            unsigned long long* sk0 = c.buf[B_GTMP1].as<unsigned long long>(m);
-            k_keys_of<<<grid_for(m, kBlock), kBlock, 0, c.stream>>>(keys, by_id, m, sk0);
+            k_rank_scatter<<<grid_for(m, kBlock), kBlock, 0, c.stream>>>(Pfull, (uint32_t)m, rk, Ps);
             SKY_LAUNCH_CHECK();
             note_launch(c, 2);
-            sort_pairs(c, sk0, Pkey2, by_id, other, m, &kcur, &order);
+        } else {
+            unsigned long long* Pkey = c.buf[B_KEY1].as<unsigned long long>(m);
+            unsigned long long* Pkey2 = c.buf[B_GTMP0].as<unsigned long long>(m);
+            unsigned long long* kcur;
+            if (ids_sorted) {
+                k_keys_of<<<grid_for(m, kBlock), kBlock, 0, c.stream>>>(keys, Pfull, m, Pkey);
+                SKY_LAUNCH_CHECK();
+                sort_pairs<unsigned long long>(c, Pkey, Pkey2, Pfull, Ps, m, 64, &kcur, &order);
+            } else {  // stable LSD: by id first, then by sum
+                unsigned long long* ik0 = c.buf[B_GTMP1].as<unsigned long long>(m);
+                k_id_keys<<<grid_for(m, kBlock), kBlock, 0, c.stream>>>(d_ids, Pfull, m, ik0);
+                SKY_LAUNCH_CHECK();
+                unsigned long long* ikc;
+                uint32_t* by_id;
+                sort_pairs<unsigned long long>(c, ik0, Pkey2, Pfull, Ps, m, 64, &ikc, &by_id);
+                uint32_t* other = by_id == Pfull ? Ps : Pfull;
+                k_keys_of<<<grid_for(m, kBlock), kBlock, 0, c.stream>>>(keys, by_id, m, Pkey);
+                SKY_LAUNCH_CHECK();
+                sort_pairs<unsigned long long>(c, Pkey, Pkey2, by_id, other, m, 64, &kcur, &order);
+            }
+            note_launch(c, 2);
         }
-
-        // ---- K4: SFS inside the prefix
         double* Av = c.buf[B_MISC].as<double>(m * d);
-        trace_mark(c, "sky: (sync) + sort prefix");
-        k_gather_aos<<<grid_for(m * d, kBlock), kBlock, 0, c.stream>>>(d_vals, d, order, m,
-                                                                        nullptr, Av);
+        k_gather_aos<<<grid_for(m * d, kBlock), kBlock, 0, c.stream>>>(d_vals, d, order, m, nullptr,
+                                                                        Av);
         SKY_LAUNCH_CHECK();
+        note_launch(c);
+        trace_mark(c, "sky: (sync) + sort prefix + gather");
+
+        // ---- K4: SFS inside the prefix, predecessors in sum order
         uint8_t* keep = c.buf[B_FLAGS].as<uint8_t>(m);
         const uint64_t wi = std::min<uint64_t>(m, (uint64_t)c.num_sms * 64);
         SKY_CUDA(cudaEventRecord(e0, c.stream));
         dispatch_d(d, [&](auto DC) {
             constexpr int D = decltype(DC)::value;
-            trace_mark(c, "sky: gather prefix");
-            k_sfs_intra_warp<D><<<(unsigned)((wi * 32 + kBlock - 1) / kBlock), kBlock, 0,
-                                  c.stream>>>(Av, (uint32_t)m, d, keep, c.d_slots + S_TESTS_SKY);
+            k_sfs_intra_sorted<D><<<(unsigned)((wi * 32 + kBlock - 1) / kBlock), kBlock, 0,
+                                    c.stream>>>(Av, (uint32_t)m, d, keep, c.d_slots + S_TESTS_SKY);
         });
         SKY_CUDA(cudaEventRecord(e1, c.stream));
         SKY_LAUNCH_CHECK();
-        note_launch(c, 2);
-        // A' (order-preserving) appended to K; its count lands in S_C2
-        {
-            size_t tmp = 0;
-            SKY_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp, order, keep, K + kc,
-                                                 c.d_slots + S_C2, (int64_t)m, c.stream));
-            void* t = c.buf[B_CUB].get(tmp);
-            SKY_CUDA(cub::DeviceSelect::Flagged(t, tmp, order, keep, K + kc, c.d_slots + S_C2,
-                                                 (int64_t)m, c.stream));
-            note_launch(c, 2);
+        note_launch(c);
+        trace_mark(c, "sky: K4 intra kernel");
+        // A' in (sum, id) order appended to K; its count lands in S_C2
+        if (m <= kCTACap) {
+            k_cta_select<<<1, 1024, 0, c.stream>>>(order, nullptr, keep, (uint32_t)m, K + kc,
+                                                   nullptr, c.d_slots + S_C2);
+            SKY_LAUNCH_CHECK();
+            note_launch(c);
+        } else {
+            select_flags<uint32_t>(c, order, m, keep, K + kc, c.d_slots + S_C2);
         }
         ++rounds;
         kernel_launches += 1;
@@ -706,63 +807,51 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
             kc += c.h_slots[S_C2];
             break;
         }
-        // ---- K5: filter the rest against A', comparators in direction-cell
-        // order (own cell first) so dominators are met early
-        int mcell = 1;
-        if (d >= 2) {
-            const double target = std::max(1.0, (double)m / 128.0);
-            mcell = (int)std::floor(std::pow(target, 1.0 / (d - 1)) + 1e-9);
-            mcell = std::max(1, std::min(mcell, 32));
-        }
+        // ---- K5: filter the rest against A', A' regrouped by direction cell
+        // (one-CTA counting sort) so a candidate meets its own cell first
         uint32_t ncells = 1;
-        for (int k = 0; k < d - 1; ++k) ncells *= (uint32_t)mcell;
-        double* Pv = c.buf[B_CSUM].as<double>(m * d);
+        int mcell = m <= kCTACap ? cells_per_dim(m, d, &ncells) : 1;
         uint32_t* seg = nullptr;
         const uint32_t* psrc = K + kc;
         if (mcell > 1) {
-            uint32_t* ck0 = c.buf[B_GTMP1].as<uint32_t>(m);
-            uint32_t* ck1 = reinterpret_cast<uint32_t*>(Pkey);  // free after the sort
-            uint32_t* ov = order;
-            uint32_t* oalt = order == Pfull ? P2 : Pfull;
+            uint32_t* Alist = c.buf[B_GTMP1].as<uint32_t>(m);
+            uint32_t* Akey = c.buf[B_GTMP0].as<uint32_t>(m);
             dispatch_d(d, [&](auto DC) {
                 constexpr int D = decltype(DC)::value;
-                k_prefix_cells<D><<<grid_for(m, kBlock), kBlock, 0, c.stream>>>(Av, (uint32_t)m, d,
-                                                                                 keep, mcell, ck0);
+                k_cell_order<D><<<1, 1024, 0, c.stream>>>(d_vals, d, K + kc, (uint32_t)m,
+                                                          c.d_slots + S_C2, mcell, ncells, Alist,
+                                                          Akey);
             });
             SKY_LAUNCH_CHECK();
-            cub::DoubleBuffer<uint32_t> kb(ck0, ck1), vb(ov, oalt);
-            size_t tmp = 0;
-            SKY_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kb, vb, (int64_t)m, 0, 32,
-                                                     c.stream));
-            void* tp = c.buf[B_CUB].get(tmp);
-            SKY_CUDA(cub::DeviceRadixSort::SortPairs(tp, tmp, kb, vb, (int64_t)m, 0, 32,
-                                                     c.stream));
-            seg = reinterpret_cast<uint32_t*>(hist) + kHistBins;
+            seg = seg_table;
             k_cell_segments<<<grid_for(ncells + 1, kBlock), kBlock, 0, c.stream>>>(
-                kb.Current(), (uint32_t)m, ncells, seg);
+                Akey, c.d_slots + S_C2, ncells, seg);
             SKY_LAUNCH_CHECK();
-            note_launch(c, 6);
-            psrc = vb.Current();
+            note_launch(c, 2);
+            psrc = Alist;
         }
+        double* Pv = c.buf[B_CSUM].as<double>(m * d);
         k_gather_aos<<<grid_for(m * d, kBlock), kBlock, 0, c.stream>>>(d_vals, d, psrc, m,
                                                                         c.d_slots + S_C2, Pv);
         SKY_LAUNCH_CHECK();
-        const uint64_t wf = std::min<uint64_t>((r + 31) / 32, (uint64_t)c.num_sms * 64);
+        note_launch(c);
+        const uint32_t bsf = batch_size(c, r);
+        const uint64_t wf = std::min<uint64_t>((r + bsf - 1) / bsf, (uint64_t)c.num_sms * 64);
         uint8_t* fkeep = c.buf[B_SV].as<uint8_t>(r);
+        trace_mark(c, "sky: select A' + segments + gather Pv");
         SKY_CUDA(cudaEventRecord(e2, c.stream));
         dispatch_d(d, [&](auto DC) {
             constexpr int D = decltype(DC)::value;
-            trace_mark(c, "sky: select A' + cells + gather Pv");
             k_sfs_filter_cells<D><<<(unsigned)((wf * 32 + kBlock - 1) / kBlock), kBlock, 0,
                                     c.stream>>>(d_vals, d, keys, R, (uint32_t)r, Pv, (uint32_t)m,
                                                 seg, mcell, c.d_slots, fkeep,
-                                                c.d_slots + S_TESTS_SKY);
+                                                c.d_slots + S_TESTS_SKY, bsf);
         });
         SKY_CUDA(cudaEventRecord(e3, c.stream));
         SKY_LAUNCH_CHECK();
-        note_launch(c, 2);
+        note_launch(c);
         trace_mark(c, "sky: K5 filter kernel");
-        select_flags(c, R, r, fkeep, Rnext, c.d_slots + S_C3);
+        select_flags<uint32_t>(c, R, r, fkeep, Rnext, c.d_slots + S_C3);
         trace_mark(c, "sky: select survivors");
         kernel_launches += 1;
         read_slots(c, S_C2, 2);  // S_C2 (A'), S_C3 (survivors)
@@ -783,6 +872,8 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
     st.ms_sky_kernel += kernel_ms;
     st.sky_kernel_launches += kernel_launches;
 
+    // K holds the skyline in the reference's output order, (sum, id): each
+    // round's A' is in that order and rounds advance through the order
     out.S = kc;
     out.d_inpos = K;
     out.d_ids = c.buf[B_SKYID].as<int64_t>(kc);
