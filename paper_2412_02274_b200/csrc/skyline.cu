@@ -18,7 +18,8 @@
 //                PREFIX of the (sum, id) order: every predecessor of a prefix
 //                member is in the prefix, so the prefix can be decided alone.
 //   K3 select    the prefix (order-preserving compaction)
-//   K3b sort     the prefix by (sum, id): one-launch rank sort (k <= 16384)
+//   K3b sort     the prefix by (sum, id): key-bucket counting sort + in-bucket
+//                rank (two short launches, k <= 16384)
 //   K4 intra     warp-per-candidate: each prefix member against its
 //                predecessors in sum order (strongest first), warp-ballot
 //                exit at the first dominator -> new skyline tuples A', already
@@ -64,6 +65,7 @@ void dispatch_d(int d, F&& f) {
 __global__ void k_score(const double* __restrict__ v, uint64_t n, int d,
                         unsigned long long* __restrict__ key,
                         unsigned long long* __restrict__ slots) {
+    unsigned long long mn = ~0ULL, mx = 0;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x) {
         double s = 0.0;
@@ -73,8 +75,22 @@ __global__ void k_score(const double* __restrict__ v, uint64_t n, int d,
             bad |= !(x >= 0.0);  // negative or NaN
             s = __dadd_rn(s, x);
         }
-        key[i] = ord_bits(s);
+        const unsigned long long b = ord_bits(s);
+        key[i] = b;
+        mn = b < mn ? b : mn;
+        mx = b > mx ? b : mx;
         if (bad) atomicMin(&slots[S_BAD], static_cast<unsigned long long>(i));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long x = __shfl_down_sync(0xffffffffu, mn, o);
+        const unsigned long long y = __shfl_down_sync(0xffffffffu, mx, o);
+        mn = x < mn ? x : mn;
+        mx = y > mx ? y : mx;
+    }
+    if ((threadIdx.x & 31) == 0) {  // key range of the relation
+        atomicMin(&slots[S_SMIN], mn);
+        atomicMax(&slots[S_SMAX], mx);
     }
 }
 
@@ -120,7 +136,9 @@ k_sample_threshold(const unsigned long long* __restrict__ key, const uint32_t* _
         const uint32_t t = R ? R[pos] : (uint32_t)pos;
         items[j] = key[t];
     }
-    Sort(tmp).Sort(items);
+    // an approximate quantile suffices (T is exact once chosen): sort the
+    // samples on their top 32 key bits only — half the radix passes
+    Sort(tmp).Sort(items, 32, 64);
     uint64_t q = want * NS / r;
     if (q >= NS) q = NS - 1;
     if (threadIdx.x == q / kSampleItems) {
@@ -293,43 +311,79 @@ __device__ __forceinline__ bool precedes(unsigned long long ka, int64_t ia,
     return ka < kb || (ka == kb && ia < ib);
 }
 
-// Rank sort of a small list (m <= 16384) by (key, id, position): element i
-// counts the elements that precede it (O(m^2) compares, split over a 2-D
-// grid of 256-element x 1024-comparator blocks staged in shared memory,
-// partial ranks combined with atomics), then scatters itself to its rank:
-// two short launches instead of a multi-pass device radix sort.
-__global__ void __launch_bounds__(256)
-k_rank_count(const uint32_t* __restrict__ in, uint32_t m, const unsigned long long* __restrict__ key,
-             const int64_t* __restrict__ ids, uint32_t* __restrict__ rank) {
-    __shared__ unsigned long long tk[1024];
-    __shared__ long long ti[1024];
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    const uint32_t base = blockIdx.y * 1024;
-    const uint32_t nt = min(1024u, m - base);
-    for (uint32_t k = threadIdx.x; k < nt; k += blockDim.x) {
-        const uint32_t q = in[base + k];
-        tk[k] = key[q];
-        ti[k] = ids[q];
+// Exact sort of the prefix (m <= 16384) by (key, id, position) in two short
+// launches, no device radix sort:
+//  1. one CTA buckets the prefix by the high bits of (key - kmin) into 4096
+//     monotone key buckets (shared-memory counting sort), so every bucket
+//     precedes the next in (sum, id) order;
+//  2. every element ranks itself inside its (small) bucket and scatters to
+//     bucket_start + rank.
+constexpr uint32_t kKeyBuckets = 4096;
+
+__global__ void __launch_bounds__(1024)
+k_bucket_order(const uint32_t* __restrict__ in, uint32_t m, const unsigned long long* __restrict__ key,
+               unsigned long long kmin, int shift, uint32_t* __restrict__ out,
+               uint32_t* __restrict__ bstart) {
+    __shared__ uint32_t cnt[kKeyBuckets + 1];
+    for (uint32_t b = threadIdx.x; b <= kKeyBuckets; b += 1024) cnt[b] = 0;
+    __syncthreads();
+    uint32_t bk[kCTAItems];
+#pragma unroll
+    for (int j = 0; j < kCTAItems; ++j) {
+        const uint32_t i = threadIdx.x + j * 1024;
+        bk[j] = 0;
+        if (i < m) {
+            const unsigned long long x = (key[in[i]] - kmin) >> shift;
+            bk[j] = x < kKeyBuckets ? (uint32_t)x : kKeyBuckets - 1;
+            atomicAdd(&cnt[bk[j]], 1u);
+        }
     }
     __syncthreads();
-    if (i >= m) return;
-    const uint32_t p = in[i];
-    const unsigned long long kp = key[p];
-    const long long ip = ids[p];
-    uint32_t r = 0;
-#pragma unroll 4
-    for (uint32_t k = 0; k < nt; ++k) {
-        const unsigned long long kq = tk[k];
-        const long long iq = ti[k];
-        r += (kq < kp) | ((kq == kp) & ((iq < ip) | ((iq == ip) & (base + k < i))));
+    if (threadIdx.x < 32) {  // exclusive scan of the bucket counts by one warp
+        uint32_t carry = 0;
+        for (uint32_t base = 0; base < kKeyBuckets; base += 32) {
+            const uint32_t b = base + threadIdx.x;
+            const uint32_t x = cnt[b];
+            uint32_t incl = x;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if ((int)threadIdx.x >= o) incl += y;
+            }
+            cnt[b] = carry + incl - x;
+            bstart[b] = carry + incl - x;
+            carry += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        if (threadIdx.x == 0) bstart[kKeyBuckets] = carry;
     }
-    atomicAdd(&rank[i], r);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kCTAItems; ++j) {
+        const uint32_t i = threadIdx.x + j * 1024;
+        if (i < m) out[atomicAdd(&cnt[bk[j]], 1u)] = in[i];
+    }
 }
 
-__global__ void k_rank_scatter(const uint32_t* __restrict__ in, uint32_t m,
-                               const uint32_t* __restrict__ rank, uint32_t* __restrict__ out) {
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
-        out[rank[i]] = in[i];
+__global__ void k_bucket_rank(const uint32_t* __restrict__ in, uint32_t m,
+                              const unsigned long long* __restrict__ key,
+                              const int64_t* __restrict__ ids, unsigned long long kmin, int shift,
+                              const uint32_t* __restrict__ bstart, uint32_t* __restrict__ out) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+        const uint32_t p = in[i];
+        const unsigned long long kp = key[p];
+        const long long ip = ids[p];
+        const unsigned long long x = (kp - kmin) >> shift;
+        const uint32_t b = x < kKeyBuckets ? (uint32_t)x : kKeyBuckets - 1;
+        const uint32_t s0 = bstart[b], s1 = bstart[b + 1];
+        uint32_t rank = 0;
+        for (uint32_t j = s0; j < s1; ++j) {
+            const uint32_t q = in[j];
+            const unsigned long long kq = key[q];
+            const long long iq = ids[q];
+            rank += (kq < kp) | ((kq == kp) & ((iq < ip) | ((iq == ip) & (q < p))));
+        }
+        out[s0 + rank] = p;
+    }
 }
 
 // K4: warp-per-candidate SFS inside the (sum, id)-sorted prefix Av[d][m]:
@@ -675,7 +729,7 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
     uint32_t* Rbuf0 = c.buf[B_R0].as<uint32_t>(n);
     uint32_t* Rbuf1 = c.buf[B_R1].as<uint32_t>(n);
     uint32_t* K = c.buf[B_KLIST].as<uint32_t>(n);
-    uint32_t* seg_table = c.buf[B_ORDER].as<uint32_t>(kMaxCells + 1);
+    uint32_t* seg_table = c.buf[B_ORDER].as<uint32_t>(kMaxCells + 1 + kKeyBuckets + 1);
     bool checked = false;
     if (n_reps > 0) {
         uint8_t* rflags = c.buf[B_FLAGS].as<uint8_t>(n);
@@ -738,12 +792,21 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
         uint32_t* Ps = c.buf[B_IDX1].as<uint32_t>(m);
         uint32_t* order = Ps;
         if (m <= kCTACap) {
-            uint32_t* rk = c.buf[B_GTMP1].as<uint32_t>(m);
-            SKY_CUDA(cudaMemsetAsync(rk, 0, m * sizeof(uint32_t), c.stream));
-            dim3 rg((unsigned)((m + 255) / 256), (unsigned)((m + 1023) / 1024));
-            k_rank_count<<<rg, 256, 0, c.stream>>>(Pfull, (uint32_t)m, keys, d_ids, rk);
+            const unsigned long long gmin = c.h_slots[S_SMIN] == ~0ULL ? 0 : c.h_slots[S_SMIN];
+            const unsigned long long thr = c.h_slots[S_THR];
+            const unsigned long long gmax = c.h_slots[S_SMAX];
+            const unsigned long long top = thr == ~0ULL || thr - 1 > gmax ? gmax : thr - 1;
+            const unsigned long long span = top > gmin ? top - gmin : 0;
+            int bits = span ? 64 - __builtin_clzll(span) : 0;
+            const int shift = bits > 12 ? bits - 12 : 0;  // 4096 buckets
+            uint32_t* Pb = c.buf[B_GTMP1].as<uint32_t>(m);
+            uint32_t* bst = c.buf[B_ORDER].as<uint32_t>(kMaxCells + 1 + kKeyBuckets + 1) +
+                            (kMaxCells + 1);
+            k_bucket_order<<<1, 1024, 0, c.stream>>>(Pfull, (uint32_t)m, keys, gmin, shift, Pb, bst);
             SKY_LAUNCH_CHECK();
-            k_rank_scatter<<<grid_for(m, kBlock), kBlock, 0, c.stream>>>(Pfull, (uint32_t)m, rk, Ps);
+            k_bucket_rank<<<grid_for(m, kBlock), kBlock, 0, c.stream>>>(Pb, (uint32_t)m, keys,
+                                                                         d_ids, gmin, shift, bst,
+                                                                         Ps);
             SKY_LAUNCH_CHECK();
             note_launch(c, 2);
         } else {
