@@ -285,7 +285,7 @@ def our_arm(args):
     sky_ms = sum(s["ms_sky_kernel"] for s in stats) / len(stats)
     gres_ms = sum(s["ms_gres_kernel"] for s in stats) / len(stats)
     st0 = stats[-1]
-    roof = roofline(st0, sky_ms, gres_ms, d, clk)
+    roof = roofline(st0, sky_ms, gres_ms, d, clk, args.workload)
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -328,27 +328,58 @@ def our_arm(args):
     return 0
 
 
-def roofline(st, sky_ms, gres_ms, d, clk):
-    """Compare roofline of the dominant dominance kernel:
-    R = N_SM * f_clk * L_pipe / I_test.  float64 path: I_test = 2d DSETP on
-    the FP64 pipe (64 lanes/clk/SM); u8 SWAR path: I_test = 5 integer ops on
-    the ALU pipe (64 lanes/clk/SM).  f_clk = median SM clock sampled during
-    the timed region (else the 1965 MHz max)."""
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "traffic.json")
+
+
+def kernel_traffic(workload, kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture
+    (profiles/traffic.json, written by scripts/ncu_summary.py), else None."""
+    try:
+        t = json.load(open(TRAFFIC_FILE))
+        return t.get(workload, {}).get(kernel)
+    except (OSError, ValueError):
+        return None
+
+
+def roofline(st, sky_ms, gres_ms, d, clk, workload="C2"):
+    """Compare roofline of the dominant dominance kernel family (SURVEY.md
+    §8(d)): R = N_SM * f_clk * L_pipe / I_test.  float64 dominance kernels:
+    I_test = 2d DSETP on the FP64 pipe (64 lanes/clk/SM); SWAR code kernels
+    (gres): 4 ALU ops per test for u32 code words (d <= 4), 8 for u64, on the
+    ALU pipe (64 lanes/clk/SM).  f_clk = median SM clock sampled during the
+    timed region (else the 1965 MHz max)."""
     f = (clk.get("sm_mhz") or 1965.0) * 1e6
-    if gres_ms > sky_ms and st["gres_kernel_launches"]:
-        kern = "k_gres_pairs_u8" if st["code_bits"] == 8 else "k_gres_pairs_f64"
-        tests, ms, launches = st["gres_tests"], gres_ms, st["gres_kernel_launches"]
-        i_test, l_pipe = (5, 64) if st["code_bits"] == 8 else (2 * d, 64)
-    else:
-        kern = "k_sfs_intra+k_sfs_filter"
-        tests, ms, launches = st["skyline_tests"], sky_ms, st["sky_kernel_launches"]
-        i_test, l_pipe = 2 * d, 64
-    peak = 148 * f * l_pipe / i_test
-    achieved = tests / (ms / 1e3) if ms > 0 else 0.0
-    return {"bound": "compare", "kernel": kern, "achieved": achieved / 1e9, "peak": peak / 1e9,
-            "unit": "Gtests/s", "frac": achieved / peak if peak else None, "traffic": None,
-            "tests_per_step": tests, "kernel_ms_per_step": ms, "launches_per_step": launches,
-            "I_test": i_test, "L_pipe": l_pipe, "f_clk_mhz": f / 1e6}
+
+    def one(kind):
+        if kind == "gres":
+            kern = "k_gres_pairs_tiled" if st["code_bits"] == 8 else "k_gres_pairs_f64"
+            tests, ms, launches = st["gres_tests"], gres_ms, st["gres_kernel_launches"]
+            if st["code_bits"] == 8:
+                i_test, pipe = (4 if d <= 4 else 8), "alu"
+            else:
+                i_test, pipe = 2 * d, "fp64"
+        else:
+            kern = "k_sfs_intra_sorted+k_sfs_filter_cells"
+            tests, ms, launches = st["skyline_tests"], sky_ms, st["sky_kernel_launches"]
+            i_test, pipe = 2 * d, "fp64"
+        l_pipe = 64
+        peak = 148 * f * l_pipe / i_test
+        achieved = tests / (ms / 1e3) if ms > 0 else 0.0
+        traffic = None
+        if launches:
+            tr = [kernel_traffic(workload, k) for k in kern.split("+")]
+            if all(t is not None for t in tr):
+                traffic = sum(tr)
+        return {"bound": "compare", "kernel": kern, "achieved": achieved / 1e9,
+                "peak": peak / 1e9, "unit": "Gtests/s", "frac": achieved / peak if peak else None,
+                "traffic": traffic, "traffic_unit": "B/launch (ncu dram read+write)",
+                "tests_per_step": tests, "kernel_ms_per_step": ms, "launches_per_step": launches,
+                "I_test": i_test, "L_pipe": l_pipe, "pipe": pipe, "f_clk_mhz": f / 1e6}
+
+    dominant = "gres" if gres_ms > sky_ms else "skyline"
+    r = one(dominant)
+    r["other"] = one("skyline" if dominant == "gres" else "gres")
+    return r
 
 
 def main():

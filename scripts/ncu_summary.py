@@ -3,7 +3,10 @@
 step) and full captures (duration, DRAM traffic, throughput, occupancy,
 stall reasons).
 
-    python scripts/ncu_summary.py gpurun_out/launches_C2.csv gpurun_out/prof_C2_*.ncu-rep > profiles/rNN_ncu_C2.md
+    python scripts/ncu_summary.py [--traffic C2] gpurun_out/launches_C2.csv gpurun_out/prof_C2_*.ncu-rep > profiles/rNN_ncu_C2.md
+
+--traffic W merges the captures' DRAM bytes per kernel into profiles/traffic.json
+(read by bench.py for roofline.traffic).
 """
 import collections
 import csv
@@ -92,9 +95,43 @@ def full_capture(path):
     return "\n".join(out)
 
 
+def traffic(path):
+    """{kernel base name: dram read+write bytes} of a full capture"""
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    out = {}
+    if len(rows) < 3:
+        return out
+    h, units = rows[0], rows[1]
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    for r in rows[2:]:
+        name = r[h.index("Kernel Name")].split("(")[0].split("<")[0].split("::")[-1]
+        tot = 0.0
+        for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            i = h.index(key)
+            tot += float(r[i].replace(",", "")) * scale.get(units[i], 1)
+        out[name] = tot
+    return out
+
+
 def main():
+    import json
+    import os
     parts = []
-    for p in sys.argv[1:]:
+    args = sys.argv[1:]
+    workload = None
+    if args and args[0] == "--traffic":
+        workload, args = args[1], args[2:]
+    if workload:
+        tf = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles",
+                          "traffic.json")
+        data = json.load(open(tf)) if os.path.exists(tf) else {}
+        for p in args:
+            if p.endswith(".ncu-rep"):
+                data.setdefault(workload, {}).update(traffic(p))
+        json.dump(data, open(tf, "w"), indent=1, sort_keys=True)
+    for p in args:
         if p.endswith(".csv"):
             parts.append("### Launch list (one step)\n\n" + launch_list(p) + "\n")
         elif p.endswith(".ncu-rep"):
