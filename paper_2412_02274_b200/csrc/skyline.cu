@@ -121,30 +121,54 @@ constexpr int kSampleItems = 4;
 __global__ void __launch_bounds__(1024)
 k_sample_threshold(const unsigned long long* __restrict__ key, const uint32_t* __restrict__ R,
                    uint64_t r, uint64_t want, unsigned long long* __restrict__ slots) {
-    using Sort = cub::BlockRadixSort<unsigned long long, 1024, kSampleItems>;
-    __shared__ typename Sort::TempStorage tmp;
+    // An approximate quantile suffices (T is exact once chosen): the samples
+    // are bucketed linearly between their min and max sum and the bucket
+    // holding the q-th sample gives T — one histogram, no sort.
+    using Scan = cub::BlockScan<uint32_t, 1024>;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ uint32_t hist[1024];
+    __shared__ unsigned long long smin, smax;
     constexpr uint64_t NS = 1024 * kSampleItems;
     if (want >= r) {
         if (threadIdx.x == 0) slots[S_THR] = ~0ULL;
         return;
     }
+    hist[threadIdx.x] = 0;
+    if (threadIdx.x == 0) smin = ~0ULL, smax = 0;
+    __syncthreads();
     unsigned long long items[kSampleItems];
+    unsigned long long mn = ~0ULL, mx = 0;
 #pragma unroll
     for (int j = 0; j < kSampleItems; ++j) {
         const uint64_t s = threadIdx.x * kSampleItems + j;
         const uint64_t pos = s * r / NS;
         const uint32_t t = R ? R[pos] : (uint32_t)pos;
         items[j] = key[t];
+        mn = items[j] < mn ? items[j] : mn;
+        mx = items[j] > mx ? items[j] : mx;
     }
-    // an approximate quantile suffices (T is exact once chosen): sort the
-    // samples on their top 32 key bits only — half the radix passes
-    Sort(tmp).Sort(items, 32, 64);
-    uint64_t q = want * NS / r;
-    if (q >= NS) q = NS - 1;
-    if (threadIdx.x == q / kSampleItems) {
+    atomicMin(&smin, mn);
+    atomicMax(&smax, mx);
+    __syncthreads();
+    const double lo = __longlong_as_double((long long)smin);
+    const double hi = __longlong_as_double((long long)smax);
+    const double scale = hi > lo ? 1024.0 / (hi - lo) : 0.0;
 #pragma unroll
-        for (int j = 0; j < kSampleItems; ++j)
-            if (j == (int)(q % kSampleItems)) slots[S_THR] = items[j] + 1;
+    for (int j = 0; j < kSampleItems; ++j) {
+        int b = (int)((__longlong_as_double((long long)items[j]) - lo) * scale);
+        b = b < 0 ? 0 : (b > 1023 ? 1023 : b);
+        atomicAdd(&hist[b], 1u);
+    }
+    __syncthreads();
+    uint32_t incl = 0;
+    Scan(tmp).InclusiveSum(hist[threadIdx.x], incl);
+    const uint64_t q = want * NS / r + 1;  // samples wanted below T
+    const uint32_t prev = incl - hist[threadIdx.x];
+    if (prev < q && incl >= q) {  // exactly one thread: the bucket holding the q-th sample
+        const double bound = lo + (double)(threadIdx.x + 1) / scale;
+        unsigned long long T = threadIdx.x == 1023 || !(scale > 0.0) ? smax + 1 : ord_bits(bound);
+        if (T <= smin) T = smin + 1;  // progress: the smallest sample is always selected
+        slots[S_THR] = T;
     }
 }
 
@@ -756,7 +780,103 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
     uint64_t kernel_launches = 0;
     uint32_t* Rnext = Rbuf1;
     bool ids_sorted = true;
+    // sort a prefix by (sum, id), decide it (K4) and append its skyline tuples
+    // to K; true when the whole undecided set was this prefix
+    auto decide_prefix = [&](uint32_t* Pfull, uint64_t m, bool final_round) -> bool {
+            // ---- sort the prefix by (sum, id)
+            uint32_t* Ps = c.buf[B_IDX1].as<uint32_t>(m);
+            uint32_t* order = Ps;
+            if (m <= kCTACap) {
+                const unsigned long long gmin = c.h_slots[S_SMIN] == ~0ULL ? 0 : c.h_slots[S_SMIN];
+                const unsigned long long thr = c.h_slots[S_THR];
+                const unsigned long long gmax = c.h_slots[S_SMAX];
+                const unsigned long long top = thr == ~0ULL || thr - 1 > gmax ? gmax : thr - 1;
+                const unsigned long long span = top > gmin ? top - gmin : 0;
+                int bits = span ? 64 - __builtin_clzll(span) : 0;
+                const int shift = bits > 12 ? bits - 12 : 0;  // 4096 buckets
+                uint32_t* Pb = c.buf[B_GTMP1].as<uint32_t>(m);
+                uint32_t* bst = c.buf[B_ORDER].as<uint32_t>(kMaxCells + 1 + kKeyBuckets + 1) +
+                                (kMaxCells + 1);
+                k_bucket_order<<<1, 1024, 0, c.stream>>>(Pfull, (uint32_t)m, keys, gmin, shift, Pb, bst);
+                SKY_LAUNCH_CHECK();
+                k_bucket_rank<<<grid_for(m, kBlock), kBlock, 0, c.stream>>>(Pb, (uint32_t)m, keys,
+                                                                             d_ids, gmin, shift, bst,
+                                                                             Ps);
+                SKY_LAUNCH_CHECK();
+                note_launch(c, 2);
+            } else {
+                unsigned long long* Pkey = c.buf[B_KEY1].as<unsigned long long>(m);
+                unsigned long long* Pkey2 = c.buf[B_GTMP0].as<unsigned long long>(m);
+                unsigned long long* kcur;
+                if (ids_sorted) {
+                    k_keys_of<<<grid_for(m, kBlock), kBlock, 0, c.stream>>>(keys, Pfull, m, Pkey);
+                    SKY_LAUNCH_CHECK();
+                    sort_pairs<unsigned long long>(c, Pkey, Pkey2, Pfull, Ps, m, 64, &kcur, &order);
+                } else {  // stable LSD: by id first, then by sum
+                    unsigned long long* ik0 = c.buf[B_GTMP1].as<unsigned long long>(m);
+                    k_id_keys<<<grid_for(m, kBlock), kBlock, 0, c.stream>>>(d_ids, Pfull, m, ik0);
+                    SKY_LAUNCH_CHECK();
+                    unsigned long long* ikc;
+                    uint32_t* by_id;
+                    sort_pairs<unsigned long long>(c, ik0, Pkey2, Pfull, Ps, m, 64, &ikc, &by_id);
+                    uint32_t* other = by_id == Pfull ? Ps : Pfull;
+                    k_keys_of<<<grid_for(m, kBlock), kBlock, 0, c.stream>>>(keys, by_id, m, Pkey);
+                    SKY_LAUNCH_CHECK();
+                    sort_pairs<unsigned long long>(c, Pkey, Pkey2, by_id, other, m, 64, &kcur, &order);
+                }
+                note_launch(c, 2);
+            }
+            double* Av = c.buf[B_MISC].as<double>(m * d);
+            k_gather_aos<<<grid_for(m * d, kBlock), kBlock, 0, c.stream>>>(d_vals, d, order, m, nullptr,
+                                                                            Av);
+            SKY_LAUNCH_CHECK();
+            note_launch(c);
+            trace_mark(c, "sky: (sync) + sort prefix + gather");
+
+            // ---- K4: SFS inside the prefix, predecessors in sum order
+            uint8_t* keep = c.buf[B_FLAGS].as<uint8_t>(m);
+            const uint64_t wi = std::min<uint64_t>(m, (uint64_t)c.num_sms * 64);
+            SKY_CUDA(cudaEventRecord(e0, c.stream));
+            dispatch_d(d, [&](auto DC) {
+                constexpr int D = decltype(DC)::value;
+                k_sfs_intra_sorted<D><<<(unsigned)((wi * 32 + kBlock - 1) / kBlock), kBlock, 0,
+                                        c.stream>>>(Av, (uint32_t)m, d, keep, c.d_slots + S_TESTS_SKY);
+            });
+            SKY_CUDA(cudaEventRecord(e1, c.stream));
+            SKY_LAUNCH_CHECK();
+            note_launch(c);
+            trace_mark(c, "sky: K4 intra kernel");
+            // A' in (sum, id) order appended to K; its count lands in S_C2
+            if (m <= kCTACap) {
+                k_cta_select<<<1, 1024, 0, c.stream>>>(order, nullptr, keep, (uint32_t)m, K + kc,
+                                                       nullptr, c.d_slots + S_C2);
+                SKY_LAUNCH_CHECK();
+                note_launch(c);
+            } else {
+                select_flags<uint32_t>(c, order, m, keep, K + kc, c.d_slots + S_C2);
+            }
+            ++rounds;
+            kernel_launches += 1;
+            if (final_round || m == r) {
+                read_slots(c, S_C2, 1);
+                float ms = 0;
+                SKY_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+                kernel_ms += ms;
+                kc += c.h_slots[S_C2];
+                return true;
+            }
+            return false;
+    };
     while (r > 0) {
+        // final round: the whole (already ordered) undecided list is the
+        // prefix — no threshold, no selection, no host synchronisation
+        if (checked && R && r <= kFinal) {
+            const uint64_t m = r;
+            c.h_slots[S_THR] = ~0ULL;
+            trace_mark(c, "sky: final round");
+            decide_prefix(R, m, /*final_round=*/true);
+            break;
+        }
         // ---- K2: sampled threshold, K3: ordered prefix selection
         const uint64_t w = r <= kFinal ? r : want;
         k_sample_threshold<<<1, 1024, 0, c.stream>>>(keys, R, r, w, c.d_slots);
@@ -788,88 +908,8 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
         const uint64_t m = c.h_slots[S_C1];
         if (m == 0) throw Error(SKYGPU_ERUNTIME, "skyline: empty prefix (internal)");
 
-        // ---- sort the prefix by (sum, id)
-        uint32_t* Ps = c.buf[B_IDX1].as<uint32_t>(m);
-        uint32_t* order = Ps;
-        if (m <= kCTACap) {
-            const unsigned long long gmin = c.h_slots[S_SMIN] == ~0ULL ? 0 : c.h_slots[S_SMIN];
-            const unsigned long long thr = c.h_slots[S_THR];
-            const unsigned long long gmax = c.h_slots[S_SMAX];
-            const unsigned long long top = thr == ~0ULL || thr - 1 > gmax ? gmax : thr - 1;
-            const unsigned long long span = top > gmin ? top - gmin : 0;
-            int bits = span ? 64 - __builtin_clzll(span) : 0;
-            const int shift = bits > 12 ? bits - 12 : 0;  // 4096 buckets
-            uint32_t* Pb = c.buf[B_GTMP1].as<uint32_t>(m);
-            uint32_t* bst = c.buf[B_ORDER].as<uint32_t>(kMaxCells + 1 + kKeyBuckets + 1) +
-                            (kMaxCells + 1);
-            k_bucket_order<<<1, 1024, 0, c.stream>>>(Pfull, (uint32_t)m, keys, gmin, shift, Pb, bst);
-            SKY_LAUNCH_CHECK();
-            k_bucket_rank<<<grid_for(m, kBlock), kBlock, 0, c.stream>>>(Pb, (uint32_t)m, keys,
-                                                                         d_ids, gmin, shift, bst,
-                                                                         Ps);
-            SKY_LAUNCH_CHECK();
-            note_launch(c, 2);
-        } else {
-            unsigned long long* Pkey = c.buf[B_KEY1].as<unsigned long long>(m);
-            unsigned long long* Pkey2 = c.buf[B_GTMP0].as<unsigned long long>(m);
-            unsigned long long* kcur;
-            if (ids_sorted) {
-                k_keys_of<<<grid_for(m, kBlock), kBlock, 0, c.stream>>>(keys, Pfull, m, Pkey);
-                SKY_LAUNCH_CHECK();
-                sort_pairs<unsigned long long>(c, Pkey, Pkey2, Pfull, Ps, m, 64, &kcur, &order);
-            } else {  // stable LSD: by id first, then by sum
-                unsigned long long* ik0 = c.buf[B_GTMP1].as<unsigned long long>(m);
-                k_id_keys<<<grid_for(m, kBlock), kBlock, 0, c.stream>>>(d_ids, Pfull, m, ik0);
-                SKY_LAUNCH_CHECK();
-                unsigned long long* ikc;
-                uint32_t* by_id;
-                sort_pairs<unsigned long long>(c, ik0, Pkey2, Pfull, Ps, m, 64, &ikc, &by_id);
-                uint32_t* other = by_id == Pfull ? Ps : Pfull;
-                k_keys_of<<<grid_for(m, kBlock), kBlock, 0, c.stream>>>(keys, by_id, m, Pkey);
-                SKY_LAUNCH_CHECK();
-                sort_pairs<unsigned long long>(c, Pkey, Pkey2, by_id, other, m, 64, &kcur, &order);
-            }
-            note_launch(c, 2);
-        }
-        double* Av = c.buf[B_MISC].as<double>(m * d);
-        k_gather_aos<<<grid_for(m * d, kBlock), kBlock, 0, c.stream>>>(d_vals, d, order, m, nullptr,
-                                                                        Av);
-        SKY_LAUNCH_CHECK();
-        note_launch(c);
-        trace_mark(c, "sky: (sync) + sort prefix + gather");
+        if (decide_prefix(Pfull, m, false)) break;
 
-        // ---- K4: SFS inside the prefix, predecessors in sum order
-        uint8_t* keep = c.buf[B_FLAGS].as<uint8_t>(m);
-        const uint64_t wi = std::min<uint64_t>(m, (uint64_t)c.num_sms * 64);
-        SKY_CUDA(cudaEventRecord(e0, c.stream));
-        dispatch_d(d, [&](auto DC) {
-            constexpr int D = decltype(DC)::value;
-            k_sfs_intra_sorted<D><<<(unsigned)((wi * 32 + kBlock - 1) / kBlock), kBlock, 0,
-                                    c.stream>>>(Av, (uint32_t)m, d, keep, c.d_slots + S_TESTS_SKY);
-        });
-        SKY_CUDA(cudaEventRecord(e1, c.stream));
-        SKY_LAUNCH_CHECK();
-        note_launch(c);
-        trace_mark(c, "sky: K4 intra kernel");
-        // A' in (sum, id) order appended to K; its count lands in S_C2
-        if (m <= kCTACap) {
-            k_cta_select<<<1, 1024, 0, c.stream>>>(order, nullptr, keep, (uint32_t)m, K + kc,
-                                                   nullptr, c.d_slots + S_C2);
-            SKY_LAUNCH_CHECK();
-            note_launch(c);
-        } else {
-            select_flags<uint32_t>(c, order, m, keep, K + kc, c.d_slots + S_C2);
-        }
-        ++rounds;
-        kernel_launches += 1;
-        if (m == r) {
-            read_slots(c, S_C2, 1);
-            float ms = 0;
-            SKY_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-            kernel_ms += ms;
-            kc += c.h_slots[S_C2];
-            break;
-        }
         // ---- K5: filter the rest against A', A' regrouped by direction cell
         // (one-CTA counting sort) so a candidate meets its own cell first
         uint32_t ncells = 1;
