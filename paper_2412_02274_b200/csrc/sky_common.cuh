@@ -67,7 +67,7 @@ enum BufId {
     B_IN_VALS, B_IN_IDS, B_KEY0, B_KEY1, B_IDX0, B_IDX1, B_SV, B_SID, B_SPOS,
     B_R0, B_R1, B_FLAGS, B_KLIST, B_CUB, B_SKYV, B_SKYID, B_CODES, B_ACT0, B_ACT1,
     B_DEN, B_GTMP0, B_GTMP1, B_OUTPOS, B_PROJ, B_REPS, B_MISC, B_CELLS, B_CSUM,
-    B_ORDER, B_COUNT
+    B_ORDER, B_AMAX, B_AQ, B_PQ, B_COUNT
 };
 
 // Device-side scalar slots (one small allocation, read back through pinned memory).

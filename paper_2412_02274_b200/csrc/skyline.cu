@@ -61,19 +61,38 @@ void dispatch_d(int d, F&& f) {
 }
 
 // K1 (core.cpp:21-23): sum with __dadd_rn from +0.0, key = ord bits (sums
-// are never -0.0: 0.0 + -0.0 = +0.0), value contract (Relation::add).
+// are never -0.0: 0.0 + -0.0 = +0.0), value contract (Relation::add), key
+// range, and (D in 1..8) the per-attribute maxima that scale the 16-bit
+// quantised codes of the dominance prefilter.
+template <int D>
 __global__ void k_score(const double* __restrict__ v, uint64_t n, int d,
                         unsigned long long* __restrict__ key,
-                        unsigned long long* __restrict__ slots) {
+                        unsigned long long* __restrict__ slots,
+                        unsigned long long* __restrict__ amax) {
+    constexpr int DA = D > 0 ? D : 1;
     unsigned long long mn = ~0ULL, mx = 0;
+    unsigned long long am[DA];
+#pragma unroll
+    for (int k = 0; k < DA; ++k) am[k] = 0;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x) {
         double s = 0.0;
         bool bad = false;
-        for (int k = 0; k < d; ++k) {
-            double x = v[i * d + k];
-            bad |= !(x >= 0.0);  // negative or NaN
-            s = __dadd_rn(s, x);
+        if (D > 0) {
+#pragma unroll
+            for (int k = 0; k < DA; ++k) {
+                const double x = v[i * DA + k];
+                bad |= !(x >= 0.0);  // negative or NaN
+                s = __dadd_rn(s, x);
+                const unsigned long long xb = ord_bits(x);
+                am[k] = xb > am[k] ? xb : am[k];
+            }
+        } else {
+            for (int k = 0; k < d; ++k) {
+                const double x = v[i * d + k];
+                bad |= !(x >= 0.0);
+                s = __dadd_rn(s, x);
+            }
         }
         const unsigned long long b = ord_bits(s);
         key[i] = b;
@@ -87,10 +106,106 @@ __global__ void k_score(const double* __restrict__ v, uint64_t n, int d,
         const unsigned long long y = __shfl_down_sync(0xffffffffu, mx, o);
         mn = x < mn ? x : mn;
         mx = y > mx ? y : mx;
+#pragma unroll
+        for (int k = 0; k < DA; ++k) {
+            const unsigned long long z = __shfl_down_sync(0xffffffffu, am[k], o);
+            am[k] = z > am[k] ? z : am[k];
+        }
     }
-    if ((threadIdx.x & 31) == 0) {  // key range of the relation
+    // block-level combine first: one set of atomics per block, not per warp
+    __shared__ unsigned long long s_mn[32], s_mx[32], s_am[32][DA];
+    const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        s_mn[warp] = mn;
+        s_mx[warp] = mx;
+#pragma unroll
+        for (int k = 0; k < DA; ++k) s_am[warp][k] = am[k];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {  // key range of the relation, per-attribute maxima
+        for (int w = 1; w < nw; ++w) {
+            mn = s_mn[w] < mn ? s_mn[w] : mn;
+            mx = s_mx[w] > mx ? s_mx[w] : mx;
+#pragma unroll
+            for (int k = 0; k < DA; ++k) am[k] = s_am[w][k] > am[k] ? s_am[w][k] : am[k];
+        }
         atomicMin(&slots[S_SMIN], mn);
         atomicMax(&slots[S_SMAX], mx);
+        if (D > 0)
+#pragma unroll
+            for (int k = 0; k < DA; ++k) atomicMax(&amax[k], am[k]);
+    }
+}
+
+// ---- 16-bit quantised codes: an exact-safe prefilter for float64 dominance.
+// q_j(x) = min(floor(x * 32767 / max_j), 32767) is monotone in x, so
+// s_j <= t_j implies q_j(s) <= q_j(t): if any q_j(s) > q_j(t), s cannot
+// dominate t (exact reject).  Only pairs that pass (true dominators and rare
+// near-ties) take the float64 test.  Four 16-bit fields per u64 word (bit 15
+// of each field is the SWAR guard): ((qt | H) - qs) & H == H  <=>  all
+// fields qs <= qt.  D <= 4: one word, D <= 8: two.
+constexpr unsigned long long kH16 = 0x8000800080008000ULL;
+
+template <int D>
+struct QW {
+    static constexpr int W = D <= 4 ? 1 : 2;
+};
+
+template <int D>
+__device__ __forceinline__ void load_scales(const unsigned long long* __restrict__ amax,
+                                            double (&sc)[D]) {
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+        const double m = __longlong_as_double((long long)amax[k]);
+        sc[k] = m > 0.0 ? __ddiv_rn(32767.0, m) : 0.0;
+    }
+}
+
+template <int D>
+__device__ __forceinline__ void encode16(const double (&t)[D], const double (&sc)[D],
+                                         unsigned long long (&w)[QW<D>::W]) {
+#pragma unroll
+    for (int k = 0; k < QW<D>::W; ++k) w[k] = 0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+        double q = floor(__dmul_rn(t[k], sc[k]));
+        q = q < 32767.0 ? q : 32767.0;
+        w[k / 4] |= (unsigned long long)(unsigned)q << (16 * (k % 4));
+    }
+}
+
+template <int D>
+__device__ __forceinline__ bool le16(const unsigned long long* __restrict__ cs,
+                                     const unsigned long long (&tg)[QW<D>::W]) {
+    bool ok = true;
+#pragma unroll
+    for (int k = 0; k < QW<D>::W; ++k) ok &= ((tg[k] - cs[k]) & kH16) == kH16;
+    return ok;
+}
+
+// compact SoA float64 copy [D][cap] plus quantised codes [cap][W] of the
+// tuples list[0..count) (count from device when given), one thread per tuple
+template <int D>
+__global__ void k_gather_q(const double* __restrict__ v, const uint32_t* __restrict__ list,
+                           uint64_t cap, const unsigned long long* __restrict__ count,
+                           const unsigned long long* __restrict__ amax, double* __restrict__ out,
+                           unsigned long long* __restrict__ qout) {
+    const uint64_t mm = count ? *count : cap;
+    double sc[D];
+    load_scales<D>(amax, sc);
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < mm;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        double t[D];
+        const uint64_t p = list[k];
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            t[a] = v[p * D + a];
+            out[(uint64_t)a * cap + k] = t[a];
+        }
+        unsigned long long w[QW<D>::W];
+        encode16<D>(t, sc, w);
+#pragma unroll
+        for (int a = 0; a < QW<D>::W; ++a) qout[k * QW<D>::W + a] = w[a];
     }
 }
 
@@ -589,6 +704,148 @@ k_sfs_filter_cells(const double* __restrict__ v, int d, const unsigned long long
     add_count(tests, cnt);
 }
 
+// K4 with the quantised prefilter (D in 1..8): candidate i against its
+// predecessors in sum order, 64 per ballot (two per lane); a comparator
+// whose 16-bit codes are not all <= the candidate's is rejected with one
+// SWAR test per code word, the rest take the exact float64 test.
+template <int D>
+__global__ void __launch_bounds__(kBlock)
+k_sfs_intra_q(const double* __restrict__ Av, const unsigned long long* __restrict__ Aq,
+              uint32_t m, uint8_t* __restrict__ keep, unsigned long long* __restrict__ tests) {
+    constexpr int W = QW<D>::W;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    unsigned long long cnt = 0;
+    for (uint32_t i = warp; i < m; i += nwarps) {
+        double t[D];
+#pragma unroll
+        for (int k = 0; k < D; ++k) t[k] = Av[(uint64_t)k * m + i];
+        unsigned long long tg[W];
+#pragma unroll
+        for (int k = 0; k < W; ++k) tg[k] = Aq[(uint64_t)i * W + k] | kH16;
+        bool dominated = false;
+        for (uint32_t j0 = 0; j0 < i; j0 += 64) {
+            bool hit = false;
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const uint32_t j = j0 + u * 32 + lane;
+                if (j < i) {
+                    ++cnt;
+                    if (le16<D>(Aq + (uint64_t)j * W, tg)) {
+                        double s[D];
+#pragma unroll
+                        for (int k = 0; k < D; ++k) s[k] = Av[(uint64_t)k * m + j];
+                        hit |= dom_f64<D>(s, t);
+                    }
+                }
+            }
+            if (__any_sync(0xffffffffu, hit)) {
+                dominated = true;
+                break;
+            }
+        }
+        if (lane == 0) keep[i] = dominated ? 0 : 1;
+    }
+    add_count(tests, cnt);
+}
+
+// K5 with the quantised prefilter (D in 1..8); see k_sfs_filter_cells for
+// the batching and the cell-ordered scan, k_sfs_intra_q for the prefilter.
+template <int D>
+__global__ void __launch_bounds__(kBlock)
+k_sfs_filter_q(const double* __restrict__ v, const unsigned long long* __restrict__ key,
+               const uint32_t* __restrict__ R, uint32_t r, const double* __restrict__ Pv,
+               const unsigned long long* __restrict__ Pq, uint32_t pcap,
+               const uint32_t* __restrict__ seg, int m, const unsigned long long* __restrict__ amax,
+               const unsigned long long* __restrict__ slots, uint8_t* __restrict__ keep,
+               unsigned long long* __restrict__ tests, uint32_t bs) {
+    constexpr int W = QW<D>::W;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    const unsigned long long T = slots[S_THR];
+    const uint32_t np = (uint32_t)slots[S_C2];
+    double sc[D];
+    load_scales<D>(amax, sc);
+    unsigned long long cnt = 0;
+    for (uint32_t base = warp * bs; base < r; base += nwarps * bs) {
+        const uint32_t idx = base + lane;
+        const bool valid = lane < bs && idx < r;
+        const uint32_t p = valid ? (R ? R[idx] : idx) : 0;
+        double t[D];
+#pragma unroll
+        for (int k = 0; k < D; ++k) t[k] = valid ? v[(uint64_t)p * D + k] : 0.0;
+        unsigned long long tq[W];
+        encode16<D>(t, sc, tq);
+        const bool need = valid && !(key[p] < T);  // not in the (decided) prefix
+        const uint32_t start = (need && seg) ? seg[direction_cell<D>(t, D, m)] : 0;
+        // phase A — every lane alone: the first kSolo comparators of its own
+        // cell (most candidates are dominated there; no shuffles, no votes)
+        constexpr uint32_t kSolo = 32;
+        bool mykeep = need, undecided = need;
+        if (need) {
+            unsigned long long tgl[W];
+#pragma unroll
+            for (int k = 0; k < W; ++k) tgl[k] = tq[k] | kH16;
+            uint32_t q = start >= np ? 0 : start;
+            const uint32_t lim = np < kSolo ? np : kSolo;
+            for (uint32_t s = 0; s < lim; ++s) {
+                ++cnt;
+                if (le16<D>(Pq + (uint64_t)q * W, tgl)) {
+                    double sv[D];
+#pragma unroll
+                    for (int k = 0; k < D; ++k) sv[k] = Pv[(uint64_t)k * pcap + q];
+                    if (dom_f64<D>(sv, t)) {
+                        mykeep = false;
+                        undecided = false;
+                        break;
+                    }
+                }
+                if (++q >= np) q = 0;
+            }
+            if (lim == np) undecided = false;  // every comparator tested
+        }
+        // phase B — warp-cooperative: the rest of the comparators for the
+        // still-undecided candidates, 32 per ballot
+        unsigned todo = __ballot_sync(0xffffffffu, undecided);
+        while (todo) {
+            const int j = __ffs(todo) - 1;
+            todo &= todo - 1;
+            double tj[D];
+#pragma unroll
+            for (int k = 0; k < D; ++k) tj[k] = __shfl_sync(0xffffffffu, t[k], j);
+            unsigned long long tg[W];
+#pragma unroll
+            for (int k = 0; k < W; ++k) tg[k] = __shfl_sync(0xffffffffu, tq[k], j) | kH16;
+            uint32_t q = __shfl_sync(0xffffffffu, start, j) + kSolo + lane;
+            while (q >= np) q -= np;
+            bool dominated = false;
+            for (uint32_t done = kSolo; done < np; done += 32) {
+                bool hit = false;
+                if (done + lane < np) {
+                    ++cnt;
+                    if (le16<D>(Pq + (uint64_t)q * W, tg)) {
+                        double s[D];
+#pragma unroll
+                        for (int k = 0; k < D; ++k) s[k] = Pv[(uint64_t)k * pcap + q];
+                        hit = dom_f64<D>(s, tj);
+                    }
+                }
+                q += 32;
+                while (q >= np) q -= np;
+                if (__any_sync(0xffffffffu, hit)) {
+                    dominated = true;
+                    break;
+                }
+            }
+            if ((int)lane == j) mykeep = !dominated;
+        }
+        if (valid) keep[idx] = mykeep ? 1 : 0;
+    }
+    add_count(tests, cnt);
+}
+
 // One-CTA order-preserving compaction of up to 16384 flagged items (and
 // their cell keys); the count lands in *count.
 __global__ void __launch_bounds__(1024)
@@ -737,7 +994,15 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
     zero_slots(c);
     auto* keys = c.buf[B_KEY0].as<unsigned long long>(n);
     trace_mark(c, "sky: start");
-    k_score<<<gb, kBlock, 0, c.stream>>>(d_vals, n, d, keys, c.d_slots);
+    // quantised prefilter for 1 <= d <= 8 (per-attribute maxima from K1)
+    const bool qpre = d >= 1 && d <= 8;
+    unsigned long long* amax = c.buf[B_AMAX].as<unsigned long long>(kMaxDims);
+    SKY_CUDA(cudaMemsetAsync(amax, 0, sizeof(unsigned long long) * kMaxDims, c.stream));
+    dispatch_d(d, [&](auto DC) {
+        constexpr int D = decltype(DC)::value;
+        k_score<D><<<grid_for(n, kBlock, c.num_sms * 8), kBlock, 0, c.stream>>>(
+            d_vals, n, d, keys, c.d_slots, amax);
+    });
     SKY_LAUNCH_CHECK();
     k_ids_check<<<gb, kBlock, 0, c.stream>>>(d_ids, n, c.d_slots);
     SKY_LAUNCH_CHECK();
@@ -827,8 +1092,16 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
                 note_launch(c, 2);
             }
             double* Av = c.buf[B_MISC].as<double>(m * d);
-            k_gather_aos<<<grid_for(m * d, kBlock), kBlock, 0, c.stream>>>(d_vals, d, order, m, nullptr,
-                                                                            Av);
+            unsigned long long* Aq = qpre ? c.buf[B_AQ].as<unsigned long long>(m * 2) : nullptr;
+            dispatch_d(d, [&](auto DC) {
+                constexpr int D = decltype(DC)::value;
+                if constexpr (D > 0)
+                    k_gather_q<D><<<grid_for(m, kBlock), kBlock, 0, c.stream>>>(
+                        d_vals, order, m, nullptr, amax, Av, Aq);
+                else
+                    k_gather_aos<<<grid_for(m * d, kBlock), kBlock, 0, c.stream>>>(
+                        d_vals, d, order, m, nullptr, Av);
+            });
             SKY_LAUNCH_CHECK();
             note_launch(c);
             trace_mark(c, "sky: (sync) + sort prefix + gather");
@@ -839,8 +1112,13 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
             SKY_CUDA(cudaEventRecord(e0, c.stream));
             dispatch_d(d, [&](auto DC) {
                 constexpr int D = decltype(DC)::value;
-                k_sfs_intra_sorted<D><<<(unsigned)((wi * 32 + kBlock - 1) / kBlock), kBlock, 0,
-                                        c.stream>>>(Av, (uint32_t)m, d, keep, c.d_slots + S_TESTS_SKY);
+                const unsigned grid = (unsigned)((wi * 32 + kBlock - 1) / kBlock);
+                if constexpr (D > 0)
+                    k_sfs_intra_q<D><<<grid, kBlock, 0, c.stream>>>(Av, Aq, (uint32_t)m, keep,
+                                                                    c.d_slots + S_TESTS_SKY);
+                else
+                    k_sfs_intra_sorted<D><<<grid, kBlock, 0, c.stream>>>(
+                        Av, (uint32_t)m, d, keep, c.d_slots + S_TESTS_SKY);
             });
             SKY_CUDA(cudaEventRecord(e1, c.stream));
             SKY_LAUNCH_CHECK();
@@ -934,8 +1212,16 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
             psrc = Alist;
         }
         double* Pv = c.buf[B_CSUM].as<double>(m * d);
-        k_gather_aos<<<grid_for(m * d, kBlock), kBlock, 0, c.stream>>>(d_vals, d, psrc, m,
-                                                                        c.d_slots + S_C2, Pv);
+        unsigned long long* Pq = qpre ? c.buf[B_PQ].as<unsigned long long>(m * 2) : nullptr;
+        dispatch_d(d, [&](auto DC) {
+            constexpr int D = decltype(DC)::value;
+            if constexpr (D > 0)
+                k_gather_q<D><<<grid_for(m, kBlock), kBlock, 0, c.stream>>>(
+                    d_vals, psrc, m, c.d_slots + S_C2, amax, Pv, Pq);
+            else
+                k_gather_aos<<<grid_for(m * d, kBlock), kBlock, 0, c.stream>>>(
+                    d_vals, d, psrc, m, c.d_slots + S_C2, Pv);
+        });
         SKY_LAUNCH_CHECK();
         note_launch(c);
         const uint32_t bsf = batch_size(c, r);
@@ -945,10 +1231,15 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
         SKY_CUDA(cudaEventRecord(e2, c.stream));
         dispatch_d(d, [&](auto DC) {
             constexpr int D = decltype(DC)::value;
-            k_sfs_filter_cells<D><<<(unsigned)((wf * 32 + kBlock - 1) / kBlock), kBlock, 0,
-                                    c.stream>>>(d_vals, d, keys, R, (uint32_t)r, Pv, (uint32_t)m,
-                                                seg, mcell, c.d_slots, fkeep,
-                                                c.d_slots + S_TESTS_SKY, bsf);
+            const unsigned grid = (unsigned)((wf * 32 + kBlock - 1) / kBlock);
+            if constexpr (D > 0)
+                k_sfs_filter_q<D><<<grid, kBlock, 0, c.stream>>>(
+                    d_vals, keys, R, (uint32_t)r, Pv, Pq, (uint32_t)m, seg, mcell, amax,
+                    c.d_slots, fkeep, c.d_slots + S_TESTS_SKY, bsf);
+            else
+                k_sfs_filter_cells<D><<<grid, kBlock, 0, c.stream>>>(
+                    d_vals, d, keys, R, (uint32_t)r, Pv, (uint32_t)m, seg, mcell, c.d_slots, fkeep,
+                    c.d_slots + S_TESTS_SKY, bsf);
         });
         SKY_CUDA(cudaEventRecord(e3, c.stream));
         SKY_LAUNCH_CHECK();
