@@ -345,6 +345,93 @@ k_gres_pairs_tiled(const W* __restrict__ codes, uint32_t S, int G, int g_max,
     add_count(tests, cnt);
 }
 
+// Resident pair kernel (default for S <= 2^21).  A block = 64 candidates
+// (8 warps x 8) x one comparator range of <= 512 tuples.  The block stages
+// ONCE the codes of every step for its range (<= 48 KB of shared memory) and
+// for its candidates; after that single barrier the 8 warps run through the
+// steps independently — no further barrier, no global load on the critical
+// path: for each g (descending) every lane tests one comparator against the
+// warp's still-undecided candidates (register-blocked, one LDS per 8 tests),
+// one redux.or per 32 comparators retires the hit candidates (answer g,
+// atomicMax(den, g)).  Exits found by blocks on other ranges arrive through
+// den, read one step ahead so the latency overlaps the scan.
+constexpr int kResCand = kCandPerWarp * (kBlock / 32);  // 64
+
+template <class W>
+__global__ void __launch_bounds__(kBlock)
+k_gres_pairs_resident(const W* __restrict__ codes, uint32_t S, int G, int g_max,
+                      const uint32_t* __restrict__ act, uint32_t na, uint32_t range,
+                      int32_t* __restrict__ den, unsigned long long* __restrict__ tests) {
+    constexpr W H = (W)kGuard;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    const uint32_t r0 = blockIdx.y * range;
+    const uint32_t rl = min(range, S - r0);
+    W* comp = reinterpret_cast<W*>(smraw);      // [G][rl]
+    W* cand = comp + (size_t)G * rl;             // [G][64]
+    for (uint32_t i = threadIdx.x; i < (uint32_t)G * rl; i += kBlock) {
+        const uint32_t gi = i / rl, k = i - gi * rl;
+        comp[i] = codes[(uint64_t)gi * S + r0 + k];
+    }
+    for (uint32_t i = threadIdx.x; i < (uint32_t)G * kResCand; i += kBlock) {
+        const uint32_t gi = i / kResCand, l = i - gi * kResCand;
+        const uint32_t idx = blockIdx.x * kResCand + l;
+        cand[i] = idx < na ? codes[(uint64_t)gi * S + act[idx]] : (W)0;
+    }
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    volatile int32_t* vden = den;
+    uint32_t t[kCandPerWarp];
+    int best[kCandPerWarp];
+#pragma unroll
+    for (int c = 0; c < kCandPerWarp; ++c) {
+        const uint32_t idx = blockIdx.x * kResCand + warp * kCandPerWarp + c;
+        t[c] = idx < na ? act[idx] : 0;
+        best[c] = idx < na ? vden[t[c]] : 0x7fffffff;
+    }
+    unsigned long long cnt = 0;
+    for (int gi = 0; gi < G; ++gi) {
+        const int g = g_max - gi;
+        unsigned alive = 0;
+#pragma unroll
+        for (int c = 0; c < kCandPerWarp; ++c)
+            if (best[c] < g) alive |= 1u << c;
+        if (!alive) break;
+        W tc[kCandPerWarp], tg[kCandPerWarp];
+        int nb[kCandPerWarp];
+#pragma unroll
+        for (int c = 0; c < kCandPerWarp; ++c) {
+            tc[c] = cand[gi * kResCand + warp * kCandPerWarp + c];
+            tg[c] = tc[c] | H;
+            nb[c] = ((alive >> c) & 1) ? vden[t[c]] : best[c];  // consumed after the scan
+        }
+        const W* cg = comp + (size_t)gi * rl;
+        for (uint32_t k0 = 0; k0 < rl && alive; k0 += 32) {
+            const uint32_t k = k0 + lane;
+            unsigned hits = 0;
+            if (k < rl) {
+                const W s = cg[k];
+#pragma unroll
+                for (int c = 0; c < kCandPerWarp; ++c)
+                    if ((alive >> c) & 1) hits |= (unsigned)dom_w<W>(s, tc[c], tg[c]) << c;
+                cnt += __popc(alive);
+            }
+            hits = __reduce_or_sync(0xffffffffu, hits);
+            if (hits) {
+                alive &= ~hits;
+#pragma unroll
+                for (int c = 0; c < kCandPerWarp; ++c)
+                    if ((hits >> c) & 1) {
+                        best[c] = g;
+                        if (lane == 0) atomicMax(&den[t[c]], g);
+                    }
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < kCandPerWarp; ++c) best[c] = max(best[c], nb[c]);
+    }
+    add_count(tests, cnt);
+}
+
 __global__ void k_finalize_den(const uint32_t* __restrict__ act, uint64_t na,
                                int32_t* __restrict__ den) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < na;
@@ -615,29 +702,60 @@ GresOut gres_device(Ctx& c, const double* d_skyv, const int64_t* d_ids, uint64_t
             k_codes_all<unsigned long long><<<cgrid, kBlock, 0, c.stream>>>(
                 d_skyv, S, d, out.g_max, G, (unsigned long long*)codes);
         SKY_LAUNCH_CHECK();
-        const uint64_t cand_tiles = (na + kCandPerBlock - 1) / kCandPerBlock;
-        const uint64_t target_blocks = (uint64_t)c.num_sms * 8;
-        uint64_t ranges = (target_blocks + cand_tiles - 1) / cand_tiles;
-        const uint64_t max_ranges = (S + 255) / 256;
-        ranges = std::max<uint64_t>(1, std::min(ranges, max_ranges));
-        uint64_t range = (S + ranges - 1) / ranges;
-        range = (range + 31) / 32 * 32;
-        ranges = (S + range - 1) / range;
-        if (ranges > 65535) {
-            ranges = 65535;
-            range = (S + ranges - 1) / ranges;
-        }
-        dim3 grid((unsigned)cand_tiles, (unsigned)ranges);
+        const bool resident = S <= (1u << 21) && !getenv("SKYGPU_GRES_TILED");
         trace_mark(c, "gres: shard list + codes");
-        SKY_CUDA(cudaEventRecord(e0, c.stream));
-        if (w32)
-            k_gres_pairs_tiled<uint32_t><<<grid, kBlock, 0, c.stream>>>(
-                (const uint32_t*)codes, (uint32_t)S, G, out.g_max, act, (uint32_t)na,
-                (uint32_t)range, d_den, c.d_slots + S_TESTS_GRES);
-        else
-            k_gres_pairs_tiled<unsigned long long><<<grid, kBlock, 0, c.stream>>>(
-                (const unsigned long long*)codes, (uint32_t)S, G, out.g_max, act, (uint32_t)na,
-                (uint32_t)range, d_den, c.d_slots + S_TESTS_GRES);
+        if (resident) {
+            const size_t wb = w32 ? 4 : 8;
+            const uint64_t tiles = (na + kResCand - 1) / kResCand;
+            // comparator range: <= 48 KB of codes per block, and enough blocks
+            // for ~8 per SM
+            uint64_t range = (48 * 1024) / ((uint64_t)G * wb);
+            range = std::max<uint64_t>(32, std::min<uint64_t>(range, 512));
+            const uint64_t want_ranges = ((uint64_t)c.num_sms * 8 + tiles - 1) / tiles;
+            range = std::min<uint64_t>(range, std::max<uint64_t>(32, (S + want_ranges - 1) / want_ranges));
+            range = (range + 31) / 32 * 32;
+            const uint64_t nranges = (S + range - 1) / range;
+            const size_t smem = ((size_t)G * range + (size_t)G * kResCand) * wb;
+            dim3 grid((unsigned)tiles, (unsigned)nranges);
+            if (nranges > 65535) throw Error(SKYGPU_ERUNTIME, "gres: too many comparator ranges");
+            SKY_CUDA(cudaEventRecord(e0, c.stream));
+            if (w32) {
+                SKY_CUDA(cudaFuncSetAttribute(k_gres_pairs_resident<uint32_t>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                k_gres_pairs_resident<uint32_t><<<grid, kBlock, smem, c.stream>>>(
+                    (const uint32_t*)codes, (uint32_t)S, G, out.g_max, act, (uint32_t)na,
+                    (uint32_t)range, d_den, c.d_slots + S_TESTS_GRES);
+            } else {
+                SKY_CUDA(cudaFuncSetAttribute(k_gres_pairs_resident<unsigned long long>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                k_gres_pairs_resident<unsigned long long><<<grid, kBlock, smem, c.stream>>>(
+                    (const unsigned long long*)codes, (uint32_t)S, G, out.g_max, act, (uint32_t)na,
+                    (uint32_t)range, d_den, c.d_slots + S_TESTS_GRES);
+            }
+        } else {
+            const uint64_t cand_tiles = (na + kCandPerBlock - 1) / kCandPerBlock;
+            const uint64_t target_blocks = (uint64_t)c.num_sms * 8;
+            uint64_t ranges = (target_blocks + cand_tiles - 1) / cand_tiles;
+            const uint64_t max_ranges = (S + 255) / 256;
+            ranges = std::max<uint64_t>(1, std::min(ranges, max_ranges));
+            uint64_t range = (S + ranges - 1) / ranges;
+            range = (range + 31) / 32 * 32;
+            ranges = (S + range - 1) / range;
+            if (ranges > 65535) {
+                ranges = 65535;
+                range = (S + ranges - 1) / ranges;
+            }
+            dim3 grid((unsigned)cand_tiles, (unsigned)ranges);
+            SKY_CUDA(cudaEventRecord(e0, c.stream));
+            if (w32)
+                k_gres_pairs_tiled<uint32_t><<<grid, kBlock, 0, c.stream>>>(
+                    (const uint32_t*)codes, (uint32_t)S, G, out.g_max, act, (uint32_t)na,
+                    (uint32_t)range, d_den, c.d_slots + S_TESTS_GRES);
+            else
+                k_gres_pairs_tiled<unsigned long long><<<grid, kBlock, 0, c.stream>>>(
+                    (const unsigned long long*)codes, (uint32_t)S, G, out.g_max, act, (uint32_t)na,
+                    (uint32_t)range, d_den, c.d_slots + S_TESTS_GRES);
+        }
         SKY_CUDA(cudaEventRecord(e1, c.stream));
         SKY_LAUNCH_CHECK();
         trace_mark(c, "gres: tiled pair kernel");

@@ -1037,7 +1037,14 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
     st.tuples_into_parallel = r;
 
     uint64_t kc = 0;
-    uint64_t want = 12000;  // stays below the one-CTA capacity despite sampling noise
+    // prefix size per round: stays below the one-CTA capacity despite
+    // sampling noise (SKYGPU_PREFIX overrides, for tuning)
+    static const uint64_t kWant = [] {
+        const char* e = getenv("SKYGPU_PREFIX");
+        const long long v = e ? atoll(e) : 0;
+        return v > 0 ? (uint64_t)v : (uint64_t)8000;
+    }();
+    uint64_t want = kWant;
     const uint64_t kMaxPrefix = 65536, kFinal = kCTACap;
     int rounds = 0;
     cudaEvent_t e0 = c.ev[8], e1 = c.ev[9], e2 = c.ev[14], e3 = c.ev[15];
