@@ -391,9 +391,15 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--engine", type=int, default=0)
+    ap.add_argument("--strategy", default=None, choices=["none", "grid", "angular", "sliced"],
+                    help="override the workload's partitioning plan (both arms)")
+    ap.add_argument("--partitions", type=int, default=None, help="override the target partitions")
     ap.add_argument("--cpu-repeat", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.strategy or args.partitions:
+        gen, n, d, seed, strat, p, cap = WORKLOADS[args.workload]
+        WORKLOADS[args.workload] = (gen, n, d, seed, args.strategy or strat, args.partitions or p, cap)
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
     if args.impl == "reference":

@@ -294,11 +294,23 @@ struct BelowThreshold {
     __device__ __forceinline__ bool operator()(uint32_t t) const { return key[t] < *thr; }
 };
 
+// Scan-order cells.  The reference partitions the relation (grid, angular,
+// sliced — partition.cpp:85-213) so that each local SFS sees nearby tuples;
+// here the plan's partition of a tuple decides which comparators its scan
+// visits FIRST (own partition, then the rest), never the result.  A cell
+// spec packs (kind << 16 | m):
+//   kind 0  direction cells: grid over u_j = t_j / sum(t), j < d-1, m bins
+//   kind 1  Grid plan: the reference's grid cell (partition.cpp:85-109), m slices
+//   kind 2  Angular plan: the reference's hyperspherical angles
+//           (partition.cpp:139-174), m slices per angle
+//   kind 3  Sliced plan: m slices of attribute 0 (equi-width over its range;
+//           the reference's exact equi-depth ranks only change the order)
+enum CellKind { kCellDirection = 0, kCellGrid = 1, kCellAngular = 2, kCellSliced = 3 };
+
 // Direction cell of a tuple: a grid over its first d-1 normalised
-// coordinates u_j = t_j / sum(t) (a cheap stand-in for the paper's angular
-// coordinates, partition.cpp:139-174).  A dominator s of t lies in the
-// orthant below t; on large-skyline data (tuples near a hyperplane) that
-// means a nearby direction, so scanning t's own cell first finds it early.
+// coordinates u_j = t_j / sum(t).  A dominator s of t lies in the orthant
+// below t; on large-skyline data (tuples near a hyperplane) that means a
+// nearby direction, so scanning t's own cell first finds it early.
 template <int DM>
 __device__ __forceinline__ uint32_t direction_cell(const double* t, int dd, int m) {
     if (dd < 2 || m <= 1) return 0;
@@ -317,12 +329,110 @@ __device__ __forceinline__ uint32_t direction_cell(const double* t, int dd, int 
     return cell;
 }
 
+// grid cell index, partition.cpp:85-109 (values validated in [0,1])
+template <int DM>
+__device__ __forceinline__ uint32_t grid_cell_id(const double* t, int dd, int m) {
+    uint32_t id = 0, w = 1;
+    for (int k = 0; k < DM; ++k) {
+        if (k >= dd) break;
+        int b = (int)(t[k] * m);
+        b = b < 0 ? 0 : (b >= m ? m - 1 : b);
+        id += (uint32_t)b * w;
+        w *= (uint32_t)m;
+    }
+    return id;
+}
+
+// angular partition id, partition.cpp:139-174 (all-zero tuple -> 0)
+template <int DM>
+__device__ __forceinline__ uint32_t angular_cell_id(const double* t, int dd, int m) {
+    bool zero = true;
+    for (int k = 0; k < DM; ++k)
+        if (k < dd) zero &= (t[k] == 0.0);
+    if (zero || dd < 2) return 0;
+    double tail[DM + 1];
+    tail[dd] = 0.0;
+    for (int k = DM - 1; k >= 0; --k)
+        if (k < dd) tail[k] = tail[k + 1] + t[k] * t[k];
+    uint32_t id = 0, w = 1;
+    for (int k = 0; k < DM - 1; ++k) {
+        if (k >= dd - 1) break;
+        const double angle = atan2(sqrt(tail[k + 1]), t[k]);
+        int b = (int)((2.0 * angle / 3.14159265358979323846) * m);
+        b = b < 0 ? 0 : (b >= m ? m - 1 : b);
+        id += (uint32_t)b * w;
+        w *= (uint32_t)m;
+    }
+    return id;
+}
+
+template <int DM>
+__device__ __forceinline__ uint32_t plan_cell(const double* t, int dd, int spec,
+                                              const unsigned long long* __restrict__ amax) {
+    const int kind = spec >> 16, m = spec & 0xFFFF;
+    switch (kind) {
+        case kCellGrid: return grid_cell_id<DM>(t, dd, m);
+        case kCellAngular: return angular_cell_id<DM>(t, dd, m);
+        case kCellSliced: {
+            const double mx = amax ? __longlong_as_double((long long)amax[0]) : 1.0;
+            int b = mx > 0.0 ? (int)(t[0] / mx * m) : 0;
+            return (uint32_t)(b < 0 ? 0 : (b >= m ? m - 1 : b));
+        }
+        default: return direction_cell<DM>(t, dd, m);
+    }
+}
+
+// Grid plan pre-merge pruning (parallel.cpp:32-42, partition.cpp:115-137): a
+// cell strictly above a non-empty cell in every dimension holds no skyline
+// tuple (each of its tuples is strictly dominated by — and so preceded by —
+// any tuple of the lower cell).  Occupancy over the m^d cells, an inclusive
+// prefix-OR along every dimension, then cell c is pruned iff the prefix-OR at
+// c - (1,..,1) is set.
+__global__ void k_grid_occ(const double* __restrict__ v, uint64_t n, int d, int m,
+                           uint8_t* __restrict__ occ) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        occ[grid_cell_id<kMaxDims>(v + i * d, d, m)] = 1;
+}
+
+__global__ void k_prefix_or_dim(uint8_t* __restrict__ occ, uint32_t ncells, int m,
+                                uint32_t stride) {
+    const uint32_t lines = ncells / m;
+    for (uint32_t l = blockIdx.x * blockDim.x + threadIdx.x; l < lines; l += gridDim.x * blockDim.x) {
+        const uint32_t lo = l % stride, hi = l / stride;
+        const uint32_t base = hi * stride * m + lo;
+        uint8_t acc = 0;
+        for (int k = 0; k < m; ++k) {
+            acc |= occ[base + (uint32_t)k * stride];
+            occ[base + (uint32_t)k * stride] = acc;
+        }
+    }
+}
+
+__global__ void k_grid_keep(const double* __restrict__ v, uint64_t n, int d, int m,
+                            const uint8_t* __restrict__ P, uint8_t* __restrict__ keep) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const double* t = v + i * d;
+        uint32_t low = 0, w = 1;
+        bool inner = true;
+        for (int k = 0; k < d; ++k) {
+            int b = (int)(t[k] * m);
+            b = b < 0 ? 0 : (b >= m ? m - 1 : b);
+            inner &= b >= 1;
+            low += (uint32_t)(b - 1) * w;
+            w *= (uint32_t)m;
+        }
+        keep[i] = !(inner && P[low]);
+    }
+}
+
 // K3b: cell of every prefix member, then a one-CTA counting sort by cell
 // (m <= 16384): cell-ordered list + cell keys.  Order inside a cell is free.
 template <int D>
 __global__ void __launch_bounds__(1024)
 k_cell_order(const double* __restrict__ v, int d, const uint32_t* __restrict__ in, uint32_t mcap,
-             const unsigned long long* __restrict__ count, int mcell, uint32_t ncells,
+             const unsigned long long* __restrict__ count, int mcell, uint32_t ncells, const unsigned long long* __restrict__ amax,
              uint32_t* __restrict__ out, uint32_t* __restrict__ out_cell) {
     constexpr int DM = D > 0 ? D : kMaxDims;
     const int dd = D > 0 ? D : d;
@@ -341,7 +451,7 @@ k_cell_order(const double* __restrict__ v, int d, const uint32_t* __restrict__ i
 #pragma unroll
             for (int k = 0; k < DM; ++k)
                 if (k < dd) t[k] = v[p * dd + k];
-            cl[j] = direction_cell<DM>(t, dd, mcell);
+            cl[j] = plan_cell<DM>(t, dd, mcell, amax);
             atomicAdd(&cnt[cl[j]], 1u);
         }
     }
@@ -375,7 +485,8 @@ k_cell_order(const double* __restrict__ v, int d, const uint32_t* __restrict__ i
 
 template <int D>
 __global__ void k_cells_of(const double* __restrict__ v, int d, const uint32_t* __restrict__ in,
-                           uint32_t m, int mcell, uint32_t* __restrict__ cell) {
+                           uint32_t m, int mcell, const unsigned long long* __restrict__ amax,
+                           uint32_t* __restrict__ cell) {
     constexpr int DM = D > 0 ? D : kMaxDims;
     const int dd = D > 0 ? D : d;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
@@ -384,7 +495,7 @@ __global__ void k_cells_of(const double* __restrict__ v, int d, const uint32_t* 
 #pragma unroll
         for (int k = 0; k < DM; ++k)
             if (k < dd) t[k] = v[p * dd + k];
-        cell[i] = direction_cell<DM>(t, dd, mcell);
+        cell[i] = plan_cell<DM>(t, dd, mcell, amax);
     }
 }
 
@@ -424,7 +535,8 @@ __global__ void k_gather_aos(const double* __restrict__ v, int d, const uint32_t
 template <int D>
 __global__ void k_rep_filter(const double* __restrict__ v, uint64_t n, int d,
                              const double* __restrict__ reps, uint32_t n_reps,
-                             uint8_t* __restrict__ keep, unsigned long long* __restrict__ tests) {
+                             uint8_t* __restrict__ keep, unsigned long long* __restrict__ tests,
+                             int and_mode) {
     constexpr int DM = D > 0 ? D : kMaxDims;
     const int dd = D > 0 ? D : d;
     unsigned long long cnt = 0;
@@ -439,7 +551,7 @@ __global__ void k_rep_filter(const double* __restrict__ v, uint64_t n, int d,
             ++cnt;
             alive = !dom_f64_dyn(reps + (uint64_t)r * dd, t, dd);
         }
-        keep[p] = alive;
+        keep[p] = and_mode ? (uint8_t)(keep[p] && alive) : (uint8_t)alive;
     }
     add_count(tests, cnt);
 }
@@ -779,7 +891,7 @@ k_sfs_filter_q(const double* __restrict__ v, const unsigned long long* __restric
         unsigned long long tq[W];
         encode16<D>(t, sc, tq);
         const bool need = valid && !(key[p] < T);  // not in the (decided) prefix
-        const uint32_t start = (need && seg) ? seg[direction_cell<D>(t, D, m)] : 0;
+        const uint32_t start = (need && seg) ? seg[plan_cell<D>(t, D, m, amax)] : 0;
         // phase A — every lane alone: the first kSolo comparators of its own
         // cell (most candidates are dominated there; no shuffles, no votes)
         constexpr uint32_t kSolo = 32;
@@ -965,6 +1077,43 @@ uint32_t batch_size(const Ctx& c, uint64_t count) {
     return (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(32, bs));
 }
 
+int cells_per_dim(uint64_t m, int d, uint32_t* ncells);
+
+// The scan-order cell spec of a plan (see plan_cell): the plan's own
+// partition when it has at most kMaxCells parts (and d <= 8 for the
+// attribute-scaled kinds), else direction cells sized for ~128 tuples each.
+int scan_cell_spec(const skygpu_plan& plan, uint64_t m, int d, bool qpre, uint32_t* ncells) {
+    auto ipow = [](uint64_t b, int e) {
+        uint64_t v = 1;
+        for (int i = 0; i < e; ++i) {
+            v *= b;
+            if (v > kMaxCells) return (uint64_t)kMaxCells + 1;
+        }
+        return v;
+    };
+    if (qpre && plan.strategy == SKYGPU_GRID && plan.slices >= 1) {
+        const uint64_t nc = ipow((uint64_t)plan.slices, d);
+        if (nc > 1 && nc <= kMaxCells) {
+            *ncells = (uint32_t)nc;
+            return (kCellGrid << 16) | plan.slices;
+        }
+    }
+    if (qpre && plan.strategy == SKYGPU_ANGULAR && plan.slices >= 1 && d >= 2) {
+        const uint64_t nc = ipow((uint64_t)plan.slices, d - 1);
+        if (nc > 1 && nc <= kMaxCells) {
+            *ncells = (uint32_t)nc;
+            return (kCellAngular << 16) | plan.slices;
+        }
+    }
+    if (qpre && plan.strategy == SKYGPU_SLICED && plan.partitions > 1) {
+        const uint32_t nc = (uint32_t)std::min<long long>(plan.partitions, kMaxCells);
+        *ncells = nc;
+        return (kCellSliced << 16) | (int)nc;
+    }
+    const int mc = cells_per_dim(m, d, ncells);
+    return mc > 1 ? mc : 0;
+}
+
 // bins per normalised coordinate so that the cells hold ~128 tuples each
 int cells_per_dim(uint64_t m, int d, uint32_t* ncells) {
     int mcell = 1;
@@ -1020,16 +1169,44 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
     uint32_t* K = c.buf[B_KLIST].as<uint32_t>(n);
     uint32_t* seg_table = c.buf[B_ORDER].as<uint32_t>(kMaxCells + 1 + kKeyBuckets + 1);
     bool checked = false;
-    if (n_reps > 0) {
-        uint8_t* rflags = c.buf[B_FLAGS].as<uint8_t>(n);
-        dispatch_d(d, [&](auto DC) {
-            constexpr int D = decltype(DC)::value;
-            k_rep_filter<D><<<gb, kBlock, 0, c.stream>>>(d_vals, n, d, d_reps, (uint32_t)n_reps,
-                                                          rflags, c.d_slots + S_TESTS_SKY);
-        });
-        SKY_LAUNCH_CHECK();
-        note_launch(c);
-        select_flags<uint32_t>(c, nullptr, n, rflags, Rbuf0, c.d_slots + S_C3);
+    // pre-merge pruning: the Grid plan's dominated cells (parallel.cpp:32-42)
+    // and the representative filter (partition.cpp:287-302)
+    uint64_t grid_cells = 0;
+    if (plan.strategy == SKYGPU_GRID && plan.slices >= 2) {
+        grid_cells = 1;
+        for (int k = 0; k < d && grid_cells <= (1u << 22); ++k) grid_cells *= (uint64_t)plan.slices;
+        if (grid_cells > (1u << 22)) grid_cells = 0;  // too fine to tabulate: skip pruning
+    }
+    if (grid_cells || n_reps > 0) {
+        uint8_t* pre = c.buf[B_FLAGS].as<uint8_t>(n);
+        if (grid_cells) {
+            const int m = plan.slices;
+            uint8_t* occ = c.buf[B_CELLS].as<uint8_t>(grid_cells);
+            SKY_CUDA(cudaMemsetAsync(occ, 0, grid_cells, c.stream));
+            k_grid_occ<<<gb, kBlock, 0, c.stream>>>(d_vals, n, d, m, occ);
+            SKY_LAUNCH_CHECK();
+            uint32_t stride = 1;
+            for (int k = 0; k < d; ++k, stride *= (uint32_t)m) {
+                k_prefix_or_dim<<<grid_for(grid_cells / m, kBlock), kBlock, 0, c.stream>>>(
+                    occ, (uint32_t)grid_cells, m, stride);
+                SKY_LAUNCH_CHECK();
+            }
+            k_grid_keep<<<gb, kBlock, 0, c.stream>>>(d_vals, n, d, m, occ, pre);
+            SKY_LAUNCH_CHECK();
+            note_launch(c, 2 + d);
+        }
+        if (n_reps > 0) {
+            dispatch_d(d, [&](auto DC) {
+                constexpr int D = decltype(DC)::value;
+                k_rep_filter<D><<<gb, kBlock, 0, c.stream>>>(d_vals, n, d, d_reps,
+                                                              (uint32_t)n_reps, pre,
+                                                              c.d_slots + S_TESTS_SKY,
+                                                              grid_cells ? 1 : 0);
+            });
+            SKY_LAUNCH_CHECK();
+            note_launch(c);
+        }
+        select_flags<uint32_t>(c, nullptr, n, pre, Rbuf0, c.d_slots + S_C3);
         read_slots(c, S_BAD, 11);  // S_BAD .. S_C3 (checks + survivors)
         R = Rbuf0;
         r = c.h_slots[S_C3];
@@ -1195,20 +1372,20 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
 
         if (decide_prefix(Pfull, m, false)) break;
 
-        // ---- K5: filter the rest against A', A' regrouped by direction cell
-        // (one-CTA counting sort) so a candidate meets its own cell first
+        // ---- K5: filter the rest against A', A' regrouped by the plan's
+        // partition (one-CTA counting sort) so a candidate meets its own first
         uint32_t ncells = 1;
-        int mcell = m <= kCTACap ? cells_per_dim(m, d, &ncells) : 1;
+        const int mcell = m <= kCTACap ? scan_cell_spec(plan, m, d, qpre, &ncells) : 0;
         uint32_t* seg = nullptr;
         const uint32_t* psrc = K + kc;
-        if (mcell > 1) {
+        if (ncells > 1) {
             uint32_t* Alist = c.buf[B_GTMP1].as<uint32_t>(m);
             uint32_t* Akey = c.buf[B_GTMP0].as<uint32_t>(m);
             dispatch_d(d, [&](auto DC) {
                 constexpr int D = decltype(DC)::value;
                 k_cell_order<D><<<1, 1024, 0, c.stream>>>(d_vals, d, K + kc, (uint32_t)m,
-                                                          c.d_slots + S_C2, mcell, ncells, Alist,
-                                                          Akey);
+                                                          c.d_slots + S_C2, mcell, ncells,
+                                                          qpre ? amax : nullptr, Alist, Akey);
             });
             SKY_LAUNCH_CHECK();
             seg = seg_table;
