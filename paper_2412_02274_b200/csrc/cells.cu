@@ -1,0 +1,232 @@
+// cells.cu — the cell-occupancy gres engine.
+//
+// At step g a skyline tuple t is ejected iff some skyline tuple's code vector
+// dominates t's (gres.cu header).  Equivalently: some OCCUPIED cell c' of the
+// code grid satisfies c' <= c(t) componentwise and c' != c(t), i.e.
+//     OR_j  P[c(t) - e_j]      (over j with c_j(t) >= 1)
+// where P is the inclusive prefix-OR of the cell occupancy.  The cost per step
+// is O(cells + S) instead of O(S^2): the right engine for huge skylines
+// (ANT d=7 at n=10^7, where S ~ n and the pair engine needs ~10^15 tests).
+//
+// Layout: one bit per cell along attribute 0 (extent e_0 <= 64 -> a u32/u64
+// word per "row"), rows indexed by attributes 1..d-1 (attribute 1 fastest).
+// Per step: memset, mark (atomicOr per skyline tuple), in-word prefix-OR
+// (attribute 0), one coalesced line sweep per attribute 1..d-1 (HBM-bound:
+// each sweep reads and writes every row once), then one query per undecided
+// candidate.  Exactness: the same codes floor(v*g) as the pair engine.
+#include <cmath>
+#include <vector>
+
+#include "sky_common.cuh"
+
+namespace skygpu {
+
+namespace {
+
+constexpr int kBlock = 256;
+constexpr int kMaxCellDims = 16;
+
+struct CellGeom {
+    int d;
+    int g;
+    uint64_t rows;
+    uint64_t stride[kMaxCellDims];  // stride of attribute j >= 1 in rows
+    uint64_t ext[kMaxCellDims];     // code extent (max code + 1) of attribute j
+};
+
+template <class W>
+__global__ void k_cells_mark(const double* __restrict__ v, uint64_t S, CellGeom geo,
+                             W* __restrict__ rows) {
+    const double gd = (double)geo.g;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < S;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t r = 0;
+        for (int j = 1; j < geo.d; ++j) r += (uint64_t)floor(__dmul_rn(v[j * S + i], gd)) * geo.stride[j];
+        const unsigned c0 = (unsigned)floor(__dmul_rn(v[i], gd));
+        atomicOr(&rows[r], (W)1 << c0);
+    }
+}
+
+// prefix-OR inside each word: bit k |= bits 0..k-1 (attribute 0)
+template <class W>
+__global__ void k_cells_or_word(W* __restrict__ rows, uint64_t n) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        W x = rows[i];
+        x |= x << 1;
+        x |= x << 2;
+        x |= x << 4;
+        x |= x << 8;
+        x |= x << 16;
+        if (sizeof(W) == 8) x |= x << (sizeof(W) == 8 ? 32 : 0);
+        rows[i] = x;
+    }
+}
+
+// prefix-OR along attribute j: each thread sweeps one line of e_j rows;
+// consecutive threads own consecutive lines (coalesced when stride >= 32)
+template <class W>
+__global__ void k_cells_or_dim(W* __restrict__ rows, uint64_t nrows, uint64_t ext,
+                               uint64_t stride) {
+    const uint64_t lines = nrows / ext;
+    for (uint64_t l = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; l < lines;
+         l += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t lo = l % stride, hi = l / stride;
+        W* p = rows + hi * stride * ext + lo;
+        W acc = 0;
+        for (uint64_t k = 0; k < ext; ++k) {
+            acc |= p[k * stride];
+            p[k * stride] = acc;
+        }
+    }
+}
+
+template <class W>
+__global__ void k_cells_query(const double* __restrict__ v, uint64_t S, CellGeom geo,
+                              const W* __restrict__ P, const uint32_t* __restrict__ act,
+                              uint64_t na, int32_t* __restrict__ den,
+                              unsigned long long* __restrict__ undecided) {
+    const double gd = (double)geo.g;
+    unsigned long long left = 0;
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < na;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t t = act[k];
+        if (den[t] != 0) continue;
+        uint64_t r = 0;
+        unsigned cj[kMaxCellDims];
+        for (int j = 1; j < geo.d; ++j) {
+            cj[j] = (unsigned)floor(__dmul_rn(v[j * S + t], gd));
+            r += (uint64_t)cj[j] * geo.stride[j];
+        }
+        const unsigned c0 = (unsigned)floor(__dmul_rn(v[t], gd));
+        bool hit = c0 >= 1 && ((P[r] >> (c0 - 1)) & 1);
+        for (int j = 1; j < geo.d && !hit; ++j)
+            if (cj[j] >= 1) hit = (P[r - geo.stride[j]] >> c0) & 1;
+        if (hit) den[t] = geo.g;
+        else ++left;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) left += __shfl_down_sync(0xffffffffu, left, o);
+    if ((threadIdx.x & 31) == 0 && left) atomicAdd(undecided, left);
+}
+
+__global__ void k_col_max(const double* __restrict__ v, uint64_t S, int d,
+                          unsigned long long* __restrict__ out) {
+    for (int j = blockIdx.y; j < d; j += gridDim.y) {
+        unsigned long long best = 0;
+        for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < S;
+             i += (uint64_t)gridDim.x * blockDim.x) {
+            const unsigned long long b = ord_bits(v[(uint64_t)j * S + i]);
+            best = b > best ? b : best;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long x = __shfl_down_sync(0xffffffffu, best, o);
+            best = x > best ? x : best;
+        }
+        if ((threadIdx.x & 31) == 0) atomicMax(&out[j], best);
+    }
+}
+
+}  // namespace
+
+// Per-step extents of the code grid; false when the engine does not apply
+// (d > 16, a code extent beyond 64 along attribute 0, or a grid that would
+// not fit the memory budget).
+static bool cells_geometry(const std::vector<double>& amax, int d, int g, uint64_t budget_rows,
+                           CellGeom* geo, uint64_t* e0) {
+    if (d < 1 || d > kMaxCellDims) return false;
+    geo->d = d;
+    geo->g = g;
+    uint64_t rows = 1;
+    for (int j = 0; j < d; ++j) {
+        const double k = std::floor(amax[j] * (double)g);  // same rounding as __dmul_rn
+        if (!(k >= 0) || k > 1e12) return false;
+        const uint64_t ext = (uint64_t)k + 1;
+        geo->ext[j] = ext;
+        if (j == 0) {
+            if (ext > 64) return false;
+            *e0 = ext;
+            continue;
+        }
+        geo->stride[j] = rows;
+        if (rows > budget_rows / ext) return false;
+        rows *= ext;
+    }
+    geo->rows = rows;
+    return true;
+}
+
+// Cell engine over S skyline tuples (SoA d_skyv), candidates act[0..na),
+// denominators into d_den (pre-zeroed); returns false (nothing done) when the
+// engine does not apply.  Runs steps g_max .. 2, stopping once every
+// candidate has its answer.
+bool gres_cells_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_max,
+                       const uint32_t* act, uint64_t na, int32_t* d_den, uint64_t* cells_swept,
+                       int* steps_run) {
+    if (g_max < 2 || S == 0 || d > kMaxCellDims) return false;
+    auto* colmax = c.buf[B_AMAX].as<unsigned long long>(kMaxDims);
+    SKY_CUDA(cudaMemsetAsync(colmax, 0, sizeof(unsigned long long) * kMaxDims, c.stream));
+    k_col_max<<<dim3(grid_for(S, kBlock, 296), (unsigned)d), kBlock, 0, c.stream>>>(d_skyv, S, d,
+                                                                                    colmax);
+    SKY_LAUNCH_CHECK();
+    note_launch(c);
+    std::vector<unsigned long long> bits(d);
+    SKY_CUDA(cudaMemcpyAsync(bits.data(), colmax, sizeof(unsigned long long) * d,
+                             cudaMemcpyDeviceToHost, c.stream));
+    SKY_CUDA(cudaStreamSynchronize(c.stream));
+    std::vector<double> amax(d);
+    for (int j = 0; j < d; ++j) memcpy(&amax[j], &bits[j], 8);
+    // memory budget: 16 GiB of rows at most
+    const uint64_t budget_rows = (16ull << 30) / 8;
+    CellGeom geo0;
+    uint64_t e0 = 0;
+    if (!cells_geometry(amax, d, g_max, budget_rows, &geo0, &e0)) return false;
+    const bool w64 = e0 > 32;
+    void* rows = c.buf[B_CELLS].get(geo0.rows * (w64 ? 8 : 4));
+    uint64_t swept = 0;
+    int steps = 0;
+    for (int g = g_max; g >= 2; --g) {
+        CellGeom geo;
+        uint64_t e0g = 0;
+        cells_geometry(amax, d, g, budget_rows, &geo, &e0g);
+        const size_t wb = w64 ? 8 : 4;
+        SKY_CUDA(cudaMemsetAsync(rows, 0, geo.rows * wb, c.stream));
+        const unsigned gs = grid_for(S, kBlock);
+        const unsigned gr = grid_for(geo.rows, kBlock);
+        if (w64) {
+            auto* R = static_cast<unsigned long long*>(rows);
+            k_cells_mark<unsigned long long><<<gs, kBlock, 0, c.stream>>>(d_skyv, S, geo, R);
+            k_cells_or_word<unsigned long long><<<gr, kBlock, 0, c.stream>>>(R, geo.rows);
+            for (int j = 1; j < d; ++j)
+                k_cells_or_dim<unsigned long long><<<grid_for(geo.rows / geo.ext[j], kBlock), kBlock,
+                                                     0, c.stream>>>(R, geo.rows, geo.ext[j],
+                                                                    geo.stride[j]);
+            reset_counts(c);
+            k_cells_query<unsigned long long><<<grid_for(na, kBlock), kBlock, 0, c.stream>>>(
+                d_skyv, S, geo, R, act, na, d_den, c.d_slots + S_C3);
+        } else {
+            auto* R = static_cast<unsigned*>(rows);
+            k_cells_mark<unsigned><<<gs, kBlock, 0, c.stream>>>(d_skyv, S, geo, R);
+            k_cells_or_word<unsigned><<<gr, kBlock, 0, c.stream>>>(R, geo.rows);
+            for (int j = 1; j < d; ++j)
+                k_cells_or_dim<unsigned><<<grid_for(geo.rows / geo.ext[j], kBlock), kBlock, 0,
+                                           c.stream>>>(R, geo.rows, geo.ext[j], geo.stride[j]);
+            reset_counts(c);
+            k_cells_query<unsigned><<<grid_for(na, kBlock), kBlock, 0, c.stream>>>(
+                d_skyv, S, geo, R, act, na, d_den, c.d_slots + S_C3);
+        }
+        SKY_LAUNCH_CHECK();
+        note_launch(c, 4 + d);
+        swept += geo.rows * (uint64_t)d;
+        ++steps;
+        // stop early once every candidate has its answer (one small read per step)
+        read_slots(c, S_C3, 1);
+        if (c.h_slots[S_C3] == 0) break;
+    }
+    *cells_swept = swept;
+    *steps_run = steps;
+    return true;
+}
+
+}  // namespace skygpu

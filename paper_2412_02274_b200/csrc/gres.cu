@@ -682,13 +682,35 @@ GresOut gres_device(Ctx& c, const double* d_skyv, const int64_t* d_ids, uint64_t
     const bool u8 = d <= 8 && code_max <= 127.0 && !ties_possible;
     st.code_bits = u8 ? 8 : 64;
     st.gres_engine = SKYGPU_GRES_PAIRS;
-    (void)engine;
 
     cudaEvent_t e0 = c.ev[10], e1 = c.ev[11];
     double kms = 0;
     uint64_t klaunch = 0;
     int steps = 0;
     const int G = out.g_max - 1;
+    // cell-occupancy engine (cells.cu): asked for, or AUTO on huge skylines
+    // where the pair engine's O(S^2) tests dominate
+    const bool want_cells = u8 && G >= 1 && na > 0 &&
+                            (engine == SKYGPU_GRES_CELLS ||
+                             (engine == SKYGPU_GRES_AUTO && S >= (1u << 18)));
+    if (want_cells) {
+        uint64_t swept = 0;
+        int steps_run = 0;
+        SKY_CUDA(cudaEventRecord(e0, c.stream));
+        if (gres_cells_device(c, d_skyv, S, d, out.g_max, act, na, d_den, &swept, &steps_run)) {
+            SKY_CUDA(cudaEventRecord(e1, c.stream));
+            k_finalize_den<<<grid_for(na, kBlock), kBlock, 0, c.stream>>>(act, na, d_den);
+            SKY_LAUNCH_CHECK();
+            note_launch(c);
+            c.gres_timing_pending = true;
+            st.gres_engine = SKYGPU_GRES_CELLS;
+            st.gres_cells = swept;
+            out.steps = G;
+            st.gres_steps = G;
+            st.gres_kernel_launches += steps_run;
+            return out;
+        }
+    }
     if (u8 && G >= 1 && na > 0) {
         // one launch for every step (north_star (b)): (candidate tile x
         // comparator range) blocks, per-step dominance with early exit

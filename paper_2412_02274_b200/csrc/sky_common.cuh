@@ -214,6 +214,11 @@ GresOut gres_device(Ctx& c, const double* d_skyv, const int64_t* d_ids, uint64_t
 // projection at step g leaves [0,1]
 void check_grid_projection(Ctx& c, const double* d_skyv, uint64_t S, int d, int g);
 
+// cells.cu: the cell-occupancy gres engine; false when it does not apply
+bool gres_cells_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_max,
+                       const uint32_t* act, uint64_t na, int32_t* d_den, uint64_t* cells_swept,
+                       int* steps_run);
+
 // float64 AoS -> SoA transpose on the device
 void aos_to_soa(Ctx& c, const double* d_aos, uint64_t n, int d, double* d_soa);
 

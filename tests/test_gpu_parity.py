@@ -141,3 +141,29 @@ def test_generic_dims_and_duplicates():
     assert res.positions.tolist() == pos.tolist()
     den, gm, _ = po.grid_resistance(v[pos], ids[pos], None)
     assert res.g_max == gm and res.den.tolist() == den.tolist()
+
+
+@pytest.mark.parametrize("name", ["C1_uni_100k_d4", "C2_ant_1M_d3", "C5_prefix_2k_d7",
+                                  "C5_prefix_10k_d7", "rand_ant_n1500_d5_angular",
+                                  "rand_lattice_n1500_d7_none", "uncapped_lattice_d3"])
+def test_cell_engine_matches_golden(name):
+    """The cell-occupancy gres engine (cells.cu) gives the reference's map."""
+    g = load_golden(name)
+    v, ids = golden_input(g, sk.generate)
+    res = sk.pipeline(v, ids, plan_of(g, v.shape[1]), cap=spec_cap(g), engine=sk.GRES_CELLS)
+    assert res.g_max == g["g_max"]
+    got = dict(zip(ids[res.positions].tolist(), res.den.tolist()))
+    assert [got[i] for i in g["skyline_ids"]] == g["den"]
+    if res.g_max >= 2:
+        assert res.stats["gres_engine"] == sk.GRES_CELLS
+
+
+@pytest.mark.parametrize("world", [2, 5])
+def test_cell_engine_shards(world):
+    v = sk.generate("ant", 30000, 6, 41)
+    full = sk.pipeline(v, cap=25, engine=sk.GRES_PAIRS)
+    acc = np.zeros_like(full.den)
+    for r in range(world):
+        part = sk.pipeline(v, cap=25, engine=sk.GRES_CELLS, shard_rank=r, shard_world=world)
+        acc = np.maximum(acc, part.den)
+    assert acc.tolist() == full.den.tolist()
