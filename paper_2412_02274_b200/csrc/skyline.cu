@@ -305,7 +305,13 @@ struct BelowThreshold {
 //           (partition.cpp:139-174), m slices per angle
 //   kind 3  Sliced plan: m slices of attribute 0 (equi-width over its range;
 //           the reference's exact equi-depth ranks only change the order)
-enum CellKind { kCellDirection = 0, kCellGrid = 1, kCellAngular = 2, kCellSliced = 3 };
+enum CellKind {
+    kCellDirection = 0,
+    kCellGrid = 1,
+    kCellAngular = 2,
+    kCellSliced = 3,
+    kCellQuantile = 4  // quantile grid over the raw attributes (qgrid_cell)
+};
 
 // Direction cell of a tuple: a grid over its first d-1 normalised
 // coordinates u_j = t_j / sum(t).  A dominator s of t lies in the orthant
@@ -366,12 +372,59 @@ __device__ __forceinline__ uint32_t angular_cell_id(const double* t, int dd, int
     return id;
 }
 
+// Quantile grid over the raw attributes (kind 4, the default scan index of
+// the filter): k bins per attribute, bounds = quantiles of the round's new
+// skyline tuples A', held in constant memory.  bin_j(t) = #bounds <= t_j is
+// monotone, so a tuple in a cell with bin_j above t's has its attribute j at
+// or above a bound that exceeds t_j.
+constexpr int kQMaxBins = 16;
+__constant__ double c_qbounds[kMaxDims * kQMaxBins];
+
+template <int DM>
+__device__ __forceinline__ uint32_t qgrid_cell(const double* t, int dd, int k) {
+    uint32_t id = 0, w = 1;
+    for (int j = 0; j < DM; ++j) {
+        if (j >= dd) break;
+        uint32_t b = 0;
+        for (int i = 0; i < k - 1; ++i) b += t[j] >= c_qbounds[j * kQMaxBins + i] ? 1u : 0u;
+        id += b * w;
+        w *= (uint32_t)k;
+    }
+    return id;
+}
+
+// bounds[j][i] = the (i+1)/k quantile of attribute j over list[0..*count)
+// (4096 strided samples, one CTA per attribute)
+__global__ void __launch_bounds__(1024)
+k_qgrid_bounds(const double* __restrict__ v, int d, const uint32_t* __restrict__ list,
+               const unsigned long long* __restrict__ count, int k, double* __restrict__ bounds) {
+    using Sort = cub::BlockRadixSort<unsigned long long, 1024, 4>;
+    __shared__ typename Sort::TempStorage tmp;
+    const int j = blockIdx.x;
+    const uint64_t m = *count;
+    unsigned long long items[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const uint64_t s = threadIdx.x * 4 + u;
+        items[u] = m ? ord_bits(v[(uint64_t)list[s * m / 4096] * d + j]) : 0ULL;
+    }
+    Sort(tmp).Sort(items);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const uint32_t rank = threadIdx.x * 4 + u;
+        for (int i = 1; i < k; ++i)
+            if (rank == (uint32_t)(i * 4096 / k))
+                bounds[j * kQMaxBins + i - 1] = __longlong_as_double((long long)items[u]);
+    }
+}
+
 template <int DM>
 __device__ __forceinline__ uint32_t plan_cell(const double* t, int dd, int spec,
                                               const unsigned long long* __restrict__ amax) {
     const int kind = spec >> 16, m = spec & 0xFFFF;
     switch (kind) {
         case kCellGrid: return grid_cell_id<DM>(t, dd, m);
+        case kCellQuantile: return qgrid_cell<DM>(t, dd, m);
         case kCellAngular: return angular_cell_id<DM>(t, dd, m);
         case kCellSliced: {
             const double mx = amax ? __longlong_as_double((long long)amax[0]) : 1.0;
@@ -862,17 +915,30 @@ k_sfs_intra_q(const double* __restrict__ Av, const unsigned long long* __restric
     add_count(tests, cnt);
 }
 
-// K5 with the quantised prefilter (D in 1..8); see k_sfs_filter_cells for
-// the batching and the cell-ordered scan, k_sfs_intra_q for the prefilter.
+// K5 with the quantised prefilter (D in 1..8).  Two scan modes:
+//  qk > 0  quantile grid (the default): the new skyline tuples A' are grouped
+//          by a k^d grid whose bin bounds are quantiles of A' itself; a
+//          comparator in a cell with any bin above the candidate's cannot
+//          dominate it (its value there is >= a bound > the candidate's), so
+//          only the cells <= the candidate's own cell are visited, own cell
+//          first, then descending — an EXACT pruning of the comparator set
+//          (the GPU recast of the paper's partition-level pruning).
+//  qk == 0 plan cells (grid / angular / sliced / direction): own partition
+//          first, then all others (scan order only).
+// Phase A: every lane alone tests the first 32 comparators of its own cell
+// (most candidates are dominated there — no shuffles, no votes); phase B:
+// warp-cooperative, 32 comparators per ballot, for the still-undecided ones.
 template <int D>
 __global__ void __launch_bounds__(kBlock)
 k_sfs_filter_q(const double* __restrict__ v, const unsigned long long* __restrict__ key,
                const uint32_t* __restrict__ R, uint32_t r, const double* __restrict__ Pv,
                const unsigned long long* __restrict__ Pq, uint32_t pcap,
-               const uint32_t* __restrict__ seg, int m, const unsigned long long* __restrict__ amax,
+               const uint32_t* __restrict__ seg, int m, int qk,
+               const unsigned long long* __restrict__ amax,
                const unsigned long long* __restrict__ slots, uint8_t* __restrict__ keep,
                unsigned long long* __restrict__ tests, uint32_t bs) {
     constexpr int W = QW<D>::W;
+    constexpr uint32_t kSolo = 32;
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -890,18 +956,26 @@ k_sfs_filter_q(const double* __restrict__ v, const unsigned long long* __restric
         for (int k = 0; k < D; ++k) t[k] = valid ? v[(uint64_t)p * D + k] : 0.0;
         unsigned long long tq[W];
         encode16<D>(t, sc, tq);
-        const bool need = valid && !(key[p] < T);  // not in the (decided) prefix
-        const uint32_t start = (need && seg) ? seg[plan_cell<D>(t, D, m, amax)] : 0;
-        // phase A — every lane alone: the first kSolo comparators of its own
-        // cell (most candidates are dominated there; no shuffles, no votes)
-        constexpr uint32_t kSolo = 32;
-        bool mykeep = need, undecided = need;
+        const bool need = valid && !(key[p] < T) && np > 0;  // not in the (decided) prefix
+        uint32_t mycell = 0, start = 0, lim = 0;
+        if (need && seg) {
+            mycell = qk > 0 ? qgrid_cell<D>(t, D, qk) : plan_cell<D>(t, D, m, amax);
+            start = seg[mycell];
+        }
         if (need) {
+            if (qk > 0) {
+                const uint32_t own = seg[mycell + 1] - start;
+                lim = own < kSolo ? own : kSolo;
+            } else {
+                lim = np < kSolo ? np : kSolo;
+            }
+        }
+        bool mykeep = need, undecided = need;
+        if (need) {  // phase A
             unsigned long long tgl[W];
 #pragma unroll
             for (int k = 0; k < W; ++k) tgl[k] = tq[k] | kH16;
             uint32_t q = start >= np ? 0 : start;
-            const uint32_t lim = np < kSolo ? np : kSolo;
             for (uint32_t s = 0; s < lim; ++s) {
                 ++cnt;
                 if (le16<D>(Pq + (uint64_t)q * W, tgl)) {
@@ -916,12 +990,10 @@ k_sfs_filter_q(const double* __restrict__ v, const unsigned long long* __restric
                 }
                 if (++q >= np) q = 0;
             }
-            if (lim == np) undecided = false;  // every comparator tested
+            if (qk == 0 && lim == np) undecided = false;  // every comparator tested
         }
-        // phase B — warp-cooperative: the rest of the comparators for the
-        // still-undecided candidates, 32 per ballot
         unsigned todo = __ballot_sync(0xffffffffu, undecided);
-        while (todo) {
+        while (todo) {  // phase B
             const int j = __ffs(todo) - 1;
             todo &= todo - 1;
             double tj[D];
@@ -930,25 +1002,73 @@ k_sfs_filter_q(const double* __restrict__ v, const unsigned long long* __restric
             unsigned long long tg[W];
 #pragma unroll
             for (int k = 0; k < W; ++k) tg[k] = __shfl_sync(0xffffffffu, tq[k], j) | kH16;
-            uint32_t q = __shfl_sync(0xffffffffu, start, j) + kSolo + lane;
-            while (q >= np) q -= np;
             bool dominated = false;
-            for (uint32_t done = kSolo; done < np; done += 32) {
-                bool hit = false;
-                if (done + lane < np) {
-                    ++cnt;
-                    if (le16<D>(Pq + (uint64_t)q * W, tg)) {
-                        double s[D];
+            if (qk > 0) {
+                // cells <= own, own first then descending (mixed-radix counter)
+                const uint32_t own = __shfl_sync(0xffffffffu, mycell, j);
+                const uint32_t skip = __shfl_sync(0xffffffffu, lim, j);
+                int od[D], dig[D];
+                uint32_t tmp = own;
 #pragma unroll
-                        for (int k = 0; k < D; ++k) s[k] = Pv[(uint64_t)k * pcap + q];
-                        hit = dom_f64<D>(s, tj);
-                    }
+                for (int k = 0; k < D; ++k) {
+                    od[k] = (int)(tmp % (uint32_t)qk);
+                    tmp /= (uint32_t)qk;
+                    dig[k] = od[k];
                 }
-                q += 32;
+                uint32_t cell = own;
+                while (true) {
+                    const uint32_t s1 = seg[cell + 1];
+                    for (uint32_t q0 = seg[cell] + (cell == own ? skip : 0); q0 < s1; q0 += 32) {
+                        const uint32_t q = q0 + lane;
+                        bool hit = false;
+                        if (q < s1) {
+                            ++cnt;
+                            if (le16<D>(Pq + (uint64_t)q * W, tg)) {
+                                double s[D];
+#pragma unroll
+                                for (int k = 0; k < D; ++k) s[k] = Pv[(uint64_t)k * pcap + q];
+                                hit = dom_f64<D>(s, tj);
+                            }
+                        }
+                        if (__any_sync(0xffffffffu, hit)) {
+                            dominated = true;
+                            break;
+                        }
+                    }
+                    if (dominated) break;
+                    int k = 0;
+                    uint32_t w = 1;
+                    for (; k < D; ++k, w *= (uint32_t)qk) {
+                        if (dig[k] > 0) {
+                            --dig[k];
+                            cell -= w;
+                            break;
+                        }
+                        dig[k] = od[k];
+                        cell += (uint32_t)od[k] * w;
+                    }
+                    if (k == D) break;  // every cell <= own visited
+                }
+            } else {
+                uint32_t q = __shfl_sync(0xffffffffu, start, j) + kSolo + lane;
                 while (q >= np) q -= np;
-                if (__any_sync(0xffffffffu, hit)) {
-                    dominated = true;
-                    break;
+                for (uint32_t done = kSolo; done < np; done += 32) {
+                    bool hit = false;
+                    if (done + lane < np) {
+                        ++cnt;
+                        if (le16<D>(Pq + (uint64_t)q * W, tg)) {
+                            double s[D];
+#pragma unroll
+                            for (int k = 0; k < D; ++k) s[k] = Pv[(uint64_t)k * pcap + q];
+                            hit = dom_f64<D>(s, tj);
+                        }
+                    }
+                    q += 32;
+                    while (q >= np) q -= np;
+                    if (__any_sync(0xffffffffu, hit)) {
+                        dominated = true;
+                        break;
+                    }
                 }
             }
             if ((int)lane == j) mykeep = !dominated;
@@ -1372,10 +1492,38 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
 
         if (decide_prefix(Pfull, m, false)) break;
 
-        // ---- K5: filter the rest against A', A' regrouped by the plan's
-        // partition (one-CTA counting sort) so a candidate meets its own first
+        // ---- K5: filter the rest against A', A' regrouped (one-CTA counting
+        // sort) by the quantile grid (exact cell pruning, default) or by the
+        // plan's partition (scan order only, SKYGPU_PLAN_CELLS=1)
+        // (the quantile grid is opt-in, SKYGPU_QGRID=1: its exact pruning pays
+        // only when candidates survive; measured slower on C2/C4)
+        static const bool qgrid = [] {
+            const char* e = getenv("SKYGPU_QGRID");
+            return e && e[0] == '1';
+        }();
         uint32_t ncells = 1;
-        const int mcell = m <= kCTACap ? scan_cell_spec(plan, m, d, qpre, &ncells) : 0;
+        int mcell = 0, qk = 0;
+        if (m <= kCTACap && qpre && qgrid) {
+            // k bins per attribute: ~32 tuples per cell, k^d <= kMaxCells
+            int k = (int)std::floor(std::pow(std::max(1.0, (double)m / 32.0), 1.0 / d) + 1e-9);
+            k = std::max(2, std::min(k, kQMaxBins));
+            while (k > 2 && std::pow((double)k, d) > kMaxCells) --k;
+            if (std::pow((double)k, d) <= kMaxCells) {
+                qk = k;
+                ncells = 1;
+                for (int j = 0; j < d; ++j) ncells *= (uint32_t)k;
+                mcell = (kCellQuantile << 16) | k;
+                double* bounds = c.buf[B_PROJ].as<double>(kMaxDims * kQMaxBins);
+                k_qgrid_bounds<<<d, 1024, 0, c.stream>>>(d_vals, d, K + kc, c.d_slots + S_C2, k,
+                                                         bounds);
+                SKY_LAUNCH_CHECK();
+                SKY_CUDA(cudaMemcpyToSymbolAsync(c_qbounds, bounds,
+                                                 sizeof(double) * kMaxDims * kQMaxBins, 0,
+                                                 cudaMemcpyDeviceToDevice, c.stream));
+                note_launch(c);
+            }
+        }
+        if (!qk && m <= kCTACap) mcell = scan_cell_spec(plan, m, d, qpre, &ncells);
         uint32_t* seg = nullptr;
         const uint32_t* psrc = K + kc;
         if (ncells > 1) {
@@ -1418,7 +1566,7 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
             const unsigned grid = (unsigned)((wf * 32 + kBlock - 1) / kBlock);
             if constexpr (D > 0)
                 k_sfs_filter_q<D><<<grid, kBlock, 0, c.stream>>>(
-                    d_vals, keys, R, (uint32_t)r, Pv, Pq, (uint32_t)m, seg, mcell, amax,
+                    d_vals, keys, R, (uint32_t)r, Pv, Pq, (uint32_t)m, seg, mcell, qk, amax,
                     c.d_slots, fkeep, c.d_slots + S_TESTS_SKY, bsf);
             else
                 k_sfs_filter_cells<D><<<grid, kBlock, 0, c.stream>>>(
