@@ -405,17 +405,33 @@ k_gres_pairs_resident(const W* __restrict__ codes, uint32_t S, int G, int g_max,
             nb[c] = ((alive >> c) & 1) ? vden[t[c]] : best[c];  // consumed after the scan
         }
         const W* cg = comp + (size_t)gi * rl;
+        // branch-free inner loop: every lane tests its comparator against all
+        // 8 candidates (x = tg - s: every guard bit set <=> s <= t bytewise;
+        // x > H <=> additionally s != t), one ballot per candidate, and the
+        // already-decided candidates are masked out afterwards.  Lanes past
+        // the range use the neutral code 0x7F..7F, which dominates nothing.
+        constexpr W kNeutral = (W)0x7F7F7F7F7F7F7F7FULL;
         for (uint32_t k0 = 0; k0 < rl && alive; k0 += 32) {
             const uint32_t k = k0 + lane;
+            const W s = k < rl ? cg[k] : kNeutral;
             unsigned hits = 0;
-            if (k < rl) {
-                const W s = cg[k];
 #pragma unroll
-                for (int c = 0; c < kCandPerWarp; ++c)
-                    if ((alive >> c) & 1) hits |= (unsigned)dom_w<W>(s, tc[c], tg[c]) << c;
-                cnt += __popc(alive);
+            for (int c = 0; c < kCandPerWarp; ++c) {
+                const W x = tg[c] - s;
+                const bool le = (x & H) == H;  // s <= t in every byte
+                unsigned bl;
+                if constexpr (sizeof(W) == 8) {
+                    // u64 words: the 64-bit strictness compare only when some
+                    // lane passed (warp-uniform branch) — fewer ALU ops per test
+                    bl = __ballot_sync(0xffffffffu, le);
+                    if (bl) bl = __ballot_sync(0xffffffffu, le & (x != H));
+                } else {
+                    bl = __ballot_sync(0xffffffffu, le & (x != H));
+                }
+                hits |= (bl != 0u ? 1u : 0u) << c;
             }
-            hits = __reduce_or_sync(0xffffffffu, hits);
+            hits &= alive;
+            if (k < rl) cnt += __popc(alive);
             if (hits) {
                 alive &= ~hits;
 #pragma unroll
