@@ -61,6 +61,8 @@ extern "C" {
 #define SKYGPU_DEVICE_PTRS 1u   /* vals/ids/outputs are device pointers */
 #define SKYGPU_CHECK_SKYLINE 2u /* O(S^2) "input is a skyline" check (gres.cpp:70-80, !NDEBUG) */
 #define SKYGPU_SKIP_GRES 4u     /* skyline only (harness mode "skyline") */
+#define SKYGPU_SKY_ROUNDS 8u    /* force the prefix-round skyline engine */
+#define SKYGPU_SKY_GRID 16u     /* force the one-pass rank-grid skyline engine (d <= 8) */
 
 /* mirrors skypar::PartitionPlan (partition.hpp:27-32) */
 typedef struct skygpu_plan {
@@ -84,7 +86,7 @@ typedef struct skygpu_stats {
     int gres_engine;               /* engine actually used */
     int code_bits;                 /* 8 = packed u8 codes, 64 = float64 projections */
     int sfs_rounds;                /* block-SFS rounds */
-    int pad_;
+    int sky_engine;                /* skyline engine used: 8 = prefix rounds, 16 = rank grid */
     double ms_total;               /* device time of the whole call (events) */
     double ms_h2d, ms_skyline, ms_gres, ms_d2h;
     double ms_gres_kernel;         /* summed time of the dominant gres kernel launches */

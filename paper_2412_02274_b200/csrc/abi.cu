@@ -522,7 +522,8 @@ int skygpu_pipeline(const double* vals, const int64_t* ids, uint64_t n, int d,
             di = bi;
         }
         Timer tsky(c, 4);
-        SkylineOut so = skyline_device(c, dv, di, n, d, pl, nullptr, 0);
+        SkylineOut so = skyline_device(c, dv, di, n, d, pl, nullptr, 0,
+                                       flags & (SKYGPU_SKY_ROUNDS | SKYGPU_SKY_GRID));
         tsky.stop(&c.st->ms_skyline);
         int32_t* den = c.buf[B_DEN].as<int32_t>(so.S ? so.S : 1);
         GresOut go;

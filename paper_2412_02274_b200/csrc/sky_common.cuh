@@ -67,7 +67,8 @@ enum BufId {
     B_IN_VALS, B_IN_IDS, B_KEY0, B_KEY1, B_IDX0, B_IDX1, B_SV, B_SID, B_SPOS,
     B_R0, B_R1, B_FLAGS, B_KLIST, B_CUB, B_SKYV, B_SKYID, B_CODES, B_ACT0, B_ACT1,
     B_DEN, B_GTMP0, B_GTMP1, B_OUTPOS, B_PROJ, B_REPS, B_MISC, B_CELLS, B_CSUM,
-    B_ORDER, B_AMAX, B_AQ, B_PQ, B_COUNT
+    B_ORDER, B_AMAX, B_AQ, B_PQ, B_GCODE, B_GCELL, B_GSCODE, B_GSIDX, B_GITEMS, B_GCNT,
+    B_COUNT
 };
 
 // Device-side scalar slots (one small allocation, read back through pinned memory).
@@ -195,8 +196,20 @@ struct SkylineOut {
 };
 
 // Skyline of n tuples already resident on the device (AoS vals, ids).
+// sky_engine: 0 auto, SKYGPU_SKY_ROUNDS or SKYGPU_SKY_GRID (skygpu.h flags)
 SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, uint64_t n, int d,
-                          const skygpu_plan& plan, const double* d_reps, uint64_t n_reps);
+                          const skygpu_plan& plan, const double* d_reps, uint64_t n_reps,
+                          unsigned sky_engine = 0);
+
+// skyline_grid.cu: the one-pass rank-grid engine for large skylines.
+// sky_grid_bins = bins per attribute for r tuples (0: shape unsupported, d > 8);
+// sky_grid_decide writes keep[i] = 1 iff tuple R[i] (R == nullptr: i) is kept
+// by the predecessor rule over R; adds the decide kernel's time to *kernel_ms
+// (synchronising on it) when kernel_ms != nullptr.
+int sky_grid_bins(uint64_t r, int d);
+void sky_grid_decide(Ctx& c, const double* d_vals, int d, const unsigned long long* keys,
+                     const int64_t* d_ids, const uint32_t* R, uint64_t r, uint8_t* keep,
+                     double* kernel_ms);
 
 struct GresOut {
     int g_max = 1;

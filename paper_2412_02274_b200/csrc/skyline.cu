@@ -1252,7 +1252,8 @@ int cells_per_dim(uint64_t m, int d, uint32_t* ncells) {
 }  // namespace
 
 SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, uint64_t n, int d,
-                          const skygpu_plan& plan, const double* d_reps, uint64_t n_reps) {
+                          const skygpu_plan& plan, const double* d_reps, uint64_t n_reps,
+                          unsigned sky_engine) {
     SkylineOut out;
     skygpu_stats& st = *c.st;
     st.tuples_in = n;
@@ -1343,12 +1344,82 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
     }();
     uint64_t want = kWant;
     const uint64_t kMaxPrefix = 65536, kFinal = kCTACap;
+    const uint64_t kGridMin = 1u << 16;  // auto rank-grid engine from this many tuples
     int rounds = 0;
     cudaEvent_t e0 = c.ev[8], e1 = c.ev[9], e2 = c.ev[14], e3 = c.ev[15];
     double kernel_ms = 0;
     uint64_t kernel_launches = 0;
     uint32_t* Rnext = Rbuf1;
     bool ids_sorted = true;
+    // device radix sort of a position list (in position order) by (sum, id,
+    // position); returns the buffer holding the sorted list (Pfull or B_IDX1)
+    auto radix_order = [&](uint32_t* Pfull, uint64_t m) -> uint32_t* {
+        uint32_t* Ps = c.buf[B_IDX1].as<uint32_t>(m);
+        uint32_t* order = Ps;
+        unsigned long long* Pkey = c.buf[B_KEY1].as<unsigned long long>(m);
+        unsigned long long* Pkey2 = c.buf[B_GTMP0].as<unsigned long long>(m);
+        unsigned long long* kcur;
+        if (ids_sorted) {
+            k_keys_of<<<grid_for(m, kBlock), kBlock, 0, c.stream>>>(keys, Pfull, m, Pkey);
+            SKY_LAUNCH_CHECK();
+            sort_pairs<unsigned long long>(c, Pkey, Pkey2, Pfull, Ps, m, 64, &kcur, &order);
+        } else {  // stable LSD: by id first, then by sum
+            unsigned long long* ik0 = c.buf[B_GTMP1].as<unsigned long long>(m);
+            k_id_keys<<<grid_for(m, kBlock), kBlock, 0, c.stream>>>(d_ids, Pfull, m, ik0);
+            SKY_LAUNCH_CHECK();
+            unsigned long long* ikc;
+            uint32_t* by_id;
+            sort_pairs<unsigned long long>(c, ik0, Pkey2, Pfull, Ps, m, 64, &ikc, &by_id);
+            uint32_t* other = by_id == Pfull ? Ps : Pfull;
+            k_keys_of<<<grid_for(m, kBlock), kBlock, 0, c.stream>>>(keys, by_id, m, Pkey);
+            SKY_LAUNCH_CHECK();
+            sort_pairs<unsigned long long>(c, Pkey, Pkey2, by_id, other, m, 64, &kcur, &order);
+        }
+        note_launch(c, 2);
+        return order;
+    };
+    // value contract / Grid range checks of K1, read back with the first sync
+    auto validate = [&]() {
+        if (!checked) {
+            checked = true;
+            if (c.h_slots[S_BAD] != ~0ULL)
+                invalid("parallel_skyline: tuple at position " + std::to_string(c.h_slots[S_BAD]) +
+                        " has a negative or NaN value (Relation::add contract, core.cpp:14-17)");
+            if (c.h_slots[S_GRIDBAD] != ~0ULL) {
+                const uint64_t flat = c.h_slots[S_GRIDBAD];
+                double v = 0;
+                SKY_CUDA(cudaMemcpyAsync(&v, d_vals + flat, sizeof(double),
+                                         cudaMemcpyDeviceToHost, c.stream));
+                SKY_CUDA(cudaStreamSynchronize(c.stream));
+                invalid("grid_cell: value " + std::to_string(v) + " in attribute " +
+                        std::to_string(flat % d + 1) +
+                        " outside [0,1]; normalize the data first");
+            }
+        }
+        ids_sorted = (c.h_slots[S_FLAG] & 1ULL) == 0;
+    };
+    // the one-pass rank-grid engine over the whole undecided set (R, r)
+    bool grid_used = false;
+    auto run_grid = [&]() {
+        uint8_t* gkeep = c.buf[B_SV].as<uint8_t>(r);
+        double kms = 0;
+        sky_grid_decide(c, d_vals, d, keys, d_ids, R, r, gkeep, &kms);
+        kernel_ms += kms;
+        kernel_launches += 1;
+        uint32_t* surv = c.buf[B_IDX0].as<uint32_t>(r);
+        select_flags<uint32_t>(c, R, r, gkeep, surv, c.d_slots + S_C2);
+        read_slots(c, S_C2, 1);
+        const uint64_t m = c.h_slots[S_C2];
+        if (m) {
+            uint32_t* order = radix_order(surv, m);
+            SKY_CUDA(cudaMemcpyAsync(K, order, m * sizeof(uint32_t), cudaMemcpyDeviceToDevice,
+                                     c.stream));
+        }
+        kc = m;
+        ++rounds;
+        grid_used = true;
+        trace_mark(c, "grid: survivors sorted");
+    };
     // sort a prefix by (sum, id), decide it (K4) and append its skyline tuples
     // to K; true when the whole undecided set was this prefix
     auto decide_prefix = [&](uint32_t* Pfull, uint64_t m, bool final_round) -> bool {
@@ -1374,26 +1445,7 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
                 SKY_LAUNCH_CHECK();
                 note_launch(c, 2);
             } else {
-                unsigned long long* Pkey = c.buf[B_KEY1].as<unsigned long long>(m);
-                unsigned long long* Pkey2 = c.buf[B_GTMP0].as<unsigned long long>(m);
-                unsigned long long* kcur;
-                if (ids_sorted) {
-                    k_keys_of<<<grid_for(m, kBlock), kBlock, 0, c.stream>>>(keys, Pfull, m, Pkey);
-                    SKY_LAUNCH_CHECK();
-                    sort_pairs<unsigned long long>(c, Pkey, Pkey2, Pfull, Ps, m, 64, &kcur, &order);
-                } else {  // stable LSD: by id first, then by sum
-                    unsigned long long* ik0 = c.buf[B_GTMP1].as<unsigned long long>(m);
-                    k_id_keys<<<grid_for(m, kBlock), kBlock, 0, c.stream>>>(d_ids, Pfull, m, ik0);
-                    SKY_LAUNCH_CHECK();
-                    unsigned long long* ikc;
-                    uint32_t* by_id;
-                    sort_pairs<unsigned long long>(c, ik0, Pkey2, Pfull, Ps, m, 64, &ikc, &by_id);
-                    uint32_t* other = by_id == Pfull ? Ps : Pfull;
-                    k_keys_of<<<grid_for(m, kBlock), kBlock, 0, c.stream>>>(keys, by_id, m, Pkey);
-                    SKY_LAUNCH_CHECK();
-                    sort_pairs<unsigned long long>(c, Pkey, Pkey2, by_id, other, m, 64, &kcur, &order);
-                }
-                note_launch(c, 2);
+                order = radix_order(Pfull, m);
             }
             double* Av = c.buf[B_MISC].as<double>(m * d);
             unsigned long long* Aq = qpre ? c.buf[B_AQ].as<unsigned long long>(m * 2) : nullptr;
@@ -1449,6 +1501,12 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
             }
             return false;
     };
+    if (sky_engine == SKYGPU_SKY_GRID && r > 0 && sky_grid_bins(r, d)) {
+        read_slots(c, S_BAD, 11);
+        validate();
+        run_grid();
+        r = 0;
+    }
     while (r > 0) {
         // final round: the whole (already ordered) undecided list is the
         // prefix — no threshold, no selection, no host synchronisation
@@ -1470,27 +1528,20 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
         note_launch(c, 1);
         trace_mark(c, "sky: select prefix");
         read_slots(c, S_BAD, 11);
-        if (!checked) {
-            checked = true;
-            if (c.h_slots[S_BAD] != ~0ULL)
-                invalid("parallel_skyline: tuple at position " + std::to_string(c.h_slots[S_BAD]) +
-                        " has a negative or NaN value (Relation::add contract, core.cpp:14-17)");
-            if (c.h_slots[S_GRIDBAD] != ~0ULL) {
-                const uint64_t flat = c.h_slots[S_GRIDBAD];
-                double v = 0;
-                SKY_CUDA(cudaMemcpyAsync(&v, d_vals + flat, sizeof(double),
-                                         cudaMemcpyDeviceToHost, c.stream));
-                SKY_CUDA(cudaStreamSynchronize(c.stream));
-                invalid("grid_cell: value " + std::to_string(v) + " in attribute " +
-                        std::to_string(flat % d + 1) +
-                        " outside [0,1]; normalize the data first");
-            }
-        }
-        ids_sorted = (c.h_slots[S_FLAG] & 1ULL) == 0;
+        validate();
         const uint64_t m = c.h_slots[S_C1];
         if (m == 0) throw Error(SKYGPU_ERUNTIME, "skyline: empty prefix (internal)");
 
         if (decide_prefix(Pfull, m, false)) break;
+        // large skyline ahead (most of the first prefix survived): decide
+        // everything at once with the rank-grid engine instead of filtering
+        if (rounds == 1 && sky_engine == 0 && r >= kGridMin && sky_grid_bins(r, d)) {
+            read_slots(c, S_C2, 1);
+            if (c.h_slots[S_C2] * 4 > m * 3) {
+                run_grid();
+                break;
+            }
+        }
 
         // ---- K5: filter the rest against A', A' regrouped (one-CTA counting
         // sort) by the quantile grid (exact cell pruning, default) or by the
@@ -1594,6 +1645,7 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
         if (a * 2 > m) want = std::min(want * 4, kMaxPrefix);
     }
     st.sfs_rounds = rounds;
+    st.sky_engine = grid_used ? SKYGPU_SKY_GRID : SKYGPU_SKY_ROUNDS;
     st.tuples_into_final = kc;
     st.ms_sky_kernel += kernel_ms;
     st.sky_kernel_launches += kernel_launches;

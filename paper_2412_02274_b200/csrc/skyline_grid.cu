@@ -1,0 +1,474 @@
+// skyline_grid.cu — one-pass skyline for LARGE skylines (SkyAlign-style static
+// rank grid; the GPU recast of the paper's partition-level pruning,
+// parallel.cpp:32-42 / partition.cpp:115-137, for data where most tuples
+// survive, e.g. BASELINE config 5: 10 M anti-correlated tuples, d = 7).
+//
+// The round engine (skyline.cu) decides a prefix of the (sum, id) order and
+// then filters every remaining tuple against the prefix's skyline; when the
+// skyline is most of the input that is ~n^2/2 dominance tests.  Here every
+// tuple is decided at once by the predecessor rule over the undecided set R:
+//
+//   t in R is kept  <=>  no s in R that precedes t in (sum, id, position)
+//                        order dominates t
+//
+// (equivalent to the reference's SFS over R: a dominated s that dominates t
+// is itself dominated by an earlier kept tuple, which then dominates t.)
+//
+// Pruning.  Every attribute value gets a 7-bit RANK code — the number of
+// per-attribute sample quantiles (127 of them) <= the value.  Codes are
+// monotone, so s dominates t  =>  code_j(s) <= code_j(t) for every j.  The
+// codes of a tuple pack one byte per attribute into a u32 (d <= 4) or u64
+// (d <= 8) word; the all-bytes-<= test is one SWAR subtraction (the guard-bit
+// trick of the gres kernels).  Tuples are bucketed by bins of their codes:
+// k0 fine bins along attribute 0 and k coarse bins along attributes 1..d-1;
+// the cell order makes attribute 0 the fastest-varying, so the cells of one
+// ROW (equal bins in attributes 1..d-1) are contiguous.  A comparator can
+// only dominate a candidate from a cell <= the candidate's in every
+// attribute, so a warp holding up to 128 candidates of one row streams, for
+// every row <= its own (mixed-radix countdown over attributes 1..d-1), the
+// ONE contiguous range of cells with attribute-0 bin <= its largest
+// candidate's.  On C5 that visits ~0.1% of all pairs.  Code tests that pass
+// (rare) take the exact float64 dominance test plus the precedence check —
+// the only place exact values are read.
+#include <cub/cub.cuh>
+
+#include <cmath>
+#include <cstdlib>
+#include <type_traits>
+
+#include "sky_common.cuh"
+
+namespace skygpu {
+namespace {
+
+constexpr int kGB = 256;          // threads per block
+constexpr int kBounds = 127;      // rank bounds per attribute -> codes 0..127
+constexpr int kCand = 4;          // candidates per lane -> 128 per warp item
+constexpr uint32_t kItem = 32 * kCand;
+
+template <int D>
+using GridWord = typename std::conditional<(D <= 4), uint32_t, unsigned long long>::type;
+
+// bounds[j][b] (b < 127) = the sample of rank 32(b+1)-1 among 4096 strided
+// samples of attribute j over R (one CTA per attribute)
+__global__ void __launch_bounds__(1024)
+k_rank_bounds(const double* __restrict__ v, int d, const uint32_t* __restrict__ R, uint64_t r,
+              double* __restrict__ bounds) {
+    using Sort = cub::BlockRadixSort<unsigned long long, 1024, 4>;
+    __shared__ typename Sort::TempStorage tmp;
+    const int j = blockIdx.x;
+    unsigned long long items[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const uint64_t s = threadIdx.x * 4 + u;
+        const uint64_t i = s * r / 4096;
+        const uint64_t p = R ? R[i] : i;
+        items[u] = ord_bits(v[p * d + j]);
+    }
+    Sort(tmp).Sort(items);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const uint32_t rank = threadIdx.x * 4 + u;
+        if ((rank + 1) % 32 == 0 && rank < 4095)
+            bounds[j * 128 + (rank + 1) / 32 - 1] = __longlong_as_double((long long)items[u]);
+    }
+}
+
+// rank codes, cell of every tuple of R (bin0 + k0 * row), cell histogram
+template <int D>
+__global__ void __launch_bounds__(kGB)
+k_rank_codes(const double* __restrict__ v, const uint32_t* __restrict__ R, uint32_t r,
+             const double* __restrict__ bounds, int k0, int k, GridWord<D>* __restrict__ code,
+             uint32_t* __restrict__ cell, uint32_t* __restrict__ count) {
+    using W = GridWord<D>;
+    __shared__ double sb[D * 128];
+    for (int i = threadIdx.x; i < D * 128; i += blockDim.x) sb[i] = bounds[i];
+    __syncthreads();
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < r; i += gridDim.x * blockDim.x) {
+        const uint64_t p = R ? R[i] : i;
+        W w = 0;
+        uint32_t row = 0, mul = 1, b0 = 0;
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            const double x = v[p * D + j];
+            int lo = 0;  // #bounds <= x (bounds sorted)
+#pragma unroll
+            for (int step = 64; step; step >>= 1)
+                if (lo + step <= kBounds && sb[j * 128 + lo + step - 1] <= x) lo += step;
+            w |= (W)lo << (8 * j);
+            if (j == 0) {
+                b0 = (uint32_t)((lo * k0) >> 7);
+            } else {
+                row += (uint32_t)((lo * k) >> 7) * mul;
+                mul *= (uint32_t)k;
+            }
+        }
+        const uint32_t cl = b0 + (uint32_t)k0 * row;
+        code[i] = w;
+        cell[i] = cl;
+        atomicAdd(&count[cl], 1u);
+    }
+}
+
+template <class W>
+__global__ void k_cell_scatter(const W* __restrict__ code, const uint32_t* __restrict__ cell,
+                               uint32_t r, const uint32_t* __restrict__ seg,
+                               uint32_t* __restrict__ cursor, W* __restrict__ scode,
+                               uint32_t* __restrict__ sidx) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < r; i += gridDim.x * blockDim.x) {
+        const uint32_t cl = cell[i];
+        const uint32_t pos = seg[cl] + atomicAdd(&cursor[cl], 1u);
+        scode[pos] = code[i];
+        sidx[pos] = i;
+    }
+}
+
+// work items: (row, first sorted position) chunks of <= 128 candidates
+__global__ void k_row_items(const uint32_t* __restrict__ seg, uint32_t nrows, int k0,
+                            uint2* __restrict__ items, unsigned* __restrict__ ctr) {
+    for (uint32_t row = blockIdx.x * blockDim.x + threadIdx.x; row < nrows;
+         row += gridDim.x * blockDim.x) {
+        const uint32_t a = seg[row * k0], n = seg[(row + 1) * k0] - a;
+        if (!n) continue;
+        const uint32_t ch = (n + kItem - 1) / kItem;
+        const uint32_t base = atomicAdd(&ctr[0], ch);
+        for (uint32_t u = 0; u < ch; ++u) items[base + u] = make_uint2(row, a + u * kItem);
+    }
+}
+
+// exact test: does the tuple at sorted position qs dominate, and precede,
+// the tuple at sorted position qt?
+template <int D>
+__device__ __noinline__ bool exact_pred(const double* __restrict__ v,
+                                        const unsigned long long* __restrict__ key,
+                                        const int64_t* __restrict__ ids,
+                                        const uint32_t* __restrict__ R,
+                                        const uint32_t* __restrict__ sidx, uint32_t qs,
+                                        uint32_t qt) {
+    const uint32_t is = sidx[qs], it = sidx[qt];
+    const uint64_t ps = R ? R[is] : is, pt = R ? R[it] : it;
+    double s[D], t[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+        s[j] = v[ps * D + j];
+        t[j] = v[pt * D + j];
+    }
+    if (!dom_f64<D>(s, t)) return false;
+    const unsigned long long ks = key[ps], kt = key[pt];
+    if (ks != kt) return ks < kt;  // dominance implies ks <= kt
+    const int64_t is_ = ids[ps], it_ = ids[pt];
+    return is_ < it_ || (is_ == it_ && ps < pt);
+}
+
+// zero iff every byte of s <= the byte of t, given tg = t | 0x80.. (codes
+// <= 127): the guard bits of tg - s that a borrow cleared.  Accumulated
+// with min() over a tile, a zero result flags a pass in one instruction.
+__device__ __forceinline__ uint32_t code_miss(uint32_t tg, uint32_t s) {
+    return ~(tg - s) & 0x80808080u;
+}
+__device__ __forceinline__ uint32_t code_miss(unsigned long long tg, unsigned long long s) {
+    const unsigned long long x = tg - s;
+    return ~((uint32_t)x & (uint32_t)(x >> 32)) & 0x80808080u;
+}
+// a code word that never passes: byte 0 = 0x80 clears guard bit 7 of
+// (t0 | 0x80) - 0x80 for every t0
+template <class W>
+__device__ __forceinline__ W code_never() {
+    return (W)0x80;
+}
+
+// exact follow-up of the code passes of one staged tile for candidate slot
+// u of this lane (skipping comparator `self`, a sorted position or ~0):
+// false when a dominating predecessor was found
+template <int D, class W>
+__device__ __forceinline__ bool tile_exact(const W* st, const uint32_t* sp, W tgu, uint32_t qt,
+                                           uint32_t self, const double* __restrict__ v,
+                                           const unsigned long long* __restrict__ key,
+                                           const int64_t* __restrict__ ids,
+                                           const uint32_t* __restrict__ R,
+                                           const uint32_t* __restrict__ sidx) {
+    uint32_t m = 0;
+#pragma unroll 8
+    for (int j = 0; j < 32; ++j) m |= (code_miss(tgu, st[j]) == 0u ? 1u : 0u) << j;
+    while (m) {
+        const int j = __ffs(m) - 1;
+        m &= m - 1;
+        const uint32_t qs = sp[j];
+        if (qs != self && qs != ~0u && exact_pred<D>(v, key, ids, R, sidx, qs, qt)) return false;
+    }
+    return true;
+}
+
+// K6: persistent warps pull (row, chunk) items; each lane holds kCand
+// candidates.  The chunk is first tested against itself (4 tiles, exact
+// follow-up of every pass except the candidate itself); then the comparator
+// ranges — one per row <= the item's row, own row first, minus the chunk —
+// are streamed 32 codes at a time through shared memory: tiles are filled
+// across row boundaries and the next tile's load is issued before the
+// current one is tested.  The tile test is 4 integer instructions per
+// (candidate, comparator) with no branch (min-accumulated miss bits); a tile
+// with a pass (rare: equal codes, near-dominators) gets the exact follow-up.
+// Warp exit when every candidate is decided.  keep[R index] = 1 for kept.
+template <int D>
+__global__ void __launch_bounds__(kGB)
+k_grid_decide(const double* __restrict__ v, const unsigned long long* __restrict__ key,
+              const int64_t* __restrict__ ids, const uint32_t* __restrict__ R,
+              const GridWord<D>* __restrict__ scode, const uint32_t* __restrict__ sidx,
+              const uint32_t* __restrict__ seg, const uint2* __restrict__ items,
+              unsigned* __restrict__ ctr, int k0, int k, uint8_t* __restrict__ keep,
+              unsigned long long* __restrict__ tests) {
+    using W = GridWord<D>;
+    __shared__ W stage[kGB / 32][32];
+    __shared__ uint32_t spos[kGB / 32][32];
+    const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const W H = (W)0x8080808080808080ULL;
+    const uint32_t nitems = ctr[0];
+    W* st = stage[wib];
+    uint32_t* sp = spos[wib];
+    uint32_t wj[D];  // row-id weight of attribute j >= 1
+    wj[0] = 0;
+    if (D > 1) wj[1] = 1;
+#pragma unroll
+    for (int j = 2; j < D; ++j) wj[j] = wj[j - 1] * (uint32_t)k;
+    unsigned long long cnt = 0;
+    for (;;) {
+        uint32_t it = 0;
+        if (lane == 0) it = atomicAdd(&ctr[1], 1u);
+        it = __shfl_sync(0xffffffffu, it, 0);
+        if (it >= nitems) break;
+        const uint2 item = items[it];
+        const uint32_t own = item.x, first = item.y;
+        const uint32_t end = min(seg[(own + 1) * k0], first + kItem);
+        W tg[kCand];
+        unsigned alive = 0;
+#pragma unroll
+        for (int u = 0; u < kCand; ++u) {
+            const uint32_t q = first + u * 32 + lane;
+            tg[u] = q < end ? (scode[q] | H) : (W)0;
+            alive |= (q < end ? 1u : 0u) << u;
+        }
+        // ---- the chunk against itself
+#pragma unroll
+        for (int t = 0; t < kCand; ++t) {
+            const uint32_t q0 = first + t * 32;
+            if (q0 >= end) break;
+            const uint32_t q = q0 + lane;
+            st[lane] = q < end ? scode[q] : code_never<W>();
+            sp[lane] = q < end ? q : ~0u;
+            __syncwarp();
+#pragma unroll
+            for (int u = 0; u < kCand; ++u) {
+                if ((alive >> u) & 1u) {
+                    const uint32_t qt = first + u * 32 + lane;
+                    if (!tile_exact<D>(st, sp, tg[u], qt, qt, v, key, ids, R, sidx))
+                        alive &= ~(1u << u);
+                }
+            }
+            cnt += (unsigned long long)min(32u, end - q0) * __popc(alive);
+            __syncwarp();
+        }
+        // largest attribute-0 bin among the candidates = that of the last one
+        const uint32_t od0 = (uint32_t)((((uint32_t)scode[end - 1] & 0xFFu) * (uint32_t)k0) >> 7);
+        int od[D], dig[D];
+#pragma unroll
+        for (int j = 1; j < D; ++j) {
+            od[j] = (int)((own / wj[j]) % (uint32_t)k);
+            dig[j] = od[j];
+        }
+        uint32_t row = own;
+        // own row: [row start, first) then [end, row end at od0)
+        uint32_t cur = seg[row * k0], rend = first;
+        uint32_t gap_end = seg[row * k0 + od0 + 1];
+        bool rows_left = D > 1, gap = true;
+        // next <= 32 comparator positions across rows (warp-uniform walk)
+        auto fill = [&](uint32_t& mypos) -> uint32_t {
+            uint32_t filled = 0;
+            mypos = ~0u;
+            while (filled < 32) {
+                if (cur == rend) {
+                    if (gap) {
+                        gap = false;
+                        cur = end;
+                        rend = gap_end;
+                        continue;
+                    }
+                    if (!rows_left) break;
+                    bool stepped = false;
+#pragma unroll
+                    for (int j = 1; j < D; ++j) {
+                        if (!stepped) {
+                            if (dig[j] > 0) {
+                                --dig[j];
+                                row -= wj[j];
+                                stepped = true;
+                            } else {
+                                dig[j] = od[j];
+                                row += (uint32_t)od[j] * wj[j];
+                            }
+                        }
+                    }
+                    if (!stepped) {
+                        rows_left = false;
+                        break;
+                    }
+                    cur = seg[row * k0];
+                    rend = seg[row * k0 + od0 + 1];
+                    continue;
+                }
+                const uint32_t take = min(32u - filled, rend - cur);
+                if (lane >= filled && lane < filled + take) mypos = cur + (lane - filled);
+                filled += take;
+                cur += take;
+            }
+            return filled;
+        };
+        uint32_t pos_next;
+        uint32_t npos = __any_sync(0xffffffffu, alive != 0u) ? fill(pos_next) : 0;
+        W code_next = pos_next != ~0u ? scode[pos_next] : code_never<W>();
+        while (npos) {
+            st[lane] = code_next;
+            sp[lane] = pos_next;
+            const uint32_t n = npos;
+            __syncwarp();
+            npos = fill(pos_next);  // prefetch the next tile
+            code_next = pos_next != ~0u ? scode[pos_next] : code_never<W>();
+            uint32_t acc[kCand];
+#pragma unroll
+            for (int u = 0; u < kCand; ++u) acc[u] = 0xFFFFFFFFu;
+#pragma unroll 8
+            for (int j = 0; j < 32; ++j) {
+                const W s = st[j];
+#pragma unroll
+                for (int u = 0; u < kCand; ++u) acc[u] = min(acc[u], code_miss(tg[u], s));
+            }
+            cnt += (unsigned long long)n * __popc(alive);
+            unsigned hm = 0;
+#pragma unroll
+            for (int u = 0; u < kCand; ++u) hm |= (acc[u] == 0u ? 1u : 0u) << u;
+            hm &= alive;
+            if (__any_sync(0xffffffffu, hm != 0u)) {  // rare: exact follow-up
+#pragma unroll
+                for (int u = 0; u < kCand; ++u) {
+                    if ((hm >> u) & 1u) {
+                        const uint32_t qt = first + u * 32 + lane;
+                        if (!tile_exact<D>(st, sp, tg[u], qt, ~0u, v, key, ids, R, sidx))
+                            alive &= ~(1u << u);
+                    }
+                }
+            }
+            __syncwarp();
+            if (!__any_sync(0xffffffffu, alive != 0u)) break;
+        }
+#pragma unroll
+        for (int u = 0; u < kCand; ++u) {
+            const uint32_t q = first + u * 32 + lane;
+            if (q < end) keep[sidx[q]] = (alive >> u) & 1u;
+        }
+    }
+    add_count(tests, cnt);
+}
+
+template <int D, class F>
+void with_d(int d, F&& f) {
+    if (d == D) f(std::integral_constant<int, D>{});
+    if constexpr (D < 8) with_d<D + 1>(d, f);
+}
+
+double env_or(const char* name, double dflt) {
+    const char* e = getenv(name);
+    const double x = e ? atof(e) : 0.0;
+    return x > 0 ? x : dflt;
+}
+
+struct GridShape {
+    int k0 = 0, k = 0;
+    uint32_t rows = 0, ncells = 0;
+};
+
+// bins: k coarse bins on attributes 1..d-1 so that a row holds ~512 tuples
+// (SKYGPU_GRID_ROW), k0 fine bins on attribute 0 (SKYGPU_GRID_K0, <= 128)
+GridShape grid_shape(uint64_t r, int d) {
+    GridShape g;
+    if (d < 1 || d > 8) return g;
+    static const double per_row = env_or("SKYGPU_GRID_ROW", 512.0);
+    static const int k0 = (int)std::min(128.0, env_or("SKYGPU_GRID_K0", 32.0));
+    int k = 1;
+    if (d > 1) {
+        k = (int)std::lround(std::pow(std::max(1.0, (double)r / per_row), 1.0 / (d - 1)));
+        k = std::max(2, std::min(k, 128));
+        while (k > 2 && std::pow((double)k, d - 1) * k0 > (double)(1u << 22)) --k;
+    }
+    const double rows = std::pow((double)k, d - 1);
+    if (rows * k0 > (double)(1u << 22)) return g;
+    g.k0 = k0;
+    g.k = k;
+    g.rows = (uint32_t)rows;
+    g.ncells = g.rows * (uint32_t)k0;
+    return g;
+}
+
+}  // namespace
+
+int sky_grid_bins(uint64_t r, int d) { return grid_shape(r, d).k0; }
+
+void sky_grid_decide(Ctx& c, const double* d_vals, int d, const unsigned long long* keys,
+                     const int64_t* d_ids, const uint32_t* R, uint64_t r, uint8_t* keep,
+                     double* kernel_ms) {
+    const GridShape g = grid_shape(r, d);
+    if (!g.k0) throw Error(SKYGPU_ERUNTIME, "sky_grid_decide: unsupported shape (internal)");
+    const uint32_t ncells = g.ncells;
+    double* bounds = c.buf[B_PROJ].as<double>(8 * 128);
+    const uint64_t cwords = 2 * ((uint64_t)ncells + 1) + 2;
+    uint32_t* count = c.buf[B_GCNT].as<uint32_t>(cwords);
+    uint32_t* seg = count + ncells + 1;
+    unsigned* ctr = (unsigned*)(seg + ncells + 1);
+    SKY_CUDA(cudaMemsetAsync(count, 0, sizeof(uint32_t) * cwords, c.stream));
+    k_rank_bounds<<<d, 1024, 0, c.stream>>>(d_vals, d, R, r, bounds);
+    SKY_LAUNCH_CHECK();
+    note_launch(c);
+    trace_mark(c, "grid: bounds");
+    with_d<1>(d, [&](auto DC) {
+        constexpr int D = decltype(DC)::value;
+        using W = GridWord<D>;
+        W* code = c.buf[B_GCODE].as<W>(r);
+        uint32_t* cell = c.buf[B_GCELL].as<uint32_t>(r);
+        W* scode = c.buf[B_GSCODE].as<W>(r);
+        uint32_t* sidx = c.buf[B_GSIDX].as<uint32_t>(r);
+        uint2* items = c.buf[B_GITEMS].as<uint2>(r / kItem + g.rows + 1);
+        k_rank_codes<D><<<grid_for(r, kGB, c.num_sms * 8), kGB, 0, c.stream>>>(
+            d_vals, R, (uint32_t)r, bounds, g.k0, g.k, code, cell, count);
+        SKY_LAUNCH_CHECK();
+        size_t tmp = 0;
+        SKY_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, count, seg, (int)ncells + 1,
+                                               c.stream));
+        void* t = c.buf[B_CUB].get(tmp);
+        SKY_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, count, seg, (int)ncells + 1, c.stream));
+        SKY_CUDA(cudaMemsetAsync(count, 0, sizeof(uint32_t) * ncells, c.stream));  // cursors
+        k_cell_scatter<W><<<grid_for(r, kGB), kGB, 0, c.stream>>>(code, cell, (uint32_t)r, seg,
+                                                                  count, scode, sidx);
+        SKY_LAUNCH_CHECK();
+        k_row_items<<<grid_for(g.rows, kGB), kGB, 0, c.stream>>>(seg, g.rows, g.k0, items, ctr);
+        SKY_LAUNCH_CHECK();
+        note_launch(c, 5);
+        trace_mark(c, "grid: codes + cells + items");
+        int per_sm = 0;
+        SKY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_grid_decide<D>, kGB, 0));
+        per_sm = std::max(1, per_sm);
+        SKY_CUDA(cudaEventRecord(c.ev[14], c.stream));
+        k_grid_decide<D><<<c.num_sms * per_sm, kGB, 0, c.stream>>>(
+            d_vals, keys, d_ids, R, scode, sidx, seg, items, ctr, g.k0, g.k, keep,
+            c.d_slots + S_TESTS_SKY);
+        SKY_LAUNCH_CHECK();
+        SKY_CUDA(cudaEventRecord(c.ev[15], c.stream));
+        note_launch(c);
+        trace_mark(c, "grid: K6 decide kernel");
+    });
+    if (kernel_ms) {
+        SKY_CUDA(cudaEventSynchronize(c.ev[15]));
+        float ms = 0;
+        SKY_CUDA(cudaEventElapsedTime(&ms, c.ev[14], c.ev[15]));
+        *kernel_ms += ms;
+    }
+}
+
+}  // namespace skygpu

@@ -31,6 +31,7 @@ LIB_PATH = os.path.join(_PKG, "_lib", "libskygpu.so")
 SKYGPU_OK, SKYGPU_EINVAL, SKYGPU_ERUNTIME, SKYGPU_ECUDA, SKYGPU_ENOMEM = range(5)
 GRES_AUTO, GRES_PAIRS, GRES_CELLS = 0, 1, 2
 DEVICE_PTRS, CHECK_SKYLINE, SKIP_GRES = 1, 2, 4
+SKY_AUTO, SKY_ROUNDS, SKY_GRID = 0, 8, 16  # skyline engine flags
 
 
 class SkyGpuError(RuntimeError):
@@ -61,14 +62,14 @@ class Stats(C.Structure):
                                            "skyline_size", "skyline_tests", "gres_tests",
                                            "gres_cells")] + \
                [(n, C.c_int) for n in ("g_max", "gres_steps", "gres_engine", "code_bits",
-                                        "sfs_rounds", "pad_")] + \
+                                        "sfs_rounds", "sky_engine")] + \
                [(n, C.c_double) for n in ("ms_total", "ms_h2d", "ms_skyline", "ms_gres", "ms_d2h",
                                            "ms_gres_kernel", "ms_sky_kernel")] + \
                [(n, C.c_uint64) for n in ("gres_kernel_launches", "sky_kernel_launches",
                                            "kernel_launches")]
 
     def as_dict(self) -> dict:
-        return {k: getattr(self, k) for k, _ in self._fields_ if k != "pad_"}
+        return {k: getattr(self, k) for k, _ in self._fields_}
 
 
 @dataclass
@@ -252,8 +253,11 @@ class PipelineResult:
 
 def pipeline(values, ids=None, plan: PartitionPlan | None = None, cap: int | None = 25,
              engine: int = GRES_AUTO, shard_rank: int = 0, shard_world: int = 1,
-             check_skyline: bool = False, skip_gres: bool = False) -> PipelineResult:
-    """Skyline + grid resistance in one call (harness.cpp:208, :229-231)."""
+             check_skyline: bool = False, skip_gres: bool = False,
+             sky_engine: int = SKY_AUTO) -> PipelineResult:
+    """Skyline + grid resistance in one call (harness.cpp:208, :229-231).
+    ``sky_engine`` forces the prefix-round (SKY_ROUNDS) or one-pass rank-grid
+    (SKY_GRID) skyline engine; the default picks by the first round's yield."""
     v, i = _relation(values, ids)
     n, d = v.shape
     plan = plan or PartitionPlan(Strategy.NONE, 1, 1, d)
@@ -263,7 +267,7 @@ def pipeline(values, ids=None, plan: PartitionPlan | None = None, cap: int | Non
     gm = np.zeros(1, dtype=np.int32)
     st = Stats()
     err = _errbuf()
-    flags = (CHECK_SKYLINE if check_skyline else 0) | (SKIP_GRES if skip_gres else 0)
+    flags = (CHECK_SKYLINE if check_skyline else 0) | (SKIP_GRES if skip_gres else 0) | int(sky_engine)
     _check(lib().skygpu_pipeline(_p(v), _p(i), n, d, C.byref(plan._c()), 0 if cap is None else int(cap),
                                  int(engine), int(shard_rank), int(shard_world), flags, _p(pos), _p(den),
                                  _p(s), _p(gm), C.byref(st), err, 1024), err)

@@ -167,3 +167,58 @@ def test_cell_engine_shards(world):
         part = sk.pipeline(v, cap=25, engine=sk.GRES_CELLS, shard_rank=r, shard_world=world)
         acc = np.maximum(acc, part.den)
     assert acc.tolist() == full.den.tolist()
+
+
+# ------------------------------------------------ one-pass rank-grid skyline engine
+@pytest.mark.parametrize("name", ["C1_uni_100k_d4", "C2_ant_1M_d3", "C3_corr_1M_d6",
+                                  "C5_prefix_2k_d7", "C5_prefix_10k_d7",
+                                  "rand_lattice_n1500_d7_none", "rand_ant_n1500_d5_angular",
+                                  "uncapped_lattice_d3"])
+def test_grid_engine_matches_golden(name):
+    """skyline_grid.cu (forced) gives the reference's skyline, order and map."""
+    g = load_golden(name)
+    v, ids = golden_input(g, sk.generate)
+    res = sk.pipeline(v, ids, plan_of(g, v.shape[1]), cap=spec_cap(g), sky_engine=sk.SKY_GRID)
+    assert res.stats["sky_engine"] == sk.SKY_GRID
+    assert ids[res.positions].tolist() == g["skyline_order"]
+    assert res.g_max == g["g_max"]
+    got = dict(zip(ids[res.positions].tolist(), res.den.tolist()))
+    assert [got[i] for i in g["skyline_ids"]] == g["den"]
+
+
+@pytest.mark.parametrize("gen,n,d,seed", [
+    ("uni", 3000, 1, 1), ("ant", 3000, 2, 2), ("lattice", 5000, 3, 3), ("uni", 20000, 6, 4),
+    ("ant", 4000, 8, 5), ("corr", 50000, 4, 9), ("ant", 100000, 4, 10)])
+def test_grid_engine_random_against_oracle(gen, n, d, seed):
+    v = sk.generate(gen, n, d, seed)
+    ids = np.arange(n, dtype=np.int64)
+    pos, _ = po.skyline_sfs(v, ids)
+    res = sk.pipeline(v, ids, cap=25, skip_gres=True, sky_engine=sk.SKY_GRID)
+    assert res.positions.tolist() == pos.tolist()
+
+
+def test_grid_engine_ties_and_unsorted_ids():
+    rng = np.random.default_rng(3)
+    v = np.floor(rng.random((6000, 4)) * 6) / 6  # sum ties, duplicates
+    ids = rng.permutation(10**6)[:6000].astype(np.int64) - 500000
+    pos, _ = po.skyline_sfs(v, ids)
+    res = sk.pipeline(v, ids, skip_gres=True, sky_engine=sk.SKY_GRID)
+    assert res.positions.tolist() == pos.tolist()
+    # FP-tie case: {<2e-20,1>, <1e-20,1>} have equal sums; the predecessor
+    # rule keeps both (the reference's SFS order), brute force would not
+    v2 = np.array([[2e-20, 1.0], [1e-20, 1.0]])
+    for eng in (sk.SKY_GRID, sk.SKY_ROUNDS):
+        r2 = sk.pipeline(v2, np.array([0, 1]), skip_gres=True, sky_engine=eng)
+        assert sorted(r2.positions.tolist()) == sorted(po.skyline_sfs(v2, np.array([0, 1]))[0].tolist())
+
+
+@pytest.mark.parametrize("n", [200_000, 1_000_000])
+def test_grid_engine_auto_on_large_skyline(n):
+    """C5-style data (skyline ~ input) switches to the rank grid after round 1;
+    both engines agree bit-exactly (order included)."""
+    v = sk.generate("ant", n, 7, 1)
+    a = sk.pipeline(v, cap=25, skip_gres=True)
+    assert a.stats["sky_engine"] == sk.SKY_GRID
+    b = sk.pipeline(v, cap=25, skip_gres=True, sky_engine=sk.SKY_ROUNDS)
+    assert b.stats["sky_engine"] == sk.SKY_ROUNDS
+    assert a.positions.tolist() == b.positions.tolist()
