@@ -44,7 +44,11 @@ WORKLOADS = {
     "C4": ("uni", 10_000_000, 5, 1, "angular", 64, 25),
     "C5p10k": ("ant", 10_000, 7, 1, "angular", 64, 25),
     "C5p20k": ("ant", 20_000, 7, 1, "angular", 64, 25),
+    "C5": ("ant", 10_000_000, 7, 1, "angular", 64, 25),
 }
+# the CPU reference cannot finish these in a bench run (C5: days); it is timed
+# on the leading prefix of the same seeded stream instead, and says so
+CPU_SAMPLE_N = {"C5": 10_000}
 METRIC = "grid-resistance skyline tuples/sec"
 UNIT = "skyline tuples/s"
 
@@ -72,6 +76,7 @@ def run_reference_cpu(wl, repeat, cores=0):
     the CPU baseline.  Falls back to the C oracle port when it was not built."""
     from oracle import pyoracle as po
     gen, n, d, seed, strat, p, cap = WORKLOADS[wl]
+    n = CPU_SAMPLE_N.get(wl, n)
     exe = po.refdrive_path(release=True)
     ncores = os.cpu_count() or 1
     if exe:
@@ -81,14 +86,22 @@ def run_reference_cpu(wl, repeat, cores=0):
         r = json.loads(subprocess.check_output(cmd, text=True))
         step_ms = r["skyline_ms_mean"] + r["gres_ms_mean"]
         return {"kind": "reference", "cores": r["cores"], "step_ms": step_ms, "S": r["skyline_size"],
-                "detail": r}
+                "detail": r, "n": n}
     v = po.generate(gen, n, d, seed)
     t0 = time.perf_counter()
     for _ in range(repeat):
         pos, _ = po.skyline_sfs(v)
         po.grid_resistance(v[pos], pos, cap)
     step_ms = (time.perf_counter() - t0) * 1e3 / repeat
-    return {"kind": "port", "cores": 1, "step_ms": step_ms, "S": len(pos), "detail": {}}
+    return {"kind": "port", "cores": 1, "step_ms": step_ms, "S": len(pos), "detail": {}, "n": n}
+
+
+def sample_text(wl, r, repeat):
+    n_full = WORKLOADS[wl][1]
+    if r.get("n", n_full) != n_full:
+        return (f"leading {r['n']} tuples of the {wl} stream x{repeat} (the full n={n_full} "
+                f"is not computable by the CPU reference within a bench run)")
+    return f"full {wl} workload x{repeat}"
 
 
 def reference_arm(args):
@@ -110,7 +123,7 @@ def reference_arm(args):
         "config": {"workload": f"{wl}: {gen} n={n} d={d} seed={seed}, {strat} p={p}, cap={cap}",
                    "cores": r["cores"], "cpu": cpu_model()},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": r["cores"], "kind": r["kind"],
-                         "sample": f"full {wl} workload x{args.steps}"},
+                         "sample": sample_text(wl, r, args.steps)},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "reference_detail": r["detail"],
     }
@@ -315,8 +328,8 @@ def our_arm(args):
             r = run_reference_cpu(args.workload, args.cpu_repeat)
             line["cpu_baseline"] = {"value": r["S"] / (r["step_ms"] / 1e3), "unit": UNIT,
                                     "cores": r["cores"], "kind": r["kind"],
-                                    "sample": f"full {args.workload} workload x{args.cpu_repeat} "
-                                              f"({r['step_ms']:.1f} ms/step, {cpu_model()})"}
+                                    "sample": sample_text(args.workload, r, args.cpu_repeat)
+                                              + f" ({r['step_ms']:.1f} ms/step, {cpu_model()})"}
         except Exception as e:  # pragma: no cover
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "port",
                                     "sample": f"unavailable: {e}"}
@@ -329,6 +342,16 @@ def our_arm(args):
 
 
 TRAFFIC_FILE = os.path.join(ROOT, "profiles", "traffic.json")
+
+
+def _hbm_peak():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except (OSError, ValueError, KeyError):
+        return 6650.0  # B200_PROFILING.md fallback ("of fallback")
+
+
+HBM_PEAK_GBS = _hbm_peak()
 
 
 def kernel_traffic(workload, kernel):
@@ -351,6 +374,30 @@ def roofline(st, sky_ms, gres_ms, d, clk, workload="C2"):
     f = (clk.get("sm_mhz") or 1965.0) * 1e6
 
     def one(kind):
+        if kind == "gres" and st["gres_engine"] == 2:  # cell-occupancy engine: HBM sweeps
+            ms = gres_ms
+            byts = st["gres_cells"]
+            achieved = byts / (ms / 1e3) if ms > 0 else 0.0
+            peak = HBM_PEAK_GBS * 1e9
+            kern = "k_cells_or_dim"
+            tr = kernel_traffic(workload, kern)
+            return {"bound": "hbm", "kernel": "cells engine (k_cells_*)", "achieved": achieved / 1e9,
+                    "peak": peak / 1e9, "unit": "GB/s", "frac": achieved / peak,
+                    "traffic": tr, "traffic_unit": "B/launch of k_cells_or_dim (ncu dram read+write)",
+                    "algorithmic_bytes_per_step": byts, "kernel_ms_per_step": ms,
+                    "launches_per_step": st["gres_kernel_launches"],
+                    "bytes_model": "per step: grid zeroed + read + written once, S*d*8 B read twice"}
+        if kind == "skyline" and st["sky_engine"] == 16:  # rank-grid engine (skyline_grid.cu)
+            tests, ms, launches = st["skyline_tests"], sky_ms, st["sky_kernel_launches"]
+            i_test, l_pipe = 3, 64  # IADD3 + LOP3 + VIMNMX on the ALU pipe (+ IMAD.X, FMA pipe)
+            peak = 148 * f * l_pipe / i_test
+            achieved = tests / (ms / 1e3) if ms > 0 else 0.0
+            return {"bound": "compare", "kernel": "k_grid_decide", "achieved": achieved / 1e9,
+                    "peak": peak / 1e9, "unit": "Gtests/s", "frac": achieved / peak,
+                    "traffic": kernel_traffic(workload, "k_grid_decide"),
+                    "traffic_unit": "B/launch (ncu dram read+write)",
+                    "tests_per_step": tests, "kernel_ms_per_step": ms, "launches_per_step": launches,
+                    "I_test": i_test, "L_pipe": l_pipe, "pipe": "alu", "f_clk_mhz": f / 1e6}
         if kind == "gres":
             kern = "k_gres_pairs_tiled" if st["code_bits"] == 8 else "k_gres_pairs_f64"
             tests, ms, launches = st["gres_tests"], gres_ms, st["gres_kernel_launches"]

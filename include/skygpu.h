@@ -80,7 +80,7 @@ typedef struct skygpu_stats {
     uint64_t skyline_size;         /* S */
     uint64_t skyline_tests;        /* dominance tests executed by the skyline kernels */
     uint64_t gres_tests;           /* (candidate, comparator, g) code tests executed */
-    uint64_t gres_cells;           /* cells swept by the cell engine */
+    uint64_t gres_cells;           /* cell engine: algorithmic bytes (3 grid sweeps + 2 value reads per step) */
     int g_max;                     /* ResistanceMetrics::g_max (gres.hpp:46) */
     int gres_steps;                /* interval counts scanned (g_max-1 or fewer) */
     int gres_engine;               /* engine actually used */

@@ -218,7 +218,10 @@ bool gres_cells_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_ma
         }
         SKY_LAUNCH_CHECK();
         note_launch(c, 4 + d);
-        swept += geo.rows * (uint64_t)d;
+        // algorithmic bytes of the step: the grid zeroed, read and written
+        // once by an ideal fused prefix-OR, plus the mark and query reads of
+        // the S x d values
+        swept += 3 * geo.rows * wb + 2 * S * (uint64_t)d * sizeof(double);
         ++steps;
         // stop early once every candidate has its answer (one small read per step)
         read_slots(c, S_C3, 1);
