@@ -10,11 +10,17 @@
 //
 // Layout: one bit per cell along attribute 0 (extent e_0 <= 64 -> a u32/u64
 // word per "row"), rows indexed by attributes 1..d-1 (attribute 1 fastest).
-// Per step: memset, mark (atomicOr per skyline tuple), in-word prefix-OR
-// (attribute 0), one coalesced line sweep per attribute 1..d-1 (HBM-bound:
-// each sweep reads and writes every row once), then one query per undecided
-// candidate.  Exactness: the same codes floor(v*g) as the pair engine.
+// Per step: memset, mark (atomicOr per skyline tuple), the prefix-OR over
+// every attribute, then one query per undecided candidate.  The prefix-OR is
+// HBM-bound (every pass reads and writes every row once), so passes are
+// fused: attributes 0 (in-word), 1 and 2 in one shared-memory slab pass,
+// then the remaining attributes two at a time (k_cells_or_pair) — 3 passes
+// for d = 7 instead of 7.  Exactness: the same codes floor(v*g) as the pair
+// engine.
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "sky_common.cuh"
@@ -77,6 +83,96 @@ __global__ void k_cells_or_dim(W* __restrict__ rows, uint64_t nrows, uint64_t ex
         for (uint64_t k = 0; k < ext; ++k) {
             acc |= p[k * stride];
             p[k * stride] = acc;
+        }
+    }
+}
+
+// ---- fused sweeps (the default): 3 passes instead of d for d = 7
+template <class W>
+__device__ __forceinline__ W word_prefix(W x) {
+    x |= x << 1;
+    x |= x << 2;
+    x |= x << 4;
+    x |= x << 8;
+    x |= x << 16;
+    if (sizeof(W) == 8) x |= x << (sizeof(W) == 8 ? 32 : 0);
+    return x;
+}
+
+// attribute 0 (in-word) + attributes 1 and 2 (e2 = 1 when d == 2): the
+// slab of e1*e2 rows of fixed attributes 3.. is contiguous; a block stages
+// whole slabs in shared memory (coalesced), sweeps them there, writes back
+constexpr uint32_t kSlabWords = 4096;
+
+template <class W>
+__global__ void __launch_bounds__(kBlock)
+k_cells_or_slab(W* __restrict__ rows, uint64_t nrows, uint32_t e1, uint32_t e2) {
+    extern __shared__ unsigned char smraw[];
+    W* sm = reinterpret_cast<W*>(smraw);
+    const uint32_t slab = e1 * e2;
+    const uint32_t spb = max(1u, kSlabWords / slab);
+    const uint64_t nslabs = nrows / slab;
+    for (uint64_t s0 = (uint64_t)blockIdx.x * spb; s0 < nslabs; s0 += (uint64_t)gridDim.x * spb) {
+        const uint32_t ns = (uint32_t)min((uint64_t)spb, nslabs - s0);
+        const uint32_t words = ns * slab;
+        W* g = rows + s0 * slab;
+        for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) sm[i] = word_prefix(g[i]);
+        __syncthreads();
+        for (uint32_t l = threadIdx.x; l < ns * e2; l += blockDim.x) {  // attribute 1
+            W* p = sm + (uint64_t)l * e1;
+            W acc = 0;
+            for (uint32_t a = 0; a < e1; ++a) {
+                acc |= p[a];
+                p[a] = acc;
+            }
+        }
+        __syncthreads();
+        if (e2 > 1) {
+            for (uint32_t l = threadIdx.x; l < ns * e1; l += blockDim.x) {  // attribute 2
+                W* p = sm + (uint64_t)(l / e1) * slab + (l % e1);
+                W acc = 0;
+                for (uint32_t b = 0; b < e2; ++b) {
+                    acc |= p[b * e1];
+                    p[b * e1] = acc;
+                }
+            }
+            __syncthreads();
+        }
+        for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) g[i] = sm[i];
+        __syncthreads();
+    }
+}
+
+// two attributes a, b = a + 1 at once (stride sa, sb = sa * ea): one thread
+// per line of the (ea x eb) plane, consecutive threads on consecutive lo
+// (coalesced); P[x][y] = v[x][y] | P[x-1][y] | P[x][y-1], a row of ea words
+// loaded ahead (ILP) and the previous row's prefixes held in registers
+constexpr int kPairMax = 32;
+
+template <class W>
+__global__ void __launch_bounds__(kBlock)
+k_cells_or_pair(W* __restrict__ rows, uint64_t nrows, uint32_t ea, uint32_t eb, uint64_t sa) {
+    const uint64_t plane = (uint64_t)ea * eb;
+    const uint64_t lines = nrows / plane;
+    for (uint64_t l = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; l < lines;
+         l += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t lo = l % sa, hi = l / sa;
+        W* base = rows + hi * sa * plane + lo;
+        W prev[kPairMax];
+#pragma unroll
+        for (int x = 0; x < kPairMax; ++x) prev[x] = 0;
+        for (uint32_t y = 0; y < eb; ++y) {
+            W* p = base + (uint64_t)y * ea * sa;
+            W v[kPairMax];
+#pragma unroll
+            for (int x = 0; x < kPairMax; ++x) v[x] = (uint32_t)x < ea ? p[(uint64_t)x * sa] : (W)0;
+            W run = 0;
+#pragma unroll
+            for (int x = 0; x < kPairMax; ++x) {
+                run |= v[x] | prev[x];
+                prev[x] = run;
+                if ((uint32_t)x < ea) p[(uint64_t)x * sa] = run;
+            }
         }
     }
 }
@@ -157,6 +253,53 @@ static bool cells_geometry(const std::vector<double>& amax, int d, int g, uint64
     return true;
 }
 
+// the prefix-OR of one step's occupancy over every attribute: fused passes
+// (slab: attributes 0-2 in shared memory; pairs of the rest in registers),
+// or one pass per attribute (SKYGPU_CELLS_UNFUSED=1, or extents too large)
+template <class W>
+void sweeps(Ctx& c, W* R, const CellGeom& geo, bool fused) {
+    const int d = geo.d;
+    auto single = [&](int j) {
+        k_cells_or_dim<W><<<grid_for(geo.rows / geo.ext[j], kBlock), kBlock, 0, c.stream>>>(
+            R, geo.rows, geo.ext[j], geo.stride[j]);
+        note_launch(c);
+    };
+    const uint32_t e1 = d >= 2 ? (uint32_t)geo.ext[1] : 1, e2 = d >= 3 ? (uint32_t)geo.ext[2] : 1;
+    if (!fused || d < 2 || (uint64_t)e1 * e2 > kSlabWords) {
+        k_cells_or_word<W><<<grid_for(geo.rows, kBlock), kBlock, 0, c.stream>>>(R, geo.rows);
+        note_launch(c);
+        for (int j = 1; j < d; ++j) single(j);
+        return;
+    }
+    const uint32_t slab = e1 * e2, spb = std::max(1u, kSlabWords / slab);
+    const size_t smem = (size_t)spb * slab * sizeof(W);
+    static bool attr_set = false;
+    if (!attr_set) {
+        SKY_CUDA(cudaFuncSetAttribute(k_cells_or_slab<unsigned>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+        SKY_CUDA(cudaFuncSetAttribute(k_cells_or_slab<unsigned long long>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+        attr_set = true;
+    }
+    const uint64_t nslabs = geo.rows / slab;
+    k_cells_or_slab<W><<<grid_for((nslabs + spb - 1) / spb, 1, c.num_sms * 8), kBlock, smem,
+                         c.stream>>>(R, geo.rows, e1, e2);
+    note_launch(c);
+    int j = 3;
+    while (j < d) {
+        if (j + 1 < d && geo.ext[j] <= (uint64_t)kPairMax) {
+            const uint64_t lines = geo.rows / (geo.ext[j] * geo.ext[j + 1]);
+            k_cells_or_pair<W><<<grid_for(lines, kBlock), kBlock, 0, c.stream>>>(
+                R, geo.rows, (uint32_t)geo.ext[j], (uint32_t)geo.ext[j + 1], geo.stride[j]);
+            note_launch(c);
+            j += 2;
+        } else {
+            single(j);
+            j += 1;
+        }
+    }
+}
+
 // Cell engine over S skyline tuples (SoA d_skyv), candidates act[0..na),
 // denominators into d_den (pre-zeroed); returns false (nothing done) when the
 // engine does not apply.  Runs steps g_max .. 2, stopping once every
@@ -186,6 +329,8 @@ bool gres_cells_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_ma
     void* rows = c.buf[B_CELLS].get(geo0.rows * (w64 ? 8 : 4));
     uint64_t swept = 0;
     int steps = 0;
+    const char* uf = getenv("SKYGPU_CELLS_UNFUSED");
+    const bool fused = !(uf && uf[0] == '1');
     for (int g = g_max; g >= 2; --g) {
         CellGeom geo;
         uint64_t e0g = 0;
@@ -193,31 +338,23 @@ bool gres_cells_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_ma
         const size_t wb = w64 ? 8 : 4;
         SKY_CUDA(cudaMemsetAsync(rows, 0, geo.rows * wb, c.stream));
         const unsigned gs = grid_for(S, kBlock);
-        const unsigned gr = grid_for(geo.rows, kBlock);
         if (w64) {
             auto* R = static_cast<unsigned long long*>(rows);
             k_cells_mark<unsigned long long><<<gs, kBlock, 0, c.stream>>>(d_skyv, S, geo, R);
-            k_cells_or_word<unsigned long long><<<gr, kBlock, 0, c.stream>>>(R, geo.rows);
-            for (int j = 1; j < d; ++j)
-                k_cells_or_dim<unsigned long long><<<grid_for(geo.rows / geo.ext[j], kBlock), kBlock,
-                                                     0, c.stream>>>(R, geo.rows, geo.ext[j],
-                                                                    geo.stride[j]);
+            sweeps<unsigned long long>(c, R, geo, fused);
             reset_counts(c);
             k_cells_query<unsigned long long><<<grid_for(na, kBlock), kBlock, 0, c.stream>>>(
                 d_skyv, S, geo, R, act, na, d_den, c.d_slots + S_C3);
         } else {
             auto* R = static_cast<unsigned*>(rows);
             k_cells_mark<unsigned><<<gs, kBlock, 0, c.stream>>>(d_skyv, S, geo, R);
-            k_cells_or_word<unsigned><<<gr, kBlock, 0, c.stream>>>(R, geo.rows);
-            for (int j = 1; j < d; ++j)
-                k_cells_or_dim<unsigned><<<grid_for(geo.rows / geo.ext[j], kBlock), kBlock, 0,
-                                           c.stream>>>(R, geo.rows, geo.ext[j], geo.stride[j]);
+            sweeps<unsigned>(c, R, geo, fused);
             reset_counts(c);
             k_cells_query<unsigned><<<grid_for(na, kBlock), kBlock, 0, c.stream>>>(
                 d_skyv, S, geo, R, act, na, d_den, c.d_slots + S_C3);
         }
         SKY_LAUNCH_CHECK();
-        note_launch(c, 4 + d);
+        note_launch(c, 3);
         // algorithmic bytes of the step: the grid zeroed, read and written
         // once by an ideal fused prefix-OR, plus the mark and query reads of
         // the S x d values
