@@ -199,8 +199,26 @@ __device__ __forceinline__ bool tile_exact(const W* st, const uint32_t* sp, W tg
     return true;
 }
 
-// K6: persistent warps pull (row, chunk) items; each lane holds kCand
-// candidates.  The chunk is first tested against itself (4 tiles, exact
+// code-pass flags of one staged tile for the first KC candidate slots
+template <int KC, class W>
+__device__ __forceinline__ unsigned tile_hits(const W* st, const W (&tg)[kCand]) {
+    uint32_t acc[KC];
+#pragma unroll
+    for (int u = 0; u < KC; ++u) acc[u] = 0xFFFFFFFFu;
+#pragma unroll 8
+    for (int j = 0; j < 32; ++j) {
+        const W s = st[j];
+#pragma unroll
+        for (int u = 0; u < KC; ++u) acc[u] = min(acc[u], code_miss(tg[u], s));
+    }
+    unsigned hm = 0;
+#pragma unroll
+    for (int u = 0; u < KC; ++u) hm |= (acc[u] == 0u ? 1u : 0u) << u;
+    return hm;
+}
+
+// K6: persistent warps pull (row, chunk) items; each lane holds up to kCand
+// candidate slots.  The chunk is first tested against itself (exact
 // follow-up of every pass except the candidate itself); then the comparator
 // ranges — one per row <= the item's row, own row first, minus the chunk —
 // are streamed 32 codes at a time through shared memory: tiles are filled
@@ -208,7 +226,10 @@ __device__ __forceinline__ bool tile_exact(const W* st, const uint32_t* sp, W tg
 // current one is tested.  The tile test is 4 integer instructions per
 // (candidate, comparator) with no branch (min-accumulated miss bits); a tile
 // with a pass (rare: equal codes, near-dominators) gets the exact follow-up.
-// Warp exit when every candidate is decided.  keep[R index] = 1 for kept.
+// Dominated candidates free their slots: when the live ones fit in fewer
+// slots the warp repacks them (shared memory) and tests only the occupied
+// slots.  Warp exit when every candidate is decided.  keep[R index] = 1 for
+// kept tuples.
 template <int D>
 __global__ void __launch_bounds__(kGB)
 k_grid_decide(const double* __restrict__ v, const unsigned long long* __restrict__ key,
@@ -220,6 +241,8 @@ k_grid_decide(const double* __restrict__ v, const unsigned long long* __restrict
     using W = GridWord<D>;
     __shared__ W stage[kGB / 32][32];
     __shared__ uint32_t spos[kGB / 32][32];
+    __shared__ W pk_tg[kGB / 32][kItem];
+    __shared__ uint32_t pk_q[kGB / 32][kItem];
     const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const W H = (W)0x8080808080808080ULL;
     const uint32_t nitems = ctr[0];
@@ -240,31 +263,30 @@ k_grid_decide(const double* __restrict__ v, const unsigned long long* __restrict
         const uint32_t own = item.x, first = item.y;
         const uint32_t end = min(seg[(own + 1) * k0], first + kItem);
         W tg[kCand];
+        uint32_t qt[kCand];
         unsigned alive = 0;
 #pragma unroll
         for (int u = 0; u < kCand; ++u) {
-            const uint32_t q = first + u * 32 + lane;
-            tg[u] = q < end ? (scode[q] | H) : (W)0;
-            alive |= (q < end ? 1u : 0u) << u;
+            qt[u] = first + u * 32 + lane;
+            tg[u] = qt[u] < end ? (scode[qt[u]] | H) : (W)0;
+            alive |= (qt[u] < end ? 1u : 0u) << u;
         }
+        unsigned valid = alive;
+        int kc = (int)((end - first + 31) / 32);  // occupied slots (warp-uniform)
         // ---- the chunk against itself
-#pragma unroll
-        for (int t = 0; t < kCand; ++t) {
-            const uint32_t q0 = first + t * 32;
-            if (q0 >= end) break;
-            const uint32_t q = q0 + lane;
+        for (int t = 0; t < kc; ++t) {
+            const uint32_t q = first + t * 32 + lane;
             st[lane] = q < end ? scode[q] : code_never<W>();
             sp[lane] = q < end ? q : ~0u;
             __syncwarp();
 #pragma unroll
             for (int u = 0; u < kCand; ++u) {
                 if ((alive >> u) & 1u) {
-                    const uint32_t qt = first + u * 32 + lane;
-                    if (!tile_exact<D>(st, sp, tg[u], qt, qt, v, key, ids, R, sidx))
+                    if (!tile_exact<D>(st, sp, tg[u], qt[u], qt[u], v, key, ids, R, sidx))
                         alive &= ~(1u << u);
                 }
             }
-            cnt += (unsigned long long)min(32u, end - q0) * __popc(alive);
+            cnt += (unsigned long long)min(32u, end - (first + t * 32)) * __popc(alive);
             __syncwarp();
         }
         // largest attribute-0 bin among the candidates = that of the last one
@@ -322,48 +344,78 @@ k_grid_decide(const double* __restrict__ v, const unsigned long long* __restrict
             }
             return filled;
         };
+        // repack the live candidates into the first slots
+        auto repack = [&](int live) {
+            unsigned mine = __popc(alive);
+            unsigned incl = mine;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+                if ((int)lane >= o) incl += y;
+            }
+            unsigned at = incl - mine;
+#pragma unroll
+            for (int u = 0; u < kCand; ++u) {
+                if ((alive >> u) & 1u) {
+                    pk_tg[wib][at] = tg[u];
+                    pk_q[wib][at] = qt[u];
+                    ++at;
+                } else if ((valid >> u) & 1u) {
+                    keep[sidx[qt[u]]] = 0;  // decided: dominated
+                }
+            }
+            __syncwarp();
+            alive = 0;
+#pragma unroll
+            for (int u = 0; u < kCand; ++u) {
+                const int i = u * 32 + (int)lane;
+                if (i < live) {
+                    tg[u] = pk_tg[wib][i];
+                    qt[u] = pk_q[wib][i];
+                    alive |= 1u << u;
+                }
+            }
+            valid = alive;
+            kc = (live + 31) / 32;
+            __syncwarp();
+        };
         uint32_t pos_next;
-        uint32_t npos = __any_sync(0xffffffffu, alive != 0u) ? fill(pos_next) : 0;
+        int live = __reduce_add_sync(0xffffffffu, __popc(alive));
+        uint32_t npos = live ? fill(pos_next) : 0;
         W code_next = pos_next != ~0u ? scode[pos_next] : code_never<W>();
         while (npos) {
+            if (live <= 32 * (kc - 1)) repack(live);
             st[lane] = code_next;
             sp[lane] = pos_next;
             const uint32_t n = npos;
             __syncwarp();
             npos = fill(pos_next);  // prefetch the next tile
             code_next = pos_next != ~0u ? scode[pos_next] : code_never<W>();
-            uint32_t acc[kCand];
-#pragma unroll
-            for (int u = 0; u < kCand; ++u) acc[u] = 0xFFFFFFFFu;
-#pragma unroll 8
-            for (int j = 0; j < 32; ++j) {
-                const W s = st[j];
-#pragma unroll
-                for (int u = 0; u < kCand; ++u) acc[u] = min(acc[u], code_miss(tg[u], s));
+            unsigned hm;
+            switch (kc) {
+                case 1: hm = tile_hits<1>(st, tg); break;
+                case 2: hm = tile_hits<2>(st, tg); break;
+                case 3: hm = tile_hits<3>(st, tg); break;
+                default: hm = tile_hits<4>(st, tg); break;
             }
             cnt += (unsigned long long)n * __popc(alive);
-            unsigned hm = 0;
-#pragma unroll
-            for (int u = 0; u < kCand; ++u) hm |= (acc[u] == 0u ? 1u : 0u) << u;
             hm &= alive;
             if (__any_sync(0xffffffffu, hm != 0u)) {  // rare: exact follow-up
 #pragma unroll
                 for (int u = 0; u < kCand; ++u) {
                     if ((hm >> u) & 1u) {
-                        const uint32_t qt = first + u * 32 + lane;
-                        if (!tile_exact<D>(st, sp, tg[u], qt, ~0u, v, key, ids, R, sidx))
+                        if (!tile_exact<D>(st, sp, tg[u], qt[u], ~0u, v, key, ids, R, sidx))
                             alive &= ~(1u << u);
                     }
                 }
             }
             __syncwarp();
-            if (!__any_sync(0xffffffffu, alive != 0u)) break;
+            live = __reduce_add_sync(0xffffffffu, __popc(alive));
+            if (!live) break;
         }
 #pragma unroll
-        for (int u = 0; u < kCand; ++u) {
-            const uint32_t q = first + u * 32 + lane;
-            if (q < end) keep[sidx[q]] = (alive >> u) & 1u;
-        }
+        for (int u = 0; u < kCand; ++u)
+            if ((valid >> u) & 1u) keep[sidx[qt[u]]] = (alive >> u) & 1u;
     }
     add_count(tests, cnt);
 }
