@@ -211,11 +211,13 @@ def our_arm(args):
     den_d = torch.empty(n, dtype=torch.int32, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     shard_rank, shard_world = (rank, world) if strong else (0, 1)
+    sky_flag = {"auto": skypar.SKY_AUTO, "rounds": skypar.SKY_ROUNDS, "grid": skypar.SKY_GRID}[args.sky_engine]
 
     def step_device():
         S, gm, st = skypar.pipeline_raw(vals_d.data_ptr(), ids_d.data_ptr(), n, d, plan, cap,
-                                        args.engine, shard_rank, shard_world, skypar.DEVICE_PTRS,
-                                        pos_d.data_ptr(), den_d.data_ptr())
+                                        args.engine, shard_rank, shard_world,
+                                        skypar.DEVICE_PTRS | sky_flag, pos_d.data_ptr(),
+                                        den_d.data_ptr())
         if strong and world > 1:  # NCCL max-reduce of the sharded denominators
             dist.all_reduce(den_d[:S], op=dist.ReduceOp.MAX)
         return S, gm, st
@@ -270,7 +272,7 @@ def our_arm(args):
 
     def step_e2e():
         S2, _, _ = skypar.pipeline_raw(pin_vals.data_ptr(), pin_ids.data_ptr(), n, d, plan, cap,
-                                       args.engine, shard_rank, shard_world, 0,
+                                       args.engine, shard_rank, shard_world, sky_flag,
                                        out_pos.data_ptr(), out_den.data_ptr())
         if strong and world > 1:
             t_den = torch.from_numpy(out_den.numpy()[:S2]).to(dev)
@@ -310,7 +312,8 @@ def our_arm(args):
                    "skyline_size": S, "g_max": gm, "l2": "flushed (256 MiB write) before each step",
                    "parallelism": f"{'sharded gres + NCCL max' if strong else 'independent instance'}"
                                   f" per GPU x{world}",
-                   "gres_engine": {0: "auto", 1: "pairs", 2: "cells"}[args.engine]},
+                   "gres_engine": {0: "auto", 1: "pairs", 2: "cells"}[args.engine],
+                   "skyline_engine": {8: "prefix rounds", 16: "rank grid"}.get(stats[-1]["sky_engine"], "?")},
         "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": n * d * 8 + n * 8,
                 "d2h_bytes_per_step": S * 4 + S * 4},
@@ -437,7 +440,9 @@ def main():
     ap.add_argument("--workload", default="C2", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
-    ap.add_argument("--engine", type=int, default=0)
+    ap.add_argument("--engine", type=int, default=0, help="gres engine: 0 auto, 1 pairs, 2 cells")
+    ap.add_argument("--sky-engine", default="auto", choices=["auto", "rounds", "grid"],
+                    help="skyline engine (default: chosen after the first prefix round)")
     ap.add_argument("--strategy", default=None, choices=["none", "grid", "angular", "sliced"],
                     help="override the workload's partitioning plan (both arms)")
     ap.add_argument("--partitions", type=int, default=None, help="override the target partitions")
