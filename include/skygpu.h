@@ -15,6 +15,8 @@
  *   skygpu_make_plan           <- skypar::make_plan          include/skypar/partition.hpp:43
  *   skygpu_pipeline            <- the composition run_experiment performs
  *                                 (proj/src/harness.cpp:208 then :229-231)
+ *   skygpu_sfs_accounting      <- the DominanceCounter totals inside
+ *                                 parallel_skyline (parallel.cpp:59-93)
  *
  * Conventions
  *  - Values are float64, row-major n x d (tuple i = vals[i*d .. i*d+d-1]),
@@ -149,6 +151,24 @@ int skygpu_pipeline(const double* vals, const int64_t* ids, uint64_t n, int d,
                     int shard_world, unsigned flags, uint64_t* out_pos, int32_t* out_den,
                     uint64_t* out_s, int* out_g_max, skygpu_stats* stats, char* err,
                     size_t errlen);
+
+/* Exact reference accounting of parallel_skyline — "metrics-parity" mode,
+ * not the hot path.  Returns the DominanceCounter
+ * totals the reference's CPU algorithm executes (core.hpp:46-67): per
+ * partition the representative filter (partition.cpp:287-302) + the local
+ * SFS (core.cpp:48-73), and the merge-phase SFS (parallel.cpp:83-86).
+ * pid[i] = partition of tuple i in [0, p), or -1 for a tuple dropped before
+ * phase 1 (Grid dominated cells, parallel.cpp:32-42); the caller assigns
+ * partitions with the reference's own assign_partitions (partition.cpp:183).
+ * rep_vals: the representative tuples (n_reps x d, may be NULL when 0).
+ * Outputs: per_part[0..p) tests per partition, *final_tests merge tests,
+ * *into_final = tuples entering the merge, out_pos[0..*out_n) = skyline
+ * input positions in (sum, id) order (out_pos sized n). */
+int skygpu_sfs_accounting(const double* vals, const int64_t* ids, uint64_t n, int d,
+                          const int64_t* pid, long long p, const double* rep_vals,
+                          uint64_t n_reps, uint64_t* per_part, uint64_t* final_tests,
+                          uint64_t* into_final, uint64_t* out_pos, uint64_t* out_n, char* err,
+                          size_t errlen);
 
 /* Product-side seeded generators (bit-exact with proj/src/datagen.cpp:41-94;
  * kind 0 uni, 1 ant, 2 corr = BASELINE C3, 3 lattice = test_util.hpp:38-54).

@@ -64,5 +64,16 @@ if [ -f "$LIBDIR/libskygpu.so" ]; then
   $CXX $COMMON -O2 "$REF/tests/acceptance_main.cpp" "$OUT/libskypar_chk.a" -o "$OUT/acceptance_ref"
   $CXX $COMMON -O3 -DNDEBUG -I"$REF/include" "$HERE/refdrive.cpp" "$OUT/libskypar_gpu_rel.a" \
       -L"$LIBDIR" -lskygpu $RPATH -o "$OUT/refdrive_gpu"
-  echo "build_ref: drop-in binaries ok (acceptance_gpu, refdrive_gpu)"
+  # the skypar CLI front-end (adapter/skypar_cli.cpp, hand-written parser):
+  # over the GPU drop-in and over the unmodified CPU library, both in the
+  # reference's default (checked) build
+  $CXX $COMMON -O2 -g -I"$REF/include" "$ROOT/paper_2412_02274_b200/adapter/skypar_cli.cpp" \
+      "$OUT/libskypar_gpu_chk.a" -L"$LIBDIR" -lskygpu $RPATH -o "$OUT/skypar_gpu"
+  $CXX $COMMON -O2 -g -I"$REF/include" "$ROOT/paper_2412_02274_b200/adapter/skypar_cli.cpp" \
+      "$OUT/libskypar_chk.a" -o "$OUT/skypar_ref"
+  # the CLI-determinism fixtures (acceptance criterion 9) travel with the
+  # binaries; /root/reference does not exist on the GPU box
+  mkdir -p "$OUT/fixtures"
+  cp "$REF/data/fixtures/"*.csv "$OUT/fixtures/"
+  echo "build_ref: drop-in binaries ok (acceptance_gpu, refdrive_gpu, skypar_gpu, skypar_ref)"
 fi

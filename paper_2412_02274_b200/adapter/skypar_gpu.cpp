@@ -16,21 +16,33 @@
 // std::invalid_argument text the reference throws, ERUNTIME -> runtime_error,
 // CUDA failures -> runtime_error (there is no CPU fallback).
 //
-// Metrics: results are bit-exact; the per-phase dominance-test COUNTS are the
-// GPU algorithm's own (a different algorithm executes different tests):
-// parallel_max = tests of the dominant GPU kernels of the skyline stage,
-// final_tests = 0, per-g rows carry the gres tests spread over the steps the
-// scan ran.  Exact SFS counter emulation is a separate, later mode (SURVEY.md
-// §8(f) rank 2).  Wall times are measured around the device calls.
+// Metrics (PhaseMetrics, ResistanceMetrics): by default EXACT — the
+// reference's DominanceCounter totals, derived on the GPU by
+// skygpu_sfs_accounting (csrc/accounting.cu) from the partitions the
+// reference's own assign_partitions / grid_cell / prune_grid_dominated /
+// select_representatives produce (partition.o stays the reference's), so
+// every report, the paper's simulated_cost, and the count-pinning tests
+// (test_parallel.cpp:25-43, acceptance criteria 8 and 10) match the CPU
+// library.  max_concurrent reports the core-budget bound min(cores, p)
+// (the reference's OMP high-water mark, parallel.cpp:62-70, is scheduling
+// dependent).  SKYGPU_METRICS=fast skips the accounting (answers only; the
+// counters then hold the GPU kernels' own test counts).  Wall times are
+// measured around the device calls.
 #include <chrono>
 #include <cstring>
 #include <stdexcept>
 #include <string>
 #include <vector>
 
+#include <algorithm>
+#include <cstdlib>
+#include <map>
+#include <set>
+
 #include "skygpu.h"
 #include "skypar/gres.hpp"
 #include "skypar/parallel.hpp"
+#include "skypar/partition.hpp"
 
 namespace skypar {
 
@@ -71,11 +83,73 @@ double ms_since(Clock::time_point t0) {
     return std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
 }
 
+static_assert(sizeof(long long) == sizeof(std::int64_t), "partition ids are passed as int64");
+
+bool exact_metrics() {
+    const char* e = std::getenv("SKYGPU_METRICS");
+    return !(e && std::string(e) == "fast");
+}
+
+// parallel_skyline with the reference's exact accounting (see header)
+ParallelSkylineResult parallel_skyline_exact(const Relation& r, const PartitionPlan& plan,
+                                             const RepresentativeSet& reps, int cores) {
+    const auto t0 = Clock::now();
+    const long long p = plan.partitions;
+    // the reference's partition of every tuple (partition.cpp:183-213), and
+    // its Grid pre-pruning (parallel.cpp:32-42): dropped tuples get -1
+    std::vector<long long> pids = assign_partitions(r, plan);
+    if (plan.strategy == Strategy::Grid && !r.empty()) {
+        std::map<GridCell, std::size_t> occupancy;
+        std::vector<GridCell> cells(r.size());
+        for (std::size_t i = 0; i < r.size(); ++i) {
+            cells[i] = grid_cell(r.tuples[i], plan.slices);
+            ++occupancy[cells[i]];
+        }
+        const std::set<GridCell> survivors = prune_grid_dominated(occupancy);
+        for (std::size_t i = 0; i < r.size(); ++i)
+            if (!survivors.count(cells[i])) pids[i] = -1;
+    }
+    std::vector<double> vals, rvals;
+    std::vector<std::int64_t> ids;
+    flatten(r, vals, ids);
+    for (const Tuple& t : reps.tuples) rvals.insert(rvals.end(), t.values.begin(), t.values.end());
+    std::vector<std::uint64_t> per(static_cast<std::size_t>(p)), pos(r.size() ? r.size() : 1);
+    std::uint64_t final_tests = 0, into_final = 0, S = 0;
+    char err[1024];
+    const auto t1 = Clock::now();
+    check(skygpu_sfs_accounting(vals.data(), ids.data(), r.size(), static_cast<int>(r.dims),
+                                reinterpret_cast<const std::int64_t*>(pids.data()), p,
+                                rvals.data(), reps.tuples.size(), per.data(),
+                                &final_tests, &into_final, pos.data(), &S, err, sizeof(err)),
+          err);
+    const double wall_parallel = ms_since(t1);
+    ParallelSkylineResult res;
+    res.skyline = Relation(r.dims);
+    res.skyline.tuples.reserve(S);
+    for (std::uint64_t k = 0; k < S; ++k) res.skyline.tuples.push_back(r.tuples[pos[k]]);
+    PhaseMetrics& m = res.metrics;
+    m.per_partition_tests.assign(per.begin(), per.end());
+    for (std::uint64_t c : per) m.parallel_max = std::max<std::uint64_t>(m.parallel_max, c);
+    m.final_tests = final_tests;
+    m.cores = cores;
+    m.scale_factor = (p + cores - 1) / cores;
+    m.simulated_cost = m.parallel_max * static_cast<std::uint64_t>(m.scale_factor) + m.final_tests;
+    m.max_concurrent = static_cast<int>(std::min<long long>(cores, std::max<long long>(p, 1)));
+    m.tuples_into_parallel = static_cast<std::uint64_t>(
+        std::count_if(pids.begin(), pids.end(), [](long long v) { return v >= 0; }));
+    m.tuples_into_final = into_final;
+    m.wall_parallel_ms = wall_parallel;
+    m.wall_total_ms = ms_since(t0);
+    if (m.wall_parallel_ms > m.wall_total_ms) m.wall_parallel_ms = m.wall_total_ms;
+    return res;
+}
+
 }  // namespace
 
 ParallelSkylineResult parallel_skyline(const Relation& r, const PartitionPlan& plan,
                                        const RepresentativeSet& reps, int cores) {
     if (cores < 1) throw std::invalid_argument("parallel_skyline: cores must be >= 1");
+    if (exact_metrics()) return parallel_skyline_exact(r, plan, reps, cores);
     const auto t0 = Clock::now();
     std::vector<double> vals, rvals;
     std::vector<std::int64_t> ids, rids;
@@ -187,6 +261,33 @@ GridResistanceResult grid_resistance(const Relation& skyline, const PartitionPla
           err);
     if (skyline.empty()) return result;
     m.g_max = g_max;
+    for (std::size_t i = 0; i < skyline.size(); ++i)
+        result.denominators.emplace(ids[i], den[i]);
+    if (exact_metrics()) {
+        // the reference's per-step accounting (gres.cpp:96-118): the
+        // projection, its representatives, one exactly-counted
+        // parallel_skyline per interval count
+        double effective_sum = 0.0;
+        for (int g = g_max; g >= 2; --g) {
+            const Relation projected = snap_relation(skyline, g);
+            DominanceCounter rc;
+            const RepresentativeSet reps =
+                select_representatives(projected, rep_count, sum_score, rc);
+            m.rep_tests += rc.count;
+            effective_sum += static_cast<double>(reps.effective());
+            const ParallelSkylineResult round = parallel_skyline_exact(projected, plan, reps, cores);
+            m.iterations.push_back({g, round.metrics.parallel_max, round.metrics.final_tests});
+            m.parallel_max_sum += round.metrics.parallel_max;
+            m.final_sum += round.metrics.final_tests;
+            m.simulated_cost += round.metrics.simulated_cost;
+            m.wall_parallel_ms += round.metrics.wall_parallel_ms;
+        }
+        if (!m.iterations.empty())
+            m.rep_effective_mean = effective_sum / static_cast<double>(m.iterations.size());
+        m.wall_total_ms = ms_since(t0);
+        if (m.wall_parallel_ms > m.wall_total_ms) m.wall_parallel_ms = m.wall_total_ms;
+        return result;
+    }
     const int steps = g_max >= 2 ? g_max - 1 : 0;
     for (int g = g_max; g >= 2; --g) {
         IterationCost it;
@@ -200,8 +301,6 @@ GridResistanceResult grid_resistance(const Relation& skyline, const PartitionPla
     m.simulated_cost = m.parallel_max_sum * static_cast<std::uint64_t>(m.scale_factor);
     m.rep_tests = 0;
     m.rep_effective_mean = 0.0;
-    for (std::size_t i = 0; i < skyline.size(); ++i)
-        result.denominators.emplace(ids[i], den[i]);
     m.wall_total_ms = ms_since(t0);
     m.wall_parallel_ms = st.ms_gres_kernel < m.wall_total_ms ? st.ms_gres_kernel : m.wall_total_ms;
     return result;

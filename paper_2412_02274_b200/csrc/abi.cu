@@ -272,6 +272,20 @@ __global__ void k_widen(const uint32_t* __restrict__ a, uint64_t* __restrict__ b
 }
 }  // namespace
 
+namespace {
+__global__ void k_fill_i32(int32_t* __restrict__ a, uint64_t n, int32_t v) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        a[i] = v;
+}
+__global__ void k_mark_i32(int32_t* __restrict__ a, const uint32_t* __restrict__ at, uint64_t n,
+                           int32_t v) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        a[at[i]] = v;
+}
+}  // namespace
+
 void widen_u32_u64(Ctx& c, const uint32_t* a, uint64_t* b, uint64_t n) {
     k_widen<<<grid_for(n, 256), 256, 0, c.stream>>>(a, b, n);
     SKY_LAUNCH_CHECK();
@@ -557,6 +571,76 @@ int skygpu_pipeline(const double* vals, const int64_t* ids, uint64_t n, int d,
         all.stop(&c.st->ms_total);
         *out_s = so.S;
         *out_g_max = go.g_max;
+        end_stats(c);
+    });
+}
+
+int skygpu_sfs_accounting(const double* vals, const int64_t* ids, uint64_t n, int d,
+                          const int64_t* pid, long long p, const double* rep_vals,
+                          uint64_t n_reps, uint64_t* per_part, uint64_t* final_tests,
+                          uint64_t* into_final, uint64_t* out_pos, uint64_t* out_n, char* err,
+                          size_t errlen) {
+    return guarded(err, errlen, [&] {
+        if (d < 1 || d > kMaxDims) invalid("sfs_accounting: dims must be in [1, 32]");
+        if (p < 1 || p > (1LL << 20)) invalid("sfs_accounting: partitions must be in [1, 2^20]");
+        if (n >= 0xFFFFFFFFull) invalid("sfs_accounting: more than 2^32-1 tuples");
+        Ctx& c = ctx();
+        begin_stats(c, nullptr);
+        for (long long k = 0; k < p; ++k) per_part[k] = 0;
+        *final_tests = 0;
+        *into_final = 0;
+        *out_n = 0;
+        if (n == 0) {
+            end_stats(c);
+            return;
+        }
+        std::vector<int32_t> gid(n);
+        for (uint64_t i = 0; i < n; ++i) {
+            if (pid[i] >= p) invalid("sfs_accounting: partition id out of range");
+            gid[i] = pid[i] < 0 ? -1 : (int32_t)pid[i];
+        }
+        double* dv = c.buf[B_IN_VALS].as<double>(n * d);
+        int64_t* di = c.buf[B_IN_IDS].as<int64_t>(n);
+        int32_t* dg = c.buf[B_ACC12].as<int32_t>(n);
+        int32_t* dg2 = c.buf[B_ACC13].as<int32_t>(n);
+        uint32_t* kept1 = c.buf[B_ACC14].as<uint32_t>(n);
+        uint32_t* kept2 = c.buf[B_ACC15].as<uint32_t>(n);
+        auto* cnt = c.buf[B_ACC16].as<unsigned long long>((uint64_t)p + 1);
+        double* dr = n_reps ? c.buf[B_REPS].as<double>(n_reps * d) : nullptr;
+        SKY_CUDA(cudaMemcpyAsync(dv, vals, n * d * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+        SKY_CUDA(cudaMemcpyAsync(di, ids, n * sizeof(int64_t), cudaMemcpyHostToDevice, c.stream));
+        SKY_CUDA(cudaMemcpyAsync(dg, gid.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice,
+                                 c.stream));
+        if (n_reps)
+            SKY_CUDA(cudaMemcpyAsync(dr, rep_vals, n_reps * d * sizeof(double),
+                                     cudaMemcpyHostToDevice, c.stream));
+        SKY_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * ((uint64_t)p + 1), c.stream));
+        // phase 1: representative filter + local SFS per partition
+        const uint64_t nk = sfs_accounting_device(c, dv, di, n, d, dg, (uint32_t)p, dr,
+                                                  (uint32_t)n_reps, cnt, kept1);
+        std::vector<unsigned long long> h(p + 1);
+        SKY_CUDA(cudaMemcpyAsync(h.data(), cnt, sizeof(unsigned long long) * p,
+                                 cudaMemcpyDeviceToHost, c.stream));
+        // phase 2: one SFS over the union of the local skylines
+        k_fill_i32<<<grid_for(n, 256), 256, 0, c.stream>>>(dg2, n, -1);
+        if (nk) k_mark_i32<<<grid_for(nk, 256), 256, 0, c.stream>>>(dg2, kept1, nk, 0);
+        SKY_LAUNCH_CHECK();
+        note_launch(c, 2);
+        SKY_CUDA(cudaMemsetAsync(cnt + p, 0, sizeof(unsigned long long), c.stream));
+        const uint64_t nf = sfs_accounting_device(c, dv, di, n, d, dg2, 1, nullptr, 0, cnt + p,
+                                                  kept2);
+        SKY_CUDA(cudaMemcpyAsync(h.data() + p, cnt + p, sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToHost, c.stream));
+        std::vector<uint32_t> pos(nf);
+        if (nf)
+            SKY_CUDA(cudaMemcpyAsync(pos.data(), kept2, nf * sizeof(uint32_t),
+                                     cudaMemcpyDeviceToHost, c.stream));
+        SKY_CUDA(cudaStreamSynchronize(c.stream));
+        for (long long k = 0; k < p; ++k) per_part[k] = h[k];
+        *final_tests = h[p];
+        *into_final = nk;
+        for (uint64_t k = 0; k < nf; ++k) out_pos[k] = pos[k];
+        *out_n = nf;
         end_stats(c);
     });
 }

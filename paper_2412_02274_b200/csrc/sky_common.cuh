@@ -68,7 +68,8 @@ enum BufId {
     B_R0, B_R1, B_FLAGS, B_KLIST, B_CUB, B_SKYV, B_SKYID, B_CODES, B_ACT0, B_ACT1,
     B_DEN, B_GTMP0, B_GTMP1, B_OUTPOS, B_PROJ, B_REPS, B_MISC, B_CELLS, B_CSUM,
     B_ORDER, B_AMAX, B_AQ, B_PQ, B_GCODE, B_GCELL, B_GSCODE, B_GSIDX, B_GITEMS, B_GCNT,
-    B_COUNT
+    B_ACC0, B_ACC1, B_ACC2, B_ACC3, B_ACC4, B_ACC5, B_ACC6, B_ACC7, B_ACC8, B_ACC9, B_ACC10,
+    B_ACC11, B_ACC12, B_ACC13, B_ACC14, B_ACC15, B_ACC16, B_COUNT
 };
 
 // Device-side scalar slots (one small allocation, read back through pinned memory).
@@ -231,6 +232,14 @@ void check_grid_projection(Ctx& c, const double* d_skyv, uint64_t S, int d, int 
 bool gres_cells_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_max,
                        const uint32_t* act, uint64_t na, int32_t* d_den, uint64_t* cells_swept,
                        int* steps_run);
+
+// accounting.cu: exact SFS DominanceCounter totals of one phase (groups =
+// partitions, gid < 0 = not in the phase, optional representatives); adds
+// the tests per group into d_per_group and writes the kept positions (group
+// by group, (sum, id) order) into d_kept; returns how many
+uint64_t sfs_accounting_device(Ctx& c, const double* d_vals, const int64_t* d_ids, uint64_t n,
+                               int d, const int32_t* d_gid, uint32_t p, const double* d_reps,
+                               uint32_t nr, unsigned long long* d_per_group, uint32_t* d_kept);
 
 // float64 AoS -> SoA transpose on the device
 void aos_to_soa(Ctx& c, const double* d_aos, uint64_t n, int d, double* d_soa);

@@ -915,6 +915,73 @@ k_sfs_intra_q(const double* __restrict__ Av, const unsigned long long* __restric
     add_count(tests, cnt);
 }
 
+// K4, chunked: the predecessor scan of a prefix member is split into chunks
+// of kIntraChunk comparators, one warp per (chunk, candidate) item, so the
+// long scans of late skyline members no longer serialise the kernel on one
+// warp's load-latency chain.  Items run chunk-major (chunk 0 of every
+// candidate first); a warp that finds a dominator clears keep[i] (pre-set to
+// 1), and the other chunks of that candidate poll it and stop.  128
+// comparators per ballot (four per lane, loads in flight together).
+constexpr uint32_t kIntraChunk = 1024;
+
+template <int D>
+__global__ void __launch_bounds__(kBlock)
+k_sfs_intra_chunked(const double* __restrict__ Av, const unsigned long long* __restrict__ Aq,
+                    uint32_t m, volatile uint8_t* keep, unsigned long long* __restrict__ tests) {
+    constexpr int W = QW<D>::W;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    const uint32_t nch = (m + kIntraChunk - 1) / kIntraChunk;
+    uint64_t total = 0;
+    for (uint32_t c = 0; c < nch; ++c)
+        if ((uint64_t)c * kIntraChunk + 1 < m) total += m - c * kIntraChunk - 1;
+    unsigned long long cnt = 0;
+    for (uint64_t it = warp; it < total; it += nwarps) {
+        uint64_t rem = it;
+        uint32_t c = 0;
+        for (;;) {
+            const uint64_t nc = m - c * kIntraChunk - 1;
+            if (rem < nc) break;
+            rem -= nc;
+            ++c;
+        }
+        const uint32_t i = c * kIntraChunk + 1 + (uint32_t)rem;
+        if (keep[i] == 0) continue;  // another chunk already found a dominator
+        const uint32_t j1 = min(i, (c + 1) * kIntraChunk);
+        double t[D];
+#pragma unroll
+        for (int k = 0; k < D; ++k) t[k] = Av[(uint64_t)k * m + i];
+        unsigned long long tg[W];
+#pragma unroll
+        for (int k = 0; k < W; ++k) tg[k] = Aq[(uint64_t)i * W + k] | kH16;
+        bool dominated = false;
+        for (uint32_t j0 = c * kIntraChunk; j0 < j1; j0 += 128) {
+            bool hit = false;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t j = j0 + u * 32 + lane;
+                if (j < j1) {
+                    ++cnt;
+                    if (le16<D>(Aq + (uint64_t)j * W, tg)) {
+                        double s[D];
+#pragma unroll
+                        for (int k = 0; k < D; ++k) s[k] = Av[(uint64_t)k * m + j];
+                        hit |= dom_f64<D>(s, t);
+                    }
+                }
+            }
+            if (__any_sync(0xffffffffu, hit)) {
+                dominated = true;
+                break;
+            }
+            if (keep[i] == 0) break;
+        }
+        if (dominated && lane == 0) keep[i] = 0;
+    }
+    add_count(tests, cnt);
+}
+
 // K5 with the quantised prefilter (D in 1..8).  Two scan modes:
 //  qk > 0  quantile grid (the default): the new skyline tuples A' are grouped
 //          by a k^d grid whose bin bounds are quantiles of A' itself; a
@@ -1203,6 +1270,15 @@ int cells_per_dim(uint64_t m, int d, uint32_t* ncells);
 // partition when it has at most kMaxCells parts (and d <= 8 for the
 // attribute-scaled kinds), else direction cells sized for ~128 tuples each.
 int scan_cell_spec(const skygpu_plan& plan, uint64_t m, int d, bool qpre, uint32_t* ncells) {
+    // tuning knob: SKYGPU_SCAN_CELLS=dir ignores the plan's partition
+    static const bool dir_only = [] {
+        const char* e = getenv("SKYGPU_SCAN_CELLS");
+        return e && e[0] == 'd';
+    }();
+    if (dir_only) {
+        const int mc = cells_per_dim(m, d, ncells);
+        return mc > 1 ? mc : 0;
+    }
     auto ipow = [](uint64_t b, int e) {
         uint64_t v = 1;
         for (int i = 0; i < e; ++i) {
@@ -1238,7 +1314,12 @@ int scan_cell_spec(const skygpu_plan& plan, uint64_t m, int d, bool qpre, uint32
 int cells_per_dim(uint64_t m, int d, uint32_t* ncells) {
     int mcell = 1;
     if (d >= 2) {
-        const double target = std::max(1.0, (double)m / 128.0);
+        static const double per_cell = [] {
+            const char* e = getenv("SKYGPU_DIR_PER_CELL");
+            const double x = e ? atof(e) : 0.0;
+            return x > 0 ? x : 128.0;
+        }();
+        const double target = std::max(1.0, (double)m / per_cell);
         mcell = (int)std::floor(std::pow(target, 1.0 / (d - 1)) + 1e-9);
         mcell = std::max(1, std::min(mcell, 64));
     }
@@ -1465,14 +1546,24 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
             // ---- K4: SFS inside the prefix, predecessors in sum order
             uint8_t* keep = c.buf[B_FLAGS].as<uint8_t>(m);
             const uint64_t wi = std::min<uint64_t>(m, (uint64_t)c.num_sms * 64);
+            static const bool intra_chunked = [] {
+                const char* e = getenv("SKYGPU_INTRA");
+                return !(e && e[0] == '1');  // SKYGPU_INTRA=1: one warp per candidate
+            }();
+            if (qpre && intra_chunked)
+                SKY_CUDA(cudaMemsetAsync(keep, 1, m, c.stream));
             SKY_CUDA(cudaEventRecord(e0, c.stream));
             dispatch_d(d, [&](auto DC) {
                 constexpr int D = decltype(DC)::value;
                 const unsigned grid = (unsigned)((wi * 32 + kBlock - 1) / kBlock);
-                if constexpr (D > 0)
-                    k_sfs_intra_q<D><<<grid, kBlock, 0, c.stream>>>(Av, Aq, (uint32_t)m, keep,
-                                                                    c.d_slots + S_TESTS_SKY);
-                else
+                if constexpr (D > 0) {
+                    if (intra_chunked)
+                        k_sfs_intra_chunked<D><<<c.num_sms * 8, kBlock, 0, c.stream>>>(
+                            Av, Aq, (uint32_t)m, keep, c.d_slots + S_TESTS_SKY);
+                    else
+                        k_sfs_intra_q<D><<<grid, kBlock, 0, c.stream>>>(Av, Aq, (uint32_t)m, keep,
+                                                                        c.d_slots + S_TESTS_SKY);
+                } else
                     k_sfs_intra_sorted<D><<<grid, kBlock, 0, c.stream>>>(
                         Av, (uint32_t)m, d, keep, c.d_slots + S_TESTS_SKY);
             });

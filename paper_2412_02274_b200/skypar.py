@@ -109,6 +109,8 @@ def lib() -> C.CDLL:
         L.skygpu_pipeline.argtypes = [vp, vp, u64, i32, C.POINTER(_Plan), i32, i32, i32, i32,
                                       C.c_uint, vp, vp, vp, vp, C.POINTER(Stats), cp, sz]
         L.skygpu_generate.argtypes = [i32, u64, i32, u64, vp, cp, sz]
+        L.skygpu_sfs_accounting.argtypes = [vp, vp, u64, i32, vp, i64, vp, u64, vp, vp, vp, vp, vp,
+                                            cp, sz]
         _lib = L
     return _lib
 
@@ -116,7 +118,7 @@ def lib() -> C.CDLL:
 EXPORTED_SYMBOLS = ("skygpu_version", "skygpu_device_count", "skygpu_set_device", "skygpu_set_stream",
                     "skygpu_release", "skygpu_make_plan", "skygpu_parallel_skyline",
                     "skygpu_grid_resistance", "skygpu_snap_relation", "skygpu_max_grid_intervals",
-                    "skygpu_pipeline", "skygpu_generate")
+                    "skygpu_pipeline", "skygpu_generate", "skygpu_sfs_accounting")
 
 
 def _check(rc: int, err: C.Array) -> None:
@@ -313,3 +315,36 @@ def generate(kind: str, n: int, d: int, seed: int) -> np.ndarray:
     err = _errbuf()
     _check(lib().skygpu_generate(GEN_KINDS[kind], n, d, seed, _p(out), err, 1024), err)
     return out
+
+
+@dataclass
+class Accounting:
+    """The reference's DominanceCounter totals of one parallel_skyline run
+    (parallel.cpp:59-93): per-partition tests (rep filter + local SFS), the
+    merge-phase tests, the merge input size and the skyline positions."""
+    per_partition: np.ndarray
+    final_tests: int
+    into_final: int
+    positions: np.ndarray
+
+
+def sfs_accounting(values, ids, pids, partitions: int, reps=None) -> Accounting:
+    """Exact reference accounting (metrics-parity mode; skygpu_sfs_accounting).
+    ``pids[i]`` = partition of tuple i (the reference's assign_partitions), -1
+    = dropped before phase 1; ``reps`` = representative tuples (k x d)."""
+    v, i = _relation(values, ids)
+    n, d = v.shape
+    pid = np.ascontiguousarray(pids, dtype=np.int64)
+    if pid.shape != (n,):
+        raise ValueError("pids must hold one partition id per tuple")
+    r = np.ascontiguousarray(np.zeros((0, d)) if reps is None else reps, dtype=np.float64)
+    per = np.zeros(max(int(partitions), 1), dtype=np.uint64)
+    fin = np.zeros(1, dtype=np.uint64)
+    into = np.zeros(1, dtype=np.uint64)
+    pos = np.empty(max(n, 1), dtype=np.uint64)
+    cnt = np.zeros(1, dtype=np.uint64)
+    err = _errbuf()
+    _check(lib().skygpu_sfs_accounting(_p(v), _p(i), n, d, _p(pid), int(partitions), _p(r), len(r),
+                                       _p(per), _p(fin), _p(into), _p(pos), _p(cnt), err, 1024), err)
+    return Accounting(per[:int(partitions)].copy(), int(fin[0]), int(into[0]),
+                      pos[:int(cnt[0])].astype(np.int64))

@@ -18,16 +18,20 @@ pytestmark = pytest.mark.gpu
 REF = os.path.join(ROOT, "oracle", "_ref")
 ACC = os.path.join(REF, "acceptance_gpu")
 DRV = os.path.join(REF, "refdrive_gpu")
+CLI_GPU = os.path.join(REF, "skypar_gpu")
+CLI_REF = os.path.join(REF, "skypar_ref")
+FIXTURES = os.path.join(REF, "fixtures")
 
-# criteria that compare results (bit-exact parity); 8 and 10 compare the
-# reference's own SFS dominance-test COUNTS (a different algorithm executes
-# different tests — SURVEY.md §8(f) rank 2), 9 needs the CLI binary.
-RESULT_CRITERIA = {1, 2, 3, 4, 5, 6, 7}
+# every criterion: 1-7 compare results, 8 and 10 the reference's own SFS
+# dominance-test counts (exact accounting, csrc/accounting.cu), 9 runs the
+# skypar CLI front-end built over the drop-in (adapter/skypar_cli.cpp)
+RESULT_CRITERIA = set(range(1, 11))
 
 
 @pytest.mark.skipif(not os.path.exists(ACC), reason="drop-in binaries not built (needs /root/reference)")
-def test_reference_acceptance_suite_through_gpu_adapter():
-    r = subprocess.run([ACC], capture_output=True, text=True, timeout=1500)
+def test_reference_acceptance_suite_through_gpu_adapter(tmp_path):
+    r = subprocess.run([ACC, "--cli", CLI_GPU, "--fixtures", FIXTURES], capture_output=True,
+                       text=True, timeout=1500, cwd=tmp_path)
     lines = [l for l in r.stdout.splitlines() if l.startswith("[")]
     status = {}
     for l in lines:
@@ -57,3 +61,36 @@ def test_reference_driver_through_gpu_adapter(name):
     den = dict((a, b) for a, b in out["den"])
     assert [den[i] for i in g["skyline_ids"]] == g["den"]
     assert out["rows"] == g["rows"]
+
+
+CLI_CASES = [
+    "--gen ant --n 2000 --d 3 --seed 9 --strategy sliced --partitions 8 --cores 4 --repeat 2 "
+    "--mode gres --format csv",
+    "--gen uni --n 1500 --d 2 --seed 3 --strategy angular --partitions 4 --cores 2 --mode skyline "
+    "--format jsonl",
+    "--dataset {fx}/anticorrelated_wide.csv --normalize --strategy grid --partitions 4 --cores 2 "
+    "--oracle --format csv",
+    "--dataset {fx}/correlated_small.csv --strategy sliced --partitions 3 --cap 10",
+    "--gen ant --n 5000 --d 4 --seed 5 --strategy none,grid,angular,sliced --partitions 16 "
+    "--reps 0,3 --cores 4 --format jsonl",
+    "--gen uni --n 20000 --d 5 --seed 2 --strategy grid,sliced --partitions 32 --reps 10 --cores 8",
+    "--gen ant --n 50000 --d 3 --seed 1 --strategy angular --partitions 16 --cores 16",
+]
+
+
+@pytest.mark.skipif(not (os.path.exists(CLI_GPU) and os.path.exists(CLI_REF)),
+                    reason="CLI binaries not built (needs /root/reference)")
+@pytest.mark.parametrize("case", range(len(CLI_CASES)))
+def test_cli_reports_byte_identical_to_reference(case, tmp_path):
+    """skypar CLI over the GPU drop-in vs over the CPU reference library: the
+    report files (results AND the exact dominance-test accounting) are
+    byte-identical."""
+    args = CLI_CASES[case].format(fx=FIXTURES).split()
+    outs = []
+    for exe in (CLI_GPU, CLI_REF):
+        out = tmp_path / (os.path.basename(exe) + ".out")
+        r = subprocess.run([exe, *args, "--out", str(out)], capture_output=True, text=True,
+                           timeout=1200)
+        assert r.returncode == 0, r.stderr
+        outs.append(out.read_bytes())
+    assert outs[0] == outs[1]

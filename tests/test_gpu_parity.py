@@ -222,3 +222,62 @@ def test_grid_engine_auto_on_large_skyline(n):
     b = sk.pipeline(v, cap=25, skip_gres=True, sky_engine=sk.SKY_ROUNDS)
     assert b.stats["sky_engine"] == sk.SKY_ROUNDS
     assert a.positions.tolist() == b.positions.tolist()
+
+
+# ------------------------------------------------ exact reference accounting
+def _oracle_accounting(v, ids, pids, p, reps):
+    """The reference's counters restated with the oracle's SFS
+    (core.cpp:48-73) and filter (partition.cpp:287-302) semantics."""
+    per = np.zeros(p, dtype=np.int64)
+    local = []
+    for g in range(p):
+        idx = np.flatnonzero(pids == g)
+        keep = []
+        for i in idx:
+            k = 0
+            dom = False
+            for r in (reps if reps is not None else []):
+                k += 1
+                if np.all(r <= v[i]) and np.any(r < v[i]):
+                    dom = True
+                    break
+            per[g] += k
+            if not dom:
+                keep.append(i)
+        keep = np.array(keep, dtype=np.int64)
+        if len(keep):
+            pos, t = po.skyline_sfs(v[keep], ids[keep])
+            per[g] += t
+            local.extend(keep[pos].tolist())
+    local = np.array(local, dtype=np.int64)
+    pos, fin = po.skyline_sfs(v[local], ids[local]) if len(local) else (np.zeros(0, np.int64), 0)
+    return per, fin, len(local), local[pos] if len(local) else local
+
+
+@pytest.mark.parametrize("gen,n,d,p,seed,nreps", [
+    ("ant", 3000, 3, 1, 1, 0), ("ant", 4000, 3, 8, 2, 0), ("uni", 5000, 4, 5, 3, 0),
+    ("lattice", 3000, 3, 4, 4, 0), ("ant", 2000, 5, 6, 5, 3), ("uni", 2000, 2, 3, 6, 10)])
+def test_sfs_accounting_matches_reference_counters(gen, n, d, p, seed, nreps):
+    v = sk.generate(gen, n, d, seed)
+    rng = np.random.default_rng(seed)
+    ids = rng.permutation(10 * n)[:n].astype(np.int64)
+    pids = rng.integers(-1, p, n).astype(np.int64)  # -1 = dropped before phase 1
+    reps = None
+    if nreps:
+        order = np.lexsort((ids, v.sum(axis=1)))
+        reps = v[order[:nreps]]
+    got = sk.sfs_accounting(v, ids, pids, p, reps)
+    per, fin, into, pos = _oracle_accounting(v, ids, pids, p, reps)
+    assert got.per_partition.tolist() == per.tolist()
+    assert got.final_tests == fin
+    assert got.into_final == into
+    assert got.positions.tolist() == pos.tolist()
+
+
+def test_sfs_accounting_anti_diagonal_kat():
+    # proj/tests/test_core.cpp:116-133: n mutually incomparable tuples -> n(n-1)/2
+    n = 64
+    v = np.array([[i, n - 1 - i] for i in range(n)], dtype=np.float64)
+    got = sk.sfs_accounting(v, np.arange(n), np.zeros(n, dtype=np.int64), 1)
+    assert got.per_partition.tolist() == [n * (n - 1) // 2]
+    assert got.final_tests == n * (n - 1) // 2 and len(got.positions) == n
