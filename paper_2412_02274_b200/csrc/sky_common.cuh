@@ -90,7 +90,8 @@ enum Slot {
     S_C1 = 13,         // prefix size
     S_C2 = 14,         // new skyline tuples of the round
     S_C3 = 15,         // survivors of the round
-    S_COUNT_ = 16
+    S_GATE = 16,       // 1: the first round asks for the rank-grid engine (K5 skipped)
+    S_COUNT_ = 17
 };
 
 struct Ctx {

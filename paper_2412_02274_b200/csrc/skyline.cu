@@ -45,6 +45,22 @@ constexpr int kCTAItems = 16;
 constexpr uint32_t kCTACap = 1024 * kCTAItems;  // single-CTA helpers up to 16384 items
 constexpr uint32_t kMaxCells = 4096;
 
+// in-place exclusive scan of a 4096-entry shared-memory table by a
+// 1024-thread block (4 entries per thread); returns the total
+__device__ __forceinline__ uint32_t block_exclusive_scan_4096(uint32_t* tab) {
+    using Scan = cub::BlockScan<uint32_t, 1024>;
+    __shared__ typename Scan::TempStorage tmp;
+    uint32_t x[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) x[j] = tab[threadIdx.x * 4 + j];
+    uint32_t total = 0;
+    Scan(tmp).ExclusiveSum(x, x, total);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) tab[threadIdx.x * 4 + j] = x[j];
+    __syncthreads();
+    return total;
+}
+
 template <class F>
 void dispatch_d(int d, F&& f) {
     switch (d) {
@@ -491,7 +507,7 @@ k_cell_order(const double* __restrict__ v, int d, const uint32_t* __restrict__ i
     const int dd = D > 0 ? D : d;
     const uint32_t m = count ? (uint32_t)*count : mcap;
     __shared__ uint32_t cnt[kMaxCells];
-    for (uint32_t c = threadIdx.x; c < ncells; c += 1024) cnt[c] = 0;
+    for (uint32_t c = threadIdx.x; c < kMaxCells; c += 1024) cnt[c] = 0;
     __syncthreads();
     uint32_t cl[kCTAItems];
 #pragma unroll
@@ -509,22 +525,7 @@ k_cell_order(const double* __restrict__ v, int d, const uint32_t* __restrict__ i
         }
     }
     __syncthreads();
-    if (threadIdx.x < 32) {  // exclusive scan of the cell counts by one warp
-        uint32_t carry = 0;
-        for (uint32_t base = 0; base < ncells; base += 32) {
-            const uint32_t c = base + threadIdx.x;
-            const uint32_t x = c < ncells ? cnt[c] : 0;
-            uint32_t incl = x;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-                if ((int)threadIdx.x >= o) incl += y;
-            }
-            if (c < ncells) cnt[c] = carry + incl - x;
-            carry += __shfl_sync(0xffffffffu, incl, 31);
-        }
-    }
-    __syncthreads();
+    block_exclusive_scan_4096(cnt);
 #pragma unroll
     for (int j = 0; j < kCTAItems; ++j) {
         const uint32_t i = threadIdx.x + j * 1024;
@@ -628,8 +629,8 @@ __global__ void __launch_bounds__(1024)
 k_bucket_order(const uint32_t* __restrict__ in, uint32_t m, const unsigned long long* __restrict__ key,
                unsigned long long kmin, int shift, uint32_t* __restrict__ out,
                uint32_t* __restrict__ bstart) {
-    __shared__ uint32_t cnt[kKeyBuckets + 1];
-    for (uint32_t b = threadIdx.x; b <= kKeyBuckets; b += 1024) cnt[b] = 0;
+    __shared__ uint32_t cnt[kKeyBuckets];
+    for (uint32_t b = threadIdx.x; b < kKeyBuckets; b += 1024) cnt[b] = 0;
     __syncthreads();
     uint32_t bk[kCTAItems];
 #pragma unroll
@@ -643,24 +644,10 @@ k_bucket_order(const uint32_t* __restrict__ in, uint32_t m, const unsigned long 
         }
     }
     __syncthreads();
-    if (threadIdx.x < 32) {  // exclusive scan of the bucket counts by one warp
-        uint32_t carry = 0;
-        for (uint32_t base = 0; base < kKeyBuckets; base += 32) {
-            const uint32_t b = base + threadIdx.x;
-            const uint32_t x = cnt[b];
-            uint32_t incl = x;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-                if ((int)threadIdx.x >= o) incl += y;
-            }
-            cnt[b] = carry + incl - x;
-            bstart[b] = carry + incl - x;
-            carry += __shfl_sync(0xffffffffu, incl, 31);
-        }
-        if (threadIdx.x == 0) bstart[kKeyBuckets] = carry;
-    }
-    __syncthreads();
+    const uint32_t total = block_exclusive_scan_4096(cnt);
+    for (uint32_t b = threadIdx.x; b < kKeyBuckets; b += 1024) bstart[b] = cnt[b];
+    if (threadIdx.x == 0) bstart[kKeyBuckets] = total;
+    __syncthreads();  // bstart read cnt before the scatter below bumps it
 #pragma unroll
     for (int j = 0; j < kCTAItems; ++j) {
         const uint32_t i = threadIdx.x + j * 1024;
@@ -1003,12 +990,27 @@ k_sfs_filter_q(const double* __restrict__ v, const unsigned long long* __restric
                const uint32_t* __restrict__ seg, int m, int qk,
                const unsigned long long* __restrict__ amax,
                const unsigned long long* __restrict__ slots, uint8_t* __restrict__ keep,
-               unsigned long long* __restrict__ tests, uint32_t bs) {
+               unsigned long long* __restrict__ tests, uint32_t bs,
+               const uint32_t* __restrict__ Ppos, const int64_t* __restrict__ ids) {
+    // Ppos != nullptr: A' is a seed that need not precede every candidate
+    // (host-overlapped first part, skygpu_pipeline); a dominating comparator
+    // then also has to precede the candidate in (sum, id, position) order
+    auto precedes_pos = [&](uint32_t ps, uint32_t pt) {
+        const unsigned long long ks = key[ps], kt = key[pt];
+        if (ks != kt) return ks < kt;
+        const int64_t is = ids[ps], it = ids[pt];
+        return is < it || (is == it && ps < pt);
+    };
     constexpr int W = QW<D>::W;
     constexpr uint32_t kSolo = 32;
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    if (slots[S_GATE]) {  // the host switches to the rank-grid engine: keep all
+        for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < r; i += gridDim.x * blockDim.x)
+            keep[i] = 1;
+        return;
+    }
     const unsigned long long T = slots[S_THR];
     const uint32_t np = (uint32_t)slots[S_C2];
     double sc[D];
@@ -1049,7 +1051,7 @@ k_sfs_filter_q(const double* __restrict__ v, const unsigned long long* __restric
                     double sv[D];
 #pragma unroll
                     for (int k = 0; k < D; ++k) sv[k] = Pv[(uint64_t)k * pcap + q];
-                    if (dom_f64<D>(sv, t)) {
+                    if (dom_f64<D>(sv, t) && (!Ppos || precedes_pos(Ppos[q], p))) {
                         mykeep = false;
                         undecided = false;
                         break;
@@ -1069,6 +1071,7 @@ k_sfs_filter_q(const double* __restrict__ v, const unsigned long long* __restric
             unsigned long long tg[W];
 #pragma unroll
             for (int k = 0; k < W; ++k) tg[k] = __shfl_sync(0xffffffffu, tq[k], j) | kH16;
+            const uint32_t pj = __shfl_sync(0xffffffffu, p, j);
             bool dominated = false;
             if (qk > 0) {
                 // cells <= own, own first then descending (mixed-radix counter)
@@ -1094,7 +1097,7 @@ k_sfs_filter_q(const double* __restrict__ v, const unsigned long long* __restric
                                 double s[D];
 #pragma unroll
                                 for (int k = 0; k < D; ++k) s[k] = Pv[(uint64_t)k * pcap + q];
-                                hit = dom_f64<D>(s, tj);
+                                hit = dom_f64<D>(s, tj) && (!Ppos || precedes_pos(Ppos[q], pj));
                             }
                         }
                         if (__any_sync(0xffffffffu, hit)) {
@@ -1127,7 +1130,7 @@ k_sfs_filter_q(const double* __restrict__ v, const unsigned long long* __restric
                             double s[D];
 #pragma unroll
                             for (int k = 0; k < D; ++k) s[k] = Pv[(uint64_t)k * pcap + q];
-                            hit = dom_f64<D>(s, tj);
+                            hit = dom_f64<D>(s, tj) && (!Ppos || precedes_pos(Ppos[q], pj));
                         }
                     }
                     q += 32;
@@ -1330,6 +1333,13 @@ int cells_per_dim(uint64_t m, int d, uint32_t* ncells) {
     return mcell;
 }
 
+}  // namespace
+
+namespace {
+// first-round engine gate: most of the prefix survived -> rank-grid engine
+__global__ void k_grid_gate(unsigned long long* slots, uint64_t m) {
+    if (threadIdx.x == 0) slots[S_GATE] = slots[S_C2] * 4 > m * 3 ? 1ULL : 0ULL;
+}
 }  // namespace
 
 SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, uint64_t n, int d,
@@ -1592,60 +1602,23 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
             }
             return false;
     };
-    if (sky_engine == SKYGPU_SKY_GRID && r > 0 && sky_grid_bins(r, d)) {
-        read_slots(c, S_BAD, 11);
-        validate();
-        run_grid();
-        r = 0;
-    }
-    while (r > 0) {
-        // final round: the whole (already ordered) undecided list is the
-        // prefix — no threshold, no selection, no host synchronisation
-        if (checked && R && r <= kFinal) {
-            const uint64_t m = r;
-            c.h_slots[S_THR] = ~0ULL;
-            trace_mark(c, "sky: final round");
-            decide_prefix(R, m, /*final_round=*/true);
-            break;
-        }
-        // ---- K2: sampled threshold, K3: ordered prefix selection
-        const uint64_t w = r <= kFinal ? r : want;
-        k_sample_threshold<<<1, 1024, 0, c.stream>>>(keys, R, r, w, c.d_slots);
-        SKY_LAUNCH_CHECK();
-        reset_counts(c);
-        uint32_t* Pfull = c.buf[B_IDX0].as<uint32_t>(r);
-        trace_mark(c, "sky: score + sample threshold");
-        select_if(c, R, r, BelowThreshold{keys, c.d_slots + S_THR}, Pfull, c.d_slots + S_C1);
-        note_launch(c, 1);
-        trace_mark(c, "sky: select prefix");
-        read_slots(c, S_BAD, 11);
-        validate();
-        const uint64_t m = c.h_slots[S_C1];
-        if (m == 0) throw Error(SKYGPU_ERUNTIME, "skyline: empty prefix (internal)");
-
-        if (decide_prefix(Pfull, m, false)) break;
-        // large skyline ahead (most of the first prefix survived): decide
-        // everything at once with the rank-grid engine instead of filtering
-        if (rounds == 1 && sky_engine == 0 && r >= kGridMin && sky_grid_bins(r, d)) {
-            read_slots(c, S_C2, 1);
-            if (c.h_slots[S_C2] * 4 > m * 3) {
-                run_grid();
-                break;
-            }
-        }
-
+    // K5 over the undecided list (R, r) against A' = alist[0..m) (positions in
+    // (sum, id) order, count also in slot S_C2); seeded: A' need not precede
+    // the candidates (precedence checked per hit).  Survivors replace (R, r);
+    // returns |A'|.
+    auto filter_against = [&](const uint32_t* alist, uint64_t m, bool seeded) -> uint64_t {
         // ---- K5: filter the rest against A', A' regrouped (one-CTA counting
         // sort) by the quantile grid (exact cell pruning, default) or by the
         // plan's partition (scan order only, SKYGPU_PLAN_CELLS=1)
         // (the quantile grid is opt-in, SKYGPU_QGRID=1: its exact pruning pays
         // only when candidates survive; measured slower on C2/C4)
-        static const bool qgrid = [] {
+        static const bool qgrid_env = [] {
             const char* e = getenv("SKYGPU_QGRID");
             return e && e[0] == '1';
         }();
         uint32_t ncells = 1;
         int mcell = 0, qk = 0;
-        if (m <= kCTACap && qpre && qgrid) {
+        if (m <= kCTACap && qpre && qgrid_env) {
             // k bins per attribute: ~32 tuples per cell, k^d <= kMaxCells
             int k = (int)std::floor(std::pow(std::max(1.0, (double)m / 32.0), 1.0 / d) + 1e-9);
             k = std::max(2, std::min(k, kQMaxBins));
@@ -1656,7 +1629,7 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
                 for (int j = 0; j < d; ++j) ncells *= (uint32_t)k;
                 mcell = (kCellQuantile << 16) | k;
                 double* bounds = c.buf[B_PROJ].as<double>(kMaxDims * kQMaxBins);
-                k_qgrid_bounds<<<d, 1024, 0, c.stream>>>(d_vals, d, K + kc, c.d_slots + S_C2, k,
+                k_qgrid_bounds<<<d, 1024, 0, c.stream>>>(d_vals, d, alist, c.d_slots + S_C2, k,
                                                          bounds);
                 SKY_LAUNCH_CHECK();
                 SKY_CUDA(cudaMemcpyToSymbolAsync(c_qbounds, bounds,
@@ -1667,13 +1640,13 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
         }
         if (!qk && m <= kCTACap) mcell = scan_cell_spec(plan, m, d, qpre, &ncells);
         uint32_t* seg = nullptr;
-        const uint32_t* psrc = K + kc;
+        const uint32_t* psrc = alist;
         if (ncells > 1) {
             uint32_t* Alist = c.buf[B_GTMP1].as<uint32_t>(m);
             uint32_t* Akey = c.buf[B_GTMP0].as<uint32_t>(m);
             dispatch_d(d, [&](auto DC) {
                 constexpr int D = decltype(DC)::value;
-                k_cell_order<D><<<1, 1024, 0, c.stream>>>(d_vals, d, K + kc, (uint32_t)m,
+                k_cell_order<D><<<1, 1024, 0, c.stream>>>(d_vals, d, alist, (uint32_t)m,
                                                           c.d_slots + S_C2, mcell, ncells,
                                                           qpre ? amax : nullptr, Alist, Akey);
             });
@@ -1709,7 +1682,8 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
             if constexpr (D > 0)
                 k_sfs_filter_q<D><<<grid, kBlock, 0, c.stream>>>(
                     d_vals, keys, R, (uint32_t)r, Pv, Pq, (uint32_t)m, seg, mcell, qk, amax,
-                    c.d_slots, fkeep, c.d_slots + S_TESTS_SKY, bsf);
+                    c.d_slots, fkeep, c.d_slots + S_TESTS_SKY, bsf, seeded ? psrc : nullptr,
+                    d_ids);
             else
                 k_sfs_filter_cells<D><<<grid, kBlock, 0, c.stream>>>(
                     d_vals, d, keys, R, (uint32_t)r, Pv, (uint32_t)m, seg, mcell, c.d_slots, fkeep,
@@ -1722,17 +1696,67 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
         select_flags<uint32_t>(c, R, r, fkeep, Rnext, c.d_slots + S_C3);
         trace_mark(c, "sky: select survivors");
         kernel_launches += 1;
-        read_slots(c, S_C2, 2);  // S_C2 (A'), S_C3 (survivors)
+        read_slots(c, S_C2, 3);  // S_C2 (A'), S_C3 (survivors), S_GATE
         float ms = 0;
-        SKY_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-        kernel_ms += ms;
         SKY_CUDA(cudaEventElapsedTime(&ms, e2, e3));
         kernel_ms += ms;
-        const uint64_t a = c.h_slots[S_C2];
-        kc += a;
         r = c.h_slots[S_C3];
         R = Rnext;
         Rnext = (Rnext == Rbuf1) ? Rbuf0 : Rbuf1;
+        return (uint64_t)c.h_slots[S_C2];
+    };
+    if (sky_engine == SKYGPU_SKY_GRID && r > 0 && sky_grid_bins(r, d)) {
+        read_slots(c, S_BAD, 11);
+        validate();
+        run_grid();
+        r = 0;
+    }
+    while (r > 0) {
+        // final round: the whole (already ordered) undecided list is the
+        // prefix — no threshold, no selection, no host synchronisation
+        if (checked && R && r <= kFinal) {
+            const uint64_t m = r;
+            c.h_slots[S_THR] = ~0ULL;
+            trace_mark(c, "sky: final round");
+            decide_prefix(R, m, /*final_round=*/true);
+            break;
+        }
+        // ---- K2: sampled threshold, K3: ordered prefix selection
+        const uint64_t w = r <= kFinal ? r : want;
+        k_sample_threshold<<<1, 1024, 0, c.stream>>>(keys, R, r, w, c.d_slots);
+        SKY_LAUNCH_CHECK();
+        reset_counts(c);
+        uint32_t* Pfull = c.buf[B_IDX0].as<uint32_t>(r);
+        trace_mark(c, "sky: score + sample threshold");
+        select_if(c, R, r, BelowThreshold{keys, c.d_slots + S_THR}, Pfull, c.d_slots + S_C1);
+        note_launch(c, 1);
+        trace_mark(c, "sky: select prefix");
+        read_slots(c, S_BAD, 11);
+        validate();
+        const uint64_t m = c.h_slots[S_C1];
+        if (m == 0) throw Error(SKYGPU_ERUNTIME, "skyline: empty prefix (internal)");
+
+        if (decide_prefix(Pfull, m, false)) break;
+        // large skyline ahead (most of the first prefix survived): decide
+        // everything at once with the rank-grid engine instead of filtering.
+        // Decided on the device (no extra host round trip): the gate makes
+        // K5 keep every candidate, the host switches after K5's sync.
+        const bool gate = rounds == 1 && sky_engine == 0 && r >= kGridMin && sky_grid_bins(r, d);
+        if (gate) {
+            k_grid_gate<<<1, 32, 0, c.stream>>>(c.d_slots, m);
+            SKY_LAUNCH_CHECK();
+            note_launch(c);
+        }
+
+        const uint64_t a = filter_against(K + kc, m, false);  // synchronises
+        if (gate && c.h_slots[S_GATE]) {
+            run_grid();
+            break;
+        }
+        float ms4 = 0;
+        SKY_CUDA(cudaEventElapsedTime(&ms4, e0, e1));
+        kernel_ms += ms4;
+        kc += a;
         if (a * 2 > m) want = std::min(want * 4, kMaxPrefix);
     }
     st.sfs_rounds = rounds;
