@@ -66,6 +66,9 @@ Ctx& ctx() {
 void trace_mark(Ctx& c, const char* label) {
     if (!c.trace || c.ntrace >= 96) return;
     c.tlabel[c.ntrace] = label;
+    c.thost[c.ntrace] = std::chrono::duration<double, std::micro>(
+                            std::chrono::steady_clock::now().time_since_epoch())
+                            .count();
     SKY_CUDA(cudaEventRecord(c.tev[c.ntrace++], c.stream));
 }
 
@@ -235,7 +238,8 @@ void end_stats(Ctx& c) {
         for (int i = 1; i < c.ntrace; ++i) {
             float ms = 0;
             SKY_CUDA(cudaEventElapsedTime(&ms, c.tev[i - 1], c.tev[i]));
-            fprintf(stderr, "[skygpu trace] %8.1f us  %s\n", ms * 1e3, c.tlabel[i]);
+            fprintf(stderr, "[skygpu trace] %8.1f us  (host issue %8.1f us)  %s\n", ms * 1e3,
+                    c.thost[i] - c.thost[i - 1], c.tlabel[i]);
         }
         float tot = 0;
         SKY_CUDA(cudaEventElapsedTime(&tot, c.tev[0], c.tev[c.ntrace - 1]));
@@ -395,13 +399,14 @@ int skygpu_parallel_skyline(const double* vals, const int64_t* ids, uint64_t n, 
                                      cudaMemcpyHostToDevice, c.stream));
         }
         SkylineOut so = skyline_device(c, dv, di, n, d, pl, dr, n_reps);
-        std::vector<uint32_t> pos(so.S);
-        if (so.S)
-            SKY_CUDA(cudaMemcpyAsync(pos.data(), so.d_inpos, so.S * sizeof(uint32_t),
+        if (so.S) {
+            uint64_t* wide = c.buf[B_OUTPOS].as<uint64_t>(so.S);
+            widen_u32_u64(c, so.d_inpos, wide, so.S);
+            SKY_CUDA(cudaMemcpyAsync(out_pos, wide, so.S * sizeof(uint64_t),
                                      cudaMemcpyDeviceToHost, c.stream));
+        }
         all.stop(&c.st->ms_total);
         end_stats(c);  // final synchronisation
-        for (uint64_t k = 0; k < so.S; ++k) out_pos[k] = pos[k];
         *out_n = so.S;
     });
 }
@@ -523,21 +528,57 @@ int skygpu_pipeline(const double* vals, const int64_t* ids, uint64_t n, int d,
         Timer all(c, 0);
         const double* dv = vals;
         const int64_t* di = ids;
+        TailFeed feed;
+        // host inputs of a large relation stream in (copy stream, 4 chunks):
+        // the skyline stage decides the first chunk while the rest is in
+        // flight (SKYGPU_OVERLAP=0 disables)
+        static const bool overlap_env = [] {
+            const char* e = getenv("SKYGPU_OVERLAP");
+            return !(e && e[0] == '0');
+        }();
+        // (worth it only when the tail's copy outlasts the head's decision,
+        // ~0.5 ms: from ~48 MB of input on)
+        const bool streamed = !dev && overlap_env && n * (uint64_t)(d + 1) * 8 >= (48ull << 20) &&
+                              d <= 8 && pl.strategy != SKYGPU_GRID && !(flags & SKYGPU_SKY_GRID);
         if (!dev) {
             Timer h2d(c, 2);
             double* bv = c.buf[B_IN_VALS].as<double>(n * d);
             int64_t* bi = c.buf[B_IN_IDS].as<int64_t>(n);
-            SKY_CUDA(cudaMemcpyAsync(bv, vals, n * d * sizeof(double), cudaMemcpyHostToDevice,
-                                     c.stream));
-            SKY_CUDA(cudaMemcpyAsync(bi, ids, n * sizeof(int64_t), cudaMemcpyHostToDevice,
-                                     c.stream));
+            if (streamed) {
+                if (!c.copy) {
+                    SKY_CUDA(cudaStreamCreateWithFlags(&c.copy, cudaStreamNonBlocking));
+                    for (auto& e : c.xev) SKY_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                }
+                // the copies follow the stream's earlier work on these buffers
+                SKY_CUDA(cudaEventRecord(c.xev[9], c.stream));
+                SKY_CUDA(cudaStreamWaitEvent(c.copy, c.xev[9], 0));
+                feed.nchunks = 4;
+                for (int ch = 0; ch <= feed.nchunks; ++ch) feed.bound[ch] = n * ch / feed.nchunks;
+                for (int ch = 0; ch < feed.nchunks; ++ch) {
+                    const uint64_t lo = feed.bound[ch], cnt = feed.bound[ch + 1] - lo;
+                    SKY_CUDA(cudaMemcpyAsync(bv + lo * d, vals + lo * d, cnt * d * sizeof(double),
+                                             cudaMemcpyHostToDevice, c.copy));
+                    SKY_CUDA(cudaMemcpyAsync(bi + lo, ids + lo, cnt * sizeof(int64_t),
+                                             cudaMemcpyHostToDevice, c.copy));
+                    SKY_CUDA(cudaEventRecord(c.xev[ch], c.copy));
+                    feed.ready[ch] = c.xev[ch];
+                }
+            } else {
+                SKY_CUDA(cudaMemcpyAsync(bv, vals, n * d * sizeof(double), cudaMemcpyHostToDevice,
+                                         c.stream));
+                SKY_CUDA(cudaMemcpyAsync(bi, ids, n * sizeof(int64_t), cudaMemcpyHostToDevice,
+                                         c.stream));
+            }
             h2d.stop(&c.st->ms_h2d);
             dv = bv;
             di = bi;
         }
         Timer tsky(c, 4);
         SkylineOut so = skyline_device(c, dv, di, n, d, pl, nullptr, 0,
-                                       flags & (SKYGPU_SKY_ROUNDS | SKYGPU_SKY_GRID));
+                                       flags & (SKYGPU_SKY_ROUNDS | SKYGPU_SKY_GRID),
+                                       streamed ? &feed : nullptr);
+        if (streamed)  // the copy stream is idle again before the call returns
+            SKY_CUDA(cudaStreamWaitEvent(c.stream, c.xev[feed.nchunks - 1], 0));
         tsky.stop(&c.st->ms_skyline);
         int32_t* den = c.buf[B_DEN].as<int32_t>(so.S ? so.S : 1);
         GresOut go;
@@ -558,14 +599,16 @@ int skygpu_pipeline(const double* vals, const int64_t* ids, uint64_t n, int d,
                 widen_u32_u64(c, so.d_inpos, out_pos, so.S);
             }
         } else if (so.S) {
-            std::vector<uint32_t> pos(so.S);
-            SKY_CUDA(cudaMemcpyAsync(pos.data(), so.d_inpos, so.S * sizeof(uint32_t),
+            // positions widened on the device, copied straight into the
+            // caller's buffer (no host-side staging or conversion loop)
+            uint64_t* wide = c.buf[B_OUTPOS].as<uint64_t>(so.S);
+            widen_u32_u64(c, so.d_inpos, wide, so.S);
+            SKY_CUDA(cudaMemcpyAsync(out_pos, wide, so.S * sizeof(uint64_t),
                                      cudaMemcpyDeviceToHost, c.stream));
             if (!(flags & SKYGPU_SKIP_GRES))
                 SKY_CUDA(cudaMemcpyAsync(out_den, den, so.S * sizeof(int32_t),
                                          cudaMemcpyDeviceToHost, c.stream));
             SKY_CUDA(cudaStreamSynchronize(c.stream));
-            for (uint64_t k = 0; k < so.S; ++k) out_pos[k] = pos[k];
         }
         d2h.stop(&c.st->ms_d2h);
         all.stop(&c.st->ms_total);

@@ -69,7 +69,7 @@ enum BufId {
     B_DEN, B_GTMP0, B_GTMP1, B_OUTPOS, B_PROJ, B_REPS, B_MISC, B_CELLS, B_CSUM,
     B_ORDER, B_AMAX, B_AQ, B_PQ, B_GCODE, B_GCELL, B_GSCODE, B_GSIDX, B_GITEMS, B_GCNT,
     B_ACC0, B_ACC1, B_ACC2, B_ACC3, B_ACC4, B_ACC5, B_ACC6, B_ACC7, B_ACC8, B_ACC9, B_ACC10,
-    B_ACC11, B_ACC12, B_ACC13, B_ACC14, B_ACC15, B_ACC16, B_COUNT
+    B_ACC11, B_ACC12, B_ACC13, B_ACC14, B_ACC15, B_ACC16, B_SEED, B_AMAX2, B_IOTA, B_COUNT
 };
 
 // Device-side scalar slots (one small allocation, read back through pinned memory).
@@ -110,8 +110,11 @@ struct Ctx {
     // printed to stderr at the end of the call
     bool trace = false;
     int ntrace = 0;
+    cudaStream_t copy = nullptr;  // H2D of streamed pipeline inputs
+    cudaEvent_t xev[10];          // chunk-ready events of the streamed input
     cudaEvent_t tev[96];
     const char* tlabel[96];
+    double thost[96];  // host clock at each mark (us): where the GPU waits for the CPU
 };
 
 // record a labelled device timestamp when tracing is on
@@ -198,10 +201,20 @@ struct SkylineOut {
 };
 
 // Skyline of n tuples already resident on the device (AoS vals, ids).
+// Input still arriving (host-pointer pipeline): chunk ch = positions
+// [bound[ch], bound[ch+1]) is on the device once ready[ch] has fired.
+// Chunk 0 (the head) is decided first while the rest is in flight; its
+// skyline then filters every later chunk as it lands (skyline.cu).
+struct TailFeed {
+    int nchunks = 0;
+    uint64_t bound[9] = {};
+    cudaEvent_t ready[8] = {};
+};
+
 // sky_engine: 0 auto, SKYGPU_SKY_ROUNDS or SKYGPU_SKY_GRID (skygpu.h flags)
 SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, uint64_t n, int d,
                           const skygpu_plan& plan, const double* d_reps, uint64_t n_reps,
-                          unsigned sky_engine = 0);
+                          unsigned sky_engine = 0, const TailFeed* feed = nullptr);
 
 // skyline_grid.cu: the one-pass rank-grid engine for large skylines.
 // sky_grid_bins = bins per attribute for r tuples (0: shape unsupported, d > 8);

@@ -84,7 +84,7 @@ template <int D>
 __global__ void k_score(const double* __restrict__ v, uint64_t n, int d,
                         unsigned long long* __restrict__ key,
                         unsigned long long* __restrict__ slots,
-                        unsigned long long* __restrict__ amax) {
+                        unsigned long long* __restrict__ amax, uint64_t base = 0) {
     constexpr int DA = D > 0 ? D : 1;
     unsigned long long mn = ~0ULL, mx = 0;
     unsigned long long am[DA];
@@ -114,7 +114,7 @@ __global__ void k_score(const double* __restrict__ v, uint64_t n, int d,
         key[i] = b;
         mn = b < mn ? b : mn;
         mx = b > mx ? b : mx;
-        if (bad) atomicMin(&slots[S_BAD], static_cast<unsigned long long>(i));
+        if (bad) atomicMin(&slots[S_BAD], static_cast<unsigned long long>(base + i));
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -1340,17 +1340,67 @@ namespace {
 __global__ void k_grid_gate(unsigned long long* slots, uint64_t m) {
     if (threadIdx.x == 0) slots[S_GATE] = slots[S_C2] * 4 > m * 3 ? 1ULL : 0ULL;
 }
+// streamed input: seeded K5 state (no decided prefix, |A'| = the seed)
+__global__ void k_seed_slots(unsigned long long* slots, uint64_t nseed) {
+    if (threadIdx.x == 0) {
+        slots[S_THR] = 0;
+        slots[S_C2] = nseed;
+    }
+}
+__global__ void k_iota(uint32_t* __restrict__ a, uint64_t n) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        a[i] = (uint32_t)i;
+}
+__global__ void k_mark_u8(uint8_t* __restrict__ f, const uint32_t* __restrict__ at, uint64_t m) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        f[at[i]] = 1;
+}
 }  // namespace
 
 SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, uint64_t n, int d,
                           const skygpu_plan& plan, const double* d_reps, uint64_t n_reps,
-                          unsigned sky_engine) {
+                          unsigned sky_engine, const TailFeed* feed) {
     SkylineOut out;
     skygpu_stats& st = *c.st;
-    st.tuples_in = n;
     if (n == 0) return out;
     if (n >= 0xFFFFFFFFull) invalid("parallel_skyline: more than 2^32-1 tuples");
     const unsigned gb = grid_for(n, kBlock);
+    // ---- streamed input: decide the head while the rest is still in flight
+    uint32_t* seed = nullptr;
+    uint64_t nseed = 0;
+    unsigned long long* scale_snap = nullptr;
+    if (feed) {
+        SKY_CUDA(cudaStreamWaitEvent(c.stream, feed->ready[0], 0));
+        const bool eligible = d >= 1 && d <= 8 && plan.strategy != SKYGPU_GRID && n_reps == 0 &&
+                              sky_engine != SKYGPU_SKY_GRID && feed->nchunks >= 2;
+        if (eligible) {
+            try {
+                const SkylineOut h = skyline_device(c, d_vals, d_ids, feed->bound[1], d, plan,
+                                                    nullptr, 0, 0, nullptr);
+                if (h.S > 0 && h.S <= kCTACap) {
+                    seed = c.buf[B_SEED].as<uint32_t>(h.S);
+                    scale_snap = c.buf[B_AMAX2].as<unsigned long long>(kMaxDims);
+                    SKY_CUDA(cudaMemcpyAsync(seed, h.d_inpos, h.S * sizeof(uint32_t),
+                                             cudaMemcpyDeviceToDevice, c.stream));
+                    SKY_CUDA(cudaMemcpyAsync(scale_snap, c.buf[B_AMAX].p,
+                                             sizeof(unsigned long long) * kMaxDims,
+                                             cudaMemcpyDeviceToDevice, c.stream));
+                    nseed = h.S;
+                }
+            } catch (const Error&) {
+                // the full pass below reports the reference's error
+            }
+        }
+        if (!nseed) {
+            for (int ch = 1; ch < feed->nchunks; ++ch)
+                SKY_CUDA(cudaStreamWaitEvent(c.stream, feed->ready[ch], 0));
+            feed = nullptr;
+        }
+        trace_mark(c, "sky: streamed head decided");
+    }
+    st.tuples_in = n;
 
     zero_slots(c);
     auto* keys = c.buf[B_KEY0].as<unsigned long long>(n);
@@ -1359,15 +1409,17 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
     const bool qpre = d >= 1 && d <= 8;
     unsigned long long* amax = c.buf[B_AMAX].as<unsigned long long>(kMaxDims);
     SKY_CUDA(cudaMemsetAsync(amax, 0, sizeof(unsigned long long) * kMaxDims, c.stream));
-    dispatch_d(d, [&](auto DC) {
-        constexpr int D = decltype(DC)::value;
-        k_score<D><<<grid_for(n, kBlock, c.num_sms * 8), kBlock, 0, c.stream>>>(
-            d_vals, n, d, keys, c.d_slots, amax);
-    });
-    SKY_LAUNCH_CHECK();
-    k_ids_check<<<gb, kBlock, 0, c.stream>>>(d_ids, n, c.d_slots);
-    SKY_LAUNCH_CHECK();
-    note_launch(c, 2);
+    if (!feed) {  // (streamed input: per chunk, below)
+        dispatch_d(d, [&](auto DC) {
+            constexpr int D = decltype(DC)::value;
+            k_score<D><<<grid_for(n, kBlock, c.num_sms * 8), kBlock, 0, c.stream>>>(
+                d_vals, n, d, keys, c.d_slots, amax);
+        });
+        SKY_LAUNCH_CHECK();
+        k_ids_check<<<gb, kBlock, 0, c.stream>>>(d_ids, n, c.d_slots);
+        SKY_LAUNCH_CHECK();
+        note_launch(c, 2);
+    }
     if (plan.strategy == SKYGPU_GRID) {
         k_grid_range<<<grid_for(n * d, kBlock), kBlock, 0, c.stream>>>(d_vals, n * d, c.d_slots);
         SKY_LAUNCH_CHECK();
@@ -1606,7 +1658,19 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
     // (sum, id) order, count also in slot S_C2); seeded: A' need not precede
     // the candidates (precedence checked per hit).  Survivors replace (R, r);
     // returns |A'|.
-    auto filter_against = [&](const uint32_t* alist, uint64_t m, bool seeded) -> uint64_t {
+    struct AScan {
+        uint32_t* seg = nullptr;
+        int mcell = 0, qk = 0;
+        const uint32_t* psrc = nullptr;
+        double* Pv = nullptr;
+        unsigned long long* Pq = nullptr;
+        uint64_t m = 0;
+    };
+    // A' = alist[0..m) (count also in slot S_C2) regrouped by cells, values
+    // and quantised codes gathered (codes scaled by `scale`, the per-attribute
+    // maxima every candidate code of the same K5 must use)
+    auto prep_aprime = [&](const uint32_t* alist, uint64_t m,
+                           const unsigned long long* scale) -> AScan {
         // ---- K5: filter the rest against A', A' regrouped (one-CTA counting
         // sort) by the quantile grid (exact cell pruning, default) or by the
         // plan's partition (scan order only, SKYGPU_PLAN_CELLS=1)
@@ -1616,6 +1680,8 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
             const char* e = getenv("SKYGPU_QGRID");
             return e && e[0] == '1';
         }();
+        AScan A;
+        A.m = m;
         uint32_t ncells = 1;
         int mcell = 0, qk = 0;
         if (m <= kCTACap && qpre && qgrid_env) {
@@ -1648,7 +1714,7 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
                 constexpr int D = decltype(DC)::value;
                 k_cell_order<D><<<1, 1024, 0, c.stream>>>(d_vals, d, alist, (uint32_t)m,
                                                           c.d_slots + S_C2, mcell, ncells,
-                                                          qpre ? amax : nullptr, Alist, Akey);
+                                                          qpre ? scale : nullptr, Alist, Akey);
             });
             SKY_LAUNCH_CHECK();
             seg = seg_table;
@@ -1664,34 +1730,50 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
             constexpr int D = decltype(DC)::value;
             if constexpr (D > 0)
                 k_gather_q<D><<<grid_for(m, kBlock), kBlock, 0, c.stream>>>(
-                    d_vals, psrc, m, c.d_slots + S_C2, amax, Pv, Pq);
+                    d_vals, psrc, m, c.d_slots + S_C2, scale, Pv, Pq);
             else
                 k_gather_aos<<<grid_for(m * d, kBlock), kBlock, 0, c.stream>>>(
                     d_vals, d, psrc, m, c.d_slots + S_C2, Pv);
         });
         SKY_LAUNCH_CHECK();
         note_launch(c);
-        const uint32_t bsf = batch_size(c, r);
-        const uint64_t wf = std::min<uint64_t>((r + bsf - 1) / bsf, (uint64_t)c.num_sms * 64);
-        uint8_t* fkeep = c.buf[B_SV].as<uint8_t>(r);
-        trace_mark(c, "sky: select A' + segments + gather Pv");
-        SKY_CUDA(cudaEventRecord(e2, c.stream));
+        A.seg = seg;
+        A.mcell = mcell;
+        A.qk = qk;
+        A.psrc = psrc;
+        A.Pv = Pv;
+        A.Pq = Pq;
+        return A;
+    };
+    // K5 launch: candidates Rl[0..rl) (nullptr: positions 0..rl), keep flags
+    // into fkeep[0..rl); seeded = A' need not precede them (checked per hit)
+    auto launch_k5 = [&](const AScan& A, const uint32_t* Rl, uint64_t rl, uint8_t* fkeep,
+                         bool seeded, const unsigned long long* scale) {
+        const uint32_t bsf = batch_size(c, rl);
+        const uint64_t wf = std::min<uint64_t>((rl + bsf - 1) / bsf, (uint64_t)c.num_sms * 64);
         dispatch_d(d, [&](auto DC) {
             constexpr int D = decltype(DC)::value;
             const unsigned grid = (unsigned)((wf * 32 + kBlock - 1) / kBlock);
             if constexpr (D > 0)
                 k_sfs_filter_q<D><<<grid, kBlock, 0, c.stream>>>(
-                    d_vals, keys, R, (uint32_t)r, Pv, Pq, (uint32_t)m, seg, mcell, qk, amax,
-                    c.d_slots, fkeep, c.d_slots + S_TESTS_SKY, bsf, seeded ? psrc : nullptr,
-                    d_ids);
+                    d_vals, keys, Rl, (uint32_t)rl, A.Pv, A.Pq, (uint32_t)A.m, A.seg, A.mcell,
+                    A.qk, scale, c.d_slots, fkeep, c.d_slots + S_TESTS_SKY, bsf,
+                    seeded ? A.psrc : nullptr, d_ids);
             else
                 k_sfs_filter_cells<D><<<grid, kBlock, 0, c.stream>>>(
-                    d_vals, d, keys, R, (uint32_t)r, Pv, (uint32_t)m, seg, mcell, c.d_slots, fkeep,
-                    c.d_slots + S_TESTS_SKY, bsf);
+                    d_vals, d, keys, Rl, (uint32_t)rl, A.Pv, (uint32_t)A.m, A.seg, A.mcell,
+                    c.d_slots, fkeep, c.d_slots + S_TESTS_SKY, bsf);
         });
-        SKY_CUDA(cudaEventRecord(e3, c.stream));
         SKY_LAUNCH_CHECK();
         note_launch(c);
+    };
+    auto filter_against = [&](const uint32_t* alist, uint64_t m, bool seeded) -> uint64_t {
+        const AScan A = prep_aprime(alist, m, amax);
+        uint8_t* fkeep = c.buf[B_SV].as<uint8_t>(r);
+        trace_mark(c, "sky: select A' + segments + gather Pv");
+        SKY_CUDA(cudaEventRecord(e2, c.stream));
+        launch_k5(A, R, r, fkeep, seeded, amax);
+        SKY_CUDA(cudaEventRecord(e3, c.stream));
         trace_mark(c, "sky: K5 filter kernel");
         select_flags<uint32_t>(c, R, r, fkeep, Rnext, c.d_slots + S_C3);
         trace_mark(c, "sky: select survivors");
@@ -1705,6 +1787,44 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
         Rnext = (Rnext == Rbuf1) ? Rbuf0 : Rbuf1;
         return (uint64_t)c.h_slots[S_C2];
     };
+    if (feed) {
+        // every chunk scored as it lands and filtered against the head's
+        // skyline (seeded K5, precedence checked per hit); the head's own
+        // non-skyline tuples are dominated inside the head.  Survivors (the
+        // head skyline included) form the undecided list of the rounds.
+        k_seed_slots<<<1, 32, 0, c.stream>>>(c.d_slots, nseed);
+        SKY_LAUNCH_CHECK();
+        const AScan A = prep_aprime(seed, nseed, scale_snap);
+        uint8_t* flags = c.buf[B_FLAGS].as<uint8_t>(n);
+        uint32_t* iota = c.buf[B_IOTA].as<uint32_t>(n);
+        k_iota<<<grid_for(n, kBlock), kBlock, 0, c.stream>>>(iota, n);
+        SKY_CUDA(cudaMemsetAsync(flags, 0, feed->bound[1], c.stream));
+        k_mark_u8<<<grid_for(nseed, kBlock), kBlock, 0, c.stream>>>(flags, seed, nseed);
+        SKY_LAUNCH_CHECK();
+        note_launch(c, 3);
+        for (int ch = 0; ch < feed->nchunks; ++ch) {
+            const uint64_t lo = feed->bound[ch], hi = feed->bound[ch + 1];
+            if (ch > 0) SKY_CUDA(cudaStreamWaitEvent(c.stream, feed->ready[ch], 0));
+            dispatch_d(d, [&](auto DC) {
+                constexpr int D = decltype(DC)::value;
+                k_score<D><<<grid_for(hi - lo, kBlock, c.num_sms * 8), kBlock, 0, c.stream>>>(
+                    d_vals + lo * d, hi - lo, d, keys + lo, c.d_slots, amax, lo);
+            });
+            const uint64_t c0 = ch ? lo - 1 : 0;  // pair (lo-1, lo) spans the boundary
+            k_ids_check<<<grid_for(hi - c0, kBlock), kBlock, 0, c.stream>>>(d_ids + c0, hi - c0,
+                                                                           c.d_slots);
+            SKY_LAUNCH_CHECK();
+            note_launch(c, 2);
+            if (ch > 0) launch_k5(A, iota + lo, hi - lo, flags + lo, true, scale_snap);
+        }
+        trace_mark(c, "sky: streamed chunks filtered");
+        select_flags<uint32_t>(c, nullptr, n, flags, Rbuf0, c.d_slots + S_C3);
+        read_slots(c, S_BAD, 11);
+        validate();
+        R = Rbuf0;
+        r = c.h_slots[S_C3];
+        st.tuples_into_parallel = r;
+    }
     if (sky_engine == SKYGPU_SKY_GRID && r > 0 && sky_grid_bins(r, d)) {
         read_slots(c, S_BAD, 11);
         validate();

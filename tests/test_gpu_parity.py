@@ -281,3 +281,51 @@ def test_sfs_accounting_anti_diagonal_kat():
     got = sk.sfs_accounting(v, np.arange(n), np.zeros(n, dtype=np.int64), 1)
     assert got.per_partition.tolist() == [n * (n - 1) // 2]
     assert got.final_tests == n * (n - 1) // 2 and len(got.positions) == n
+
+
+# ------------------------------------------------ streamed host input (H2D overlap)
+def _host_vs_device(v, ids, plan=None, cap=25):
+    """pipeline() from host arrays (>= 48 MB of input: the streamed, chunk-
+    overlapped path) vs the same call on device pointers (one-shot path)."""
+    import torch
+    host = sk.pipeline(v, ids, plan, cap=cap)
+    n, d = v.shape
+    dv = torch.from_numpy(np.ascontiguousarray(v)).cuda()
+    di = torch.from_numpy(np.ascontiguousarray(ids)).cuda()
+    pos = torch.empty(n, dtype=torch.int64, device="cuda")
+    den = torch.empty(n, dtype=torch.int32, device="cuda")
+    from paper_2412_02274_b200 import skypar
+    S, gm, _ = skypar.pipeline_raw(dv.data_ptr(), di.data_ptr(), n, d,
+                                   plan or sk.make_plan("none", 1, d), cap, 0, 0, 1,
+                                   skypar.DEVICE_PTRS, pos.data_ptr(), den.data_ptr())
+    torch.cuda.synchronize()
+    assert host.positions.tolist() == pos[:S].cpu().tolist()
+    assert host.g_max == gm and host.den.tolist() == den[:S].cpu().tolist()
+    return host
+
+
+@pytest.mark.parametrize("gen,n,d,seed", [("ant", 2_000_000, 3, 3), ("uni", 1_500_000, 5, 4),
+                                          ("corr", 1_600_000, 4, 5), ("lattice", 2_000_000, 3, 6)])
+def test_streamed_host_input_matches_device_path(gen, n, d, seed):
+    v = sk.generate(gen, n, d, seed)
+    rng = np.random.default_rng(seed)
+    ids = rng.permutation(3 * n)[:n].astype(np.int64)  # unsorted ids: (sum, id) ties matter
+    res = _host_vs_device(v, ids)
+    pos, _ = po.skyline_sfs(v, ids)
+    assert res.positions.tolist() == pos.tolist()
+
+
+def test_streamed_fp_tie_across_chunks():
+    """A head tuple dominating a tail tuple of EQUAL sum but larger id does
+    not precede it: the reference keeps both."""
+    n = 2_100_000
+    rng = np.random.default_rng(9)
+    v = 2.0 + rng.random((n, 2))           # filler, dominated by the pair below
+    v[0] = [1e-20, 1.0]                    # head: dominates t, same sum 1.0
+    v[n - 1] = [2e-20, 1.0]                # tail
+    ids = np.arange(n, dtype=np.int64) + 10
+    ids[0], ids[n - 1] = 9, 5              # t has the smaller id -> t first
+    res = _host_vs_device(v, ids)
+    pos, _ = po.skyline_sfs(v, ids)
+    assert res.positions.tolist() == pos.tolist()
+    assert sorted(res.positions.tolist()) == [0, n - 1]
