@@ -408,6 +408,13 @@ def roofline(st, sky_ms, gres_ms, d, clk, workload="C2"):
                 i_test, pipe = (4 if d <= 4 else 8), "alu"
             else:
                 i_test, pipe = 2 * d, "fp64"
+        elif d <= 8:
+            # 16-bit quantised SWAR prefilter (one u64 word per 4 attributes):
+            # IADD3, IADD3.X, 2 LOP3, 2 ISETP per word on the ALU pipe; the
+            # exact float64 test runs only on a code pass
+            kern = "k_sfs_intra_chunked+k_sfs_filter_q"
+            tests, ms, launches = st["skyline_tests"], sky_ms, st["sky_kernel_launches"]
+            i_test, pipe = 6 * (1 if d <= 4 else 2), "alu"
         else:
             kern = "k_sfs_intra_sorted+k_sfs_filter_cells"
             tests, ms, launches = st["skyline_tests"], sky_ms, st["sky_kernel_launches"]

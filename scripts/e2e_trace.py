@@ -21,3 +21,18 @@ for i in range(6):
     skypar.pipeline_raw(pv.data_ptr(), pi.data_ptr(), n, d, plan, 25, 0, 0, 1, 0, pos.data_ptr(),
                         den.data_ptr())
     print(f"call {i}: {1e3 * (time.perf_counter() - t0):.3f} ms", file=sys.stderr, flush=True)
+flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+for mode in ("flush+sync", "sync only", "sleep 1ms"):
+    ts = []
+    for i in range(10):
+        if mode == "flush+sync":
+            flush.zero_()
+        torch.cuda.synchronize()
+        if mode == "sleep 1ms":
+            time.sleep(0.001)
+        t0 = time.perf_counter()
+        skypar.pipeline_raw(pv.data_ptr(), pi.data_ptr(), n, d, plan, 25, 0, 0, 1, 0, pos.data_ptr(),
+                            den.data_ptr())
+        ts.append(1e3 * (time.perf_counter() - t0))
+    ts.sort()
+    print(f"{mode}: median {ts[5]:.3f} ms min {ts[0]:.3f}", file=sys.stderr, flush=True)
