@@ -21,6 +21,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 #include <vector>
 
 #include "sky_common.cuh"
@@ -206,6 +207,61 @@ __global__ void k_cells_query(const double* __restrict__ v, uint64_t S, CellGeom
     if ((threadIdx.x & 31) == 0 && left) atomicAdd(undecided, left);
 }
 
+// ---- packed-code variants: the codes floor(v*g) of every step computed
+// once (one byte per attribute, codes <= 127 on this engine's path), so each
+// step reads S code words instead of S x d float64 values, twice
+template <class CW>
+__global__ void k_cells_codes(const double* __restrict__ v, uint64_t S, int d, int g_hi, int G,
+                              CW* __restrict__ codes) {
+    const uint64_t total = S * (uint64_t)G;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t gi = i / S, t = i - gi * S;
+        const double gd = (double)(g_hi - (int)gi);
+        CW w = 0;
+        for (int k = 0; k < d; ++k)
+            w |= (CW)(unsigned)floor(__dmul_rn(v[(uint64_t)k * S + t], gd)) << (8 * k);
+        codes[i] = w;
+    }
+}
+
+template <class W, class CW>
+__global__ void k_cells_mark_c(const CW* __restrict__ code, uint64_t S, CellGeom geo,
+                               W* __restrict__ rows) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < S;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const CW w = code[i];
+        uint64_t r = 0;
+        for (int j = 1; j < geo.d; ++j) r += (uint64_t)((w >> (8 * j)) & 0xFF) * geo.stride[j];
+        atomicOr(&rows[r], (W)1 << (unsigned)(w & 0xFF));
+    }
+}
+
+template <class W, class CW>
+__global__ void k_cells_query_c(const CW* __restrict__ code, CellGeom geo,
+                                const W* __restrict__ P, const uint32_t* __restrict__ act,
+                                uint64_t na, int32_t* __restrict__ den,
+                                unsigned long long* __restrict__ undecided) {
+    unsigned long long left = 0;
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < na;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t t = act[k];
+        if (den[t] != 0) continue;
+        const CW w = code[t];
+        uint64_t r = 0;
+        for (int j = 1; j < geo.d; ++j) r += (uint64_t)((w >> (8 * j)) & 0xFF) * geo.stride[j];
+        const unsigned c0 = (unsigned)(w & 0xFF);
+        bool hit = c0 >= 1 && ((P[r] >> (c0 - 1)) & 1);
+        for (int j = 1; j < geo.d && !hit; ++j)
+            if (((w >> (8 * j)) & 0xFF) >= 1) hit = (P[r - geo.stride[j]] >> c0) & 1;
+        if (hit) den[t] = geo.g;
+        else ++left;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) left += __shfl_down_sync(0xffffffffu, left, o);
+    if ((threadIdx.x & 31) == 0 && left) atomicAdd(undecided, left);
+}
+
 __global__ void k_col_max(const double* __restrict__ v, uint64_t S, int d,
                           unsigned long long* __restrict__ out) {
     for (int j = blockIdx.y; j < d; j += gridDim.y) {
@@ -327,7 +383,24 @@ bool gres_cells_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_ma
     if (!cells_geometry(amax, d, g_max, budget_rows, &geo0, &e0)) return false;
     const bool w64 = e0 > 32;
     void* rows = c.buf[B_CELLS].get(geo0.rows * (w64 ? 8 : 4));
-    uint64_t swept = 0;
+    // codes of every step, once (packed bytes; d <= 8 here), within 16 GiB
+    const bool cw32 = d <= 4;
+    const size_t cwb = cw32 ? 4 : 8;
+    const int G = g_max - 1;
+    void* codes = nullptr;
+    if (d <= 8 && S * (uint64_t)G * cwb <= (16ull << 30)) {
+        codes = c.buf[B_CODES].get(S * (uint64_t)G * cwb);
+        if (cw32)
+            k_cells_codes<uint32_t><<<grid_for(S * (uint64_t)G, kBlock), kBlock, 0, c.stream>>>(
+                d_skyv, S, d, g_max, G, (uint32_t*)codes);
+        else
+            k_cells_codes<unsigned long long>
+                <<<grid_for(S * (uint64_t)G, kBlock), kBlock, 0, c.stream>>>(
+                    d_skyv, S, d, g_max, G, (unsigned long long*)codes);
+        SKY_LAUNCH_CHECK();
+        note_launch(c);
+    }
+    uint64_t swept = codes ? S * (uint64_t)d * sizeof(double) + S * (uint64_t)G * cwb : 0;
     int steps = 0;
     const char* uf = getenv("SKYGPU_CELLS_UNFUSED");
     const bool fused = !(uf && uf[0] == '1');
@@ -338,7 +411,25 @@ bool gres_cells_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_ma
         const size_t wb = w64 ? 8 : 4;
         SKY_CUDA(cudaMemsetAsync(rows, 0, geo.rows * wb, c.stream));
         const unsigned gs = grid_for(S, kBlock);
-        if (w64) {
+        auto run_codes = [&](auto* R, auto* cg) {
+            using WR = std::remove_pointer_t<decltype(R)>;
+            using CW = std::remove_const_t<std::remove_pointer_t<decltype(cg)>>;
+            k_cells_mark_c<WR, CW><<<gs, kBlock, 0, c.stream>>>(cg, S, geo, R);
+            sweeps<WR>(c, R, geo, fused);
+            reset_counts(c);
+            k_cells_query_c<WR, CW><<<grid_for(na, kBlock), kBlock, 0, c.stream>>>(
+                cg, geo, R, act, na, d_den, c.d_slots + S_C3);
+        };
+        const uint64_t coff = (uint64_t)(g_max - g) * S;
+        if (codes && w64 && cw32)
+            run_codes(static_cast<unsigned long long*>(rows), (const uint32_t*)codes + coff);
+        else if (codes && w64)
+            run_codes(static_cast<unsigned long long*>(rows), (const unsigned long long*)codes + coff);
+        else if (codes && cw32)
+            run_codes(static_cast<unsigned*>(rows), (const uint32_t*)codes + coff);
+        else if (codes)
+            run_codes(static_cast<unsigned*>(rows), (const unsigned long long*)codes + coff);
+        else if (w64) {
             auto* R = static_cast<unsigned long long*>(rows);
             k_cells_mark<unsigned long long><<<gs, kBlock, 0, c.stream>>>(d_skyv, S, geo, R);
             sweeps<unsigned long long>(c, R, geo, fused);
@@ -358,7 +449,7 @@ bool gres_cells_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_ma
         // algorithmic bytes of the step: the grid zeroed, read and written
         // once by an ideal fused prefix-OR, plus the mark and query reads of
         // the S x d values
-        swept += 3 * geo.rows * wb + 2 * S * (uint64_t)d * sizeof(double);
+        swept += 3 * geo.rows * wb + 2 * S * (codes ? cwb : (uint64_t)d * sizeof(double));
         ++steps;
         // stop early once every candidate has its answer (one small read per step)
         read_slots(c, S_C3, 1);

@@ -198,7 +198,12 @@ struct SkylineOut {
     uint32_t* d_inpos = nullptr;
     int64_t* d_ids = nullptr;
     double* d_skyv = nullptr;  // SoA [d][S]
+    bool aborted = false;      // kSkyAbortIfLarge: the first round asked for the rank grid
 };
+
+// internal sky_engine bit: give up (aborted = true) instead of switching to
+// the rank-grid engine — the streamed head only wants a small skyline
+constexpr unsigned kSkyAbortIfLarge = 0x100u;
 
 // Skyline of n tuples already resident on the device (AoS vals, ids).
 // Input still arriving (host-pointer pipeline): chunk ch = positions

@@ -1378,8 +1378,8 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
         if (eligible) {
             try {
                 const SkylineOut h = skyline_device(c, d_vals, d_ids, feed->bound[1], d, plan,
-                                                    nullptr, 0, 0, nullptr);
-                if (h.S > 0 && h.S <= kCTACap) {
+                                                    nullptr, 0, kSkyAbortIfLarge, nullptr);
+                if (!h.aborted && h.S > 0 && h.S <= kCTACap) {
                     seed = c.buf[B_SEED].as<uint32_t>(h.S);
                     scale_snap = c.buf[B_AMAX2].as<unsigned long long>(kMaxDims);
                     SKY_CUDA(cudaMemcpyAsync(seed, h.d_inpos, h.S * sizeof(uint32_t),
@@ -1861,7 +1861,8 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
         // everything at once with the rank-grid engine instead of filtering.
         // Decided on the device (no extra host round trip): the gate makes
         // K5 keep every candidate, the host switches after K5's sync.
-        const bool gate = rounds == 1 && sky_engine == 0 && r >= kGridMin && sky_grid_bins(r, d);
+        const bool gate = rounds == 1 && (sky_engine & ~kSkyAbortIfLarge) == 0 && r >= kGridMin &&
+                          sky_grid_bins(r, d);
         if (gate) {
             k_grid_gate<<<1, 32, 0, c.stream>>>(c.d_slots, m);
             SKY_LAUNCH_CHECK();
@@ -1870,6 +1871,10 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
 
         const uint64_t a = filter_against(K + kc, m, false);  // synchronises
         if (gate && c.h_slots[S_GATE]) {
+            if (sky_engine & kSkyAbortIfLarge) {
+                out.aborted = true;
+                return out;
+            }
             run_grid();
             break;
         }
