@@ -402,7 +402,9 @@ def roofline(st, sky_ms, gres_ms, d, clk, workload="C2"):
                     "tests_per_step": tests, "kernel_ms_per_step": ms, "launches_per_step": launches,
                     "I_test": i_test, "L_pipe": l_pipe, "pipe": "alu", "f_clk_mhz": f / 1e6}
         if kind == "gres":
-            kern = "k_gres_pairs_tiled" if st["code_bits"] == 8 else "k_gres_pairs_f64"
+            # gres.cu: the resident pair kernel up to 2^21 skyline tuples, tiled beyond
+            kern = ("k_gres_pairs_resident" if st["skyline_size"] <= (1 << 21) else
+                    "k_gres_pairs_tiled") if st["code_bits"] == 8 else "k_gres_pairs_f64"
             tests, ms, launches = st["gres_tests"], gres_ms, st["gres_kernel_launches"]
             if st["code_bits"] == 8:
                 i_test, pipe = (4 if d <= 4 else 8), "alu"

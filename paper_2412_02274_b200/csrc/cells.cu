@@ -213,15 +213,18 @@ __global__ void k_cells_query(const double* __restrict__ v, uint64_t S, CellGeom
 template <class CW>
 __global__ void k_cells_codes(const double* __restrict__ v, uint64_t S, int d, int g_hi, int G,
                               CW* __restrict__ codes) {
-    const uint64_t total = S * (uint64_t)G;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t gi = i / S, t = i - gi * S;
-        const double gd = (double)(g_hi - (int)gi);
-        CW w = 0;
-        for (int k = 0; k < d; ++k)
-            w |= (CW)(unsigned)floor(__dmul_rn(v[(uint64_t)k * S + t], gd)) << (8 * k);
-        codes[i] = w;
+    // one thread per tuple: its d values read once, the codes of all G steps
+    // written (coalesced across the warp at every step)
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < S;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        double x[8];
+        for (int k = 0; k < d; ++k) x[k] = v[(uint64_t)k * S + t];
+        for (int gi = 0; gi < G; ++gi) {
+            const double gd = (double)(g_hi - gi);
+            CW w = 0;
+            for (int k = 0; k < d; ++k) w |= (CW)(unsigned)floor(__dmul_rn(x[k], gd)) << (8 * k);
+            codes[(uint64_t)gi * S + t] = w;
+        }
     }
 }
 
@@ -391,12 +394,11 @@ bool gres_cells_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_ma
     if (d <= 8 && S * (uint64_t)G * cwb <= (16ull << 30)) {
         codes = c.buf[B_CODES].get(S * (uint64_t)G * cwb);
         if (cw32)
-            k_cells_codes<uint32_t><<<grid_for(S * (uint64_t)G, kBlock), kBlock, 0, c.stream>>>(
+            k_cells_codes<uint32_t><<<grid_for(S, kBlock), kBlock, 0, c.stream>>>(
                 d_skyv, S, d, g_max, G, (uint32_t*)codes);
         else
-            k_cells_codes<unsigned long long>
-                <<<grid_for(S * (uint64_t)G, kBlock), kBlock, 0, c.stream>>>(
-                    d_skyv, S, d, g_max, G, (unsigned long long*)codes);
+            k_cells_codes<unsigned long long><<<grid_for(S, kBlock), kBlock, 0, c.stream>>>(
+                d_skyv, S, d, g_max, G, (unsigned long long*)codes);
         SKY_LAUNCH_CHECK();
         note_launch(c);
     }

@@ -566,7 +566,10 @@ __global__ void k_gap_witness(const double* __restrict__ v, uint64_t S, int d, i
         if (!(x >= 0.0 && x < 1.0) || found) continue;
         int b = (int)floor(__dmul_rn(x, (double)nb));
         b = b < 0 ? 0 : (b >= nb ? nb - 1 : b);
-        const unsigned long long old = atomicCAS(&table[j * nb + b], 0ULL, bits + 1);
+        // a plain read first: the 2*cap buckets per attribute fill at once,
+        // after that a CAS per value would serialise on a few addresses
+        unsigned long long old = *(volatile unsigned long long*)&table[j * nb + b];
+        if (old == 0ULL) old = atomicCAS(&table[j * nb + b], 0ULL, bits + 1);
         if (old != 0ULL && old != bits + 1) {
             const unsigned long long ob = old - 1;
             const double w = __longlong_as_double((long long)ob);

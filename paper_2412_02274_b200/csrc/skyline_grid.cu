@@ -443,7 +443,7 @@ GridShape grid_shape(uint64_t r, int d) {
     GridShape g;
     if (d < 1 || d > 8) return g;
     static const double per_row = env_or("SKYGPU_GRID_ROW", 512.0);
-    static const int k0 = (int)std::min(128.0, env_or("SKYGPU_GRID_K0", 32.0));
+    static const int k0 = (int)std::min(128.0, env_or("SKYGPU_GRID_K0", 64.0));
     int k = 1;
     if (d > 1) {
         k = (int)std::lround(std::pow(std::max(1.0, (double)r / per_row), 1.0 / (d - 1)));
