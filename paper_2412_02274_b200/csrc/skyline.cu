@@ -84,7 +84,8 @@ template <int D>
 __global__ void k_score(const double* __restrict__ v, uint64_t n, int d,
                         unsigned long long* __restrict__ key,
                         unsigned long long* __restrict__ slots,
-                        unsigned long long* __restrict__ amax, uint64_t base = 0) {
+                        unsigned long long* __restrict__ amax, uint64_t base = 0,
+                        const int64_t* __restrict__ ids = nullptr) {
     constexpr int DA = D > 0 ? D : 1;
     unsigned long long mn = ~0ULL, mx = 0;
     unsigned long long am[DA];
@@ -115,6 +116,7 @@ __global__ void k_score(const double* __restrict__ v, uint64_t n, int d,
         mn = b < mn ? b : mn;
         mx = b > mx ? b : mx;
         if (bad) atomicMin(&slots[S_BAD], static_cast<unsigned long long>(base + i));
+        if (ids && i + 1 < n && ids[i] >= ids[i + 1]) atomicOr(&slots[S_FLAG], 1ULL);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -502,7 +504,8 @@ template <int D>
 __global__ void __launch_bounds__(1024)
 k_cell_order(const double* __restrict__ v, int d, const uint32_t* __restrict__ in, uint32_t mcap,
              const unsigned long long* __restrict__ count, int mcell, uint32_t ncells, const unsigned long long* __restrict__ amax,
-             uint32_t* __restrict__ out, uint32_t* __restrict__ out_cell) {
+             uint32_t* __restrict__ out, uint32_t* __restrict__ out_cell,
+             uint32_t* __restrict__ seg) {
     constexpr int DM = D > 0 ? D : kMaxDims;
     const int dd = D > 0 ? D : d;
     const uint32_t m = count ? (uint32_t)*count : mcap;
@@ -526,6 +529,11 @@ k_cell_order(const double* __restrict__ v, int d, const uint32_t* __restrict__ i
     }
     __syncthreads();
     block_exclusive_scan_4096(cnt);
+    if (seg) {  // segment table: seg[c] = first position of cell c, seg[ncells] = m
+        for (uint32_t c = threadIdx.x; c < ncells; c += 1024) seg[c] = cnt[c];
+        if (threadIdx.x == 0) seg[ncells] = m;
+        __syncthreads();  // read cnt before the scatter below bumps it
+    }
 #pragma unroll
     for (int j = 0; j < kCTAItems; ++j) {
         const uint32_t i = threadIdx.x + j * 1024;
@@ -991,7 +999,8 @@ k_sfs_filter_q(const double* __restrict__ v, const unsigned long long* __restric
                const unsigned long long* __restrict__ amax,
                const unsigned long long* __restrict__ slots, uint8_t* __restrict__ keep,
                unsigned long long* __restrict__ tests, uint32_t bs,
-               const uint32_t* __restrict__ Ppos, const int64_t* __restrict__ ids) {
+               const uint32_t* __restrict__ Ppos, const int64_t* __restrict__ ids,
+               uint32_t kSolo) {
     // Ppos != nullptr: A' is a seed that need not precede every candidate
     // (host-overlapped first part, skygpu_pipeline); a dominating comparator
     // then also has to precede the candidate in (sum, id, position) order
@@ -1002,7 +1011,6 @@ k_sfs_filter_q(const double* __restrict__ v, const unsigned long long* __restric
         return is < it || (is == it && ps < pt);
     };
     constexpr int W = QW<D>::W;
-    constexpr uint32_t kSolo = 32;
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -1413,12 +1421,10 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
         dispatch_d(d, [&](auto DC) {
             constexpr int D = decltype(DC)::value;
             k_score<D><<<grid_for(n, kBlock, c.num_sms * 8), kBlock, 0, c.stream>>>(
-                d_vals, n, d, keys, c.d_slots, amax);
+                d_vals, n, d, keys, c.d_slots, amax, 0, d_ids);  // + ids sortedness
         });
         SKY_LAUNCH_CHECK();
-        k_ids_check<<<gb, kBlock, 0, c.stream>>>(d_ids, n, c.d_slots);
-        SKY_LAUNCH_CHECK();
-        note_launch(c, 2);
+        note_launch(c, 1);
     }
     if (plan.strategy == SKYGPU_GRID) {
         k_grid_range<<<grid_for(n * d, kBlock), kBlock, 0, c.stream>>>(d_vals, n * d, c.d_slots);
@@ -1580,7 +1586,10 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
                 uint32_t* Pb = c.buf[B_GTMP1].as<uint32_t>(m);
                 uint32_t* bst = c.buf[B_ORDER].as<uint32_t>(kMaxCells + 1 + kKeyBuckets + 1) +
                                 (kMaxCells + 1);
-                k_bucket_order<<<1, 1024, 0, c.stream>>>(Pfull, (uint32_t)m, keys, gmin, shift, Pb, bst);
+                // (the in-bucket rank stays a many-CTA kernel: a bucket of
+                // equal sums — C3's zero tuples — would serialise one CTA)
+                k_bucket_order<<<1, 1024, 0, c.stream>>>(Pfull, (uint32_t)m, keys, gmin, shift, Pb,
+                                                         bst);
                 SKY_LAUNCH_CHECK();
                 k_bucket_rank<<<grid_for(m, kBlock), kBlock, 0, c.stream>>>(Pb, (uint32_t)m, keys,
                                                                              d_ids, gmin, shift, bst,
@@ -1714,14 +1723,12 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
                 constexpr int D = decltype(DC)::value;
                 k_cell_order<D><<<1, 1024, 0, c.stream>>>(d_vals, d, alist, (uint32_t)m,
                                                           c.d_slots + S_C2, mcell, ncells,
-                                                          qpre ? scale : nullptr, Alist, Akey);
+                                                          qpre ? scale : nullptr, Alist, Akey,
+                                                          seg_table);
             });
             SKY_LAUNCH_CHECK();
             seg = seg_table;
-            k_cell_segments<<<grid_for(ncells + 1, kBlock), kBlock, 0, c.stream>>>(
-                Akey, c.d_slots + S_C2, ncells, seg);
-            SKY_LAUNCH_CHECK();
-            note_launch(c, 2);
+            note_launch(c, 1);
             psrc = Alist;
         }
         double* Pv = c.buf[B_CSUM].as<double>(m * d);
@@ -1749,6 +1756,12 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
     // into fkeep[0..rl); seeded = A' need not precede them (checked per hit)
     auto launch_k5 = [&](const AScan& A, const uint32_t* Rl, uint64_t rl, uint8_t* fkeep,
                          bool seeded, const unsigned long long* scale) {
+        // comparators each lane tests alone (phase A) before the warp-wide scan
+        static const uint32_t solo = [] {
+            const char* e = getenv("SKYGPU_SOLO");
+            const int v = e ? atoi(e) : 0;
+            return v > 0 ? (uint32_t)v : 8u;
+        }();
         const uint32_t bsf = batch_size(c, rl);
         const uint64_t wf = std::min<uint64_t>((rl + bsf - 1) / bsf, (uint64_t)c.num_sms * 64);
         dispatch_d(d, [&](auto DC) {
@@ -1758,7 +1771,7 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
                 k_sfs_filter_q<D><<<grid, kBlock, 0, c.stream>>>(
                     d_vals, keys, Rl, (uint32_t)rl, A.Pv, A.Pq, (uint32_t)A.m, A.seg, A.mcell,
                     A.qk, scale, c.d_slots, fkeep, c.d_slots + S_TESTS_SKY, bsf,
-                    seeded ? A.psrc : nullptr, d_ids);
+                    seeded ? A.psrc : nullptr, d_ids, solo);
             else
                 k_sfs_filter_cells<D><<<grid, kBlock, 0, c.stream>>>(
                     d_vals, d, keys, Rl, (uint32_t)rl, A.Pv, (uint32_t)A.m, A.seg, A.mcell,
