@@ -71,6 +71,11 @@ if [ -f "$LIBDIR/libskygpu.so" ]; then
       "$OUT/libskypar_gpu_chk.a" -L"$LIBDIR" -lskygpu $RPATH -o "$OUT/skypar_gpu"
   $CXX $COMMON -O2 -g -I"$REF/include" "$ROOT/paper_2412_02274_b200/adapter/skypar_cli.cpp" \
       "$OUT/libskypar_chk.a" -o "$OUT/skypar_ref"
+  # the skypar-bench front end (adapter/skypar_bench_cli.cpp), both ways
+  $CXX $COMMON -O2 -g -I"$REF/include" "$ROOT/paper_2412_02274_b200/adapter/skypar_bench_cli.cpp" \
+      "$OUT/libskypar_gpu_chk.a" -L"$LIBDIR" -lskygpu $RPATH -o "$OUT/skypar_bench_gpu"
+  $CXX $COMMON -O2 -g -I"$REF/include" "$ROOT/paper_2412_02274_b200/adapter/skypar_bench_cli.cpp" \
+      "$OUT/libskypar_chk.a" -o "$OUT/skypar_bench_ref"
   # the CLI-determinism fixtures (acceptance criterion 9) travel with the
   # binaries; /root/reference does not exist on the GPU box
   mkdir -p "$OUT/fixtures"

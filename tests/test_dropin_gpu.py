@@ -94,3 +94,32 @@ def test_cli_reports_byte_identical_to_reference(case, tmp_path):
         assert r.returncode == 0, r.stderr
         outs.append(out.read_bytes())
     assert outs[0] == outs[1]
+
+
+BENCH_GPU = os.path.join(REF, "skypar_bench_gpu")
+BENCH_REF = os.path.join(REF, "skypar_bench_ref")
+
+
+def _count_columns(text):
+    """The skypar-bench tables without the wall-time and speed-up columns."""
+    out = []
+    for line in text.splitlines():
+        f = line.split()
+        if len(f) == 6 and f[1].isdigit():
+            out.append(tuple(f[:4]))
+        elif line.startswith(("dataset", "phase")):
+            out.append(line.strip())
+    return out
+
+
+@pytest.mark.skipif(not (os.path.exists(BENCH_GPU) and os.path.exists(BENCH_REF)),
+                    reason="skypar-bench binaries not built (needs /root/reference)")
+@pytest.mark.parametrize("args", ["--n 20000 --d 3 --gen ant --partitions 16 --cores 8",
+                                  "--n 30000 --d 4 --gen uni --partitions 32 --reps 5 --cap 20"])
+def test_skypar_bench_tool_counts_match_reference(args):
+    outs = []
+    for exe in (BENCH_GPU, BENCH_REF):
+        r = subprocess.run([exe, *args.split()], capture_output=True, text=True, timeout=900)
+        assert r.returncode == 0, r.stderr
+        outs.append(_count_columns(r.stdout))
+    assert outs[0] == outs[1] and len(outs[0]) >= 12
