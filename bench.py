@@ -213,14 +213,17 @@ def our_arm(args):
     shard_rank, shard_world = (rank, world) if strong else (0, 1)
     sky_flag = {"auto": skypar.SKY_AUTO, "rounds": skypar.SKY_ROUNDS, "grid": skypar.SKY_GRID}[args.sky_engine]
 
+    if strong and world > 1:
+        # the library's exchange steps (rank-grid keep flags, denominators:
+        # MAX all-reduce) go through NCCL via torch.distributed
+        from paper_2412_02274_b200 import dist as skydist
+        skydist.install_collective()
+
     def step_device():
-        S, gm, st = skypar.pipeline_raw(vals_d.data_ptr(), ids_d.data_ptr(), n, d, plan, cap,
-                                        args.engine, shard_rank, shard_world,
-                                        skypar.DEVICE_PTRS | sky_flag, pos_d.data_ptr(),
-                                        den_d.data_ptr())
-        if strong and world > 1:  # NCCL max-reduce of the sharded denominators
-            dist.all_reduce(den_d[:S], op=dist.ReduceOp.MAX)
-        return S, gm, st
+        return skypar.pipeline_raw(vals_d.data_ptr(), ids_d.data_ptr(), n, d, plan, cap,
+                                   args.engine, shard_rank, shard_world,
+                                   skypar.DEVICE_PTRS | sky_flag, pos_d.data_ptr(),
+                                   den_d.data_ptr())
 
     for _ in range(args.warmup):
         step_device()
@@ -274,10 +277,6 @@ def our_arm(args):
         S2, _, _ = skypar.pipeline_raw(pin_vals.data_ptr(), pin_ids.data_ptr(), n, d, plan, cap,
                                        args.engine, shard_rank, shard_world, sky_flag,
                                        out_pos.data_ptr(), out_den.data_ptr())
-        if strong and world > 1:
-            t_den = torch.from_numpy(out_den.numpy()[:S2]).to(dev)
-            dist.all_reduce(t_den, op=dist.ReduceOp.MAX)
-            out_den[:S2].copy_(t_den.cpu())
         return S2
 
     for _ in range(max(1, args.warmup)):
@@ -310,7 +309,7 @@ def our_arm(args):
         "config": {"workload": f"{args.workload}: {gen} n={n} d={d} seed={seed}"
                                f"{'' if strong or world == 1 else '+rank'}, {strat} p={p}, cap={cap}",
                    "skyline_size": S, "g_max": gm, "l2": "flushed (256 MiB write) before each step",
-                   "parallelism": f"{'sharded gres + NCCL max' if strong else 'independent instance'}"
+                   "parallelism": f"{'sharded rank-grid rows + gres tuples, NCCL MAX exchanges' if strong else 'independent instance'}"
                                   f" per GPU x{world}",
                    "gres_engine": {0: "auto", 1: "pairs", 2: "cells"}[args.engine],
                    "skyline_engine": {8: "prefix rounds", 16: "rank grid"}.get(stats[-1]["sky_engine"], "?")},

@@ -152,6 +152,19 @@ int skygpu_pipeline(const double* vals, const int64_t* ids, uint64_t n, int d,
                     uint64_t* out_s, int* out_g_max, skygpu_stats* stats, char* err,
                     size_t errlen);
 
+/* The exchange step of sharded pipeline calls (shard_world > 1): an
+ * element-wise MAX all-reduce, across the shard group, of `count` elements of
+ * `elem_bytes` bytes (1 = uint8, 4 = int32) at the DEVICE pointer dev_ptr;
+ * work queued on `cuda_stream` before the call must be complete in the
+ * reduction, and the result must be in place when the function returns.
+ * Returns 0 on success.  With a collective installed, skygpu_pipeline shards
+ * the rank-grid skyline engine by grid row (keep flags MAX-reduced) and
+ * returns the FULL denominator map on every rank (den MAX-reduced); without
+ * one, only the gres stage is sharded and the caller reduces the map. */
+typedef int (*skygpu_allreduce_max_fn)(void* dev_ptr, uint64_t count, int elem_bytes,
+                                       void* cuda_stream, void* user);
+int skygpu_set_collective(skygpu_allreduce_max_fn fn, void* user, char* err, size_t errlen);
+
 /* Exact reference accounting of parallel_skyline — "metrics-parity" mode,
  * not the hot path.  Returns the DominanceCounter
  * totals the reference's CPU algorithm executes (core.hpp:46-67): per

@@ -290,6 +290,15 @@ __global__ void k_mark_i32(int32_t* __restrict__ a, const uint32_t* __restrict__
 }
 }  // namespace
 
+void shard_allreduce_max(Ctx& c, void* dev_ptr, uint64_t count, int elem_bytes) {
+    if (!c.coll || c.shard_world <= 1 || count == 0) return;
+    SKY_CUDA(cudaStreamSynchronize(c.stream));  // the reduced data is complete
+    const int rc = c.coll(dev_ptr, count, elem_bytes, (void*)c.stream, c.coll_user);
+    if (rc != 0)
+        throw Error(SKYGPU_ERUNTIME, "sharded pipeline: the installed collective failed (" +
+                                         std::to_string(rc) + ")");
+}
+
 void widen_u32_u64(Ctx& c, const uint32_t* a, uint64_t* b, uint64_t n) {
     k_widen<<<grid_for(n, 256), 256, 0, c.stream>>>(a, b, n);
     SKY_LAUNCH_CHECK();
@@ -574,6 +583,19 @@ int skygpu_pipeline(const double* vals, const int64_t* ids, uint64_t n, int d,
             di = bi;
         }
         Timer tsky(c, 4);
+        // sharded call with a collective: the rank-grid skyline is split by
+        // grid row and the denominators are reduced here (skygpu.h)
+        struct ShardScope {
+            Ctx& c;
+            ShardScope(Ctx& cc, int r, int w) : c(cc) {
+                c.shard_rank = c.coll ? r : 0;
+                c.shard_world = c.coll ? w : 1;
+            }
+            ~ShardScope() {
+                c.shard_rank = 0;
+                c.shard_world = 1;
+            }
+        } shard_scope(c, shard_rank, shard_world);
         SkylineOut so = skyline_device(c, dv, di, n, d, pl, nullptr, 0,
                                        flags & (SKYGPU_SKY_ROUNDS | SKYGPU_SKY_GRID),
                                        streamed ? &feed : nullptr);
@@ -586,6 +608,7 @@ int skygpu_pipeline(const double* vals, const int64_t* ids, uint64_t n, int d,
             Timer tg(c, 6);
             go = gres_device(c, so.d_skyv, so.d_ids, so.S, d, cap, gres_engine, shard_rank,
                              shard_world, (flags & SKYGPU_CHECK_SKYLINE) != 0, den);
+            if (c.shard_world > 1) shard_allreduce_max(c, den, so.S, 4);  // the full map
             tg.stop(&c.st->ms_gres);
         }
         trace_mark(c, "gres: finalize");
@@ -615,6 +638,14 @@ int skygpu_pipeline(const double* vals, const int64_t* ids, uint64_t n, int d,
         *out_s = so.S;
         *out_g_max = go.g_max;
         end_stats(c);
+    });
+}
+
+int skygpu_set_collective(skygpu_allreduce_max_fn fn, void* user, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        Ctx& c = ctx();
+        c.coll = fn;
+        c.coll_user = user;
     });
 }
 

@@ -111,6 +111,10 @@ struct Ctx {
     bool trace = false;
     int ntrace = 0;
     cudaStream_t copy = nullptr;  // H2D of streamed pipeline inputs
+    // sharded pipeline call in progress (skygpu_set_collective installed)
+    skygpu_allreduce_max_fn coll = nullptr;
+    void* coll_user = nullptr;
+    int shard_rank = 0, shard_world = 1;
     cudaEvent_t xev[10];          // chunk-ready events of the streamed input
     cudaEvent_t tev[96];
     const char* tlabel[96];
@@ -229,7 +233,10 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
 int sky_grid_bins(uint64_t r, int d);
 void sky_grid_decide(Ctx& c, const double* d_vals, int d, const unsigned long long* keys,
                      const int64_t* d_ids, const uint32_t* R, uint64_t r, uint8_t* keep,
-                     double* kernel_ms);
+                     double* kernel_ms, int shard_rank = 0, int shard_world = 1);
+
+// the installed MAX all-reduce over the shard group (see skygpu.h)
+void shard_allreduce_max(Ctx& c, void* dev_ptr, uint64_t count, int elem_bytes);
 
 struct GresOut {
     int g_max = 1;

@@ -1552,7 +1552,9 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
     auto run_grid = [&]() {
         uint8_t* gkeep = c.buf[B_SV].as<uint8_t>(r);
         double kms = 0;
-        sky_grid_decide(c, d_vals, d, keys, d_ids, R, r, gkeep, &kms);
+        sky_grid_decide(c, d_vals, d, keys, d_ids, R, r, gkeep, &kms, c.shard_rank,
+                        c.shard_world);
+        if (c.shard_world > 1) shard_allreduce_max(c, gkeep, r, 1);  // every row decided somewhere
         kernel_ms += kms;
         kernel_launches += 1;
         uint32_t* surv = c.buf[B_IDX0].as<uint32_t>(r);

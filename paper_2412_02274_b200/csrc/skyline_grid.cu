@@ -123,11 +123,14 @@ __global__ void k_cell_scatter(const W* __restrict__ code, const uint32_t* __res
     }
 }
 
-// work items: (row, first sorted position) chunks of <= 128 candidates
+// work items: (row, first sorted position) chunks of <= 128 candidates; a
+// sharded call keeps only the rows this shard owns (row % world == rank)
 __global__ void k_row_items(const uint32_t* __restrict__ seg, uint32_t nrows, int k0,
-                            uint2* __restrict__ items, unsigned* __restrict__ ctr) {
+                            uint2* __restrict__ items, unsigned* __restrict__ ctr, int rank,
+                            int world) {
     for (uint32_t row = blockIdx.x * blockDim.x + threadIdx.x; row < nrows;
          row += gridDim.x * blockDim.x) {
+        if ((int)(row % (uint32_t)world) != rank) continue;
         const uint32_t a = seg[row * k0], n = seg[(row + 1) * k0] - a;
         if (!n) continue;
         const uint32_t ch = (n + kItem - 1) / kItem;
@@ -465,8 +468,10 @@ int sky_grid_bins(uint64_t r, int d) { return grid_shape(r, d).k0; }
 
 void sky_grid_decide(Ctx& c, const double* d_vals, int d, const unsigned long long* keys,
                      const int64_t* d_ids, const uint32_t* R, uint64_t r, uint8_t* keep,
-                     double* kernel_ms) {
+                     double* kernel_ms, int shard_rank, int shard_world) {
     const GridShape g = grid_shape(r, d);
+    if (shard_world > 1)  // tuples of rows other shards own stay 0 until the MAX reduce
+        SKY_CUDA(cudaMemsetAsync(keep, 0, r, c.stream));
     if (!g.k0) throw Error(SKYGPU_ERUNTIME, "sky_grid_decide: unsupported shape (internal)");
     const uint32_t ncells = g.ncells;
     double* bounds = c.buf[B_PROJ].as<double>(8 * 128);
@@ -499,7 +504,8 @@ void sky_grid_decide(Ctx& c, const double* d_vals, int d, const unsigned long lo
         k_cell_scatter<W><<<grid_for(r, kGB), kGB, 0, c.stream>>>(code, cell, (uint32_t)r, seg,
                                                                   count, scode, sidx);
         SKY_LAUNCH_CHECK();
-        k_row_items<<<grid_for(g.rows, kGB), kGB, 0, c.stream>>>(seg, g.rows, g.k0, items, ctr);
+        k_row_items<<<grid_for(g.rows, kGB), kGB, 0, c.stream>>>(seg, g.rows, g.k0, items, ctr,
+                                                                 shard_rank, shard_world);
         SKY_LAUNCH_CHECK();
         note_launch(c, 5);
         trace_mark(c, "grid: codes + cells + items");

@@ -6,7 +6,10 @@ chunks r, r + world, r + 2*world, ... of the skyline (libskygpu's
 k_shard_iota; interleaving balances the early-exit work, SURVEY.md §7.4
 item 5).  Each rank writes the denominators of its own tuples and 0 for the
 others, so one MAX all-reduce (NCCL over NVLink on GPUs, gloo on CPU) yields
-the full map — the only exchange on the path.
+the full map.  With install_collective(), the library also splits the
+rank-grid skyline engine (large skylines, BASELINE config 5) by grid row and
+MAX-reduces its keep flags — the second exchange — and returns the full map
+on every rank by itself.
 """
 from __future__ import annotations
 
@@ -51,3 +54,30 @@ def gres_sharded(values, ids=None, plan=None, cap=25, rank: int = 0, world: int 
         combine_denominators(den, group)
         den = den.cpu()
     return res.positions, den.numpy(), res.g_max
+
+
+class _DeviceBuffer:
+    """A raw device buffer seen by torch through __cuda_array_interface__."""
+
+    def __init__(self, ptr: int, count: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (count,), "typestr": typestr,
+                                         "data": (ptr, False), "version": 3}
+
+
+def install_collective(group=None):
+    """Route libskygpu's sharded-call exchange (uint8 keep flags, int32
+    denominators; MAX) through torch.distributed — NCCL over NVLink/NVSwitch
+    on GPUs."""
+    import torch
+    import torch.distributed as dist
+
+    from . import skypar
+
+    def allreduce_max(ptr, count, elem_bytes, stream):
+        t = torch.as_tensor(_DeviceBuffer(ptr, count, "|u1" if elem_bytes == 1 else "<i4"),
+                            device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+        torch.cuda.current_stream().synchronize()  # in place before the library continues
+        return 0
+
+    skypar.set_collective(allreduce_max)

@@ -111,6 +111,7 @@ def lib() -> C.CDLL:
         L.skygpu_generate.argtypes = [i32, u64, i32, u64, vp, cp, sz]
         L.skygpu_sfs_accounting.argtypes = [vp, vp, u64, i32, vp, i64, vp, u64, vp, vp, vp, vp, vp,
                                             cp, sz]
+        L.skygpu_set_collective.argtypes = [vp, vp, cp, sz]
         _lib = L
     return _lib
 
@@ -118,7 +119,8 @@ def lib() -> C.CDLL:
 EXPORTED_SYMBOLS = ("skygpu_version", "skygpu_device_count", "skygpu_set_device", "skygpu_set_stream",
                     "skygpu_release", "skygpu_make_plan", "skygpu_parallel_skyline",
                     "skygpu_grid_resistance", "skygpu_snap_relation", "skygpu_max_grid_intervals",
-                    "skygpu_pipeline", "skygpu_generate", "skygpu_sfs_accounting")
+                    "skygpu_pipeline", "skygpu_generate", "skygpu_sfs_accounting",
+                    "skygpu_set_collective")
 
 
 def _check(rc: int, err: C.Array) -> None:
@@ -348,3 +350,32 @@ def sfs_accounting(values, ids, pids, partitions: int, reps=None) -> Accounting:
                                        _p(per), _p(fin), _p(into), _p(pos), _p(cnt), err, 1024), err)
     return Accounting(per[:int(partitions)].copy(), int(fin[0]), int(into[0]),
                       pos[:int(cnt[0])].astype(np.int64))
+
+
+# skygpu_allreduce_max_fn(dev_ptr, count, elem_bytes, cuda_stream, user) -> int
+COLLECTIVE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint64, C.c_int, C.c_void_p, C.c_void_p)
+_collective_ref = None  # keeps the installed callback alive
+
+
+def set_collective(fn=None) -> None:
+    """Install the exchange step of sharded pipeline calls (skygpu.h:
+    skygpu_set_collective): ``fn(dev_ptr, count, elem_bytes, stream)`` must
+    MAX-all-reduce the device buffer in place across the shard group and
+    return 0.  ``None`` uninstalls it."""
+    global _collective_ref
+    err = _errbuf()
+    if fn is None:
+        _collective_ref = None
+        _check(lib().skygpu_set_collective(None, None, err, 1024), err)
+        return
+
+    def tramp(ptr, count, elem_bytes, stream, user):
+        try:
+            return int(fn(int(ptr or 0), int(count), int(elem_bytes), int(stream or 0)) or 0)
+        except Exception:  # an exception must not unwind through C
+            import traceback
+            traceback.print_exc()
+            return 1
+
+    _collective_ref = COLLECTIVE_FN(tramp)
+    _check(lib().skygpu_set_collective(C.cast(_collective_ref, C.c_void_p), None, err, 1024), err)

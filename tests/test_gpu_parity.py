@@ -329,3 +329,68 @@ def test_streamed_fp_tie_across_chunks():
     pos, _ = po.skyline_sfs(v, ids)
     assert res.positions.tolist() == pos.tolist()
     assert sorted(res.positions.tolist()) == [0, n - 1]
+
+
+# ------------------------------------------------ sharded calls with an installed collective
+def _emulated_two_ranks(run):
+    """Emulate a 2-rank group on one GPU: rank 1 runs first and its MAX
+    all-reduce inputs are recorded; rank 0 then runs with a collective that
+    MAX-combines each buffer with rank 1's recording of the same call index.
+    Returns rank 0's result (what every rank would hold)."""
+    import torch
+    from paper_2412_02274_b200 import skypar
+    from paper_2412_02274_b200.dist import _DeviceBuffer
+
+    def view(ptr, count, eb):
+        return torch.as_tensor(_DeviceBuffer(ptr, count, "|u1" if eb == 1 else "<i4"),
+                               device="cuda")
+
+    recorded = []
+
+    def record(ptr, count, eb, stream):
+        torch.cuda.synchronize()
+        recorded.append(view(ptr, count, eb).clone())
+        return 0
+
+    calls = iter(range(100))
+
+    def combine(ptr, count, eb, stream):
+        torch.cuda.synchronize()
+        t = view(ptr, count, eb)
+        t.copy_(torch.maximum(t, recorded[next(calls)]))
+        torch.cuda.synchronize()
+        return 0
+
+    try:
+        skypar.set_collective(record)
+        run(1)
+        skypar.set_collective(combine)
+        out = run(0)
+    finally:
+        skypar.set_collective(None)
+    return out, recorded
+
+
+def test_sharded_rank_grid_skyline_exchange():
+    """The rank-grid engine split by grid row: each rank decides its rows,
+    the keep flags are MAX-reduced (skyline only here: in the one-GPU
+    emulation rank 1 never sees rank 0's flags, so its gres input differs)."""
+    v = sk.generate("ant", 300_000, 7, 2)
+    full = sk.pipeline(v, cap=25, skip_gres=True)
+    assert full.stats["sky_engine"] == sk.SKY_GRID
+    out, recorded = _emulated_two_ranks(
+        lambda rank: sk.pipeline(v, cap=25, skip_gres=True, shard_rank=rank, shard_world=2))
+    keep1 = recorded[0].cpu().numpy()
+    assert len(recorded) == 1 and 0 < keep1.sum() < len(full.positions)  # rank 1: its rows only
+    assert out.positions.tolist() == full.positions.tolist()
+
+
+def test_sharded_gres_exchange_returns_full_map():
+    v = sk.generate("ant", 50_000, 4, 3)
+    full = sk.pipeline(v, cap=25)
+    out, recorded = _emulated_two_ranks(
+        lambda rank: sk.pipeline(v, cap=25, shard_rank=rank, shard_world=2))
+    assert len(recorded) == 1 and recorded[0].dtype.itemsize == 4  # only the den exchange
+    assert (recorded[0].cpu().numpy() == 0).any()  # rank 1 left rank 0's tuples at 0
+    assert out.positions.tolist() == full.positions.tolist()
+    assert out.den.tolist() == full.den.tolist()
