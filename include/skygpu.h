@@ -17,6 +17,9 @@
  *                                 (proj/src/harness.cpp:208 then :229-231)
  *   skygpu_sfs_accounting      <- the DominanceCounter totals inside
  *                                 parallel_skyline (parallel.cpp:59-93)
+ *   skygpu_set_collective      <- (no reference counterpart: the reference is
+ *                                 one process; this installs the multi-GPU
+ *                                 exchange)
  *
  * Conventions
  *  - Values are float64, row-major n x d (tuple i = vals[i*d .. i*d+d-1]),
