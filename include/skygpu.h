@@ -17,6 +17,8 @@
  *                                 (proj/src/harness.cpp:208 then :229-231)
  *   skygpu_sfs_accounting      <- the DominanceCounter totals inside
  *                                 parallel_skyline (parallel.cpp:59-93)
+ *   skygpu_normalize           <- skypar::normalize            include/skypar/harness.hpp
+ *   skygpu_select_representatives <- skypar::select_representatives partition.hpp
  *   skygpu_set_collective      <- (no reference counterpart: the reference is
  *                                 one process; this installs the multi-GPU
  *                                 exchange)
@@ -68,6 +70,7 @@ extern "C" {
 #define SKYGPU_SKIP_GRES 4u     /* skyline only (harness mode "skyline") */
 #define SKYGPU_SKY_ROUNDS 8u    /* force the prefix-round skyline engine */
 #define SKYGPU_SKY_GRID 16u     /* force the one-pass rank-grid skyline engine (d <= 8) */
+#define SKYGPU_NORMALIZE 32u    /* min-max normalise on the device first (harness.cpp:161-177) */
 
 /* mirrors skypar::PartitionPlan (partition.hpp:27-32) */
 typedef struct skygpu_plan {
@@ -185,6 +188,20 @@ int skygpu_sfs_accounting(const double* vals, const int64_t* ids, uint64_t n, in
                           uint64_t n_reps, uint64_t* per_part, uint64_t* final_tests,
                           uint64_t* into_final, uint64_t* out_pos, uint64_t* out_n, char* err,
                           size_t errlen);
+
+/* harness.cpp:161-177 normalize on the device: per attribute (v - min) /
+ * (max - min), 0 for a constant attribute; bit-identical to the reference.
+ * Host pointers; out may alias vals. */
+int skygpu_normalize(const double* vals, uint64_t n, int d, double* out, char* err,
+                     size_t errlen);
+
+/* partition.cpp:249-271 select_representatives(r, k, sum_score, c) on the
+ * device: out_pos[0..*out_n) = input positions of the kept picks in (sum, id)
+ * order (out_pos sized min(k, n)); *tests = the pruning's DominanceCounter
+ * total.  Host pointers. */
+int skygpu_select_representatives(const double* vals, const int64_t* ids, uint64_t n, int d,
+                                  uint64_t k, uint64_t* out_pos, uint64_t* out_n,
+                                  uint64_t* tests, char* err, size_t errlen);
 
 /* Product-side seeded generators (bit-exact with proj/src/datagen.cpp:41-94;
  * kind 0 uni, 1 ant, 2 corr = BASELINE C3, 3 lattice = test_util.hpp:38-54).

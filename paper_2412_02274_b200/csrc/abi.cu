@@ -547,7 +547,8 @@ int skygpu_pipeline(const double* vals, const int64_t* ids, uint64_t n, int d,
         }();
         // (worth it only when the tail's copy outlasts the head's decision,
         // ~0.5 ms: from ~48 MB of input on)
-        const bool streamed = !dev && overlap_env && n * (uint64_t)(d + 1) * 8 >= (48ull << 20) &&
+        const bool streamed = !dev && overlap_env && !(flags & SKYGPU_NORMALIZE) &&
+                              n * (uint64_t)(d + 1) * 8 >= (48ull << 20) &&
                               d <= 8 && pl.strategy != SKYGPU_GRID && !(flags & SKYGPU_SKY_GRID);
         if (!dev) {
             Timer h2d(c, 2);
@@ -581,6 +582,11 @@ int skygpu_pipeline(const double* vals, const int64_t* ids, uint64_t n, int d,
             h2d.stop(&c.st->ms_h2d);
             dv = bv;
             di = bi;
+        }
+        if (flags & SKYGPU_NORMALIZE) {  // run_experiment's --normalize, on the device
+            double* nv = c.buf[B_NORM].as<double>(n * d);
+            normalize_device(c, dv, n, d, nv);
+            dv = nv;
         }
         Timer tsky(c, 4);
         // sharded call with a collective: the rank-grid skyline is split by
@@ -637,6 +643,59 @@ int skygpu_pipeline(const double* vals, const int64_t* ids, uint64_t n, int d,
         all.stop(&c.st->ms_total);
         *out_s = so.S;
         *out_g_max = go.g_max;
+        end_stats(c);
+    });
+}
+
+int skygpu_normalize(const double* vals, uint64_t n, int d, double* out, char* err,
+                     size_t errlen) {
+    return guarded(err, errlen, [&] {
+        if (d < 1 || d > kMaxDims) invalid("normalize: dims must be in [1, 32]");
+        if (n == 0) return;
+        Ctx& c = ctx();
+        begin_stats(c, nullptr);
+        double* dv = c.buf[B_IN_VALS].as<double>(n * d);
+        double* dout = c.buf[B_PROJ].as<double>(n * d);
+        SKY_CUDA(cudaMemcpyAsync(dv, vals, n * d * sizeof(double), cudaMemcpyHostToDevice,
+                                 c.stream));
+        normalize_device(c, dv, n, d, dout);
+        SKY_CUDA(cudaMemcpyAsync(out, dout, n * d * sizeof(double), cudaMemcpyDeviceToHost,
+                                 c.stream));
+        end_stats(c);
+    });
+}
+
+int skygpu_select_representatives(const double* vals, const int64_t* ids, uint64_t n, int d,
+                                  uint64_t k, uint64_t* out_pos, uint64_t* out_n,
+                                  uint64_t* tests, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        if (d < 1 || d > kMaxDims) invalid("select_representatives: dims must be in [1, 32]");
+        *out_n = 0;
+        *tests = 0;
+        if (n == 0 || k == 0) return;
+        if (n >= 0xFFFFFFFFull) invalid("select_representatives: more than 2^32-1 tuples");
+        Ctx& c = ctx();
+        begin_stats(c, nullptr);
+        double* dv = c.buf[B_IN_VALS].as<double>(n * d);
+        int64_t* di = c.buf[B_IN_IDS].as<int64_t>(n);
+        SKY_CUDA(cudaMemcpyAsync(dv, vals, n * d * sizeof(double), cudaMemcpyHostToDevice,
+                                 c.stream));
+        SKY_CUDA(cudaMemcpyAsync(di, ids, n * sizeof(int64_t), cudaMemcpyHostToDevice, c.stream));
+        const uint64_t kk = k < n ? k : n;
+        uint32_t* picks = c.buf[B_ACC8].as<uint32_t>(kk);
+        auto* t = c.buf[B_ACC9].as<unsigned long long>(1);
+        SKY_CUDA(cudaMemsetAsync(t, 0, sizeof(unsigned long long), c.stream));
+        const uint64_t m = select_representatives_device(c, dv, di, n, d, kk, picks, t);
+        std::vector<uint32_t> h(m);
+        unsigned long long ht = 0;
+        if (m)
+            SKY_CUDA(cudaMemcpyAsync(h.data(), picks, m * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                                     c.stream));
+        SKY_CUDA(cudaMemcpyAsync(&ht, t, sizeof(ht), cudaMemcpyDeviceToHost, c.stream));
+        SKY_CUDA(cudaStreamSynchronize(c.stream));
+        for (uint64_t i = 0; i < m; ++i) out_pos[i] = h[i];
+        *out_n = m;
+        *tests = ht;
         end_stats(c);
     });
 }

@@ -69,7 +69,7 @@ enum BufId {
     B_DEN, B_GTMP0, B_GTMP1, B_OUTPOS, B_PROJ, B_REPS, B_MISC, B_CELLS, B_CSUM,
     B_ORDER, B_AMAX, B_AQ, B_PQ, B_GCODE, B_GCELL, B_GSCODE, B_GSIDX, B_GITEMS, B_GCNT,
     B_ACC0, B_ACC1, B_ACC2, B_ACC3, B_ACC4, B_ACC5, B_ACC6, B_ACC7, B_ACC8, B_ACC9, B_ACC10,
-    B_ACC11, B_ACC12, B_ACC13, B_ACC14, B_ACC15, B_ACC16, B_SEED, B_AMAX2, B_IOTA, B_COUNT
+    B_ACC11, B_ACC12, B_ACC13, B_ACC14, B_ACC15, B_ACC16, B_SEED, B_AMAX2, B_IOTA, B_NORM, B_COUNT
 };
 
 // Device-side scalar slots (one small allocation, read back through pinned memory).
@@ -266,6 +266,14 @@ bool gres_cells_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_ma
 uint64_t sfs_accounting_device(Ctx& c, const double* d_vals, const int64_t* d_ids, uint64_t n,
                                int d, const int32_t* d_gid, uint32_t p, const double* d_reps,
                                uint32_t nr, unsigned long long* d_per_group, uint32_t* d_kept);
+
+// ingest.cu: min-max normalisation (harness.cpp:161-177), bit-exact; and the
+// representative selection (partition.cpp:229-271): writes the kept picks'
+// positions in (sum, id) order, adds the pruning tests to *d_tests
+void normalize_device(Ctx& c, const double* d_in, uint64_t n, int d, double* d_out);
+uint64_t select_representatives_device(Ctx& c, const double* d_vals, const int64_t* d_ids,
+                                       uint64_t n, int d, uint64_t k, uint32_t* d_out,
+                                       unsigned long long* d_tests);
 
 // float64 AoS -> SoA transpose on the device
 void aos_to_soa(Ctx& c, const double* d_aos, uint64_t n, int d, double* d_soa);

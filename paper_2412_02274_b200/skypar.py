@@ -32,6 +32,7 @@ SKYGPU_OK, SKYGPU_EINVAL, SKYGPU_ERUNTIME, SKYGPU_ECUDA, SKYGPU_ENOMEM = range(5
 GRES_AUTO, GRES_PAIRS, GRES_CELLS = 0, 1, 2
 DEVICE_PTRS, CHECK_SKYLINE, SKIP_GRES = 1, 2, 4
 SKY_AUTO, SKY_ROUNDS, SKY_GRID = 0, 8, 16  # skyline engine flags
+NORMALIZE = 32  # pipeline flag: min-max normalise on the device first
 
 
 class SkyGpuError(RuntimeError):
@@ -112,6 +113,8 @@ def lib() -> C.CDLL:
         L.skygpu_sfs_accounting.argtypes = [vp, vp, u64, i32, vp, i64, vp, u64, vp, vp, vp, vp, vp,
                                             cp, sz]
         L.skygpu_set_collective.argtypes = [vp, vp, cp, sz]
+        L.skygpu_normalize.argtypes = [vp, u64, i32, vp, cp, sz]
+        L.skygpu_select_representatives.argtypes = [vp, vp, u64, i32, u64, vp, vp, vp, cp, sz]
         _lib = L
     return _lib
 
@@ -120,7 +123,7 @@ EXPORTED_SYMBOLS = ("skygpu_version", "skygpu_device_count", "skygpu_set_device"
                     "skygpu_release", "skygpu_make_plan", "skygpu_parallel_skyline",
                     "skygpu_grid_resistance", "skygpu_snap_relation", "skygpu_max_grid_intervals",
                     "skygpu_pipeline", "skygpu_generate", "skygpu_sfs_accounting",
-                    "skygpu_set_collective")
+                    "skygpu_set_collective", "skygpu_normalize", "skygpu_select_representatives")
 
 
 def _check(rc: int, err: C.Array) -> None:
@@ -258,7 +261,7 @@ class PipelineResult:
 def pipeline(values, ids=None, plan: PartitionPlan | None = None, cap: int | None = 25,
              engine: int = GRES_AUTO, shard_rank: int = 0, shard_world: int = 1,
              check_skyline: bool = False, skip_gres: bool = False,
-             sky_engine: int = SKY_AUTO) -> PipelineResult:
+             sky_engine: int = SKY_AUTO, normalize: bool = False) -> PipelineResult:
     """Skyline + grid resistance in one call (harness.cpp:208, :229-231).
     ``sky_engine`` forces the prefix-round (SKY_ROUNDS) or one-pass rank-grid
     (SKY_GRID) skyline engine; the default picks by the first round's yield."""
@@ -272,6 +275,7 @@ def pipeline(values, ids=None, plan: PartitionPlan | None = None, cap: int | Non
     st = Stats()
     err = _errbuf()
     flags = (CHECK_SKYLINE if check_skyline else 0) | (SKIP_GRES if skip_gres else 0) | int(sky_engine)
+    flags |= NORMALIZE if normalize else 0
     _check(lib().skygpu_pipeline(_p(v), _p(i), n, d, C.byref(plan._c()), 0 if cap is None else int(cap),
                                  int(engine), int(shard_rank), int(shard_world), flags, _p(pos), _p(den),
                                  _p(s), _p(gm), C.byref(st), err, 1024), err)
@@ -379,3 +383,27 @@ def set_collective(fn=None) -> None:
 
     _collective_ref = COLLECTIVE_FN(tramp)
     _check(lib().skygpu_set_collective(C.cast(_collective_ref, C.c_void_p), None, err, 1024), err)
+
+
+def normalize(values) -> np.ndarray:
+    """harness.cpp:161-177 normalize on the device (bit-identical)."""
+    v = np.ascontiguousarray(values, dtype=np.float64)
+    n, d = v.shape
+    out = np.empty_like(v)
+    err = _errbuf()
+    _check(lib().skygpu_normalize(_p(v), n, d, _p(out), err, 1024), err)
+    return out
+
+
+def select_representatives(values, ids=None, k: int = 1):
+    """partition.cpp:249-271 with sum_score on the device: (positions of the
+    kept picks in (sum, id) order, the pruning's dominance-test count)."""
+    v, i = _relation(values, ids)
+    n, d = v.shape
+    pos = np.empty(max(min(int(k), n), 1), dtype=np.uint64)
+    cnt = np.zeros(1, dtype=np.uint64)
+    tests = np.zeros(1, dtype=np.uint64)
+    err = _errbuf()
+    _check(lib().skygpu_select_representatives(_p(v), _p(i), n, d, int(k), _p(pos), _p(cnt),
+                                                _p(tests), err, 1024), err)
+    return pos[:int(cnt[0])].astype(np.int64), int(tests[0])

@@ -394,3 +394,63 @@ def test_sharded_gres_exchange_returns_full_map():
     assert (recorded[0].cpu().numpy() == 0).any()  # rank 1 left rank 0's tuples at 0
     assert out.positions.tolist() == full.positions.tolist()
     assert out.den.tolist() == full.den.tolist()
+
+
+# ------------------------------------------------ device-side input preparation
+def _np_normalize(v):
+    """harness.cpp:161-177 in numpy: std::min/std::max keep the FIRST of equal
+    candidates, so a zero minimum carries the sign of the first zero."""
+    out = np.zeros_like(v)
+    for j in range(v.shape[1]):
+        col = v[:, j]
+        lo, hi = np.inf, -np.inf
+        for x in col:  # literal left-to-right std::min / std::max
+            lo = x if x < lo else lo
+            hi = x if hi < x else hi
+        out[:, j] = (col - lo) / (hi - lo) if hi > lo else 0.0
+    return out
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_normalize_bit_identical(seed):
+    rng = np.random.default_rng(seed)
+    v = rng.random((3000, 5)) * [1, 10, 1e-300, 7, 1]
+    v[:, 3] = 7.0                      # constant attribute -> 0
+    v[5, 4], v[10, 4], v[20, 4] = 0.0, -0.0, 0.0   # zero minimum, first zero +0.0
+    v[2, 0] = -0.0                     # zero minimum, first zero -0.0
+    v[7, 0] = 0.0
+    got = sk.normalize(v)
+    want = _np_normalize(v)
+    assert got.tobytes() == want.tobytes()
+
+
+@pytest.mark.parametrize("gen,n,d,k", [("ant", 5000, 3, 10), ("uni", 3000, 4, 100),
+                                       ("lattice", 2000, 3, 25), ("ant", 50, 2, 100)])
+def test_select_representatives_matches_reference_rule(gen, n, d, k):
+    v = sk.generate(gen, n, d, 7)
+    rng = np.random.default_rng(7)
+    ids = rng.permutation(5 * n)[:n].astype(np.int64)
+    pos, tests = sk.select_representatives(v, ids, k)
+    s = np.array([sum(row) for row in v.tolist()])  # left-to-right sums
+    picked = np.lexsort((ids, s))[:min(k, n)]
+    want, want_tests = [], 0
+    for i in picked:  # partition.cpp:229-245
+        dom = False
+        for j in picked:
+            if j == i:
+                continue
+            want_tests += 1
+            if np.all(v[j] <= v[i]) and np.any(v[j] < v[i]):
+                dom = True
+                break
+        if not dom:
+            want.append(int(i))
+    assert pos.tolist() == want and tests == want_tests
+
+
+def test_pipeline_normalize_flag_equals_normalized_input():
+    v = sk.generate("ant", 20000, 3, 4) * [3.0, 0.5, 100.0]
+    a = sk.pipeline(v, cap=25, normalize=True)
+    b = sk.pipeline(_np_normalize(v), cap=25)
+    assert a.positions.tolist() == b.positions.tolist()
+    assert a.g_max == b.g_max and a.den.tolist() == b.den.tolist()
