@@ -19,15 +19,17 @@
 // So at step g, t is ejected iff some skyline tuple's code vector dominates
 // t's — every skyline tuple is a comparator; no order bookkeeping.
 //
-// Pair engine (the dominance-test kernel the metric counts): one launch per
-// g over the still-undecided candidates (descending g, exit at the first
-// dominating step), comparators streamed through shared-memory tiles.
-//  - u8 path (d <= 8, max code <= 127): a tuple's codes at step g packed one
-//    byte per attribute in a u64; one test = SWAR subtract + mask + compare
-//    (dom_u8), 4 candidates per thread share each broadcast LDS.64.
-//  - f64 path (anything else): the reference's own projections
-//    floor(v*g)/g compared as float64, with the exact (psum, id) order check
-//    when ties are possible.
+// Engines:
+//  - pair engine, u8 codes (d <= 8, max code <= 127): a tuple's codes of
+//    every step packed one byte per attribute (u32 words for d <= 4, u64 for
+//    d <= 8); ONE launch covers all steps — the resident kernel (all steps'
+//    codes of a comparator range staged once in shared memory, S <= 2^21) or
+//    the tiled one; one test = SWAR subtract + mask + compare; a candidate
+//    leaves at its first (largest) dominating step.
+//  - cell engine (cells.cu), same codes, O(cells + S) per step: huge S.
+//  - f64 path (anything else): one launch per step on the reference's own
+//    projections floor(v*g)/g compared as float64, with the exact (psum, id)
+//    order check when ties are possible.
 #include <cub/cub.cuh>
 
 #include <cmath>
@@ -140,21 +142,6 @@ k_check_skyline(const double* __restrict__ v, uint64_t S, int d,
     }
 }
 
-// codes at step g, one byte per attribute: k = floor(v*g) (gres.cpp:46)
-__global__ void k_codes_u8(const double* __restrict__ v, uint64_t S, int d, int g,
-                           unsigned long long* __restrict__ codes) {
-    const double gd = (double)g;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < S;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        unsigned long long w = 0;
-        for (int k = 0; k < d; ++k) {
-            double q = floor(__dmul_rn(v[k * S + i], gd));
-            w |= (unsigned long long)(unsigned)q << (8 * k);
-        }
-        codes[i] = w;
-    }
-}
-
 // projections at step g exactly as the reference: floor(v*g)/g (gres.cpp:46)
 __global__ void k_project(const double* __restrict__ v, uint64_t total, int g,
                           double* __restrict__ q) {
@@ -179,62 +166,6 @@ __global__ void k_fill_den(const uint32_t* __restrict__ act, uint64_t na, int va
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < na;
          i += (uint64_t)gridDim.x * blockDim.x)
         den[act[i]] = value;
-}
-
-// ---- pair engine, u8 path ---------------------------------------------
-constexpr int kTileU8 = 2048;
-constexpr int kCandU8 = 4;
-
-__global__ void __launch_bounds__(kBlock)
-k_gres_pairs_u8(const unsigned long long* __restrict__ codes, uint32_t S,
-                const uint32_t* __restrict__ act, uint32_t na, int g,
-                int32_t* __restrict__ den, uint8_t* __restrict__ still,
-                unsigned long long* __restrict__ tests) {
-    __shared__ unsigned long long tile[kTileU8];
-    unsigned long long tc[kCandU8], tg[kCandU8];
-    uint32_t ti[kCandU8];
-    bool alive[kCandU8];
-    const uint32_t base_i = blockIdx.x * (kBlock * kCandU8);
-#pragma unroll
-    for (int c = 0; c < kCandU8; ++c) {
-        const uint32_t idx = base_i + c * kBlock + threadIdx.x;
-        alive[c] = idx < na;
-        ti[c] = alive[c] ? act[idx] : 0;
-        tc[c] = alive[c] ? codes[ti[c]] : 0;
-        tg[c] = tc[c] | kGuard;
-    }
-    unsigned long long cnt = 0;
-    bool any = alive[0] | alive[1] | alive[2] | alive[3];
-    for (uint32_t base = 0; base < S; base += kTileU8) {
-        const uint32_t nt = min((uint32_t)kTileU8, S - base);
-        for (uint32_t k = threadIdx.x; k < nt; k += kBlock) tile[k] = codes[base + k];
-        __syncthreads();
-        if (any) {
-            for (uint32_t k0 = 0; k0 < nt; k0 += 32) {
-                const uint32_t k1 = min(nt, k0 + 32);
-                for (uint32_t k = k0; k < k1; ++k) {
-                    const unsigned long long s = tile[k];
-#pragma unroll
-                    for (int c = 0; c < kCandU8; ++c) {
-                        cnt += alive[c];
-                        alive[c] &= !dom_u8(s, tc[c], tg[c]);
-                    }
-                }
-                any = alive[0] | alive[1] | alive[2] | alive[3];
-                if (!any) break;
-            }
-        }
-        if (!__syncthreads_or(any)) break;
-    }
-#pragma unroll
-    for (int c = 0; c < kCandU8; ++c) {
-        const uint32_t idx = base_i + c * kBlock + threadIdx.x;
-        if (idx < na) {
-            still[idx] = alive[c];
-            if (!alive[c]) den[ti[c]] = g;
-        }
-    }
-    add_count(tests, cnt);
 }
 
 // ---- pair engine, u8 path, all steps in ONE launch ----------------------
@@ -809,34 +740,23 @@ GresOut gres_device(Ctx& c, const double* d_skyv, const int64_t* d_ids, uint64_t
         st.gres_kernel_launches += 1;
         return out;
     }
-    unsigned long long* codes = u8 ? c.buf[B_CODES].as<unsigned long long>(S) : nullptr;
-    double* q = u8 ? nullptr : c.buf[B_PROJ].as<double>(S * d);
+    // float64 path (codes above 127, d > 8, or projected-sum ties possible):
+    // one step at a time on the reference's own projections floor(v*g)/g
+    double* q = c.buf[B_PROJ].as<double>(S * d);
     for (int g = out.g_max; g >= 2 && na > 0; --g) {
         ++steps;
-        if (u8) {
-            k_codes_u8<<<gb, kBlock, 0, c.stream>>>(d_skyv, S, d, g, codes);
-            SKY_LAUNCH_CHECK();
-            const unsigned blocks = (unsigned)((na + kBlock * kCandU8 - 1) / (kBlock * kCandU8));
+        k_project<<<grid_for(S * d, kBlock), kBlock, 0, c.stream>>>(d_skyv, S * d, g, q);
+        SKY_LAUNCH_CHECK();
+        dispatch_d(d, [&](auto DC) {
+            constexpr int D = decltype(DC)::value;
+            const size_t smem = sizeof(double) * (D > 0 ? 256 : 128) * (D > 0 ? D : d);
             SKY_CUDA(cudaEventRecord(e0, c.stream));
-            k_gres_pairs_u8<<<blocks, kBlock, 0, c.stream>>>(codes, (uint32_t)S, act,
-                                                             (uint32_t)na, g, d_den, still,
-                                                             c.d_slots + S_TESTS_GRES);
+            k_gres_pairs_f64<D><<<grid_for(na, kBlock, 1 << 30), kBlock, smem, c.stream>>>(
+                q, (uint32_t)S, d, d_ids, act, (uint32_t)na, g, ties_possible ? 1 : 0, d_den,
+                still, c.d_slots + S_TESTS_GRES);
             SKY_CUDA(cudaEventRecord(e1, c.stream));
-            SKY_LAUNCH_CHECK();
-        } else {
-            k_project<<<grid_for(S * d, kBlock), kBlock, 0, c.stream>>>(d_skyv, S * d, g, q);
-            SKY_LAUNCH_CHECK();
-            dispatch_d(d, [&](auto DC) {
-                constexpr int D = decltype(DC)::value;
-                const size_t smem = sizeof(double) * (D > 0 ? 256 : 128) * (D > 0 ? D : d);
-                SKY_CUDA(cudaEventRecord(e0, c.stream));
-                k_gres_pairs_f64<D><<<grid_for(na, kBlock, 1 << 30), kBlock, smem, c.stream>>>(
-                    q, (uint32_t)S, d, d_ids, act, (uint32_t)na, g, ties_possible ? 1 : 0,
-                    d_den, still, c.d_slots + S_TESTS_GRES);
-                SKY_CUDA(cudaEventRecord(e1, c.stream));
-            });
-            SKY_LAUNCH_CHECK();
-        }
+        });
+        SKY_LAUNCH_CHECK();
         note_launch(c, 2);
         na = select_flagged(c, act, still, act2, na);
         std::swap(act, act2);

@@ -545,39 +545,6 @@ k_cell_order(const double* __restrict__ v, int d, const uint32_t* __restrict__ i
     }
 }
 
-template <int D>
-__global__ void k_cells_of(const double* __restrict__ v, int d, const uint32_t* __restrict__ in,
-                           uint32_t m, int mcell, const unsigned long long* __restrict__ amax,
-                           uint32_t* __restrict__ cell) {
-    constexpr int DM = D > 0 ? D : kMaxDims;
-    const int dd = D > 0 ? D : d;
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
-        double t[DM];
-        const uint64_t p = in[i];
-#pragma unroll
-        for (int k = 0; k < DM; ++k)
-            if (k < dd) t[k] = v[p * dd + k];
-        cell[i] = plan_cell<DM>(t, dd, mcell, amax);
-    }
-}
-
-// seg[c] = first position of cell >= c in a cell-sorted list of *count items
-__global__ void k_cell_segments(const uint32_t* __restrict__ ckey,
-                                const unsigned long long* __restrict__ count, uint32_t ncells,
-                                uint32_t* __restrict__ seg) {
-    const uint32_t mcount = (uint32_t)*count;
-    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c <= ncells;
-         c += gridDim.x * blockDim.x) {
-        uint32_t lo = 0, hi = mcount;
-        while (lo < hi) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (ckey[mid] < c) lo = mid + 1;
-            else hi = mid;
-        }
-        seg[c] = lo;
-    }
-}
-
 // compact SoA copy [d][cap] of the tuples list[0..m) from the AoS input; the
 // count is read from device memory when `count` is given (no host sync)
 __global__ void k_gather_aos(const double* __restrict__ v, int d, const uint32_t* __restrict__ list,
@@ -722,77 +689,6 @@ k_sfs_intra_sorted(const double* __restrict__ Av, uint32_t m, int d, uint8_t* __
             }
         }
         if (lane == 0) keep[i] = dominated ? 0 : 1;
-    }
-    add_count(tests, cnt);
-}
-
-// K4: warp-per-candidate decision of the prefix.  The prefix is in cell
-// order (list P, SoA values Av[d][m], cell keys); candidate i scans all
-// members starting in its own cell and wrapping around; a dominance hit
-// counts only when the dominator precedes it (dominance already implies
-// key_j <= key_i, so only exact sum ties need the id check).
-template <int D>
-__global__ void __launch_bounds__(kBlock)
-k_sfs_intra_cells(const double* __restrict__ Av, const uint32_t* __restrict__ P, uint32_t m,
-                  int d, const unsigned long long* __restrict__ key,
-                  const int64_t* __restrict__ ids, const uint32_t* __restrict__ cellof,
-                  const uint32_t* __restrict__ seg, uint8_t* __restrict__ keep,
-                  unsigned long long* __restrict__ tests, uint32_t bs) {
-    constexpr int DM = D > 0 ? D : kMaxDims;
-    const int dd = D > 0 ? D : d;
-    const uint32_t lane = threadIdx.x & 31;
-    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-    unsigned long long cnt = 0;
-    for (uint32_t base = warp * bs; base < m; base += nwarps * bs) {
-        const uint32_t idx = base + lane;
-        const bool valid = lane < bs && idx < m;
-        double t[DM];
-#pragma unroll
-        for (int k = 0; k < DM; ++k)
-            if (k < dd) t[k] = valid ? Av[(uint64_t)k * m + idx] : 0.0;
-        const uint32_t p = valid ? P[idx] : 0;
-        const unsigned long long kt = valid ? key[p] : 0;
-        const int64_t it = valid ? ids[p] : 0;
-        const uint32_t start = (valid && seg) ? seg[cellof[idx]] : 0;
-        bool mykeep = valid;
-        unsigned todo = __ballot_sync(0xffffffffu, valid);
-        while (todo) {
-            const int j = __ffs(todo) - 1;
-            todo &= todo - 1;
-            double tj[DM];
-#pragma unroll
-            for (int k = 0; k < DM; ++k)
-                if (k < dd) tj[k] = __shfl_sync(0xffffffffu, t[k], j);
-            const unsigned long long ktj = __shfl_sync(0xffffffffu, kt, j);
-            const int64_t itj = __shfl_sync(0xffffffffu, it, j);
-            uint32_t q = __shfl_sync(0xffffffffu, start, j) + lane;
-            if (q >= m) q -= m;
-            bool dominated = false;
-            for (uint32_t done = 0; done < m; done += 32) {
-                bool hit = false;
-                if (done + lane < m) {
-                    double s[DM];
-#pragma unroll
-                    for (int k = 0; k < DM; ++k)
-                        if (k < dd) s[k] = Av[(uint64_t)k * m + q];
-                    hit = D > 0 ? dom_f64<(D > 0 ? D : 1)>(s, tj) : dom_f64_dyn(s, tj, dd);
-                    if (hit) {
-                        const uint32_t pq = P[q];
-                        hit = precedes(key[pq], ids[pq], ktj, itj);
-                    }
-                    ++cnt;
-                }
-                if (__any_sync(0xffffffffu, hit)) {
-                    dominated = true;
-                    break;
-                }
-                q += 32;
-                if (q >= m) q -= m;
-            }
-            if ((int)lane == j) mykeep = !dominated;
-        }
-        if (valid) keep[idx] = mykeep ? 1 : 0;
     }
     add_count(tests, cnt);
 }
