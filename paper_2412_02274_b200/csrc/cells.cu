@@ -107,11 +107,12 @@ constexpr uint32_t kSlabWords = 4096;
 
 template <class W>
 __global__ void __launch_bounds__(kBlock)
-k_cells_or_slab(W* __restrict__ rows, uint64_t nrows, uint32_t e1, uint32_t e2) {
+k_cells_or_slab(W* __restrict__ rows, uint64_t nrows, uint32_t e1, uint32_t e2,
+                uint32_t slab_words) {
     extern __shared__ unsigned char smraw[];
     W* sm = reinterpret_cast<W*>(smraw);
     const uint32_t slab = e1 * e2;
-    const uint32_t spb = max(1u, kSlabWords / slab);
+    const uint32_t spb = max(1u, slab_words / slab);
     const uint64_t nslabs = nrows / slab;
     for (uint64_t s0 = (uint64_t)blockIdx.x * spb; s0 < nslabs; s0 += (uint64_t)gridDim.x * spb) {
         const uint32_t ns = (uint32_t)min((uint64_t)spb, nslabs - s0);
@@ -324,25 +325,30 @@ void sweeps(Ctx& c, W* R, const CellGeom& geo, bool fused) {
         note_launch(c);
     };
     const uint32_t e1 = d >= 2 ? (uint32_t)geo.ext[1] : 1, e2 = d >= 3 ? (uint32_t)geo.ext[2] : 1;
-    if (!fused || d < 2 || (uint64_t)e1 * e2 > kSlabWords) {
+    if (!fused || d < 2 || (uint64_t)e1 * e2 * sizeof(W) > 128 * 1024) {
         k_cells_or_word<W><<<grid_for(geo.rows, kBlock), kBlock, 0, c.stream>>>(R, geo.rows);
         note_launch(c);
         for (int j = 1; j < d; ++j) single(j);
         return;
     }
-    const uint32_t slab = e1 * e2, spb = std::max(1u, kSlabWords / slab);
+    static const uint32_t slab_words = [] {
+        const char* e = getenv("SKYGPU_SLAB_WORDS");
+        const int v = e ? atoi(e) : 0;
+        return v >= 1024 && v <= 16384 ? (uint32_t)v : kSlabWords;
+    }();
+    const uint32_t slab = e1 * e2, spb = std::max(1u, slab_words / slab);
     const size_t smem = (size_t)spb * slab * sizeof(W);
     static bool attr_set = false;
     if (!attr_set) {
         SKY_CUDA(cudaFuncSetAttribute(k_cells_or_slab<unsigned>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
         SKY_CUDA(cudaFuncSetAttribute(k_cells_or_slab<unsigned long long>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
         attr_set = true;
     }
     const uint64_t nslabs = geo.rows / slab;
     k_cells_or_slab<W><<<grid_for((nslabs + spb - 1) / spb, 1, c.num_sms * 8), kBlock, smem,
-                         c.stream>>>(R, geo.rows, e1, e2);
+                         c.stream>>>(R, geo.rows, e1, e2, slab_words);
     note_launch(c);
     int j = 3;
     while (j < d) {
