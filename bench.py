@@ -315,7 +315,7 @@ def our_arm(args):
                    "skyline_engine": {8: "prefix rounds", 16: "rank grid"}.get(stats[-1]["sky_engine"], "?")},
         "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": n * d * 8 + n * 8,
-                "d2h_bytes_per_step": S * 4 + S * 4},
+                "d2h_bytes_per_step": S * 8 + S * 4},  # u64 positions + i32 denominators
         "gpu_launches": int(sum(s["kernel_launches"] for s in stats)),
         "roofline": roof,
         "clocks": clk,
