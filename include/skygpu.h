@@ -17,6 +17,8 @@
  *                                 (proj/src/harness.cpp:208 then :229-231)
  *   skygpu_sfs_accounting      <- the DominanceCounter totals inside
  *                                 parallel_skyline (parallel.cpp:59-93)
+ *   skygpu_read_csv            <- skypar::read_dataset_csv     include/skypar/harness.hpp
+ *   skygpu_pipeline_csv        <- run_experiment with --dataset (harness.cpp:191-231)
  *   skygpu_normalize           <- skypar::normalize            include/skypar/harness.hpp
  *   skygpu_select_representatives <- skypar::select_representatives partition.hpp
  *   skygpu_set_collective      <- (no reference counterpart: the reference is
@@ -202,6 +204,30 @@ int skygpu_normalize(const double* vals, uint64_t n, int d, double* out, char* e
 int skygpu_select_representatives(const double* vals, const int64_t* ids, uint64_t n, int d,
                                   uint64_t k, uint64_t* out_pos, uint64_t* out_n,
                                   uint64_t* tests, char* err, size_t errlen);
+
+/* harness.cpp:93-134 read_dataset_csv on the device: `bytes` = the whole file
+ * (len bytes), `name` = the path used in error texts.  The header line fixes
+ * the width; empty lines are skipped; ids are row order.  On success
+ * out_vals[0 .. rows*dims) holds the relation (row-major) — out_vals must hold
+ * `out_cap` doubles ((len + 1) / 2 always suffices) — and *out_rows/*out_dims
+ * are set.  Format errors return SKYGPU_ERUNTIME with the reference's exact
+ * text (runtime_error); a too-small buffer returns SKYGPU_EINVAL with
+ * *out_rows/*out_dims set. */
+int skygpu_read_csv(const char* bytes, uint64_t len, const char* name, double* out_vals,
+                    uint64_t out_cap, uint64_t* out_rows, int* out_dims, char* err,
+                    size_t errlen);
+
+/* run_experiment with --dataset (harness.cpp:191-208, :229-231) on the device:
+ * the CSV parsed by skygpu_read_csv's parser without leaving the GPU, the
+ * plan sized for the file's width (make_plan(strategy, target, dims)), then
+ * the skyline + grid-resistance pipeline (flags as skygpu_pipeline, incl.
+ * SKYGPU_NORMALIZE for --normalize; outputs are HOST buffers of out_cap
+ * tuples).  *out_rows / *out_dims give the relation's shape. */
+int skygpu_pipeline_csv(const char* bytes, uint64_t len, const char* name, int strategy,
+                        long long target_partitions, int cap, int gres_engine, unsigned flags,
+                        uint64_t* out_pos, int32_t* out_den, uint64_t out_cap, uint64_t* out_s,
+                        int* out_g_max, uint64_t* out_rows, int* out_dims, skygpu_stats* stats,
+                        char* err, size_t errlen);
 
 /* Product-side seeded generators (bit-exact with proj/src/datagen.cpp:41-94;
  * kind 0 uni, 1 ant, 2 corr = BASELINE C3, 3 lattice = test_util.hpp:38-54).

@@ -9,6 +9,10 @@
 //            print the results as one JSON object (sorted skyline ids, the
 //            skyline in output order, g_max, the denominators map, per-g rows).
 //   dump   : write the generated input as raw float64 (generator parity).
+//   csv    : parse --input with the reference's load_dataset_csv
+//            (harness.cpp:93-134) and print the relation (value bits in hex,
+//            ids) or the exception text — golden vectors for the device CSV
+//            parser.
 //   bench  : time parallel_skyline + grid_resistance with steady_clock on the
 //            given core budget, the way proj/tools/bench_main.cpp:66-101 does,
 //            generation excluded; print one JSON line.
@@ -33,6 +37,7 @@
 
 #include "skypar/datagen.hpp"
 #include "skypar/gres.hpp"
+#include "skypar/harness.hpp"
 #include "skypar/oracle.hpp"
 #include "skypar/parallel.hpp"
 
@@ -294,6 +299,45 @@ int run_bench(const Args& a) {
     return 0;
 }
 
+std::string json_escape(const std::string& in) {
+    std::string out;
+    for (unsigned char ch : in) {
+        if (ch == '"' || ch == '\\') {
+            out += '\\';
+            out += (char)ch;
+        } else if (ch < 0x20 || ch >= 0x7f) {
+            char buf[8];
+            std::snprintf(buf, sizeof(buf), "\\u%04x", ch);
+            out += buf;
+        } else {
+            out += (char)ch;
+        }
+    }
+    return out;
+}
+
+int run_csv(const Args& a) {
+    try {
+        const Relation r = load_dataset_csv(a.input);
+        std::printf("{\"rows\":%zu,\"dims\":%zu,\"ids\":[", r.size(), r.dims);
+        for (std::size_t i = 0; i < r.size(); ++i)
+            std::printf("%s%lld", i ? "," : "", (long long)r.tuples[i].id);
+        std::printf("],\"bits\":[");
+        bool first = true;
+        for (const Tuple& t : r.tuples)
+            for (double v : t.values) {
+                std::uint64_t b;
+                std::memcpy(&b, &v, 8);
+                std::printf("%s\"%016llx\"", first ? "" : ",", (unsigned long long)b);
+                first = false;
+            }
+        std::printf("]}\n");
+    } catch (const std::exception& e) {
+        std::printf("{\"csv_error\":\"%s\"}\n", json_escape(e.what()).c_str());
+    }
+    return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -302,6 +346,7 @@ int main(int argc, char** argv) {
         if (a.mode == "golden") return run_golden(a);
         if (a.mode == "bench") return run_bench(a);
         if (a.mode == "dump") return run_dump(a);
+        if (a.mode == "csv") return run_csv(a);
         throw std::runtime_error("unknown --mode " + a.mode);
     } catch (const std::exception& e) {
         std::printf("{\"error\":\"%s\"}\n", e.what());

@@ -4,6 +4,7 @@ this package is the host-side mirror of the reference interface."""
 from .skypar import (  # noqa: F401
     GRES_AUTO, GRES_CELLS, GRES_PAIRS, SKY_AUTO, SKY_GRID, SKY_ROUNDS, GridResistanceResult, PartitionPlan, SkyGpuError,
     SkylineResult, Strategy, device_count, generate, grid_resistance, make_plan,
-    max_grid_intervals, normalize, parallel_skyline, pipeline, select_representatives, sfs_accounting,
+    load_dataset_csv, max_grid_intervals, normalize, parallel_skyline, pipeline_csv,
+    read_csv_bytes, pipeline, select_representatives, sfs_accounting,
     snap_relation, snap_to_grid,
 )

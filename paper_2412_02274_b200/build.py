@@ -25,7 +25,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC",
                      "-Xcompiler", "-ffp-contract=off", "-ccbin", HOST_CXX, "-I", INCLUDE,
                      "-I", CSRC, "--expt-relaxed-constexpr"]
-CU_SOURCES = ["skyline.cu", "skyline_grid.cu", "gres.cu", "cells.cu", "accounting.cu", "ingest.cu", "abi.cu"]
+CU_SOURCES = ["skyline.cu", "skyline_grid.cu", "gres.cu", "cells.cu", "accounting.cu", "ingest.cu", "csv.cu",
+              "abi.cu"]
 CXX_SOURCES = ["hostgen.cpp"]
 
 

@@ -277,6 +277,11 @@ __global__ void k_widen(const uint32_t* __restrict__ a, uint64_t* __restrict__ b
 }  // namespace
 
 namespace {
+__global__ void k_iota64(int64_t* __restrict__ a, uint64_t n) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        a[i] = (int64_t)i;
+}
 __global__ void k_fill_i32(int32_t* __restrict__ a, uint64_t n, int32_t v) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x)
@@ -299,6 +304,12 @@ void shard_allreduce_max(Ctx& c, void* dev_ptr, uint64_t count, int elem_bytes) 
                                          std::to_string(rc) + ")");
 }
 
+void iota64(Ctx& c, int64_t* a, uint64_t n) {
+    k_iota64<<<grid_for(n, 256), 256, 0, c.stream>>>(a, n);
+    SKY_LAUNCH_CHECK();
+    note_launch(c);
+}
+
 void widen_u32_u64(Ctx& c, const uint32_t* a, uint64_t* b, uint64_t n) {
     k_widen<<<grid_for(n, 256), 256, 0, c.stream>>>(a, b, n);
     SKY_LAUNCH_CHECK();
@@ -315,6 +326,9 @@ void aos_to_soa(Ctx& c, const double* d_aos, uint64_t n, int d, double* d_soa) {
 }  // namespace skygpu
 
 using namespace skygpu;
+
+// internal pipeline flag: inputs already on the device, outputs to the host
+static constexpr unsigned kInputsOnDevice = 1u << 30;
 
 extern "C" {
 
@@ -527,6 +541,8 @@ int skygpu_pipeline(const double* vals, const int64_t* ids, uint64_t n, int d,
         skygpu_plan pl = plan ? *plan : skygpu_plan{SKYGPU_NONE, 1, 1, d};
         Ctx& c = ctx();
         begin_stats(c, stats);
+        // kInputsOnDevice (internal): device inputs, host outputs (the CSV path)
+        const bool dev_in = flags & (SKYGPU_DEVICE_PTRS | kInputsOnDevice);
         const bool dev = flags & SKYGPU_DEVICE_PTRS;
         *out_s = 0;
         *out_g_max = 1;
@@ -547,10 +563,10 @@ int skygpu_pipeline(const double* vals, const int64_t* ids, uint64_t n, int d,
         }();
         // (worth it only when the tail's copy outlasts the head's decision,
         // ~0.5 ms: from ~48 MB of input on)
-        const bool streamed = !dev && overlap_env && !(flags & SKYGPU_NORMALIZE) &&
+        const bool streamed = !dev_in && overlap_env && !(flags & SKYGPU_NORMALIZE) &&
                               n * (uint64_t)(d + 1) * 8 >= (48ull << 20) &&
                               d <= 8 && pl.strategy != SKYGPU_GRID && !(flags & SKYGPU_SKY_GRID);
-        if (!dev) {
+        if (!dev_in) {
             Timer h2d(c, 2);
             double* bv = c.buf[B_IN_VALS].as<double>(n * d);
             int64_t* bi = c.buf[B_IN_IDS].as<int64_t>(n);
@@ -645,6 +661,126 @@ int skygpu_pipeline(const double* vals, const int64_t* ids, uint64_t n, int d,
         *out_g_max = go.g_max;
         end_stats(c);
     });
+}
+
+// the CSV bytes parsed on the device (harness.cpp:93-134); throws the
+// reference's runtime_error texts; returns the device values (rows x dims)
+static double* csv_to_device(Ctx& c, const char* bytes, uint64_t len, const std::string& nm,
+                             uint64_t* rows_out, int* dims_out) {
+    // header (harness.cpp:94-100): the first getline; its width fixes dims
+    if (len == 0) throw Error(SKYGPU_ERUNTIME, nm + ": empty file, expected a header line");
+    uint64_t h = 0;
+    int commas = 0;
+    bool content = false;
+    for (; h < len && bytes[h] != '\n'; ++h) {
+        commas += bytes[h] == ',';
+        content |= bytes[h] != ',' && bytes[h] != '\r';
+    }
+    if (commas == 0 && !content) throw Error(SKYGPU_ERUNTIME, nm + ": header line has no columns");
+    const int dims = commas + 1;
+    *dims_out = dims;
+    char* db = c.buf[B_CSV].as<char>(len);
+    SKY_CUDA(cudaMemcpyAsync(db, bytes, len, cudaMemcpyHostToDevice, c.stream));
+    const uint64_t cap = (len + 1) / 2 + 1;
+    double* dv = c.buf[B_CSVVAL].as<double>(cap);
+    uint64_t rows = 0, eline = 0;
+    int ecol = 0, ekind = 0, internal = 0;
+    const int rc = csv_parse_device(c, db, len, dims, &rows, dv, cap, &eline, &ecol, &ekind,
+                                    &internal);
+    *rows_out = rows;
+    if (internal) throw Error(SKYGPU_ERUNTIME, nm + ": a field exceeds the device parser's limits");
+    if (rc == 2) {
+        // the reference's message, from the offending line's bytes
+        uint64_t s = 0, line = 1;
+        while (line < eline && s < len) {
+            if (bytes[s] == '\n') ++line;
+            ++s;
+        }
+        uint64_t e = s;
+        while (e < len && bytes[e] != '\n') ++e;
+        const std::string where = nm + ": line " + std::to_string(eline);
+        if (ekind == 1) {
+            int k = 1;
+            for (uint64_t i = s; i < e; ++i) k += bytes[i] == ',';
+            throw Error(SKYGPU_ERUNTIME, where + ": expected " + std::to_string(dims) +
+                                             " fields, got " + std::to_string(k));
+        }
+        std::string field;
+        int col = 1;
+        for (uint64_t i = s; i < e; ++i) {
+            if (bytes[i] == ',') {
+                if (col == ecol) break;
+                ++col;
+                field.clear();
+            } else if (bytes[i] != '\r') {
+                field += bytes[i];
+            }
+        }
+        const std::string at = where + ", column " + std::to_string(ecol);
+        if (ekind == 2) throw Error(SKYGPU_ERUNTIME, at + ": not a number: '" + field + "'");
+        throw Error(SKYGPU_ERUNTIME, at + ": negative value " + field);
+    }
+    return dv;
+}
+
+int skygpu_read_csv(const char* bytes, uint64_t len, const char* name, double* out_vals,
+                    uint64_t out_cap, uint64_t* out_rows, int* out_dims, char* err,
+                    size_t errlen) {
+    return guarded(err, errlen, [&] {
+        *out_rows = 0;
+        *out_dims = 0;
+        Ctx& c = ctx();
+        begin_stats(c, nullptr);
+        uint64_t rows = 0;
+        int dims = 0;
+        const double* dv = csv_to_device(c, bytes, len, name ? name : "", &rows, &dims);
+        *out_rows = rows;
+        *out_dims = dims;
+        if (rows * (uint64_t)dims > out_cap)
+            invalid("read_csv: output buffer holds " + std::to_string(out_cap) +
+                    " values, need " + std::to_string(rows * (uint64_t)dims));
+        if (rows)
+            SKY_CUDA(cudaMemcpyAsync(out_vals, dv, rows * dims * sizeof(double),
+                                     cudaMemcpyDeviceToHost, c.stream));
+        end_stats(c);
+    });
+}
+
+int skygpu_pipeline_csv(const char* bytes, uint64_t len, const char* name, int strategy,
+                        long long target_partitions, int cap, int gres_engine, unsigned flags,
+                        uint64_t* out_pos, int32_t* out_den, uint64_t out_cap, uint64_t* out_s,
+                        int* out_g_max, uint64_t* out_rows, int* out_dims, skygpu_stats* stats,
+                        char* err, size_t errlen) {
+    uint64_t rows = 0;
+    int dims = 0;
+    double* dv = nullptr;
+    int64_t* di = nullptr;
+    skygpu_plan plan{};
+    const int rc = guarded(err, errlen, [&] {
+        *out_s = 0;
+        *out_g_max = 1;
+        Ctx& c = ctx();
+        begin_stats(c, nullptr);
+        dv = csv_to_device(c, bytes, len, name ? name : "", &rows, &dims);
+        *out_rows = rows;
+        *out_dims = dims;
+        if (rows > out_cap)
+            invalid("pipeline_csv: output buffers hold " + std::to_string(out_cap) +
+                    " tuples, need " + std::to_string(rows));
+        di = c.buf[B_IN_IDS].as<int64_t>(rows ? rows : 1);  // ids = row order
+        if (rows) iota64(c, di, rows);
+        char perr[512];
+        if (skygpu_make_plan(strategy, target_partitions, dims, &plan, perr, sizeof perr) !=
+            SKYGPU_OK)
+            invalid(perr);
+        end_stats(c);
+    });
+    if (rc != SKYGPU_OK) return rc;
+    // the rest of run_experiment on the device-resident relation; results to
+    // the caller's host buffers
+    return skygpu_pipeline(dv, di, rows, dims, &plan, cap, gres_engine, 0, 1,
+                           (flags & ~SKYGPU_DEVICE_PTRS) | kInputsOnDevice, out_pos, out_den,
+                           out_s, out_g_max, stats, err, errlen);
 }
 
 int skygpu_normalize(const double* vals, uint64_t n, int d, double* out, char* err,

@@ -69,7 +69,7 @@ enum BufId {
     B_DEN, B_GTMP0, B_GTMP1, B_OUTPOS, B_PROJ, B_REPS, B_MISC, B_CELLS, B_CSUM,
     B_ORDER, B_AMAX, B_AQ, B_PQ, B_GCODE, B_GCELL, B_GSCODE, B_GSIDX, B_GITEMS, B_GCNT,
     B_ACC0, B_ACC1, B_ACC2, B_ACC3, B_ACC4, B_ACC5, B_ACC6, B_ACC7, B_ACC8, B_ACC9, B_ACC10,
-    B_ACC11, B_ACC12, B_ACC13, B_ACC14, B_ACC15, B_ACC16, B_SEED, B_AMAX2, B_IOTA, B_NORM, B_COUNT
+    B_ACC11, B_ACC12, B_ACC13, B_ACC14, B_ACC15, B_ACC16, B_SEED, B_AMAX2, B_IOTA, B_NORM, B_CSV, B_CSVVAL, B_COUNT
 };
 
 // Device-side scalar slots (one small allocation, read back through pinned memory).
@@ -274,6 +274,14 @@ void normalize_device(Ctx& c, const double* d_in, uint64_t n, int d, double* d_o
 uint64_t select_representatives_device(Ctx& c, const double* d_vals, const int64_t* d_ids,
                                        uint64_t n, int d, uint64_t k, uint32_t* d_out,
                                        unsigned long long* d_tests);
+
+// csv.cu: the reference's read_dataset_csv on the device (data lines only;
+// the header fixes dims).  0 ok; 1 d_vals too small (*rows set); 2 a format
+// error at (*err_line, *err_col, *err_kind: 1 field count, 2 not a number,
+// 3 negative); *internal != 0 when a field exceeded the device parser's limits
+int csv_parse_device(Ctx& c, const char* d_bytes, uint64_t len, int dims, uint64_t* rows,
+                     double* d_vals, uint64_t vals_cap, uint64_t* err_line, int* err_col,
+                     int* err_kind, int* internal);
 
 // float64 AoS -> SoA transpose on the device
 void aos_to_soa(Ctx& c, const double* d_aos, uint64_t n, int d, double* d_soa);

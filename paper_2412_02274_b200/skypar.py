@@ -114,6 +114,9 @@ def lib() -> C.CDLL:
                                             cp, sz]
         L.skygpu_set_collective.argtypes = [vp, vp, cp, sz]
         L.skygpu_normalize.argtypes = [vp, u64, i32, vp, cp, sz]
+        L.skygpu_read_csv.argtypes = [cp, u64, cp, vp, u64, vp, vp, cp, sz]
+        L.skygpu_pipeline_csv.argtypes = [cp, u64, cp, i32, i64, i32, i32, C.c_uint, vp, vp, u64,
+                                          vp, vp, vp, vp, C.POINTER(Stats), cp, sz]
         L.skygpu_select_representatives.argtypes = [vp, vp, u64, i32, u64, vp, vp, vp, cp, sz]
         _lib = L
     return _lib
@@ -123,7 +126,8 @@ EXPORTED_SYMBOLS = ("skygpu_version", "skygpu_device_count", "skygpu_set_device"
                     "skygpu_release", "skygpu_make_plan", "skygpu_parallel_skyline",
                     "skygpu_grid_resistance", "skygpu_snap_relation", "skygpu_max_grid_intervals",
                     "skygpu_pipeline", "skygpu_generate", "skygpu_sfs_accounting",
-                    "skygpu_set_collective", "skygpu_normalize", "skygpu_select_representatives")
+                    "skygpu_set_collective", "skygpu_normalize", "skygpu_select_representatives",
+                    "skygpu_read_csv", "skygpu_pipeline_csv")
 
 
 def _check(rc: int, err: C.Array) -> None:
@@ -407,3 +411,53 @@ def select_representatives(values, ids=None, k: int = 1):
     _check(lib().skygpu_select_representatives(_p(v), _p(i), n, d, int(k), _p(pos), _p(cnt),
                                                 _p(tests), err, 1024), err)
     return pos[:int(cnt[0])].astype(np.int64), int(tests[0])
+
+
+def read_csv_bytes(data: bytes, name: str = ""):
+    """harness.cpp:93-134 read_dataset_csv on the device: (values rows x dims,
+    ids).  Format errors raise RuntimeError with the reference's text (the
+    `name` it reports is the path the reference would print)."""
+    cap = (len(data) + 1) // 2 + 1
+    out = np.empty(cap, dtype=np.float64)
+    rows = np.zeros(1, dtype=np.uint64)
+    dims = np.zeros(1, dtype=np.int32)
+    err = C.create_string_buffer(4096)  # the reference's texts quote the field
+    _check(lib().skygpu_read_csv(data, len(data), name.encode(), _p(out), cap, _p(rows), _p(dims),
+                                 err, 4096), err)
+    r, d = int(rows[0]), int(dims[0])
+    return out[:r * d].reshape(r, d).copy(), np.arange(r, dtype=np.int64)
+
+
+def load_dataset_csv(path: str):
+    """harness.cpp:127-131 load_dataset_csv (the file read on the host, parsed
+    on the device)."""
+    try:
+        with open(path, "rb") as f:
+            data = f.read()
+    except OSError:
+        raise RuntimeError("cannot open dataset file: " + path) from None
+    return read_csv_bytes(data, path)
+
+
+def pipeline_csv(data: bytes, name: str = "", strategy: str = "none", target_partitions: int = 1,
+                 cap: int | None = 25, engine: int = GRES_AUTO, normalize: bool = False):
+    """run_experiment with --dataset on the device: the CSV bytes parsed on the
+    GPU (optionally normalised there) and fed to the pipeline without a host
+    round trip.  Returns (PipelineResult, (rows, dims))."""
+    cap_t = (len(data) + 1) // 2 + 1
+    pos = np.empty(cap_t, dtype=np.uint64)
+    den = np.zeros(cap_t, dtype=np.int32)
+    s = np.zeros(1, dtype=np.uint64)
+    gm = np.zeros(1, dtype=np.int32)
+    rows = np.zeros(1, dtype=np.uint64)
+    dims = np.zeros(1, dtype=np.int32)
+    st = Stats()
+    err = C.create_string_buffer(4096)
+    _check(lib().skygpu_pipeline_csv(data, len(data), name.encode(), int(Strategy.from_name(strategy)),
+                                     int(target_partitions), 0 if cap is None else int(cap),
+                                     int(engine), NORMALIZE if normalize else 0, _p(pos), _p(den),
+                                     cap_t, _p(s), _p(gm), _p(rows), _p(dims), C.byref(st), err,
+                                     4096), err)
+    S = int(s[0])
+    res = PipelineResult(pos[:S].astype(np.int64), den[:S].copy(), int(gm[0]), st.as_dict())
+    return res, (int(rows[0]), int(dims[0]))
