@@ -376,6 +376,13 @@ def roofline(st, sky_ms, gres_ms, d, clk, workload="C2"):
     f = (clk.get("sm_mhz") or 1965.0) * 1e6
 
     def one(kind):
+        if kind == "gres" and st["gres_engine"] == 2 and st["gres_cells"] == 0:
+            # small-grid cell engine: all steps in one launch, grids in shared
+            # memory — no HBM sweeps, no pair tests: launch-latency bound
+            return {"bound": "latency", "kernel": "k_cells_smem", "achieved": None,
+                    "peak": None, "unit": None, "frac": None, "traffic": None,
+                    "kernel_ms_per_step": gres_ms,
+                    "launches_per_step": st["gres_kernel_launches"]}
         if kind == "gres" and st["gres_engine"] == 2:  # cell-occupancy engine: HBM sweeps
             ms = gres_ms
             byts = st["gres_cells"]

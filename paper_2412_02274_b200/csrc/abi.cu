@@ -563,8 +563,12 @@ int skygpu_pipeline(const double* vals, const int64_t* ids, uint64_t n, int d,
         }();
         // (worth it only when the tail's copy outlasts the head's decision,
         // ~0.5 ms: from ~48 MB of input on)
+        static const uint64_t stream_min = [] {  // SKYGPU_STREAM_MIN_MB: tuning override
+            const char* e = getenv("SKYGPU_STREAM_MIN_MB");
+            return (uint64_t)(e ? atoll(e) : 48) << 20;
+        }();
         const bool streamed = !dev_in && overlap_env && !(flags & SKYGPU_NORMALIZE) &&
-                              n * (uint64_t)(d + 1) * 8 >= (48ull << 20) &&
+                              n * (uint64_t)(d + 1) * 8 >= stream_min &&
                               d <= 8 && pl.strategy != SKYGPU_GRID && !(flags & SKYGPU_SKY_GRID);
         if (!dev_in) {
             Timer h2d(c, 2);

@@ -365,6 +365,118 @@ void sweeps(Ctx& c, W* R, const CellGeom& geo, bool fused) {
     }
 }
 
+namespace {
+
+constexpr int kSmemBlock = 512;
+constexpr size_t kSmemGridMax = 200 * 1024;  // bytes of row words per step
+
+// Every step in ONE launch, each step's grid in shared memory (small grids:
+// d <= 4 and code extent e <= 32, so the grid is e^(d-1) u32 row words).
+// blockIdx.y = step (g = g_max - y); every block of a step builds that
+// step's prefix-OR grid from all S tuples (cheap: S shared-memory atomics),
+// then answers its slice of the candidates.  den = the largest g at which t
+// is dominated = the first ejection of the descending scan (atomicMax).
+__global__ void __launch_bounds__(kSmemBlock)
+    k_cells_smem(const double* __restrict__ v, uint32_t S, int d, int g_max, double maxv,
+                 const uint32_t* __restrict__ act, uint32_t na, uint32_t per_block,
+                 int32_t* __restrict__ den) {
+    extern __shared__ uint32_t P[];
+    const int g = g_max - (int)blockIdx.y;
+    const double gd = (double)g;
+    const uint32_t e = (uint32_t)floor(__dmul_rn(maxv, gd)) + 1;  // codes 0 .. e-1
+    uint32_t stride[4] = {0, 1, e, e * e};
+    uint32_t rows = 1;
+    for (int j = 1; j < d; ++j) rows *= e;
+    for (uint32_t w = threadIdx.x; w < rows; w += blockDim.x) P[w] = 0;
+    __syncthreads();
+    auto code = [&](uint32_t i, int j) { return (uint32_t)floor(__dmul_rn(v[(uint64_t)j * S + i], gd)); };
+    for (uint32_t i = threadIdx.x; i < S; i += blockDim.x) {
+        uint32_t r = 0;
+#pragma unroll
+        for (int j = 1; j < 4; ++j)
+            if (j < d) r += code(i, j) * stride[j];
+        atomicOr(&P[r], 1u << code(i, 0));
+    }
+    __syncthreads();
+    for (uint32_t w = threadIdx.x; w < rows; w += blockDim.x) {  // attribute 0, in-word
+        uint32_t x = P[w];
+        x |= x << 1;
+        x |= x << 2;
+        x |= x << 4;
+        x |= x << 8;
+        x |= x << 16;
+        P[w] = x;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 1; j < 4; ++j) {  // attributes 1 .. d-1: one thread per line
+        if (j < d) {
+            const uint32_t sj = stride[j], lines = rows / e;
+            for (uint32_t l = threadIdx.x; l < lines; l += blockDim.x) {
+                uint32_t at = (l / sj) * sj * e + l % sj;
+                uint32_t acc = P[at];
+                for (uint32_t k = 1; k < e; ++k) {
+                    at += sj;
+                    acc |= P[at];
+                    P[at] = acc;
+                }
+            }
+        }
+        __syncthreads();
+    }
+    const uint32_t q0 = blockIdx.x * per_block;
+    const uint32_t q1 = min(na, q0 + per_block);
+    for (uint32_t q = q0 + threadIdx.x; q < q1; q += blockDim.x) {
+        const uint32_t t = act[q];
+        uint32_t c[4] = {0, 0, 0, 0}, r = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (j < d) c[j] = code(t, j);
+#pragma unroll
+        for (int j = 1; j < 4; ++j) r += c[j] * stride[j];
+        // dominated iff some occupied cell <= c, != c: OR_j P[c - e_j]
+        bool dom = c[0] >= 1 && ((P[r] >> (c[0] - 1)) & 1u);
+#pragma unroll
+        for (int j = 1; j < 4; ++j)
+            if (j < d && c[j] >= 1) dom |= (P[r - stride[j]] >> c[0]) & 1u;
+        if (dom) atomicMax(&den[t], g);
+    }
+}
+
+}  // namespace
+
+// All steps in one launch with the grids in shared memory; false (nothing
+// done) unless d <= 4 and every step's grid fits (kSmemGridMax).
+bool gres_cells_smem_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_max,
+                            double maxv, const uint32_t* act, uint64_t na, int32_t* d_den) {
+    if (g_max < 2 || S == 0 || na == 0 || d < 1 || d > 4 || !(maxv >= 0.0)) return false;
+    const char* off = getenv("SKYGPU_CELLS_SMEM");  // "0": the per-step HBM variant (tests)
+    if (off && off[0] == '0') return false;
+    const double emax = std::floor(maxv * (double)g_max) + 1.0;
+    if (emax > 32.0) return false;
+    const uint64_t e = (uint64_t)emax;
+    uint64_t rows = 1;
+    for (int j = 1; j < d; ++j) rows *= e;
+    const size_t smem = rows * sizeof(uint32_t);
+    if (smem > kSmemGridMax) return false;
+    static bool attr_set = false;
+    if (!attr_set) {
+        SKY_CUDA(cudaFuncSetAttribute(k_cells_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)kSmemGridMax));
+        attr_set = true;
+    }
+    const uint32_t G = (uint32_t)(g_max - 1);
+    // ~2 blocks per SM over all steps, at least 64 candidates per block
+    uint64_t per_step = ((uint64_t)c.num_sms * 2 + G - 1) / G;
+    per_step = std::max<uint64_t>(1, std::min<uint64_t>(per_step, (na + 63) / 64));
+    const uint32_t per_block = (uint32_t)((na + per_step - 1) / per_step);
+    k_cells_smem<<<dim3((unsigned)per_step, G), kSmemBlock, smem, c.stream>>>(
+        d_skyv, (uint32_t)S, d, g_max, maxv, act, (uint32_t)na, per_block, d_den);
+    SKY_LAUNCH_CHECK();
+    note_launch(c);
+    return true;
+}
+
 // Cell engine over S skyline tuples (SoA d_skyv), candidates act[0..na),
 // denominators into d_den (pre-zeroed); returns false (nothing done) when the
 // engine does not apply.  Runs steps g_max .. 2, stopping once every

@@ -26,7 +26,10 @@
 //    codes of a comparator range staged once in shared memory, S <= 2^21) or
 //    the tiled one; one test = SWAR subtract + mask + compare; a candidate
 //    leaves at its first (largest) dominating step.
-//  - cell engine (cells.cu), same codes, O(cells + S) per step: huge S.
+//  - cell engine (cells.cu), same codes, O(cells + S) per step: huge S;
+//    its small-grid variant (d <= 4, code extent <= 32) runs every step in
+//    ONE launch with each step's grid in shared memory and is preferred
+//    whenever it applies (C1, C2).
 //  - f64 path (anything else): one launch per step on the reference's own
 //    projections floor(v*g)/g compared as float64, with the exact (psum, id)
 //    order check when ties are possible.
@@ -643,6 +646,25 @@ GresOut gres_device(Ctx& c, const double* d_skyv, const int64_t* d_ids, uint64_t
     const bool want_cells = u8 && G >= 1 && na > 0 &&
                             (engine == SKYGPU_GRES_CELLS ||
                              (engine == SKYGPU_GRES_AUTO && S >= (1u << 18)));
+    // small grids (d <= 4): every step in one launch, grids in shared memory
+    // — the cheapest engine whenever it applies
+    if (u8 && G >= 1 && na > 0 && engine != SKYGPU_GRES_PAIRS) {
+        SKY_CUDA(cudaEventRecord(e0, c.stream));
+        if (gres_cells_smem_device(c, d_skyv, S, d, out.g_max, maxv, act, na, d_den)) {
+            SKY_CUDA(cudaEventRecord(e1, c.stream));
+            trace_mark(c, "gres: shared-memory cell kernel");
+            k_finalize_den<<<grid_for(na, kBlock), kBlock, 0, c.stream>>>(act, na, d_den);
+            SKY_LAUNCH_CHECK();
+            note_launch(c);
+            c.gres_timing_pending = true;
+            st.gres_engine = SKYGPU_GRES_CELLS;
+            st.gres_cells = 0;  // no HBM sweeps (bench.py reads 0 as this variant)
+            out.steps = G;
+            st.gres_steps = G;
+            st.gres_kernel_launches += 1;
+            return out;
+        }
+    }
     if (want_cells) {
         uint64_t swept = 0;
         int steps_run = 0;

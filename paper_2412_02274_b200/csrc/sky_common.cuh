@@ -208,12 +208,15 @@ struct SkylineOut {
 // internal sky_engine bit: give up (aborted = true) instead of switching to
 // the rank-grid engine — the streamed head only wants a small skyline
 constexpr unsigned kSkyAbortIfLarge = 0x100u;
+// internal sky_engine bit: stop after the first round and return that
+// prefix's skyline (a seed: not final, any dominating predecessor filters)
+constexpr unsigned kSkyFirstPrefix = 0x200u;
 
 // Skyline of n tuples already resident on the device (AoS vals, ids).
 // Input still arriving (host-pointer pipeline): chunk ch = positions
 // [bound[ch], bound[ch+1]) is on the device once ready[ch] has fired.
-// Chunk 0 (the head) is decided first while the rest is in flight; its
-// skyline then filters every later chunk as it lands (skyline.cu).
+// The first prefix of chunk 0 (the head) is decided while the rest is in
+// flight; its skyline then filters every chunk as it lands (skyline.cu).
 struct TailFeed {
     int nchunks = 0;
     uint64_t bound[9] = {};
@@ -258,6 +261,10 @@ void check_grid_projection(Ctx& c, const double* d_skyv, uint64_t S, int d, int 
 bool gres_cells_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_max,
                        const uint32_t* act, uint64_t na, int32_t* d_den, uint64_t* cells_swept,
                        int* steps_run);
+// cells.cu: the same engine with every step in one launch and the grids in
+// shared memory (d <= 4, small code extents); false when it does not apply
+bool gres_cells_smem_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_max,
+                            double maxv, const uint32_t* act, uint64_t na, int32_t* d_den);
 
 // accounting.cu: exact SFS DominanceCounter totals of one phase (groups =
 // partitions, gid < 0 = not in the phase, optional representatives); adds

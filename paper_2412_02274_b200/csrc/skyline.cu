@@ -1256,11 +1256,6 @@ __global__ void k_iota(uint32_t* __restrict__ a, uint64_t n) {
          i += (uint64_t)gridDim.x * blockDim.x)
         a[i] = (uint32_t)i;
 }
-__global__ void k_mark_u8(uint8_t* __restrict__ f, const uint32_t* __restrict__ at, uint64_t m) {
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
-         i += (uint64_t)gridDim.x * blockDim.x)
-        f[at[i]] = 1;
-}
 }  // namespace
 
 SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, uint64_t n, int d,
@@ -1271,7 +1266,7 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
     if (n == 0) return out;
     if (n >= 0xFFFFFFFFull) invalid("parallel_skyline: more than 2^32-1 tuples");
     const unsigned gb = grid_for(n, kBlock);
-    // ---- streamed input: decide the head while the rest is still in flight
+    // ---- streamed input: seed from the head while the rest is still in flight
     uint32_t* seed = nullptr;
     uint64_t nseed = 0;
     unsigned long long* scale_snap = nullptr;
@@ -1281,8 +1276,9 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
                               sky_engine != SKYGPU_SKY_GRID && feed->nchunks >= 2;
         if (eligible) {
             try {
-                const SkylineOut h = skyline_device(c, d_vals, d_ids, feed->bound[1], d, plan,
-                                                    nullptr, 0, kSkyAbortIfLarge, nullptr);
+                const SkylineOut h =
+                    skyline_device(c, d_vals, d_ids, feed->bound[1], d, plan, nullptr, 0,
+                                   kSkyAbortIfLarge | kSkyFirstPrefix, nullptr);
                 if (!h.aborted && h.S > 0 && h.S <= kCTACap) {
                     seed = c.buf[B_SEED].as<uint32_t>(h.S);
                     scale_snap = c.buf[B_AMAX2].as<unsigned long long>(kMaxDims);
@@ -1302,7 +1298,7 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
                 SKY_CUDA(cudaStreamWaitEvent(c.stream, feed->ready[ch], 0));
             feed = nullptr;
         }
-        trace_mark(c, "sky: streamed head decided");
+        trace_mark(c, "sky: streamed head seed");
     }
     st.tuples_in = n;
 
@@ -1699,20 +1695,19 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
         return (uint64_t)c.h_slots[S_C2];
     };
     if (feed) {
-        // every chunk scored as it lands and filtered against the head's
-        // skyline (seeded K5, precedence checked per hit); the head's own
-        // non-skyline tuples are dominated inside the head.  Survivors (the
-        // head skyline included) form the undecided list of the rounds.
+        // every chunk (the head included) scored as it lands and filtered
+        // against the seed — the skyline of the head's first prefix — by the
+        // seeded K5 (precedence checked per hit: a dominating predecessor
+        // rules a tuple out whether or not it is a skyline tuple itself).
+        // Survivors (the seed included) form the undecided list of the rounds.
         k_seed_slots<<<1, 32, 0, c.stream>>>(c.d_slots, nseed);
         SKY_LAUNCH_CHECK();
         const AScan A = prep_aprime(seed, nseed, scale_snap);
         uint8_t* flags = c.buf[B_FLAGS].as<uint8_t>(n);
         uint32_t* iota = c.buf[B_IOTA].as<uint32_t>(n);
         k_iota<<<grid_for(n, kBlock), kBlock, 0, c.stream>>>(iota, n);
-        SKY_CUDA(cudaMemsetAsync(flags, 0, feed->bound[1], c.stream));
-        k_mark_u8<<<grid_for(nseed, kBlock), kBlock, 0, c.stream>>>(flags, seed, nseed);
         SKY_LAUNCH_CHECK();
-        note_launch(c, 3);
+        note_launch(c, 1);
         for (int ch = 0; ch < feed->nchunks; ++ch) {
             const uint64_t lo = feed->bound[ch], hi = feed->bound[ch + 1];
             if (ch > 0) SKY_CUDA(cudaStreamWaitEvent(c.stream, feed->ready[ch], 0));
@@ -1726,7 +1721,7 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
                                                                            c.d_slots);
             SKY_LAUNCH_CHECK();
             note_launch(c, 2);
-            if (ch > 0) launch_k5(A, iota + lo, hi - lo, flags + lo, true, scale_snap);
+            launch_k5(A, iota + lo, hi - lo, flags + lo, true, scale_snap);
         }
         trace_mark(c, "sky: streamed chunks filtered");
         select_flags<uint32_t>(c, nullptr, n, flags, Rbuf0, c.d_slots + S_C3);
@@ -1768,6 +1763,17 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
         if (m == 0) throw Error(SKYGPU_ERUNTIME, "skyline: empty prefix (internal)");
 
         if (decide_prefix(Pfull, m, false)) break;
+        if (sky_engine & kSkyFirstPrefix) {  // the streamed head's seed
+            read_slots(c, S_C2, 1);
+            const uint64_t a = c.h_slots[S_C2];
+            if ((sky_engine & kSkyAbortIfLarge) && r >= kGridMin && a * 4 > m * 3 &&
+                sky_grid_bins(r, d)) {
+                out.aborted = true;
+                return out;
+            }
+            kc += a;
+            break;
+        }
         // large skyline ahead (most of the first prefix survived): decide
         // everything at once with the rank-grid engine instead of filtering.
         // Decided on the device (no extra host round trip): the gate makes

@@ -169,6 +169,42 @@ def test_cell_engine_shards(world):
     assert acc.tolist() == full.den.tolist()
 
 
+@pytest.mark.parametrize("gen,d", [("ant", 1), ("ant", 2), ("ant", 3), ("uni", 4),
+                                   ("lattice", 3), ("corr", 4)])
+def test_cell_engine_smem_matches_pairs(gen, d):
+    """The shared-memory cell kernel (all steps in one launch, d <= 4) and
+    the per-step HBM variant give the pair engine's map."""
+    v = sk.generate(gen, 20000, d, 50 + d)
+    full = sk.pipeline(v, cap=25, engine=sk.GRES_PAIRS)
+    auto = sk.pipeline(v, cap=25)
+    assert auto.positions.tolist() == full.positions.tolist()
+    assert auto.den.tolist() == full.den.tolist()
+    if auto.g_max >= 2:
+        assert auto.stats["gres_engine"] == sk.GRES_CELLS and auto.stats["gres_cells"] == 0
+        assert auto.stats["gres_kernel_launches"] == 1
+
+
+def test_cell_engine_hbm_variant_small_d(monkeypatch):
+    monkeypatch.setenv("SKYGPU_CELLS_SMEM", "0")
+    v = sk.generate("ant", 50000, 3, 61)
+    full = sk.pipeline(v, cap=25, engine=sk.GRES_PAIRS)
+    cells = sk.pipeline(v, cap=25, engine=sk.GRES_CELLS)
+    assert cells.stats["gres_engine"] == sk.GRES_CELLS and cells.stats["gres_cells"] > 0
+    assert cells.den.tolist() == full.den.tolist()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_cell_engine_smem_shards(world):
+    v = sk.generate("ant", 30000, 3, 43)
+    full = sk.pipeline(v, cap=25, engine=sk.GRES_PAIRS)
+    acc = np.zeros_like(full.den)
+    for r in range(world):
+        part = sk.pipeline(v, cap=25, shard_rank=r, shard_world=world)
+        assert part.stats["gres_cells"] == 0
+        acc = np.maximum(acc, part.den)
+    assert acc.tolist() == full.den.tolist()
+
+
 # ------------------------------------------------ one-pass rank-grid skyline engine
 @pytest.mark.parametrize("name", ["C1_uni_100k_d4", "C2_ant_1M_d3", "C3_corr_1M_d6",
                                   "C5_prefix_2k_d7", "C5_prefix_10k_d7",
@@ -329,6 +365,24 @@ def test_streamed_fp_tie_across_chunks():
     pos, _ = po.skyline_sfs(v, ids)
     assert res.positions.tolist() == pos.tolist()
     assert sorted(res.positions.tolist()) == [0, n - 1]
+
+
+def test_streamed_seed_dominated_by_tail():
+    """The seed (skyline of the head's first prefix) is not final: a tail
+    tuple can dominate a seed tuple, and a seed tuple still rules out the
+    head tuples it dominates."""
+    n = 2_100_000
+    rng = np.random.default_rng(11)
+    v = 0.7 + 0.3 * rng.random((n, 3))
+    v[3] = [0.5, 0.5, 0.5]                 # head seed, dominated by the tail tuple below
+    v[7] = [0.6, 0.55, 0.6]                # head, dominated by both
+    v[n - 2] = [0.4, 0.45, 0.4]            # tail
+    v[n - 1] = [0.1, 0.9, 0.65]            # tail, incomparable with the rest
+    ids = np.arange(n, dtype=np.int64)
+    res = _host_vs_device(v, ids)
+    pos, _ = po.skyline_sfs(v, ids)
+    assert res.positions.tolist() == pos.tolist()
+    assert 3 not in res.positions.tolist() and n - 2 in res.positions.tolist()
 
 
 # ------------------------------------------------ sharded calls with an installed collective
