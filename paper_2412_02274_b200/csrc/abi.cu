@@ -241,6 +241,12 @@ void end_stats(Ctx& c) {
             fprintf(stderr, "[skygpu trace] %8.1f us  (host issue %8.1f us)  %s\n", ms * 1e3,
                     c.thost[i] - c.thost[i - 1], c.tlabel[i]);
         }
+        for (int ch = 0; ch < c.trace_chunks; ++ch) {  // streamed input: chunk arrivals
+            float at = 0;
+            SKY_CUDA(cudaEventElapsedTime(&at, c.tev[0], c.xev[ch]));
+            fprintf(stderr, "[skygpu trace] chunk %d on the device at %8.1f us\n", ch, at * 1e3);
+        }
+        c.trace_chunks = 0;
         float tot = 0;
         SKY_CUDA(cudaEventElapsedTime(&tot, c.tev[0], c.tev[c.ntrace - 1]));
         fprintf(stderr, "[skygpu trace] %8.1f us  TOTAL (%llu launches)\n", tot * 1e3,
@@ -577,12 +583,15 @@ int skygpu_pipeline(const double* vals, const int64_t* ids, uint64_t n, int d,
             if (streamed) {
                 if (!c.copy) {
                     SKY_CUDA(cudaStreamCreateWithFlags(&c.copy, cudaStreamNonBlocking));
-                    for (auto& e : c.xev) SKY_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                    for (auto& e : c.xev)
+                        SKY_CUDA(cudaEventCreateWithFlags(
+                            &e, c.trace ? cudaEventDefault : cudaEventDisableTiming));
                 }
                 // the copies follow the stream's earlier work on these buffers
                 SKY_CUDA(cudaEventRecord(c.xev[9], c.stream));
                 SKY_CUDA(cudaStreamWaitEvent(c.copy, c.xev[9], 0));
                 feed.nchunks = 4;
+                c.trace_chunks = feed.nchunks;
                 for (int ch = 0; ch <= feed.nchunks; ++ch) feed.bound[ch] = n * ch / feed.nchunks;
                 for (int ch = 0; ch < feed.nchunks; ++ch) {
                     const uint64_t lo = feed.bound[ch], cnt = feed.bound[ch + 1] - lo;

@@ -119,6 +119,7 @@ struct Ctx {
     cudaEvent_t tev[96];
     const char* tlabel[96];
     double thost[96];  // host clock at each mark (us): where the GPU waits for the CPU
+    int trace_chunks = 0;  // streamed chunks whose arrival the trace reports
 };
 
 // record a labelled device timestamp when tracing is on

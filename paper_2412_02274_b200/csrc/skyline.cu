@@ -1383,7 +1383,12 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
         const long long v = e ? atoll(e) : 0;
         return v > 0 ? (uint64_t)v : (uint64_t)8000;
     }();
-    uint64_t want = kWant;
+    static const uint64_t kSeedWant = [] {  // the streamed head's seed prefix
+        const char* e = getenv("SKYGPU_SEED_PREFIX");
+        const long long v = e ? atoll(e) : 0;
+        return v > 0 ? (uint64_t)v : (uint64_t)8000;
+    }();
+    uint64_t want = (sky_engine & kSkyFirstPrefix) ? kSeedWant : kWant;
     const uint64_t kMaxPrefix = 65536, kFinal = kCTACap;
     const uint64_t kGridMin = 1u << 16;  // auto rank-grid engine from this many tuples
     int rounds = 0;
@@ -1730,6 +1735,9 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
         R = Rbuf0;
         r = c.h_slots[S_C3];
         st.tuples_into_parallel = r;
+        if (c.trace)
+            fprintf(stderr, "[skygpu trace] streamed: seed %llu, survivors %llu of %llu\n",
+                    (unsigned long long)nseed, (unsigned long long)r, (unsigned long long)n);
     }
     if (sky_engine == SKYGPU_SKY_GRID && r > 0 && sky_grid_bins(r, d)) {
         read_slots(c, S_BAD, 11);
@@ -1787,6 +1795,9 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
         }
 
         const uint64_t a = filter_against(K + kc, m, false);  // synchronises
+        if (c.trace)
+            fprintf(stderr, "[skygpu trace] round %d: prefix %llu, A' %llu, survivors %llu\n",
+                    rounds, (unsigned long long)m, (unsigned long long)a, (unsigned long long)r);
         if (gate && c.h_slots[S_GATE]) {
             if (sky_engine & kSkyAbortIfLarge) {
                 out.aborted = true;
