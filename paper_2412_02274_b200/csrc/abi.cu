@@ -96,7 +96,7 @@ __global__ void k_init_slots(unsigned long long* slots, int mode) {
         if (i == S_SMAX) slots[i] = 0;
         return;
     }
-    if (i == S_TESTS_SKY || i == S_TESTS_GRES) return;
+    if (i == S_TESTS_SKY || i == S_TESTS_GRES || i == S_SPEC) return;
     unsigned long long v = 0;
     if (i == S_BAD || i == S_PAIR || i == S_GRIDBAD || i == S_SMIN) v = ~0ULL;
     if (i == S_MINGAP) v = 0x7FF0000000000000ULL;
@@ -642,18 +642,23 @@ int skygpu_pipeline(const double* vals, const int64_t* ids, uint64_t n, int d,
         if (!(flags & SKYGPU_SKIP_GRES)) {
             Timer tg(c, 6);
             go = gres_device(c, so.d_skyv, so.d_ids, so.S, d, cap, gres_engine, shard_rank,
-                             shard_world, (flags & SKYGPU_CHECK_SKYLINE) != 0, den);
+                             shard_world, (flags & SKYGPU_CHECK_SKYLINE) != 0, den,
+                             /*allow_spec=*/true);
             if (c.shard_world > 1) shard_allreduce_max(c, den, so.S, 4);  // the full map
             tg.stop(&c.st->ms_gres);
         }
         trace_mark(c, "gres: finalize");
         Timer d2h(c, 12);
+        auto copy_den = [&] {
+            if (!(flags & SKYGPU_SKIP_GRES))
+                SKY_CUDA(cudaMemcpyAsync(out_den, den, so.S * sizeof(int32_t),
+                                         dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                                         c.stream));
+        };
         if (dev) {
             // outputs stay on the device; positions widened to u64
             if (so.S) {
-                if (!(flags & SKYGPU_SKIP_GRES))
-                    SKY_CUDA(cudaMemcpyAsync(out_den, den, so.S * sizeof(int32_t),
-                                             cudaMemcpyDeviceToDevice, c.stream));
+                copy_den();
                 widen_u32_u64(c, so.d_inpos, out_pos, so.S);
             }
         } else if (so.S) {
@@ -663,9 +668,15 @@ int skygpu_pipeline(const double* vals, const int64_t* ids, uint64_t n, int d,
             widen_u32_u64(c, so.d_inpos, wide, so.S);
             SKY_CUDA(cudaMemcpyAsync(out_pos, wide, so.S * sizeof(uint64_t),
                                      cudaMemcpyDeviceToHost, c.stream));
-            if (!(flags & SKYGPU_SKIP_GRES))
-                SKY_CUDA(cudaMemcpyAsync(out_den, den, so.S * sizeof(int32_t),
-                                         cudaMemcpyDeviceToHost, c.stream));
+            copy_den();
+        }
+        gres_spec_fetch(c);
+        SKY_CUDA(cudaStreamSynchronize(c.stream));
+        if (gres_spec_failed(c)) {  // the speculative gres launch did not apply: redo
+            trace_mark(c, "gres: speculation missed, exact path");
+            go = gres_device(c, so.d_skyv, so.d_ids, so.S, d, cap, gres_engine, shard_rank,
+                             shard_world, false, den);
+            copy_den();
             SKY_CUDA(cudaStreamSynchronize(c.stream));
         }
         d2h.stop(&c.st->ms_d2h);

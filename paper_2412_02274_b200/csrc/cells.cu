@@ -376,11 +376,26 @@ constexpr size_t kSmemGridMax = 200 * 1024;  // bytes of row words per step
 // step's prefix-OR grid from all S tuples (cheap: S shared-memory atomics),
 // then answers its slice of the candidates.  den = the largest g at which t
 // is dominated = the first ejection of the descending scan (atomicMax).
+//
+// spec != nullptr (speculative launch, gres_cells_smem_spec): g_max and the
+// value maximum come from the device (the gap witness, slots[S_FLAG] bit 0 and
+// slots[S_MAXV]); every block checks the launch applies — g_max = cap and the
+// top code extent within ealloc — or block (0,0) raises slots[S_SPEC].
 __global__ void __launch_bounds__(kSmemBlock)
     k_cells_smem(const double* __restrict__ v, uint32_t S, int d, int g_max, double maxv,
                  const uint32_t* __restrict__ act, uint32_t na, uint32_t per_block,
-                 int32_t* __restrict__ den) {
+                 int32_t* __restrict__ den, unsigned long long* __restrict__ spec,
+                 uint32_t ealloc) {
     extern __shared__ uint32_t P[];
+    if (spec) {
+        maxv = __longlong_as_double((long long)spec[S_MAXV]);
+        const bool ok = (spec[S_FLAG] & 1ULL) &&
+                        floor(__dmul_rn(maxv, (double)g_max)) + 1.0 <= (double)ealloc;
+        if (!ok) {
+            if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) spec[S_SPEC] = 1;
+            return;
+        }
+    }
     const int g = g_max - (int)blockIdx.y;
     const double gd = (double)g;
     const uint32_t e = (uint32_t)floor(__dmul_rn(maxv, gd)) + 1;  // codes 0 .. e-1
@@ -471,7 +486,35 @@ bool gres_cells_smem_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int
     per_step = std::max<uint64_t>(1, std::min<uint64_t>(per_step, (na + 63) / 64));
     const uint32_t per_block = (uint32_t)((na + per_step - 1) / per_step);
     k_cells_smem<<<dim3((unsigned)per_step, G), kSmemBlock, smem, c.stream>>>(
-        d_skyv, (uint32_t)S, d, g_max, maxv, act, (uint32_t)na, per_block, d_den);
+        d_skyv, (uint32_t)S, d, g_max, maxv, act, (uint32_t)na, per_block, d_den, nullptr, 0);
+    SKY_LAUNCH_CHECK();
+    note_launch(c);
+    return true;
+}
+
+bool gres_cells_smem_spec(Ctx& c, const double* d_skyv, uint64_t S, int d, int cap,
+                          const uint32_t* act, uint64_t na, int32_t* d_den) {
+    if (cap < 2 || cap > 31 || S < 2 || na == 0 || d < 1 || d > 4) return false;
+    const char* off = getenv("SKYGPU_CELLS_SMEM");
+    if (off && off[0] == '0') return false;
+    const uint32_t ealloc = (uint32_t)cap + 1;  // values in [0, 1]: codes 0 .. cap
+    uint64_t rows = 1;
+    for (int j = 1; j < d; ++j) rows *= ealloc;
+    const size_t smem = rows * sizeof(uint32_t);
+    if (smem > kSmemGridMax) return false;
+    static bool attr_set = false;
+    if (!attr_set) {
+        SKY_CUDA(cudaFuncSetAttribute(k_cells_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)kSmemGridMax));
+        attr_set = true;
+    }
+    const uint32_t G = (uint32_t)(cap - 1);
+    uint64_t per_step = ((uint64_t)c.num_sms * 2 + G - 1) / G;
+    per_step = std::max<uint64_t>(1, std::min<uint64_t>(per_step, (na + 63) / 64));
+    const uint32_t per_block = (uint32_t)((na + per_step - 1) / per_step);
+    k_cells_smem<<<dim3((unsigned)per_step, G), kSmemBlock, smem, c.stream>>>(
+        d_skyv, (uint32_t)S, d, cap, 0.0, act, (uint32_t)na, per_block, d_den, c.d_slots,
+        ealloc);
     SKY_LAUNCH_CHECK();
     note_launch(c);
     return true;

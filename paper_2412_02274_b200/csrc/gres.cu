@@ -164,6 +164,26 @@ __global__ void k_shard_iota(uint64_t na, int rank, int world, uint32_t* __restr
     }
 }
 
+// the speculative path's set-up in one launch: flags, the witness table,
+// den = 0 and the identity candidate list
+__global__ void k_gres_spec_init(unsigned long long* __restrict__ slots,
+                                 unsigned long long* __restrict__ table, uint64_t ntab,
+                                 int32_t* __restrict__ den, uint64_t S, uint32_t* __restrict__ act) {
+    const uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i0 == 0) {
+        slots[S_FLAG] = 0;
+        slots[S_MAXV] = 0;
+        slots[S_SPEC] = 0;
+    }
+    for (uint64_t i = i0; i < S || i < ntab; i += (uint64_t)gridDim.x * blockDim.x) {
+        if (i < ntab) table[i] = 0;
+        if (i < S) {
+            den[i] = 0;
+            act[i] = (uint32_t)i;
+        }
+    }
+}
+
 __global__ void k_fill_den(const uint32_t* __restrict__ act, uint64_t na, int value,
                            int32_t* __restrict__ den) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < na;
@@ -577,14 +597,66 @@ int g_max_device(Ctx& c, const double* d_soa, uint64_t S, int d, int cap, double
     return intervals_from_gap(gap, cap);
 }
 
+void gres_spec_fetch(Ctx& c) {
+    if (c.gres_spec)
+        SKY_CUDA(cudaMemcpyAsync(c.h_slots + S_SPEC, c.d_slots + S_SPEC, sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToHost, c.stream));
+}
+
+bool gres_spec_failed(Ctx& c) {
+    if (!c.gres_spec) return false;
+    c.gres_spec = false;
+    return c.h_slots[S_SPEC] != 0;
+}
+
 GresOut gres_device(Ctx& c, const double* d_skyv, const int64_t* d_ids, uint64_t S, int d,
                     int cap, int engine, int shard_rank, int shard_world, bool check_skyline,
-                    int32_t* d_den) {
+                    int32_t* d_den, bool allow_spec) {
     GresOut out;
     skygpu_stats& st = *c.st;
     if (S >= 0x7FFFFFFFull) invalid("grid_resistance: more than 2^31-1 skyline tuples");
     if (S == 0) return out;
     if (shard_world < 1) shard_world = 1;
+
+    // speculative capped scan without a host round trip: the gap witness,
+    // then the shared-memory cell kernel reading g_max (= cap when the
+    // witness fired) and the value maximum from the device; if either does
+    // not hold the kernel raises S_SPEC and the caller re-runs this call
+    // with allow_spec = false after its final synchronisation
+    c.gres_spec = false;
+    if (allow_spec && !check_skyline && shard_world == 1 && engine != SKYGPU_GRES_PAIRS &&
+        cap >= 2 && cap <= 31 && S >= 2 && d >= 1 && d <= 4) {
+        const uint64_t ntab = (uint64_t)d * 2 * cap;
+        unsigned long long* table = c.buf[B_CELLS].as<unsigned long long>(ntab);
+        uint32_t* act = c.buf[B_ACT0].as<uint32_t>(S);
+        trace_mark(c, "gres: start (speculative)");
+        k_gres_spec_init<<<grid_for(S > ntab ? S : ntab, kBlock), kBlock, 0, c.stream>>>(
+            c.d_slots, table, ntab, d_den, S, act);
+        k_gap_witness<<<grid_for(S * d, kBlock), kBlock, 0, c.stream>>>(d_skyv, S, d, cap, table,
+                                                                         c.d_slots);
+        SKY_LAUNCH_CHECK();
+        note_launch(c, 2);
+        cudaEvent_t e0 = c.ev[10], e1 = c.ev[11];
+        SKY_CUDA(cudaEventRecord(e0, c.stream));
+        if (gres_cells_smem_spec(c, d_skyv, S, d, cap, act, S, d_den)) {
+            SKY_CUDA(cudaEventRecord(e1, c.stream));
+            trace_mark(c, "gres: shared-memory cell kernel");
+            k_finalize_den<<<grid_for(S, kBlock), kBlock, 0, c.stream>>>(act, S, d_den);
+            SKY_LAUNCH_CHECK();
+            note_launch(c);
+            c.gres_timing_pending = true;
+            c.gres_spec = true;
+            out.g_max = cap;
+            out.steps = cap - 1;
+            st.g_max = cap;
+            st.code_bits = 8;
+            st.gres_engine = SKYGPU_GRES_CELLS;
+            st.gres_cells = 0;
+            st.gres_steps = cap - 1;
+            st.gres_kernel_launches += 1;
+            return out;
+        }
+    }
 
     if (check_skyline) {
         zero_slots(c);

@@ -91,7 +91,8 @@ enum Slot {
     S_C2 = 14,         // new skyline tuples of the round
     S_C3 = 15,         // survivors of the round
     S_GATE = 16,       // 1: the first round asks for the rank-grid engine (K5 skipped)
-    S_COUNT_ = 17
+    S_SPEC = 17,       // 1: the speculative gres launch did not apply (gres.cu), redo
+    S_COUNT_ = 18
 };
 
 struct Ctx {
@@ -120,6 +121,7 @@ struct Ctx {
     const char* tlabel[96];
     double thost[96];  // host clock at each mark (us): where the GPU waits for the CPU
     int trace_chunks = 0;  // streamed chunks whose arrival the trace reports
+    bool gres_spec = false;  // a speculative gres launch awaits its S_SPEC check
 };
 
 // record a labelled device timestamp when tracing is on
@@ -250,9 +252,15 @@ struct GresOut {
 // Grid resistance of S skyline tuples held SoA on the device (d_skyv[d][S]).
 // d_den (S entries) receives the denominators (0 for tuples outside this
 // shard).  Throws Error(EINVAL, ...) exactly where the reference throws.
+// allow_spec: the caller checks gres_spec_failed() after its final
+// synchronisation (and re-runs with allow_spec = false when it did)
 GresOut gres_device(Ctx& c, const double* d_skyv, const int64_t* d_ids, uint64_t S, int d,
                     int cap, int engine, int shard_rank, int shard_world, bool check_skyline,
-                    int32_t* d_den);
+                    int32_t* d_den, bool allow_spec = false);
+// queue the read of the speculation flag (before the caller's final sync)
+void gres_spec_fetch(Ctx& c);
+// after that sync: true when the speculative launch did not apply
+bool gres_spec_failed(Ctx& c);
 
 // Grid plan inside the scan: throw the reference's grid_cell error when a
 // projection at step g leaves [0,1]
@@ -266,6 +274,11 @@ bool gres_cells_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_ma
 // shared memory (d <= 4, small code extents); false when it does not apply
 bool gres_cells_smem_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_max,
                             double maxv, const uint32_t* act, uint64_t na, int32_t* d_den);
+// the same launch before g_max and the value range are known on the host
+// (capped scans): g_max = cap when the device gap witness fired, codes within
+// an extent of cap + 1; otherwise it sets S_SPEC and does nothing
+bool gres_cells_smem_spec(Ctx& c, const double* d_skyv, uint64_t S, int d, int cap,
+                          const uint32_t* act, uint64_t na, int32_t* d_den);
 
 // accounting.cu: exact SFS DominanceCounter totals of one phase (groups =
 // partitions, gid < 0 = not in the phase, optional representatives); adds

@@ -184,6 +184,31 @@ def test_cell_engine_smem_matches_pairs(gen, d):
         assert auto.stats["gres_kernel_launches"] == 1
 
 
+@pytest.mark.parametrize("case", ["witness_fires", "coarse_gaps", "values_above_one",
+                                  "value_exactly_one", "cap_31", "cap_2"])
+def test_speculative_gres_launch(case):
+    """The pipeline's speculative capped scan (g_max = cap from the device
+    gap witness, codes within cap + 1) and its fallback when either does not
+    hold: the map is the oracle's in every case."""
+    rng = np.random.default_rng(71)
+    cap = {"cap_31": 31, "cap_2": 2}.get(case, 25)
+    if case == "coarse_gaps":          # min positive gap 0.1 -> g_max = 10 < cap
+        v = rng.integers(0, 10, size=(3000, 3)) / 10.0
+    elif case == "values_above_one":   # codes beyond cap + 1
+        v = 3.0 * sk.generate("ant", 3000, 3, 5)
+    elif case == "value_exactly_one":
+        v = sk.generate("ant", 3000, 3, 6)
+        v[0] = [1.0, 0.0, 0.0]
+    else:
+        v = sk.generate("ant", 3000, 3, 7)
+    ids = np.arange(len(v), dtype=np.int64)
+    res = sk.pipeline(v, ids, cap=cap)
+    pos, _ = po.skyline_sfs(v, ids)
+    assert res.positions.tolist() == pos.tolist()
+    den, gm, _ = po.grid_resistance(v[pos], ids[pos], cap)
+    assert res.g_max == gm and res.den.tolist() == den.tolist()
+
+
 def test_cell_engine_hbm_variant_small_d(monkeypatch):
     monkeypatch.setenv("SKYGPU_CELLS_SMEM", "0")
     v = sk.generate("ant", 50000, 3, 61)
