@@ -102,7 +102,7 @@ struct Ctx {
     DevBuf buf[B_COUNT];
     unsigned long long* d_slots = nullptr;
     unsigned long long* h_slots = nullptr;  // pinned mirror
-    cudaEvent_t ev[16];
+    cudaEvent_t ev[18];
     skygpu_stats* st = nullptr;
     uint64_t launches = 0;
     int num_sms = 148;

@@ -209,6 +209,7 @@ __global__ void k_gather_q(const double* __restrict__ v, const uint32_t* __restr
                            const unsigned long long* __restrict__ amax, double* __restrict__ out,
                            unsigned long long* __restrict__ qout) {
     const uint64_t mm = count ? *count : cap;
+    if (mm > cap) return;  // (a speculative count above the capacity: no-op)
     double sc[D];
     load_scales<D>(amax, sc);
     for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < mm;
@@ -600,10 +601,22 @@ __device__ __forceinline__ bool precedes(unsigned long long ka, int64_t ia,
 //     bucket_start + rank.
 constexpr uint32_t kKeyBuckets = 4096;
 
+// device-sized launch (the speculative final round): the item count lives in
+// *mdev; a count above the launch's capacity m means the launch does not
+// apply and every kernel returns at once
+__device__ __forceinline__ bool dev_count(const unsigned long long* mdev, uint32_t& m) {
+    if (!mdev) return true;
+    const unsigned long long x = *mdev;
+    if (x > m) return false;
+    m = (uint32_t)x;
+    return true;
+}
+
 __global__ void __launch_bounds__(1024)
 k_bucket_order(const uint32_t* __restrict__ in, uint32_t m, const unsigned long long* __restrict__ key,
                unsigned long long kmin, int shift, uint32_t* __restrict__ out,
-               uint32_t* __restrict__ bstart) {
+               uint32_t* __restrict__ bstart, const unsigned long long* __restrict__ mdev) {
+    if (!dev_count(mdev, m)) return;
     __shared__ uint32_t cnt[kKeyBuckets];
     for (uint32_t b = threadIdx.x; b < kKeyBuckets; b += 1024) cnt[b] = 0;
     __syncthreads();
@@ -633,7 +646,9 @@ k_bucket_order(const uint32_t* __restrict__ in, uint32_t m, const unsigned long 
 __global__ void k_bucket_rank(const uint32_t* __restrict__ in, uint32_t m,
                               const unsigned long long* __restrict__ key,
                               const int64_t* __restrict__ ids, unsigned long long kmin, int shift,
-                              const uint32_t* __restrict__ bstart, uint32_t* __restrict__ out) {
+                              const uint32_t* __restrict__ bstart, uint32_t* __restrict__ out,
+                              const unsigned long long* __restrict__ mdev) {
+    if (!dev_count(mdev, m)) return;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
         const uint32_t p = in[i];
         const unsigned long long kp = key[p];
@@ -818,7 +833,9 @@ constexpr uint32_t kIntraChunk = 1024;
 template <int D>
 __global__ void __launch_bounds__(kBlock)
 k_sfs_intra_chunked(const double* __restrict__ Av, const unsigned long long* __restrict__ Aq,
-                    uint32_t m, volatile uint8_t* keep, unsigned long long* __restrict__ tests) {
+                    uint32_t m, volatile uint8_t* keep, unsigned long long* __restrict__ tests,
+                    uint32_t astride, const unsigned long long* __restrict__ mdev) {
+    if (!dev_count(mdev, m)) return;
     constexpr int W = QW<D>::W;
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -842,7 +859,7 @@ k_sfs_intra_chunked(const double* __restrict__ Av, const unsigned long long* __r
         const uint32_t j1 = min(i, (c + 1) * kIntraChunk);
         double t[D];
 #pragma unroll
-        for (int k = 0; k < D; ++k) t[k] = Av[(uint64_t)k * m + i];
+        for (int k = 0; k < D; ++k) t[k] = Av[(uint64_t)k * astride + i];
         unsigned long long tg[W];
 #pragma unroll
         for (int k = 0; k < W; ++k) tg[k] = Aq[(uint64_t)i * W + k] | kH16;
@@ -857,7 +874,7 @@ k_sfs_intra_chunked(const double* __restrict__ Av, const unsigned long long* __r
                     if (le16<D>(Aq + (uint64_t)j * W, tg)) {
                         double s[D];
 #pragma unroll
-                        for (int k = 0; k < D; ++k) s[k] = Av[(uint64_t)k * m + j];
+                        for (int k = 0; k < D; ++k) s[k] = Av[(uint64_t)k * astride + j];
                         hit |= dom_f64<D>(s, t);
                     }
                 }
@@ -1057,7 +1074,11 @@ k_sfs_filter_q(const double* __restrict__ v, const unsigned long long* __restric
 __global__ void __launch_bounds__(1024)
 k_cta_select(const uint32_t* __restrict__ in, const uint32_t* __restrict__ in_cell,
              const uint8_t* __restrict__ flags, uint32_t m, uint32_t* __restrict__ out,
-             uint32_t* __restrict__ out_cell, unsigned long long* __restrict__ count) {
+             uint32_t* __restrict__ out_cell, unsigned long long* __restrict__ count,
+             const unsigned long long* __restrict__ mdev = nullptr,
+             const unsigned long long* __restrict__ out_off = nullptr) {
+    if (!dev_count(mdev, m)) return;
+    if (out_off) out += *out_off;
     using Scan = cub::BlockScan<uint32_t, 1024>;
     __shared__ typename Scan::TempStorage tmp;
     uint32_t f[kCTAItems];
@@ -1470,7 +1491,16 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
     };
     // sort a prefix by (sum, id), decide it (K4) and append its skyline tuples
     // to K; true when the whole undecided set was this prefix
-    auto decide_prefix = [&](uint32_t* Pfull, uint64_t m, bool final_round) -> bool {
+    static const bool intra_chunked = [] {
+        const char* e = getenv("SKYGPU_INTRA");
+        return !(e && e[0] == '1');  // SKYGPU_INTRA=1: one warp per candidate
+    }();
+    // mdev (speculative final round): the prefix count lives in *mdev, m is
+    // the capacity (kCTACap); nothing is read back — the caller checks the
+    // count and the appended A' count (slot S_SEL2, appended after the
+    // round's A' at K + kc + slots[S_C2])
+    auto decide_prefix = [&](uint32_t* Pfull, uint64_t m, bool final_round,
+                             const unsigned long long* mdev = nullptr) -> bool {
             // ---- sort the prefix by (sum, id)
             uint32_t* Ps = c.buf[B_IDX1].as<uint32_t>(m);
             uint32_t* order = Ps;
@@ -1488,11 +1518,11 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
                 // (the in-bucket rank stays a many-CTA kernel: a bucket of
                 // equal sums — C3's zero tuples — would serialise one CTA)
                 k_bucket_order<<<1, 1024, 0, c.stream>>>(Pfull, (uint32_t)m, keys, gmin, shift, Pb,
-                                                         bst);
+                                                         bst, mdev);
                 SKY_LAUNCH_CHECK();
                 k_bucket_rank<<<grid_for(m, kBlock), kBlock, 0, c.stream>>>(Pb, (uint32_t)m, keys,
                                                                              d_ids, gmin, shift, bst,
-                                                                             Ps);
+                                                                             Ps, mdev);
                 SKY_LAUNCH_CHECK();
                 note_launch(c, 2);
             } else {
@@ -1504,7 +1534,7 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
                 constexpr int D = decltype(DC)::value;
                 if constexpr (D > 0)
                     k_gather_q<D><<<grid_for(m, kBlock), kBlock, 0, c.stream>>>(
-                        d_vals, order, m, nullptr, amax, Av, Aq);
+                        d_vals, order, m, mdev, amax, Av, Aq);
                 else
                     k_gather_aos<<<grid_for(m * d, kBlock), kBlock, 0, c.stream>>>(
                         d_vals, d, order, m, nullptr, Av);
@@ -1516,20 +1546,17 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
             // ---- K4: SFS inside the prefix, predecessors in sum order
             uint8_t* keep = c.buf[B_FLAGS].as<uint8_t>(m);
             const uint64_t wi = std::min<uint64_t>(m, (uint64_t)c.num_sms * 64);
-            static const bool intra_chunked = [] {
-                const char* e = getenv("SKYGPU_INTRA");
-                return !(e && e[0] == '1');  // SKYGPU_INTRA=1: one warp per candidate
-            }();
             if (qpre && intra_chunked)
                 SKY_CUDA(cudaMemsetAsync(keep, 1, m, c.stream));
-            SKY_CUDA(cudaEventRecord(e0, c.stream));
+            cudaEvent_t k0 = mdev ? c.ev[16] : e0, k1 = mdev ? c.ev[17] : e1;
+            SKY_CUDA(cudaEventRecord(k0, c.stream));
             dispatch_d(d, [&](auto DC) {
                 constexpr int D = decltype(DC)::value;
                 const unsigned grid = (unsigned)((wi * 32 + kBlock - 1) / kBlock);
                 if constexpr (D > 0) {
                     if (intra_chunked)
                         k_sfs_intra_chunked<D><<<c.num_sms * 8, kBlock, 0, c.stream>>>(
-                            Av, Aq, (uint32_t)m, keep, c.d_slots + S_TESTS_SKY);
+                            Av, Aq, (uint32_t)m, keep, c.d_slots + S_TESTS_SKY, (uint32_t)m, mdev);
                     else
                         k_sfs_intra_q<D><<<grid, kBlock, 0, c.stream>>>(Av, Aq, (uint32_t)m, keep,
                                                                         c.d_slots + S_TESTS_SKY);
@@ -1537,11 +1564,19 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
                     k_sfs_intra_sorted<D><<<grid, kBlock, 0, c.stream>>>(
                         Av, (uint32_t)m, d, keep, c.d_slots + S_TESTS_SKY);
             });
-            SKY_CUDA(cudaEventRecord(e1, c.stream));
+            SKY_CUDA(cudaEventRecord(k1, c.stream));
             SKY_LAUNCH_CHECK();
             note_launch(c);
             trace_mark(c, "sky: K4 intra kernel");
             // A' in (sum, id) order appended to K; its count lands in S_C2
+            if (mdev) {
+                k_cta_select<<<1, 1024, 0, c.stream>>>(order, nullptr, keep, (uint32_t)m, K + kc,
+                                                       nullptr, c.d_slots + S_SEL2, mdev,
+                                                       c.d_slots + S_C2);
+                SKY_LAUNCH_CHECK();
+                note_launch(c);
+                return false;
+            }
             if (m <= kCTACap) {
                 k_cta_select<<<1, 1024, 0, c.stream>>>(order, nullptr, keep, (uint32_t)m, K + kc,
                                                        nullptr, c.d_slots + S_C2);
@@ -1679,7 +1714,12 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
         SKY_LAUNCH_CHECK();
         note_launch(c);
     };
-    auto filter_against = [&](const uint32_t* alist, uint64_t m, bool seeded) -> uint64_t {
+    // spec_final: the final round over the survivors is queued at once,
+    // sized on the device (decide_prefix with mdev = slots[S_C3]); *spec_done
+    // tells whether it applied (survivors <= kCTACap) — one host round trip
+    // for the round and the final round instead of two
+    auto filter_against = [&](const uint32_t* alist, uint64_t m, bool seeded,
+                              bool spec_final = false, bool* spec_done = nullptr) -> uint64_t {
         const AScan A = prep_aprime(alist, m, amax);
         uint8_t* fkeep = c.buf[B_SV].as<uint8_t>(r);
         trace_mark(c, "sky: select A' + segments + gather Pv");
@@ -1690,7 +1730,16 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
         select_flags<uint32_t>(c, R, r, fkeep, Rnext, c.d_slots + S_C3);
         trace_mark(c, "sky: select survivors");
         kernel_launches += 1;
-        read_slots(c, S_C2, 3);  // S_C2 (A'), S_C3 (survivors), S_GATE
+        if (spec_final) {
+            c.h_slots[S_THR] = ~0ULL;  // the final round: no threshold
+            decide_prefix(Rnext, kCTACap, true, c.d_slots + S_C3);
+            trace_mark(c, "sky: speculative final round queued");
+            read_slots(c, S_SEL2, 9);  // S_SEL2 .. S_GATE
+            const uint64_t sv = c.h_slots[S_C3];
+            *spec_done = sv > 0 && sv <= kCTACap && !c.h_slots[S_GATE];
+        } else {
+            read_slots(c, S_C2, 3);  // S_C2 (A'), S_C3 (survivors), S_GATE
+        }
         float ms = 0;
         SKY_CUDA(cudaEventElapsedTime(&ms, e2, e3));
         kernel_ms += ms;
@@ -1794,7 +1843,11 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
             note_launch(c);
         }
 
-        const uint64_t a = filter_against(K + kc, m, false);  // synchronises
+        // the final round rides along when the survivors fit one CTA
+        // (checked on the device; the host only sees the outcome)
+        const bool spec_ok = qpre && intra_chunked && !getenv("SKYGPU_NO_SPEC_FINAL");
+        bool spec_done = false;
+        const uint64_t a = filter_against(K + kc, m, false, spec_ok, &spec_done);  // synchronises
         if (c.trace)
             fprintf(stderr, "[skygpu trace] round %d: prefix %llu, A' %llu, survivors %llu\n",
                     rounds, (unsigned long long)m, (unsigned long long)a, (unsigned long long)r);
@@ -1810,6 +1863,14 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
         SKY_CUDA(cudaEventElapsedTime(&ms4, e0, e1));
         kernel_ms += ms4;
         kc += a;
+        if (spec_done) {  // the survivors' final round already ran
+            SKY_CUDA(cudaEventElapsedTime(&ms4, c.ev[16], c.ev[17]));
+            kernel_ms += ms4;
+            kc += c.h_slots[S_SEL2];
+            ++rounds;
+            kernel_launches += 1;
+            break;
+        }
         if (a * 2 > m) want = std::min(want * 4, kMaxPrefix);
     }
     st.sfs_rounds = rounds;
