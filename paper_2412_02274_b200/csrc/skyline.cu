@@ -890,6 +890,61 @@ k_sfs_intra_chunked(const double* __restrict__ Av, const unsigned long long* __r
     add_count(tests, cnt);
 }
 
+// K4 with the prefix's codes resident in shared memory (D <= 4: one u64
+// code word per tuple, m <= 16384 -> <= 128 KB): one CTA per SM loads the
+// codes once, then each warp takes a candidate (longest first: candidate i
+// has i predecessors) and scans its predecessors in sum order, 64 per vote
+// (two per lane), shared-memory latency instead of L2 latency per step; the
+// exact float64 test runs only on a code pass.  keep[i] is written for
+// every i < m.
+constexpr uint32_t kIntraSmemMax = 16384;
+
+template <int D>
+__global__ void __launch_bounds__(1024, 1)
+k_sfs_intra_smem(const double* __restrict__ Av, const unsigned long long* __restrict__ Aq,
+                 uint32_t m, uint8_t* __restrict__ keep, unsigned long long* __restrict__ tests,
+                 uint32_t astride, const unsigned long long* __restrict__ mdev) {
+    static_assert(QW<D>::W == 1, "one code word per tuple");
+    if (!dev_count(mdev, m)) return;
+    extern __shared__ unsigned long long sq[];
+    for (uint32_t j = threadIdx.x; j < m; j += blockDim.x) sq[j] = Aq[j];
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    unsigned long long cnt = 0;
+    for (uint32_t k = warp; k < m; k += nwarps) {
+        const uint32_t i = m - 1 - k;
+        const unsigned long long tg = sq[i] | kH16;
+        double t[D];
+#pragma unroll
+        for (int a = 0; a < D; ++a) t[a] = Av[(uint64_t)a * astride + i];
+        bool dominated = false;
+        for (uint32_t j0 = 0; j0 < i; j0 += 64) {
+            bool hit = false;
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const uint32_t j = j0 + u * 32 + lane;
+                if (j < i) {
+                    ++cnt;
+                    if (((tg - sq[j]) & kH16) == kH16) {
+                        double sv[D];
+#pragma unroll
+                        for (int a = 0; a < D; ++a) sv[a] = Av[(uint64_t)a * astride + j];
+                        hit |= dom_f64<D>(sv, t);
+                    }
+                }
+            }
+            if (__any_sync(0xffffffffu, hit)) {
+                dominated = true;
+                break;
+            }
+        }
+        if (lane == 0) keep[i] = dominated ? 0 : 1;
+    }
+    add_count(tests, cnt);
+}
+
 // K5 with the quantised prefilter (D in 1..8).  Two scan modes:
 //  qk > 0  quantile grid (the default): the new skyline tuples A' are grouped
 //          by a k^d grid whose bin bounds are quantiles of A' itself; a
@@ -1495,6 +1550,10 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
         const char* e = getenv("SKYGPU_INTRA");
         return !(e && e[0] == '1');  // SKYGPU_INTRA=1: one warp per candidate
     }();
+    static const bool intra_smem = [] {  // SKYGPU_INTRA=2: chunked K4 even for d <= 4
+        const char* e = getenv("SKYGPU_INTRA");
+        return !(e && e[0] == '2');
+    }();
     // mdev (speculative final round): the prefix count lives in *mdev, m is
     // the capacity (kCTACap); nothing is read back — the caller checks the
     // count and the appended A' count (slot S_SEL2, appended after the
@@ -1553,6 +1612,22 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
             dispatch_d(d, [&](auto DC) {
                 constexpr int D = decltype(DC)::value;
                 const unsigned grid = (unsigned)((wi * 32 + kBlock - 1) / kBlock);
+                if constexpr (D > 0 && D <= 4) {
+                    if (intra_chunked && intra_smem && m <= kIntraSmemMax) {
+                        static bool attr = false;
+                        if (!attr) {
+                            SKY_CUDA(cudaFuncSetAttribute(
+                                k_sfs_intra_smem<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(kIntraSmemMax * sizeof(unsigned long long))));
+                            attr = true;
+                        }
+                        k_sfs_intra_smem<D><<<c.num_sms, 1024, m * sizeof(unsigned long long),
+                                              c.stream>>>(Av, Aq, (uint32_t)m, keep,
+                                                          c.d_slots + S_TESTS_SKY, (uint32_t)m,
+                                                          mdev);
+                        return;
+                    }
+                }
                 if constexpr (D > 0) {
                     if (intra_chunked)
                         k_sfs_intra_chunked<D><<<c.num_sms * 8, kBlock, 0, c.stream>>>(
