@@ -910,7 +910,8 @@ k_sfs_intra_smem(const double* __restrict__ Av, const unsigned long long* __rest
     for (uint32_t j = threadIdx.x; j < m; j += blockDim.x) sq[j] = Aq[j];
     __syncthreads();
     const uint32_t lane = threadIdx.x & 31;
-    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    // consecutive candidates (similar cost) on different SMs
+    const uint32_t warp = (threadIdx.x >> 5) * gridDim.x + blockIdx.x;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
     unsigned long long cnt = 0;
     for (uint32_t k = warp; k < m; k += nwarps) {
@@ -920,24 +921,34 @@ k_sfs_intra_smem(const double* __restrict__ Av, const unsigned long long* __rest
 #pragma unroll
         for (int a = 0; a < D; ++a) t[a] = Av[(uint64_t)a * astride + i];
         bool dominated = false;
-        for (uint32_t j0 = 0; j0 < i; j0 += 64) {
-            bool hit = false;
+        // 128 comparators per step, the code tests branch-free; only a step
+        // with a code pass somewhere in the warp takes the exact tests
+        for (uint32_t j0 = 0; j0 < i; j0 += 128) {
+            unsigned pm = 0;
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
+            for (int u = 0; u < 4; ++u) {
                 const uint32_t j = j0 + u * 32 + lane;
-                if (j < i) {
-                    ++cnt;
-                    if (((tg - sq[j]) & kH16) == kH16) {
+                const bool in = j < i;
+                cnt += in;
+                const unsigned long long cq = in ? sq[j] : 0ULL;
+                pm |= (unsigned)(in && ((tg - cq) & kH16) == kH16) << u;
+            }
+            if (__any_sync(0xffffffffu, pm != 0)) {
+                bool hit = false;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    if ((pm >> u) & 1u) {
+                        const uint32_t j = j0 + u * 32 + lane;
                         double sv[D];
 #pragma unroll
                         for (int a = 0; a < D; ++a) sv[a] = Av[(uint64_t)a * astride + j];
                         hit |= dom_f64<D>(sv, t);
                     }
                 }
-            }
-            if (__any_sync(0xffffffffu, hit)) {
-                dominated = true;
-                break;
+                if (__any_sync(0xffffffffu, hit)) {
+                    dominated = true;
+                    break;
+                }
             }
         }
         if (lane == 0) keep[i] = dominated ? 0 : 1;
