@@ -343,11 +343,11 @@ __device__ __forceinline__ uint32_t direction_cell(const double* t, int dd, int 
     for (int k = 0; k < DM; ++k)
         if (k < dd) s += t[k];
     if (!(s > 0.0)) return 0;
-    const double inv = (double)m / s;
+    const float inv = (float)m / (float)s;  // (scan order only: float32 suffices)
     uint32_t cell = 0;
     for (int k = DM - 2; k >= 0; --k) {
         if (k >= dd - 1) continue;
-        int b = (int)(t[k] * inv);
+        int b = (int)((float)t[k] * inv);
         b = b < 0 ? 0 : (b >= m ? m - 1 : b);
         cell = cell * (uint32_t)m + (uint32_t)b;
     }
@@ -371,19 +371,25 @@ __device__ __forceinline__ uint32_t grid_cell_id(const double* t, int dd, int m)
 // angular partition id, partition.cpp:139-174 (all-zero tuple -> 0)
 template <int DM>
 __device__ __forceinline__ uint32_t angular_cell_id(const double* t, int dd, int m) {
+    // (K5 scan order only — never a partition id the results depend on — so
+    // float32 and the SFU: atan2/sqrt in float64 cost ~100 instructions per
+    // candidate)
     bool zero = true;
     for (int k = 0; k < DM; ++k)
         if (k < dd) zero &= (t[k] == 0.0);
     if (zero || dd < 2) return 0;
-    double tail[DM + 1];
-    tail[dd] = 0.0;
+    float tail[DM + 1];
+    tail[dd] = 0.0f;
     for (int k = DM - 1; k >= 0; --k)
-        if (k < dd) tail[k] = tail[k + 1] + t[k] * t[k];
+        if (k < dd) {
+            const float x = (float)t[k];
+            tail[k] = tail[k + 1] + x * x;
+        }
     uint32_t id = 0, w = 1;
     for (int k = 0; k < DM - 1; ++k) {
         if (k >= dd - 1) break;
-        const double angle = atan2(sqrt(tail[k + 1]), t[k]);
-        int b = (int)((2.0 * angle / 3.14159265358979323846) * m);
+        const float angle = atan2f(sqrtf(tail[k + 1]), (float)t[k]);
+        int b = (int)(angle * (0.63661977236758134f * (float)m));
         b = b < 0 ? 0 : (b >= m ? m - 1 : b);
         id += (uint32_t)b * w;
         w *= (uint32_t)m;
