@@ -96,7 +96,7 @@ __global__ void k_init_slots(unsigned long long* slots, int mode) {
         if (i == S_SMAX) slots[i] = 0;
         return;
     }
-    if (i == S_TESTS_SKY || i == S_TESTS_GRES || i == S_SPEC) return;
+    if (i == S_TESTS_SKY || i == S_TESTS_GRES || i == S_SPEC || i == S_IDSBAD) return;
     unsigned long long v = 0;
     if (i == S_BAD || i == S_PAIR || i == S_GRIDBAD || i == S_SMIN) v = ~0ULL;
     if (i == S_MINGAP) v = 0x7FF0000000000000ULL;
@@ -275,6 +275,8 @@ int closest_slices(long long target, int e) {
 }  // namespace
 
 namespace {
+__global__ void k_clear_slot(unsigned long long* slots, int i) { slots[i] = 0; }
+
 __global__ void k_widen(const uint32_t* __restrict__ a, uint64_t* __restrict__ b, uint64_t n) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x)
@@ -576,6 +578,19 @@ int skygpu_pipeline(const double* vals, const int64_t* ids, uint64_t n, int d,
         const bool streamed = !dev_in && overlap_env && !(flags & SKYGPU_NORMALIZE) &&
                               n * (uint64_t)(d + 1) * 8 >= stream_min &&
                               d <= 8 && pl.strategy != SKYGPU_GRID && !(flags & SKYGPU_SKY_GRID);
+        // host ids travel behind the values and are only waited for at the
+        // end of the skyline (speculating they are strictly increasing, the
+        // usual row-order ids; otherwise the call re-runs once they are in)
+        static const bool ids_late_env = [] {
+            const char* e = getenv("SKYGPU_IDS_LATE");
+            return !(e && e[0] == '0');
+        }();
+        const bool ids_late = !dev_in && !streamed && ids_late_env && n >= (1u << 16) &&
+                              !(flags & SKYGPU_NORMALIZE);
+        struct IdsScope {  // the ids event never outlives the call
+            Ctx& c;
+            ~IdsScope() { c.ids_ready = nullptr; }
+        } ids_scope{c};
         if (!dev_in) {
             Timer h2d(c, 2);
             double* bv = c.buf[B_IN_VALS].as<double>(n * d);
@@ -602,6 +617,25 @@ int skygpu_pipeline(const double* vals, const int64_t* ids, uint64_t n, int d,
                     SKY_CUDA(cudaEventRecord(c.xev[ch], c.copy));
                     feed.ready[ch] = c.xev[ch];
                 }
+            } else if (ids_late) {
+                // values first (the skyline starts as soon as they land), the
+                // ids behind them on the copy stream, overlapping the skyline
+                if (!c.copy) {
+                    SKY_CUDA(cudaStreamCreateWithFlags(&c.copy, cudaStreamNonBlocking));
+                    for (auto& e : c.xev)
+                        SKY_CUDA(cudaEventCreateWithFlags(
+                            &e, c.trace ? cudaEventDefault : cudaEventDisableTiming));
+                }
+                k_clear_slot<<<1, 1, 0, c.stream>>>(c.d_slots, S_IDSBAD);
+                SKY_LAUNCH_CHECK();
+                SKY_CUDA(cudaMemcpyAsync(bv, vals, n * d * sizeof(double), cudaMemcpyHostToDevice,
+                                         c.stream));
+                SKY_CUDA(cudaEventRecord(c.xev[5], c.stream));
+                SKY_CUDA(cudaStreamWaitEvent(c.copy, c.xev[5], 0));
+                SKY_CUDA(cudaMemcpyAsync(bi, ids, n * sizeof(int64_t), cudaMemcpyHostToDevice,
+                                         c.copy));
+                SKY_CUDA(cudaEventRecord(c.xev[6], c.copy));
+                c.ids_ready = c.xev[6];
             } else {
                 SKY_CUDA(cudaMemcpyAsync(bv, vals, n * d * sizeof(double), cudaMemcpyHostToDevice,
                                          c.stream));
@@ -671,7 +705,33 @@ int skygpu_pipeline(const double* vals, const int64_t* ids, uint64_t n, int d,
             copy_den();
         }
         gres_spec_fetch(c);
+        if (ids_late)
+            SKY_CUDA(cudaMemcpyAsync(c.h_slots + S_IDSBAD, c.d_slots + S_IDSBAD,
+                                     sizeof(unsigned long long), cudaMemcpyDeviceToHost, c.stream));
         SKY_CUDA(cudaStreamSynchronize(c.stream));
+        if (ids_late && c.h_slots[S_IDSBAD]) {
+            // the ids are not strictly increasing: (sum, id) ties may order
+            // differently from positions — the whole call again, ids resident
+            trace_mark(c, "ids not in position order: re-run");
+            c.ids_ready = nullptr;
+            c.gres_spec = false;
+            so = skyline_device(c, dv, di, n, d, pl, nullptr, 0,
+                                flags & (SKYGPU_SKY_ROUNDS | SKYGPU_SKY_GRID), nullptr);
+            den = c.buf[B_DEN].as<int32_t>(so.S ? so.S : 1);
+            if (!(flags & SKYGPU_SKIP_GRES)) {
+                go = gres_device(c, so.d_skyv, so.d_ids, so.S, d, cap, gres_engine, shard_rank,
+                                 shard_world, (flags & SKYGPU_CHECK_SKYLINE) != 0, den);
+                if (c.shard_world > 1) shard_allreduce_max(c, den, so.S, 4);
+            }
+            if (so.S) {
+                uint64_t* wide = c.buf[B_OUTPOS].as<uint64_t>(so.S);
+                widen_u32_u64(c, so.d_inpos, wide, so.S);
+                SKY_CUDA(cudaMemcpyAsync(out_pos, wide, so.S * sizeof(uint64_t),
+                                         cudaMemcpyDeviceToHost, c.stream));
+                copy_den();
+            }
+            SKY_CUDA(cudaStreamSynchronize(c.stream));
+        }
         if (gres_spec_failed(c)) {  // the speculative gres launch did not apply: redo
             trace_mark(c, "gres: speculation missed, exact path");
             go = gres_device(c, so.d_skyv, so.d_ids, so.S, d, cap, gres_engine, shard_rank,

@@ -92,7 +92,8 @@ enum Slot {
     S_C3 = 15,         // survivors of the round
     S_GATE = 16,       // 1: the first round asks for the rank-grid engine (K5 skipped)
     S_SPEC = 17,       // 1: the speculative gres launch did not apply (gres.cu), redo
-    S_COUNT_ = 18
+    S_IDSBAD = 18,     // 1: ids that arrived late were not strictly increasing, redo
+    S_COUNT_ = 19
 };
 
 struct Ctx {
@@ -122,6 +123,10 @@ struct Ctx {
     double thost[96];  // host clock at each mark (us): where the GPU waits for the CPU
     int trace_chunks = 0;  // streamed chunks whose arrival the trace reports
     bool gres_spec = false;  // a speculative gres launch awaits its S_SPEC check
+    // host-pointer pipeline: the ids are still in flight (copy stream) until
+    // this event; the skyline runs on the speculation that they are strictly
+    // increasing (ties by position) and checks them at the end (S_IDSBAD)
+    cudaEvent_t ids_ready = nullptr;
 };
 
 // record a labelled device timestamp when tracing is on

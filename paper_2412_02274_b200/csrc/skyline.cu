@@ -229,10 +229,10 @@ __global__ void k_gather_q(const double* __restrict__ v, const uint32_t* __restr
 }
 
 __global__ void k_ids_check(const int64_t* __restrict__ ids, uint64_t n,
-                            unsigned long long* __restrict__ slots) {
+                            unsigned long long* __restrict__ slots, int slot = S_FLAG) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i + 1 < n;
          i += (uint64_t)gridDim.x * blockDim.x)
-        if (ids[i] >= ids[i + 1]) atomicOr(&slots[S_FLAG], 1ULL);
+        if (ids[i] >= ids[i + 1]) atomicOr(&slots[slot], 1ULL);
 }
 
 // Grid strategy contract (partition.cpp:88-95): values must lie in [0,1];
@@ -658,7 +658,7 @@ __global__ void k_bucket_rank(const uint32_t* __restrict__ in, uint32_t m,
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
         const uint32_t p = in[i];
         const unsigned long long kp = key[p];
-        const long long ip = ids[p];
+        const long long ip = ids ? ids[p] : (long long)p;  // (no ids: position order)
         const unsigned long long x = (kp - kmin) >> shift;
         const uint32_t b = x < kKeyBuckets ? (uint32_t)x : kKeyBuckets - 1;
         const uint32_t s0 = bstart[b], s1 = bstart[b + 1];
@@ -666,7 +666,7 @@ __global__ void k_bucket_rank(const uint32_t* __restrict__ in, uint32_t m,
         for (uint32_t j = s0; j < s1; ++j) {
             const uint32_t q = in[j];
             const unsigned long long kq = key[q];
-            const long long iq = ids[q];
+            const long long iq = ids ? ids[q] : (long long)q;
             rank += (kq < kp) | ((kq == kp) & ((iq < ip) | ((iq == ip) & (q < p))));
         }
         out[s0 + rank] = p;
@@ -1394,6 +1394,19 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
         trace_mark(c, "sky: streamed head seed");
     }
     st.tuples_in = n;
+    // ids still in flight (host-pointer pipeline): ties by position until the
+    // ids are needed (rank grid, output); their strict order is checked then
+    const bool ids_late = c.ids_ready != nullptr && !feed;
+    const int64_t* tie_ids = ids_late ? nullptr : d_ids;
+    bool ids_waited = false;
+    auto ensure_ids = [&]() {
+        if (!ids_late || ids_waited) return;
+        ids_waited = true;
+        SKY_CUDA(cudaStreamWaitEvent(c.stream, c.ids_ready, 0));
+        k_ids_check<<<grid_for(n, kBlock), kBlock, 0, c.stream>>>(d_ids, n, c.d_slots, S_IDSBAD);
+        SKY_LAUNCH_CHECK();
+        note_launch(c);
+    };
 
     zero_slots(c);
     auto* keys = c.buf[B_KEY0].as<unsigned long long>(n);
@@ -1406,7 +1419,7 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
         dispatch_d(d, [&](auto DC) {
             constexpr int D = decltype(DC)::value;
             k_score<D><<<grid_for(n, kBlock, c.num_sms * 8), kBlock, 0, c.stream>>>(
-                d_vals, n, d, keys, c.d_slots, amax, 0, d_ids);  // + ids sortedness
+                d_vals, n, d, keys, c.d_slots, amax, 0, tie_ids);  // + ids sortedness
         });
         SKY_LAUNCH_CHECK();
         note_launch(c, 1);
@@ -1540,6 +1553,7 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
     // the one-pass rank-grid engine over the whole undecided set (R, r)
     bool grid_used = false;
     auto run_grid = [&]() {
+        ensure_ids();
         uint8_t* gkeep = c.buf[B_SV].as<uint8_t>(r);
         double kms = 0;
         sky_grid_decide(c, d_vals, d, keys, d_ids, R, r, gkeep, &kms, c.shard_rank,
@@ -1597,7 +1611,7 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
                                                          bst, mdev);
                 SKY_LAUNCH_CHECK();
                 k_bucket_rank<<<grid_for(m, kBlock), kBlock, 0, c.stream>>>(Pb, (uint32_t)m, keys,
-                                                                             d_ids, gmin, shift, bst,
+                                                                             tie_ids, gmin, shift, bst,
                                                                              Ps, mdev);
                 SKY_LAUNCH_CHECK();
                 note_launch(c, 2);
@@ -1977,6 +1991,7 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
     out.d_inpos = K;
     out.d_ids = c.buf[B_SKYID].as<int64_t>(kc);
     out.d_skyv = c.buf[B_SKYV].as<double>(kc * d);
+    ensure_ids();
     if (kc) {
         trace_mark(c, "sky: rounds done (sync)");
         k_emit_skyline<<<grid_for(kc, kBlock), kBlock, 0, c.stream>>>(K, kc, d_vals, d, d_ids,

@@ -410,6 +410,35 @@ def test_streamed_seed_dominated_by_tail():
     assert 3 not in res.positions.tolist() and n - 2 in res.positions.tolist()
 
 
+@pytest.mark.parametrize("gen,ids_kind", [("ant", "permuted"), ("lattice", "permuted"),
+                                           ("lattice", "strided"), ("lattice", "one_swap"),
+                                           ("uni", "duplicate")])
+def test_late_ids_speculation(gen, ids_kind):
+    """Host inputs below the streaming size: the ids travel behind the values
+    and the skyline runs on the speculation that they are strictly increasing
+    (ties by position); any other ids re-run the call once they are in.  The
+    lattice generator makes (sum, id) ties plentiful, so a wrong tie order
+    would show."""
+    n = 200_000
+    v = sk.generate(gen, n, 3, 17)
+    rng = np.random.default_rng(17)
+    if ids_kind == "permuted":
+        ids = rng.permutation(n).astype(np.int64)
+    elif ids_kind == "strided":
+        ids = 5 + 3 * np.arange(n, dtype=np.int64)
+    elif ids_kind == "one_swap":
+        ids = np.arange(n, dtype=np.int64)
+        ids[n - 2], ids[n - 1] = ids[n - 1], ids[n - 2]
+    else:  # a repeated id: not strictly increasing
+        ids = np.arange(n, dtype=np.int64)
+        ids[n // 2] = ids[n // 2 - 1]
+    res = sk.pipeline(v, ids, cap=25)
+    pos, _ = po.skyline_sfs(v, ids)
+    assert res.positions.tolist() == pos.tolist()
+    den, gm, _ = po.grid_resistance(v[pos], ids[pos], 25)
+    assert res.g_max == gm and res.den.tolist() == den.tolist()
+
+
 # ------------------------------------------------ sharded calls with an installed collective
 def _emulated_two_ranks(run):
     """Emulate a 2-rank group on one GPU: rank 1 runs first and its MAX
