@@ -585,7 +585,7 @@ int skygpu_pipeline(const double* vals, const int64_t* ids, uint64_t n, int d,
             const char* e = getenv("SKYGPU_IDS_LATE");
             return !(e && e[0] == '0');
         }();
-        const bool ids_late = !dev_in && !streamed && ids_late_env && n >= (1u << 16) &&
+        const bool ids_late = !dev_in && ids_late_env && n >= (1u << 16) &&
                               !(flags & SKYGPU_NORMALIZE);
         struct IdsScope {  // the ids event never outlives the call
             Ctx& c;
@@ -602,20 +602,29 @@ int skygpu_pipeline(const double* vals, const int64_t* ids, uint64_t n, int d,
                         SKY_CUDA(cudaEventCreateWithFlags(
                             &e, c.trace ? cudaEventDefault : cudaEventDisableTiming));
                 }
-                // the copies follow the stream's earlier work on these buffers
-                SKY_CUDA(cudaEventRecord(c.xev[9], c.stream));
-                SKY_CUDA(cudaStreamWaitEvent(c.copy, c.xev[9], 0));
                 feed.nchunks = 4;
                 c.trace_chunks = feed.nchunks;
                 for (int ch = 0; ch <= feed.nchunks; ++ch) feed.bound[ch] = n * ch / feed.nchunks;
+                if (ids_late) k_clear_slot<<<1, 1, 0, c.stream>>>(c.d_slots, S_IDSBAD);
+                SKY_LAUNCH_CHECK();
+                // the copies follow the stream's earlier work on these buffers
+                SKY_CUDA(cudaEventRecord(c.xev[9], c.stream));
+                SKY_CUDA(cudaStreamWaitEvent(c.copy, c.xev[9], 0));
                 for (int ch = 0; ch < feed.nchunks; ++ch) {
                     const uint64_t lo = feed.bound[ch], cnt = feed.bound[ch + 1] - lo;
                     SKY_CUDA(cudaMemcpyAsync(bv + lo * d, vals + lo * d, cnt * d * sizeof(double),
                                              cudaMemcpyHostToDevice, c.copy));
-                    SKY_CUDA(cudaMemcpyAsync(bi + lo, ids + lo, cnt * sizeof(int64_t),
-                                             cudaMemcpyHostToDevice, c.copy));
+                    if (!ids_late)
+                        SKY_CUDA(cudaMemcpyAsync(bi + lo, ids + lo, cnt * sizeof(int64_t),
+                                                 cudaMemcpyHostToDevice, c.copy));
                     SKY_CUDA(cudaEventRecord(c.xev[ch], c.copy));
                     feed.ready[ch] = c.xev[ch];
+                }
+                if (ids_late) {  // every value first, then the ids
+                    SKY_CUDA(cudaMemcpyAsync(bi, ids, n * sizeof(int64_t),
+                                             cudaMemcpyHostToDevice, c.copy));
+                    SKY_CUDA(cudaEventRecord(c.xev[6], c.copy));
+                    c.ids_ready = c.xev[6];
                 }
             } else if (ids_late) {
                 // values first (the skyline starts as soon as they land), the

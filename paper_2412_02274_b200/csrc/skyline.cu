@@ -992,6 +992,7 @@ k_sfs_filter_q(const double* __restrict__ v, const unsigned long long* __restric
     auto precedes_pos = [&](uint32_t ps, uint32_t pt) {
         const unsigned long long ks = key[ps], kt = key[pt];
         if (ks != kt) return ks < kt;
+        if (!ids) return ps < pt;  // (ids in flight: position order, checked later)
         const int64_t is = ids[ps], it = ids[pt];
         return is < it || (is == it && ps < pt);
     };
@@ -1197,7 +1198,7 @@ __global__ void k_emit_skyline(const uint32_t* __restrict__ K, uint64_t S,
     for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < S;
          k += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t p = K[k];
-        oid[k] = ids[p];
+        if (ids) oid[k] = ids[p];
         for (int a = 0; a < d; ++a) skyv[a * S + k] = v[(uint64_t)p * d + a];
     }
 }
@@ -1396,11 +1397,12 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
     st.tuples_in = n;
     // ids still in flight (host-pointer pipeline): ties by position until the
     // ids are needed (rank grid, output); their strict order is checked then
-    const bool ids_late = c.ids_ready != nullptr && !feed;
+    const bool ids_late = c.ids_ready != nullptr;
     const int64_t* tie_ids = ids_late ? nullptr : d_ids;
     bool ids_waited = false;
     auto ensure_ids = [&]() {
-        if (!ids_late || ids_waited) return;
+        // (the streamed head's seed never waits: its ids are not an output)
+        if (!ids_late || ids_waited || (sky_engine & kSkyFirstPrefix)) return;
         ids_waited = true;
         SKY_CUDA(cudaStreamWaitEvent(c.stream, c.ids_ready, 0));
         k_ids_check<<<grid_for(n, kBlock), kBlock, 0, c.stream>>>(d_ids, n, c.d_slots, S_IDSBAD);
@@ -1553,10 +1555,9 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
     // the one-pass rank-grid engine over the whole undecided set (R, r)
     bool grid_used = false;
     auto run_grid = [&]() {
-        ensure_ids();
         uint8_t* gkeep = c.buf[B_SV].as<uint8_t>(r);
         double kms = 0;
-        sky_grid_decide(c, d_vals, d, keys, d_ids, R, r, gkeep, &kms, c.shard_rank,
+        sky_grid_decide(c, d_vals, d, keys, tie_ids, R, r, gkeep, &kms, c.shard_rank,
                         c.shard_world);
         if (c.shard_world > 1) shard_allreduce_max(c, gkeep, r, 1);  // every row decided somewhere
         kernel_ms += kms;
@@ -1811,7 +1812,7 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
                 k_sfs_filter_q<D><<<grid, kBlock, 0, c.stream>>>(
                     d_vals, keys, Rl, (uint32_t)rl, A.Pv, A.Pq, (uint32_t)A.m, A.seg, A.mcell,
                     A.qk, scale, c.d_slots, fkeep, c.d_slots + S_TESTS_SKY, bsf,
-                    seeded ? A.psrc : nullptr, d_ids, solo);
+                    seeded ? A.psrc : nullptr, tie_ids, solo);
             else
                 k_sfs_filter_cells<D><<<grid, kBlock, 0, c.stream>>>(
                     d_vals, d, keys, Rl, (uint32_t)rl, A.Pv, (uint32_t)A.m, A.seg, A.mcell,
@@ -1876,11 +1877,14 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
                 k_score<D><<<grid_for(hi - lo, kBlock, c.num_sms * 8), kBlock, 0, c.stream>>>(
                     d_vals + lo * d, hi - lo, d, keys + lo, c.d_slots, amax, lo);
             });
-            const uint64_t c0 = ch ? lo - 1 : 0;  // pair (lo-1, lo) spans the boundary
-            k_ids_check<<<grid_for(hi - c0, kBlock), kBlock, 0, c.stream>>>(d_ids + c0, hi - c0,
-                                                                           c.d_slots);
+            if (!ids_late) {  // (late ids: checked whole, once they are in)
+                const uint64_t c0 = ch ? lo - 1 : 0;  // pair (lo-1, lo) spans the boundary
+                k_ids_check<<<grid_for(hi - c0, kBlock), kBlock, 0, c.stream>>>(
+                    d_ids + c0, hi - c0, c.d_slots);
+                note_launch(c);
+            }
             SKY_LAUNCH_CHECK();
-            note_launch(c, 2);
+            note_launch(c);
             launch_k5(A, iota + lo, hi - lo, flags + lo, true, scale_snap);
         }
         trace_mark(c, "sky: streamed chunks filtered");
@@ -1994,8 +1998,8 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
     ensure_ids();
     if (kc) {
         trace_mark(c, "sky: rounds done (sync)");
-        k_emit_skyline<<<grid_for(kc, kBlock), kBlock, 0, c.stream>>>(K, kc, d_vals, d, d_ids,
-                                                                      out.d_ids, out.d_skyv);
+        k_emit_skyline<<<grid_for(kc, kBlock), kBlock, 0, c.stream>>>(
+            K, kc, d_vals, d, (ids_late && !ids_waited) ? nullptr : d_ids, out.d_ids, out.d_skyv);
         SKY_LAUNCH_CHECK();
         note_launch(c);
     }

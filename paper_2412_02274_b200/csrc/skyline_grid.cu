@@ -159,6 +159,7 @@ __device__ __noinline__ bool exact_pred(const double* __restrict__ v,
     if (!dom_f64<D>(s, t)) return false;
     const unsigned long long ks = key[ps], kt = key[pt];
     if (ks != kt) return ks < kt;  // dominance implies ks <= kt
+    if (!ids) return ps < pt;  // (ids in flight: position order, checked later)
     const int64_t is_ = ids[ps], it_ = ids[pt];
     return is_ < it_ || (is_ == it_ && ps < pt);
 }

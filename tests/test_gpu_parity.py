@@ -439,6 +439,26 @@ def test_late_ids_speculation(gen, ids_kind):
     assert res.g_max == gm and res.den.tolist() == den.tolist()
 
 
+@pytest.mark.parametrize("gen,d,ids_kind", [("ant", 3, "permuted"), ("lattice", 3, "permuted"),
+                                             ("ant", 7, "one_swap"), ("ant", 7, "sorted")])
+def test_late_ids_streamed(gen, d, ids_kind):
+    """Streamed host inputs (>= 48 MB): every value chunk first, the ids last;
+    the head seed, the seeded filter and the rank-grid engine (ant d = 7)
+    order ties by position until the ids are in and checked."""
+    n = 2_000_000 if d == 3 else 1_000_000
+    v = sk.generate(gen, n, d, 23)
+    rng = np.random.default_rng(23)
+    ids = np.arange(n, dtype=np.int64)
+    if ids_kind == "permuted":
+        ids = rng.permutation(n).astype(np.int64)
+    elif ids_kind == "one_swap":
+        ids[0], ids[1] = ids[1], ids[0]
+    res = _host_vs_device(v, ids)
+    if d == 3:
+        pos, _ = po.skyline_sfs(v, ids)
+        assert res.positions.tolist() == pos.tolist()
+
+
 # ------------------------------------------------ sharded calls with an installed collective
 def _emulated_two_ranks(run):
     """Emulate a 2-rank group on one GPU: rank 1 runs first and its MAX
