@@ -540,6 +540,70 @@ __global__ void k_gap_witness(const double* __restrict__ v, uint64_t S, int d, i
     if (found) atomicOr(&slots[S_FLAG], 1ULL);
 }
 
+// The same witness with the buckets in shared memory, one attribute per
+// blockIdx.y (cap <= kWitnessSmemCap): each block looks for a pair in its own
+// share of the column — no global CAS contention (the global-table form
+// serialises millions of CAS on d x 2cap addresses at C5).  Any pair proves
+// the cap, so block-local detection is exact; S <= 4096 runs one block per
+// attribute (the whole column, like the global table).
+constexpr int kWitnessSmemCap = 2048;
+
+__global__ void __launch_bounds__(256)
+    k_gap_witness_smem(const double* __restrict__ v, uint64_t S, int cap,
+                       unsigned long long* __restrict__ slots) {
+    __shared__ unsigned long long tab[2 * kWitnessSmemCap];
+    __shared__ int any;
+    const int nb = 2 * cap;
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) tab[b] = 0;
+    if (threadIdx.x == 0) any = 0;
+    __syncthreads();
+    const double* col = v + (uint64_t)blockIdx.y * S;
+    unsigned long long mx = 0;
+    bool found = false;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < S;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const double x = col[i];
+        const unsigned long long bits = ord_bits(x);
+        mx = bits > mx ? bits : mx;
+        if (!(x >= 0.0 && x < 1.0) || found) continue;
+        int b = (int)floor(__dmul_rn(x, (double)nb));
+        b = b < 0 ? 0 : (b >= nb ? nb - 1 : b);
+        unsigned long long old = tab[b];
+        if (old == 0ULL) old = atomicCAS(&tab[b], 0ULL, bits + 1);
+        if (old != 0ULL && old != bits + 1) {
+            const double w = __longlong_as_double((long long)(old - 1));
+            const double gap = x > w ? __dsub_rn(x, w) : __dsub_rn(w, x);
+            if (gap > 0.0 && __ddiv_rn(1.0, gap) >= (double)cap) found = true;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long x = __shfl_down_sync(0xffffffffu, mx, o);
+        mx = x > mx ? x : mx;
+    }
+    if ((threadIdx.x & 31) == 0) atomicMax(&slots[S_MAXV], mx);
+    if (found) any = 1;
+    __syncthreads();
+    if (threadIdx.x == 0 && any) atomicOr(&slots[S_FLAG], 1ULL);
+}
+
+// one launch of the witness (shared-memory buckets when cap allows)
+void launch_gap_witness(Ctx& c, const double* d_soa, uint64_t S, int d, int cap,
+                        unsigned long long* table) {
+    if (cap <= kWitnessSmemCap) {
+        const uint64_t want = (S + 4095) / 4096;
+        const unsigned bx = (unsigned)std::max<uint64_t>(
+            1, std::min<uint64_t>(want, (uint64_t)c.num_sms * 8 / (uint64_t)d + 1));
+        k_gap_witness_smem<<<dim3(bx, (unsigned)d), 256, 0, c.stream>>>(d_soa, S, cap, c.d_slots);
+    } else {
+        SKY_CUDA(cudaMemsetAsync(table, 0, sizeof(unsigned long long) * d * 2 * cap, c.stream));
+        k_gap_witness<<<grid_for(S * d, kBlock), kBlock, 0, c.stream>>>(d_soa, S, d, cap, table,
+                                                                         c.d_slots);
+    }
+    SKY_LAUNCH_CHECK();
+    note_launch(c);
+}
+
 // gres.cpp:15-28 on the device: per column sort + adjacent-difference min.
 // Returns false when every attribute is constant.
 bool min_positive_gap_device(Ctx& c, const double* d_soa, uint64_t S, int d, double* gap,
@@ -580,11 +644,7 @@ int g_max_device(Ctx& c, const double* d_soa, uint64_t S, int d, int cap, double
     if (cap > 0 && cap <= 65536 && S >= 2) {
         zero_slots(c);
         unsigned long long* table = c.buf[B_CELLS].as<unsigned long long>((uint64_t)d * 2 * cap);
-        SKY_CUDA(cudaMemsetAsync(table, 0, sizeof(unsigned long long) * d * 2 * cap, c.stream));
-        k_gap_witness<<<grid_for(S * d, kBlock), kBlock, 0, c.stream>>>(d_soa, S, d, cap, table,
-                                                                         c.d_slots);
-        SKY_LAUNCH_CHECK();
-        note_launch(c);
+        launch_gap_witness(c, d_soa, S, d, cap, table);
         read_slots(c, S_MAXV, 3);  // S_MAXV, S_BAD, S_FLAG
         if (c.h_slots[S_FLAG] & 1ULL) {
             unsigned long long mb = c.h_slots[S_MAXV];
@@ -632,10 +692,9 @@ GresOut gres_device(Ctx& c, const double* d_skyv, const int64_t* d_ids, uint64_t
         trace_mark(c, "gres: start (speculative)");
         k_gres_spec_init<<<grid_for(S > ntab ? S : ntab, kBlock), kBlock, 0, c.stream>>>(
             c.d_slots, table, ntab, d_den, S, act);
-        k_gap_witness<<<grid_for(S * d, kBlock), kBlock, 0, c.stream>>>(d_skyv, S, d, cap, table,
-                                                                         c.d_slots);
         SKY_LAUNCH_CHECK();
-        note_launch(c, 2);
+        note_launch(c);
+        launch_gap_witness(c, d_skyv, S, d, cap, table);
         cudaEvent_t e0 = c.ev[10], e1 = c.ev[11];
         SKY_CUDA(cudaEventRecord(e0, c.stream));
         if (gres_cells_smem_spec(c, d_skyv, S, d, cap, act, S, d_den)) {

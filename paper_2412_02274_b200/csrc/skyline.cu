@@ -1363,6 +1363,7 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
     // ---- streamed input: seed from the head while the rest is still in flight
     uint32_t* seed = nullptr;
     uint64_t nseed = 0;
+    bool head_grid = false;
     unsigned long long* scale_snap = nullptr;
     if (feed) {
         SKY_CUDA(cudaStreamWaitEvent(c.stream, feed->ready[0], 0));
@@ -1373,6 +1374,7 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
                 const SkylineOut h =
                     skyline_device(c, d_vals, d_ids, feed->bound[1], d, plan, nullptr, 0,
                                    kSkyAbortIfLarge | kSkyFirstPrefix, nullptr);
+                head_grid = h.aborted;  // the head's first prefix asked for the rank grid
                 if (!h.aborted && h.S > 0 && h.S <= kCTACap) {
                     seed = c.buf[B_SEED].as<uint32_t>(h.S);
                     scale_snap = c.buf[B_AMAX2].as<unsigned long long>(kMaxDims);
@@ -1898,7 +1900,10 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
             fprintf(stderr, "[skygpu trace] streamed: seed %llu, survivors %llu of %llu\n",
                     (unsigned long long)nseed, (unsigned long long)r, (unsigned long long)n);
     }
-    if (sky_engine == SKYGPU_SKY_GRID && r > 0 && sky_grid_bins(r, d)) {
+    // the rank grid at once: asked for, or the streamed head's first prefix
+    // already showed a large skyline (no first round to repeat on all n)
+    if ((sky_engine == SKYGPU_SKY_GRID || (head_grid && sky_engine == 0)) && r > 0 &&
+        sky_grid_bins(r, d)) {
         read_slots(c, S_BAD, 11);
         validate();
         run_grid();
