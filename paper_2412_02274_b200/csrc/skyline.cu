@@ -113,7 +113,7 @@ __global__ void k_score(const double* __restrict__ v, uint64_t n, int d,
         }
         const unsigned long long b = ord_bits(s);
         key[i] = b;
-        mn = b < mn ? b : mn;
+        mn = b < mn && b > 0 ? b : mn;  // min POSITIVE key (zero sums: bucket 0 below)
         mx = b > mx ? b : mx;
         if (bad) atomicMin(&slots[S_BAD], static_cast<unsigned long long>(base + i));
         if (ids && i + 1 < n && ids[i] >= ids[i + 1]) atomicOr(&slots[S_FLAG], 1ULL);
@@ -607,6 +607,33 @@ __device__ __forceinline__ bool precedes(unsigned long long ka, int64_t ia,
 //     bucket_start + rank.
 constexpr uint32_t kKeyBuckets = 4096;
 
+// bucket parameters of the prefix sort computed on the device from the
+// round's slots (a round sized on the device: the host has not read them):
+// kmin = min key; keys up to the threshold - 1 (or the max key) spread over
+// 4096 buckets — the host's formula in decide_prefix
+// monotone key -> bucket map: keys below kmin (the zero sums; kmin is the
+// smallest POSITIVE key) share bucket 0, the rest spread linearly over the
+// raw bits from kmin — a zero sum no longer stretches the span (C3: 149 zero
+// tuples once crowded the whole prefix into a couple of buckets)
+__device__ __forceinline__ uint32_t key_bucket(unsigned long long key, unsigned long long kmin,
+                                               int shift) {
+    if (key < kmin) return 0;
+    const unsigned long long x = ((key - kmin) >> shift) + 1;
+    return x < kKeyBuckets ? (uint32_t)x : kKeyBuckets - 1;
+}
+
+__device__ __forceinline__ void bucket_params_dev(const unsigned long long* __restrict__ slots,
+                                                  int use_thr, unsigned long long& kmin,
+                                                  int& shift) {
+    const unsigned long long gmin = slots[S_SMIN] == ~0ULL ? 0 : slots[S_SMIN];
+    const unsigned long long thr = use_thr ? slots[S_THR] : ~0ULL, gmax = slots[S_SMAX];
+    const unsigned long long top = thr == ~0ULL || thr - 1 > gmax ? gmax : thr - 1;
+    const unsigned long long span = top > gmin ? top - gmin : 0;
+    const int bits = span ? 64 - __clzll((long long)span) : 0;
+    kmin = gmin;
+    shift = bits > 12 ? bits - 12 : 0;
+}
+
 // device-sized launch (the speculative final round): the item count lives in
 // *mdev; a count above the launch's capacity m means the launch does not
 // apply and every kernel returns at once
@@ -621,8 +648,10 @@ __device__ __forceinline__ bool dev_count(const unsigned long long* mdev, uint32
 __global__ void __launch_bounds__(1024)
 k_bucket_order(const uint32_t* __restrict__ in, uint32_t m, const unsigned long long* __restrict__ key,
                unsigned long long kmin, int shift, uint32_t* __restrict__ out,
-               uint32_t* __restrict__ bstart, const unsigned long long* __restrict__ mdev) {
+               uint32_t* __restrict__ bstart, const unsigned long long* __restrict__ mdev,
+               const unsigned long long* __restrict__ pslots = nullptr, int use_thr = 1) {
     if (!dev_count(mdev, m)) return;
+    if (pslots) bucket_params_dev(pslots, use_thr, kmin, shift);
     __shared__ uint32_t cnt[kKeyBuckets];
     for (uint32_t b = threadIdx.x; b < kKeyBuckets; b += 1024) cnt[b] = 0;
     __syncthreads();
@@ -632,8 +661,7 @@ k_bucket_order(const uint32_t* __restrict__ in, uint32_t m, const unsigned long 
         const uint32_t i = threadIdx.x + j * 1024;
         bk[j] = 0;
         if (i < m) {
-            const unsigned long long x = (key[in[i]] - kmin) >> shift;
-            bk[j] = x < kKeyBuckets ? (uint32_t)x : kKeyBuckets - 1;
+            bk[j] = key_bucket(key[in[i]], kmin, shift);
             atomicAdd(&cnt[bk[j]], 1u);
         }
     }
@@ -653,14 +681,16 @@ __global__ void k_bucket_rank(const uint32_t* __restrict__ in, uint32_t m,
                               const unsigned long long* __restrict__ key,
                               const int64_t* __restrict__ ids, unsigned long long kmin, int shift,
                               const uint32_t* __restrict__ bstart, uint32_t* __restrict__ out,
-                              const unsigned long long* __restrict__ mdev) {
+                              const unsigned long long* __restrict__ mdev,
+                              const unsigned long long* __restrict__ pslots = nullptr,
+                              int use_thr = 1) {
     if (!dev_count(mdev, m)) return;
+    if (pslots) bucket_params_dev(pslots, use_thr, kmin, shift);
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
         const uint32_t p = in[i];
         const unsigned long long kp = key[p];
         const long long ip = ids ? ids[p] : (long long)p;  // (no ids: position order)
-        const unsigned long long x = (kp - kmin) >> shift;
-        const uint32_t b = x < kKeyBuckets ? (uint32_t)x : kKeyBuckets - 1;
+        const uint32_t b = key_bucket(kp, kmin, shift);
         const uint32_t s0 = bstart[b], s1 = bstart[b + 1];
         uint32_t rank = 0;
         for (uint32_t j = s0; j < s1; ++j) {
@@ -1336,6 +1366,7 @@ int cells_per_dim(uint64_t m, int d, uint32_t* ncells) {
 namespace {
 // first-round engine gate: most of the prefix survived -> rank-grid engine
 __global__ void k_grid_gate(unsigned long long* slots, uint64_t m) {
+    if (m == 0) m = slots[S_C1];  // (a device-sized round: the prefix count)
     if (threadIdx.x == 0) slots[S_GATE] = slots[S_C2] * 4 > m * 3 ? 1ULL : 0ULL;
 }
 // streamed input: seeded K5 state (no decided prefix, |A'| = the seed)
@@ -1580,6 +1611,13 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
     };
     // sort a prefix by (sum, id), decide it (K4) and append its skyline tuples
     // to K; true when the whole undecided set was this prefix
+    // capacity of a device-sized round (one CTA's 16384; SKYGPU_DEV_CAP lowers
+    // it so tests can drive the redo paths)
+    const uint64_t dev_cap = [] {
+        const char* e = getenv("SKYGPU_DEV_CAP");
+        const long long v = e ? atoll(e) : 0;
+        return v > 0 && v < (long long)kCTACap ? (uint64_t)v : (uint64_t)kCTACap;
+    }();
     static const bool intra_chunked = [] {
         const char* e = getenv("SKYGPU_INTRA");
         return !(e && e[0] == '1');  // SKYGPU_INTRA=1: one warp per candidate
@@ -1610,12 +1648,17 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
                                 (kMaxCells + 1);
                 // (the in-bucket rank stays a many-CTA kernel: a bucket of
                 // equal sums — C3's zero tuples — would serialise one CTA)
+                // (a device-sized round: the host may not have seen the key
+                // range or the threshold yet, the kernels derive the bucket
+                // parameters from the slots; a final round has no threshold)
+                const unsigned long long* ps = mdev ? c.d_slots : nullptr;
+                const int use_thr = final_round ? 0 : 1;
                 k_bucket_order<<<1, 1024, 0, c.stream>>>(Pfull, (uint32_t)m, keys, gmin, shift, Pb,
-                                                         bst, mdev);
+                                                         bst, mdev, ps, use_thr);
                 SKY_LAUNCH_CHECK();
                 k_bucket_rank<<<grid_for(m, kBlock), kBlock, 0, c.stream>>>(Pb, (uint32_t)m, keys,
                                                                              tie_ids, gmin, shift, bst,
-                                                                             Ps, mdev);
+                                                                             Ps, mdev, ps, use_thr);
                 SKY_LAUNCH_CHECK();
                 note_launch(c, 2);
             } else {
@@ -1641,7 +1684,8 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
             const uint64_t wi = std::min<uint64_t>(m, (uint64_t)c.num_sms * 64);
             if (qpre && intra_chunked)
                 SKY_CUDA(cudaMemsetAsync(keep, 1, m, c.stream));
-            cudaEvent_t k0 = mdev ? c.ev[16] : e0, k1 = mdev ? c.ev[17] : e1;
+            cudaEvent_t k0 = (mdev && final_round) ? c.ev[16] : e0;
+            cudaEvent_t k1 = (mdev && final_round) ? c.ev[17] : e1;
             SKY_CUDA(cudaEventRecord(k0, c.stream));
             dispatch_d(d, [&](auto DC) {
                 constexpr int D = decltype(DC)::value;
@@ -1678,10 +1722,11 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
             note_launch(c);
             trace_mark(c, "sky: K4 intra kernel");
             // A' in (sum, id) order appended to K; its count lands in S_C2
-            if (mdev) {
-                k_cta_select<<<1, 1024, 0, c.stream>>>(order, nullptr, keep, (uint32_t)m, K + kc,
-                                                       nullptr, c.d_slots + S_SEL2, mdev,
-                                                       c.d_slots + S_C2);
+            if (mdev) {  // final: count in S_SEL2, after the round's A' (S_C2)
+                k_cta_select<<<1, 1024, 0, c.stream>>>(
+                    order, nullptr, keep, (uint32_t)m, K + kc, nullptr,
+                    c.d_slots + (final_round ? S_SEL2 : S_C2), mdev,
+                    final_round ? c.d_slots + S_C2 : nullptr);
                 SKY_LAUNCH_CHECK();
                 note_launch(c);
                 return false;
@@ -1841,11 +1886,11 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
         kernel_launches += 1;
         if (spec_final) {
             c.h_slots[S_THR] = ~0ULL;  // the final round: no threshold
-            decide_prefix(Rnext, kCTACap, true, c.d_slots + S_C3);
+            decide_prefix(Rnext, dev_cap, true, c.d_slots + S_C3);
             trace_mark(c, "sky: speculative final round queued");
-            read_slots(c, S_SEL2, 9);  // S_SEL2 .. S_GATE
+            read_slots(c, S_BAD, 12);  // S_BAD .. S_GATE (a device-sized round validates here)
             const uint64_t sv = c.h_slots[S_C3];
-            *spec_done = sv > 0 && sv <= kCTACap && !c.h_slots[S_GATE];
+            *spec_done = sv > 0 && sv <= dev_cap && !c.h_slots[S_GATE];
         } else {
             read_slots(c, S_C2, 3);  // S_C2 (A'), S_C3 (survivors), S_GATE
         }
@@ -1929,8 +1974,69 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
         select_if(c, R, r, BelowThreshold{keys, c.d_slots + S_THR}, Pfull, c.d_slots + S_C1);
         note_launch(c, 1);
         trace_mark(c, "sky: select prefix");
-        read_slots(c, S_BAD, 11);
-        validate();
+        // the round sized on the device — no host round trip before K5: the
+        // prefix sort, K4, K5, the survivor selection and the ride-along final
+        // round read the prefix count from its slot; the host checks it with
+        // the round's one read-back and, in the rare case the prefix did not
+        // fit one CTA (every sized kernel then returned at once), redoes the
+        // round the synchronous way
+        const bool gate_cond = rounds == 0 && (sky_engine & ~kSkyAbortIfLarge) == 0 &&
+                               r >= kGridMin && sky_grid_bins(r, d);
+        const bool spec_ok = qpre && intra_chunked && !getenv("SKYGPU_NO_SPEC_FINAL");
+        if (spec_ok && !(sky_engine & kSkyFirstPrefix) && w <= kCTACap / 2 && r > w &&
+            !getenv("SKYGPU_NO_DEV_ROUND")) {
+            uint32_t* const Rin = R;
+            const uint64_t rin = r;
+            decide_prefix(Pfull, dev_cap, false, c.d_slots + S_C1);
+            if (gate_cond) {
+                k_grid_gate<<<1, 32, 0, c.stream>>>(c.d_slots, 0);
+                SKY_LAUNCH_CHECK();
+                note_launch(c);
+            }
+            bool spec_done = false;
+            const uint64_t a = filter_against(K + kc, dev_cap, false, true, &spec_done);
+            validate();
+            const uint64_t m = c.h_slots[S_C1];
+            if (m == 0) throw Error(SKYGPU_ERUNTIME, "skyline: empty prefix (internal)");
+            if (m <= dev_cap) {
+                ++rounds;  // (decide_prefix's own count: the round ran)
+                kernel_launches += 1;
+                if (c.trace)
+                    fprintf(stderr, "[skygpu trace] round %d (device-sized): prefix %llu, A' %llu, "
+                            "survivors %llu\n", rounds, (unsigned long long)m,
+                            (unsigned long long)a, (unsigned long long)r);
+                if (gate_cond && c.h_slots[S_GATE]) {
+                    if (sky_engine & kSkyAbortIfLarge) {
+                        out.aborted = true;
+                        return out;
+                    }
+                    run_grid();
+                    break;
+                }
+                float ms4 = 0;
+                SKY_CUDA(cudaEventElapsedTime(&ms4, e0, e1));
+                kernel_ms += ms4;
+                kc += a;
+                if (spec_done) {
+                    SKY_CUDA(cudaEventElapsedTime(&ms4, c.ev[16], c.ev[17]));
+                    kernel_ms += ms4;
+                    kc += c.h_slots[S_SEL2];
+                    ++rounds;
+                    kernel_launches += 1;
+                    break;
+                }
+                if (a * 2 > m) want = std::min(want * 4, kMaxPrefix);
+                continue;
+            }
+            // the prefix did not fit: back to the round's input, synchronous
+            R = Rin;
+            r = rin;
+            Rnext = (Rin == Rbuf1) ? Rbuf0 : Rbuf1;
+            trace_mark(c, "sky: device-sized round missed, synchronous redo");
+        } else {
+            read_slots(c, S_BAD, 11);
+            validate();
+        }
         const uint64_t m = c.h_slots[S_C1];
         if (m == 0) throw Error(SKYGPU_ERUNTIME, "skyline: empty prefix (internal)");
 
@@ -1950,8 +2056,7 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
         // everything at once with the rank-grid engine instead of filtering.
         // Decided on the device (no extra host round trip): the gate makes
         // K5 keep every candidate, the host switches after K5's sync.
-        const bool gate = rounds == 1 && (sky_engine & ~kSkyAbortIfLarge) == 0 && r >= kGridMin &&
-                          sky_grid_bins(r, d);
+        const bool gate = rounds == 1 && gate_cond;
         if (gate) {
             k_grid_gate<<<1, 32, 0, c.stream>>>(c.d_slots, m);
             SKY_LAUNCH_CHECK();
@@ -1960,7 +2065,6 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
 
         // the final round rides along when the survivors fit one CTA
         // (checked on the device; the host only sees the outcome)
-        const bool spec_ok = qpre && intra_chunked && !getenv("SKYGPU_NO_SPEC_FINAL");
         bool spec_done = false;
         const uint64_t a = filter_against(K + kc, m, false, spec_ok, &spec_done);  // synchronises
         if (c.trace)

@@ -26,7 +26,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "_lib", "libskygpu.so")
+# (SKYGPU_LIB_PATH: an alternative in-tree build, for A/B measurements)
+LIB_PATH = os.environ.get("SKYGPU_LIB_PATH") or os.path.join(_PKG, "_lib", "libskygpu.so")
 
 SKYGPU_OK, SKYGPU_EINVAL, SKYGPU_ERUNTIME, SKYGPU_ECUDA, SKYGPU_ENOMEM = range(5)
 GRES_AUTO, GRES_PAIRS, GRES_CELLS = 0, 1, 2

@@ -410,6 +410,23 @@ def test_streamed_seed_dominated_by_tail():
     assert 3 not in res.positions.tolist() and n - 2 in res.positions.tolist()
 
 
+@pytest.mark.parametrize("cap", ["1000", "6000", "20000"])
+@pytest.mark.parametrize("gen,d", [("ant", 3), ("uni", 4), ("corr", 6), ("lattice", 2)])
+def test_device_sized_rounds_and_their_redo(monkeypatch, gen, d, cap):
+    """The round sized on the device (prefix count never read before K5)
+    and the ride-along final round; a lowered capacity (SKYGPU_DEV_CAP) makes
+    the prefix or the survivors miss it, which must redo the round the
+    synchronous way with the same result."""
+    monkeypatch.setenv("SKYGPU_DEV_CAP", cap)
+    v = sk.generate(gen, 300_000, d, 31)
+    ids = np.arange(len(v), dtype=np.int64)
+    res = sk.pipeline(v, ids, cap=25)
+    pos, _ = po.skyline_sfs(v, ids)
+    assert res.positions.tolist() == pos.tolist()
+    den, gm, _ = po.grid_resistance(v[pos], ids[pos], 25)
+    assert res.g_max == gm and res.den.tolist() == den.tolist()
+
+
 @pytest.mark.parametrize("gen,ids_kind", [("ant", "permuted"), ("lattice", "permuted"),
                                            ("lattice", "strided"), ("lattice", "one_swap"),
                                            ("uni", "duplicate")])
