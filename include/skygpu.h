@@ -62,9 +62,12 @@ extern "C" {
 #define SKYGPU_SLICED 3
 
 /* gres engines */
-#define SKYGPU_GRES_AUTO 0  /* pair-dominance kernel unless the cell engine is far cheaper */
+#define SKYGPU_GRES_AUTO 0  /* the small-grid cell kernel when it applies (d <= 4, codes <= 31),
+                               else pairs unless the per-step cell engine is far cheaper */
 #define SKYGPU_GRES_PAIRS 1 /* (tuple, comparator, step) dominance tests, early exit */
-#define SKYGPU_GRES_CELLS 2 /* per-step occupancy prefix-OR over the code grid */
+#define SKYGPU_GRES_CELLS 2 /* occupancy prefix-OR over the code grid: every step in one
+                               shared-memory launch for small grids, per step in HBM otherwise
+                               (stats: gres_cells = 0 for the former) */
 
 /* skygpu_pipeline flags */
 #define SKYGPU_DEVICE_PTRS 1u   /* vals/ids/outputs are device pointers */
@@ -90,7 +93,8 @@ typedef struct skygpu_stats {
     uint64_t skyline_size;         /* S */
     uint64_t skyline_tests;        /* dominance tests executed by the skyline kernels */
     uint64_t gres_tests;           /* (candidate, comparator, g) code tests executed */
-    uint64_t gres_cells;           /* cell engine: algorithmic bytes (3 grid sweeps + 2 value reads per step) */
+    uint64_t gres_cells;           /* per-step cell engine: algorithmic bytes (3 grid sweeps + 2 value
+                                      reads per step); 0 for the shared-memory small-grid kernel */
     int g_max;                     /* ResistanceMetrics::g_max (gres.hpp:46) */
     int gres_steps;                /* interval counts scanned (g_max-1 or fewer) */
     int gres_engine;               /* engine actually used */
