@@ -81,6 +81,7 @@ void read_slots(Ctx& c, int first, int count) {
 
 namespace {
 __global__ void k_init_slots(unsigned long long* slots, int mode) {
+    pdl_wait();
     const int i = threadIdx.x;
     if (i >= S_COUNT_) return;
     if (mode == 1) {  // test counters only
@@ -105,25 +106,25 @@ __global__ void k_init_slots(unsigned long long* slots, int mode) {
 }  // namespace
 
 void zero_slots(Ctx& c) {
-    k_init_slots<<<1, 32, 0, c.stream>>>(c.d_slots, 0);
+    pdl_launch(k_init_slots, 1, 32, 0, c.stream, c.d_slots, 0);
     SKY_LAUNCH_CHECK();
     note_launch(c);
 }
 
 void reset_tests(Ctx& c) {
-    k_init_slots<<<1, 32, 0, c.stream>>>(c.d_slots, 1);
+    pdl_launch(k_init_slots, 1, 32, 0, c.stream, c.d_slots, 1);
     SKY_LAUNCH_CHECK();
     note_launch(c);
 }
 
 void reset_counts(Ctx& c) {
-    k_init_slots<<<1, 32, 0, c.stream>>>(c.d_slots, 2);
+    pdl_launch(k_init_slots, 1, 32, 0, c.stream, c.d_slots, 2);
     SKY_LAUNCH_CHECK();
     note_launch(c);
 }
 
 void reset_range(Ctx& c) {
-    k_init_slots<<<1, 32, 0, c.stream>>>(c.d_slots, 3);
+    pdl_launch(k_init_slots, 1, 32, 0, c.stream, c.d_slots, 3);
     SKY_LAUNCH_CHECK();
     note_launch(c);
 }
@@ -136,6 +137,7 @@ namespace {
 
 __global__ void k_aos_to_soa(const double* __restrict__ a, uint64_t n, int d,
                              double* __restrict__ s) {
+    pdl_wait();
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n * d;
          i += (uint64_t)gridDim.x * blockDim.x) {
         uint64_t t = i / d;
@@ -146,6 +148,7 @@ __global__ void k_aos_to_soa(const double* __restrict__ a, uint64_t n, int d,
 
 __global__ void k_snap(const double* __restrict__ v, uint64_t total, int g,
                        double* __restrict__ out) {
+    pdl_wait();
     const double gd = (double)g;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
          i += (uint64_t)gridDim.x * blockDim.x)
@@ -154,6 +157,7 @@ __global__ void k_snap(const double* __restrict__ v, uint64_t total, int g,
 
 __global__ void k_check_values(const double* __restrict__ v, uint64_t total,
                                unsigned long long* __restrict__ slots) {
+    pdl_wait();
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
          i += (uint64_t)gridDim.x * blockDim.x)
         if (!(v[i] >= 0.0)) atomicMin(&slots[S_BAD], (unsigned long long)i);
@@ -275,9 +279,11 @@ int closest_slices(long long target, int e) {
 }  // namespace
 
 namespace {
-__global__ void k_clear_slot(unsigned long long* slots, int i) { slots[i] = 0; }
+__global__ void k_clear_slot(unsigned long long* slots, int i) {
+    pdl_wait(); slots[i] = 0; }
 
 __global__ void k_widen(const uint32_t* __restrict__ a, uint64_t* __restrict__ b, uint64_t n) {
+    pdl_wait();
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x)
         b[i] = a[i];
@@ -286,17 +292,20 @@ __global__ void k_widen(const uint32_t* __restrict__ a, uint64_t* __restrict__ b
 
 namespace {
 __global__ void k_iota64(int64_t* __restrict__ a, uint64_t n) {
+    pdl_wait();
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x)
         a[i] = (int64_t)i;
 }
 __global__ void k_fill_i32(int32_t* __restrict__ a, uint64_t n, int32_t v) {
+    pdl_wait();
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x)
         a[i] = v;
 }
 __global__ void k_mark_i32(int32_t* __restrict__ a, const uint32_t* __restrict__ at, uint64_t n,
                            int32_t v) {
+    pdl_wait();
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x)
         a[at[i]] = v;
@@ -313,20 +322,20 @@ void shard_allreduce_max(Ctx& c, void* dev_ptr, uint64_t count, int elem_bytes) 
 }
 
 void iota64(Ctx& c, int64_t* a, uint64_t n) {
-    k_iota64<<<grid_for(n, 256), 256, 0, c.stream>>>(a, n);
+    pdl_launch(k_iota64, grid_for(n, 256), 256, 0, c.stream, a, n);
     SKY_LAUNCH_CHECK();
     note_launch(c);
 }
 
 void widen_u32_u64(Ctx& c, const uint32_t* a, uint64_t* b, uint64_t n) {
-    k_widen<<<grid_for(n, 256), 256, 0, c.stream>>>(a, b, n);
+    pdl_launch(k_widen, grid_for(n, 256), 256, 0, c.stream, a, b, n);
     SKY_LAUNCH_CHECK();
     note_launch(c);
 }
 
 void aos_to_soa(Ctx& c, const double* d_aos, uint64_t n, int d, double* d_soa) {
     if (n == 0) return;
-    k_aos_to_soa<<<grid_for(n * d, 256), 256, 0, c.stream>>>(d_aos, n, d, d_soa);
+    pdl_launch(k_aos_to_soa, grid_for(n * d, 256), 256, 0, c.stream, d_aos, n, d, d_soa);
     SKY_LAUNCH_CHECK();
     note_launch(c);
 }
@@ -468,7 +477,7 @@ int skygpu_grid_resistance(const double* sky_vals, const int64_t* sky_ids, uint6
         SKY_CUDA(cudaMemcpyAsync(di, sky_ids, s * sizeof(int64_t), cudaMemcpyHostToDevice,
                                  c.stream));
         zero_slots(c);
-        k_check_values<<<grid_for(s * d, 256), 256, 0, c.stream>>>(dv, s * d, c.d_slots);
+        pdl_launch(k_check_values, grid_for(s * d, 256), 256, 0, c.stream, dv, s * d, c.d_slots);
         SKY_LAUNCH_CHECK();
         note_launch(c);
         read_slots(c, S_BAD, 1);
@@ -498,7 +507,7 @@ int skygpu_snap_relation(const double* vals, uint64_t count, int intervals, doub
         double* dq = c.buf[B_PROJ].as<double>(count);
         SKY_CUDA(cudaMemcpyAsync(dv, vals, count * sizeof(double), cudaMemcpyHostToDevice,
                                  c.stream));
-        k_snap<<<grid_for(count, 256), 256, 0, c.stream>>>(dv, count, intervals, dq);
+        pdl_launch(k_snap, grid_for(count, 256), 256, 0, c.stream, dv, count, intervals, dq);
         SKY_LAUNCH_CHECK();
         SKY_CUDA(cudaMemcpyAsync(out, dq, count * sizeof(double), cudaMemcpyDeviceToHost,
                                  c.stream));
@@ -605,7 +614,7 @@ int skygpu_pipeline(const double* vals, const int64_t* ids, uint64_t n, int d,
                 feed.nchunks = 4;
                 c.trace_chunks = feed.nchunks;
                 for (int ch = 0; ch <= feed.nchunks; ++ch) feed.bound[ch] = n * ch / feed.nchunks;
-                if (ids_late) k_clear_slot<<<1, 1, 0, c.stream>>>(c.d_slots, S_IDSBAD);
+                if (ids_late) pdl_launch(k_clear_slot, 1, 1, 0, c.stream, c.d_slots, S_IDSBAD);
                 SKY_LAUNCH_CHECK();
                 // the copies follow the stream's earlier work on these buffers
                 SKY_CUDA(cudaEventRecord(c.xev[9], c.stream));
@@ -635,7 +644,7 @@ int skygpu_pipeline(const double* vals, const int64_t* ids, uint64_t n, int d,
                         SKY_CUDA(cudaEventCreateWithFlags(
                             &e, c.trace ? cudaEventDefault : cudaEventDisableTiming));
                 }
-                k_clear_slot<<<1, 1, 0, c.stream>>>(c.d_slots, S_IDSBAD);
+                pdl_launch(k_clear_slot, 1, 1, 0, c.stream, c.d_slots, S_IDSBAD);
                 SKY_LAUNCH_CHECK();
                 SKY_CUDA(cudaMemcpyAsync(bv, vals, n * d * sizeof(double), cudaMemcpyHostToDevice,
                                          c.stream));
@@ -984,8 +993,8 @@ int skygpu_sfs_accounting(const double* vals, const int64_t* ids, uint64_t n, in
         SKY_CUDA(cudaMemcpyAsync(h.data(), cnt, sizeof(unsigned long long) * p,
                                  cudaMemcpyDeviceToHost, c.stream));
         // phase 2: one SFS over the union of the local skylines
-        k_fill_i32<<<grid_for(n, 256), 256, 0, c.stream>>>(dg2, n, -1);
-        if (nk) k_mark_i32<<<grid_for(nk, 256), 256, 0, c.stream>>>(dg2, kept1, nk, 0);
+        pdl_launch(k_fill_i32, grid_for(n, 256), 256, 0, c.stream, dg2, n, -1);
+        if (nk) pdl_launch(k_mark_i32, grid_for(nk, 256), 256, 0, c.stream, dg2, kept1, nk, 0);
         SKY_LAUNCH_CHECK();
         note_launch(c, 2);
         SKY_CUDA(cudaMemsetAsync(cnt + p, 0, sizeof(unsigned long long), c.stream));

@@ -44,6 +44,7 @@ struct CellGeom {
 template <class W>
 __global__ void k_cells_mark(const double* __restrict__ v, uint64_t S, CellGeom geo,
                              W* __restrict__ rows) {
+    pdl_wait();
     const double gd = (double)geo.g;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < S;
          i += (uint64_t)gridDim.x * blockDim.x) {
@@ -57,6 +58,7 @@ __global__ void k_cells_mark(const double* __restrict__ v, uint64_t S, CellGeom 
 // prefix-OR inside each word: bit k |= bits 0..k-1 (attribute 0)
 template <class W>
 __global__ void k_cells_or_word(W* __restrict__ rows, uint64_t n) {
+    pdl_wait();
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x) {
         W x = rows[i];
@@ -75,6 +77,7 @@ __global__ void k_cells_or_word(W* __restrict__ rows, uint64_t n) {
 template <class W>
 __global__ void k_cells_or_dim(W* __restrict__ rows, uint64_t nrows, uint64_t ext,
                                uint64_t stride) {
+    pdl_wait();
     const uint64_t lines = nrows / ext;
     for (uint64_t l = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; l < lines;
          l += (uint64_t)gridDim.x * blockDim.x) {
@@ -109,6 +112,7 @@ template <class W>
 __global__ void __launch_bounds__(kBlock)
 k_cells_or_slab(W* __restrict__ rows, uint64_t nrows, uint32_t e1, uint32_t e2,
                 uint32_t slab_words) {
+    pdl_wait();
     extern __shared__ unsigned char smraw[];
     W* sm = reinterpret_cast<W*>(smraw);
     const uint32_t slab = e1 * e2;
@@ -154,6 +158,7 @@ constexpr int kPairMax = 32;
 template <class W>
 __global__ void __launch_bounds__(kBlock)
 k_cells_or_pair(W* __restrict__ rows, uint64_t nrows, uint32_t ea, uint32_t eb, uint64_t sa) {
+    pdl_wait();
     const uint64_t plane = (uint64_t)ea * eb;
     const uint64_t lines = nrows / plane;
     for (uint64_t l = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; l < lines;
@@ -184,6 +189,7 @@ __global__ void k_cells_query(const double* __restrict__ v, uint64_t S, CellGeom
                               const W* __restrict__ P, const uint32_t* __restrict__ act,
                               uint64_t na, int32_t* __restrict__ den,
                               unsigned long long* __restrict__ undecided) {
+    pdl_wait();
     const double gd = (double)geo.g;
     unsigned long long left = 0;
     for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < na;
@@ -214,6 +220,7 @@ __global__ void k_cells_query(const double* __restrict__ v, uint64_t S, CellGeom
 template <class CW>
 __global__ void k_cells_codes(const double* __restrict__ v, uint64_t S, int d, int g_hi, int G,
                               CW* __restrict__ codes) {
+    pdl_wait();
     // one thread per tuple: its d values read once, the codes of all G steps
     // written (coalesced across the warp at every step)
     for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < S;
@@ -232,6 +239,7 @@ __global__ void k_cells_codes(const double* __restrict__ v, uint64_t S, int d, i
 template <class W, class CW>
 __global__ void k_cells_mark_c(const CW* __restrict__ code, uint64_t S, CellGeom geo,
                                W* __restrict__ rows) {
+    pdl_wait();
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < S;
          i += (uint64_t)gridDim.x * blockDim.x) {
         const CW w = code[i];
@@ -246,6 +254,7 @@ __global__ void k_cells_query_c(const CW* __restrict__ code, CellGeom geo,
                                 const W* __restrict__ P, const uint32_t* __restrict__ act,
                                 uint64_t na, int32_t* __restrict__ den,
                                 unsigned long long* __restrict__ undecided) {
+    pdl_wait();
     unsigned long long left = 0;
     for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < na;
          k += (uint64_t)gridDim.x * blockDim.x) {
@@ -268,6 +277,7 @@ __global__ void k_cells_query_c(const CW* __restrict__ code, CellGeom geo,
 
 __global__ void k_col_max(const double* __restrict__ v, uint64_t S, int d,
                           unsigned long long* __restrict__ out) {
+    pdl_wait();
     for (int j = blockIdx.y; j < d; j += gridDim.y) {
         unsigned long long best = 0;
         for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < S;
@@ -320,13 +330,13 @@ template <class W>
 void sweeps(Ctx& c, W* R, const CellGeom& geo, bool fused) {
     const int d = geo.d;
     auto single = [&](int j) {
-        k_cells_or_dim<W><<<grid_for(geo.rows / geo.ext[j], kBlock), kBlock, 0, c.stream>>>(
+        pdl_launch(k_cells_or_dim<W>, grid_for(geo.rows / geo.ext[j], kBlock), kBlock, 0, c.stream, 
             R, geo.rows, geo.ext[j], geo.stride[j]);
         note_launch(c);
     };
     const uint32_t e1 = d >= 2 ? (uint32_t)geo.ext[1] : 1, e2 = d >= 3 ? (uint32_t)geo.ext[2] : 1;
     if (!fused || d < 2 || (uint64_t)e1 * e2 * sizeof(W) > 128 * 1024) {
-        k_cells_or_word<W><<<grid_for(geo.rows, kBlock), kBlock, 0, c.stream>>>(R, geo.rows);
+        pdl_launch(k_cells_or_word<W>, grid_for(geo.rows, kBlock), kBlock, 0, c.stream, R, geo.rows);
         note_launch(c);
         for (int j = 1; j < d; ++j) single(j);
         return;
@@ -347,14 +357,13 @@ void sweeps(Ctx& c, W* R, const CellGeom& geo, bool fused) {
         attr_set = true;
     }
     const uint64_t nslabs = geo.rows / slab;
-    k_cells_or_slab<W><<<grid_for((nslabs + spb - 1) / spb, 1, c.num_sms * 8), kBlock, smem,
-                         c.stream>>>(R, geo.rows, e1, e2, slab_words);
+    pdl_launch(k_cells_or_slab<W>, grid_for((nslabs + spb - 1) / spb, 1, c.num_sms * 8), kBlock, smem, c.stream, R, geo.rows, e1, e2, slab_words);
     note_launch(c);
     int j = 3;
     while (j < d) {
         if (j + 1 < d && geo.ext[j] <= (uint64_t)kPairMax) {
             const uint64_t lines = geo.rows / (geo.ext[j] * geo.ext[j + 1]);
-            k_cells_or_pair<W><<<grid_for(lines, kBlock), kBlock, 0, c.stream>>>(
+            pdl_launch(k_cells_or_pair<W>, grid_for(lines, kBlock), kBlock, 0, c.stream, 
                 R, geo.rows, (uint32_t)geo.ext[j], (uint32_t)geo.ext[j + 1], geo.stride[j]);
             note_launch(c);
             j += 2;
@@ -386,6 +395,7 @@ __global__ void __launch_bounds__(kSmemBlock)
                  const uint32_t* __restrict__ act, uint32_t na, uint32_t per_block,
                  int32_t* __restrict__ den, unsigned long long* __restrict__ spec,
                  uint32_t ealloc) {
+    pdl_wait();
     extern __shared__ uint32_t P[];
     if (spec) {
         maxv = __longlong_as_double((long long)spec[S_MAXV]);
@@ -485,7 +495,7 @@ bool gres_cells_smem_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int
     uint64_t per_step = ((uint64_t)c.num_sms * 2 + G - 1) / G;
     per_step = std::max<uint64_t>(1, std::min<uint64_t>(per_step, (na + 63) / 64));
     const uint32_t per_block = (uint32_t)((na + per_step - 1) / per_step);
-    k_cells_smem<<<dim3((unsigned)per_step, G), kSmemBlock, smem, c.stream>>>(
+    pdl_launch(k_cells_smem, dim3((unsigned)per_step, G), kSmemBlock, smem, c.stream, 
         d_skyv, (uint32_t)S, d, g_max, maxv, act, (uint32_t)na, per_block, d_den, nullptr, 0);
     SKY_LAUNCH_CHECK();
     note_launch(c);
@@ -512,7 +522,7 @@ bool gres_cells_smem_spec(Ctx& c, const double* d_skyv, uint64_t S, int d, int c
     uint64_t per_step = ((uint64_t)c.num_sms * 2 + G - 1) / G;
     per_step = std::max<uint64_t>(1, std::min<uint64_t>(per_step, (na + 63) / 64));
     const uint32_t per_block = (uint32_t)((na + per_step - 1) / per_step);
-    k_cells_smem<<<dim3((unsigned)per_step, G), kSmemBlock, smem, c.stream>>>(
+    pdl_launch(k_cells_smem, dim3((unsigned)per_step, G), kSmemBlock, smem, c.stream, 
         d_skyv, (uint32_t)S, d, cap, 0.0, act, (uint32_t)na, per_block, d_den, c.d_slots,
         ealloc);
     SKY_LAUNCH_CHECK();
@@ -530,7 +540,7 @@ bool gres_cells_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_ma
     if (g_max < 2 || S == 0 || d > kMaxCellDims) return false;
     auto* colmax = c.buf[B_AMAX].as<unsigned long long>(kMaxDims);
     SKY_CUDA(cudaMemsetAsync(colmax, 0, sizeof(unsigned long long) * kMaxDims, c.stream));
-    k_col_max<<<dim3(grid_for(S, kBlock, 296), (unsigned)d), kBlock, 0, c.stream>>>(d_skyv, S, d,
+    pdl_launch(k_col_max, dim3(grid_for(S, kBlock, 296), (unsigned)d), kBlock, 0, c.stream, d_skyv, S, d,
                                                                                     colmax);
     SKY_LAUNCH_CHECK();
     note_launch(c);
@@ -555,10 +565,10 @@ bool gres_cells_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_ma
     if (d <= 8 && S * (uint64_t)G * cwb <= (16ull << 30)) {
         codes = c.buf[B_CODES].get(S * (uint64_t)G * cwb);
         if (cw32)
-            k_cells_codes<uint32_t><<<grid_for(S, kBlock), kBlock, 0, c.stream>>>(
+            pdl_launch(k_cells_codes<uint32_t>, grid_for(S, kBlock), kBlock, 0, c.stream, 
                 d_skyv, S, d, g_max, G, (uint32_t*)codes);
         else
-            k_cells_codes<unsigned long long><<<grid_for(S, kBlock), kBlock, 0, c.stream>>>(
+            pdl_launch(k_cells_codes<unsigned long long>, grid_for(S, kBlock), kBlock, 0, c.stream, 
                 d_skyv, S, d, g_max, G, (unsigned long long*)codes);
         SKY_LAUNCH_CHECK();
         note_launch(c);
@@ -577,10 +587,10 @@ bool gres_cells_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_ma
         auto run_codes = [&](auto* R, auto* cg) {
             using WR = std::remove_pointer_t<decltype(R)>;
             using CW = std::remove_const_t<std::remove_pointer_t<decltype(cg)>>;
-            k_cells_mark_c<WR, CW><<<gs, kBlock, 0, c.stream>>>(cg, S, geo, R);
+            pdl_launch(k_cells_mark_c<WR, CW>, gs, kBlock, 0, c.stream, cg, S, geo, R);
             sweeps<WR>(c, R, geo, fused);
             reset_counts(c);
-            k_cells_query_c<WR, CW><<<grid_for(na, kBlock), kBlock, 0, c.stream>>>(
+            pdl_launch(k_cells_query_c<WR, CW>, grid_for(na, kBlock), kBlock, 0, c.stream, 
                 cg, geo, R, act, na, d_den, c.d_slots + S_C3);
         };
         const uint64_t coff = (uint64_t)(g_max - g) * S;
@@ -594,17 +604,17 @@ bool gres_cells_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_ma
             run_codes(static_cast<unsigned*>(rows), (const unsigned long long*)codes + coff);
         else if (w64) {
             auto* R = static_cast<unsigned long long*>(rows);
-            k_cells_mark<unsigned long long><<<gs, kBlock, 0, c.stream>>>(d_skyv, S, geo, R);
+            pdl_launch(k_cells_mark<unsigned long long>, gs, kBlock, 0, c.stream, d_skyv, S, geo, R);
             sweeps<unsigned long long>(c, R, geo, fused);
             reset_counts(c);
-            k_cells_query<unsigned long long><<<grid_for(na, kBlock), kBlock, 0, c.stream>>>(
+            pdl_launch(k_cells_query<unsigned long long>, grid_for(na, kBlock), kBlock, 0, c.stream, 
                 d_skyv, S, geo, R, act, na, d_den, c.d_slots + S_C3);
         } else {
             auto* R = static_cast<unsigned*>(rows);
-            k_cells_mark<unsigned><<<gs, kBlock, 0, c.stream>>>(d_skyv, S, geo, R);
+            pdl_launch(k_cells_mark<unsigned>, gs, kBlock, 0, c.stream, d_skyv, S, geo, R);
             sweeps<unsigned>(c, R, geo, fused);
             reset_counts(c);
-            k_cells_query<unsigned><<<grid_for(na, kBlock), kBlock, 0, c.stream>>>(
+            pdl_launch(k_cells_query<unsigned>, grid_for(na, kBlock), kBlock, 0, c.stream, 
                 d_skyv, S, geo, R, act, na, d_den, c.d_slots + S_C3);
         }
         SKY_LAUNCH_CHECK();

@@ -63,6 +63,7 @@ void dispatch_d(int d, F&& f) {
 
 // column j of the SoA skyline into a contiguous buffer (for the gap sort)
 __global__ void k_copy(const double* __restrict__ src, uint64_t n, double* __restrict__ dst) {
+    pdl_wait();
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x)
         dst[i] = src[i];
@@ -71,6 +72,7 @@ __global__ void k_copy(const double* __restrict__ src, uint64_t n, double* __res
 // gres.cpp:20-24: min positive adjacent difference of a sorted column
 __global__ void k_min_gap(const double* __restrict__ col, uint64_t n,
                           unsigned long long* __restrict__ slots) {
+    pdl_wait();
     unsigned long long best = 0x7FF0000000000000ULL;  // +inf
     for (uint64_t i = 1 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x) {
@@ -90,6 +92,7 @@ __global__ void k_min_gap(const double* __restrict__ col, uint64_t n,
 
 __global__ void k_max_value(const double* __restrict__ v, uint64_t n,
                             unsigned long long* __restrict__ slots) {
+    pdl_wait();
     unsigned long long best = 0;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x) {
@@ -111,6 +114,7 @@ template <int D>
 __global__ void __launch_bounds__(kBlock)
 k_check_skyline(const double* __restrict__ v, uint64_t S, int d,
                 unsigned long long* __restrict__ slots) {
+    pdl_wait();
     constexpr int TILE = D > 0 ? 256 : 128;
     constexpr int DM = D > 0 ? D : kMaxDims;
     extern __shared__ double tile[];
@@ -148,6 +152,7 @@ k_check_skyline(const double* __restrict__ v, uint64_t S, int d,
 // projections at step g exactly as the reference: floor(v*g)/g (gres.cpp:46)
 __global__ void k_project(const double* __restrict__ v, uint64_t total, int g,
                           double* __restrict__ q) {
+    pdl_wait();
     const double gd = (double)g;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
          i += (uint64_t)gridDim.x * blockDim.x)
@@ -157,6 +162,7 @@ __global__ void k_project(const double* __restrict__ v, uint64_t total, int g,
 // candidate list of this shard, ascending: the k-th owned tuple of the
 // interleaved 256-tuple chunks rank, rank + world, rank + 2*world, ...
 __global__ void k_shard_iota(uint64_t na, int rank, int world, uint32_t* __restrict__ act) {
+    pdl_wait();
     for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < na;
          k += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t chunk = (uint64_t)rank + (uint64_t)world * (k >> 8);
@@ -169,6 +175,7 @@ __global__ void k_shard_iota(uint64_t na, int rank, int world, uint32_t* __restr
 __global__ void k_gres_spec_init(unsigned long long* __restrict__ slots,
                                  unsigned long long* __restrict__ table, uint64_t ntab,
                                  int32_t* __restrict__ den, uint64_t S, uint32_t* __restrict__ act) {
+    pdl_wait();
     const uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (i0 == 0) {
         slots[S_FLAG] = 0;
@@ -186,6 +193,7 @@ __global__ void k_gres_spec_init(unsigned long long* __restrict__ slots,
 
 __global__ void k_fill_den(const uint32_t* __restrict__ act, uint64_t na, int value,
                            int32_t* __restrict__ den) {
+    pdl_wait();
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < na;
          i += (uint64_t)gridDim.x * blockDim.x)
         den[act[i]] = value;
@@ -216,6 +224,7 @@ __device__ __forceinline__ bool dom_w(W s, W t, W tg) {
 template <class W>
 __global__ void k_codes_all(const double* __restrict__ v, uint64_t S, int d, int g_max, int G,
                             W* __restrict__ codes) {
+    pdl_wait();
     const uint64_t total = S * (uint64_t)G;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
          i += (uint64_t)gridDim.x * blockDim.x) {
@@ -235,6 +244,7 @@ __global__ void __launch_bounds__(kBlock)
 k_gres_pairs_tiled(const W* __restrict__ codes, uint32_t S, int G, int g_max,
                    const uint32_t* __restrict__ act, uint32_t na, uint32_t range,
                    int32_t* __restrict__ den, unsigned long long* __restrict__ tests) {
+    pdl_wait();
     constexpr W H = (W)kGuard;
     __shared__ W tile[kTileCodes];
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -316,6 +326,7 @@ __global__ void __launch_bounds__(kBlock)
 k_gres_pairs_resident(const W* __restrict__ codes, uint32_t S, int G, int g_max,
                       const uint32_t* __restrict__ act, uint32_t na, uint32_t range,
                       int32_t* __restrict__ den, unsigned long long* __restrict__ tests) {
+    pdl_wait();
     constexpr W H = (W)kGuard;
     extern __shared__ __align__(16) unsigned char smraw[];
     const uint32_t r0 = blockIdx.y * range;
@@ -404,6 +415,7 @@ k_gres_pairs_resident(const W* __restrict__ codes, uint32_t S, int G, int g_max,
 
 __global__ void k_finalize_den(const uint32_t* __restrict__ act, uint64_t na,
                                int32_t* __restrict__ den) {
+    pdl_wait();
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < na;
          i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t t = act[i];
@@ -432,6 +444,7 @@ k_gres_pairs_f64(const double* __restrict__ q, uint32_t S, int d,
                  const int64_t* __restrict__ ids, const uint32_t* __restrict__ act,
                  uint32_t na, int g, int tiecheck, int32_t* __restrict__ den,
                  uint8_t* __restrict__ still, unsigned long long* __restrict__ tests) {
+    pdl_wait();
     constexpr int TILE = D > 0 ? 256 : 128;
     constexpr int DM = D > 0 ? D : kMaxDims;
     extern __shared__ double tile[];
@@ -508,6 +521,7 @@ static int intervals_from_gap(double gap, int cap) {
 __global__ void k_gap_witness(const double* __restrict__ v, uint64_t S, int d, int cap,
                               unsigned long long* __restrict__ table,
                               unsigned long long* __restrict__ slots) {
+    pdl_wait();
     const int nb = 2 * cap;
     unsigned long long mx = 0;
     bool found = false;
@@ -551,6 +565,7 @@ constexpr int kWitnessSmemCap = 2048;
 __global__ void __launch_bounds__(256)
     k_gap_witness_smem(const double* __restrict__ v, uint64_t S, int cap,
                        unsigned long long* __restrict__ slots) {
+    pdl_wait();
     __shared__ unsigned long long tab[2 * kWitnessSmemCap];
     __shared__ int any;
     const int nb = 2 * cap;
@@ -594,10 +609,10 @@ void launch_gap_witness(Ctx& c, const double* d_soa, uint64_t S, int d, int cap,
         const uint64_t want = (S + 4095) / 4096;
         const unsigned bx = (unsigned)std::max<uint64_t>(
             1, std::min<uint64_t>(want, (uint64_t)c.num_sms * 8 / (uint64_t)d + 1));
-        k_gap_witness_smem<<<dim3(bx, (unsigned)d), 256, 0, c.stream>>>(d_soa, S, cap, c.d_slots);
+        pdl_launch(k_gap_witness_smem, dim3(bx, (unsigned)d), 256, 0, c.stream, d_soa, S, cap, c.d_slots);
     } else {
         SKY_CUDA(cudaMemsetAsync(table, 0, sizeof(unsigned long long) * d * 2 * cap, c.stream));
-        k_gap_witness<<<grid_for(S * d, kBlock), kBlock, 0, c.stream>>>(d_soa, S, d, cap, table,
+        pdl_launch(k_gap_witness, grid_for(S * d, kBlock), kBlock, 0, c.stream, d_soa, S, d, cap, table,
                                                                          c.d_slots);
     }
     SKY_LAUNCH_CHECK();
@@ -613,18 +628,18 @@ bool min_positive_gap_device(Ctx& c, const double* d_soa, uint64_t S, int d, dou
     double* srt = c.buf[B_GTMP1].as<double>(S);
     const unsigned gb = grid_for(S, kBlock);
     for (int j = 0; j < d; ++j) {
-        k_copy<<<gb, kBlock, 0, c.stream>>>(d_soa + (uint64_t)j * S, S, col);
+        pdl_launch(k_copy, gb, kBlock, 0, c.stream, d_soa + (uint64_t)j * S, S, col);
         SKY_LAUNCH_CHECK();
         size_t tmp = 0;
         SKY_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, col, srt, (int64_t)S, 0, 64,
                                                  c.stream));
         void* t = c.buf[B_CUB].get(tmp);
         SKY_CUDA(cub::DeviceRadixSort::SortKeys(t, tmp, col, srt, (int64_t)S, 0, 64, c.stream));
-        k_min_gap<<<gb, kBlock, 0, c.stream>>>(srt, S, c.d_slots);
+        pdl_launch(k_min_gap, gb, kBlock, 0, c.stream, srt, S, c.d_slots);
         SKY_LAUNCH_CHECK();
         note_launch(c, 6);
     }
-    k_max_value<<<grid_for(S * d, kBlock), kBlock, 0, c.stream>>>(d_soa, S * d, c.d_slots);
+    pdl_launch(k_max_value, grid_for(S * d, kBlock), kBlock, 0, c.stream, d_soa, S * d, c.d_slots);
     SKY_LAUNCH_CHECK();
     note_launch(c);
     read_slots(c, S_MINGAP, 2);
@@ -690,7 +705,7 @@ GresOut gres_device(Ctx& c, const double* d_skyv, const int64_t* d_ids, uint64_t
         unsigned long long* table = c.buf[B_CELLS].as<unsigned long long>(ntab);
         uint32_t* act = c.buf[B_ACT0].as<uint32_t>(S);
         trace_mark(c, "gres: start (speculative)");
-        k_gres_spec_init<<<grid_for(S > ntab ? S : ntab, kBlock), kBlock, 0, c.stream>>>(
+        pdl_launch(k_gres_spec_init, grid_for(S > ntab ? S : ntab, kBlock), kBlock, 0, c.stream, 
             c.d_slots, table, ntab, d_den, S, act);
         SKY_LAUNCH_CHECK();
         note_launch(c);
@@ -700,7 +715,7 @@ GresOut gres_device(Ctx& c, const double* d_skyv, const int64_t* d_ids, uint64_t
         if (gres_cells_smem_spec(c, d_skyv, S, d, cap, act, S, d_den)) {
             SKY_CUDA(cudaEventRecord(e1, c.stream));
             trace_mark(c, "gres: shared-memory cell kernel");
-            k_finalize_den<<<grid_for(S, kBlock), kBlock, 0, c.stream>>>(act, S, d_den);
+            pdl_launch(k_finalize_den, grid_for(S, kBlock), kBlock, 0, c.stream, act, S, d_den);
             SKY_LAUNCH_CHECK();
             note_launch(c);
             c.gres_timing_pending = true;
@@ -722,7 +737,7 @@ GresOut gres_device(Ctx& c, const double* d_skyv, const int64_t* d_ids, uint64_t
         dispatch_d(d, [&](auto DC) {
             constexpr int D = decltype(DC)::value;
             const size_t smem = sizeof(double) * (D > 0 ? 256 : 128) * (D > 0 ? D : d);
-            k_check_skyline<D><<<grid_for(S, kBlock, 1 << 30), kBlock, smem, c.stream>>>(
+            pdl_launch(k_check_skyline<D>, grid_for(S, kBlock, 1 << 30), kBlock, smem, c.stream, 
                 d_skyv, S, d, c.d_slots);
         });
         SKY_LAUNCH_CHECK();
@@ -754,7 +769,7 @@ GresOut gres_device(Ctx& c, const double* d_skyv, const int64_t* d_ids, uint64_t
     uint64_t na = 0;  // owned tuples: interleaved 256-tuple chunks (load balance)
     for (uint64_t ch = shard_rank; ch * 256 < S; ch += shard_world)
         na += std::min<uint64_t>(256, S - ch * 256);
-    k_shard_iota<<<grid_for(na ? na : 1, kBlock), kBlock, 0, c.stream>>>(na, shard_rank,
+    pdl_launch(k_shard_iota, grid_for(na ? na : 1, kBlock), kBlock, 0, c.stream, na, shard_rank,
                                                                            shard_world, act);
     SKY_LAUNCH_CHECK();
     note_launch(c);
@@ -784,7 +799,7 @@ GresOut gres_device(Ctx& c, const double* d_skyv, const int64_t* d_ids, uint64_t
         if (gres_cells_smem_device(c, d_skyv, S, d, out.g_max, maxv, act, na, d_den)) {
             SKY_CUDA(cudaEventRecord(e1, c.stream));
             trace_mark(c, "gres: shared-memory cell kernel");
-            k_finalize_den<<<grid_for(na, kBlock), kBlock, 0, c.stream>>>(act, na, d_den);
+            pdl_launch(k_finalize_den, grid_for(na, kBlock), kBlock, 0, c.stream, act, na, d_den);
             SKY_LAUNCH_CHECK();
             note_launch(c);
             c.gres_timing_pending = true;
@@ -802,7 +817,7 @@ GresOut gres_device(Ctx& c, const double* d_skyv, const int64_t* d_ids, uint64_t
         SKY_CUDA(cudaEventRecord(e0, c.stream));
         if (gres_cells_device(c, d_skyv, S, d, out.g_max, act, na, d_den, &swept, &steps_run)) {
             SKY_CUDA(cudaEventRecord(e1, c.stream));
-            k_finalize_den<<<grid_for(na, kBlock), kBlock, 0, c.stream>>>(act, na, d_den);
+            pdl_launch(k_finalize_den, grid_for(na, kBlock), kBlock, 0, c.stream, act, na, d_den);
             SKY_LAUNCH_CHECK();
             note_launch(c);
             c.gres_timing_pending = true;
@@ -821,10 +836,10 @@ GresOut gres_device(Ctx& c, const double* d_skyv, const int64_t* d_ids, uint64_t
         void* codes = c.buf[B_CODES].get(S * (uint64_t)G * (w32 ? 4 : 8));
         const unsigned cgrid = grid_for(S * (uint64_t)G, kBlock);
         if (w32)
-            k_codes_all<uint32_t><<<cgrid, kBlock, 0, c.stream>>>(d_skyv, S, d, out.g_max, G,
+            pdl_launch(k_codes_all<uint32_t>, cgrid, kBlock, 0, c.stream, d_skyv, S, d, out.g_max, G,
                                                                   (uint32_t*)codes);
         else
-            k_codes_all<unsigned long long><<<cgrid, kBlock, 0, c.stream>>>(
+            pdl_launch(k_codes_all<unsigned long long>, cgrid, kBlock, 0, c.stream, 
                 d_skyv, S, d, out.g_max, G, (unsigned long long*)codes);
         SKY_LAUNCH_CHECK();
         const bool resident = S <= (1u << 21) && !getenv("SKYGPU_GRES_TILED");
@@ -847,13 +862,13 @@ GresOut gres_device(Ctx& c, const double* d_skyv, const int64_t* d_ids, uint64_t
             if (w32) {
                 SKY_CUDA(cudaFuncSetAttribute(k_gres_pairs_resident<uint32_t>,
                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-                k_gres_pairs_resident<uint32_t><<<grid, kBlock, smem, c.stream>>>(
+                pdl_launch(k_gres_pairs_resident<uint32_t>, grid, kBlock, smem, c.stream, 
                     (const uint32_t*)codes, (uint32_t)S, G, out.g_max, act, (uint32_t)na,
                     (uint32_t)range, d_den, c.d_slots + S_TESTS_GRES);
             } else {
                 SKY_CUDA(cudaFuncSetAttribute(k_gres_pairs_resident<unsigned long long>,
                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-                k_gres_pairs_resident<unsigned long long><<<grid, kBlock, smem, c.stream>>>(
+                pdl_launch(k_gres_pairs_resident<unsigned long long>, grid, kBlock, smem, c.stream, 
                     (const unsigned long long*)codes, (uint32_t)S, G, out.g_max, act, (uint32_t)na,
                     (uint32_t)range, d_den, c.d_slots + S_TESTS_GRES);
             }
@@ -873,18 +888,18 @@ GresOut gres_device(Ctx& c, const double* d_skyv, const int64_t* d_ids, uint64_t
             dim3 grid((unsigned)cand_tiles, (unsigned)ranges);
             SKY_CUDA(cudaEventRecord(e0, c.stream));
             if (w32)
-                k_gres_pairs_tiled<uint32_t><<<grid, kBlock, 0, c.stream>>>(
+                pdl_launch(k_gres_pairs_tiled<uint32_t>, grid, kBlock, 0, c.stream, 
                     (const uint32_t*)codes, (uint32_t)S, G, out.g_max, act, (uint32_t)na,
                     (uint32_t)range, d_den, c.d_slots + S_TESTS_GRES);
             else
-                k_gres_pairs_tiled<unsigned long long><<<grid, kBlock, 0, c.stream>>>(
+                pdl_launch(k_gres_pairs_tiled<unsigned long long>, grid, kBlock, 0, c.stream, 
                     (const unsigned long long*)codes, (uint32_t)S, G, out.g_max, act, (uint32_t)na,
                     (uint32_t)range, d_den, c.d_slots + S_TESTS_GRES);
         }
         SKY_CUDA(cudaEventRecord(e1, c.stream));
         SKY_LAUNCH_CHECK();
         trace_mark(c, "gres: tiled pair kernel");
-        k_finalize_den<<<grid_for(na, kBlock), kBlock, 0, c.stream>>>(act, na, d_den);
+        pdl_launch(k_finalize_den, grid_for(na, kBlock), kBlock, 0, c.stream, act, na, d_den);
         SKY_LAUNCH_CHECK();
         note_launch(c, 3);
         c.gres_timing_pending = true;  // resolved after the call's final sync
@@ -898,13 +913,13 @@ GresOut gres_device(Ctx& c, const double* d_skyv, const int64_t* d_ids, uint64_t
     double* q = c.buf[B_PROJ].as<double>(S * d);
     for (int g = out.g_max; g >= 2 && na > 0; --g) {
         ++steps;
-        k_project<<<grid_for(S * d, kBlock), kBlock, 0, c.stream>>>(d_skyv, S * d, g, q);
+        pdl_launch(k_project, grid_for(S * d, kBlock), kBlock, 0, c.stream, d_skyv, S * d, g, q);
         SKY_LAUNCH_CHECK();
         dispatch_d(d, [&](auto DC) {
             constexpr int D = decltype(DC)::value;
             const size_t smem = sizeof(double) * (D > 0 ? 256 : 128) * (D > 0 ? D : d);
             SKY_CUDA(cudaEventRecord(e0, c.stream));
-            k_gres_pairs_f64<D><<<grid_for(na, kBlock, 1 << 30), kBlock, smem, c.stream>>>(
+            pdl_launch(k_gres_pairs_f64<D>, grid_for(na, kBlock, 1 << 30), kBlock, smem, c.stream, 
                 q, (uint32_t)S, d, d_ids, act, (uint32_t)na, g, ties_possible ? 1 : 0, d_den,
                 still, c.d_slots + S_TESTS_GRES);
             SKY_CUDA(cudaEventRecord(e1, c.stream));
@@ -919,7 +934,7 @@ GresOut gres_device(Ctx& c, const double* d_skyv, const int64_t* d_ids, uint64_t
         ++klaunch;
     }
     if (na > 0) {
-        k_fill_den<<<grid_for(na, kBlock), kBlock, 0, c.stream>>>(act, na, 1, d_den);
+        pdl_launch(k_fill_den, grid_for(na, kBlock), kBlock, 0, c.stream, act, na, 1, d_den);
         SKY_LAUNCH_CHECK();
         note_launch(c);
     }
@@ -940,6 +955,7 @@ namespace {
 // order, at the first step g = g_max.
 __global__ void k_grid_projection_range(const double* __restrict__ v, uint64_t S, int d, int g,
                                         unsigned long long* __restrict__ slots) {
+    pdl_wait();
     const double gd = (double)g;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < S * d;
          i += (uint64_t)gridDim.x * blockDim.x) {
@@ -952,7 +968,7 @@ __global__ void k_grid_projection_range(const double* __restrict__ v, uint64_t S
 
 void check_grid_projection(Ctx& c, const double* d_skyv, uint64_t S, int d, int g) {
     zero_slots(c);
-    k_grid_projection_range<<<grid_for(S * d, 256), 256, 0, c.stream>>>(d_skyv, S, d, g,
+    pdl_launch(k_grid_projection_range, grid_for(S * d, 256), 256, 0, c.stream, d_skyv, S, d, g,
                                                                          c.d_slots);
     SKY_LAUNCH_CHECK();
     note_launch(c);

@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "skygpu.h"
@@ -35,6 +36,37 @@ struct Error : std::runtime_error {
     } while (0)
 
 #define SKY_LAUNCH_CHECK() SKY_CUDA(cudaGetLastError())
+
+// Programmatic dependent launch: every kernel of the library starts with
+// pdl_wait() (griddepcontrol.wait: a no-op for a normally launched grid; for a
+// PDL-launched one it waits until the preceding grid's memory is visible), so
+// each launch may let the next grid be scheduled early — the kernel-to-kernel
+// bubble of a ~30-launch call shrinks.  SKYGPU_PDL=0 launches normally.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+inline bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("SKYGPU_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+template <typename... KArgs, typename... Args>
+inline void pdl_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t stream, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    SKY_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
 
 inline void invalid(const std::string& m) { throw Error(SKYGPU_EINVAL, m); }
 

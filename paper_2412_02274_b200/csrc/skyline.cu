@@ -86,6 +86,7 @@ __global__ void k_score(const double* __restrict__ v, uint64_t n, int d,
                         unsigned long long* __restrict__ slots,
                         unsigned long long* __restrict__ amax, uint64_t base = 0,
                         const int64_t* __restrict__ ids = nullptr) {
+    pdl_wait();
     constexpr int DA = D > 0 ? D : 1;
     unsigned long long mn = ~0ULL, mx = 0;
     unsigned long long am[DA];
@@ -208,6 +209,7 @@ __global__ void k_gather_q(const double* __restrict__ v, const uint32_t* __restr
                            uint64_t cap, const unsigned long long* __restrict__ count,
                            const unsigned long long* __restrict__ amax, double* __restrict__ out,
                            unsigned long long* __restrict__ qout) {
+    pdl_wait();
     const uint64_t mm = count ? *count : cap;
     if (mm > cap) return;  // (a speculative count above the capacity: no-op)
     double sc[D];
@@ -230,6 +232,7 @@ __global__ void k_gather_q(const double* __restrict__ v, const uint32_t* __restr
 
 __global__ void k_ids_check(const int64_t* __restrict__ ids, uint64_t n,
                             unsigned long long* __restrict__ slots, int slot = S_FLAG) {
+    pdl_wait();
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i + 1 < n;
          i += (uint64_t)gridDim.x * blockDim.x)
         if (ids[i] >= ids[i + 1]) atomicOr(&slots[slot], 1ULL);
@@ -239,6 +242,7 @@ __global__ void k_ids_check(const int64_t* __restrict__ ids, uint64_t n,
 // the first offending (tuple, attribute) in input order is reported.
 __global__ void k_grid_range(const double* __restrict__ v, uint64_t total,
                              unsigned long long* __restrict__ slots) {
+    pdl_wait();
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
          i += (uint64_t)gridDim.x * blockDim.x) {
         double x = v[i];
@@ -255,6 +259,7 @@ constexpr int kSampleItems = 4;
 __global__ void __launch_bounds__(1024)
 k_sample_threshold(const unsigned long long* __restrict__ key, const uint32_t* __restrict__ R,
                    uint64_t r, uint64_t want, unsigned long long* __restrict__ slots) {
+    pdl_wait();
     // An approximate quantile suffices (T is exact once chosen): the samples
     // are bucketed linearly between their min and max sum and the bucket
     // holding the q-th sample gives T — one histogram, no sort.
@@ -423,6 +428,7 @@ __device__ __forceinline__ uint32_t qgrid_cell(const double* t, int dd, int k) {
 __global__ void __launch_bounds__(1024)
 k_qgrid_bounds(const double* __restrict__ v, int d, const uint32_t* __restrict__ list,
                const unsigned long long* __restrict__ count, int k, double* __restrict__ bounds) {
+    pdl_wait();
     using Sort = cub::BlockRadixSort<unsigned long long, 1024, 4>;
     __shared__ typename Sort::TempStorage tmp;
     const int j = blockIdx.x;
@@ -468,6 +474,7 @@ __device__ __forceinline__ uint32_t plan_cell(const double* t, int dd, int spec,
 // c - (1,..,1) is set.
 __global__ void k_grid_occ(const double* __restrict__ v, uint64_t n, int d, int m,
                            uint8_t* __restrict__ occ) {
+    pdl_wait();
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x)
         occ[grid_cell_id<kMaxDims>(v + i * d, d, m)] = 1;
@@ -475,6 +482,7 @@ __global__ void k_grid_occ(const double* __restrict__ v, uint64_t n, int d, int 
 
 __global__ void k_prefix_or_dim(uint8_t* __restrict__ occ, uint32_t ncells, int m,
                                 uint32_t stride) {
+    pdl_wait();
     const uint32_t lines = ncells / m;
     for (uint32_t l = blockIdx.x * blockDim.x + threadIdx.x; l < lines; l += gridDim.x * blockDim.x) {
         const uint32_t lo = l % stride, hi = l / stride;
@@ -489,6 +497,7 @@ __global__ void k_prefix_or_dim(uint8_t* __restrict__ occ, uint32_t ncells, int 
 
 __global__ void k_grid_keep(const double* __restrict__ v, uint64_t n, int d, int m,
                             const uint8_t* __restrict__ P, uint8_t* __restrict__ keep) {
+    pdl_wait();
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x) {
         const double* t = v + i * d;
@@ -513,6 +522,7 @@ k_cell_order(const double* __restrict__ v, int d, const uint32_t* __restrict__ i
              const unsigned long long* __restrict__ count, int mcell, uint32_t ncells, const unsigned long long* __restrict__ amax,
              uint32_t* __restrict__ out, uint32_t* __restrict__ out_cell,
              uint32_t* __restrict__ seg) {
+    pdl_wait();
     constexpr int DM = D > 0 ? D : kMaxDims;
     const int dd = D > 0 ? D : d;
     const uint32_t m = count ? (uint32_t)*count : mcap;
@@ -557,6 +567,7 @@ k_cell_order(const double* __restrict__ v, int d, const uint32_t* __restrict__ i
 __global__ void k_gather_aos(const double* __restrict__ v, int d, const uint32_t* __restrict__ list,
                              uint64_t cap, const unsigned long long* __restrict__ count,
                              double* __restrict__ out) {
+    pdl_wait();
     const uint64_t mm = count ? *count : cap;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < mm * d;
          i += (uint64_t)gridDim.x * blockDim.x) {
@@ -573,6 +584,7 @@ __global__ void k_rep_filter(const double* __restrict__ v, uint64_t n, int d,
                              const double* __restrict__ reps, uint32_t n_reps,
                              uint8_t* __restrict__ keep, unsigned long long* __restrict__ tests,
                              int and_mode) {
+    pdl_wait();
     constexpr int DM = D > 0 ? D : kMaxDims;
     const int dd = D > 0 ? D : d;
     unsigned long long cnt = 0;
@@ -650,6 +662,7 @@ k_bucket_order(const uint32_t* __restrict__ in, uint32_t m, const unsigned long 
                unsigned long long kmin, int shift, uint32_t* __restrict__ out,
                uint32_t* __restrict__ bstart, const unsigned long long* __restrict__ mdev,
                const unsigned long long* __restrict__ pslots = nullptr, int use_thr = 1) {
+    pdl_wait();
     if (!dev_count(mdev, m)) return;
     if (pslots) bucket_params_dev(pslots, use_thr, kmin, shift);
     __shared__ uint32_t cnt[kKeyBuckets];
@@ -684,6 +697,7 @@ __global__ void k_bucket_rank(const uint32_t* __restrict__ in, uint32_t m,
                               const unsigned long long* __restrict__ mdev,
                               const unsigned long long* __restrict__ pslots = nullptr,
                               int use_thr = 1) {
+    pdl_wait();
     if (!dev_count(mdev, m)) return;
     if (pslots) bucket_params_dev(pslots, use_thr, kmin, shift);
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
@@ -711,6 +725,7 @@ template <int D>
 __global__ void __launch_bounds__(kBlock)
 k_sfs_intra_sorted(const double* __restrict__ Av, uint32_t m, int d, uint8_t* __restrict__ keep,
                    unsigned long long* __restrict__ tests) {
+    pdl_wait();
     constexpr int DM = D > 0 ? D : kMaxDims;
     const int dd = D > 0 ? D : d;
     const uint32_t lane = threadIdx.x & 31;
@@ -757,6 +772,7 @@ k_sfs_filter_cells(const double* __restrict__ v, int d, const unsigned long long
                    uint32_t pcap, const uint32_t* __restrict__ seg, int m,
                    const unsigned long long* __restrict__ slots, uint8_t* __restrict__ keep,
                    unsigned long long* __restrict__ tests, uint32_t bs) {
+    pdl_wait();
     constexpr int DM = D > 0 ? D : kMaxDims;
     const int dd = D > 0 ? D : d;
     const uint32_t lane = threadIdx.x & 31;
@@ -819,6 +835,7 @@ template <int D>
 __global__ void __launch_bounds__(kBlock)
 k_sfs_intra_q(const double* __restrict__ Av, const unsigned long long* __restrict__ Aq,
               uint32_t m, uint8_t* __restrict__ keep, unsigned long long* __restrict__ tests) {
+    pdl_wait();
     constexpr int W = QW<D>::W;
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -871,6 +888,7 @@ __global__ void __launch_bounds__(kBlock)
 k_sfs_intra_chunked(const double* __restrict__ Av, const unsigned long long* __restrict__ Aq,
                     uint32_t m, volatile uint8_t* keep, unsigned long long* __restrict__ tests,
                     uint32_t astride, const unsigned long long* __restrict__ mdev) {
+    pdl_wait();
     if (!dev_count(mdev, m)) return;
     constexpr int W = QW<D>::W;
     const uint32_t lane = threadIdx.x & 31;
@@ -940,6 +958,7 @@ __global__ void __launch_bounds__(1024, 1)
 k_sfs_intra_smem(const double* __restrict__ Av, const unsigned long long* __restrict__ Aq,
                  uint32_t m, uint8_t* __restrict__ keep, unsigned long long* __restrict__ tests,
                  uint32_t astride, const unsigned long long* __restrict__ mdev) {
+    pdl_wait();
     static_assert(QW<D>::W == 1, "one code word per tuple");
     if (!dev_count(mdev, m)) return;
     extern __shared__ unsigned long long sq[];
@@ -1016,6 +1035,7 @@ k_sfs_filter_q(const double* __restrict__ v, const unsigned long long* __restric
                unsigned long long* __restrict__ tests, uint32_t bs,
                const uint32_t* __restrict__ Ppos, const int64_t* __restrict__ ids,
                uint32_t kSolo) {
+    pdl_wait();
     // Ppos != nullptr: A' is a seed that need not precede every candidate
     // (host-overlapped first part, skygpu_pipeline); a dominating comparator
     // then also has to precede the candidate in (sum, id, position) order
@@ -1180,6 +1200,7 @@ k_cta_select(const uint32_t* __restrict__ in, const uint32_t* __restrict__ in_ce
              uint32_t* __restrict__ out_cell, unsigned long long* __restrict__ count,
              const unsigned long long* __restrict__ mdev = nullptr,
              const unsigned long long* __restrict__ out_off = nullptr) {
+    pdl_wait();
     if (!dev_count(mdev, m)) return;
     if (out_off) out += *out_off;
     using Scan = cub::BlockScan<uint32_t, 1024>;
@@ -1209,6 +1230,7 @@ k_cta_select(const uint32_t* __restrict__ in, const uint32_t* __restrict__ in_ce
 __global__ void k_keys_of(const unsigned long long* __restrict__ key,
                           const uint32_t* __restrict__ list, uint64_t m,
                           unsigned long long* __restrict__ out) {
+    pdl_wait();
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
          i += (uint64_t)gridDim.x * blockDim.x)
         out[i] = key[list[i]];
@@ -1216,6 +1238,7 @@ __global__ void k_keys_of(const unsigned long long* __restrict__ key,
 
 __global__ void k_id_keys(const int64_t* __restrict__ ids, const uint32_t* __restrict__ list,
                           uint64_t m, unsigned long long* __restrict__ out) {
+    pdl_wait();
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
          i += (uint64_t)gridDim.x * blockDim.x)
         out[i] = static_cast<unsigned long long>(ids[list[i]]) ^ 0x8000000000000000ULL;
@@ -1225,6 +1248,7 @@ __global__ void k_emit_skyline(const uint32_t* __restrict__ K, uint64_t S,
                                const double* __restrict__ v, int d,
                                const int64_t* __restrict__ ids, int64_t* __restrict__ oid,
                                double* __restrict__ skyv) {
+    pdl_wait();
     for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < S;
          k += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t p = K[k];
@@ -1366,17 +1390,20 @@ int cells_per_dim(uint64_t m, int d, uint32_t* ncells) {
 namespace {
 // first-round engine gate: most of the prefix survived -> rank-grid engine
 __global__ void k_grid_gate(unsigned long long* slots, uint64_t m) {
+    pdl_wait();
     if (m == 0) m = slots[S_C1];  // (a device-sized round: the prefix count)
     if (threadIdx.x == 0) slots[S_GATE] = slots[S_C2] * 4 > m * 3 ? 1ULL : 0ULL;
 }
 // streamed input: seeded K5 state (no decided prefix, |A'| = the seed)
 __global__ void k_seed_slots(unsigned long long* slots, uint64_t nseed) {
+    pdl_wait();
     if (threadIdx.x == 0) {
         slots[S_THR] = 0;
         slots[S_C2] = nseed;
     }
 }
 __global__ void k_iota(uint32_t* __restrict__ a, uint64_t n) {
+    pdl_wait();
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x)
         a[i] = (uint32_t)i;
@@ -1438,7 +1465,7 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
         if (!ids_late || ids_waited || (sky_engine & kSkyFirstPrefix)) return;
         ids_waited = true;
         SKY_CUDA(cudaStreamWaitEvent(c.stream, c.ids_ready, 0));
-        k_ids_check<<<grid_for(n, kBlock), kBlock, 0, c.stream>>>(d_ids, n, c.d_slots, S_IDSBAD);
+        pdl_launch(k_ids_check, grid_for(n, kBlock), kBlock, 0, c.stream, d_ids, n, c.d_slots, S_IDSBAD);
         SKY_LAUNCH_CHECK();
         note_launch(c);
     };
@@ -1453,14 +1480,14 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
     if (!feed) {  // (streamed input: per chunk, below)
         dispatch_d(d, [&](auto DC) {
             constexpr int D = decltype(DC)::value;
-            k_score<D><<<grid_for(n, kBlock, c.num_sms * 8), kBlock, 0, c.stream>>>(
+            pdl_launch(k_score<D>, grid_for(n, kBlock, c.num_sms * 8), kBlock, 0, c.stream, 
                 d_vals, n, d, keys, c.d_slots, amax, 0, tie_ids);  // + ids sortedness
         });
         SKY_LAUNCH_CHECK();
         note_launch(c, 1);
     }
     if (plan.strategy == SKYGPU_GRID) {
-        k_grid_range<<<grid_for(n * d, kBlock), kBlock, 0, c.stream>>>(d_vals, n * d, c.d_slots);
+        pdl_launch(k_grid_range, grid_for(n * d, kBlock), kBlock, 0, c.stream, d_vals, n * d, c.d_slots);
         SKY_LAUNCH_CHECK();
         note_launch(c);
     }
@@ -1486,22 +1513,22 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
             const int m = plan.slices;
             uint8_t* occ = c.buf[B_CELLS].as<uint8_t>(grid_cells);
             SKY_CUDA(cudaMemsetAsync(occ, 0, grid_cells, c.stream));
-            k_grid_occ<<<gb, kBlock, 0, c.stream>>>(d_vals, n, d, m, occ);
+            pdl_launch(k_grid_occ, gb, kBlock, 0, c.stream, d_vals, n, d, m, occ);
             SKY_LAUNCH_CHECK();
             uint32_t stride = 1;
             for (int k = 0; k < d; ++k, stride *= (uint32_t)m) {
-                k_prefix_or_dim<<<grid_for(grid_cells / m, kBlock), kBlock, 0, c.stream>>>(
+                pdl_launch(k_prefix_or_dim, grid_for(grid_cells / m, kBlock), kBlock, 0, c.stream, 
                     occ, (uint32_t)grid_cells, m, stride);
                 SKY_LAUNCH_CHECK();
             }
-            k_grid_keep<<<gb, kBlock, 0, c.stream>>>(d_vals, n, d, m, occ, pre);
+            pdl_launch(k_grid_keep, gb, kBlock, 0, c.stream, d_vals, n, d, m, occ, pre);
             SKY_LAUNCH_CHECK();
             note_launch(c, 2 + d);
         }
         if (n_reps > 0) {
             dispatch_d(d, [&](auto DC) {
                 constexpr int D = decltype(DC)::value;
-                k_rep_filter<D><<<gb, kBlock, 0, c.stream>>>(d_vals, n, d, d_reps,
+                pdl_launch(k_rep_filter<D>, gb, kBlock, 0, c.stream, d_vals, n, d, d_reps,
                                                               (uint32_t)n_reps, pre,
                                                               c.d_slots + S_TESTS_SKY,
                                                               grid_cells ? 1 : 0);
@@ -1547,18 +1574,18 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
         unsigned long long* Pkey2 = c.buf[B_GTMP0].as<unsigned long long>(m);
         unsigned long long* kcur;
         if (ids_sorted) {
-            k_keys_of<<<grid_for(m, kBlock), kBlock, 0, c.stream>>>(keys, Pfull, m, Pkey);
+            pdl_launch(k_keys_of, grid_for(m, kBlock), kBlock, 0, c.stream, keys, Pfull, m, Pkey);
             SKY_LAUNCH_CHECK();
             sort_pairs<unsigned long long>(c, Pkey, Pkey2, Pfull, Ps, m, 64, &kcur, &order);
         } else {  // stable LSD: by id first, then by sum
             unsigned long long* ik0 = c.buf[B_GTMP1].as<unsigned long long>(m);
-            k_id_keys<<<grid_for(m, kBlock), kBlock, 0, c.stream>>>(d_ids, Pfull, m, ik0);
+            pdl_launch(k_id_keys, grid_for(m, kBlock), kBlock, 0, c.stream, d_ids, Pfull, m, ik0);
             SKY_LAUNCH_CHECK();
             unsigned long long* ikc;
             uint32_t* by_id;
             sort_pairs<unsigned long long>(c, ik0, Pkey2, Pfull, Ps, m, 64, &ikc, &by_id);
             uint32_t* other = by_id == Pfull ? Ps : Pfull;
-            k_keys_of<<<grid_for(m, kBlock), kBlock, 0, c.stream>>>(keys, by_id, m, Pkey);
+            pdl_launch(k_keys_of, grid_for(m, kBlock), kBlock, 0, c.stream, keys, by_id, m, Pkey);
             SKY_LAUNCH_CHECK();
             sort_pairs<unsigned long long>(c, Pkey, Pkey2, by_id, other, m, 64, &kcur, &order);
         }
@@ -1653,10 +1680,10 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
                 // parameters from the slots; a final round has no threshold)
                 const unsigned long long* ps = mdev ? c.d_slots : nullptr;
                 const int use_thr = final_round ? 0 : 1;
-                k_bucket_order<<<1, 1024, 0, c.stream>>>(Pfull, (uint32_t)m, keys, gmin, shift, Pb,
+                pdl_launch(k_bucket_order, 1, 1024, 0, c.stream, Pfull, (uint32_t)m, keys, gmin, shift, Pb,
                                                          bst, mdev, ps, use_thr);
                 SKY_LAUNCH_CHECK();
-                k_bucket_rank<<<grid_for(m, kBlock), kBlock, 0, c.stream>>>(Pb, (uint32_t)m, keys,
+                pdl_launch(k_bucket_rank, grid_for(m, kBlock), kBlock, 0, c.stream, Pb, (uint32_t)m, keys,
                                                                              tie_ids, gmin, shift, bst,
                                                                              Ps, mdev, ps, use_thr);
                 SKY_LAUNCH_CHECK();
@@ -1669,10 +1696,10 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
             dispatch_d(d, [&](auto DC) {
                 constexpr int D = decltype(DC)::value;
                 if constexpr (D > 0)
-                    k_gather_q<D><<<grid_for(m, kBlock), kBlock, 0, c.stream>>>(
+                    pdl_launch(k_gather_q<D>, grid_for(m, kBlock), kBlock, 0, c.stream, 
                         d_vals, order, m, mdev, amax, Av, Aq);
                 else
-                    k_gather_aos<<<grid_for(m * d, kBlock), kBlock, 0, c.stream>>>(
+                    pdl_launch(k_gather_aos, grid_for(m * d, kBlock), kBlock, 0, c.stream, 
                         d_vals, d, order, m, nullptr, Av);
             });
             SKY_LAUNCH_CHECK();
@@ -1699,8 +1726,7 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
                                 (int)(kIntraSmemMax * sizeof(unsigned long long))));
                             attr = true;
                         }
-                        k_sfs_intra_smem<D><<<c.num_sms, 1024, m * sizeof(unsigned long long),
-                                              c.stream>>>(Av, Aq, (uint32_t)m, keep,
+                        pdl_launch(k_sfs_intra_smem<D>, c.num_sms, 1024, m * sizeof(unsigned long long), c.stream, Av, Aq, (uint32_t)m, keep,
                                                           c.d_slots + S_TESTS_SKY, (uint32_t)m,
                                                           mdev);
                         return;
@@ -1708,13 +1734,13 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
                 }
                 if constexpr (D > 0) {
                     if (intra_chunked)
-                        k_sfs_intra_chunked<D><<<c.num_sms * 8, kBlock, 0, c.stream>>>(
+                        pdl_launch(k_sfs_intra_chunked<D>, c.num_sms * 8, kBlock, 0, c.stream, 
                             Av, Aq, (uint32_t)m, keep, c.d_slots + S_TESTS_SKY, (uint32_t)m, mdev);
                     else
-                        k_sfs_intra_q<D><<<grid, kBlock, 0, c.stream>>>(Av, Aq, (uint32_t)m, keep,
+                        pdl_launch(k_sfs_intra_q<D>, grid, kBlock, 0, c.stream, Av, Aq, (uint32_t)m, keep,
                                                                         c.d_slots + S_TESTS_SKY);
                 } else
-                    k_sfs_intra_sorted<D><<<grid, kBlock, 0, c.stream>>>(
+                    pdl_launch(k_sfs_intra_sorted<D>, grid, kBlock, 0, c.stream, 
                         Av, (uint32_t)m, d, keep, c.d_slots + S_TESTS_SKY);
             });
             SKY_CUDA(cudaEventRecord(k1, c.stream));
@@ -1723,7 +1749,7 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
             trace_mark(c, "sky: K4 intra kernel");
             // A' in (sum, id) order appended to K; its count lands in S_C2
             if (mdev) {  // final: count in S_SEL2, after the round's A' (S_C2)
-                k_cta_select<<<1, 1024, 0, c.stream>>>(
+                pdl_launch(k_cta_select, 1, 1024, 0, c.stream, 
                     order, nullptr, keep, (uint32_t)m, K + kc, nullptr,
                     c.d_slots + (final_round ? S_SEL2 : S_C2), mdev,
                     final_round ? c.d_slots + S_C2 : nullptr);
@@ -1732,8 +1758,8 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
                 return false;
             }
             if (m <= kCTACap) {
-                k_cta_select<<<1, 1024, 0, c.stream>>>(order, nullptr, keep, (uint32_t)m, K + kc,
-                                                       nullptr, c.d_slots + S_C2);
+                pdl_launch(k_cta_select, 1, 1024, 0, c.stream, order, nullptr, keep, (uint32_t)m, K + kc,
+                           nullptr, c.d_slots + S_C2, nullptr, nullptr);
                 SKY_LAUNCH_CHECK();
                 note_launch(c);
             } else {
@@ -1792,7 +1818,7 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
                 for (int j = 0; j < d; ++j) ncells *= (uint32_t)k;
                 mcell = (kCellQuantile << 16) | k;
                 double* bounds = c.buf[B_PROJ].as<double>(kMaxDims * kQMaxBins);
-                k_qgrid_bounds<<<d, 1024, 0, c.stream>>>(d_vals, d, alist, c.d_slots + S_C2, k,
+                pdl_launch(k_qgrid_bounds, d, 1024, 0, c.stream, d_vals, d, alist, c.d_slots + S_C2, k,
                                                          bounds);
                 SKY_LAUNCH_CHECK();
                 SKY_CUDA(cudaMemcpyToSymbolAsync(c_qbounds, bounds,
@@ -1809,7 +1835,7 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
             uint32_t* Akey = c.buf[B_GTMP0].as<uint32_t>(m);
             dispatch_d(d, [&](auto DC) {
                 constexpr int D = decltype(DC)::value;
-                k_cell_order<D><<<1, 1024, 0, c.stream>>>(d_vals, d, alist, (uint32_t)m,
+                pdl_launch(k_cell_order<D>, 1, 1024, 0, c.stream, d_vals, d, alist, (uint32_t)m,
                                                           c.d_slots + S_C2, mcell, ncells,
                                                           qpre ? scale : nullptr, Alist, Akey,
                                                           seg_table);
@@ -1824,10 +1850,10 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
         dispatch_d(d, [&](auto DC) {
             constexpr int D = decltype(DC)::value;
             if constexpr (D > 0)
-                k_gather_q<D><<<grid_for(m, kBlock), kBlock, 0, c.stream>>>(
+                pdl_launch(k_gather_q<D>, grid_for(m, kBlock), kBlock, 0, c.stream, 
                     d_vals, psrc, m, c.d_slots + S_C2, scale, Pv, Pq);
             else
-                k_gather_aos<<<grid_for(m * d, kBlock), kBlock, 0, c.stream>>>(
+                pdl_launch(k_gather_aos, grid_for(m * d, kBlock), kBlock, 0, c.stream, 
                     d_vals, d, psrc, m, c.d_slots + S_C2, Pv);
         });
         SKY_LAUNCH_CHECK();
@@ -1856,12 +1882,12 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
             constexpr int D = decltype(DC)::value;
             const unsigned grid = (unsigned)((wf * 32 + kBlock - 1) / kBlock);
             if constexpr (D > 0)
-                k_sfs_filter_q<D><<<grid, kBlock, 0, c.stream>>>(
+                pdl_launch(k_sfs_filter_q<D>, grid, kBlock, 0, c.stream, 
                     d_vals, keys, Rl, (uint32_t)rl, A.Pv, A.Pq, (uint32_t)A.m, A.seg, A.mcell,
                     A.qk, scale, c.d_slots, fkeep, c.d_slots + S_TESTS_SKY, bsf,
                     seeded ? A.psrc : nullptr, tie_ids, solo);
             else
-                k_sfs_filter_cells<D><<<grid, kBlock, 0, c.stream>>>(
+                pdl_launch(k_sfs_filter_cells<D>, grid, kBlock, 0, c.stream, 
                     d_vals, d, keys, Rl, (uint32_t)rl, A.Pv, (uint32_t)A.m, A.seg, A.mcell,
                     c.d_slots, fkeep, c.d_slots + S_TESTS_SKY, bsf);
         });
@@ -1908,12 +1934,12 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
         // seeded K5 (precedence checked per hit: a dominating predecessor
         // rules a tuple out whether or not it is a skyline tuple itself).
         // Survivors (the seed included) form the undecided list of the rounds.
-        k_seed_slots<<<1, 32, 0, c.stream>>>(c.d_slots, nseed);
+        pdl_launch(k_seed_slots, 1, 32, 0, c.stream, c.d_slots, nseed);
         SKY_LAUNCH_CHECK();
         const AScan A = prep_aprime(seed, nseed, scale_snap);
         uint8_t* flags = c.buf[B_FLAGS].as<uint8_t>(n);
         uint32_t* iota = c.buf[B_IOTA].as<uint32_t>(n);
-        k_iota<<<grid_for(n, kBlock), kBlock, 0, c.stream>>>(iota, n);
+        pdl_launch(k_iota, grid_for(n, kBlock), kBlock, 0, c.stream, iota, n);
         SKY_LAUNCH_CHECK();
         note_launch(c, 1);
         for (int ch = 0; ch < feed->nchunks; ++ch) {
@@ -1921,13 +1947,13 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
             if (ch > 0) SKY_CUDA(cudaStreamWaitEvent(c.stream, feed->ready[ch], 0));
             dispatch_d(d, [&](auto DC) {
                 constexpr int D = decltype(DC)::value;
-                k_score<D><<<grid_for(hi - lo, kBlock, c.num_sms * 8), kBlock, 0, c.stream>>>(
-                    d_vals + lo * d, hi - lo, d, keys + lo, c.d_slots, amax, lo);
+                pdl_launch(k_score<D>, grid_for(hi - lo, kBlock, c.num_sms * 8), kBlock, 0, c.stream, 
+                    d_vals + lo * d, hi - lo, d, keys + lo, c.d_slots, amax, lo, nullptr);
             });
             if (!ids_late) {  // (late ids: checked whole, once they are in)
                 const uint64_t c0 = ch ? lo - 1 : 0;  // pair (lo-1, lo) spans the boundary
-                k_ids_check<<<grid_for(hi - c0, kBlock), kBlock, 0, c.stream>>>(
-                    d_ids + c0, hi - c0, c.d_slots);
+                pdl_launch(k_ids_check, grid_for(hi - c0, kBlock), kBlock, 0, c.stream, 
+                    d_ids + c0, hi - c0, c.d_slots, (int)S_FLAG);
                 note_launch(c);
             }
             SKY_LAUNCH_CHECK();
@@ -1966,7 +1992,7 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
         }
         // ---- K2: sampled threshold, K3: ordered prefix selection
         const uint64_t w = r <= kFinal ? r : want;
-        k_sample_threshold<<<1, 1024, 0, c.stream>>>(keys, R, r, w, c.d_slots);
+        pdl_launch(k_sample_threshold, 1, 1024, 0, c.stream, keys, R, r, w, c.d_slots);
         SKY_LAUNCH_CHECK();
         reset_counts(c);
         uint32_t* Pfull = c.buf[B_IDX0].as<uint32_t>(r);
@@ -1989,7 +2015,7 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
             const uint64_t rin = r;
             decide_prefix(Pfull, dev_cap, false, c.d_slots + S_C1);
             if (gate_cond) {
-                k_grid_gate<<<1, 32, 0, c.stream>>>(c.d_slots, 0);
+                pdl_launch(k_grid_gate, 1, 32, 0, c.stream, c.d_slots, 0);
                 SKY_LAUNCH_CHECK();
                 note_launch(c);
             }
@@ -2058,7 +2084,7 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
         // K5 keep every candidate, the host switches after K5's sync.
         const bool gate = rounds == 1 && gate_cond;
         if (gate) {
-            k_grid_gate<<<1, 32, 0, c.stream>>>(c.d_slots, m);
+            pdl_launch(k_grid_gate, 1, 32, 0, c.stream, c.d_slots, m);
             SKY_LAUNCH_CHECK();
             note_launch(c);
         }
@@ -2107,7 +2133,7 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
     ensure_ids();
     if (kc) {
         trace_mark(c, "sky: rounds done (sync)");
-        k_emit_skyline<<<grid_for(kc, kBlock), kBlock, 0, c.stream>>>(
+        pdl_launch(k_emit_skyline, grid_for(kc, kBlock), kBlock, 0, c.stream, 
             K, kc, d_vals, d, (ids_late && !ids_waited) ? nullptr : d_ids, out.d_ids, out.d_skyv);
         SKY_LAUNCH_CHECK();
         note_launch(c);

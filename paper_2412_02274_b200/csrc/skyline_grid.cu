@@ -54,6 +54,7 @@ using GridWord = typename std::conditional<(D <= 4), uint32_t, unsigned long lon
 __global__ void __launch_bounds__(1024)
 k_rank_bounds(const double* __restrict__ v, int d, const uint32_t* __restrict__ R, uint64_t r,
               double* __restrict__ bounds) {
+    pdl_wait();
     using Sort = cub::BlockRadixSort<unsigned long long, 1024, 4>;
     __shared__ typename Sort::TempStorage tmp;
     const int j = blockIdx.x;
@@ -80,6 +81,7 @@ __global__ void __launch_bounds__(kGB)
 k_rank_codes(const double* __restrict__ v, const uint32_t* __restrict__ R, uint32_t r,
              const double* __restrict__ bounds, int k0, int k, GridWord<D>* __restrict__ code,
              uint32_t* __restrict__ cell, uint32_t* __restrict__ count) {
+    pdl_wait();
     using W = GridWord<D>;
     __shared__ double sb[D * 128];
     for (int i = threadIdx.x; i < D * 128; i += blockDim.x) sb[i] = bounds[i];
@@ -115,6 +117,7 @@ __global__ void k_cell_scatter(const W* __restrict__ code, const uint32_t* __res
                                uint32_t r, const uint32_t* __restrict__ seg,
                                uint32_t* __restrict__ cursor, W* __restrict__ scode,
                                uint32_t* __restrict__ sidx) {
+    pdl_wait();
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < r; i += gridDim.x * blockDim.x) {
         const uint32_t cl = cell[i];
         const uint32_t pos = seg[cl] + atomicAdd(&cursor[cl], 1u);
@@ -128,6 +131,7 @@ __global__ void k_cell_scatter(const W* __restrict__ code, const uint32_t* __res
 __global__ void k_row_items(const uint32_t* __restrict__ seg, uint32_t nrows, int k0,
                             uint2* __restrict__ items, unsigned* __restrict__ ctr, int rank,
                             int world) {
+    pdl_wait();
     for (uint32_t row = blockIdx.x * blockDim.x + threadIdx.x; row < nrows;
          row += gridDim.x * blockDim.x) {
         if ((int)(row % (uint32_t)world) != rank) continue;
@@ -242,6 +246,7 @@ k_grid_decide(const double* __restrict__ v, const unsigned long long* __restrict
               const uint32_t* __restrict__ seg, const uint2* __restrict__ items,
               unsigned* __restrict__ ctr, int k0, int k, uint8_t* __restrict__ keep,
               unsigned long long* __restrict__ tests) {
+    pdl_wait();
     using W = GridWord<D>;
     __shared__ W stage[kGB / 32][32];
     __shared__ uint32_t spos[kGB / 32][32];
@@ -481,7 +486,7 @@ void sky_grid_decide(Ctx& c, const double* d_vals, int d, const unsigned long lo
     uint32_t* seg = count + ncells + 1;
     unsigned* ctr = (unsigned*)(seg + ncells + 1);
     SKY_CUDA(cudaMemsetAsync(count, 0, sizeof(uint32_t) * cwords, c.stream));
-    k_rank_bounds<<<d, 1024, 0, c.stream>>>(d_vals, d, R, r, bounds);
+    pdl_launch(k_rank_bounds, d, 1024, 0, c.stream, d_vals, d, R, r, bounds);
     SKY_LAUNCH_CHECK();
     note_launch(c);
     trace_mark(c, "grid: bounds");
@@ -493,7 +498,7 @@ void sky_grid_decide(Ctx& c, const double* d_vals, int d, const unsigned long lo
         W* scode = c.buf[B_GSCODE].as<W>(r);
         uint32_t* sidx = c.buf[B_GSIDX].as<uint32_t>(r);
         uint2* items = c.buf[B_GITEMS].as<uint2>(r / kItem + g.rows + 1);
-        k_rank_codes<D><<<grid_for(r, kGB, c.num_sms * 8), kGB, 0, c.stream>>>(
+        pdl_launch(k_rank_codes<D>, grid_for(r, kGB, c.num_sms * 8), kGB, 0, c.stream, 
             d_vals, R, (uint32_t)r, bounds, g.k0, g.k, code, cell, count);
         SKY_LAUNCH_CHECK();
         size_t tmp = 0;
@@ -502,10 +507,10 @@ void sky_grid_decide(Ctx& c, const double* d_vals, int d, const unsigned long lo
         void* t = c.buf[B_CUB].get(tmp);
         SKY_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, count, seg, (int)ncells + 1, c.stream));
         SKY_CUDA(cudaMemsetAsync(count, 0, sizeof(uint32_t) * ncells, c.stream));  // cursors
-        k_cell_scatter<W><<<grid_for(r, kGB), kGB, 0, c.stream>>>(code, cell, (uint32_t)r, seg,
+        pdl_launch(k_cell_scatter<W>, grid_for(r, kGB), kGB, 0, c.stream, code, cell, (uint32_t)r, seg,
                                                                   count, scode, sidx);
         SKY_LAUNCH_CHECK();
-        k_row_items<<<grid_for(g.rows, kGB), kGB, 0, c.stream>>>(seg, g.rows, g.k0, items, ctr,
+        pdl_launch(k_row_items, grid_for(g.rows, kGB), kGB, 0, c.stream, seg, g.rows, g.k0, items, ctr,
                                                                  shard_rank, shard_world);
         SKY_LAUNCH_CHECK();
         note_launch(c, 5);
@@ -514,7 +519,7 @@ void sky_grid_decide(Ctx& c, const double* d_vals, int d, const unsigned long lo
         SKY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_grid_decide<D>, kGB, 0));
         per_sm = std::max(1, per_sm);
         SKY_CUDA(cudaEventRecord(c.ev[14], c.stream));
-        k_grid_decide<D><<<c.num_sms * per_sm, kGB, 0, c.stream>>>(
+        pdl_launch(k_grid_decide<D>, c.num_sms * per_sm, kGB, 0, c.stream, 
             d_vals, keys, d_ids, R, scode, sidx, seg, items, ctr, g.k0, g.k, keep,
             c.d_slots + S_TESTS_SKY);
         SKY_LAUNCH_CHECK();
