@@ -300,17 +300,32 @@ k_grid_decide(const double* __restrict__ v, const unsigned long long* __restrict
         }
         // largest attribute-0 bin among the candidates = that of the last one
         const uint32_t od0 = (uint32_t)((((uint32_t)scode[end - 1] & 0xFFu) * (uint32_t)k0) >> 7);
-        int od[D], dig[D];
+        // the rows <= own in every coarse attribute, in mixed-radix countdown
+        // order (attribute 1 fastest): position p -> digit j = od[j] -
+        // (p / base[j]) % (od[j] + 1).  Position 0 is the own row.
+        uint32_t od[D], base[D];
+        uint32_t total = 1;
 #pragma unroll
         for (int j = 1; j < D; ++j) {
-            od[j] = (int)((own / wj[j]) % (uint32_t)k);
-            dig[j] = od[j];
+            od[j] = (own / wj[j]) % (uint32_t)k;
+            base[j] = total;
+            total *= od[j] + 1;
         }
-        uint32_t row = own;
+        auto row_at = [&](uint32_t p) -> uint32_t {
+            uint32_t rw = 0;
+#pragma unroll
+            for (int j = 1; j < D; ++j) rw += (od[j] - (p / base[j]) % (od[j] + 1)) * wj[j];
+            return rw;
+        };
         // own row: [row start, first) then [end, row end at od0)
-        uint32_t cur = seg[row * k0], rend = first;
-        uint32_t gap_end = seg[row * k0 + od0 + 1];
-        bool rows_left = D > 1, gap = true;
+        uint32_t cur = seg[own * k0], rend = first;
+        uint32_t gap_end = seg[own * k0 + od0 + 1];
+        bool rows_left = D > 1 && total > 1, gap = true;
+        // the other rows are opened from a window of 32 consecutive countdown
+        // positions whose comparator ranges the lanes load in parallel (one
+        // row each): empty rows cost nothing, a non-empty one a shuffle
+        uint32_t lin = 1, wlo = 0, whi = 0;  // next window start; this lane's range
+        unsigned nzmask = 0;                    // window rows not yet opened, non-empty
         // next <= 32 comparator positions across rows (warp-uniform walk)
         auto fill = [&](uint32_t& mypos) -> uint32_t {
             uint32_t filled = 0;
@@ -323,27 +338,26 @@ k_grid_decide(const double* __restrict__ v, const unsigned long long* __restrict
                         rend = gap_end;
                         continue;
                     }
-                    if (!rows_left) break;
-                    bool stepped = false;
-#pragma unroll
-                    for (int j = 1; j < D; ++j) {
-                        if (!stepped) {
-                            if (dig[j] > 0) {
-                                --dig[j];
-                                row -= wj[j];
-                                stepped = true;
-                            } else {
-                                dig[j] = od[j];
-                                row += (uint32_t)od[j] * wj[j];
-                            }
+                    if (!nzmask) {
+                        if (!rows_left || lin >= total) {
+                            rows_left = false;
+                            break;
                         }
+                        const uint32_t p = lin + lane;
+                        wlo = whi = 0;
+                        if (p < total) {
+                            const uint32_t rw = row_at(p);
+                            wlo = seg[rw * k0];
+                            whi = seg[rw * k0 + od0 + 1];
+                        }
+                        nzmask = __ballot_sync(0xffffffffu, whi > wlo);
+                        lin += 32;
+                        continue;
                     }
-                    if (!stepped) {
-                        rows_left = false;
-                        break;
-                    }
-                    cur = seg[row * k0];
-                    rend = seg[row * k0 + od0 + 1];
+                    const int f = __ffs(nzmask) - 1;
+                    nzmask &= nzmask - 1;
+                    cur = __shfl_sync(0xffffffffu, wlo, f);
+                    rend = __shfl_sync(0xffffffffu, whi, f);
                     continue;
                 }
                 const uint32_t take = min(32u - filled, rend - cur);
