@@ -1021,7 +1021,7 @@ k_sfs_intra_smem(const double* __restrict__ Av, const unsigned long long* __rest
 //          (the GPU recast of the paper's partition-level pruning).
 //  qk == 0 plan cells (grid / angular / sliced / direction): own partition
 //          first, then all others (scan order only).
-// Phase A: every lane alone tests the first 32 comparators of its own cell
+// Phase A: every lane alone tests the first kSolo (16) comparators of its own cell
 // (most candidates are dominated there — no shuffles, no votes); phase B:
 // warp-cooperative, 32 comparators per ballot, for the still-undecided ones.
 template <int D>
@@ -1874,7 +1874,7 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
         static const uint32_t solo = [] {
             const char* e = getenv("SKYGPU_SOLO");
             const int v = e ? atoi(e) : 0;
-            return v > 0 ? (uint32_t)v : 8u;
+            return v > 0 ? (uint32_t)v : 16u;
         }();
         const uint32_t bsf = batch_size(c, rl);
         const uint64_t wf = std::min<uint64_t>((rl + bsf - 1) / bsf, (uint64_t)c.num_sms * 64);

@@ -1,0 +1,9 @@
+run() { tag=$1; w=$2; shift; shift; env "$@" timeout 300 python bench.py --no-cpu-baseline --steps 40 --workload $w > gpurun_out/sw3_${tag}_$w.log 2>&1; python -c "
+import json;j=json.loads(open('gpurun_out/sw3_${tag}_$w.log').read().strip().splitlines()[-1]);print('$tag $w',round(j['ms_per_step'],4))"; }
+for w in C2 C4 C1 C3; do
+run s8 $w X=1
+run s12 $w SKYGPU_SOLO=12
+run s16 $w SKYGPU_SOLO=16
+run s24 $w SKYGPU_SOLO=24
+run s8b $w X=1
+done
