@@ -278,9 +278,22 @@ int closest_slices(long long target, int e) {
 
 }  // namespace
 
+void issue_late_ids(Ctx& c) {
+    if (!c.ids_host) return;
+    SKY_CUDA(cudaEventRecord(c.xev[5], c.stream));
+    SKY_CUDA(cudaStreamWaitEvent(c.copy, c.xev[5], 0));
+    SKY_CUDA(cudaMemcpyAsync(c.ids_dev, c.ids_host, c.ids_n * sizeof(int64_t),
+                             cudaMemcpyHostToDevice, c.copy));
+    SKY_CUDA(cudaEventRecord(c.xev[6], c.copy));
+    c.ids_ready = c.xev[6];
+    c.ids_host = nullptr;
+}
+
 namespace {
 __global__ void k_clear_slot(unsigned long long* slots, int i) {
-    pdl_wait(); slots[i] = 0; }
+    pdl_wait();
+    slots[i] = 0;
+}
 
 __global__ void k_widen(const uint32_t* __restrict__ a, uint64_t* __restrict__ b, uint64_t n) {
     pdl_wait();
@@ -598,7 +611,10 @@ int skygpu_pipeline(const double* vals, const int64_t* ids, uint64_t n, int d,
                               !(flags & SKYGPU_NORMALIZE);
         struct IdsScope {  // the ids event never outlives the call
             Ctx& c;
-            ~IdsScope() { c.ids_ready = nullptr; }
+            ~IdsScope() {
+                c.ids_ready = nullptr;
+                c.ids_host = nullptr;
+            }
         } ids_scope{c};
         if (!dev_in) {
             Timer h2d(c, 2);
@@ -648,12 +664,9 @@ int skygpu_pipeline(const double* vals, const int64_t* ids, uint64_t n, int d,
                 SKY_LAUNCH_CHECK();
                 SKY_CUDA(cudaMemcpyAsync(bv, vals, n * d * sizeof(double), cudaMemcpyHostToDevice,
                                          c.stream));
-                SKY_CUDA(cudaEventRecord(c.xev[5], c.stream));
-                SKY_CUDA(cudaStreamWaitEvent(c.copy, c.xev[5], 0));
-                SKY_CUDA(cudaMemcpyAsync(bi, ids, n * sizeof(int64_t), cudaMemcpyHostToDevice,
-                                         c.copy));
-                SKY_CUDA(cudaEventRecord(c.xev[6], c.copy));
-                c.ids_ready = c.xev[6];
+                c.ids_host = ids;  // copied when K5 starts (issue_late_ids)
+                c.ids_dev = bi;
+                c.ids_n = n;
             } else {
                 SKY_CUDA(cudaMemcpyAsync(bv, vals, n * d * sizeof(double), cudaMemcpyHostToDevice,
                                          c.stream));

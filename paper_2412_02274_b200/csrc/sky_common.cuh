@@ -159,6 +159,12 @@ struct Ctx {
     // this event; the skyline runs on the speculation that they are strictly
     // increasing (ties by position) and checks them at the end (S_IDSBAD)
     cudaEvent_t ids_ready = nullptr;
+    // (or not yet issued: the copy of these host ids is queued by the
+    // skyline itself when K5 starts — a latency-bound kernel the copy's
+    // traffic barely slows, unlike the HBM-bound ones before it)
+    const int64_t* ids_host = nullptr;
+    int64_t* ids_dev = nullptr;
+    uint64_t ids_n = 0;
 };
 
 // record a labelled device timestamp when tracing is on
@@ -294,6 +300,8 @@ struct GresOut {
 GresOut gres_device(Ctx& c, const double* d_skyv, const int64_t* d_ids, uint64_t S, int d,
                     int cap, int engine, int shard_rank, int shard_world, bool check_skyline,
                     int32_t* d_den, bool allow_spec = false);
+// queue the deferred copy of the host ids (Ctx::ids_host), once
+void issue_late_ids(Ctx& c);
 // queue the read of the speculation flag (before the caller's final sync)
 void gres_spec_fetch(Ctx& c);
 // after that sync: true when the speculative launch did not apply

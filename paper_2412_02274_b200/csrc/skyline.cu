@@ -1457,13 +1457,14 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
     st.tuples_in = n;
     // ids still in flight (host-pointer pipeline): ties by position until the
     // ids are needed (rank grid, output); their strict order is checked then
-    const bool ids_late = c.ids_ready != nullptr;
+    const bool ids_late = c.ids_ready != nullptr || c.ids_host != nullptr;
     const int64_t* tie_ids = ids_late ? nullptr : d_ids;
     bool ids_waited = false;
     auto ensure_ids = [&]() {
         // (the streamed head's seed never waits: its ids are not an output)
         if (!ids_late || ids_waited || (sky_engine & kSkyFirstPrefix)) return;
         ids_waited = true;
+        issue_late_ids(c);  // (if K5 never ran)
         SKY_CUDA(cudaStreamWaitEvent(c.stream, c.ids_ready, 0));
         pdl_launch(k_ids_check, grid_for(n, kBlock), kBlock, 0, c.stream, d_ids, n, c.d_slots, S_IDSBAD);
         SKY_LAUNCH_CHECK();
@@ -1904,6 +1905,7 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
         uint8_t* fkeep = c.buf[B_SV].as<uint8_t>(r);
         trace_mark(c, "sky: select A' + segments + gather Pv");
         SKY_CUDA(cudaEventRecord(e2, c.stream));
+        issue_late_ids(c);  // the deferred ids copy overlaps K5
         launch_k5(A, R, r, fkeep, seeded, amax);
         SKY_CUDA(cudaEventRecord(e3, c.stream));
         trace_mark(c, "sky: K5 filter kernel");
