@@ -645,11 +645,10 @@ int skygpu_pipeline(const double* vals, const int64_t* ids, uint64_t n, int d,
                     SKY_CUDA(cudaEventRecord(c.xev[ch], c.copy));
                     feed.ready[ch] = c.xev[ch];
                 }
-                if (ids_late) {  // every value first, then the ids
-                    SKY_CUDA(cudaMemcpyAsync(bi, ids, n * sizeof(int64_t),
-                                             cudaMemcpyHostToDevice, c.copy));
-                    SKY_CUDA(cudaEventRecord(c.xev[6], c.copy));
-                    c.ids_ready = c.xev[6];
+                if (ids_late) {  // every value first; the ids when the skyline asks
+                    c.ids_host = ids;  // (issue_late_ids: behind the values, or at
+                    c.ids_dev = bi;    //  the rank-grid kernel's start)
+                    c.ids_n = n;
                 }
             } else if (ids_late) {
                 // values first (the skyline starts as soon as they land), the

@@ -1447,6 +1447,10 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
                 // the full pass below reports the reference's error
             }
         }
+        // deferred ids: straight behind the values (the tail work after the
+        // last chunk is short), unless the rank grid comes next — then at its
+        // compute-bound kernel, clear of the HBM-bound code passes
+        if (!head_grid) issue_late_ids(c);
         if (!nseed) {
             for (int ch = 1; ch < feed->nchunks; ++ch)
                 SKY_CUDA(cudaStreamWaitEvent(c.stream, feed->ready[ch], 0));

@@ -533,6 +533,7 @@ void sky_grid_decide(Ctx& c, const double* d_vals, int d, const unsigned long lo
         SKY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_grid_decide<D>, kGB, 0));
         per_sm = std::max(1, per_sm);
         SKY_CUDA(cudaEventRecord(c.ev[14], c.stream));
+        issue_late_ids(c);  // (deferred host ids: their copy overlaps K6)
         pdl_launch(k_grid_decide<D>, c.num_sms * per_sm, kGB, 0, c.stream, 
             d_vals, keys, d_ids, R, scode, sidx, seg, items, ctr, g.k0, g.k, keep,
             c.d_slots + S_TESTS_SKY);
