@@ -559,7 +559,8 @@ __global__ void k_gap_witness(const double* __restrict__ v, uint64_t S, int d, i
 // share of the column — no global CAS contention (the global-table form
 // serialises millions of CAS on d x 2cap addresses at C5).  Any pair proves
 // the cap, so block-local detection is exact; S <= 4096 runs one block per
-// attribute (the whole column, like the global table).
+// attribute (the whole column, like the global table); a block per 1024
+// values otherwise (any pigeonhole pair of distinct values proves the cap).
 constexpr int kWitnessSmemCap = 2048;
 
 __global__ void __launch_bounds__(256)
@@ -606,7 +607,7 @@ __global__ void __launch_bounds__(256)
 void launch_gap_witness(Ctx& c, const double* d_soa, uint64_t S, int d, int cap,
                         unsigned long long* table) {
     if (cap <= kWitnessSmemCap) {
-        const uint64_t want = (S + 4095) / 4096;
+        const uint64_t want = S <= 4096 ? 1 : (S + 1023) / 1024;
         const unsigned bx = (unsigned)std::max<uint64_t>(
             1, std::min<uint64_t>(want, (uint64_t)c.num_sms * 8 / (uint64_t)d + 1));
         pdl_launch(k_gap_witness_smem, dim3(bx, (unsigned)d), 256, 0, c.stream, d_soa, S, cap, c.d_slots);
