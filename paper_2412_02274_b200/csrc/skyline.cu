@@ -944,8 +944,8 @@ k_sfs_intra_chunked(const double* __restrict__ Av, const unsigned long long* __r
     add_count(tests, cnt);
 }
 
-// K4 with the prefix's codes resident in shared memory (D <= 4: one u64
-// code word per tuple, m <= 16384 -> <= 128 KB): one CTA per SM loads the
+// K4 with the prefix's codes resident in shared memory (one u64 code word
+// per tuple for d <= 4, two for d <= 8; <= 16384 words = 128 KB): one CTA per SM loads the
 // codes once, then each warp takes a candidate (longest first: candidate i
 // has i predecessors) and scans its predecessors in sum order, 64 per vote
 // (two per lane), shared-memory latency instead of L2 latency per step; the
@@ -957,57 +957,77 @@ template <int D>
 __global__ void __launch_bounds__(1024, 1)
 k_sfs_intra_smem(const double* __restrict__ Av, const unsigned long long* __restrict__ Aq,
                  uint32_t m, uint8_t* __restrict__ keep, unsigned long long* __restrict__ tests,
-                 uint32_t astride, const unsigned long long* __restrict__ mdev) {
+                 uint32_t astride, const unsigned long long* __restrict__ mdev,
+                 uint32_t scap) {
     pdl_wait();
-    static_assert(QW<D>::W == 1, "one code word per tuple");
+    constexpr int W = QW<D>::W;  // code words per tuple (1: d <= 4, 2: d <= 8)
     if (!dev_count(mdev, m)) return;
-    extern __shared__ unsigned long long sq[];
-    for (uint32_t j = threadIdx.x; j < m; j += blockDim.x) sq[j] = Aq[j];
+    // the codes in shared memory when they fit the launch's allocation
+    // (scap words), else read through L1 (a device-sized round larger than
+    // expected): same results either way
+    extern __shared__ unsigned long long sq_sm[];
+    const bool in_smem = (uint64_t)m * W <= scap;
+    if (in_smem)
+        for (uint32_t j = threadIdx.x; j < m * W; j += blockDim.x) sq_sm[j] = Aq[j];
     __syncthreads();
-    const uint32_t lane = threadIdx.x & 31;
-    // consecutive candidates (similar cost) on different SMs
-    const uint32_t warp = (threadIdx.x >> 5) * gridDim.x + blockIdx.x;
-    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    // (two instantiations of the scan so the shared-memory one keeps LDS)
     unsigned long long cnt = 0;
-    for (uint32_t k = warp; k < m; k += nwarps) {
-        const uint32_t i = m - 1 - k;
-        const unsigned long long tg = sq[i] | kH16;
-        double t[D];
+    auto scan = [&](const unsigned long long* __restrict__ sq) {
+        const uint32_t lane = threadIdx.x & 31;
+        // consecutive candidates (similar cost) on different SMs
+        const uint32_t warp = (threadIdx.x >> 5) * gridDim.x + blockIdx.x;
+        const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+        for (uint32_t k = warp; k < m; k += nwarps) {
+            const uint32_t i = m - 1 - k;
+            unsigned long long tg[W];
 #pragma unroll
-        for (int a = 0; a < D; ++a) t[a] = Av[(uint64_t)a * astride + i];
-        bool dominated = false;
-        // 128 comparators per step, the code tests branch-free; only a step
-        // with a code pass somewhere in the warp takes the exact tests
-        for (uint32_t j0 = 0; j0 < i; j0 += 128) {
-            unsigned pm = 0;
+            for (int w = 0; w < W; ++w) tg[w] = sq[(uint64_t)i * W + w] | kH16;
+            double t[D];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const uint32_t j = j0 + u * 32 + lane;
-                const bool in = j < i;
-                cnt += in;
-                const unsigned long long cq = in ? sq[j] : 0ULL;
-                pm |= (unsigned)(in && ((tg - cq) & kH16) == kH16) << u;
-            }
-            if (__any_sync(0xffffffffu, pm != 0)) {
-                bool hit = false;
+            for (int a = 0; a < D; ++a) t[a] = Av[(uint64_t)a * astride + i];
+            bool dominated = false;
+            // 128 comparators per step, the code tests branch-free; only a step
+            // with a code pass somewhere in the warp takes the exact tests
+            for (uint32_t j0 = 0; j0 < i; j0 += 128) {
+                unsigned pm = 0;
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                    if ((pm >> u) & 1u) {
-                        const uint32_t j = j0 + u * 32 + lane;
-                        double sv[D];
+                    const uint32_t j = j0 + u * 32 + lane;
+                    const bool in = j < i;
+                    cnt += in;
+                    bool ok = in;
 #pragma unroll
-                        for (int a = 0; a < D; ++a) sv[a] = Av[(uint64_t)a * astride + j];
-                        hit |= dom_f64<D>(sv, t);
+                    for (int w = 0; w < W; ++w) {
+                        const unsigned long long cq = in ? sq[(uint64_t)j * W + w] : 0ULL;
+                        ok &= ((tg[w] - cq) & kH16) == kH16;
+                    }
+                    pm |= (unsigned)ok << u;
+                }
+                if (__any_sync(0xffffffffu, pm != 0)) {
+                    bool hit = false;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        if ((pm >> u) & 1u) {
+                            const uint32_t j = j0 + u * 32 + lane;
+                            double sv[D];
+#pragma unroll
+                            for (int a = 0; a < D; ++a) sv[a] = Av[(uint64_t)a * astride + j];
+                            hit |= dom_f64<D>(sv, t);
+                        }
+                    }
+                    if (__any_sync(0xffffffffu, hit)) {
+                        dominated = true;
+                        break;
                     }
                 }
-                if (__any_sync(0xffffffffu, hit)) {
-                    dominated = true;
-                    break;
-                }
             }
+            if (lane == 0) keep[i] = dominated ? 0 : 1;
         }
-        if (lane == 0) keep[i] = dominated ? 0 : 1;
-    }
+    };
+    if (in_smem)
+        scan(sq_sm);
+    else
+        scan(Aq);
     add_count(tests, cnt);
 }
 
@@ -1722,8 +1742,11 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
             dispatch_d(d, [&](auto DC) {
                 constexpr int D = decltype(DC)::value;
                 const unsigned grid = (unsigned)((wi * 32 + kBlock - 1) / kBlock);
-                if constexpr (D > 0 && D <= 4) {
+                if constexpr (D > 0 && D <= 8) {
+                    constexpr uint32_t kWq = QW<D>::W;
                     if (intra_chunked && intra_smem && m <= kIntraSmemMax) {
+                        const uint32_t scap =
+                            (uint32_t)std::min<uint64_t>(m * kWq, kIntraSmemMax);
                         static bool attr = false;
                         if (!attr) {
                             SKY_CUDA(cudaFuncSetAttribute(
@@ -1731,9 +1754,10 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
                                 (int)(kIntraSmemMax * sizeof(unsigned long long))));
                             attr = true;
                         }
-                        pdl_launch(k_sfs_intra_smem<D>, c.num_sms, 1024, m * sizeof(unsigned long long), c.stream, Av, Aq, (uint32_t)m, keep,
-                                                          c.d_slots + S_TESTS_SKY, (uint32_t)m,
-                                                          mdev);
+                        pdl_launch(k_sfs_intra_smem<D>, c.num_sms, 1024,
+                                   scap * sizeof(unsigned long long), c.stream, Av, Aq,
+                                   (uint32_t)m, keep, c.d_slots + S_TESTS_SKY, (uint32_t)m, mdev,
+                                   scap);
                         return;
                     }
                 }
