@@ -420,7 +420,7 @@ def roofline(st, sky_ms, gres_ms, d, clk, workload="C2"):
             # 16-bit quantised SWAR prefilter (one u64 word per 4 attributes):
             # IADD3, IADD3.X, 2 LOP3, 2 ISETP per word on the ALU pipe; the
             # exact float64 test runs only on a code pass
-            kern = ("k_sfs_intra_smem" if d <= 4 else "k_sfs_intra_chunked") + "+k_sfs_filter_q"
+            kern = "k_sfs_intra_smem+k_sfs_filter_q"
             tests, ms, launches = st["skyline_tests"], sky_ms, st["sky_kernel_launches"]
             i_test, pipe = 6 * (1 if d <= 4 else 2), "alu"
         else:
