@@ -1264,6 +1264,8 @@ __global__ void k_id_keys(const int64_t* __restrict__ ids, const uint32_t* __res
         out[i] = static_cast<unsigned long long>(ids[list[i]]) ^ 0x8000000000000000ULL;
 }
 
+// (D > 0: the tuple's D values loaded together, then stored per attribute)
+template <int D>
 __global__ void k_emit_skyline(const uint32_t* __restrict__ K, uint64_t S,
                                const double* __restrict__ v, int d,
                                const int64_t* __restrict__ ids, int64_t* __restrict__ oid,
@@ -1273,7 +1275,15 @@ __global__ void k_emit_skyline(const uint32_t* __restrict__ K, uint64_t S,
          k += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t p = K[k];
         if (ids) oid[k] = ids[p];
-        for (int a = 0; a < d; ++a) skyv[a * S + k] = v[(uint64_t)p * d + a];
+        if constexpr (D > 0) {
+            double t[D];
+#pragma unroll
+            for (int a = 0; a < D; ++a) t[a] = v[(uint64_t)p * D + a];
+#pragma unroll
+            for (int a = 0; a < D; ++a) skyv[a * S + k] = t[a];
+        } else {
+            for (int a = 0; a < d; ++a) skyv[a * S + k] = v[(uint64_t)p * d + a];
+        }
     }
 }
 
@@ -2163,8 +2173,12 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
     ensure_ids();
     if (kc) {
         trace_mark(c, "sky: rounds done (sync)");
-        pdl_launch(k_emit_skyline, grid_for(kc, kBlock), kBlock, 0, c.stream, 
-            K, kc, d_vals, d, (ids_late && !ids_waited) ? nullptr : d_ids, out.d_ids, out.d_skyv);
+        dispatch_d(d, [&](auto DC) {
+            constexpr int D = decltype(DC)::value;
+            pdl_launch(k_emit_skyline<D>, grid_for(kc, kBlock), kBlock, 0, c.stream, K, kc,
+                       d_vals, d, (ids_late && !ids_waited) ? nullptr : d_ids, out.d_ids,
+                       out.d_skyv);
+        });
         SKY_LAUNCH_CHECK();
         note_launch(c);
     }
