@@ -1351,14 +1351,16 @@ uint32_t batch_size(const Ctx& c, uint64_t count) {
 
 int cells_per_dim(uint64_t m, int d, uint32_t* ncells);
 
-// The scan-order cell spec of a plan (see plan_cell): the plan's own
-// partition when it has at most kMaxCells parts (and d <= 8 for the
-// attribute-scaled kinds), else direction cells sized for ~128 tuples each.
+// The scan-order cell spec (see plan_cell): direction cells sized for ~128
+// tuples each — measured faster than the plan's own partition (C2 -4%, C1
+// -3%, C4/C3 even: one float division per candidate instead of the angular
+// plan's arctangents); SKYGPU_SCAN_CELLS=plan scans in the plan's partition
+// when it has at most kMaxCells parts (and d <= 8 for the attribute-scaled
+// kinds).  Scan order only: the results never depend on it.
 int scan_cell_spec(const skygpu_plan& plan, uint64_t m, int d, bool qpre, uint32_t* ncells) {
-    // tuning knob: SKYGPU_SCAN_CELLS=dir ignores the plan's partition
     static const bool dir_only = [] {
         const char* e = getenv("SKYGPU_SCAN_CELLS");
-        return e && e[0] == 'd';
+        return !(e && e[0] == 'p');
     }();
     if (dir_only) {
         const int mc = cells_per_dim(m, d, ncells);
