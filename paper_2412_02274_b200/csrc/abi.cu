@@ -221,8 +221,21 @@ void begin_stats(Ctx& c, skygpu_stats* st) {
 }
 
 // the call's final synchronisation: test counters and event spans
+// queue the read of the test counters with a call's outputs (before its
+// final synchronisation), so end_stats needs no round trip of its own
+void fetch_test_counters(Ctx& c) {
+    SKY_CUDA(cudaMemcpyAsync(c.h_slots + S_TESTS_SKY, c.d_slots + S_TESTS_SKY,
+                             2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c.stream));
+    c.counters_fetched = true;
+}
+
 void end_stats(Ctx& c) {
-    read_slots(c, S_TESTS_SKY, 2);
+    if (c.counters_fetched) {  // read with the outputs: only the timing events
+        c.counters_fetched = false;  // recorded since then are left to complete
+        SKY_CUDA(cudaStreamSynchronize(c.stream));
+    } else {
+        read_slots(c, S_TESTS_SKY, 2);
+    }
     c.st->skyline_tests = c.h_slots[S_TESTS_SKY];
     c.st->gres_tests = c.h_slots[S_TESTS_GRES];
     for (int i = 0; i < g_nspans; ++i) {
@@ -738,8 +751,10 @@ int skygpu_pipeline(const double* vals, const int64_t* ids, uint64_t n, int d,
         if (ids_late)
             SKY_CUDA(cudaMemcpyAsync(c.h_slots + S_IDSBAD, c.d_slots + S_IDSBAD,
                                      sizeof(unsigned long long), cudaMemcpyDeviceToHost, c.stream));
+        fetch_test_counters(c);
         SKY_CUDA(cudaStreamSynchronize(c.stream));
         if (ids_late && c.h_slots[S_IDSBAD]) {
+            c.counters_fetched = false;  // (the redo adds tests)
             // the ids are not strictly increasing: (sum, id) ties may order
             // differently from positions — the whole call again, ids resident
             trace_mark(c, "ids not in position order: re-run");
@@ -763,6 +778,7 @@ int skygpu_pipeline(const double* vals, const int64_t* ids, uint64_t n, int d,
             SKY_CUDA(cudaStreamSynchronize(c.stream));
         }
         if (gres_spec_failed(c)) {  // the speculative gres launch did not apply: redo
+            c.counters_fetched = false;  // (the redo adds tests)
             trace_mark(c, "gres: speculation missed, exact path");
             go = gres_device(c, so.d_skyv, so.d_ids, so.S, d, cap, gres_engine, shard_rank,
                              shard_world, false, den);

@@ -155,6 +155,7 @@ struct Ctx {
     double thost[96];  // host clock at each mark (us): where the GPU waits for the CPU
     int trace_chunks = 0;  // streamed chunks whose arrival the trace reports
     bool gres_spec = false;  // a speculative gres launch awaits its S_SPEC check
+    bool counters_fetched = false;  // test counters already read with the outputs
     // host-pointer pipeline: the ids are still in flight (copy stream) until
     // this event; the skyline runs on the speculation that they are strictly
     // increasing (ties by position) and checks them at the end (S_IDSBAD)
