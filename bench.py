@@ -314,6 +314,8 @@ def our_arm(args):
                    "gres_engine": {0: "auto", 1: "pairs", 2: "cells"}[args.engine],
                    "skyline_engine": {8: "prefix rounds", 16: "rank grid"}.get(stats[-1]["sky_engine"], "?")},
         "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms,
+                # (the spread of the host-timed steps: host noise shows here)
+                "ms_min": min(e2e_times), "ms_median": sorted(e2e_times)[len(e2e_times) // 2],
                 "h2d_bytes_per_step": n * d * 8 + n * 8,
                 "d2h_bytes_per_step": S * 8 + S * 4},  # u64 positions + i32 denominators
         "gpu_launches": int(sum(s["kernel_launches"] for s in stats)),
