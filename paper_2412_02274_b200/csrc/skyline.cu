@@ -987,14 +987,14 @@ k_sfs_intra_smem(const double* __restrict__ Av, const unsigned long long* __rest
             for (int a = 0; a < D; ++a) t[a] = Av[(uint64_t)a * astride + i];
             bool dominated = false;
             // 128 comparators per step, the code tests branch-free; only a step
-            // with a code pass somewhere in the warp takes the exact tests
-            for (uint32_t j0 = 0; j0 < i; j0 += 128) {
+            // with a code pass somewhere in the warp takes the exact tests.
+            // Full steps carry no bounds checks; the partial last one does.
+            auto step = [&](uint32_t j0, bool full) -> bool {
                 unsigned pm = 0;
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     const uint32_t j = j0 + u * 32 + lane;
-                    const bool in = j < i;
-                    cnt += in;
+                    const bool in = full || j < i;
                     bool ok = in;
 #pragma unroll
                     for (int w = 0; w < W; ++w) {
@@ -1003,25 +1003,30 @@ k_sfs_intra_smem(const double* __restrict__ Av, const unsigned long long* __rest
                     }
                     pm |= (unsigned)ok << u;
                 }
-                if (__any_sync(0xffffffffu, pm != 0)) {
-                    bool hit = false;
+                if (!__any_sync(0xffffffffu, pm != 0)) return false;
+                bool hit = false;
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        if ((pm >> u) & 1u) {
-                            const uint32_t j = j0 + u * 32 + lane;
-                            double sv[D];
+                for (int u = 0; u < 4; ++u) {
+                    if ((pm >> u) & 1u) {
+                        const uint32_t j = j0 + u * 32 + lane;
+                        double sv[D];
 #pragma unroll
-                            for (int a = 0; a < D; ++a) sv[a] = Av[(uint64_t)a * astride + j];
-                            hit |= dom_f64<D>(sv, t);
-                        }
-                    }
-                    if (__any_sync(0xffffffffu, hit)) {
-                        dominated = true;
-                        break;
+                        for (int a = 0; a < D; ++a) sv[a] = Av[(uint64_t)a * astride + j];
+                        hit |= dom_f64<D>(sv, t);
                     }
                 }
+                return __any_sync(0xffffffffu, hit);
+            };
+            uint32_t j0 = 0;
+            for (; j0 + 128 <= i && !dominated; j0 += 128) dominated = step(j0, true);
+            if (!dominated && j0 < i) {
+                dominated = step(j0, false);
+                j0 += 128;
             }
-            if (lane == 0) keep[i] = dominated ? 0 : 1;
+            if (lane == 0) {
+                cnt += j0 < i ? j0 : i;  // comparators examined (whole steps)
+                keep[i] = dominated ? 0 : 1;
+            }
         }
     };
     if (in_smem)
