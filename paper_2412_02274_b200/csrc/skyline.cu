@@ -1191,10 +1191,10 @@ k_sfs_filter_q(const double* __restrict__ v, const unsigned long long* __restric
             } else {
                 uint32_t q = __shfl_sync(0xffffffffu, start, j) + kSolo + lane;
                 while (q >= np) q -= np;
-                for (uint32_t done = kSolo; done < np; done += 32) {
+                uint32_t done = kSolo;
+                for (; done < np; done += 32) {
                     bool hit = false;
                     if (done + lane < np) {
-                        ++cnt;
                         if (le16<D>(Pq + (uint64_t)q * W, tg)) {
                             double s[D];
 #pragma unroll
@@ -1206,9 +1206,12 @@ k_sfs_filter_q(const double* __restrict__ v, const unsigned long long* __restric
                     while (q >= np) q -= np;
                     if (__any_sync(0xffffffffu, hit)) {
                         dominated = true;
+                        done += 32;
                         break;
                     }
                 }
+                // comparators examined, counted once (not per lane and step)
+                if ((int)lane == j && np > kSolo) cnt += min(done, np) - kSolo;
             }
             if ((int)lane == j) mykeep = !dominated;
         }
