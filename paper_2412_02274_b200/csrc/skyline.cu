@@ -85,7 +85,8 @@ __global__ void k_score(const double* __restrict__ v, uint64_t n, int d,
                         unsigned long long* __restrict__ key,
                         unsigned long long* __restrict__ slots,
                         unsigned long long* __restrict__ amax, uint64_t base = 0,
-                        const int64_t* __restrict__ ids = nullptr) {
+                        const int64_t* __restrict__ ids = nullptr,
+                        uint32_t* __restrict__ prefix = nullptr) {
     pdl_wait();
     constexpr int DA = D > 0 ? D : 1;
     unsigned long long mn = ~0ULL, mx = 0;
@@ -114,6 +115,19 @@ __global__ void k_score(const double* __restrict__ v, uint64_t n, int d,
         }
         const unsigned long long b = ord_bits(s);
         key[i] = b;
+        if (prefix) {  // the first round's prefix {key < T} appended (unordered:
+            // the prefix sort orders it fully by (sum, id, position))
+            const bool in = b < slots[S_THR];
+            const unsigned am_ = __activemask();
+            const unsigned bal = __ballot_sync(am_, in);
+            if (bal) {
+                const int lane = threadIdx.x & 31, leader = __ffs(bal) - 1;
+                unsigned long long at = 0;
+                if (lane == leader) at = atomicAdd(&slots[S_C1], (unsigned long long)__popc(bal));
+                at = __shfl_sync(am_, at, leader);
+                if (in) prefix[at + __popc(bal & ((1u << lane) - 1u))] = (uint32_t)i;
+            }
+        }
         mn = b < mn && b > 0 ? b : mn;  // min POSITIVE key (zero sums: bucket 0 below)
         mx = b > mx ? b : mx;
         if (bad) atomicMin(&slots[S_BAD], static_cast<unsigned long long>(base + i));
@@ -258,7 +272,8 @@ __global__ void k_grid_range(const double* __restrict__ v, uint64_t total,
 constexpr int kSampleItems = 4;
 __global__ void __launch_bounds__(1024)
 k_sample_threshold(const unsigned long long* __restrict__ key, const uint32_t* __restrict__ R,
-                   uint64_t r, uint64_t want, unsigned long long* __restrict__ slots) {
+                   uint64_t r, uint64_t want, unsigned long long* __restrict__ slots,
+                   const double* __restrict__ v, int d) {
     pdl_wait();
     // An approximate quantile suffices (T is exact once chosen): the samples
     // are bucketed linearly between their min and max sum and the bucket
@@ -282,7 +297,13 @@ k_sample_threshold(const unsigned long long* __restrict__ key, const uint32_t* _
         const uint64_t s = threadIdx.x * kSampleItems + j;
         const uint64_t pos = s * r / NS;
         const uint32_t t = R ? R[pos] : (uint32_t)pos;
-        items[j] = key[t];
+        if (v) {  // (before the keys exist: the sampled tuple's sum, K1's order)
+            double sum = 0.0;
+            for (int a = 0; a < d; ++a) sum = __dadd_rn(sum, v[(uint64_t)t * d + a]);
+            items[j] = ord_bits(sum);
+        } else {
+            items[j] = key[t];
+        }
         mn = items[j] < mn ? items[j] : mn;
         mx = items[j] > mx ? items[j] : mx;
     }
@@ -1522,11 +1543,33 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
     const bool qpre = d >= 1 && d <= 8;
     unsigned long long* amax = c.buf[B_AMAX].as<unsigned long long>(kMaxDims);
     SKY_CUDA(cudaMemsetAsync(amax, 0, sizeof(unsigned long long) * kMaxDims, c.stream));
+    // prefix size per round: stays below the one-CTA capacity despite
+    // sampling noise (SKYGPU_PREFIX overrides, for tuning)
+    static const uint64_t kWant = [] {
+        const char* e = getenv("SKYGPU_PREFIX");
+        const long long v = e ? atoll(e) : 0;
+        return v > 0 ? (uint64_t)v : (uint64_t)8000;
+    }();
+    static const bool fused_sel_on = [] {  // SKYGPU_FUSED_SELECT=0: CUB selection
+        const char* e = getenv("SKYGPU_FUSED_SELECT");
+        return !(e && e[0] == '0');
+    }();
+    // the first round's threshold sampled from the values and its prefix
+    // appended by K1 itself (no separate selection pass) — plain rounds only
+    bool fused_first = !feed && sky_engine == 0 && !(plan.strategy == SKYGPU_GRID) &&
+                       n_reps == 0 && qpre && n > kCTACap && fused_sel_on;
+    if (fused_first) {
+        pdl_launch(k_sample_threshold, 1, 1024, 0, c.stream, (const unsigned long long*)nullptr,
+                   (const uint32_t*)nullptr, n, kWant, c.d_slots, d_vals, d);
+        SKY_LAUNCH_CHECK();
+        note_launch(c);
+    }
     if (!feed) {  // (streamed input: per chunk, below)
+        uint32_t* pre = fused_first ? c.buf[B_IDX0].as<uint32_t>(n) : nullptr;
         dispatch_d(d, [&](auto DC) {
             constexpr int D = decltype(DC)::value;
-            pdl_launch(k_score<D>, grid_for(n, kBlock, c.num_sms * 8), kBlock, 0, c.stream, 
-                d_vals, n, d, keys, c.d_slots, amax, 0, tie_ids);  // + ids sortedness
+            pdl_launch(k_score<D>, grid_for(n, kBlock, c.num_sms * 8), kBlock, 0, c.stream,
+                       d_vals, n, d, keys, c.d_slots, amax, 0, tie_ids, pre);  // + ids order
         });
         SKY_LAUNCH_CHECK();
         note_launch(c, 1);
@@ -1589,13 +1632,6 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
     st.tuples_into_parallel = r;
 
     uint64_t kc = 0;
-    // prefix size per round: stays below the one-CTA capacity despite
-    // sampling noise (SKYGPU_PREFIX overrides, for tuning)
-    static const uint64_t kWant = [] {
-        const char* e = getenv("SKYGPU_PREFIX");
-        const long long v = e ? atoll(e) : 0;
-        return v > 0 ? (uint64_t)v : (uint64_t)8000;
-    }();
     static const uint64_t kSeedWant = [] {  // the streamed head's seed prefix
         const char* e = getenv("SKYGPU_SEED_PREFIX");
         const long long v = e ? atoll(e) : 0;
@@ -1998,7 +2034,7 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
             dispatch_d(d, [&](auto DC) {
                 constexpr int D = decltype(DC)::value;
                 pdl_launch(k_score<D>, grid_for(hi - lo, kBlock, c.num_sms * 8), kBlock, 0, c.stream, 
-                    d_vals + lo * d, hi - lo, d, keys + lo, c.d_slots, amax, lo, nullptr);
+                    d_vals + lo * d, hi - lo, d, keys + lo, c.d_slots, amax, lo, nullptr, nullptr);
             });
             if (!ids_late) {  // (late ids: checked whole, once they are in)
                 const uint64_t c0 = ch ? lo - 1 : 0;  // pair (lo-1, lo) spans the boundary
@@ -2042,14 +2078,20 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
         }
         // ---- K2: sampled threshold, K3: ordered prefix selection
         const uint64_t w = r <= kFinal ? r : want;
-        pdl_launch(k_sample_threshold, 1, 1024, 0, c.stream, keys, R, r, w, c.d_slots);
+        if (!fused_first)
+            pdl_launch(k_sample_threshold, 1, 1024, 0, c.stream, keys, R, r, w, c.d_slots,
+                       (const double*)nullptr, 0);
         SKY_LAUNCH_CHECK();
-        reset_counts(c);
         uint32_t* Pfull = c.buf[B_IDX0].as<uint32_t>(r);
-        trace_mark(c, "sky: score + sample threshold");
-        select_if(c, R, r, BelowThreshold{keys, c.d_slots + S_THR}, Pfull, c.d_slots + S_C1);
-        note_launch(c, 1);
-        trace_mark(c, "sky: select prefix");
+        if (!fused_first) {
+            reset_counts(c);
+            trace_mark(c, "sky: score + sample threshold");
+            select_if(c, R, r, BelowThreshold{keys, c.d_slots + S_THR}, Pfull, c.d_slots + S_C1);
+            note_launch(c, 1);
+            trace_mark(c, "sky: select prefix");
+        }
+        const bool unordered_prefix = fused_first;
+        fused_first = false;
         // the round sized on the device — no host round trip before K5: the
         // prefix sort, K4, K5, the survivor selection and the ride-along final
         // round read the prefix count from its slot; the host checks it with
@@ -2112,6 +2154,12 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
         } else {
             read_slots(c, S_BAD, 11);
             validate();
+        }
+        if (unordered_prefix) {  // the synchronous path sorts stably: re-select in order
+            reset_counts(c);
+            select_if(c, R, r, BelowThreshold{keys, c.d_slots + S_THR}, Pfull, c.d_slots + S_C1);
+            note_launch(c, 1);
+            read_slots(c, S_BAD, 11);
         }
         const uint64_t m = c.h_slots[S_C1];
         if (m == 0) throw Error(SKYGPU_ERUNTIME, "skyline: empty prefix (internal)");
