@@ -465,12 +465,9 @@ int skygpu_parallel_skyline(const double* vals, const int64_t* ids, uint64_t n, 
                                      cudaMemcpyHostToDevice, c.stream));
         }
         SkylineOut so = skyline_device(c, dv, di, n, d, pl, dr, n_reps);
-        if (so.S) {
-            uint64_t* wide = c.buf[B_OUTPOS].as<uint64_t>(so.S);
-            widen_u32_u64(c, so.d_inpos, wide, so.S);
-            SKY_CUDA(cudaMemcpyAsync(out_pos, wide, so.S * sizeof(uint64_t),
+        if (so.S)
+            SKY_CUDA(cudaMemcpyAsync(out_pos, so.d_pos64, so.S * sizeof(uint64_t),
                                      cudaMemcpyDeviceToHost, c.stream));
-        }
         all.stop(&c.st->ms_total);
         end_stats(c);  // final synchronisation
         *out_n = so.S;
@@ -741,9 +738,8 @@ int skygpu_pipeline(const double* vals, const int64_t* ids, uint64_t n, int d,
         } else if (so.S) {
             // positions widened on the device, copied straight into the
             // caller's buffer (no host-side staging or conversion loop)
-            uint64_t* wide = c.buf[B_OUTPOS].as<uint64_t>(so.S);
-            widen_u32_u64(c, so.d_inpos, wide, so.S);
-            SKY_CUDA(cudaMemcpyAsync(out_pos, wide, so.S * sizeof(uint64_t),
+            // (widened by the skyline's emit kernel, SkylineOut::d_pos64)
+            SKY_CUDA(cudaMemcpyAsync(out_pos, so.d_pos64, so.S * sizeof(uint64_t),
                                      cudaMemcpyDeviceToHost, c.stream));
             copy_den();
         }
@@ -769,9 +765,7 @@ int skygpu_pipeline(const double* vals, const int64_t* ids, uint64_t n, int d,
                 if (c.shard_world > 1) shard_allreduce_max(c, den, so.S, 4);
             }
             if (so.S) {
-                uint64_t* wide = c.buf[B_OUTPOS].as<uint64_t>(so.S);
-                widen_u32_u64(c, so.d_inpos, wide, so.S);
-                SKY_CUDA(cudaMemcpyAsync(out_pos, wide, so.S * sizeof(uint64_t),
+                SKY_CUDA(cudaMemcpyAsync(out_pos, so.d_pos64, so.S * sizeof(uint64_t),
                                          cudaMemcpyDeviceToHost, c.stream));
                 copy_den();
             }

@@ -249,6 +249,7 @@ struct SkylineOut {
     uint32_t* d_inpos = nullptr;
     int64_t* d_ids = nullptr;
     double* d_skyv = nullptr;  // SoA [d][S]
+    uint64_t* d_pos64 = nullptr;  // the input positions widened to u64 (the output format)
     bool aborted = false;      // kSkyAbortIfLarge: the first round asked for the rank grid
 };
 

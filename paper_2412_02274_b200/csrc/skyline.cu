@@ -1298,12 +1298,13 @@ template <int D>
 __global__ void k_emit_skyline(const uint32_t* __restrict__ K, uint64_t S,
                                const double* __restrict__ v, int d,
                                const int64_t* __restrict__ ids, int64_t* __restrict__ oid,
-                               double* __restrict__ skyv) {
+                               double* __restrict__ skyv, uint64_t* __restrict__ pos64) {
     pdl_wait();
     for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < S;
          k += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t p = K[k];
         if (ids) oid[k] = ids[p];
+        pos64[k] = p;  // (the output's u64 positions, no separate widening pass)
         if constexpr (D > 0) {
             double t[D];
 #pragma unroll
@@ -2228,6 +2229,7 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
     out.d_inpos = K;
     out.d_ids = c.buf[B_SKYID].as<int64_t>(kc);
     out.d_skyv = c.buf[B_SKYV].as<double>(kc * d);
+    out.d_pos64 = c.buf[B_OUTPOS].as<uint64_t>(kc ? kc : 1);
     ensure_ids();
     if (kc) {
         trace_mark(c, "sky: rounds done (sync)");
@@ -2235,7 +2237,7 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
             constexpr int D = decltype(DC)::value;
             pdl_launch(k_emit_skyline<D>, grid_for(kc, kBlock), kBlock, 0, c.stream, K, kc,
                        d_vals, d, (ids_late && !ids_waited) ? nullptr : d_ids, out.d_ids,
-                       out.d_skyv);
+                       out.d_skyv, out.d_pos64);
         });
         SKY_LAUNCH_CHECK();
         note_launch(c);
