@@ -345,13 +345,14 @@ template <class W>
 void sweeps(Ctx& c, W* R, const CellGeom& geo, bool fused) {
     const int d = geo.d;
     auto single = [&](int j) {
-        pdl_launch(k_cells_or_dim<W>, grid_for(geo.rows / geo.ext[j], kBlock), kBlock, 0, c.stream, 
+        pdl_launch(k_cells_or_dim<W>, grid_for(geo.rows / geo.ext[j], kBlock), kBlock, 0, c.stream,
             R, geo.rows, geo.ext[j], geo.stride[j]);
         note_launch(c);
     };
     const uint32_t e1 = d >= 2 ? (uint32_t)geo.ext[1] : 1, e2 = d >= 3 ? (uint32_t)geo.ext[2] : 1;
     if (!fused || d < 2 || (uint64_t)e1 * e2 * sizeof(W) > 128 * 1024) {
-        pdl_launch(k_cells_or_word<W>, grid_for(geo.rows, kBlock), kBlock, 0, c.stream, R, geo.rows);
+        pdl_launch(k_cells_or_word<W>, grid_for(geo.rows, kBlock), kBlock, 0, c.stream, R,
+                   geo.rows);
         note_launch(c);
         for (int j = 1; j < d; ++j) single(j);
         return;
@@ -381,7 +382,7 @@ void sweeps(Ctx& c, W* R, const CellGeom& geo, bool fused) {
     while (j < d) {
         if (j + 1 < d && geo.ext[j] <= (uint64_t)kPairMax) {
             const uint64_t lines = geo.rows / (geo.ext[j] * geo.ext[j + 1]);
-            pdl_launch(k_cells_or_pair<W>, grid_for(lines, kBlock), kBlock, 0, c.stream, 
+            pdl_launch(k_cells_or_pair<W>, grid_for(lines, kBlock), kBlock, 0, c.stream,
                 R, geo.rows, (uint32_t)geo.ext[j], (uint32_t)geo.ext[j + 1], geo.stride[j]);
             note_launch(c);
             j += 2;
@@ -513,7 +514,7 @@ bool gres_cells_smem_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int
     uint64_t per_step = ((uint64_t)c.num_sms * 2 + G - 1) / G;
     per_step = std::max<uint64_t>(1, std::min<uint64_t>(per_step, (na + 63) / 64));
     const uint32_t per_block = (uint32_t)((na + per_step - 1) / per_step);
-    pdl_launch(k_cells_smem, dim3((unsigned)per_step, G), kSmemBlock, smem, c.stream, 
+    pdl_launch(k_cells_smem, dim3((unsigned)per_step, G), kSmemBlock, smem, c.stream,
         d_skyv, (uint32_t)S, d, g_max, maxv, act, (uint32_t)na, per_block, d_den, nullptr, 0);
     SKY_LAUNCH_CHECK();
     note_launch(c);
@@ -540,7 +541,7 @@ bool gres_cells_smem_spec(Ctx& c, const double* d_skyv, uint64_t S, int d, int c
     uint64_t per_step = ((uint64_t)c.num_sms * 2 + G - 1) / G;
     per_step = std::max<uint64_t>(1, std::min<uint64_t>(per_step, (na + 63) / 64));
     const uint32_t per_block = (uint32_t)((na + per_step - 1) / per_step);
-    pdl_launch(k_cells_smem, dim3((unsigned)per_step, G), kSmemBlock, smem, c.stream, 
+    pdl_launch(k_cells_smem, dim3((unsigned)per_step, G), kSmemBlock, smem, c.stream,
         d_skyv, (uint32_t)S, d, cap, 0.0, act, (uint32_t)na, per_block, d_den, c.d_slots,
         ealloc);
     SKY_LAUNCH_CHECK();
@@ -558,7 +559,8 @@ bool gres_cells_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_ma
     if (g_max < 2 || S == 0 || d > kMaxCellDims) return false;
     auto* colmax = c.buf[B_AMAX].as<unsigned long long>(kMaxDims);
     SKY_CUDA(cudaMemsetAsync(colmax, 0, sizeof(unsigned long long) * kMaxDims, c.stream));
-    pdl_launch(k_col_max, dim3(grid_for(S, kBlock, 296), (unsigned)d), kBlock, 0, c.stream, d_skyv, S, d,
+    pdl_launch(k_col_max, dim3(grid_for(S, kBlock, 296), (unsigned)d), kBlock, 0, c.stream, d_skyv,
+               S, d,
                                                                                     colmax);
     SKY_LAUNCH_CHECK();
     note_launch(c);
@@ -583,10 +585,10 @@ bool gres_cells_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_ma
     if (d <= 8 && S * (uint64_t)G * cwb <= (16ull << 30)) {
         codes = c.buf[B_CODES].get(S * (uint64_t)G * cwb);
         if (cw32)
-            pdl_launch(k_cells_codes<uint32_t>, grid_for(S, kBlock), kBlock, 0, c.stream, 
+            pdl_launch(k_cells_codes<uint32_t>, grid_for(S, kBlock), kBlock, 0, c.stream,
                 d_skyv, S, d, g_max, G, (uint32_t*)codes);
         else
-            pdl_launch(k_cells_codes<unsigned long long>, grid_for(S, kBlock), kBlock, 0, c.stream, 
+            pdl_launch(k_cells_codes<unsigned long long>, grid_for(S, kBlock), kBlock, 0, c.stream,
                 d_skyv, S, d, g_max, G, (unsigned long long*)codes);
         SKY_LAUNCH_CHECK();
         note_launch(c);
@@ -608,7 +610,7 @@ bool gres_cells_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_ma
             pdl_launch(k_cells_mark_c<WR, CW>, gs, kBlock, 0, c.stream, cg, S, geo, R);
             sweeps<WR>(c, R, geo, fused);
             reset_counts(c);
-            pdl_launch(k_cells_query_c<WR, CW>, grid_for(na, kBlock), kBlock, 0, c.stream, 
+            pdl_launch(k_cells_query_c<WR, CW>, grid_for(na, kBlock), kBlock, 0, c.stream,
                 cg, geo, R, act, na, d_den, c.d_slots + S_C3);
         };
         const uint64_t coff = (uint64_t)(g_max - g) * S;
@@ -622,17 +624,18 @@ bool gres_cells_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_ma
             run_codes(static_cast<unsigned*>(rows), (const unsigned long long*)codes + coff);
         else if (w64) {
             auto* R = static_cast<unsigned long long*>(rows);
-            pdl_launch(k_cells_mark<unsigned long long>, gs, kBlock, 0, c.stream, d_skyv, S, geo, R);
+            pdl_launch(k_cells_mark<unsigned long long>, gs, kBlock, 0, c.stream, d_skyv, S, geo,
+                       R);
             sweeps<unsigned long long>(c, R, geo, fused);
             reset_counts(c);
-            pdl_launch(k_cells_query<unsigned long long>, grid_for(na, kBlock), kBlock, 0, c.stream, 
+            pdl_launch(k_cells_query<unsigned long long>, grid_for(na, kBlock), kBlock, 0, c.stream,
                 d_skyv, S, geo, R, act, na, d_den, c.d_slots + S_C3);
         } else {
             auto* R = static_cast<unsigned*>(rows);
             pdl_launch(k_cells_mark<unsigned>, gs, kBlock, 0, c.stream, d_skyv, S, geo, R);
             sweeps<unsigned>(c, R, geo, fused);
             reset_counts(c);
-            pdl_launch(k_cells_query<unsigned>, grid_for(na, kBlock), kBlock, 0, c.stream, 
+            pdl_launch(k_cells_query<unsigned>, grid_for(na, kBlock), kBlock, 0, c.stream,
                 d_skyv, S, geo, R, act, na, d_den, c.d_slots + S_C3);
         }
         SKY_LAUNCH_CHECK();

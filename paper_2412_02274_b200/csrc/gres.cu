@@ -610,10 +610,12 @@ void launch_gap_witness(Ctx& c, const double* d_soa, uint64_t S, int d, int cap,
         const uint64_t want = S <= 4096 ? 1 : (S + 1023) / 1024;
         const unsigned bx = (unsigned)std::max<uint64_t>(
             1, std::min<uint64_t>(want, (uint64_t)c.num_sms * 8 / (uint64_t)d + 1));
-        pdl_launch(k_gap_witness_smem, dim3(bx, (unsigned)d), 256, 0, c.stream, d_soa, S, cap, c.d_slots);
+        pdl_launch(k_gap_witness_smem, dim3(bx, (unsigned)d), 256, 0, c.stream, d_soa, S, cap,
+                   c.d_slots);
     } else {
         SKY_CUDA(cudaMemsetAsync(table, 0, sizeof(unsigned long long) * d * 2 * cap, c.stream));
-        pdl_launch(k_gap_witness, grid_for(S * d, kBlock), kBlock, 0, c.stream, d_soa, S, d, cap, table,
+        pdl_launch(k_gap_witness, grid_for(S * d, kBlock), kBlock, 0, c.stream, d_soa, S, d, cap,
+                   table,
                                                                          c.d_slots);
     }
     SKY_LAUNCH_CHECK();
@@ -706,7 +708,7 @@ GresOut gres_device(Ctx& c, const double* d_skyv, const int64_t* d_ids, uint64_t
         unsigned long long* table = c.buf[B_CELLS].as<unsigned long long>(ntab);
         uint32_t* act = c.buf[B_ACT0].as<uint32_t>(S);
         trace_mark(c, "gres: start (speculative)");
-        pdl_launch(k_gres_spec_init, grid_for(S > ntab ? S : ntab, kBlock), kBlock, 0, c.stream, 
+        pdl_launch(k_gres_spec_init, grid_for(S > ntab ? S : ntab, kBlock), kBlock, 0, c.stream,
             c.d_slots, table, ntab, d_den, S, act);
         SKY_LAUNCH_CHECK();
         note_launch(c);
@@ -738,7 +740,7 @@ GresOut gres_device(Ctx& c, const double* d_skyv, const int64_t* d_ids, uint64_t
         dispatch_d(d, [&](auto DC) {
             constexpr int D = decltype(DC)::value;
             const size_t smem = sizeof(double) * (D > 0 ? 256 : 128) * (D > 0 ? D : d);
-            pdl_launch(k_check_skyline<D>, grid_for(S, kBlock, 1 << 30), kBlock, smem, c.stream, 
+            pdl_launch(k_check_skyline<D>, grid_for(S, kBlock, 1 << 30), kBlock, smem, c.stream,
                 d_skyv, S, d, c.d_slots);
         });
         SKY_LAUNCH_CHECK();
@@ -837,10 +839,11 @@ GresOut gres_device(Ctx& c, const double* d_skyv, const int64_t* d_ids, uint64_t
         void* codes = c.buf[B_CODES].get(S * (uint64_t)G * (w32 ? 4 : 8));
         const unsigned cgrid = grid_for(S * (uint64_t)G, kBlock);
         if (w32)
-            pdl_launch(k_codes_all<uint32_t>, cgrid, kBlock, 0, c.stream, d_skyv, S, d, out.g_max, G,
+            pdl_launch(k_codes_all<uint32_t>, cgrid, kBlock, 0, c.stream, d_skyv, S, d, out.g_max,
+                       G,
                                                                   (uint32_t*)codes);
         else
-            pdl_launch(k_codes_all<unsigned long long>, cgrid, kBlock, 0, c.stream, 
+            pdl_launch(k_codes_all<unsigned long long>, cgrid, kBlock, 0, c.stream,
                 d_skyv, S, d, out.g_max, G, (unsigned long long*)codes);
         SKY_LAUNCH_CHECK();
         const bool resident = S <= (1u << 21) && !getenv("SKYGPU_GRES_TILED");
@@ -863,13 +866,13 @@ GresOut gres_device(Ctx& c, const double* d_skyv, const int64_t* d_ids, uint64_t
             if (w32) {
                 SKY_CUDA(cudaFuncSetAttribute(k_gres_pairs_resident<uint32_t>,
                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-                pdl_launch(k_gres_pairs_resident<uint32_t>, grid, kBlock, smem, c.stream, 
+                pdl_launch(k_gres_pairs_resident<uint32_t>, grid, kBlock, smem, c.stream,
                     (const uint32_t*)codes, (uint32_t)S, G, out.g_max, act, (uint32_t)na,
                     (uint32_t)range, d_den, c.d_slots + S_TESTS_GRES);
             } else {
                 SKY_CUDA(cudaFuncSetAttribute(k_gres_pairs_resident<unsigned long long>,
                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-                pdl_launch(k_gres_pairs_resident<unsigned long long>, grid, kBlock, smem, c.stream, 
+                pdl_launch(k_gres_pairs_resident<unsigned long long>, grid, kBlock, smem, c.stream,
                     (const unsigned long long*)codes, (uint32_t)S, G, out.g_max, act, (uint32_t)na,
                     (uint32_t)range, d_den, c.d_slots + S_TESTS_GRES);
             }
@@ -889,11 +892,11 @@ GresOut gres_device(Ctx& c, const double* d_skyv, const int64_t* d_ids, uint64_t
             dim3 grid((unsigned)cand_tiles, (unsigned)ranges);
             SKY_CUDA(cudaEventRecord(e0, c.stream));
             if (w32)
-                pdl_launch(k_gres_pairs_tiled<uint32_t>, grid, kBlock, 0, c.stream, 
+                pdl_launch(k_gres_pairs_tiled<uint32_t>, grid, kBlock, 0, c.stream,
                     (const uint32_t*)codes, (uint32_t)S, G, out.g_max, act, (uint32_t)na,
                     (uint32_t)range, d_den, c.d_slots + S_TESTS_GRES);
             else
-                pdl_launch(k_gres_pairs_tiled<unsigned long long>, grid, kBlock, 0, c.stream, 
+                pdl_launch(k_gres_pairs_tiled<unsigned long long>, grid, kBlock, 0, c.stream,
                     (const unsigned long long*)codes, (uint32_t)S, G, out.g_max, act, (uint32_t)na,
                     (uint32_t)range, d_den, c.d_slots + S_TESTS_GRES);
         }
@@ -920,7 +923,7 @@ GresOut gres_device(Ctx& c, const double* d_skyv, const int64_t* d_ids, uint64_t
             constexpr int D = decltype(DC)::value;
             const size_t smem = sizeof(double) * (D > 0 ? 256 : 128) * (D > 0 ? D : d);
             SKY_CUDA(cudaEventRecord(e0, c.stream));
-            pdl_launch(k_gres_pairs_f64<D>, grid_for(na, kBlock, 1 << 30), kBlock, smem, c.stream, 
+            pdl_launch(k_gres_pairs_f64<D>, grid_for(na, kBlock, 1 << 30), kBlock, smem, c.stream,
                 q, (uint32_t)S, d, d_ids, act, (uint32_t)na, g, ties_possible ? 1 : 0, d_den,
                 still, c.d_slots + S_TESTS_GRES);
             SKY_CUDA(cudaEventRecord(e1, c.stream));

@@ -540,7 +540,8 @@ __global__ void k_grid_keep(const double* __restrict__ v, uint64_t n, int d, int
 template <int D>
 __global__ void __launch_bounds__(1024)
 k_cell_order(const double* __restrict__ v, int d, const uint32_t* __restrict__ in, uint32_t mcap,
-             const unsigned long long* __restrict__ count, int mcell, uint32_t ncells, const unsigned long long* __restrict__ amax,
+             const unsigned long long* __restrict__ count, int mcell, uint32_t ncells,
+             const unsigned long long* __restrict__ amax,
              uint32_t* __restrict__ out, uint32_t* __restrict__ out_cell,
              uint32_t* __restrict__ seg) {
     pdl_wait();
@@ -1532,7 +1533,8 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
         ids_waited = true;
         issue_late_ids(c);  // (if K5 never ran)
         SKY_CUDA(cudaStreamWaitEvent(c.stream, c.ids_ready, 0));
-        pdl_launch(k_ids_check, grid_for(n, kBlock), kBlock, 0, c.stream, d_ids, n, c.d_slots, S_IDSBAD);
+        pdl_launch(k_ids_check, grid_for(n, kBlock), kBlock, 0, c.stream, d_ids, n, c.d_slots,
+                   S_IDSBAD);
         SKY_LAUNCH_CHECK();
         note_launch(c);
     };
@@ -1576,7 +1578,8 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
         note_launch(c, 1);
     }
     if (plan.strategy == SKYGPU_GRID) {
-        pdl_launch(k_grid_range, grid_for(n * d, kBlock), kBlock, 0, c.stream, d_vals, n * d, c.d_slots);
+        pdl_launch(k_grid_range, grid_for(n * d, kBlock), kBlock, 0, c.stream, d_vals, n * d,
+                   c.d_slots);
         SKY_LAUNCH_CHECK();
         note_launch(c);
     }
@@ -1606,7 +1609,7 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
             SKY_LAUNCH_CHECK();
             uint32_t stride = 1;
             for (int k = 0; k < d; ++k, stride *= (uint32_t)m) {
-                pdl_launch(k_prefix_or_dim, grid_for(grid_cells / m, kBlock), kBlock, 0, c.stream, 
+                pdl_launch(k_prefix_or_dim, grid_for(grid_cells / m, kBlock), kBlock, 0, c.stream,
                     occ, (uint32_t)grid_cells, m, stride);
                 SKY_LAUNCH_CHECK();
             }
@@ -1762,10 +1765,12 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
                 // parameters from the slots; a final round has no threshold)
                 const unsigned long long* ps = mdev ? c.d_slots : nullptr;
                 const int use_thr = final_round ? 0 : 1;
-                pdl_launch(k_bucket_order, 1, 1024, 0, c.stream, Pfull, (uint32_t)m, keys, gmin, shift, Pb,
+                pdl_launch(k_bucket_order, 1, 1024, 0, c.stream, Pfull, (uint32_t)m, keys, gmin,
+                           shift, Pb,
                                                          bst, mdev, ps, use_thr);
                 SKY_LAUNCH_CHECK();
-                pdl_launch(k_bucket_rank, grid_for(m, kBlock), kBlock, 0, c.stream, Pb, (uint32_t)m, keys,
+                pdl_launch(k_bucket_rank, grid_for(m, kBlock), kBlock, 0, c.stream, Pb, (uint32_t)m,
+                           keys,
                                                                              tie_ids, gmin, shift, bst,
                                                                              Ps, mdev, ps, use_thr);
                 SKY_LAUNCH_CHECK();
@@ -1778,10 +1783,10 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
             dispatch_d(d, [&](auto DC) {
                 constexpr int D = decltype(DC)::value;
                 if constexpr (D > 0)
-                    pdl_launch(k_gather_q<D>, grid_for(m, kBlock), kBlock, 0, c.stream, 
+                    pdl_launch(k_gather_q<D>, grid_for(m, kBlock), kBlock, 0, c.stream,
                         d_vals, order, m, mdev, amax, Av, Aq);
                 else
-                    pdl_launch(k_gather_aos, grid_for(m * d, kBlock), kBlock, 0, c.stream, 
+                    pdl_launch(k_gather_aos, grid_for(m * d, kBlock), kBlock, 0, c.stream,
                         d_vals, d, order, m, nullptr, Av);
             });
             SKY_LAUNCH_CHECK();
@@ -1820,13 +1825,14 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
                 }
                 if constexpr (D > 0) {
                     if (intra_chunked)
-                        pdl_launch(k_sfs_intra_chunked<D>, c.num_sms * 8, kBlock, 0, c.stream, 
+                        pdl_launch(k_sfs_intra_chunked<D>, c.num_sms * 8, kBlock, 0, c.stream,
                             Av, Aq, (uint32_t)m, keep, c.d_slots + S_TESTS_SKY, (uint32_t)m, mdev);
                     else
-                        pdl_launch(k_sfs_intra_q<D>, grid, kBlock, 0, c.stream, Av, Aq, (uint32_t)m, keep,
+                        pdl_launch(k_sfs_intra_q<D>, grid, kBlock, 0, c.stream, Av, Aq, (uint32_t)m,
+                                   keep,
                                                                         c.d_slots + S_TESTS_SKY);
                 } else
-                    pdl_launch(k_sfs_intra_sorted<D>, grid, kBlock, 0, c.stream, 
+                    pdl_launch(k_sfs_intra_sorted<D>, grid, kBlock, 0, c.stream,
                         Av, (uint32_t)m, d, keep, c.d_slots + S_TESTS_SKY);
             });
             SKY_CUDA(cudaEventRecord(k1, c.stream));
@@ -1835,7 +1841,7 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
             trace_mark(c, "sky: K4 intra kernel");
             // A' in (sum, id) order appended to K; its count lands in S_C2
             if (mdev) {  // final: count in S_SEL2, after the round's A' (S_C2)
-                pdl_launch(k_cta_select, 1, 1024, 0, c.stream, 
+                pdl_launch(k_cta_select, 1, 1024, 0, c.stream,
                     order, nullptr, keep, (uint32_t)m, K + kc, nullptr,
                     c.d_slots + (final_round ? S_SEL2 : S_C2), mdev,
                     final_round ? c.d_slots + S_C2 : nullptr);
@@ -1844,7 +1850,8 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
                 return false;
             }
             if (m <= kCTACap) {
-                pdl_launch(k_cta_select, 1, 1024, 0, c.stream, order, nullptr, keep, (uint32_t)m, K + kc,
+                pdl_launch(k_cta_select, 1, 1024, 0, c.stream, order, nullptr, keep, (uint32_t)m,
+                           K + kc,
                            nullptr, c.d_slots + S_C2, nullptr, nullptr);
                 SKY_LAUNCH_CHECK();
                 note_launch(c);
@@ -1904,7 +1911,8 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
                 for (int j = 0; j < d; ++j) ncells *= (uint32_t)k;
                 mcell = (kCellQuantile << 16) | k;
                 double* bounds = c.buf[B_PROJ].as<double>(kMaxDims * kQMaxBins);
-                pdl_launch(k_qgrid_bounds, d, 1024, 0, c.stream, d_vals, d, alist, c.d_slots + S_C2, k,
+                pdl_launch(k_qgrid_bounds, d, 1024, 0, c.stream, d_vals, d, alist, c.d_slots + S_C2,
+                           k,
                                                          bounds);
                 SKY_LAUNCH_CHECK();
                 SKY_CUDA(cudaMemcpyToSymbolAsync(c_qbounds, bounds,
@@ -1936,10 +1944,10 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
         dispatch_d(d, [&](auto DC) {
             constexpr int D = decltype(DC)::value;
             if constexpr (D > 0)
-                pdl_launch(k_gather_q<D>, grid_for(m, kBlock), kBlock, 0, c.stream, 
+                pdl_launch(k_gather_q<D>, grid_for(m, kBlock), kBlock, 0, c.stream,
                     d_vals, psrc, m, c.d_slots + S_C2, scale, Pv, Pq);
             else
-                pdl_launch(k_gather_aos, grid_for(m * d, kBlock), kBlock, 0, c.stream, 
+                pdl_launch(k_gather_aos, grid_for(m * d, kBlock), kBlock, 0, c.stream,
                     d_vals, d, psrc, m, c.d_slots + S_C2, Pv);
         });
         SKY_LAUNCH_CHECK();
@@ -1968,12 +1976,12 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
             constexpr int D = decltype(DC)::value;
             const unsigned grid = (unsigned)((wf * 32 + kBlock - 1) / kBlock);
             if constexpr (D > 0)
-                pdl_launch(k_sfs_filter_q<D>, grid, kBlock, 0, c.stream, 
+                pdl_launch(k_sfs_filter_q<D>, grid, kBlock, 0, c.stream,
                     d_vals, keys, Rl, (uint32_t)rl, A.Pv, A.Pq, (uint32_t)A.m, A.seg, A.mcell,
                     A.qk, scale, c.d_slots, fkeep, c.d_slots + S_TESTS_SKY, bsf,
                     seeded ? A.psrc : nullptr, tie_ids, solo);
             else
-                pdl_launch(k_sfs_filter_cells<D>, grid, kBlock, 0, c.stream, 
+                pdl_launch(k_sfs_filter_cells<D>, grid, kBlock, 0, c.stream,
                     d_vals, d, keys, Rl, (uint32_t)rl, A.Pv, (uint32_t)A.m, A.seg, A.mcell,
                     c.d_slots, fkeep, c.d_slots + S_TESTS_SKY, bsf);
         });
@@ -2034,12 +2042,13 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
             if (ch > 0) SKY_CUDA(cudaStreamWaitEvent(c.stream, feed->ready[ch], 0));
             dispatch_d(d, [&](auto DC) {
                 constexpr int D = decltype(DC)::value;
-                pdl_launch(k_score<D>, grid_for(hi - lo, kBlock, c.num_sms * 8), kBlock, 0, c.stream, 
+                pdl_launch(k_score<D>, grid_for(hi - lo, kBlock, c.num_sms * 8), kBlock, 0,
+                           c.stream,
                     d_vals + lo * d, hi - lo, d, keys + lo, c.d_slots, amax, lo, nullptr, nullptr);
             });
             if (!ids_late) {  // (late ids: checked whole, once they are in)
                 const uint64_t c0 = ch ? lo - 1 : 0;  // pair (lo-1, lo) spans the boundary
-                pdl_launch(k_ids_check, grid_for(hi - c0, kBlock), kBlock, 0, c.stream, 
+                pdl_launch(k_ids_check, grid_for(hi - c0, kBlock), kBlock, 0, c.stream,
                     d_ids + c0, hi - c0, c.d_slots, (int)S_FLAG);
                 note_launch(c);
             }

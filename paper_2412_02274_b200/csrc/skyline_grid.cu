@@ -512,7 +512,7 @@ void sky_grid_decide(Ctx& c, const double* d_vals, int d, const unsigned long lo
         W* scode = c.buf[B_GSCODE].as<W>(r);
         uint32_t* sidx = c.buf[B_GSIDX].as<uint32_t>(r);
         uint2* items = c.buf[B_GITEMS].as<uint2>(r / kItem + g.rows + 1);
-        pdl_launch(k_rank_codes<D>, grid_for(r, kGB, c.num_sms * 8), kGB, 0, c.stream, 
+        pdl_launch(k_rank_codes<D>, grid_for(r, kGB, c.num_sms * 8), kGB, 0, c.stream,
             d_vals, R, (uint32_t)r, bounds, g.k0, g.k, code, cell, count);
         SKY_LAUNCH_CHECK();
         size_t tmp = 0;
@@ -521,10 +521,12 @@ void sky_grid_decide(Ctx& c, const double* d_vals, int d, const unsigned long lo
         void* t = c.buf[B_CUB].get(tmp);
         SKY_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, count, seg, (int)ncells + 1, c.stream));
         SKY_CUDA(cudaMemsetAsync(count, 0, sizeof(uint32_t) * ncells, c.stream));  // cursors
-        pdl_launch(k_cell_scatter<W>, grid_for(r, kGB), kGB, 0, c.stream, code, cell, (uint32_t)r, seg,
+        pdl_launch(k_cell_scatter<W>, grid_for(r, kGB), kGB, 0, c.stream, code, cell, (uint32_t)r,
+                   seg,
                                                                   count, scode, sidx);
         SKY_LAUNCH_CHECK();
-        pdl_launch(k_row_items, grid_for(g.rows, kGB), kGB, 0, c.stream, seg, g.rows, g.k0, items, ctr,
+        pdl_launch(k_row_items, grid_for(g.rows, kGB), kGB, 0, c.stream, seg, g.rows, g.k0, items,
+                   ctr,
                                                                  shard_rank, shard_world);
         SKY_LAUNCH_CHECK();
         note_launch(c, 5);
@@ -534,7 +536,7 @@ void sky_grid_decide(Ctx& c, const double* d_vals, int d, const unsigned long lo
         per_sm = std::max(1, per_sm);
         SKY_CUDA(cudaEventRecord(c.ev[14], c.stream));
         issue_late_ids(c);  // (deferred host ids: their copy overlaps K6)
-        pdl_launch(k_grid_decide<D>, c.num_sms * per_sm, kGB, 0, c.stream, 
+        pdl_launch(k_grid_decide<D>, c.num_sms * per_sm, kGB, 0, c.stream,
             d_vals, keys, d_ids, R, scode, sidx, seg, items, ctr, g.k0, g.k, keep,
             c.d_slots + S_TESTS_SKY);
         SKY_LAUNCH_CHECK();
