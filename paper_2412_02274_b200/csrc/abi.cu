@@ -213,6 +213,7 @@ void begin_stats(Ctx& c, skygpu_stats* st) {
     c.st = st ? st : &g_scratch_stats;
     memset(c.st, 0, sizeof(skygpu_stats));
     c.launches = 0;
+    c.chist_zeroed = false;  // (zeroed once per call: an earlier call may have thrown mid-round)
     c.gres_timing_pending = false;
     g_nspans = 0;
     c.ntrace = 0;

@@ -584,6 +584,58 @@ k_cell_order(const double* __restrict__ v, int d, const uint32_t* __restrict__ i
     }
 }
 
+// The same regrouping over many CTAs (A' of a few thousand tuples: one CTA
+// walking it serially was a latency chain): cell ids + a global histogram,
+// one CTA's exclusive scan into the segment table (and the scatter cursors),
+// an atomic scatter.  The order inside a cell is immaterial (K5's scan order
+// only), so the scatter needs no stability.
+template <int D>
+__global__ void k_cell_hist(const double* __restrict__ v, int d, const uint32_t* __restrict__ in,
+                            uint32_t mcap, const unsigned long long* __restrict__ count,
+                            int mcell, const unsigned long long* __restrict__ amax,
+                            uint32_t* __restrict__ cell_of, uint32_t* __restrict__ hist) {
+    pdl_wait();
+    constexpr int DM = D > 0 ? D : kMaxDims;
+    const int dd = D > 0 ? D : d;
+    const uint32_t m = count ? min((uint32_t)*count, mcap) : mcap;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+        double t[DM];
+        const uint64_t p = in[i];
+#pragma unroll
+        for (int k = 0; k < DM; ++k)
+            if (k < dd) t[k] = v[p * dd + k];
+        const uint32_t cl = plan_cell<DM>(t, dd, mcell, amax);
+        cell_of[i] = cl;
+        atomicAdd(&hist[cl], 1u);
+    }
+}
+
+__global__ void __launch_bounds__(1024)
+k_cell_seg(uint32_t* __restrict__ hist, uint32_t ncells, const unsigned long long* __restrict__ count,
+           uint32_t mcap, uint32_t* __restrict__ seg, uint32_t* __restrict__ cursor) {
+    pdl_wait();
+    __shared__ uint32_t cnt[kMaxCells];
+    for (uint32_t c = threadIdx.x; c < kMaxCells; c += 1024) cnt[c] = c < ncells ? hist[c] : 0u;
+    __syncthreads();
+    block_exclusive_scan_4096(cnt);
+    for (uint32_t c = threadIdx.x; c < ncells; c += 1024) {
+        seg[c] = cnt[c];
+        cursor[c] = cnt[c];
+        hist[c] = 0;  // (ready for the next round)
+    }
+    if (threadIdx.x == 0) seg[ncells] = count ? min((uint32_t)*count, mcap) : mcap;
+}
+
+__global__ void k_cell_scatter_a(const uint32_t* __restrict__ in, uint32_t mcap,
+                                 const unsigned long long* __restrict__ count,
+                                 const uint32_t* __restrict__ cell_of, uint32_t* __restrict__ cursor,
+                                 uint32_t* __restrict__ out) {
+    pdl_wait();
+    const uint32_t m = count ? min((uint32_t)*count, mcap) : mcap;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
+        out[atomicAdd(&cursor[cell_of[i]], 1u)] = in[i];
+}
+
 // compact SoA copy [d][cap] of the tuples list[0..m) from the AoS input; the
 // count is read from device memory when `count` is given (no host sync)
 __global__ void k_gather_aos(const double* __restrict__ v, int d, const uint32_t* __restrict__ list,
@@ -1927,16 +1979,42 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
         if (ncells > 1) {
             uint32_t* Alist = c.buf[B_GTMP1].as<uint32_t>(m);
             uint32_t* Akey = c.buf[B_GTMP0].as<uint32_t>(m);
-            dispatch_d(d, [&](auto DC) {
-                constexpr int D = decltype(DC)::value;
-                pdl_launch(k_cell_order<D>, 1, 1024, 0, c.stream, d_vals, d, alist, (uint32_t)m,
-                                                          c.d_slots + S_C2, mcell, ncells,
-                                                          qpre ? scale : nullptr, Alist, Akey,
-                                                          seg_table);
-            });
+            static const bool one_cta = [] {  // SKYGPU_CELL_ORDER=1: the one-CTA kernel
+                const char* e = getenv("SKYGPU_CELL_ORDER");
+                return e && e[0] == '1';
+            }();
+            if (one_cta) {
+                dispatch_d(d, [&](auto DC) {
+                    constexpr int D = decltype(DC)::value;
+                    pdl_launch(k_cell_order<D>, 1, 1024, 0, c.stream, d_vals, d, alist,
+                               (uint32_t)m, c.d_slots + S_C2, mcell, ncells,
+                               qpre ? scale : nullptr, Alist, Akey, seg_table);
+                });
+                note_launch(c, 1);
+            } else {
+                // the histogram is zeroed once per call, then kept zeroed
+                // between rounds by k_cell_seg
+                uint32_t* hist = c.buf[B_CHIST].as<uint32_t>(kMaxCells);
+                uint32_t* curs = c.buf[B_CCUR].as<uint32_t>(kMaxCells);
+                if (!c.chist_zeroed) {
+                    SKY_CUDA(cudaMemsetAsync(hist, 0, kMaxCells * sizeof(uint32_t), c.stream));
+                    c.chist_zeroed = true;
+                }
+                const unsigned gm = grid_for(m, kBlock);
+                dispatch_d(d, [&](auto DC) {
+                    constexpr int D = decltype(DC)::value;
+                    pdl_launch(k_cell_hist<D>, gm, kBlock, 0, c.stream, d_vals, d, alist,
+                               (uint32_t)m, c.d_slots + S_C2, mcell, qpre ? scale : nullptr,
+                               Akey, hist);
+                });
+                pdl_launch(k_cell_seg, 1, 1024, 0, c.stream, hist, ncells, c.d_slots + S_C2,
+                           (uint32_t)m, seg_table, curs);
+                pdl_launch(k_cell_scatter_a, gm, kBlock, 0, c.stream, alist, (uint32_t)m,
+                           c.d_slots + S_C2, Akey, curs, Alist);
+                note_launch(c, 3);
+            }
             SKY_LAUNCH_CHECK();
             seg = seg_table;
-            note_launch(c, 1);
             psrc = Alist;
         }
         double* Pv = c.buf[B_CSUM].as<double>(m * d);

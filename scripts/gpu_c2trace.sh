@@ -1,1 +1,2 @@
-SKYGPU_TRACE=1 timeout 300 python bench.py --steps 2 --warmup 3 --workload C2 --no-cpu-baseline > gpurun_out/trc2_dev.log 2>&1
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pt_all.log 2>&1; echo "pt rc=$?"
+WS="C2 C4 C1" bash scripts/gpu_ab2.sh
