@@ -1,13 +1,17 @@
 #!/usr/bin/env python
 """Benchmark of the grid-resistance hot path (skyline + descending-g scan).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C5]
                     [--impl ours|reference] [--scaling weak|strong]
 
 One STEP = one pass of the hot path over one seeded synthetic relation:
 parallel_skyline of the n tuples, then grid_resistance of every skyline tuple
-(proj/src/harness.cpp:208, :229-231).  Default workload C2 (BASELINE.json
-configs[1]: anti-correlated n=1,000,000, d=3, seed 1, cap 25, angular p=16).
+(proj/src/harness.cpp:208, :229-231).  Default workload C5, the LARGEST
+BASELINE.json configuration that fits one GPU (configs[4]: anti-correlated
+n=10,000,000, d=7, seed 1, cap 25, angular p=64; 560 MB of float64).
+--gpus N without torchrun's WORLD_SIZE re-launches itself under
+torch.distributed.run with N ranks (127.0.0.1); N > 1 defaults to strong
+scaling (one C5 instance sharded over the ranks).
 
 value  = skyline tuples whose resistance was computed per second, whole job,
          inputs resident in HBM (device-event timed, max over ranks).
@@ -46,9 +50,15 @@ WORKLOADS = {
     "C5p20k": ("ant", 20_000, 7, 1, "angular", 64, 25),
     "C5": ("ant", 10_000_000, 7, 1, "angular", 64, 25),
 }
-# the CPU reference cannot finish these in a bench run (C5: days); it is timed
-# on the leading prefix of the same seeded stream instead, and says so
-CPU_SAMPLE_N = {"C5": 10_000}
+# the CPU reference cannot finish these in a bench run (C5: days; its SFS merge
+# is quadratic in the skyline, S ~ 0.65 n); it is timed on the leading prefix
+# of the same seeded stream instead (the generator is per-tuple sequential, so
+# a prefix IS the first tuples of the full relation), and the line says so
+CPU_SAMPLE_N = {"C5": 20_000}
+# timed repetitions of the reference arm when one sampled step is long (the
+# C5 20k prefix is ~20-40 s of CPU per step): the arm stays within minutes
+REF_MAX_STEPS = {"C5": 4}
+DEFAULT_WORKLOAD = "C5"
 METRIC = "grid-resistance skyline tuples/sec"
 UNIT = "skyline tuples/s"
 
@@ -99,8 +109,9 @@ def run_reference_cpu(wl, repeat, cores=0):
 def sample_text(wl, r, repeat):
     n_full = WORKLOADS[wl][1]
     if r.get("n", n_full) != n_full:
-        return (f"leading {r['n']} tuples of the {wl} stream x{repeat} (the full n={n_full} "
-                f"is not computable by the CPU reference within a bench run)")
+        return (f"leading {r['n']}-tuple prefix of the {wl} stream (same seed; the generator is "
+                f"per-tuple sequential) x{repeat}: the full n={n_full} is not computable by the "
+                f"CPU reference within a bench run (its SFS merge is quadratic in the skyline)")
     return f"full {wl} workload x{repeat}"
 
 
@@ -109,21 +120,27 @@ def reference_arm(args):
     if rank != 0:
         return 0
     wl = args.workload
-    # warm-up runs are discarded; K timed runs (one step = one full pass)
+    # warm-up runs are discarded (one is enough on a CPU); K timed runs (one
+    # step = one full pass over the sample), at most REF_MAX_STEPS[wl]
+    steps = max(1, min(args.steps, REF_MAX_STEPS.get(wl, args.steps)))
     if args.warmup:
         run_reference_cpu(wl, 1)
-    r = run_reference_cpu(wl, max(1, args.steps))
+    r = run_reference_cpu(wl, steps)
     value = r["S"] / (r["step_ms"] / 1e3)
     gen, n, d, seed, strat, p, cap = WORKLOADS[wl]
+    sampled = r["n"] != n
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["step_ms"],
+        "steps_timed": steps,
         "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference generator, seeded)",
-        "config": {"workload": f"{wl}: {gen} n={n} d={d} seed={seed}, {strat} p={p}, cap={cap}",
+        "config": {"workload": f"{wl}: {gen} n={n} d={d} seed={seed}, {strat} p={p}, cap={cap}"
+                               + (f" [reference timed on the leading {r['n']}-tuple prefix]"
+                                  if sampled else ""),
                    "cores": r["cores"], "cpu": cpu_model()},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": r["cores"], "kind": r["kind"],
-                         "sample": sample_text(wl, r, args.steps)},
+                         "sample": sample_text(wl, r, steps)},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "reference_detail": r["detail"],
     }
@@ -329,10 +346,12 @@ def our_arm(args):
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            r = run_reference_cpu(args.workload, args.cpu_repeat)
+            # ~10-30 s of CPU work: one pass over the C5 prefix, 3 elsewhere
+            rep = args.cpu_repeat or (1 if args.workload == "C5" else 3)
+            r = run_reference_cpu(args.workload, rep)
             line["cpu_baseline"] = {"value": r["S"] / (r["step_ms"] / 1e3), "unit": UNIT,
                                     "cores": r["cores"], "kind": r["kind"],
-                                    "sample": sample_text(args.workload, r, args.cpu_repeat)
+                                    "sample": sample_text(args.workload, r, rep)
                                               + f" ({r['step_ms']:.1f} ms/step, {cpu_model()})"}
         except Exception as e:  # pragma: no cover
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "port",
@@ -449,23 +468,43 @@ def roofline(st, sky_ms, gres_ms, d, clk, workload="C2"):
     return r
 
 
+def spawn_ranks(n):
+    """bench.py --gpus N run without torchrun: re-launch under
+    torch.distributed.run, one rank per GPU, rendezvous on 127.0.0.1; rank 0's
+    JSON line is relayed as this process's output."""
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="C2", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--scaling", default=None, choices=["weak", "strong"],
+                    help="default: strong for N > 1 (one instance sharded over the ranks)")
     ap.add_argument("--engine", type=int, default=0, help="gres engine: 0 auto, 1 pairs, 2 cells")
     ap.add_argument("--sky-engine", default="auto", choices=["auto", "rounds", "grid"],
                     help="skyline engine (default: chosen after the first prefix round)")
     ap.add_argument("--strategy", default=None, choices=["none", "grid", "angular", "sliced"],
                     help="override the workload's partitioning plan (both arms)")
     ap.add_argument("--partitions", type=int, default=None, help="override the target partitions")
-    ap.add_argument("--cpu-repeat", type=int, default=3)
+    ap.add_argument("--cpu-repeat", type=int, default=0, help="0: 1 for C5, else 3")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.scaling is None:
+        args.scaling = "strong" if args.gpus > 1 else "weak"
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args.gpus)
     if args.strategy or args.partitions:
         gen, n, d, seed, strat, p, cap = WORKLOADS[args.workload]
         WORKLOADS[args.workload] = (gen, n, d, seed, args.strategy or strat, args.partitions or p, cap)

@@ -165,20 +165,13 @@ __global__ void k_check_values(const double* __restrict__ v, uint64_t total,
 
 // Event span on the call's stream; stop() only records — the elapsed time
 // is resolved by end_stats after the call's single final synchronisation.
-struct PendingSpan {
-    int a;
-    double* dst;
-};
-PendingSpan g_spans[8];
-int g_nspans = 0;
-
 struct Timer {
     Ctx& c;
     int a;
     Timer(Ctx& cc, int ea) : c(cc), a(ea) { SKY_CUDA(cudaEventRecord(c.ev[a], c.stream)); }
     void stop(double* dst) {
         SKY_CUDA(cudaEventRecord(c.ev[a + 1], c.stream));
-        if (g_nspans < 8) g_spans[g_nspans++] = PendingSpan{a, dst};
+        if (c.nspans < 8) c.spans[c.nspans++] = Ctx::Span{a, dst};
     }
 };
 
@@ -207,15 +200,18 @@ int guarded(char* err, size_t errlen, F&& f) {
     }
 }
 
-skygpu_stats g_scratch_stats;
-
 void begin_stats(Ctx& c, skygpu_stats* st) {
-    c.st = st ? st : &g_scratch_stats;
+    c.st = st ? st : &c.scratch_stats;
     memset(c.st, 0, sizeof(skygpu_stats));
     c.launches = 0;
-    c.chist_zeroed = false;  // (zeroed once per call: an earlier call may have thrown mid-round)
+    // per-call flags start clear: an earlier call on this device may have
+    // thrown mid-pipeline (after fetching its counters, with a speculative
+    // gres launch pending, or mid-round)
+    c.chist_zeroed = false;
+    c.counters_fetched = false;
+    c.gres_spec = false;
     c.gres_timing_pending = false;
-    g_nspans = 0;
+    c.nspans = 0;
     c.ntrace = 0;
     trace_mark(c, "begin");
     reset_tests(c);
@@ -239,12 +235,12 @@ void end_stats(Ctx& c) {
     }
     c.st->skyline_tests = c.h_slots[S_TESTS_SKY];
     c.st->gres_tests = c.h_slots[S_TESTS_GRES];
-    for (int i = 0; i < g_nspans; ++i) {
+    for (int i = 0; i < c.nspans; ++i) {
         float ms = 0;
-        SKY_CUDA(cudaEventElapsedTime(&ms, c.ev[g_spans[i].a], c.ev[g_spans[i].a + 1]));
-        *g_spans[i].dst = ms;
+        SKY_CUDA(cudaEventElapsedTime(&ms, c.ev[c.spans[i].a], c.ev[c.spans[i].a + 1]));
+        *c.spans[i].dst = ms;
     }
-    g_nspans = 0;
+    c.nspans = 0;
     if (c.gres_timing_pending) {
         float ms = 0;
         SKY_CUDA(cudaEventElapsedTime(&ms, c.ev[10], c.ev[11]));

@@ -157,6 +157,15 @@ struct Ctx {
     bool gres_spec = false;  // a speculative gres launch awaits its S_SPEC check
     bool counters_fetched = false;  // test counters already read with the outputs
     bool chist_zeroed = false;      // the A' cell histogram (B_CHIST) starts zeroed
+    // event spans of the current call, resolved by end_stats after the call's
+    // final synchronisation (per context: one host thread per device may run
+    // calls concurrently with another device's)
+    struct Span {
+        int a;
+        double* dst;
+    } spans[8];
+    int nspans = 0;
+    skygpu_stats scratch_stats;  // the call's stats when the caller passed none
     // host-pointer pipeline: the ids are still in flight (copy stream) until
     // this event; the skyline runs on the speculation that they are strictly
     // increasing (ties by position) and checks them at the end (S_IDSBAD)

@@ -74,10 +74,17 @@ def install_collective(group=None):
     from . import skypar
 
     def allreduce_max(ptr, count, elem_bytes, stream):
+        # the library's buffer lives on the library's device, not necessarily
+        # torch's current one: build the view there and refuse a copy (a copy
+        # would be reduced while the library's buffer stays partial)
+        dev = torch.device("cuda", skypar.current_device())
         t = torch.as_tensor(_DeviceBuffer(ptr, count, "|u1" if elem_bytes == 1 else "<i4"),
-                            device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
-        torch.cuda.current_stream().synchronize()  # in place before the library continues
+                            device=dev)
+        if t.data_ptr() != ptr:
+            return 1
+        with torch.cuda.device(dev):
+            dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+            torch.cuda.current_stream(dev).synchronize()  # in place before the library continues
         return 0
 
     skypar.set_collective(allreduce_max)

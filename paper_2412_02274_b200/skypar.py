@@ -303,9 +303,19 @@ def pipeline_raw(vals_ptr: int, ids_ptr: int, n: int, d: int, plan: PartitionPla
     return int(s[0]), int(gm[0]), st.as_dict()
 
 
+_DEVICE = 0  # the device the library's calls run on (set_device)
+
+
 def set_device(device: int) -> None:
+    global _DEVICE
     err = _errbuf()
     _check(lib().skygpu_set_device(int(device), err, 1024), err)
+    _DEVICE = int(device)
+
+
+def current_device() -> int:
+    """The device set with set_device (the library's buffers live there)."""
+    return _DEVICE
 
 
 def set_stream(stream_ptr: int | None) -> None:
