@@ -126,6 +126,35 @@ __global__ void k_cell_scatter(const W* __restrict__ code, const uint32_t* __res
     }
 }
 
+// the same scatter plus each tuple's exact record in cell order: its D
+// float64 values and its sum key, (D + 1) doubles at rec[pos * (D + 1)] —
+// the TMA decide kernel's exact follow-up then reads one contiguous record
+// per side instead of chasing sidx -> R -> values and keys
+template <int D>
+__global__ void k_cell_scatter_rec(const GridWord<D>* __restrict__ code,
+                                   const uint32_t* __restrict__ cell, uint32_t r,
+                                   const uint32_t* __restrict__ seg, uint32_t* __restrict__ cursor,
+                                   const double* __restrict__ v,
+                                   const unsigned long long* __restrict__ key,
+                                   const uint32_t* __restrict__ R, GridWord<D>* __restrict__ scode,
+                                   uint32_t* __restrict__ sidx, double* __restrict__ rec) {
+    pdl_wait();
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < r; i += gridDim.x * blockDim.x) {
+        const uint32_t cl = cell[i];
+        const uint32_t pos = seg[cl] + atomicAdd(&cursor[cl], 1u);
+        scode[pos] = code[i];
+        sidx[pos] = i;
+        const uint64_t p = R ? R[i] : i;
+        double x[D];
+#pragma unroll
+        for (int j = 0; j < D; ++j) x[j] = v[p * D + j];
+        double* o = rec + (uint64_t)pos * (D + 1);
+#pragma unroll
+        for (int j = 0; j < D; ++j) o[j] = x[j];
+        o[D] = __longlong_as_double((long long)key[p]);
+    }
+}
+
 // work items: (row, first sorted position) chunks of <= 128 candidates; a
 // sharded call keeps only the rows this shard owns (row % world == rank)
 __global__ void k_row_items(const uint32_t* __restrict__ seg, uint32_t nrows, int k0,
@@ -205,6 +234,33 @@ __device__ __forceinline__ bool tile_exact(const W* st, const uint32_t* sp, W tg
         if (qs != self && qs != ~0u && exact_pred<D>(v, key, ids, R, sidx, qs, qt)) return false;
     }
     return true;
+}
+
+// exact_pred over the cell-ordered records (k_cell_scatter_rec): values and
+// key from one record per side; ties of the key fall back to ids/positions
+template <int D>
+__device__ __forceinline__ bool exact_rec(const double* __restrict__ rec,
+                                          const int64_t* __restrict__ ids,
+                                          const uint32_t* __restrict__ R,
+                                          const uint32_t* __restrict__ sidx, uint32_t qs,
+                                          uint32_t qt) {
+    const double* a = rec + (uint64_t)qs * (D + 1);
+    const double* b = rec + (uint64_t)qt * (D + 1);
+    double s[D + 1], t[D + 1];
+#pragma unroll
+    for (int j = 0; j <= D; ++j) {
+        s[j] = a[j];
+        t[j] = b[j];
+    }
+    if (!dom_f64<D>(s, t)) return false;
+    const unsigned long long ks = (unsigned long long)__double_as_longlong(s[D]);
+    const unsigned long long kt = (unsigned long long)__double_as_longlong(t[D]);
+    if (ks != kt) return ks < kt;  // dominance implies ks <= kt
+    const uint32_t is = sidx[qs], it = sidx[qt];
+    const uint64_t ps = R ? R[is] : is, pt = R ? R[it] : it;
+    if (!ids) return ps < pt;  // (ids in flight: position order, checked later)
+    const int64_t is_ = ids[ps], it_ = ids[pt];
+    return is_ < it_ || (is_ == it_ && ps < pt);
 }
 
 // code-pass flags of one staged tile for the first KC candidate slots
@@ -443,6 +499,365 @@ k_grid_decide(const double* __restrict__ v, const unsigned long long* __restrict
     add_count(tests, cnt);
 }
 
+// ---------------------------------------------------------------------------
+// K6 (default): the same decision, restructured around two facts of the ALU
+// kernel above — (1) a (candidate, comparator) code test costs ~6 issued ALU
+// instructions there (3 for the test, the rest the per-lane tile walk), and
+// (2) each comparator row is fetched by per-lane loads whose L2 latency the
+// warp must hide on its own.
+//
+//  * Bitset test.  An item's 128 candidates are turned into per-attribute
+//    tables in shared memory: tab[j][r] = the 128-bit set of candidates whose
+//    rank code on attribute j is >= r (one ballot per (j, r) inside the
+//    candidates' code range).  The candidates a comparator s code-dominates
+//    are then AND_j tab[j][code_j(s)]: D 16-byte shared loads and ~3D/2 LOP3
+//    test s against all 128 candidates at once (bitmap skyline technique),
+//    instead of 128 SWAR tests.
+//  * TMA bulk staging.  Warp 0 of the CTA is a producer: it walks the same
+//    comparator ranges (own chunk, own row, then every row <= the item's
+//    row) and streams them with cp.async.bulk into a 4-stage shared-memory
+//    ring (mbarrier complete_tx); warps 1..3 consume stages.  Ranges are
+//    copied at 16-byte granularity, so up to one code on either side of a
+//    range is an extra comparator — harmless: the predecessor rule may test
+//    t against ANY tuple of R (a tuple never dominates itself).
+//  * Code passes take the exact float64 + precedence test (exact_pred), as
+//    before; a confirmed dominator clears the candidate's bit in the CTA's
+//    alive mask, and the item ends as soon as no candidate is alive.
+// ---------------------------------------------------------------------------
+constexpr int kTB = 128;          // threads: warp 0 producer, warps 1..3 consumers
+constexpr int kTCons = kTB / 32 - 1;
+constexpr int kStages = 4;
+constexpr int kStageCap = 256;    // codes per stage
+constexpr int kMaxPieces = 16;    // ranges per stage
+constexpr int kTabR = 129;        // table entries per attribute: codes 0..127, 128 = never
+constexpr int kHitCap = 128;      // batched exact follow-ups per consumer warp
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = smem_u32(bar);
+    uint32_t ok = 0;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(a), "r"(parity)
+            : "memory");
+    } while (!ok);
+}
+// global -> shared bulk copy (16-byte aligned, size a multiple of 16),
+// completion counted on `bar` in bytes
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// x / b for x < 2^24 from a float reciprocal (one correction step each way):
+// the producer's mixed-radix row walk without integer division
+__device__ __forceinline__ uint32_t div_rcp(uint32_t x, uint32_t b, float inv) {
+    uint32_t q = __float2uint_rz(__uint2float_rn(x) * inv);
+    if (q * b > x) --q;
+    if ((q + 1) * b <= x) ++q;
+    return q;
+}
+
+template <int D>
+struct alignas(16) DecideSmem {
+    using W = GridWord<D>;
+    uint4 tab[D * kTabR];                 // candidate bitsets per (attribute, code)
+    W ring[kStages][kStageCap];           // staged comparator codes
+    uint32_t pslot[kStages][kMaxPieces];  // first slot of each staged range
+    uint32_t ppos[kStages][kMaxPieces];   // its sorted position
+    uint32_t nslot[kStages], npiece[kStages], nreal[kStages], last[kStages];
+    uint64_t full[kStages], empty[kStages];
+    uint32_t alive[4];
+    uint32_t item;
+    uint2 hits[kTCons][kHitCap];          // a consumer warp's code passes, tested in parallel
+};
+
+template <int D>
+__global__ void __launch_bounds__(kTB, 8)
+k_grid_decide_tma(const double* __restrict__ rec, const int64_t* __restrict__ ids,
+                  const uint32_t* __restrict__ R,
+                  const GridWord<D>* __restrict__ scode, const uint32_t* __restrict__ sidx,
+                  const uint32_t* __restrict__ seg, const uint2* __restrict__ items,
+                  unsigned* __restrict__ ctr, int k0, int k, uint8_t* __restrict__ keep,
+                  unsigned long long* __restrict__ tests) {
+    pdl_wait();
+    using W = GridWord<D>;
+    constexpr uint32_t kAlign = 16 / sizeof(W);  // codes per 16 bytes
+    __shared__ DecideSmem<D> sm;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&sm.full[s], 1);
+            mbar_init(&sm.empty[s], kTCons);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+    const uint32_t nitems = ctr[0];
+    uint32_t wj[D];
+    wj[0] = 0;
+    if (D > 1) wj[1] = 1;
+#pragma unroll
+    for (int j = 2; j < D; ++j) wj[j] = wj[j - 1] * (uint32_t)k;
+    uint32_t ps = 0, pphase = 0;  // producer ring position (warp 0)
+    uint32_t cs = 0, cphase = 0;  // consumer ring position (warps 1..3)
+    unsigned long long cnt = 0;
+    for (;;) {
+        if (threadIdx.x == 0) sm.item = atomicAdd(&ctr[1], 1u);
+        __syncthreads();
+        const uint32_t it = sm.item;
+        if (it >= nitems) break;
+        const uint2 item = items[it];
+        const uint32_t own = item.x, first = item.y;
+        const uint32_t end = min(seg[(own + 1) * k0], first + kItem);
+        // ---- candidate bitset tables: warp w builds word w of every entry
+        {
+            const uint32_t q = first + threadIdx.x;
+            const bool valid = q < end;
+            const W cw = valid ? scode[q] : (W)0;
+            const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                const uint32_t x = (uint32_t)(cw >> (8 * j)) & 0xFFu;
+                const uint32_t lo = __reduce_min_sync(0xffffffffu, valid ? x : 255u);
+                const uint32_t hi = __reduce_max_sync(0xffffffffu, valid ? x : 0u);
+                uint32_t* T = reinterpret_cast<uint32_t*>(&sm.tab[j * kTabR]) + warp;
+                for (uint32_t r = lane; r < (uint32_t)kTabR; r += 32)
+                    if (r <= lo || r > hi) T[r * 4] = r <= lo ? vmask : 0u;
+                for (uint32_t r = lo + 1; r <= hi; ++r) {
+                    const unsigned b = __ballot_sync(0xffffffffu, valid && x >= r);
+                    if ((r & 31u) == lane) T[r * 4] = b;
+                }
+            }
+            if (lane == 0) sm.alive[warp] = vmask;
+        }
+        __syncthreads();
+        if (warp == 0) {
+            // ================= producer: walk the comparator ranges
+            uint32_t used = 0, np = 0, nr = 0;
+            bool open = false, stop = false;
+            auto all_dead = [&]() {
+                const volatile uint32_t* a = sm.alive;
+                return (a[0] | a[1] | a[2] | a[3]) == 0u;
+            };
+            auto close = [&](bool fin) {
+                if (lane == 0) {
+                    sm.nslot[ps] = used;
+                    sm.npiece[ps] = np;
+                    sm.nreal[ps] = nr;
+                    sm.last[ps] = fin ? 1u : 0u;
+                    mbar_arrive(&sm.full[ps]);
+                }
+                __syncwarp();
+                if (++ps == kStages) {
+                    ps = 0;
+                    pphase ^= 1u;
+                }
+                open = false;
+            };
+            auto emit = [&](uint32_t lo, uint32_t hi) {
+                while (lo < hi && !stop) {
+                    if (!open) {
+                        if (all_dead()) {
+                            stop = true;
+                            break;
+                        }
+                        mbar_wait(&sm.empty[ps], pphase ^ 1u);
+                        used = np = nr = 0;
+                        open = true;
+                    }
+                    const int space = kStageCap - (int)used - 2 * (int)(kAlign - 1);
+                    if (space <= 0 || np == (uint32_t)kMaxPieces) {
+                        close(false);
+                        continue;
+                    }
+                    const uint32_t take = min(hi - lo, (uint32_t)space);
+                    const uint32_t a = lo & ~(kAlign - 1);
+                    const uint32_t b = (lo + take + kAlign - 1) & ~(kAlign - 1);
+                    if (lane == 0) {
+                        const uint32_t bytes = (b - a) * (uint32_t)sizeof(W);
+                        mbar_expect_tx(&sm.full[ps], bytes);
+                        bulk_g2s(&sm.ring[ps][used], scode + a, bytes, &sm.full[ps]);
+                        sm.pslot[ps][np] = used;
+                        sm.ppos[ps][np] = a;
+                    }
+                    used += b - a;
+                    ++np;
+                    nr += take;
+                    lo += take;
+                }
+            };
+            // the chunk itself, then the own row around it
+            emit(first, end);
+            const uint32_t od0 =
+                (uint32_t)((((uint32_t)scode[end - 1] & 0xFFu) * (uint32_t)k0) >> 7);
+            emit(seg[own * k0], first);
+            emit(end, seg[own * k0 + od0 + 1]);
+            // rows <= own in every coarse attribute (mixed-radix countdown,
+            // attribute 1 fastest), 32 rows per window (one per lane)
+            uint32_t od[D], base[D];
+            float ib[D], ir[D];
+            uint32_t total = 1;
+#pragma unroll
+            for (int j = 1; j < D; ++j) {
+                od[j] = (own / wj[j]) % (uint32_t)k;
+                base[j] = total;
+                ib[j] = 1.0f / (float)total;
+                ir[j] = 1.0f / (float)(od[j] + 1);
+                total *= od[j] + 1;
+            }
+            for (uint32_t lin = 1; lin < total && !stop; lin += 32) {
+                const uint32_t p = lin + lane;
+                uint32_t wlo = 0, whi = 0;
+                if (p < total) {  // (total <= rows < 2^22: div_rcp is exact)
+                    uint32_t rw = 0;
+#pragma unroll
+                    for (int j = 1; j < D; ++j) {
+                        const uint32_t t = div_rcp(p, base[j], ib[j]);
+                        const uint32_t dj = t - div_rcp(t, od[j] + 1, ir[j]) * (od[j] + 1);
+                        rw += (od[j] - dj) * wj[j];
+                    }
+                    wlo = seg[rw * k0];
+                    whi = seg[rw * k0 + od0 + 1];
+                }
+                unsigned nz = __ballot_sync(0xffffffffu, whi > wlo);
+                while (nz && !stop) {
+                    const int f = __ffs(nz) - 1;
+                    nz &= nz - 1;
+                    emit(__shfl_sync(0xffffffffu, wlo, f), __shfl_sync(0xffffffffu, whi, f));
+                }
+            }
+            if (!open) {  // an empty stage carries the end marker
+                mbar_wait(&sm.empty[ps], pphase ^ 1u);
+                used = np = nr = 0;
+            }
+            close(true);
+        } else {
+            // ================= consumers: test staged comparators
+            const uint32_t cw = warp - 1;
+            for (;;) {
+                mbar_wait(&sm.full[cs], cphase);
+                const uint32_t n = sm.nslot[cs];
+                const bool fin = sm.last[cs] != 0u;
+                const volatile uint32_t* av = sm.alive;
+                uint32_t al[4] = {av[0], av[1], av[2], av[3]};
+                if ((al[0] | al[1] | al[2] | al[3]) != 0u) {
+                    if (cw == 0 && lane == 0)
+                        cnt += (unsigned long long)sm.nreal[cs] *
+                               (__popc(al[0]) + __popc(al[1]) + __popc(al[2]) + __popc(al[3]));
+                    uint2* hb = sm.hits[cw];
+                    for (uint32_t s0 = cw * 32; s0 < n; s0 += 32 * kTCons) {
+                        const uint32_t s = s0 + lane;
+                        uint4 m = make_uint4(0u, 0u, 0u, 0u);
+                        if (s < n) {
+                            const W c = sm.ring[cs][s];
+                            m = make_uint4(al[0], al[1], al[2], al[3]);
+#pragma unroll
+                            for (int j = 0; j < D; ++j) {
+                                const uint4 e =
+                                    sm.tab[j * kTabR + ((uint32_t)(c >> (8 * j)) & 0xFFu)];
+                                m.x &= e.x;
+                                m.y &= e.y;
+                                m.z &= e.z;
+                                m.w &= e.w;
+                            }
+                        }
+                        const bool hit = (m.x | m.y | m.z | m.w) != 0u;
+                        if (!__any_sync(0xffffffffu, hit)) continue;
+                        // code passes (rare): the exact float64 + precedence
+                        // test, the warp's (comparator, candidate) pairs
+                        // gathered and tested one per lane
+                        uint32_t qs = 0, nb = 0;
+                        if (hit) {
+                            uint32_t pi = 0;
+                            const uint32_t npc = sm.npiece[cs];
+                            while (pi + 1 < npc && sm.pslot[cs][pi + 1] <= s) ++pi;
+                            qs = sm.ppos[cs][pi] + (s - sm.pslot[cs][pi]);
+                            nb = __popc(m.x) + __popc(m.y) + __popc(m.z) + __popc(m.w);
+                        }
+                        uint32_t incl = nb;
+#pragma unroll
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                            if ((int)lane >= o) incl += y;
+                        }
+                        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+                        const uint32_t mw[4] = {m.x, m.y, m.z, m.w};
+                        if (total <= (uint32_t)kHitCap) {
+                            uint32_t at = incl - nb;
+#pragma unroll
+                            for (int w = 0; w < 4; ++w) {
+                                uint32_t b = mw[w];
+                                while (b) {
+                                    const uint32_t i = (uint32_t)__ffs(b) - 1u;
+                                    b &= b - 1;
+                                    hb[at++] = make_uint2(qs, 32u * w + i);
+                                }
+                            }
+                            __syncwarp();
+                            for (uint32_t h = lane; h < total; h += 32) {
+                                const uint2 pr = hb[h];
+                                if (exact_rec<D>(rec, ids, R, sidx, pr.x, first + pr.y))
+                                    atomicAnd(&sm.alive[pr.y >> 5], ~(1u << (pr.y & 31u)));
+                            }
+                            __syncwarp();
+                        } else {
+#pragma unroll
+                            for (int w = 0; w < 4; ++w) {
+                                uint32_t b = mw[w];
+                                while (b) {
+                                    const int i = __ffs(b) - 1;
+                                    b &= b - 1;
+                                    if (exact_rec<D>(rec, ids, R, sidx, qs,
+                                                     first + 32 * w + (uint32_t)i))
+                                        atomicAnd(&sm.alive[w], ~(1u << i));
+                                }
+                            }
+                        }
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sm.empty[cs]);
+                if (++cs == kStages) {
+                    cs = 0;
+                    cphase ^= 1u;
+                }
+                if (fin) break;
+            }
+        }
+        __syncthreads();
+        {
+            const uint32_t q = first + threadIdx.x;
+            if (q < end) keep[sidx[q]] = (uint8_t)((sm.alive[warp] >> lane) & 1u);
+        }
+    }
+    add_count(tests, cnt);
+}
+
 template <int D, class F>
 void with_d(int d, F&& f) {
     if (d == D) f(std::integral_constant<int, D>{});
@@ -509,7 +924,10 @@ void sky_grid_decide(Ctx& c, const double* d_vals, int d, const unsigned long lo
         using W = GridWord<D>;
         W* code = c.buf[B_GCODE].as<W>(r);
         uint32_t* cell = c.buf[B_GCELL].as<uint32_t>(r);
-        W* scode = c.buf[B_GSCODE].as<W>(r);
+        // (+ 16 bytes of never-passing codes: the bulk copies of the TMA
+        // decide kernel round the last range up to 16 bytes)
+        W* scode = c.buf[B_GSCODE].as<W>(r + 16 / sizeof(W));
+        SKY_CUDA(cudaMemsetAsync(scode + r, 0x80, 16, c.stream));
         uint32_t* sidx = c.buf[B_GSIDX].as<uint32_t>(r);
         uint2* items = c.buf[B_GITEMS].as<uint2>(r / kItem + g.rows + 1);
         pdl_launch(k_rank_codes<D>, grid_for(r, kGB, c.num_sms * 8), kGB, 0, c.stream,
@@ -521,9 +939,21 @@ void sky_grid_decide(Ctx& c, const double* d_vals, int d, const unsigned long lo
         void* t = c.buf[B_CUB].get(tmp);
         SKY_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, count, seg, (int)ncells + 1, c.stream));
         SKY_CUDA(cudaMemsetAsync(count, 0, sizeof(uint32_t) * ncells, c.stream));  // cursors
-        pdl_launch(k_cell_scatter<W>, grid_for(r, kGB), kGB, 0, c.stream, code, cell, (uint32_t)r,
-                   seg,
-                                                                  count, scode, sidx);
+        // K6: the TMA-staged bitset kernel (default) or the per-lane ALU
+        // kernel (SKYGPU_GRID_KERNEL=alu, kept for A/B measurement)
+        static const bool alu = [] {
+            const char* e = getenv("SKYGPU_GRID_KERNEL");
+            return e && e[0] == 'a';
+        }();
+        double* rec = nullptr;
+        if (alu) {
+            pdl_launch(k_cell_scatter<W>, grid_for(r, kGB), kGB, 0, c.stream, code, cell,
+                       (uint32_t)r, seg, count, scode, sidx);
+        } else {
+            rec = c.buf[B_GREC].as<double>(r * (D + 1));
+            pdl_launch(k_cell_scatter_rec<D>, grid_for(r, kGB), kGB, 0, c.stream, code, cell,
+                       (uint32_t)r, seg, count, d_vals, keys, R, scode, sidx, rec);
+        }
         SKY_LAUNCH_CHECK();
         pdl_launch(k_row_items, grid_for(g.rows, kGB), kGB, 0, c.stream, seg, g.rows, g.k0, items,
                    ctr,
@@ -532,13 +962,22 @@ void sky_grid_decide(Ctx& c, const double* d_vals, int d, const unsigned long lo
         note_launch(c, 5);
         trace_mark(c, "grid: codes + cells + items");
         int per_sm = 0;
-        SKY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_grid_decide<D>, kGB, 0));
+        if (alu)
+            SKY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_grid_decide<D>, kGB, 0));
+        else
+            SKY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_grid_decide_tma<D>,
+                                                                   kTB, 0));
         per_sm = std::max(1, per_sm);
         SKY_CUDA(cudaEventRecord(c.ev[14], c.stream));
         issue_late_ids(c);  // (deferred host ids: their copy overlaps K6)
-        pdl_launch(k_grid_decide<D>, c.num_sms * per_sm, kGB, 0, c.stream,
-            d_vals, keys, d_ids, R, scode, sidx, seg, items, ctr, g.k0, g.k, keep,
-            c.d_slots + S_TESTS_SKY);
+        if (alu)
+            pdl_launch(k_grid_decide<D>, c.num_sms * per_sm, kGB, 0, c.stream,
+                d_vals, keys, d_ids, R, scode, sidx, seg, items, ctr, g.k0, g.k, keep,
+                c.d_slots + S_TESTS_SKY);
+        else
+            pdl_launch(k_grid_decide_tma<D>, c.num_sms * per_sm, kTB, 0, c.stream,
+                (const double*)rec, d_ids, R, scode, sidx, seg, items, ctr, g.k0, g.k, keep,
+                c.d_slots + S_TESTS_SKY);
         SKY_LAUNCH_CHECK();
         SKY_CUDA(cudaEventRecord(c.ev[15], c.stream));
         note_launch(c);

@@ -1,0 +1,3 @@
+python scripts/c5_sky_dump.py /tmp/x.npy > /dev/null 2>&1
+ncu --set full --import-source on --clock-control none -k regex:k_grid_decide_tma -s 1 -c 1 -o gpurun_out/prof_C5_k6tma -f python scripts/c5_sky_dump.py /tmp/x.npy > gpurun_out/ncu_k6.log 2>&1; echo "ncu rc=$?"
+tail -3 gpurun_out/ncu_k6.log
