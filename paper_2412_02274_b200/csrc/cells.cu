@@ -33,6 +33,28 @@ namespace {
 constexpr int kBlock = 256;
 constexpr int kMaxCellDims = 16;
 
+// Steps run back to back with no host round trip: each step's kernels read
+// the previous step's undecided count (live) and return at once when it is
+// zero (live == nullptr: the first step, always run).
+__device__ __forceinline__ bool step_dead(const unsigned long long* live) {
+    return live && *(volatile const unsigned long long*)live == 0ULL;
+}
+
+__global__ void k_clear_slot_c(unsigned long long* p) {
+    pdl_wait();
+    *p = 0;
+}
+
+// zero a step's grid (replaces a memset so that a dead step costs nothing)
+__global__ void k_cells_zero(uint4* __restrict__ p, uint64_t n16, const unsigned long long* live) {
+    pdl_wait();
+    if (step_dead(live)) return;
+    const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n16;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        p[i] = z;
+}
+
 struct CellGeom {
     int d;
     int g;
@@ -43,22 +65,24 @@ struct CellGeom {
 
 template <class W>
 __global__ void k_cells_mark(const double* __restrict__ v, uint64_t S, CellGeom geo,
-                             W* __restrict__ rows) {
+                             W* __restrict__ rows, const unsigned long long* live) {
     pdl_wait();
+    if (step_dead(live)) return;
     const double gd = (double)geo.g;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < S;
          i += (uint64_t)gridDim.x * blockDim.x) {
         uint64_t r = 0;
         for (int j = 1; j < geo.d; ++j) r += (uint64_t)floor(__dmul_rn(v[j * S + i], gd)) * geo.stride[j];
-        const unsigned c0 = (unsigned)floor(__dmul_rn(v[i], gd));
-        atomicOr(&rows[r], (W)1 << c0);
+        const W bit = (W)1 << (unsigned)floor(__dmul_rn(v[i], gd));
+        if (!(rows[r] & bit)) atomicOr(&rows[r], bit);
     }
 }
 
 // prefix-OR inside each word: bit k |= bits 0..k-1 (attribute 0)
 template <class W>
-__global__ void k_cells_or_word(W* __restrict__ rows, uint64_t n) {
+__global__ void k_cells_or_word(W* __restrict__ rows, uint64_t n, const unsigned long long* live) {
     pdl_wait();
+    if (step_dead(live)) return;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x) {
         W x = rows[i];
@@ -76,8 +100,9 @@ __global__ void k_cells_or_word(W* __restrict__ rows, uint64_t n) {
 // consecutive threads own consecutive lines (coalesced when stride >= 32)
 template <class W>
 __global__ void k_cells_or_dim(W* __restrict__ rows, uint64_t nrows, uint64_t ext,
-                               uint64_t stride) {
+                               uint64_t stride, const unsigned long long* live) {
     pdl_wait();
+    if (step_dead(live)) return;
     const uint64_t lines = nrows / ext;
     for (uint64_t l = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; l < lines;
          l += (uint64_t)gridDim.x * blockDim.x) {
@@ -111,8 +136,9 @@ constexpr uint32_t kSlabWords = 4096;
 template <class W>
 __global__ void __launch_bounds__(kBlock)
 k_cells_or_slab(W* __restrict__ rows, uint64_t nrows, uint32_t e1, uint32_t e2,
-                uint32_t spb) {
+                uint32_t spb, const unsigned long long* live) {
     pdl_wait();
+    if (step_dead(live)) return;
     extern __shared__ __align__(16) unsigned char smraw[];
     W* sm = reinterpret_cast<W*>(smraw);
     const uint32_t slab = e1 * e2;
@@ -172,8 +198,10 @@ constexpr int kPairMax = 32;
 
 template <class W>
 __global__ void __launch_bounds__(kBlock)
-k_cells_or_pair(W* __restrict__ rows, uint64_t nrows, uint32_t ea, uint32_t eb, uint64_t sa) {
+k_cells_or_pair(W* __restrict__ rows, uint64_t nrows, uint32_t ea, uint32_t eb, uint64_t sa,
+                const unsigned long long* live) {
     pdl_wait();
+    if (step_dead(live)) return;
     const uint64_t plane = (uint64_t)ea * eb;
     const uint64_t lines = nrows / plane;
     for (uint64_t l = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; l < lines;
@@ -201,32 +229,42 @@ k_cells_or_pair(W* __restrict__ rows, uint64_t nrows, uint32_t ea, uint32_t eb, 
 
 template <class W>
 __global__ void k_cells_query(const double* __restrict__ v, uint64_t S, CellGeom geo,
-                              const W* __restrict__ P, const uint32_t* __restrict__ act,
-                              uint64_t na, int32_t* __restrict__ den,
-                              unsigned long long* __restrict__ undecided) {
+                              const W* __restrict__ P, const uint32_t* __restrict__ act_in,
+                              uint64_t na, const unsigned long long* n_in,
+                              int32_t* __restrict__ den, uint32_t* __restrict__ act_out,
+                              unsigned long long* __restrict__ n_out) {
     pdl_wait();
+    if (n_in) na = *(volatile const unsigned long long*)n_in;
     const double gd = (double)geo.g;
-    unsigned long long left = 0;
-    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < na;
-         k += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t t = act[k];
-        if (den[t] != 0) continue;
-        uint64_t r = 0;
-        unsigned cj[kMaxCellDims];
-        for (int j = 1; j < geo.d; ++j) {
-            cj[j] = (unsigned)floor(__dmul_rn(v[j * S + t], gd));
-            r += (uint64_t)cj[j] * geo.stride[j];
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warp0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) & ~31ULL;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t k0 = warp0; k0 < na; k0 += stride) {
+        const uint64_t k = k0 + lane;
+        bool keep = false;
+        uint32_t t = 0;
+        if (k < na) {
+            t = act_in[k];
+            uint64_t r = 0;
+            unsigned cj[kMaxCellDims];
+            for (int j = 1; j < geo.d; ++j) {
+                cj[j] = (unsigned)floor(__dmul_rn(v[j * S + t], gd));
+                r += (uint64_t)cj[j] * geo.stride[j];
+            }
+            const unsigned c0 = (unsigned)floor(__dmul_rn(v[t], gd));
+            bool hit = c0 >= 1 && ((P[r] >> (c0 - 1)) & 1);
+            for (int j = 1; j < geo.d && !hit; ++j)
+                if (cj[j] >= 1) hit = (P[r - geo.stride[j]] >> c0) & 1;
+            if (hit) den[t] = geo.g;
+            keep = !hit;
         }
-        const unsigned c0 = (unsigned)floor(__dmul_rn(v[t], gd));
-        bool hit = c0 >= 1 && ((P[r] >> (c0 - 1)) & 1);
-        for (int j = 1; j < geo.d && !hit; ++j)
-            if (cj[j] >= 1) hit = (P[r - geo.stride[j]] >> c0) & 1;
-        if (hit) den[t] = geo.g;
-        else ++left;
+        const unsigned m = __ballot_sync(0xffffffffu, keep);
+        if (!m) continue;
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(n_out, (unsigned long long)__popc(m));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (keep) act_out[base + __popc(m & ((1u << lane) - 1u))] = t;
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) left += __shfl_down_sync(0xffffffffu, left, o);
-    if ((threadIdx.x & 31) == 0 && left) atomicAdd(undecided, left);
 }
 
 // ---- packed-code variants: the codes floor(v*g) of every step computed
@@ -251,43 +289,62 @@ __global__ void k_cells_codes(const double* __restrict__ v, uint64_t S, int d, i
     }
 }
 
+// marking skips a bit that is already set (a plain read first): at small
+// steps millions of tuples share a few thousand words, and the atomics on
+// those words serialise (g = 2: 0.73 ms) while the reads hit L1/L2.  A
+// stale 0 only costs the atomic; bits are never cleared within a step.
 template <class W, class CW>
 __global__ void k_cells_mark_c(const CW* __restrict__ code, uint64_t S, CellGeom geo,
-                               W* __restrict__ rows) {
+                               W* __restrict__ rows, const unsigned long long* live) {
     pdl_wait();
+    if (step_dead(live)) return;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < S;
          i += (uint64_t)gridDim.x * blockDim.x) {
         const CW w = code[i];
         uint64_t r = 0;
         for (int j = 1; j < geo.d; ++j) r += (uint64_t)((w >> (8 * j)) & 0xFF) * geo.stride[j];
-        atomicOr(&rows[r], (W)1 << (unsigned)(w & 0xFF));
+        const W bit = (W)1 << (unsigned)(w & 0xFF);
+        if (!(rows[r] & bit)) atomicOr(&rows[r], bit);
     }
 }
 
+// one query per undecided candidate (act_in[0 .. *n_in), or na when n_in
+// is null); ejected ones get den = g, the rest are appended to act_out
+// (warp-aggregated) and counted in *n_out — the next step's candidates
 template <class W, class CW>
 __global__ void k_cells_query_c(const CW* __restrict__ code, CellGeom geo,
-                                const W* __restrict__ P, const uint32_t* __restrict__ act,
-                                uint64_t na, int32_t* __restrict__ den,
-                                unsigned long long* __restrict__ undecided) {
+                                const W* __restrict__ P, const uint32_t* __restrict__ act_in,
+                                uint64_t na, const unsigned long long* n_in,
+                                int32_t* __restrict__ den, uint32_t* __restrict__ act_out,
+                                unsigned long long* __restrict__ n_out) {
     pdl_wait();
-    unsigned long long left = 0;
-    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < na;
-         k += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t t = act[k];
-        if (den[t] != 0) continue;
-        const CW w = code[t];
-        uint64_t r = 0;
-        for (int j = 1; j < geo.d; ++j) r += (uint64_t)((w >> (8 * j)) & 0xFF) * geo.stride[j];
-        const unsigned c0 = (unsigned)(w & 0xFF);
-        bool hit = c0 >= 1 && ((P[r] >> (c0 - 1)) & 1);
-        for (int j = 1; j < geo.d && !hit; ++j)
-            if (((w >> (8 * j)) & 0xFF) >= 1) hit = (P[r - geo.stride[j]] >> c0) & 1;
-        if (hit) den[t] = geo.g;
-        else ++left;
+    if (n_in) na = *(volatile const unsigned long long*)n_in;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warp0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) & ~31ULL;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t k0 = warp0; k0 < na; k0 += stride) {
+        const uint64_t k = k0 + lane;
+        bool keep = false;
+        uint32_t t = 0;
+        if (k < na) {
+            t = act_in[k];
+            const CW w = code[t];
+            uint64_t r = 0;
+            for (int j = 1; j < geo.d; ++j) r += (uint64_t)((w >> (8 * j)) & 0xFF) * geo.stride[j];
+            const unsigned c0 = (unsigned)(w & 0xFF);
+            bool hit = c0 >= 1 && ((P[r] >> (c0 - 1)) & 1);
+            for (int j = 1; j < geo.d && !hit; ++j)
+                if (((w >> (8 * j)) & 0xFF) >= 1) hit = (P[r - geo.stride[j]] >> c0) & 1;
+            if (hit) den[t] = geo.g;
+            keep = !hit;
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, keep);
+        if (!m) continue;
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(n_out, (unsigned long long)__popc(m));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (keep) act_out[base + __popc(m & ((1u << lane) - 1u))] = t;
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) left += __shfl_down_sync(0xffffffffu, left, o);
-    if ((threadIdx.x & 31) == 0 && left) atomicAdd(undecided, left);
 }
 
 __global__ void k_col_max(const double* __restrict__ v, uint64_t S, int d,
@@ -342,17 +399,17 @@ static bool cells_geometry(const std::vector<double>& amax, int d, int g, uint64
 // (slab: attributes 0-2 in shared memory; pairs of the rest in registers),
 // or one pass per attribute (SKYGPU_CELLS_UNFUSED=1, or extents too large)
 template <class W>
-void sweeps(Ctx& c, W* R, const CellGeom& geo, bool fused) {
+void sweeps(Ctx& c, W* R, const CellGeom& geo, bool fused, const unsigned long long* live) {
     const int d = geo.d;
     auto single = [&](int j) {
         pdl_launch(k_cells_or_dim<W>, grid_for(geo.rows / geo.ext[j], kBlock), kBlock, 0, c.stream,
-            R, geo.rows, geo.ext[j], geo.stride[j]);
+            R, geo.rows, geo.ext[j], geo.stride[j], live);
         note_launch(c);
     };
     const uint32_t e1 = d >= 2 ? (uint32_t)geo.ext[1] : 1, e2 = d >= 3 ? (uint32_t)geo.ext[2] : 1;
     if (!fused || d < 2 || (uint64_t)e1 * e2 * sizeof(W) > 128 * 1024) {
         pdl_launch(k_cells_or_word<W>, grid_for(geo.rows, kBlock), kBlock, 0, c.stream, R,
-                   geo.rows);
+                   geo.rows, live);
         note_launch(c);
         for (int j = 1; j < d; ++j) single(j);
         return;
@@ -376,14 +433,14 @@ void sweeps(Ctx& c, W* R, const CellGeom& geo, bool fused) {
     }
     const uint64_t nslabs = geo.rows / slab;
     pdl_launch(k_cells_or_slab<W>, grid_for((nslabs + spb - 1) / spb, 1, c.num_sms * 8), kBlock,
-               smem, c.stream, R, geo.rows, e1, e2, spb);
+               smem, c.stream, R, geo.rows, e1, e2, spb, live);
     note_launch(c);
     int j = 3;
     while (j < d) {
         if (j + 1 < d && geo.ext[j] <= (uint64_t)kPairMax) {
             const uint64_t lines = geo.rows / (geo.ext[j] * geo.ext[j + 1]);
             pdl_launch(k_cells_or_pair<W>, grid_for(lines, kBlock), kBlock, 0, c.stream,
-                R, geo.rows, (uint32_t)geo.ext[j], (uint32_t)geo.ext[j + 1], geo.stride[j]);
+                R, geo.rows, (uint32_t)geo.ext[j], (uint32_t)geo.ext[j + 1], geo.stride[j], live);
             note_launch(c);
             j += 2;
         } else {
@@ -597,21 +654,38 @@ bool gres_cells_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_ma
     int steps = 0;
     const char* uf = getenv("SKYGPU_CELLS_UNFUSED");
     const bool fused = !(uf && uf[0] == '1');
+    // undecided candidates ping-pong between two lists; a step's count lives
+    // in a device slot that gates every kernel of the next step, so the
+    // steps are queued back to back without a host round trip
+    uint32_t* lists[2] = {c.buf[B_CACT0].as<uint32_t>(na), c.buf[B_CACT1].as<uint32_t>(na)};
+    unsigned long long* cnt[2] = {c.d_slots + S_LIVE0, c.d_slots + S_LIVE1};
+    const uint32_t* in = act;
+    const unsigned long long* n_in = nullptr;
+    int cur = 0;
     for (int g = g_max; g >= 2; --g) {
         CellGeom geo;
         uint64_t e0g = 0;
         cells_geometry(amax, d, g, budget_rows, &geo, &e0g);
         const size_t wb = w64 ? 8 : 4;
-        SKY_CUDA(cudaMemsetAsync(rows, 0, geo.rows * wb, c.stream));
+        const uint64_t n16 = (geo.rows * wb + 15) / 16;
+        pdl_launch(k_cells_zero, grid_for(n16, kBlock), kBlock, 0, c.stream, (uint4*)rows, n16, n_in);
+        pdl_launch(k_clear_slot_c, 1, 1, 0, c.stream, cnt[cur]);
         const unsigned gs = grid_for(S, kBlock);
+        const unsigned gq = grid_for(na, kBlock);
         auto run_codes = [&](auto* R, auto* cg) {
             using WR = std::remove_pointer_t<decltype(R)>;
             using CW = std::remove_const_t<std::remove_pointer_t<decltype(cg)>>;
-            pdl_launch(k_cells_mark_c<WR, CW>, gs, kBlock, 0, c.stream, cg, S, geo, R);
-            sweeps<WR>(c, R, geo, fused);
-            reset_counts(c);
-            pdl_launch(k_cells_query_c<WR, CW>, grid_for(na, kBlock), kBlock, 0, c.stream,
-                cg, geo, R, act, na, d_den, c.d_slots + S_C3);
+            pdl_launch(k_cells_mark_c<WR, CW>, gs, kBlock, 0, c.stream, cg, S, geo, R, n_in);
+            sweeps<WR>(c, R, geo, fused, n_in);
+            pdl_launch(k_cells_query_c<WR, CW>, gq, kBlock, 0, c.stream, cg, geo,
+                       (const WR*)R, in, na, n_in, d_den, lists[cur], cnt[cur]);
+        };
+        auto run_vals = [&](auto* R) {
+            using WR = std::remove_pointer_t<decltype(R)>;
+            pdl_launch(k_cells_mark<WR>, gs, kBlock, 0, c.stream, d_skyv, S, geo, R, n_in);
+            sweeps<WR>(c, R, geo, fused, n_in);
+            pdl_launch(k_cells_query<WR>, gq, kBlock, 0, c.stream, d_skyv, S, geo, (const WR*)R,
+                       in, na, n_in, d_den, lists[cur], cnt[cur]);
         };
         const uint64_t coff = (uint64_t)(g_max - g) * S;
         if (codes && w64 && cw32)
@@ -622,32 +696,20 @@ bool gres_cells_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_ma
             run_codes(static_cast<unsigned*>(rows), (const uint32_t*)codes + coff);
         else if (codes)
             run_codes(static_cast<unsigned*>(rows), (const unsigned long long*)codes + coff);
-        else if (w64) {
-            auto* R = static_cast<unsigned long long*>(rows);
-            pdl_launch(k_cells_mark<unsigned long long>, gs, kBlock, 0, c.stream, d_skyv, S, geo,
-                       R);
-            sweeps<unsigned long long>(c, R, geo, fused);
-            reset_counts(c);
-            pdl_launch(k_cells_query<unsigned long long>, grid_for(na, kBlock), kBlock, 0, c.stream,
-                d_skyv, S, geo, R, act, na, d_den, c.d_slots + S_C3);
-        } else {
-            auto* R = static_cast<unsigned*>(rows);
-            pdl_launch(k_cells_mark<unsigned>, gs, kBlock, 0, c.stream, d_skyv, S, geo, R);
-            sweeps<unsigned>(c, R, geo, fused);
-            reset_counts(c);
-            pdl_launch(k_cells_query<unsigned>, grid_for(na, kBlock), kBlock, 0, c.stream,
-                d_skyv, S, geo, R, act, na, d_den, c.d_slots + S_C3);
-        }
+        else if (w64)
+            run_vals(static_cast<unsigned long long*>(rows));
+        else
+            run_vals(static_cast<unsigned*>(rows));
         SKY_LAUNCH_CHECK();
-        note_launch(c, 3);
+        note_launch(c, 4);
         // algorithmic bytes of the step: the grid zeroed, read and written
         // once by an ideal fused prefix-OR, plus the mark and query reads of
         // the S x d values
         swept += 3 * geo.rows * wb + 2 * S * (codes ? cwb : (uint64_t)d * sizeof(double));
         ++steps;
-        // stop early once every candidate has its answer (one small read per step)
-        read_slots(c, S_C3, 1);
-        if (c.h_slots[S_C3] == 0) break;
+        in = lists[cur];
+        n_in = cnt[cur];
+        cur ^= 1;
     }
     *cells_swept = swept;
     *steps_run = steps;

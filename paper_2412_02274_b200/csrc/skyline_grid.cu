@@ -126,32 +126,27 @@ __global__ void k_cell_scatter(const W* __restrict__ code, const uint32_t* __res
     }
 }
 
-// the same scatter plus each tuple's exact record in cell order: its D
-// float64 values and its sum key, (D + 1) doubles at rec[pos * (D + 1)] —
-// the TMA decide kernel's exact follow-up then reads one contiguous record
-// per side instead of chasing sidx -> R -> values and keys
+// each tuple's exact record in cell order: its D float64 values and its
+// sum key, (D + 1) doubles at rec[pos * (D + 1)] — the TMA decide kernel's
+// exact follow-up then reads one contiguous record per side instead of
+// chasing sidx -> R -> values and keys.  Gathered (writes coalesced, the
+// 64-byte reads random) after the scatter.
 template <int D>
-__global__ void k_cell_scatter_rec(const GridWord<D>* __restrict__ code,
-                                   const uint32_t* __restrict__ cell, uint32_t r,
-                                   const uint32_t* __restrict__ seg, uint32_t* __restrict__ cursor,
-                                   const double* __restrict__ v,
-                                   const unsigned long long* __restrict__ key,
-                                   const uint32_t* __restrict__ R, GridWord<D>* __restrict__ scode,
-                                   uint32_t* __restrict__ sidx, double* __restrict__ rec) {
+__global__ void k_gather_rec(const uint32_t* __restrict__ sidx, uint32_t r,
+                             const double* __restrict__ v,
+                             const unsigned long long* __restrict__ key,
+                             const uint32_t* __restrict__ R, double* __restrict__ rec) {
     pdl_wait();
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < r; i += gridDim.x * blockDim.x) {
-        const uint32_t cl = cell[i];
-        const uint32_t pos = seg[cl] + atomicAdd(&cursor[cl], 1u);
-        scode[pos] = code[i];
-        sidx[pos] = i;
+    for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < r; q += gridDim.x * blockDim.x) {
+        const uint32_t i = sidx[q];
         const uint64_t p = R ? R[i] : i;
-        double x[D];
+        double x[D + 1];
 #pragma unroll
         for (int j = 0; j < D; ++j) x[j] = v[p * D + j];
-        double* o = rec + (uint64_t)pos * (D + 1);
+        x[D] = __longlong_as_double((long long)key[p]);
+        double* o = rec + (uint64_t)q * (D + 1);
 #pragma unroll
-        for (int j = 0; j < D; ++j) o[j] = x[j];
-        o[D] = __longlong_as_double((long long)key[p]);
+        for (int j = 0; j <= D; ++j) o[j] = x[j];
     }
 }
 
@@ -946,13 +941,12 @@ void sky_grid_decide(Ctx& c, const double* d_vals, int d, const unsigned long lo
             return e && e[0] == 'a';
         }();
         double* rec = nullptr;
-        if (alu) {
-            pdl_launch(k_cell_scatter<W>, grid_for(r, kGB), kGB, 0, c.stream, code, cell,
-                       (uint32_t)r, seg, count, scode, sidx);
-        } else {
+        pdl_launch(k_cell_scatter<W>, grid_for(r, kGB), kGB, 0, c.stream, code, cell,
+                   (uint32_t)r, seg, count, scode, sidx);
+        if (!alu) {
             rec = c.buf[B_GREC].as<double>(r * (D + 1));
-            pdl_launch(k_cell_scatter_rec<D>, grid_for(r, kGB), kGB, 0, c.stream, code, cell,
-                       (uint32_t)r, seg, count, d_vals, keys, R, scode, sidx, rec);
+            pdl_launch(k_gather_rec<D>, grid_for(r, kGB), kGB, 0, c.stream, sidx, (uint32_t)r,
+                       d_vals, keys, R, rec);
         }
         SKY_LAUNCH_CHECK();
         pdl_launch(k_row_items, grid_for(g.rows, kGB), kGB, 0, c.stream, seg, g.rows, g.k0, items,
