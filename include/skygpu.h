@@ -119,6 +119,13 @@ int skygpu_set_device(int device, char* err, size_t errlen);
 int skygpu_set_stream(void* cuda_stream, char* err, size_t errlen);
 /* release cached device buffers of the current device */
 int skygpu_release(void);
+/* a page-locked host staging buffer of at least `bytes`, owned by the
+ * current device's context (grow-only; `slot` 0..3 are independent buffers,
+ * valid until the next call with the same slot and a larger size or
+ * skygpu_release).  A caller that flattens its relation into it gets DMA-rate
+ * host->device copies (the C++ drop-in's Relation flattening: the reference
+ * API has no device pointers, parallel.hpp:46-47). */
+int skygpu_host_buffer(uint64_t bytes, int slot, void** out, char* err, size_t errlen);
 
 /* partition.hpp:43 make_plan */
 int skygpu_make_plan(int strategy, long long target_partitions, int dims, skygpu_plan* out,

@@ -16,22 +16,31 @@
 // std::invalid_argument text the reference throws, ERUNTIME -> runtime_error,
 // CUDA failures -> runtime_error (there is no CPU fallback).
 //
-// Metrics (PhaseMetrics, ResistanceMetrics): by default EXACT — the
-// reference's DominanceCounter totals, derived on the GPU by
-// skygpu_sfs_accounting (csrc/accounting.cu) from the partitions the
-// reference's own assign_partitions / grid_cell / prune_grid_dominated /
+// Metrics (PhaseMetrics, ResistanceMetrics).  By default the answers come
+// from the GPU engines alone (skyline_device / gres_device through the
+// C-ABI) and the counters hold the GPU kernels' OWN executed test counts
+// (per_partition_tests[0] = all skyline-stage tests, final_tests = 0; one
+// IterationCost row per step with the gres tests spread evenly) — a
+// different algorithm does different work, so these are not the
+// reference's SFS DominanceCounter totals.  The relation is flattened by
+// several threads straight into pinned staging buffers (skygpu_host_buffer).
+//
+// SKYGPU_METRICS=exact (opt-in: reports and the count-pinning tests,
+// test_parallel.cpp:25-43, acceptance criteria 8 and 10) adds the
+// reference's EXACT totals, derived on the GPU by skygpu_sfs_accounting
+// (csrc/accounting.cu) from the partitions the reference's own
+// assign_partitions / grid_cell / prune_grid_dominated /
 // select_representatives produce (partition.o stays the reference's), so
-// every report, the paper's simulated_cost, and the count-pinning tests
-// (test_parallel.cpp:25-43, acceptance criteria 8 and 10) match the CPU
-// library.  max_concurrent reports the core-budget bound min(cores, p)
-// (the reference's OMP high-water mark, parallel.cpp:62-70, is scheduling
-// dependent).  SKYGPU_METRICS=fast skips the accounting (answers only; the
-// counters then hold the GPU kernels' own test counts).  Wall times are
-// measured around the device calls.
+// every report and the paper's simulated_cost match the CPU library byte
+// for byte; it costs roughly the reference's own per-step host work.
+// max_concurrent reports the core-budget bound min(cores, p) (the
+// reference's OMP high-water mark, parallel.cpp:62-70, is scheduling
+// dependent).  Wall times are measured around the device calls.
 #include <chrono>
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <algorithm>
@@ -62,6 +71,53 @@ skygpu_plan to_c(const PartitionPlan& p) {
     return skygpu_plan{static_cast<int>(p.strategy), p.slices, p.partitions, p.dims};
 }
 
+[[noreturn]] void arity(std::size_t got, std::size_t d) {
+    throw std::invalid_argument("dominates: arity mismatch (" + std::to_string(got) + " vs " +
+                                std::to_string(d) + ")");
+}
+
+// Relation (AoS of heap vectors, core.hpp:25-44) -> contiguous float64 + ids
+// in the library's pinned staging buffers (slots 0 and 1), by up to 16
+// threads for large relations (the tuples are separate heap blocks: the
+// copy is latency-bound per tuple)
+void flatten_pinned(const Relation& r, double** vals, std::int64_t** ids) {
+    const std::size_t n = r.size(), d = r.dims;
+    void* pv = nullptr;
+    void* pi = nullptr;
+    char err[256];
+    check(skygpu_host_buffer(n * d * sizeof(double) + 16, 0, &pv, err, sizeof(err)), err);
+    check(skygpu_host_buffer(n * sizeof(std::int64_t) + 16, 1, &pi, err, sizeof(err)), err);
+    *vals = static_cast<double*>(pv);
+    *ids = static_cast<std::int64_t*>(pi);
+    double* V = *vals;
+    std::int64_t* I = *ids;
+    std::size_t bad = n;  // first tuple of the wrong arity (reported like dominates)
+    auto part = [&](std::size_t lo, std::size_t hi, std::size_t* first_bad) {
+        for (std::size_t i = lo; i < hi; ++i) {
+            const Tuple& t = r.tuples[i];
+            if (t.values.size() != d) {
+                *first_bad = i;
+                return;
+            }
+            std::memcpy(V + i * d, t.values.data(), d * sizeof(double));
+            I[i] = t.id;
+        }
+    };
+    const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    if (n < (1u << 16) || hw == 1) {
+        part(0, n, &bad);
+    } else {
+        std::vector<std::thread> th;
+        std::vector<std::size_t> fb(hw, n);
+        const std::size_t chunk = (n + hw - 1) / hw;
+        for (unsigned k = 0; k < hw; ++k)
+            th.emplace_back(part, std::min(n, k * chunk), std::min(n, (k + 1) * chunk), &fb[k]);
+        for (auto& x : th) x.join();
+        for (std::size_t b : fb) bad = std::min(bad, b);
+    }
+    if (bad < n) arity(r.tuples[bad].values.size(), d);
+}
+
 // Relation (AoS of heap vectors, core.hpp:25-44) -> contiguous float64 + ids
 void flatten(const Relation& r, std::vector<double>& vals, std::vector<std::int64_t>& ids) {
     const std::size_t n = r.size(), d = r.dims;
@@ -87,7 +143,7 @@ static_assert(sizeof(long long) == sizeof(std::int64_t), "partition ids are pass
 
 bool exact_metrics() {
     const char* e = std::getenv("SKYGPU_METRICS");
-    return !(e && std::string(e) == "fast");
+    return e && std::string(e) == "exact";
 }
 
 // parallel_skyline with the reference's exact accounting (see header)
@@ -151,22 +207,26 @@ ParallelSkylineResult parallel_skyline(const Relation& r, const PartitionPlan& p
     if (cores < 1) throw std::invalid_argument("parallel_skyline: cores must be >= 1");
     if (exact_metrics()) return parallel_skyline_exact(r, plan, reps, cores);
     const auto t0 = Clock::now();
-    std::vector<double> vals, rvals;
-    std::vector<std::int64_t> ids, rids;
-    flatten(r, vals, ids);
+    std::vector<double> rvals;
+    std::vector<std::int64_t> rids;
+    double* vals = nullptr;
+    std::int64_t* ids = nullptr;
+    flatten_pinned(r, &vals, &ids);
     for (const Tuple& t : reps.tuples) {
         rvals.insert(rvals.end(), t.values.begin(), t.values.end());
         rids.push_back(t.id);
     }
-    std::vector<std::uint64_t> pos(r.size() ? r.size() : 1);
+    void* pp = nullptr;
     std::uint64_t S = 0;
     skygpu_stats st;
     char err[1024];
+    check(skygpu_host_buffer((r.size() + 1) * sizeof(std::uint64_t), 2, &pp, err, sizeof(err)), err);
+    const std::uint64_t* pos = static_cast<const std::uint64_t*>(pp);
     const skygpu_plan cp = to_c(plan);
     const auto t1 = Clock::now();
-    check(skygpu_parallel_skyline(vals.data(), ids.data(), r.size(), static_cast<int>(r.dims), &cp,
-                                  rvals.data(), rids.data(), rids.size(), cores, pos.data(), &S,
-                                  &st, err, sizeof(err)),
+    check(skygpu_parallel_skyline(vals, ids, r.size(), static_cast<int>(r.dims), &cp,
+                                  rvals.data(), rids.data(), rids.size(), cores,
+                                  static_cast<std::uint64_t*>(pp), &S, &st, err, sizeof(err)),
           err);
     const double wall_parallel = ms_since(t1);
 

@@ -399,8 +399,33 @@ int skygpu_release(void) {
     if (g_ctx[dev]) {
         cudaStreamSynchronize(g_ctx[dev]->stream);
         for (auto& b : g_ctx[dev]->buf) b.release();
+        for (int i = 0; i < 4; ++i) {
+            if (g_ctx[dev]->hbuf[i]) cudaFreeHost(g_ctx[dev]->hbuf[i]);
+            g_ctx[dev]->hbuf[i] = nullptr;
+            g_ctx[dev]->hcap[i] = 0;
+        }
     }
     return SKYGPU_OK;
+}
+
+int skygpu_host_buffer(uint64_t bytes, int slot, void** out, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        if (slot < 0 || slot > 3) invalid("host_buffer: slot must be in [0, 3]");
+        if (!out) invalid("host_buffer: out is NULL");
+        Ctx& c = ctx();
+        if (bytes > c.hcap[slot]) {
+            if (c.hbuf[slot]) {
+                SKY_CUDA(cudaStreamSynchronize(c.stream));  // (a copy may still read it)
+                SKY_CUDA(cudaFreeHost(c.hbuf[slot]));
+                c.hbuf[slot] = nullptr;
+                c.hcap[slot] = 0;
+            }
+            const size_t want = bytes + bytes / 8 + 4096;
+            SKY_CUDA(cudaHostAlloc(&c.hbuf[slot], want, cudaHostAllocPortable));
+            c.hcap[slot] = want;
+        }
+        *out = c.hbuf[slot];
+    });
 }
 
 int skygpu_make_plan(int strategy, long long target, int dims, skygpu_plan* out, char* err,

@@ -168,6 +168,8 @@ struct Ctx {
     } spans[8];
     int nspans = 0;
     skygpu_stats scratch_stats;  // the call's stats when the caller passed none
+    void* hbuf[4] = {nullptr, nullptr, nullptr, nullptr};  // pinned staging (skygpu_host_buffer)
+    size_t hcap[4] = {0, 0, 0, 0};
     // host-pointer pipeline: the ids are still in flight (copy stream) until
     // this event; the skyline runs on the speculation that they are strictly
     // increasing (ties by position) and checks them at the end (S_IDSBAD)

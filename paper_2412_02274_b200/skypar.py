@@ -128,7 +128,7 @@ EXPORTED_SYMBOLS = ("skygpu_version", "skygpu_device_count", "skygpu_set_device"
                     "skygpu_grid_resistance", "skygpu_snap_relation", "skygpu_max_grid_intervals",
                     "skygpu_pipeline", "skygpu_generate", "skygpu_sfs_accounting",
                     "skygpu_set_collective", "skygpu_normalize", "skygpu_select_representatives",
-                    "skygpu_read_csv", "skygpu_pipeline_csv")
+                    "skygpu_read_csv", "skygpu_pipeline_csv", "skygpu_host_buffer")
 
 
 def _check(rc: int, err: C.Array) -> None:

@@ -143,6 +143,18 @@ def main(which):
     if which in ("all", "big"):
         gen_case("C4_uni_10M_d5", "uni", 10000000, 5, 1, strategy="angular", p=64, release=True,
                  cores=8)
+    if which in ("all", "big", "big2"):
+        # config 4 names all three plans at target 64 (grid -> m=2, p=32;
+        # sliced -> 64; angular above); the reference's plan invariance
+        # (acceptance_main.cpp:145-184) says the answers agree — pinned here
+        # through the reference itself for each plan
+        gen_case("C4_uni_10M_d5_grid64", "uni", 10000000, 5, 1, strategy="grid", p=64,
+                 release=True, cores=8)
+        gen_case("C4_uni_10M_d5_sliced64", "uni", 10000000, 5, 1, strategy="sliced", p=64,
+                 release=True, cores=8)
+        # the C5 stream's 20k prefix (the reference arm's bench sample)
+        gen_case("C5_prefix_20k_d7", "ant", 20000, 7, 1, strategy="angular", p=64, release=True,
+                 cores=8)
 
 
 if __name__ == "__main__":

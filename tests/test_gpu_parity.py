@@ -51,7 +51,8 @@ def test_small_goldens(name):
 
 @pytest.mark.parametrize("name", ["C1_uni_100k_d4", "C1_uni_100k_d4_sliced16", "C2_ant_1M_d3",
                                   "C3_corr_1M_d6", "C5_prefix_2k_d7", "C5_prefix_10k_d7",
-                                  "C4_uni_10M_d5"])
+                                  "C5_prefix_20k_d7", "C4_uni_10M_d5", "C4_uni_10M_d5_grid64",
+                                  "C4_uni_10M_d5_sliced64"])
 def test_config_goldens(name):
     check_pipeline_against_golden(load_golden(name))
 

@@ -1,0 +1,55 @@
+"""The process-static alternatives of the library (SKYGPU_* switches, read
+once per process) against the reference goldens: each runs in its own
+subprocess.  Covers the one-CTA A' regrouping (SKYGPU_CELL_ORDER=1), the
+quantile-grid K5 pruning (SKYGPU_QGRID=1), the plan-cell K5 scan order
+(SKYGPU_SCAN_CELLS=plan, the paper's grid/angular/sliced partitions as the
+scan order) and the per-lane ALU rank-grid decide kernel
+(SKYGPU_GRID_KERNEL=alu) — all three skyline engine choices each."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CASES = ",".join(["C1_uni_100k_d4", "C2_ant_1M_d3", "C5_prefix_10k_d7", "rand_ant_n1500_d5_angular",
+                  "rand_lattice_n1500_d4_angular", "rand_uni_n1500_d3_grid",
+                  "rand_lattice_n1500_d3_sliced", "uncapped_lattice_d3", "huge_values_ties"])
+
+
+def _run(env, *extra):
+    e = dict(os.environ)
+    e.update(env)
+    out = subprocess.check_output([sys.executable, os.path.join(HERE, "_env_variant.py"), CASES,
+                                   *extra], env=e, text=True, timeout=900)
+    return json.loads(out.strip().splitlines()[-1])
+
+
+@pytest.mark.parametrize("env", [{"SKYGPU_CELL_ORDER": "1"}, {"SKYGPU_QGRID": "1"},
+                                 {"SKYGPU_SCAN_CELLS": "plan"},
+                                 {"SKYGPU_QGRID": "1", "SKYGPU_CELL_ORDER": "1"},
+                                 {"SKYGPU_PDL": "0"}, {"SKYGPU_CELLS_UNFUSED": "1"},
+                                 {"SKYGPU_CELLS_SMEM": "0"}, {"SKYGPU_GRES_TILED": "1"},
+                                 {"SKYGPU_INTRA": "1"}, {"SKYGPU_INTRA": "2"},
+                                 {"SKYGPU_FUSED_SELECT": "0"}, {"SKYGPU_NO_SPEC_FINAL": "1"},
+                                 {"SKYGPU_NO_DEV_ROUND": "1"}, {"SKYGPU_OVERLAP": "0"},
+                                 {"SKYGPU_PREFIX": "1500", "SKYGPU_SOLO": "4",
+                                  "SKYGPU_DIR_PER_CELL": "32"},
+                                 {"SKYGPU_IDS_LATE": "0"}, {"SKYGPU_GRID_ROW": "128",
+                                                            "SKYGPU_GRID_K0": "16"}])
+def test_env_variant_matches_goldens(env):
+    r = _run(env)
+    assert r["bad"] == [], r
+
+
+def test_grid_decide_alu_and_tma_kernels_agree(tmp_path):
+    """The two K6 kernels (TMA bitset default, per-lane ALU) on a C5-shaped
+    1M-tuple relation (rank-grid engine): identical skyline, ids and order."""
+    path = str(tmp_path / "pos.npy")
+    a = _run({"SKYGPU_GRID_KERNEL": "alu"}, "1000000", path)
+    assert a["bad"] == [], a
+    b = _run({}, "1000000", path)
+    assert b["bad"] == [], b

@@ -7,7 +7,7 @@ import pytest
 from conftest import golden_input, golden_names, load_golden, spec_cap
 from oracle import pyoracle as po
 
-SMALL = golden_names(exclude=("C4_", "C5_prefix_10k"))
+SMALL = golden_names(exclude=("C4_", "C5_prefix_10k", "C5_prefix_20k"))
 
 
 @pytest.mark.parametrize("name", SMALL)
