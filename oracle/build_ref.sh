@@ -64,18 +64,19 @@ if [ -f "$LIBDIR/libskygpu.so" ]; then
   $CXX $COMMON -O2 "$REF/tests/acceptance_main.cpp" "$OUT/libskypar_chk.a" -o "$OUT/acceptance_ref"
   $CXX $COMMON -O3 -DNDEBUG -I"$REF/include" "$HERE/refdrive.cpp" "$OUT/libskypar_gpu_rel.a" \
       -L"$LIBDIR" -lskygpu $RPATH -o "$OUT/refdrive_gpu"
-  # the skypar CLI front-end (adapter/skypar_cli.cpp, hand-written parser):
-  # over the GPU drop-in and over the unmodified CPU library, both in the
-  # reference's default (checked) build
-  $CXX $COMMON -O2 -g -I"$REF/include" "$ROOT/paper_2412_02274_b200/adapter/skypar_cli.cpp" \
-      "$OUT/libskypar_gpu_chk.a" -L"$LIBDIR" -lskygpu $RPATH -o "$OUT/skypar_gpu"
-  $CXX $COMMON -O2 -g -I"$REF/include" "$ROOT/paper_2412_02274_b200/adapter/skypar_cli.cpp" \
-      "$OUT/libskypar_chk.a" -o "$OUT/skypar_ref"
-  # the skypar-bench front end (adapter/skypar_bench_cli.cpp), both ways
-  $CXX $COMMON -O2 -g -I"$REF/include" "$ROOT/paper_2412_02274_b200/adapter/skypar_bench_cli.cpp" \
-      "$OUT/libskypar_gpu_chk.a" -L"$LIBDIR" -lskygpu $RPATH -o "$OUT/skypar_bench_gpu"
-  $CXX $COMMON -O2 -g -I"$REF/include" "$ROOT/paper_2412_02274_b200/adapter/skypar_bench_cli.cpp" \
-      "$OUT/libskypar_chk.a" -o "$OUT/skypar_bench_ref"
+  # the reference's own tools, UNMODIFIED (proj/tools/skypar_main.cpp and
+  # bench_main.cpp), compiled against an original CLI11-subset header
+  # (adapter/cli11_subset/CLI11.hpp; the real CLI11 is not vendored) — over
+  # the GPU drop-in and over the CPU library, in the reference's default
+  # (checked) build
+  CLI_INC="-I$ROOT/paper_2412_02274_b200/adapter/cli11_subset"
+  $CXX $COMMON -O2 -g $CLI_INC "$REF/tools/skypar_main.cpp" "$OUT/libskypar_gpu_chk.a" \
+      -L"$LIBDIR" -lskygpu $RPATH -o "$OUT/skypar_gpu"
+  $CXX $COMMON -O2 -g $CLI_INC "$REF/tools/skypar_main.cpp" "$OUT/libskypar_chk.a" -o "$OUT/skypar_ref"
+  $CXX $COMMON -O2 -g $CLI_INC "$REF/tools/bench_main.cpp" "$OUT/libskypar_gpu_chk.a" \
+      -L"$LIBDIR" -lskygpu $RPATH -o "$OUT/skypar_bench_gpu"
+  $CXX $COMMON -O2 -g $CLI_INC "$REF/tools/bench_main.cpp" "$OUT/libskypar_chk.a" \
+      -o "$OUT/skypar_bench_ref"
   # the CLI-determinism fixtures (acceptance criterion 9) travel with the
   # binaries; /root/reference does not exist on the GPU box
   mkdir -p "$OUT/fixtures"

@@ -1,7 +1,8 @@
-"""The skypar CLI front-end's argument handling (adapter/skypar_cli.cpp), on
-CPU: the binary built over the unmodified reference library (skypar_ref)
-shares the parser with the GPU build, and --help / usage errors never touch
-a device."""
+"""The skypar CLI — the reference's UNMODIFIED proj/tools/skypar_main.cpp
+compiled against the original CLI11-subset header
+(adapter/cli11_subset/CLI11.hpp) — argument handling, on CPU: the binary
+built over the unmodified reference library (skypar_ref) shares the parser
+with the GPU build, and --help / usage errors never touch a device."""
 import os
 import subprocess
 
