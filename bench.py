@@ -231,10 +231,11 @@ def our_arm(args):
     sky_flag = {"auto": skypar.SKY_AUTO, "rounds": skypar.SKY_ROUNDS, "grid": skypar.SKY_GRID}[args.sky_engine]
 
     if strong and world > 1:
-        # the library's exchange steps (rank-grid keep flags, denominators:
-        # MAX all-reduce) go through NCCL via torch.distributed
+        # the library's own NCCL group (unique id shipped over
+        # torch.distributed): its exchange steps (rank-grid keep flags,
+        # denominators) are ncclAllReduce(MAX) on the library's stream
         from paper_2412_02274_b200 import dist as skydist
-        skydist.install_collective()
+        skydist.init_library_nccl()
 
     def step_device():
         return skypar.pipeline_raw(vals_d.data_ptr(), ids_d.data_ptr(), n, d, plan, cap,
@@ -326,7 +327,7 @@ def our_arm(args):
         "config": {"workload": f"{args.workload}: {gen} n={n} d={d} seed={seed}"
                                f"{'' if strong or world == 1 else '+rank'}, {strat} p={p}, cap={cap}",
                    "skyline_size": S, "g_max": gm, "l2": "flushed (256 MiB write) before each step",
-                   "parallelism": f"{'sharded rank-grid rows + gres tuples, NCCL MAX exchanges' if strong else 'independent instance'}"
+                   "parallelism": f"{'one instance sharded: rank-grid rows, cell-engine steps (or gres tuples), libskygpu NCCL MAX all-reduces' if strong else 'independent instance'}"
                                   f" per GPU x{world}",
                    "gres_engine": {0: "auto", 1: "pairs", 2: "cells"}[args.engine],
                    "skyline_engine": {8: "prefix rounds", 16: "rank grid"}.get(stats[-1]["sky_engine"], "?")},

@@ -184,6 +184,28 @@ typedef int (*skygpu_allreduce_max_fn)(void* dev_ptr, uint64_t count, int elem_b
                                        void* cuda_stream, void* user);
 int skygpu_set_collective(skygpu_allreduce_max_fn fn, void* user, char* err, size_t errlen);
 
+/* The library's OWN NCCL path for the same exchange steps (preferred over
+ * skygpu_set_collective): one process per GPU; rank 0 makes a 128-byte
+ * unique id, the caller ships it to every rank (any out-of-band channel —
+ * torch.distributed's broadcast in dist.py), and every rank joins the
+ * communicator on the current device.  Sharded pipeline calls then queue
+ * ncclAllReduce(ncclMax) in place on the library's stream — no host
+ * synchronisation around the exchange.  libnccl.so.2 is loaded at run time
+ * (the copy already in the process, e.g. torch's, when there is one).
+ * The group's world size and rank must match the shard_world / shard_rank
+ * of the calls. */
+int skygpu_nccl_unique_id(void* out_id128, char* err, size_t errlen);
+int skygpu_nccl_init(const void* id128, int nranks, int rank, char* err, size_t errlen);
+int skygpu_nccl_release(void);
+
+/* The step split of the cell-occupancy resistance engine (host only, no
+ * device): the steps of g_max .. 2 that shard `rank` of `world` runs, in
+ * descending order — longest-processing-time over the per-step cost model of
+ * cells.cu (grid rows from the per-attribute maxima col_max[d] of the
+ * skyline, plus the S-tuple mark and query).  out_steps holds g_max - 1. */
+int skygpu_cells_step_plan(const double* col_max, int d, int g_max, uint64_t s, int rank,
+                           int world, int* out_steps, int* out_n, char* err, size_t errlen);
+
 /* Exact reference accounting of parallel_skyline — "metrics-parity" mode,
  * not the hot path.  Returns the DominanceCounter
  * totals the reference's CPU algorithm executes (core.hpp:46-67): per

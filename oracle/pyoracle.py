@@ -56,6 +56,7 @@ def lib():
         L.so_grid_resistance.argtypes = [dp, dp, u64, i32, i32, dp, dp, dp]
         L.so_gres_bruteforce.argtypes = [dp, dp, u64, i32, i32]
         L.so_gres_cells.argtypes = [dp, u64, i32, i32, dp]
+        L.so_gres_cells_steps.argtypes = [dp, u64, i32, dp, i32, dp]
         L.so_make_plan.argtypes = [i32, i64, i32, dp, dp]
         _lib = L
     return _lib
@@ -156,6 +157,18 @@ def gres_cells(sky: np.ndarray, g_max: int) -> np.ndarray:
     rc = lib().so_gres_cells(_p(sky), s, d, g_max, _p(den))
     if rc:
         raise ValueError(f"so_gres_cells unsupported input (rc={rc})")
+    return den[:s]
+
+
+def gres_cells_steps(sky: np.ndarray, steps) -> np.ndarray:
+    """The cell scan over a subset of the steps (a shard of the step split)."""
+    sky = np.ascontiguousarray(sky, dtype=np.float64)
+    s, d = sky.shape
+    st = np.ascontiguousarray(sorted(steps, reverse=True), dtype=np.int32)
+    den = np.zeros(max(s, 1), dtype=np.int32)
+    rc = lib().so_gres_cells_steps(_p(sky), s, d, _p(st), len(st), _p(den))
+    if rc:
+        raise ValueError(f"so_gres_cells_steps unsupported input (rc={rc})")
     return den[:s]
 
 

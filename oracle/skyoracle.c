@@ -334,11 +334,28 @@ int so_gres_bruteforce(const double* t, const double* r, uint64_t n, int d, int 
  * Codes k = floor(v*g) (strict order of k == strict order of k/g for
  * k < 2^52).  Rows are u64 bitmasks along attribute 0 (extent <= 64).
  * den must be pre-sized s; g_max given.  Returns 0, or -6 if unsupported. */
+/* The same scan over a SUBSET of the steps (descending list): a shard of the
+ * step-split resistance engine; den = the largest listed step at which the
+ * tuple is dominated, else 1 (the MAX over shards covering every step is
+ * the full scan's map). */
+int so_gres_cells_steps(const double* sky, uint64_t s, int d, const int* steps, int nsteps,
+                        int32_t* den);
+
 int so_gres_cells(const double* sky, uint64_t s, int d, int g_max, int32_t* den) {
+    int steps[4096];
+    int n = 0;
+    for (int g = g_max; g >= 2 && n < 4096; --g) steps[n++] = g;
+    if (g_max - 1 > 4096) return -6;
+    return so_gres_cells_steps(sky, s, d, steps, n, den);
+}
+
+int so_gres_cells_steps(const double* sky, uint64_t s, int d, const int* steps, int nsteps,
+                        int32_t* den) {
     for (uint64_t i = 0; i < s; ++i) den[i] = 0;
     if (d < 1 || d > 16) return -6;
     uint32_t* codes = (uint32_t*)malloc(sizeof(uint32_t) * (s ? s : 1) * d);
-    for (int g = g_max; g >= 2; --g) {
+    for (int si = 0; si < nsteps; ++si) {
+        const int g = steps[si];
         uint64_t ext[16];
         for (int j = 0; j < d; ++j) ext[j] = 1;
         for (uint64_t i = 0; i < s; ++i)

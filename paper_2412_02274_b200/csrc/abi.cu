@@ -5,6 +5,9 @@
 #include <cmath>
 #include <cstring>
 #include <mutex>
+#include <string>
+
+#include <dlfcn.h>
 
 #include "sky_common.cuh"
 
@@ -335,8 +338,64 @@ __global__ void k_mark_i32(int32_t* __restrict__ a, const uint32_t* __restrict__
 }
 }  // namespace
 
+// ---- NCCL, loaded at run time (dlopen: the process's copy when torch has
+// already loaded one — same soname — else the system's libnccl.so.2)
+namespace nccl {
+typedef struct {
+    char internal[128];
+} UniqueId;
+typedef void* Comm;
+enum { kUint8 = 1, kInt32 = 2 };  // ncclDataType_t (nccl.h)
+enum { kMax = 2 };                // ncclRedOp_t
+struct Api {
+    int (*get_unique_id)(UniqueId*) = nullptr;
+    int (*comm_init_rank)(Comm*, int, UniqueId, int) = nullptr;
+    int (*all_reduce)(const void*, void*, size_t, int, int, Comm, cudaStream_t) = nullptr;
+    int (*comm_destroy)(Comm) = nullptr;
+    const char* (*error_string)(int) = nullptr;
+    bool ok = false;
+    std::string why;
+};
+Api& api() {
+    static Api a = [] {
+        Api x;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            x.why = std::string("libnccl.so.2 not loadable: ") + dlerror();
+            return x;
+        }
+        x.get_unique_id = (int (*)(UniqueId*))dlsym(h, "ncclGetUniqueId");
+        x.comm_init_rank = (int (*)(Comm*, int, UniqueId, int))dlsym(h, "ncclCommInitRank");
+        x.all_reduce = (int (*)(const void*, void*, size_t, int, int, Comm, cudaStream_t))dlsym(
+            h, "ncclAllReduce");
+        x.comm_destroy = (int (*)(Comm))dlsym(h, "ncclCommDestroy");
+        x.error_string = (const char* (*)(int))dlsym(h, "ncclGetErrorString");
+        x.ok = x.get_unique_id && x.comm_init_rank && x.all_reduce && x.comm_destroy;
+        if (!x.ok) x.why = "libnccl.so.2 lacks the expected symbols";
+        return x;
+    }();
+    return a;
+}
+void check(int rc, const char* what) {
+    if (rc != 0)
+        throw Error(SKYGPU_ERUNTIME, std::string(what) + " failed: " +
+                                         (api().error_string ? api().error_string(rc) : "?"));
+}
+}  // namespace nccl
+
 void shard_allreduce_max(Ctx& c, void* dev_ptr, uint64_t count, int elem_bytes) {
-    if (!c.coll || c.shard_world <= 1 || count == 0) return;
+    if (c.shard_world <= 1 || count == 0) return;
+    if (c.nccl) {  // stream-ordered, in place; no host synchronisation
+        if (c.nccl_world != c.shard_world || c.nccl_rank != c.shard_rank)
+            invalid("sharded pipeline: shard rank/world differ from the NCCL group's");
+        nccl::check(nccl::api().all_reduce(dev_ptr, dev_ptr, count,
+                                           elem_bytes == 1 ? nccl::kUint8 : nccl::kInt32,
+                                           nccl::kMax, (nccl::Comm)c.nccl, c.stream),
+                    "ncclAllReduce");
+        return;
+    }
+    if (!c.coll) return;
     SKY_CUDA(cudaStreamSynchronize(c.stream));  // the reduced data is complete
     const int rc = c.coll(dev_ptr, count, elem_bytes, (void*)c.stream, c.coll_user);
     if (rc != 0)
@@ -719,8 +778,9 @@ int skygpu_pipeline(const double* vals, const int64_t* ids, uint64_t n, int d,
         struct ShardScope {
             Ctx& c;
             ShardScope(Ctx& cc, int r, int w) : c(cc) {
-                c.shard_rank = c.coll ? r : 0;
-                c.shard_world = c.coll ? w : 1;
+                const bool coll = c.coll || c.nccl;
+                c.shard_rank = coll ? r : 0;
+                c.shard_world = coll ? w : 1;
             }
             ~ShardScope() {
                 c.shard_rank = 0;
@@ -979,6 +1039,61 @@ int skygpu_select_representatives(const double* vals, const int64_t* ids, uint64
         *out_n = m;
         *tests = ht;
         end_stats(c);
+    });
+}
+
+int skygpu_nccl_unique_id(void* out_id128, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        if (!out_id128) invalid("nccl_unique_id: out is NULL");
+        if (!nccl::api().ok) throw Error(SKYGPU_ERUNTIME, nccl::api().why);
+        nccl::UniqueId id;
+        nccl::check(nccl::api().get_unique_id(&id), "ncclGetUniqueId");
+        memcpy(out_id128, &id, sizeof(id));
+    });
+}
+
+int skygpu_nccl_init(const void* id128, int nranks, int rank, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        if (!id128) invalid("nccl_init: id is NULL");
+        if (nranks < 1 || rank < 0 || rank >= nranks) invalid("nccl_init: bad rank / nranks");
+        if (!nccl::api().ok) throw Error(SKYGPU_ERUNTIME, nccl::api().why);
+        Ctx& c = ctx();
+        if (c.nccl) {
+            nccl::api().comm_destroy((nccl::Comm)c.nccl);
+            c.nccl = nullptr;
+        }
+        nccl::UniqueId id;
+        memcpy(&id, id128, sizeof(id));
+        nccl::Comm comm = nullptr;
+        nccl::check(nccl::api().comm_init_rank(&comm, nranks, id, rank), "ncclCommInitRank");
+        c.nccl = comm;
+        c.nccl_rank = rank;
+        c.nccl_world = nranks;
+    });
+}
+
+int skygpu_nccl_release(void) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return SKYGPU_ECUDA;
+    if (g_ctx[dev] && g_ctx[dev]->nccl) {
+        cudaStreamSynchronize(g_ctx[dev]->stream);
+        nccl::api().comm_destroy((nccl::Comm)g_ctx[dev]->nccl);
+        g_ctx[dev]->nccl = nullptr;
+        g_ctx[dev]->nccl_rank = 0;
+        g_ctx[dev]->nccl_world = 1;
+    }
+    return SKYGPU_OK;
+}
+
+int skygpu_cells_step_plan(const double* col_max, int d, int g_max, uint64_t s, int rank,
+                           int world, int* out_steps, int* out_n, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        if (d < 1 || d > kMaxDims) invalid("cells_step_plan: dims must be in [1, 32]");
+        if (world < 1 || rank < 0 || rank >= world) invalid("cells_step_plan: bad rank / world");
+        const std::vector<double> amax(col_max, col_max + d);
+        const std::vector<int> st = cells_step_plan(amax, d, g_max, s, rank, world);
+        for (size_t i = 0; i < st.size(); ++i) out_steps[i] = st[i];
+        *out_n = (int)st.size();
     });
 }
 

@@ -270,29 +270,31 @@ __global__ void k_cells_query(const double* __restrict__ v, uint64_t S, CellGeom
 // ---- packed-code variants: the codes floor(v*g) of every step computed
 // once (one byte per attribute, codes <= 127 on this engine's path), so each
 // step reads S code words instead of S x d float64 values, twice
+// the steps whose codes one launch computes (descending g; <= 64 at a time)
+struct StepList {
+    int n;
+    int g[64];
+};
+
 template <class CW>
-__global__ void k_cells_codes(const double* __restrict__ v, uint64_t S, int d, int g_hi, int G,
+__global__ void k_cells_codes(const double* __restrict__ v, uint64_t S, int d, StepList steps,
                               CW* __restrict__ codes) {
     pdl_wait();
-    // one thread per tuple: its d values read once, the codes of all G steps
-    // written (coalesced across the warp at every step)
+    // one thread per tuple: its d values read once, the codes of the listed
+    // steps written (coalesced across the warp at every step)
     for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < S;
          t += (uint64_t)gridDim.x * blockDim.x) {
         double x[8];
         for (int k = 0; k < d; ++k) x[k] = v[(uint64_t)k * S + t];
-        for (int gi = 0; gi < G; ++gi) {
-            const double gd = (double)(g_hi - gi);
+        for (int li = 0; li < steps.n; ++li) {
+            const double gd = (double)steps.g[li];
             CW w = 0;
             for (int k = 0; k < d; ++k) w |= (CW)(unsigned)floor(__dmul_rn(x[k], gd)) << (8 * k);
-            codes[(uint64_t)gi * S + t] = w;
+            codes[(uint64_t)li * S + t] = w;
         }
     }
 }
 
-// marking skips a bit that is already set (a plain read first): at small
-// steps millions of tuples share a few thousand words, and the atomics on
-// those words serialise (g = 2: 0.73 ms) while the reads hit L1/L2.  A
-// stale 0 only costs the atomic; bits are never cleared within a step.
 template <class W, class CW>
 __global__ void k_cells_mark_c(const CW* __restrict__ code, uint64_t S, CellGeom geo,
                                W* __restrict__ rows, const unsigned long long* live) {
@@ -610,15 +612,55 @@ bool gres_cells_smem_spec(Ctx& c, const double* d_skyv, uint64_t S, int d, int c
 // denominators into d_den (pre-zeroed); returns false (nothing done) when the
 // engine does not apply.  Runs steps g_max .. 2, stopping once every
 // candidate has its answer.
+// The steps a shard of the scan runs (shard_world > 1: the cell engine is
+// split by STEP, every candidate on every rank — den = the MAX over ranks of
+// each rank's largest dominated step, so one MAX all-reduce combines them).
+// Longest-processing-time assignment over a per-step cost model (grid bytes
+// swept ~7 x rows x word, plus the mark and query reads of S codes); the
+// same on every rank (it depends only on the replicated skyline).
+std::vector<int> cells_step_plan(const std::vector<double>& amax, int d, int g_max, uint64_t S,
+                                 int rank, int world) {
+    std::vector<int> mine;
+    if (world <= 1) {
+        for (int g = g_max; g >= 2; --g) mine.push_back(g);
+        return mine;
+    }
+    std::vector<std::pair<double, int>> cost;
+    for (int g = g_max; g >= 2; --g) {
+        CellGeom geo;
+        uint64_t e0 = 0;
+        const double rows = cells_geometry(amax, d, g, ~0ULL, &geo, &e0) ? (double)geo.rows : 0.0;
+        cost.push_back({7.0 * 4.0 * rows + 24.0 * (double)S, g});
+    }
+    std::stable_sort(cost.begin(), cost.end(),
+                     [](const std::pair<double, int>& x, const std::pair<double, int>& y) {
+                         return x.first > y.first;
+                     });
+    std::vector<double> load(world, 0.0);
+    for (const auto& cg : cost) {
+        int best = 0;
+        for (int r = 1; r < world; ++r)
+            if (load[r] < load[best]) best = r;
+        load[best] += cg.first;
+        if (best == rank) mine.push_back(cg.second);
+    }
+    std::sort(mine.begin(), mine.end(), [](int x, int y) { return x > y; });
+    return mine;
+}
+
+// Cell engine over S skyline tuples (SoA d_skyv), candidates act[0..na),
+// denominators into d_den (pre-zeroed); returns false (nothing done) when the
+// engine does not apply.  Runs this shard's steps (all of g_max .. 2 when
+// unsharded) in descending order, each step's candidates the previous step's
+// undecided ones.
 bool gres_cells_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_max,
                        const uint32_t* act, uint64_t na, int32_t* d_den, uint64_t* cells_swept,
-                       int* steps_run) {
+                       int* steps_run, int step_rank, int step_world) {
     if (g_max < 2 || S == 0 || d > kMaxCellDims) return false;
     auto* colmax = c.buf[B_AMAX].as<unsigned long long>(kMaxDims);
     SKY_CUDA(cudaMemsetAsync(colmax, 0, sizeof(unsigned long long) * kMaxDims, c.stream));
     pdl_launch(k_col_max, dim3(grid_for(S, kBlock, 296), (unsigned)d), kBlock, 0, c.stream, d_skyv,
-               S, d,
-                                                                                    colmax);
+               S, d, colmax);
     SKY_LAUNCH_CHECK();
     note_launch(c);
     std::vector<unsigned long long> bits(d);
@@ -633,25 +675,25 @@ bool gres_cells_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_ma
     uint64_t e0 = 0;
     if (!cells_geometry(amax, d, g_max, budget_rows, &geo0, &e0)) return false;
     const bool w64 = e0 > 32;
-    void* rows = c.buf[B_CELLS].get(geo0.rows * (w64 ? 8 : 4));
-    // codes of every step, once (packed bytes; d <= 8 here), within 16 GiB
+    const std::vector<int> steps = cells_step_plan(amax, d, g_max, S, step_rank, step_world);
+    *cells_swept = 0;
+    *steps_run = 0;
+    if (steps.empty()) return true;  // (more ranks than steps: nothing here)
+    {
+        CellGeom gt;
+        uint64_t et = 0;
+        cells_geometry(amax, d, steps[0], budget_rows, &gt, &et);
+        c.buf[B_CELLS].get(gt.rows * (w64 ? 8 : 4));
+    }
+    void* rows = c.buf[B_CELLS].p;
+    // codes of up to 64 steps at a time (packed bytes; d <= 8 here)
     const bool cw32 = d <= 4;
     const size_t cwb = cw32 ? 4 : 8;
-    const int G = g_max - 1;
-    void* codes = nullptr;
-    if (d <= 8 && S * (uint64_t)G * cwb <= (16ull << 30)) {
-        codes = c.buf[B_CODES].get(S * (uint64_t)G * cwb);
-        if (cw32)
-            pdl_launch(k_cells_codes<uint32_t>, grid_for(S, kBlock), kBlock, 0, c.stream,
-                d_skyv, S, d, g_max, G, (uint32_t*)codes);
-        else
-            pdl_launch(k_cells_codes<unsigned long long>, grid_for(S, kBlock), kBlock, 0, c.stream,
-                d_skyv, S, d, g_max, G, (unsigned long long*)codes);
-        SKY_LAUNCH_CHECK();
-        note_launch(c);
-    }
-    uint64_t swept = codes ? S * (uint64_t)d * sizeof(double) + S * (uint64_t)G * cwb : 0;
-    int steps = 0;
+    const uint64_t chunk = std::min<uint64_t>(64, steps.size());
+    const bool use_codes = d <= 8 && S * chunk * cwb <= (16ull << 30);
+    void* codes = use_codes ? c.buf[B_CODES].get(S * chunk * cwb) : nullptr;
+    uint64_t swept = 0;
+    int nrun = 0;
     const char* uf = getenv("SKYGPU_CELLS_UNFUSED");
     const bool fused = !(uf && uf[0] == '1');
     // undecided candidates ping-pong between two lists; a step's count lives
@@ -662,57 +704,76 @@ bool gres_cells_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_ma
     const uint32_t* in = act;
     const unsigned long long* n_in = nullptr;
     int cur = 0;
-    for (int g = g_max; g >= 2; --g) {
-        CellGeom geo;
-        uint64_t e0g = 0;
-        cells_geometry(amax, d, g, budget_rows, &geo, &e0g);
-        const size_t wb = w64 ? 8 : 4;
-        const uint64_t n16 = (geo.rows * wb + 15) / 16;
-        pdl_launch(k_cells_zero, grid_for(n16, kBlock), kBlock, 0, c.stream, (uint4*)rows, n16, n_in);
-        pdl_launch(k_clear_slot_c, 1, 1, 0, c.stream, cnt[cur]);
-        const unsigned gs = grid_for(S, kBlock);
-        const unsigned gq = grid_for(na, kBlock);
-        auto run_codes = [&](auto* R, auto* cg) {
-            using WR = std::remove_pointer_t<decltype(R)>;
-            using CW = std::remove_const_t<std::remove_pointer_t<decltype(cg)>>;
-            pdl_launch(k_cells_mark_c<WR, CW>, gs, kBlock, 0, c.stream, cg, S, geo, R, n_in);
-            sweeps<WR>(c, R, geo, fused, n_in);
-            pdl_launch(k_cells_query_c<WR, CW>, gq, kBlock, 0, c.stream, cg, geo,
-                       (const WR*)R, in, na, n_in, d_den, lists[cur], cnt[cur]);
-        };
-        auto run_vals = [&](auto* R) {
-            using WR = std::remove_pointer_t<decltype(R)>;
-            pdl_launch(k_cells_mark<WR>, gs, kBlock, 0, c.stream, d_skyv, S, geo, R, n_in);
-            sweeps<WR>(c, R, geo, fused, n_in);
-            pdl_launch(k_cells_query<WR>, gq, kBlock, 0, c.stream, d_skyv, S, geo, (const WR*)R,
-                       in, na, n_in, d_den, lists[cur], cnt[cur]);
-        };
-        const uint64_t coff = (uint64_t)(g_max - g) * S;
-        if (codes && w64 && cw32)
-            run_codes(static_cast<unsigned long long*>(rows), (const uint32_t*)codes + coff);
-        else if (codes && w64)
-            run_codes(static_cast<unsigned long long*>(rows), (const unsigned long long*)codes + coff);
-        else if (codes && cw32)
-            run_codes(static_cast<unsigned*>(rows), (const uint32_t*)codes + coff);
-        else if (codes)
-            run_codes(static_cast<unsigned*>(rows), (const unsigned long long*)codes + coff);
-        else if (w64)
-            run_vals(static_cast<unsigned long long*>(rows));
-        else
-            run_vals(static_cast<unsigned*>(rows));
-        SKY_LAUNCH_CHECK();
-        note_launch(c, 4);
-        // algorithmic bytes of the step: the grid zeroed, read and written
-        // once by an ideal fused prefix-OR, plus the mark and query reads of
-        // the S x d values
-        swept += 3 * geo.rows * wb + 2 * S * (codes ? cwb : (uint64_t)d * sizeof(double));
-        ++steps;
-        in = lists[cur];
-        n_in = cnt[cur];
-        cur ^= 1;
+    for (size_t s0 = 0; s0 < steps.size(); s0 += chunk) {
+        StepList sl;
+        sl.n = (int)std::min<uint64_t>(chunk, steps.size() - s0);
+        for (int i = 0; i < sl.n; ++i) sl.g[i] = steps[s0 + i];
+        if (codes) {
+            if (cw32)
+                pdl_launch(k_cells_codes<uint32_t>, grid_for(S, kBlock), kBlock, 0, c.stream,
+                           d_skyv, S, d, sl, (uint32_t*)codes);
+            else
+                pdl_launch(k_cells_codes<unsigned long long>, grid_for(S, kBlock), kBlock, 0,
+                           c.stream, d_skyv, S, d, sl, (unsigned long long*)codes);
+            SKY_LAUNCH_CHECK();
+            note_launch(c);
+            swept += S * (uint64_t)d * sizeof(double) + S * (uint64_t)sl.n * cwb;
+        }
+        for (int li = 0; li < sl.n; ++li) {
+            const int g = sl.g[li];
+            CellGeom geo;
+            uint64_t e0g = 0;
+            cells_geometry(amax, d, g, budget_rows, &geo, &e0g);
+            const size_t wb = w64 ? 8 : 4;
+            const uint64_t n16 = (geo.rows * wb + 15) / 16;
+            pdl_launch(k_cells_zero, grid_for(n16, kBlock), kBlock, 0, c.stream, (uint4*)rows, n16,
+                       n_in);
+            pdl_launch(k_clear_slot_c, 1, 1, 0, c.stream, cnt[cur]);
+            const unsigned gs = grid_for(S, kBlock);
+            const unsigned gq = grid_for(na, kBlock);
+            auto run_codes = [&](auto* R, auto* cg) {
+                using WR = std::remove_pointer_t<decltype(R)>;
+                using CW = std::remove_const_t<std::remove_pointer_t<decltype(cg)>>;
+                pdl_launch(k_cells_mark_c<WR, CW>, gs, kBlock, 0, c.stream, cg, S, geo, R, n_in);
+                sweeps<WR>(c, R, geo, fused, n_in);
+                pdl_launch(k_cells_query_c<WR, CW>, gq, kBlock, 0, c.stream, cg, geo,
+                           (const WR*)R, in, na, n_in, d_den, lists[cur], cnt[cur]);
+            };
+            auto run_vals = [&](auto* R) {
+                using WR = std::remove_pointer_t<decltype(R)>;
+                pdl_launch(k_cells_mark<WR>, gs, kBlock, 0, c.stream, d_skyv, S, geo, R, n_in);
+                sweeps<WR>(c, R, geo, fused, n_in);
+                pdl_launch(k_cells_query<WR>, gq, kBlock, 0, c.stream, d_skyv, S, geo,
+                           (const WR*)R, in, na, n_in, d_den, lists[cur], cnt[cur]);
+            };
+            const uint64_t coff = (uint64_t)li * S;
+            if (codes && w64 && cw32)
+                run_codes(static_cast<unsigned long long*>(rows), (const uint32_t*)codes + coff);
+            else if (codes && w64)
+                run_codes(static_cast<unsigned long long*>(rows),
+                          (const unsigned long long*)codes + coff);
+            else if (codes && cw32)
+                run_codes(static_cast<unsigned*>(rows), (const uint32_t*)codes + coff);
+            else if (codes)
+                run_codes(static_cast<unsigned*>(rows), (const unsigned long long*)codes + coff);
+            else if (w64)
+                run_vals(static_cast<unsigned long long*>(rows));
+            else
+                run_vals(static_cast<unsigned*>(rows));
+            SKY_LAUNCH_CHECK();
+            note_launch(c, 4);
+            // algorithmic bytes of the step: the grid zeroed, read and
+            // written once by an ideal fused prefix-OR, plus the mark and
+            // query reads of the S codes (or values)
+            swept += 3 * geo.rows * wb + 2 * S * (codes ? cwb : (uint64_t)d * sizeof(double));
+            ++nrun;
+            in = lists[cur];
+            n_in = cnt[cur];
+            cur ^= 1;
+        }
     }
     *cells_swept = swept;
-    *steps_run = steps;
+    *steps_run = nrun;
     return true;
 }
 

@@ -792,7 +792,7 @@ GresOut gres_device(Ctx& c, const double* d_skyv, const int64_t* d_ids, uint64_t
     const int G = out.g_max - 1;
     // cell-occupancy engine (cells.cu): asked for, or AUTO on huge skylines
     // where the pair engine's O(S^2) tests dominate
-    const bool want_cells = u8 && G >= 1 && na > 0 &&
+    const bool want_cells = u8 && G >= 1 && (na > 0 || shard_world > 1) &&
                             (engine == SKYGPU_GRES_CELLS ||
                              (engine == SKYGPU_GRES_AUTO && S >= (1u << 18)));
     // small grids (d <= 4): every step in one launch, grids in shared memory
@@ -817,10 +817,25 @@ GresOut gres_device(Ctx& c, const double* d_skyv, const int64_t* d_ids, uint64_t
     if (want_cells) {
         uint64_t swept = 0;
         int steps_run = 0;
+        // sharded: the cell engine splits the STEPS over the shards (every
+        // candidate on every rank; a rank's den = its largest dominated step,
+        // 1 if none — the MAX over ranks is the reference's map), instead of
+        // the tuples: the grid build of a step is the cost, not its queries
+        uint32_t* cact = act;
+        uint64_t cna = na;
+        if (shard_world > 1) {
+            cact = c.buf[B_ACT1].as<uint32_t>(S);
+            cna = S;
+            pdl_launch(k_shard_iota, grid_for(S, kBlock), kBlock, 0, c.stream, S, 0, 1, cact);
+            SKY_LAUNCH_CHECK();
+            note_launch(c);
+        }
         SKY_CUDA(cudaEventRecord(e0, c.stream));
-        if (gres_cells_device(c, d_skyv, S, d, out.g_max, act, na, d_den, &swept, &steps_run)) {
+        if (gres_cells_device(c, d_skyv, S, d, out.g_max, cact, cna, d_den, &swept, &steps_run,
+                              shard_rank, shard_world)) {
             SKY_CUDA(cudaEventRecord(e1, c.stream));
-            pdl_launch(k_finalize_den, grid_for(na, kBlock), kBlock, 0, c.stream, act, na, d_den);
+            pdl_launch(k_finalize_den, grid_for(cna, kBlock), kBlock, 0, c.stream, cact, cna,
+                       d_den);
             SKY_LAUNCH_CHECK();
             note_launch(c);
             c.gres_timing_pending = true;

@@ -150,6 +150,10 @@ struct Ctx {
     // sharded pipeline call in progress (skygpu_set_collective installed)
     skygpu_allreduce_max_fn coll = nullptr;
     void* coll_user = nullptr;
+    // NCCL communicator of the shard group (skygpu_nccl_init): when set, the
+    // exchange steps are ncclAllReduce(MAX) queued on this context's stream
+    void* nccl = nullptr;
+    int nccl_rank = 0, nccl_world = 1;
     int shard_rank = 0, shard_world = 1;
     cudaEvent_t xev[10];          // chunk-ready events of the streamed input
     cudaEvent_t tev[96];
@@ -328,9 +332,13 @@ bool gres_spec_failed(Ctx& c);
 void check_grid_projection(Ctx& c, const double* d_skyv, uint64_t S, int d, int g);
 
 // cells.cu: the cell-occupancy gres engine; false when it does not apply
+// step_rank / step_world: this shard's steps of the scan (cells_step_plan);
+// (0, 1) runs them all
 bool gres_cells_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_max,
                        const uint32_t* act, uint64_t na, int32_t* d_den, uint64_t* cells_swept,
-                       int* steps_run);
+                       int* steps_run, int step_rank = 0, int step_world = 1);
+std::vector<int> cells_step_plan(const std::vector<double>& amax, int d, int g_max, uint64_t S,
+                                 int rank, int world);
 // cells.cu: the same engine with every step in one launch and the grids in
 // shared memory (d <= 4, small code extents); false when it does not apply
 bool gres_cells_smem_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_max,

@@ -1,15 +1,23 @@
 """Multi-GPU plumbing for the grid-resistance path.
 
 One process per GPU (torchrun), the relation replicated on every rank.  The
-gres work is sharded by SKYLINE TUPLE: rank r owns the interleaved 256-tuple
-chunks r, r + world, r + 2*world, ... of the skyline (libskygpu's
-k_shard_iota; interleaving balances the early-exit work, SURVEY.md §7.4
-item 5).  Each rank writes the denominators of its own tuples and 0 for the
-others, so one MAX all-reduce (NCCL over NVLink on GPUs, gloo on CPU) yields
-the full map.  With install_collective(), the library also splits the
-rank-grid skyline engine (large skylines, BASELINE config 5) by grid row and
-MAX-reduces its keep flags — the second exchange — and returns the full map
-on every rank by itself.
+library splits the work itself (skygpu_pipeline shard_rank / shard_world):
+
+* rank-grid skyline engine (large skylines, BASELINE config 5): by grid ROW
+  (row % world == rank), keep flags MAX-reduced;
+* cell-occupancy resistance engine (huge skylines): by STEP g of the scan
+  (longest-processing-time over the per-step cost, cells.cu
+  cells_step_plan), every candidate on every rank, den MAX-reduced;
+* pair engines: by SKYLINE TUPLE — interleaved 256-tuple chunks r, r + world,
+  ... (k_shard_iota; interleaving balances the early-exit work, SURVEY.md
+  §7.4 item 5), den MAX-reduced.
+
+init_library_nccl() gives the library its OWN NCCL communicator (the unique
+id made by rank 0 and broadcast over torch.distributed): the exchanges are
+then ncclAllReduce(MAX) queued on the library's stream, no host sync.
+install_collective() is the older route through a torch.distributed callback.
+Without either, only the resistance stage is sharded and the caller reduces
+the map (combine_denominators).
 """
 from __future__ import annotations
 
@@ -27,6 +35,22 @@ def owned_positions(S: int, rank: int, world: int) -> np.ndarray:
     """Ascending skyline positions owned by `rank` (the kernel's candidate list)."""
     idx = np.arange(S, dtype=np.int64)
     return idx[shard_owner(idx, world) == rank]
+
+
+def init_library_nccl(group=None):
+    """Give libskygpu its own NCCL group over the torch.distributed world:
+    rank 0 makes the unique id, a broadcast ships it (any backend: gloo on
+    CPU works), every rank joins on the library's current device."""
+    import torch.distributed as dist
+
+    from . import skypar
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    uid = skypar.nccl_unique_id() if rank == 0 else bytes(128)
+    obj = [uid]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    skypar.nccl_init(obj[0], world, rank)
+    return rank, world
 
 
 def combine_denominators(partial, group=None):

@@ -128,7 +128,9 @@ EXPORTED_SYMBOLS = ("skygpu_version", "skygpu_device_count", "skygpu_set_device"
                     "skygpu_grid_resistance", "skygpu_snap_relation", "skygpu_max_grid_intervals",
                     "skygpu_pipeline", "skygpu_generate", "skygpu_sfs_accounting",
                     "skygpu_set_collective", "skygpu_normalize", "skygpu_select_representatives",
-                    "skygpu_read_csv", "skygpu_pipeline_csv", "skygpu_host_buffer")
+                    "skygpu_read_csv", "skygpu_pipeline_csv", "skygpu_host_buffer",
+                    "skygpu_nccl_unique_id", "skygpu_nccl_init", "skygpu_nccl_release",
+                    "skygpu_cells_step_plan")
 
 
 def _check(rc: int, err: C.Array) -> None:
@@ -369,6 +371,41 @@ def sfs_accounting(values, ids, pids, partitions: int, reps=None) -> Accounting:
                                        _p(per), _p(fin), _p(into), _p(pos), _p(cnt), err, 1024), err)
     return Accounting(per[:int(partitions)].copy(), int(fin[0]), int(into[0]),
                       pos[:int(cnt[0])].astype(np.int64))
+
+
+def cells_step_plan(col_max, g_max: int, s: int, rank: int, world: int) -> list:
+    """Steps of the cell engine's scan that shard `rank` of `world` runs
+    (host only; the split of a sharded pipeline call)."""
+    cm = np.ascontiguousarray(col_max, dtype=np.float64)
+    out = np.zeros(max(int(g_max), 1), dtype=np.int32)
+    n = np.zeros(1, dtype=np.int32)
+    err = _errbuf()
+    _check(lib().skygpu_cells_step_plan(_p(cm), len(cm), int(g_max), int(s), int(rank), int(world),
+                                        _p(out), _p(n), err, 1024), err)
+    return out[:int(n[0])].tolist()
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (skygpu_nccl_unique_id) — made on one rank,
+    shipped to the others out of band."""
+    buf = C.create_string_buffer(128)
+    err = _errbuf()
+    _check(lib().skygpu_nccl_unique_id(buf, err, 1024), err)
+    return buf.raw
+
+
+def nccl_init(uid: bytes, nranks: int, rank: int) -> None:
+    """Join the library's own NCCL group on the current device: sharded
+    pipeline calls then MAX-all-reduce in place on the library's stream."""
+    if len(uid) != 128:
+        raise ValueError("nccl_init: the unique id is 128 bytes")
+    err = _errbuf()
+    _check(lib().skygpu_nccl_init(C.create_string_buffer(uid, 128), int(nranks), int(rank), err,
+                                  1024), err)
+
+
+def nccl_release() -> None:
+    lib().skygpu_nccl_release()
 
 
 # skygpu_allreduce_max_fn(dev_ptr, count, elem_bytes, cuda_stream, user) -> int

@@ -103,6 +103,39 @@ def test_shards_max_reduce_to_full_map(world):
     assert acc.tolist() == full.den.tolist()
 
 
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_step_sharded_cells_max_reduce_to_full_map(world):
+    """Cell engine, sharded by STEP (cells_step_plan): each shard's map is its
+    largest dominated step (1 if none); the MAX over shards is the full map,
+    and each shard ran exactly its planned steps."""
+    v = sk.generate("ant", 60000, 5, 41)
+    full = sk.pipeline(v, cap=25, engine=sk.GRES_CELLS)
+    assert full.stats["gres_engine"] == sk.GRES_CELLS
+    acc = np.zeros_like(full.den)
+    for r in range(world):
+        part = sk.pipeline(v, cap=25, engine=sk.GRES_CELLS, shard_rank=r, shard_world=world)
+        assert part.positions.tolist() == full.positions.tolist()
+        assert (part.den >= 1).all() and (part.den <= full.den).all()
+        acc = np.maximum(acc, part.den)
+    assert acc.tolist() == full.den.tolist()
+
+
+def test_library_nccl_group_of_one():
+    """The library's own NCCL path on one GPU: a group of one joins, sharded
+    calls with world 1 run unchanged, the group is released."""
+    from paper_2412_02274_b200 import skypar
+    uid = skypar.nccl_unique_id()
+    assert len(uid) == 128
+    skypar.nccl_init(uid, 1, 0)
+    try:
+        v = sk.generate("ant", 300000, 7, 3)
+        a = sk.pipeline(v, cap=25, shard_rank=0, shard_world=1)
+    finally:
+        skypar.nccl_release()
+    b = sk.pipeline(v, cap=25)
+    assert a.positions.tolist() == b.positions.tolist() and a.den.tolist() == b.den.tolist()
+
+
 def test_api_kats():
     # proj/tests/test_gres.cpp:26-34, 61-73, 91-97, 163-170, 172-177
     assert sk.snap_to_grid([0.30, 0.62], 5).tolist() == [0.2, 0.6]
