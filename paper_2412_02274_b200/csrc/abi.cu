@@ -359,8 +359,13 @@ struct Api {
 Api& api() {
     static Api a = [] {
         Api x;
-        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        // the copy already in the process first (torch's, when torch was
+        // imported: a second NCCL of the same soname would be bound by
+        // torch's own references), then SKYGPU_NCCL_LIB, then the system's;
+        // loaded RTLD_LOCAL so it never shadows another copy's symbols
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h && getenv("SKYGPU_NCCL_LIB")) h = dlopen(getenv("SKYGPU_NCCL_LIB"), RTLD_NOW | RTLD_LOCAL);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
         if (!h) {
             x.why = std::string("libnccl.so.2 not loadable: ") + dlerror();
             return x;

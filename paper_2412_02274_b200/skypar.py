@@ -385,9 +385,22 @@ def cells_step_plan(col_max, g_max: int, s: int, rank: int, world: int) -> list:
     return out[:int(n[0])].tolist()
 
 
+def _share_torch_nccl() -> None:
+    """Load torch (and with it torch's libnccl.so.2) before the library
+    loads NCCL, so the process holds ONE NCCL copy: libskygpu then binds the
+    copy already present (RTLD_NOLOAD) instead of the system's older one,
+    which torch's own NCCL references would otherwise resolve to."""
+    try:
+        import torch  # noqa: F401
+        torch.cuda.is_available()
+    except Exception:
+        pass
+
+
 def nccl_unique_id() -> bytes:
     """128-byte NCCL unique id (skygpu_nccl_unique_id) — made on one rank,
     shipped to the others out of band."""
+    _share_torch_nccl()
     buf = C.create_string_buffer(128)
     err = _errbuf()
     _check(lib().skygpu_nccl_unique_id(buf, err, 1024), err)
@@ -399,6 +412,7 @@ def nccl_init(uid: bytes, nranks: int, rank: int) -> None:
     pipeline calls then MAX-all-reduce in place on the library's stream."""
     if len(uid) != 128:
         raise ValueError("nccl_init: the unique id is 128 bytes")
+    _share_torch_nccl()
     err = _errbuf()
     _check(lib().skygpu_nccl_init(C.create_string_buffer(uid, 128), int(nranks), int(rank), err,
                                   1024), err)
