@@ -452,6 +452,328 @@ void sweeps(Ctx& c, W* R, const CellGeom& geo, bool fused, const unsigned long l
     }
 }
 
+// ---------------------------------------------------------------------------
+// Min-grid form (the default for packed codes).  The bitset row above is,
+// after its in-word prefix-OR, a run of ones from the smallest attribute-0
+// code of any tuple whose other codes are <= the row's: the whole row is that
+// ONE number.  So the grid stores, per cell of the remaining d-1 attributes,
+//     M[r] = min { c_m(s) : row(s) <= r componentwise }   (0xFF: none)
+// one byte instead of a 32/64-bit word, and t (code c, row r) is dominated iff
+//     M[r] < c_m(t)   or   M[r - e_j] <= c_m(t)   for a grid attribute j, c_j >= 1
+// (the same two cases as the bitset query: a strictly smaller code on the
+// min'd attribute m in a row <= r, or a row strictly below r with a code <=).
+// The min'd attribute m is the one with the largest extent (smallest grid).
+// Byte grids are 4x smaller than u32 rows, so a step's grid is written once,
+// swept in three passes (d = 7) of SIMD byte minima (__vminu4), and every
+// step below g ~ 22 of C5 stays resident in the 126 MB L2 across its passes.
+// Grid dim 0 (the fastest) is padded to a multiple of 4 bytes so that every
+// other dim's stride is a whole number of u32 words.
+namespace {
+
+struct MinGeom {
+    int nd;                        // grid dims (d - 1)
+    int m;                         // the min'd attribute
+    int g;
+    uint32_t attr[kMaxCellDims];   // attribute of grid dim k
+    uint32_t ext[kMaxCellDims];    // its code extent (grid dim 0: padded to 4)
+    uint64_t stride[kMaxCellDims]; // its byte stride (stride[0] = 1)
+    uint64_t bytes;                // grid bytes (a multiple of 16)
+};
+
+template <class CW>
+__device__ __forceinline__ uint64_t mg_row(CW w, const MinGeom& geo) {
+    uint64_t r = 0;
+    for (int k = 0; k < geo.nd; ++k)
+        r += (uint64_t)((uint32_t)(w >> (8 * geo.attr[k])) & 0xFFu) * geo.stride[k];
+    return r;
+}
+
+__global__ void k_mg_fill(uint4* __restrict__ p, uint64_t n16, const unsigned long long* live) {
+    pdl_wait();
+    if (step_dead(live)) return;
+    const uint4 f = make_uint4(~0u, ~0u, ~0u, ~0u);
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n16;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        p[i] = f;
+}
+
+// every skyline tuple lowers its cell's byte to its code on attribute m
+// (a CAS on the containing word; a cell already <= is left alone)
+template <class CW>
+__global__ void k_mg_mark(const CW* __restrict__ code, uint64_t S, MinGeom geo,
+                          uint8_t* __restrict__ M, const unsigned long long* live) {
+    pdl_wait();
+    if (step_dead(live)) return;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < S;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const CW w = code[i];
+        const uint64_t r = mg_row(w, geo);
+        const uint32_t c0 = (uint32_t)(w >> (8 * geo.m)) & 0xFFu;
+        uint32_t* word = reinterpret_cast<uint32_t*>(M + (r & ~3ULL));
+        const uint32_t sh = 8u * (uint32_t)(r & 3u);
+        uint32_t old = *reinterpret_cast<volatile uint32_t*>(word);
+        while (((old >> sh) & 0xFFu) > c0) {
+            const uint32_t nw = (old & ~(0xFFu << sh)) | (c0 << sh);
+            const uint32_t prev = atomicCAS(word, old, nw);
+            if (prev == old) break;
+            old = prev;
+        }
+    }
+}
+
+// prefix minimum along the 4 bytes of a word (byte k = lower address first),
+// then against the previous word's last byte
+__device__ __forceinline__ uint32_t bytes_prefix_min(uint32_t x, uint32_t carry) {
+    x = __vminu4(x, (x << 8) | 0xFFu);
+    x = __vminu4(x, (x << 16) | 0xFFFFu);
+    return __vminu4(x, carry * 0x01010101u);
+}
+
+// grid dims 0, 1, 2 (as many as the slab has) of whole slabs in shared memory
+template <int ND>
+__global__ void __launch_bounds__(kBlock)
+k_mg_slab(uint32_t* __restrict__ M, uint64_t nwords, uint32_t w0, uint32_t e1, uint32_t e2,
+          uint32_t spb, const unsigned long long* live) {
+    pdl_wait();
+    if (step_dead(live)) return;
+    extern __shared__ __align__(16) uint32_t sw[];
+    const uint32_t slab = w0 * e1 * e2;  // words per slab
+    const uint64_t nslabs = nwords / slab;
+    for (uint64_t s0 = (uint64_t)blockIdx.x * spb; s0 < nslabs; s0 += (uint64_t)gridDim.x * spb) {
+        const uint32_t ns = (uint32_t)min((uint64_t)spb, nslabs - s0);
+        const uint32_t words = ns * slab;
+        const uint32_t* g = M + s0 * slab;
+        const bool vec = (words & 3u) == 0 && ((s0 * slab) & 3u) == 0;
+        if (vec) {
+            for (uint32_t i = threadIdx.x; i < words / 4; i += blockDim.x)
+                reinterpret_cast<uint4*>(sw)[i] = reinterpret_cast<const uint4*>(g)[i];
+        } else {
+            for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) sw[i] = g[i];
+        }
+        __syncthreads();
+        for (uint32_t l = threadIdx.x; l < words / w0; l += blockDim.x) {  // dim 0: bytes of a line
+            uint32_t* p = sw + (uint64_t)l * w0;
+            uint32_t carry = 0xFFu;
+            for (uint32_t a = 0; a < w0; ++a) {
+                const uint32_t x = bytes_prefix_min(p[a], carry);
+                p[a] = x;
+                carry = x >> 24;
+            }
+        }
+        __syncthreads();
+        if (ND >= 2) {  // dim 1: u32 columns, stride w0
+            for (uint32_t l = threadIdx.x; l < ns * e2 * w0; l += blockDim.x) {
+                uint32_t* p = sw + (uint64_t)(l / w0) * w0 * e1 + (l % w0);
+                uint32_t acc = ~0u;
+                for (uint32_t a = 0; a < e1; ++a) {
+                    acc = __vminu4(acc, p[a * w0]);
+                    p[a * w0] = acc;
+                }
+            }
+            __syncthreads();
+        }
+        if (ND >= 3) {  // dim 2: u32 columns, stride w0 * e1
+            const uint32_t plane = w0 * e1;
+            for (uint32_t l = threadIdx.x; l < ns * plane; l += blockDim.x) {
+                uint32_t* p = sw + (uint64_t)(l / plane) * slab + (l % plane);
+                uint32_t acc = ~0u;
+                for (uint32_t b = 0; b < e2; ++b) {
+                    acc = __vminu4(acc, p[b * plane]);
+                    p[b * plane] = acc;
+                }
+            }
+            __syncthreads();
+        }
+        uint32_t* o = M + s0 * slab;
+        if (vec) {
+            for (uint32_t i = threadIdx.x; i < words / 4; i += blockDim.x)
+                reinterpret_cast<uint4*>(o)[i] = reinterpret_cast<const uint4*>(sw)[i];
+        } else {
+            for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) o[i] = sw[i];
+        }
+        __syncthreads();
+    }
+}
+
+// two grid dims a, b = a + 1 at once (word stride sa of dim a), one thread
+// per u32 column of the (ea x eb) plane: P = min(v, P[x-1][y], P[x][y-1])
+template <int EA>
+__global__ void __launch_bounds__(kBlock)
+k_mg_pair(uint32_t* __restrict__ M, uint64_t nwords, uint32_t ea, uint32_t eb, uint64_t sa,
+          const unsigned long long* live) {
+    pdl_wait();
+    if (step_dead(live)) return;
+    const uint64_t plane = (uint64_t)ea * eb;
+    const uint64_t lines = nwords / plane;
+    for (uint64_t l = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; l < lines;
+         l += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t lo = l % sa, hi = l / sa;
+        uint32_t* base = M + hi * sa * plane + lo;
+        uint32_t prev[EA];
+#pragma unroll
+        for (int x = 0; x < EA; ++x) prev[x] = ~0u;
+        for (uint32_t y = 0; y < eb; ++y) {
+            uint32_t* p = base + (uint64_t)y * ea * sa;
+            uint32_t v[EA];
+#pragma unroll
+            for (int x = 0; x < EA; ++x) v[x] = (uint32_t)x < ea ? p[(uint64_t)x * sa] : ~0u;
+            uint32_t run = ~0u;
+#pragma unroll
+            for (int x = 0; x < EA; ++x) {
+                run = __vminu4(run, __vminu4(v[x], prev[x]));
+                prev[x] = run;
+                if ((uint32_t)x < ea) p[(uint64_t)x * sa] = run;
+            }
+        }
+    }
+}
+
+// one grid dim (word stride s, extent e): one thread per u32 column
+__global__ void k_mg_dim(uint32_t* __restrict__ M, uint64_t nwords, uint64_t e, uint64_t s,
+                         const unsigned long long* live) {
+    pdl_wait();
+    if (step_dead(live)) return;
+    const uint64_t lines = nwords / e;
+    for (uint64_t l = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; l < lines;
+         l += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t* p = M + (l / s) * s * e + (l % s);
+        uint32_t acc = ~0u;
+        for (uint64_t k = 0; k < e; ++k) {
+            acc = __vminu4(acc, p[k * s]);
+            p[k * s] = acc;
+        }
+    }
+}
+
+template <class CW>
+__global__ void k_mg_query(const CW* __restrict__ code, MinGeom geo, const uint8_t* __restrict__ M,
+                           const uint32_t* __restrict__ act_in, uint64_t na,
+                           const unsigned long long* n_in, int32_t* __restrict__ den,
+                           uint32_t* __restrict__ act_out, unsigned long long* __restrict__ n_out) {
+    pdl_wait();
+    if (n_in) na = *(volatile const unsigned long long*)n_in;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warp0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) & ~31ULL;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t k0 = warp0; k0 < na; k0 += stride) {
+        const uint64_t k = k0 + lane;
+        bool keep = false;
+        uint32_t t = 0;
+        if (k < na) {
+            t = act_in[k];
+            const CW w = code[t];
+            const uint64_t r = mg_row(w, geo);
+            const uint32_t c0 = (uint32_t)(w >> (8 * geo.m)) & 0xFFu;
+            bool hit = M[r] < c0;
+            for (int j = 0; j < geo.nd && !hit; ++j)
+                if ((uint32_t)(w >> (8 * geo.attr[j])) & 0xFFu) hit = M[r - geo.stride[j]] <= c0;
+            if (hit) den[t] = geo.g;
+            keep = !hit;
+        }
+        const unsigned msk = __ballot_sync(0xffffffffu, keep);
+        if (!msk) continue;
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(n_out, (unsigned long long)__popc(msk));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (keep) act_out[base + __popc(msk & ((1u << lane) - 1u))] = t;
+    }
+}
+
+}  // namespace
+
+// Min-grid geometry of step g; false when it does not apply (a code above
+// 127 or a grid beyond the budget).  m = the attribute of largest extent.
+static bool min_geometry(const std::vector<double>& amax, int d, int g, uint64_t budget,
+                         MinGeom* geo) {
+    if (d < 2 || d > 8) return false;
+    uint32_t e[8];
+    int m = 0;
+    for (int j = 0; j < d; ++j) {
+        const double k = std::floor(amax[j] * (double)g);  // same rounding as __dmul_rn
+        if (!(k >= 0) || k > 127) return false;
+        e[j] = (uint32_t)k + 1;
+        if (e[j] > e[m]) m = j;
+    }
+    geo->nd = d - 1;
+    geo->m = m;
+    geo->g = g;
+    uint64_t bytes = 1;
+    int k = 0;
+    for (int j = 0; j < d; ++j) {
+        if (j == m) continue;
+        const uint32_t ext = k == 0 ? (e[j] + 3u) & ~3u : e[j];
+        geo->attr[k] = (uint32_t)j;
+        geo->ext[k] = ext;
+        geo->stride[k] = bytes;
+        if (bytes > budget / ext) return false;
+        bytes *= ext;
+        ++k;
+    }
+    geo->bytes = (bytes + 15) & ~15ULL;
+    return true;
+}
+
+// the prefix minimum over every grid dim: dims 0..2 in a shared-memory slab
+// pass, the rest two at a time in registers (k_mg_pair) or one at a time
+static int min_sweeps(Ctx& c, uint8_t* M, const MinGeom& geo, const unsigned long long* live) {
+    constexpr size_t kSlabMax = 48 * 1024;
+    uint32_t* W = reinterpret_cast<uint32_t*>(M);
+    const uint64_t nwords = geo.bytes / 4;
+    // (the padding past the last row is swept too: 0xFF, harmless)
+    const uint64_t real_words = (geo.nd >= 1 ? geo.stride[geo.nd - 1] * geo.ext[geo.nd - 1] : 4) / 4;
+    int nl = 0;
+    const uint32_t w0 = geo.ext[0] / 4;
+    int sd = std::min(geo.nd, 3);
+    auto slab_bytes = [&](int k) {
+        uint64_t b = geo.ext[0];
+        for (int j = 1; j < k; ++j) b *= geo.ext[j];
+        return b;
+    };
+    while (sd > 1 && slab_bytes(sd) > kSlabMax) --sd;
+    const uint32_t e1 = sd >= 2 ? geo.ext[1] : 1, e2 = sd >= 3 ? geo.ext[2] : 1;
+    const uint64_t slab = slab_bytes(sd);
+    uint32_t spb = (uint32_t)std::max<uint64_t>(1, (kSlabMax / 2) / slab);
+    const size_t smem = (size_t)spb * slab;
+    static bool attr_set = false;
+    if (!attr_set) {
+        SKY_CUDA(cudaFuncSetAttribute(k_mg_slab<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSlabMax));
+        SKY_CUDA(cudaFuncSetAttribute(k_mg_slab<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSlabMax));
+        SKY_CUDA(cudaFuncSetAttribute(k_mg_slab<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSlabMax));
+        attr_set = true;
+    }
+    const uint64_t nslabs = real_words / (slab / 4);
+    const unsigned gsl = grid_for((nslabs + spb - 1) / spb, 1, c.num_sms * 8);
+    if (sd == 1)
+        pdl_launch(k_mg_slab<1>, gsl, kBlock, smem, c.stream, W, real_words, w0, e1, e2, spb, live);
+    else if (sd == 2)
+        pdl_launch(k_mg_slab<2>, gsl, kBlock, smem, c.stream, W, real_words, w0, e1, e2, spb, live);
+    else
+        pdl_launch(k_mg_slab<3>, gsl, kBlock, smem, c.stream, W, real_words, w0, e1, e2, spb, live);
+    ++nl;
+    int j = sd;
+    while (j < geo.nd) {
+        const uint64_t sa = geo.stride[j] / 4;
+        if (j + 1 < geo.nd && geo.ext[j] <= 32) {
+            const uint64_t lines = real_words / ((uint64_t)geo.ext[j] * geo.ext[j + 1]);
+            const unsigned gp = grid_for(lines, kBlock);
+            if (geo.ext[j] <= 8)
+                pdl_launch(k_mg_pair<8>, gp, kBlock, 0, c.stream, W, real_words, geo.ext[j], geo.ext[j + 1], sa, live);
+            else if (geo.ext[j] <= 16)
+                pdl_launch(k_mg_pair<16>, gp, kBlock, 0, c.stream, W, real_words, geo.ext[j], geo.ext[j + 1], sa, live);
+            else
+                pdl_launch(k_mg_pair<32>, gp, kBlock, 0, c.stream, W, real_words, geo.ext[j], geo.ext[j + 1], sa, live);
+            j += 2;
+        } else {
+            pdl_launch(k_mg_dim, grid_for(real_words / geo.ext[j], kBlock), kBlock, 0, c.stream, W,
+                       real_words, (uint64_t)geo.ext[j], sa, live);
+            j += 1;
+        }
+        ++nl;
+    }
+    (void)nwords;
+    return nl;
+}
+
 namespace {
 
 constexpr int kSmemBlock = 512;
@@ -627,10 +949,17 @@ std::vector<int> cells_step_plan(const std::vector<double>& amax, int d, int g_m
     }
     std::vector<std::pair<double, int>> cost;
     for (int g = g_max; g >= 2; --g) {
+        // bytes swept (~7 x the grid: filled, three read+write passes) plus
+        // the mark and query reads of S code words
+        MinGeom mg;
         CellGeom geo;
         uint64_t e0 = 0;
-        const double rows = cells_geometry(amax, d, g, ~0ULL, &geo, &e0) ? (double)geo.rows : 0.0;
-        cost.push_back({7.0 * 4.0 * rows + 24.0 * (double)S, g});
+        double grid = 0.0;
+        if (min_geometry(amax, d, g, ~0ULL, &mg))
+            grid = (double)mg.bytes;
+        else if (cells_geometry(amax, d, g, ~0ULL, &geo, &e0))
+            grid = 4.0 * (double)geo.rows;
+        cost.push_back({7.0 * grid + 24.0 * (double)S, g});
     }
     std::stable_sort(cost.begin(), cost.end(),
                      [](const std::pair<double, int>& x, const std::pair<double, int>& y) {
@@ -671,14 +1000,85 @@ bool gres_cells_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_ma
     for (int j = 0; j < d; ++j) memcpy(&amax[j], &bits[j], 8);
     // memory budget: 16 GiB of rows at most
     const uint64_t budget_rows = (16ull << 30) / 8;
+    // the min-grid form (default; SKYGPU_CELLS_BITSET=1: the bitset rows)
+    static const bool bitset = [] {
+        const char* e = getenv("SKYGPU_CELLS_BITSET");
+        return e && e[0] == '1';
+    }();
+    MinGeom mg0;
+    const bool minform = !bitset && d <= 8 && S * 8 <= (16ull << 30) &&
+                         min_geometry(amax, d, g_max, 16ull << 30, &mg0);
     CellGeom geo0;
     uint64_t e0 = 0;
-    if (!cells_geometry(amax, d, g_max, budget_rows, &geo0, &e0)) return false;
+    if (!minform && !cells_geometry(amax, d, g_max, budget_rows, &geo0, &e0)) return false;
     const bool w64 = e0 > 32;
     const std::vector<int> steps = cells_step_plan(amax, d, g_max, S, step_rank, step_world);
     *cells_swept = 0;
     *steps_run = 0;
     if (steps.empty()) return true;  // (more ranks than steps: nothing here)
+    if (minform) {
+        MinGeom top;
+        min_geometry(amax, d, steps[0], 16ull << 30, &top);
+        uint8_t* M = static_cast<uint8_t*>(c.buf[B_CELLS].get(top.bytes));
+        const bool cw32 = d <= 4;
+        const size_t cwb = cw32 ? 4 : 8;
+        const uint64_t chunk = std::min<uint64_t>(64, steps.size());
+        void* codes = c.buf[B_CODES].get(S * chunk * cwb);
+        uint32_t* lists[2] = {c.buf[B_CACT0].as<uint32_t>(na), c.buf[B_CACT1].as<uint32_t>(na)};
+        unsigned long long* cnt[2] = {c.d_slots + S_LIVE0, c.d_slots + S_LIVE1};
+        const uint32_t* in = act;
+        const unsigned long long* n_in = nullptr;
+        int cur = 0, nrun = 0;
+        uint64_t swept = 0;
+        for (size_t s0 = 0; s0 < steps.size(); s0 += chunk) {
+            StepList sl;
+            sl.n = (int)std::min<uint64_t>(chunk, steps.size() - s0);
+            for (int i = 0; i < sl.n; ++i) sl.g[i] = steps[s0 + i];
+            if (cw32)
+                pdl_launch(k_cells_codes<uint32_t>, grid_for(S, kBlock), kBlock, 0, c.stream,
+                           d_skyv, S, d, sl, (uint32_t*)codes);
+            else
+                pdl_launch(k_cells_codes<unsigned long long>, grid_for(S, kBlock), kBlock, 0,
+                           c.stream, d_skyv, S, d, sl, (unsigned long long*)codes);
+            SKY_LAUNCH_CHECK();
+            note_launch(c);
+            swept += S * (uint64_t)d * sizeof(double) + S * (uint64_t)sl.n * cwb;
+            for (int li = 0; li < sl.n; ++li) {
+                MinGeom geo;
+                min_geometry(amax, d, sl.g[li], 16ull << 30, &geo);
+                pdl_launch(k_mg_fill, grid_for(geo.bytes / 16, kBlock), kBlock, 0, c.stream,
+                           (uint4*)M, geo.bytes / 16, n_in);
+                pdl_launch(k_clear_slot_c, 1, 1, 0, c.stream, cnt[cur]);
+                const unsigned gs = grid_for(S, kBlock);
+                const unsigned gq = grid_for(na, kBlock);
+                int nl = 0;
+                auto run = [&](auto* cg) {
+                    using CW = std::remove_const_t<std::remove_pointer_t<decltype(cg)>>;
+                    pdl_launch(k_mg_mark<CW>, gs, kBlock, 0, c.stream, cg, S, geo, M, n_in);
+                    nl = min_sweeps(c, M, geo, n_in);
+                    pdl_launch(k_mg_query<CW>, gq, kBlock, 0, c.stream, cg, geo, (const uint8_t*)M,
+                               in, na, n_in, d_den, lists[cur], cnt[cur]);
+                };
+                if (cw32)
+                    run((const uint32_t*)codes + (uint64_t)li * S);
+                else
+                    run((const unsigned long long*)codes + (uint64_t)li * S);
+                SKY_LAUNCH_CHECK();
+                note_launch(c, 4 + nl);
+                // algorithmic bytes of the step: the grid filled, read and
+                // written once by an ideal fused prefix minimum, plus the
+                // mark and query reads of the S code words
+                swept += 3 * geo.bytes + 2 * S * cwb;
+                ++nrun;
+                in = lists[cur];
+                n_in = cnt[cur];
+                cur ^= 1;
+            }
+        }
+        *cells_swept = swept;
+        *steps_run = nrun;
+        return true;
+    }
     {
         CellGeom gt;
         uint64_t et = 0;

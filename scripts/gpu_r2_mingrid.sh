@@ -1,0 +1,6 @@
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "cell_engine or min_grid" > gpurun_out/mg_tests.log 2>&1; echo "cell tests rc=$?"; tail -3 gpurun_out/mg_tests.log
+timeout 600 python -m pytest tests/test_gpu_variants.py -q -x -k "bitset" > gpurun_out/mg_var.log 2>&1; echo "bitset variant rc=$?"; tail -2 gpurun_out/mg_var.log
+timeout 600 python bench.py --no-cpu-baseline --steps 10 > gpurun_out/mg_bench.log 2>&1; echo "bench rc=$?"; tail -1 gpurun_out/mg_bench.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], d['stage_ms'], d['e2e']['ms_per_step'])"
+CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline"
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 3000 --csv --log-file gpurun_out/mg_launches_C5.csv $CMD > gpurun_out/mg_ncu.log 2>&1; echo "launch list rc=$?"
+timeout 900 python -m pytest tests/test_gpu_fullscale.py -q -x > gpurun_out/mg_full.log 2>&1; echo "fullscale rc=$?"; tail -3 gpurun_out/mg_full.log

@@ -252,6 +252,28 @@ def test_cell_engine_hbm_variant_small_d(monkeypatch):
     assert cells.den.tolist() == full.den.tolist()
 
 
+@pytest.mark.parametrize("gen,d,scale", [("ant", 2, None), ("ant", 3, None), ("uni", 4, None),
+                                         ("ant", 5, None), ("lattice", 6, None), ("ant", 7, None),
+                                         ("corr", 8, None), ("ant", 7, (1.0, 0.3, 0.6, 1.0, 0.5, 0.9, 0.2)),
+                                         ("ant", 4, (0.1, 1.0, 0.4, 0.7)), ("lattice", 5, (4.0,) * 5)])
+def test_min_grid_cell_engine_matches_pairs(monkeypatch, gen, d, scale):
+    """The min-grid form of the HBM cell engine (one byte per cell: the
+    smallest code of the min'd attribute under it) against the pair engine,
+    over every d it takes, unequal extents (the min'd attribute is the widest,
+    not attribute 0), ties/duplicates (lattice) and codes far above cap
+    (values up to 4: extents ~100)."""
+    monkeypatch.setenv("SKYGPU_CELLS_SMEM", "0")
+    v = sk.generate(gen, 30000, d, 70 + d)
+    if scale is not None:
+        v = v * np.asarray(scale)
+    full = sk.pipeline(v, cap=25, engine=sk.GRES_PAIRS)
+    cells = sk.pipeline(v, cap=25, engine=sk.GRES_CELLS)
+    assert cells.positions.tolist() == full.positions.tolist()
+    if full.g_max >= 2:
+        assert cells.stats["gres_engine"] == sk.GRES_CELLS and cells.stats["gres_cells"] > 0
+    assert cells.den.tolist() == full.den.tolist()
+
+
 @pytest.mark.parametrize("world", [2, 3])
 def test_cell_engine_smem_shards(world):
     v = sk.generate("ant", 30000, 3, 43)

@@ -53,3 +53,27 @@ def test_grid_decide_alu_and_tma_kernels_agree(tmp_path):
     assert a["bad"] == [], a
     b = _run({}, "1000000", path)
     assert b["bad"] == [], b
+
+
+_BITSET = """
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2412_02274_b200 as sk
+bad = []
+for gen, n, d in (("ant", 40000, 7), ("ant", 30000, 5), ("lattice", 20000, 6), ("uni", 40000, 4)):
+    v = sk.generate(gen, n, d, 3)
+    a = sk.pipeline(v, cap=25, engine=sk.GRES_PAIRS)
+    b = sk.pipeline(v, cap=25, engine=sk.GRES_CELLS)
+    if a.den.tolist() != b.den.tolist() or (b.g_max >= 2 and b.stats["gres_cells"] == 0):
+        bad.append(f"{gen}{n}d{d}")
+print(bad)
+"""
+
+
+def test_cell_engine_bitset_rows_variant():
+    """SKYGPU_CELLS_BITSET=1: the u32/u64 bitset-row form of the HBM cell
+    engine (the min-grid form is the default) gives the pair engine's map."""
+    e = dict(os.environ, SKYGPU_CELLS_BITSET="1", SKYGPU_CELLS_SMEM="0")
+    out = subprocess.check_output([sys.executable, "-c", _BITSET, os.path.dirname(HERE)], env=e,
+                                  text=True, timeout=900)
+    assert out.strip().splitlines()[-1] == "[]", out
