@@ -17,6 +17,8 @@
 // then the remaining attributes two at a time (k_cells_or_pair) — 3 passes
 // for d = 7 instead of 7.  Exactness: the same codes floor(v*g) as the pair
 // engine.
+#include <cub/cub.cuh>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -529,7 +531,47 @@ __device__ __forceinline__ uint32_t bytes_prefix_min(uint32_t x, uint32_t carry)
     return __vminu4(x, carry * 0x01010101u);
 }
 
-// grid dims 0, 1, 2 (as many as the slab has) of whole slabs in shared memory
+// grid dims 0, 1, 2 (ND of them) of ns whole slabs staged in shared memory
+template <int ND>
+__device__ __forceinline__ void slab_prefix(uint32_t* sw, uint32_t ns, uint32_t w0, uint32_t e1,
+                                            uint32_t e2) {
+    const uint32_t slab = w0 * e1 * e2;
+    const uint32_t words = ns * slab;
+    for (uint32_t l = threadIdx.x; l < words / w0; l += blockDim.x) {  // dim 0: bytes of a line
+        uint32_t* p = sw + (uint64_t)l * w0;
+        uint32_t carry = 0xFFu;
+        for (uint32_t a = 0; a < w0; ++a) {
+            const uint32_t x = bytes_prefix_min(p[a], carry);
+            p[a] = x;
+            carry = x >> 24;
+        }
+    }
+    __syncthreads();
+    if (ND >= 2) {  // dim 1: u32 columns, stride w0
+        for (uint32_t l = threadIdx.x; l < ns * e2 * w0; l += blockDim.x) {
+            uint32_t* p = sw + (uint64_t)(l / w0) * w0 * e1 + (l % w0);
+            uint32_t acc = ~0u;
+            for (uint32_t a = 0; a < e1; ++a) {
+                acc = __vminu4(acc, p[a * w0]);
+                p[a * w0] = acc;
+            }
+        }
+        __syncthreads();
+    }
+    if (ND >= 3) {  // dim 2: u32 columns, stride w0 * e1
+        const uint32_t plane = w0 * e1;
+        for (uint32_t l = threadIdx.x; l < ns * plane; l += blockDim.x) {
+            uint32_t* p = sw + (uint64_t)(l / plane) * slab + (l % plane);
+            uint32_t acc = ~0u;
+            for (uint32_t b = 0; b < e2; ++b) {
+                acc = __vminu4(acc, p[b * plane]);
+                p[b * plane] = acc;
+            }
+        }
+        __syncthreads();
+    }
+}
+
 template <int ND>
 __global__ void __launch_bounds__(kBlock)
 k_mg_slab(uint32_t* __restrict__ M, uint64_t nwords, uint32_t w0, uint32_t e1, uint32_t e2,
@@ -551,39 +593,7 @@ k_mg_slab(uint32_t* __restrict__ M, uint64_t nwords, uint32_t w0, uint32_t e1, u
             for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) sw[i] = g[i];
         }
         __syncthreads();
-        for (uint32_t l = threadIdx.x; l < words / w0; l += blockDim.x) {  // dim 0: bytes of a line
-            uint32_t* p = sw + (uint64_t)l * w0;
-            uint32_t carry = 0xFFu;
-            for (uint32_t a = 0; a < w0; ++a) {
-                const uint32_t x = bytes_prefix_min(p[a], carry);
-                p[a] = x;
-                carry = x >> 24;
-            }
-        }
-        __syncthreads();
-        if (ND >= 2) {  // dim 1: u32 columns, stride w0
-            for (uint32_t l = threadIdx.x; l < ns * e2 * w0; l += blockDim.x) {
-                uint32_t* p = sw + (uint64_t)(l / w0) * w0 * e1 + (l % w0);
-                uint32_t acc = ~0u;
-                for (uint32_t a = 0; a < e1; ++a) {
-                    acc = __vminu4(acc, p[a * w0]);
-                    p[a * w0] = acc;
-                }
-            }
-            __syncthreads();
-        }
-        if (ND >= 3) {  // dim 2: u32 columns, stride w0 * e1
-            const uint32_t plane = w0 * e1;
-            for (uint32_t l = threadIdx.x; l < ns * plane; l += blockDim.x) {
-                uint32_t* p = sw + (uint64_t)(l / plane) * slab + (l % plane);
-                uint32_t acc = ~0u;
-                for (uint32_t b = 0; b < e2; ++b) {
-                    acc = __vminu4(acc, p[b * plane]);
-                    p[b * plane] = acc;
-                }
-            }
-            __syncthreads();
-        }
+        slab_prefix<ND>(sw, ns, w0, e1, e2);
         uint32_t* o = M + s0 * slab;
         if (vec) {
             for (uint32_t i = threadIdx.x; i < words / 4; i += blockDim.x)
@@ -592,6 +602,57 @@ k_mg_slab(uint32_t* __restrict__ M, uint64_t nwords, uint32_t w0, uint32_t e1, u
             for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) o[i] = sw[i];
         }
         __syncthreads();
+    }
+}
+
+// grid dims 0..3 in ONE pass: a block owns a column of e3 consecutive slabs
+// (dims 0..2; fixed dims 4..), prefixes each in shared memory and carries a
+// running elementwise minimum from slab to slab — the prefix along dim 3.
+// The next slab's words are loaded into registers (kPer per thread) while
+// the current one is swept.
+constexpr int kColPer = 20;  // slab words per thread (slab <= 5120 words)
+
+__global__ void __launch_bounds__(kBlock)
+k_mg_slabcol(uint32_t* __restrict__ M, uint32_t ncols, uint32_t w0, uint32_t e1, uint32_t e2,
+             uint32_t e3, const unsigned long long* live) {
+    pdl_wait();
+    if (step_dead(live)) return;
+    extern __shared__ __align__(16) uint32_t sw[];
+    const uint32_t slab = w0 * e1 * e2;
+    uint32_t* run = sw + slab;
+    for (uint32_t col = blockIdx.x; col < ncols; col += gridDim.x) {
+        uint32_t* base = M + (uint64_t)col * e3 * slab;
+        uint32_t pre[kColPer];
+#pragma unroll
+        for (int k = 0; k < kColPer; ++k) {
+            const uint32_t i = threadIdx.x + k * kBlock;
+            pre[k] = i < slab ? base[i] : ~0u;
+        }
+        for (uint32_t c3 = 0; c3 < e3; ++c3) {
+#pragma unroll
+            for (int k = 0; k < kColPer; ++k) {
+                const uint32_t i = threadIdx.x + k * kBlock;
+                if (i < slab) sw[i] = pre[k];
+            }
+            __syncthreads();
+            if (c3 + 1 < e3) {
+                const uint32_t* nx = base + (uint64_t)(c3 + 1) * slab;
+#pragma unroll
+                for (int k = 0; k < kColPer; ++k) {
+                    const uint32_t i = threadIdx.x + k * kBlock;
+                    pre[k] = i < slab ? nx[i] : ~0u;
+                }
+            }
+            slab_prefix<3>(sw, 1, w0, e1, e2);
+            uint32_t* o = base + (uint64_t)c3 * slab;
+            for (uint32_t i = threadIdx.x; i < slab; i += blockDim.x) {
+                uint32_t x = sw[i];
+                if (c3) x = __vminu4(x, run[i]);
+                run[i] = x;
+                o[i] = x;
+            }
+            __syncthreads();
+        }
     }
 }
 
@@ -628,19 +689,34 @@ k_mg_pair(uint32_t* __restrict__ M, uint64_t nwords, uint32_t ea, uint32_t eb, u
     }
 }
 
-// one grid dim (word stride s, extent e): one thread per u32 column
-__global__ void k_mg_dim(uint32_t* __restrict__ M, uint64_t nwords, uint64_t e, uint64_t s,
-                         const unsigned long long* live) {
+// one grid dim (word stride s, extent e <= E): one thread per u32 column,
+// the column's words loaded together (independent loads in flight)
+template <int E>
+__global__ void __launch_bounds__(kBlock)
+k_mg_dim(uint32_t* __restrict__ M, uint64_t nwords, uint32_t e, uint64_t s,
+         const unsigned long long* live) {
     pdl_wait();
     if (step_dead(live)) return;
     const uint64_t lines = nwords / e;
     for (uint64_t l = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; l < lines;
          l += (uint64_t)gridDim.x * blockDim.x) {
         uint32_t* p = M + (l / s) * s * e + (l % s);
-        uint32_t acc = ~0u;
-        for (uint64_t k = 0; k < e; ++k) {
-            acc = __vminu4(acc, p[k * s]);
-            p[k * s] = acc;
+        if (E > 0) {
+            uint32_t v[E > 0 ? E : 1];
+#pragma unroll
+            for (int k = 0; k < E; ++k) v[k] = (uint32_t)k < e ? p[(uint64_t)k * s] : ~0u;
+            uint32_t acc = ~0u;
+#pragma unroll
+            for (int k = 0; k < E; ++k) {
+                acc = __vminu4(acc, v[k]);
+                if ((uint32_t)k < e) p[(uint64_t)k * s] = acc;
+            }
+        } else {
+            uint32_t acc = ~0u;
+            for (uint64_t k = 0; k < e; ++k) {
+                acc = __vminu4(acc, p[k * s]);
+                p[k * s] = acc;
+            }
         }
     }
 }
@@ -649,6 +725,7 @@ template <class CW>
 __global__ void k_mg_query(const CW* __restrict__ code, MinGeom geo, const uint8_t* __restrict__ M,
                            const uint32_t* __restrict__ act_in, uint64_t na,
                            const unsigned long long* n_in, int32_t* __restrict__ den,
+                           const uint32_t* __restrict__ perm,
                            uint32_t* __restrict__ act_out, unsigned long long* __restrict__ n_out) {
     pdl_wait();
     if (n_in) na = *(volatile const unsigned long long*)n_in;
@@ -660,14 +737,14 @@ __global__ void k_mg_query(const CW* __restrict__ code, MinGeom geo, const uint8
         bool keep = false;
         uint32_t t = 0;
         if (k < na) {
-            t = act_in[k];
+            t = act_in ? act_in[k] : (uint32_t)k;
             const CW w = code[t];
             const uint64_t r = mg_row(w, geo);
             const uint32_t c0 = (uint32_t)(w >> (8 * geo.m)) & 0xFFu;
             bool hit = M[r] < c0;
             for (int j = 0; j < geo.nd && !hit; ++j)
                 if ((uint32_t)(w >> (8 * geo.attr[j])) & 0xFFu) hit = M[r - geo.stride[j]] <= c0;
-            if (hit) den[t] = geo.g;
+            if (hit) den[perm ? perm[t] : t] = geo.g;
             keep = !hit;
         }
         const unsigned msk = __ballot_sync(0xffffffffu, keep);
@@ -676,6 +753,34 @@ __global__ void k_mg_query(const CW* __restrict__ code, MinGeom geo, const uint8
         if (lane == 0) base = atomicAdd(n_out, (unsigned long long)__popc(msk));
         base = __shfl_sync(0xffffffffu, base, 0);
         if (keep) act_out[base + __popc(msk & ((1u << lane) - 1u))] = t;
+    }
+}
+
+// locality order of the skyline for the min-grid steps: the row of every
+// tuple in the top step's grid (its codes there), sorted once per call — at
+// every lower step consecutive tuples then mark and query nearby cells
+__global__ void k_mg_sortkey(const double* __restrict__ v, uint64_t S, int d, MinGeom geo,
+                             unsigned long long* __restrict__ key, uint32_t* __restrict__ idx) {
+    pdl_wait();
+    const double gd = (double)geo.g;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < S;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t r = 0;
+        for (int k = 0; k < geo.nd; ++k)
+            r += (uint64_t)floor(__dmul_rn(v[(uint64_t)geo.attr[k] * S + i], gd)) * geo.stride[k];
+        key[i] = r;
+        idx[i] = (uint32_t)i;
+    }
+}
+
+// the SoA values in that order
+__global__ void k_mg_permute(const double* __restrict__ v, uint64_t S, int d,
+                             const uint32_t* __restrict__ perm, double* __restrict__ out) {
+    pdl_wait();
+    for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < S;
+         q += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t t = perm[q];
+        for (int j = 0; j < d; ++j) out[(uint64_t)j * S + q] = v[(uint64_t)j * S + t];
     }
 }
 
@@ -713,14 +818,19 @@ static bool min_geometry(const std::vector<double>& amax, int d, int g, uint64_t
     return true;
 }
 
-// the prefix minimum over every grid dim: dims 0..2 in a shared-memory slab
-// pass, the rest two at a time in registers (k_mg_pair) or one at a time
+// the prefix minimum over every grid dim: dims 0..3 in one slab-column pass
+// (k_mg_slabcol; dims 0..2 in a slab pass when there is no dim 3 or the slab
+// is too large), the rest two at a time in registers (k_mg_pair) or one at a
+// time (k_mg_dim) — 2 passes for d = 7
 static int min_sweeps(Ctx& c, uint8_t* M, const MinGeom& geo, const unsigned long long* live) {
     constexpr size_t kSlabMax = 48 * 1024;
+    static const bool nocol = [] {
+        const char* e = getenv("SKYGPU_MG_NOCOL");
+        return e && e[0] == '1';
+    }();
     uint32_t* W = reinterpret_cast<uint32_t*>(M);
-    const uint64_t nwords = geo.bytes / 4;
-    // (the padding past the last row is swept too: 0xFF, harmless)
-    const uint64_t real_words = (geo.nd >= 1 ? geo.stride[geo.nd - 1] * geo.ext[geo.nd - 1] : 4) / 4;
+    // (whole rows only: the 16-byte padding of the fill stays 0xFF)
+    const uint64_t real_words = geo.stride[geo.nd - 1] * geo.ext[geo.nd - 1] / 4;
     int nl = 0;
     const uint32_t w0 = geo.ext[0] / 4;
     int sd = std::min(geo.nd, 3);
@@ -732,45 +842,60 @@ static int min_sweeps(Ctx& c, uint8_t* M, const MinGeom& geo, const unsigned lon
     while (sd > 1 && slab_bytes(sd) > kSlabMax) --sd;
     const uint32_t e1 = sd >= 2 ? geo.ext[1] : 1, e2 = sd >= 3 ? geo.ext[2] : 1;
     const uint64_t slab = slab_bytes(sd);
-    uint32_t spb = (uint32_t)std::max<uint64_t>(1, (kSlabMax / 2) / slab);
-    const size_t smem = (size_t)spb * slab;
     static bool attr_set = false;
     if (!attr_set) {
         SKY_CUDA(cudaFuncSetAttribute(k_mg_slab<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSlabMax));
         SKY_CUDA(cudaFuncSetAttribute(k_mg_slab<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSlabMax));
         SKY_CUDA(cudaFuncSetAttribute(k_mg_slab<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSlabMax));
+        SKY_CUDA(cudaFuncSetAttribute(k_mg_slabcol, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSlabMax));
         attr_set = true;
     }
     const uint64_t nslabs = real_words / (slab / 4);
-    const unsigned gsl = grid_for((nslabs + spb - 1) / spb, 1, c.num_sms * 8);
-    if (sd == 1)
-        pdl_launch(k_mg_slab<1>, gsl, kBlock, smem, c.stream, W, real_words, w0, e1, e2, spb, live);
-    else if (sd == 2)
-        pdl_launch(k_mg_slab<2>, gsl, kBlock, smem, c.stream, W, real_words, w0, e1, e2, spb, live);
-    else
-        pdl_launch(k_mg_slab<3>, gsl, kBlock, smem, c.stream, W, real_words, w0, e1, e2, spb, live);
-    ++nl;
     int j = sd;
+    if (!nocol && sd == 3 && geo.nd >= 4 && slab / 4 <= (uint64_t)kColPer * kBlock) {
+        const uint32_t e3 = geo.ext[3];
+        const uint64_t ncols = nslabs / e3;
+        pdl_launch(k_mg_slabcol, grid_for(ncols, 1, c.num_sms * 8), kBlock, (size_t)2 * slab,
+                   c.stream, W, (uint32_t)ncols, w0, e1, e2, e3, live);
+        j = 4;
+    } else {
+        const uint32_t spb = (uint32_t)std::max<uint64_t>(1, (kSlabMax / 2) / slab);
+        const size_t smem = (size_t)spb * slab;
+        const unsigned gsl = grid_for((nslabs + spb - 1) / spb, 1, c.num_sms * 8);
+        if (sd == 1)
+            pdl_launch(k_mg_slab<1>, gsl, kBlock, smem, c.stream, W, real_words, w0, e1, e2, spb, live);
+        else if (sd == 2)
+            pdl_launch(k_mg_slab<2>, gsl, kBlock, smem, c.stream, W, real_words, w0, e1, e2, spb, live);
+        else
+            pdl_launch(k_mg_slab<3>, gsl, kBlock, smem, c.stream, W, real_words, w0, e1, e2, spb, live);
+    }
+    ++nl;
     while (j < geo.nd) {
         const uint64_t sa = geo.stride[j] / 4;
-        if (j + 1 < geo.nd && geo.ext[j] <= 32) {
-            const uint64_t lines = real_words / ((uint64_t)geo.ext[j] * geo.ext[j + 1]);
+        const uint32_t ea = geo.ext[j];
+        if (j + 1 < geo.nd && ea <= 32) {
+            const uint64_t lines = real_words / ((uint64_t)ea * geo.ext[j + 1]);
             const unsigned gp = grid_for(lines, kBlock);
-            if (geo.ext[j] <= 8)
-                pdl_launch(k_mg_pair<8>, gp, kBlock, 0, c.stream, W, real_words, geo.ext[j], geo.ext[j + 1], sa, live);
-            else if (geo.ext[j] <= 16)
-                pdl_launch(k_mg_pair<16>, gp, kBlock, 0, c.stream, W, real_words, geo.ext[j], geo.ext[j + 1], sa, live);
+            const uint32_t eb = geo.ext[j + 1];
+            if (ea <= 8)
+                pdl_launch(k_mg_pair<8>, gp, kBlock, 0, c.stream, W, real_words, ea, eb, sa, live);
+            else if (ea <= 16)
+                pdl_launch(k_mg_pair<16>, gp, kBlock, 0, c.stream, W, real_words, ea, eb, sa, live);
             else
-                pdl_launch(k_mg_pair<32>, gp, kBlock, 0, c.stream, W, real_words, geo.ext[j], geo.ext[j + 1], sa, live);
+                pdl_launch(k_mg_pair<32>, gp, kBlock, 0, c.stream, W, real_words, ea, eb, sa, live);
             j += 2;
         } else {
-            pdl_launch(k_mg_dim, grid_for(real_words / geo.ext[j], kBlock), kBlock, 0, c.stream, W,
-                       real_words, (uint64_t)geo.ext[j], sa, live);
+            const unsigned gd = grid_for(real_words / ea, kBlock);
+            if (ea <= 8)
+                pdl_launch(k_mg_dim<8>, gd, kBlock, 0, c.stream, W, real_words, ea, sa, live);
+            else if (ea <= 32)
+                pdl_launch(k_mg_dim<32>, gd, kBlock, 0, c.stream, W, real_words, ea, sa, live);
+            else
+                pdl_launch(k_mg_dim<0>, gd, kBlock, 0, c.stream, W, real_words, ea, sa, live);
             j += 1;
         }
         ++nl;
     }
-    (void)nwords;
     return nl;
 }
 
@@ -1030,16 +1155,52 @@ bool gres_cells_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_ma
         const unsigned long long* n_in = nullptr;
         int cur = 0, nrun = 0;
         uint64_t swept = 0;
+        // locality order (every candidate asked: na == S with act the
+        // identity, the only way this engine is called): values permuted by
+        // the top step's row, candidates = sorted positions, den written
+        // through the permutation (SKYGPU_CELLS_NOSORT=1: input order)
+        static const bool nosort = [] {
+            const char* e = getenv("SKYGPU_CELLS_NOSORT");
+            return e && e[0] == '1';
+        }();
+        const double* vals = d_skyv;
+        const uint32_t* perm = nullptr;
+        if (!nosort && na == S) {
+            auto* k0 = c.buf[B_MGKEY0].as<unsigned long long>(S);
+            auto* k1 = c.buf[B_MGKEY1].as<unsigned long long>(S);
+            auto* i0 = c.buf[B_MGIDX0].as<uint32_t>(S);
+            auto* i1 = c.buf[B_MGIDX1].as<uint32_t>(S);
+            double* pv = c.buf[B_MGVALS].as<double>(S * (uint64_t)d);
+            pdl_launch(k_mg_sortkey, grid_for(S, kBlock), kBlock, 0, c.stream, d_skyv, S, d, top, k0,
+                       i0);
+            SKY_LAUNCH_CHECK();
+            cub::DoubleBuffer<unsigned long long> kb(k0, k1);
+            cub::DoubleBuffer<uint32_t> vb(i0, i1);
+            const int end_bit = std::max(1, 64 - __builtin_clzll(top.bytes));
+            size_t tmp = 0;
+            SKY_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kb, vb, (int64_t)S, 0, end_bit,
+                                                     c.stream));
+            void* t = c.buf[B_CUB].get(tmp);
+            SKY_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, kb, vb, (int64_t)S, 0, end_bit,
+                                                     c.stream));
+            perm = vb.Current();
+            pdl_launch(k_mg_permute, grid_for(S, kBlock), kBlock, 0, c.stream, d_skyv, S, d, perm, pv);
+            SKY_LAUNCH_CHECK();
+            note_launch(c, 6);
+            vals = pv;
+            in = nullptr;  // the identity over sorted positions
+            swept += S * (uint64_t)d * 8 * 2 + S * 24;
+        }
         for (size_t s0 = 0; s0 < steps.size(); s0 += chunk) {
             StepList sl;
             sl.n = (int)std::min<uint64_t>(chunk, steps.size() - s0);
             for (int i = 0; i < sl.n; ++i) sl.g[i] = steps[s0 + i];
             if (cw32)
                 pdl_launch(k_cells_codes<uint32_t>, grid_for(S, kBlock), kBlock, 0, c.stream,
-                           d_skyv, S, d, sl, (uint32_t*)codes);
+                           vals, S, d, sl, (uint32_t*)codes);
             else
                 pdl_launch(k_cells_codes<unsigned long long>, grid_for(S, kBlock), kBlock, 0,
-                           c.stream, d_skyv, S, d, sl, (unsigned long long*)codes);
+                           c.stream, vals, S, d, sl, (unsigned long long*)codes);
             SKY_LAUNCH_CHECK();
             note_launch(c);
             swept += S * (uint64_t)d * sizeof(double) + S * (uint64_t)sl.n * cwb;
@@ -1057,7 +1218,7 @@ bool gres_cells_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_ma
                     pdl_launch(k_mg_mark<CW>, gs, kBlock, 0, c.stream, cg, S, geo, M, n_in);
                     nl = min_sweeps(c, M, geo, n_in);
                     pdl_launch(k_mg_query<CW>, gq, kBlock, 0, c.stream, cg, geo, (const uint8_t*)M,
-                               in, na, n_in, d_den, lists[cur], cnt[cur]);
+                               in, na, n_in, d_den, perm, lists[cur], cnt[cur]);
                 };
                 if (cw32)
                     run((const uint32_t*)codes + (uint64_t)li * S);

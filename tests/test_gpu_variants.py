@@ -70,10 +70,15 @@ print(bad)
 """
 
 
-def test_cell_engine_bitset_rows_variant():
-    """SKYGPU_CELLS_BITSET=1: the u32/u64 bitset-row form of the HBM cell
-    engine (the min-grid form is the default) gives the pair engine's map."""
-    e = dict(os.environ, SKYGPU_CELLS_BITSET="1", SKYGPU_CELLS_SMEM="0")
+@pytest.mark.parametrize("env", [{"SKYGPU_CELLS_BITSET": "1"}, {"SKYGPU_CELLS_NOSORT": "1"},
+                                 {"SKYGPU_MG_NOCOL": "1"}])
+def test_cell_engine_variants(env):
+    """The HBM cell engine's alternatives against the pair engine's map:
+    SKYGPU_CELLS_BITSET=1 the u32/u64 bitset-row form (the min-grid form is
+    the default), SKYGPU_CELLS_NOSORT=1 the min-grid over the input order (no
+    locality sort), SKYGPU_MG_NOCOL=1 the slab pass without the dim-3 running
+    minimum (one more sweep)."""
+    e = dict(os.environ, SKYGPU_CELLS_SMEM="0", **env)
     out = subprocess.check_output([sys.executable, "-c", _BITSET, os.path.dirname(HERE)], env=e,
                                   text=True, timeout=900)
     assert out.strip().splitlines()[-1] == "[]", out
