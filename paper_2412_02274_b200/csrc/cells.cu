@@ -459,14 +459,14 @@ void sweeps(Ctx& c, W* R, const CellGeom& geo, bool fused, const unsigned long l
 // after its in-word prefix-OR, a run of ones from the smallest attribute-0
 // code of any tuple whose other codes are <= the row's: the whole row is that
 // ONE number.  So the grid stores, per cell of the remaining d-1 attributes,
-//     M[r] = min { c_m(s) : row(s) <= r componentwise }   (0xFF: none)
+//     M[r] = min { c_m(s) : row(s) <= r componentwise }   (0x7F: none)
 // one byte instead of a 32/64-bit word, and t (code c, row r) is dominated iff
 //     M[r] < c_m(t)   or   M[r - e_j] <= c_m(t)   for a grid attribute j, c_j >= 1
 // (the same two cases as the bitset query: a strictly smaller code on the
 // min'd attribute m in a row <= r, or a row strictly below r with a code <=).
 // The min'd attribute m is the one with the largest extent (smallest grid).
 // Byte grids are 4x smaller than u32 rows, so a step's grid is written once,
-// swept in three passes (d = 7) of SIMD byte minima (__vminu4), and every
+// swept in two passes (d = 7) of SIMD byte minima (min7), and every
 // step below g ~ 22 of C5 stays resident in the 126 MB L2 across its passes.
 // Grid dim 0 (the fastest) is padded to a multiple of 4 bytes so that every
 // other dim's stride is a whole number of u32 words.
@@ -482,6 +482,20 @@ struct MinGeom {
     uint64_t bytes;                // grid bytes (a multiple of 16)
 };
 
+// Cells hold 7-bit values (codes <= 126; 0x7F = empty), so a bytewise
+// minimum is 3 instructions instead of __vminu4's emulated 7: t = a + 0x80 -
+// b per byte cannot carry or borrow across bytes, its top bit is a >= b,
+// PRMT replicates that bit over the byte, a LOP3 selects.
+constexpr uint32_t kEmpty = 0x7Fu;
+constexpr uint32_t kEmpty4 = 0x7F7F7F7Fu;
+
+__device__ __forceinline__ uint32_t min7(uint32_t a, uint32_t b) {
+    const uint32_t t = a + 0x80808080u - b;
+    uint32_t m;
+    asm("prmt.b32 %0, %1, 0, 0xBA98;" : "=r"(m) : "r"(t));  // 0xFF where a >= b
+    return (b & m) | (a & ~m);
+}
+
 template <class CW>
 __device__ __forceinline__ uint64_t mg_row(CW w, const MinGeom& geo) {
     uint64_t r = 0;
@@ -493,42 +507,107 @@ __device__ __forceinline__ uint64_t mg_row(CW w, const MinGeom& geo) {
 __global__ void k_mg_fill(uint4* __restrict__ p, uint64_t n16, const unsigned long long* live) {
     pdl_wait();
     if (step_dead(live)) return;
-    const uint4 f = make_uint4(~0u, ~0u, ~0u, ~0u);
+    const uint4 f = make_uint4(kEmpty4, kEmpty4, kEmpty4, kEmpty4);
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n16;
          i += (uint64_t)gridDim.x * blockDim.x)
         p[i] = f;
 }
 
-// every skyline tuple lowers its cell's byte to its code on attribute m
-// (a CAS on the containing word; a cell already <= is left alone)
+// every skyline tuple lowers its cell's byte to its code on attribute m.
+// Lanes of a warp that hit the same word combine first (match + byte
+// minima), then one CAS per word, optimistic about a fresh (0x7F) word.
 template <class CW>
-__global__ void k_mg_mark(const CW* __restrict__ code, uint64_t S, MinGeom geo,
-                          uint8_t* __restrict__ M, const unsigned long long* live) {
+__global__ void __launch_bounds__(kBlock)
+k_mg_mark(const CW* __restrict__ code, uint64_t S, MinGeom geo, uint8_t* __restrict__ M,
+          const unsigned long long* live) {
     pdl_wait();
     if (step_dead(live)) return;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < S;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        const CW w = code[i];
-        const uint64_t r = mg_row(w, geo);
-        const uint32_t c0 = (uint32_t)(w >> (8 * geo.m)) & 0xFFu;
-        uint32_t* word = reinterpret_cast<uint32_t*>(M + (r & ~3ULL));
-        const uint32_t sh = 8u * (uint32_t)(r & 3u);
-        uint32_t old = *reinterpret_cast<volatile uint32_t*>(word);
-        while (((old >> sh) & 0xFFu) > c0) {
-            const uint32_t nw = (old & ~(0xFFu << sh)) | (c0 << sh);
-            const uint32_t prev = atomicCAS(word, old, nw);
-            if (prev == old) break;
-            old = prev;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t b = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) & ~31ULL; b < S; b += stride) {
+        const uint64_t i = b + lane;
+        uint32_t mine = kEmpty4;
+        uint64_t wi = ~0ULL;
+        if (i < S) {
+            const CW w = code[i];
+            const uint64_t r = mg_row(w, geo);
+            const uint32_t c0 = (uint32_t)(w >> (8 * geo.m)) & 0xFFu;
+            const uint32_t sh = 8u * (uint32_t)(r & 3u);
+            wi = r >> 2;
+            mine = (kEmpty4 & ~(0xFFu << sh)) | (c0 << sh);
         }
+        const unsigned peers = __match_any_sync(0xffffffffu, wi);
+        uint32_t acc = mine;
+        if (__any_sync(0xffffffffu, __popc(peers) > 1)) {
+#pragma unroll 8
+            for (int k = 0; k < 32; ++k) {
+                const uint32_t v = __shfl_sync(0xffffffffu, mine, k);
+                if ((peers >> k) & 1u) acc = min7(acc, v);
+            }
+        }
+        if (i < S && (uint32_t)(__ffs(peers) - 1) == lane) {
+            uint32_t* word = reinterpret_cast<uint32_t*>(M) + wi;
+            uint32_t old = atomicCAS(word, kEmpty4, acc);
+            while (old != kEmpty4) {
+                const uint32_t nw = min7(old, acc);
+                if (nw == old) break;
+                const uint32_t prev = atomicCAS(word, old, nw);
+                if (prev == old) break;
+                old = prev;
+            }
+        }
+    }
+}
+
+// small grids (<= kPrivCells cells: the low steps, where CAS contention on
+// few words would serialise the mark): each block takes a contiguous share
+// of the tuples into a private u32-per-cell copy in shared memory (native
+// atomicMin), then stores it packed to its staging slot; k_mg_mark_reduce
+// takes the bytewise minimum over the slots (and so also fills the grid)
+constexpr uint32_t kPrivCells = 40960;
+
+template <class CW>
+__global__ void __launch_bounds__(kBlock)
+k_mg_mark_priv(const CW* __restrict__ code, uint64_t S, MinGeom geo, uint32_t* __restrict__ stage,
+               const unsigned long long* live) {
+    pdl_wait();
+    if (step_dead(live)) return;
+    extern __shared__ uint32_t cm[];
+    const uint32_t ncells = (uint32_t)geo.bytes;
+    for (uint32_t i = threadIdx.x; i < ncells; i += blockDim.x) cm[i] = kEmpty;
+    __syncthreads();
+    const uint64_t per = (S + gridDim.x - 1) / gridDim.x;
+    const uint64_t lo = blockIdx.x * per, hi = min(S, lo + per);
+    for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        const CW w = code[i];
+        const uint32_t r = (uint32_t)mg_row(w, geo);
+        const uint32_t c0 = (uint32_t)(w >> (8 * geo.m)) & 0xFFu;
+        if (cm[r] > c0) atomicMin(&cm[r], c0);
+    }
+    __syncthreads();
+    uint32_t* out = stage + (uint64_t)blockIdx.x * (ncells / 4);
+    for (uint32_t q = threadIdx.x; q < ncells / 4; q += blockDim.x)
+        out[q] = cm[4 * q] | (cm[4 * q + 1] << 8) | (cm[4 * q + 2] << 16) | (cm[4 * q + 3] << 24);
+}
+
+__global__ void k_mg_mark_reduce(const uint32_t* __restrict__ stage, uint32_t nslots,
+                                 uint32_t nwords, uint32_t* __restrict__ M,
+                                 const unsigned long long* live) {
+    pdl_wait();
+    if (step_dead(live)) return;
+    for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < nwords; q += gridDim.x * blockDim.x) {
+        uint32_t acc = kEmpty4;
+        for (uint32_t b = 0; b < nslots; ++b) acc = min7(acc, stage[(uint64_t)b * nwords + q]);
+        M[q] = acc;
     }
 }
 
 // prefix minimum along the 4 bytes of a word (byte k = lower address first),
 // then against the previous word's last byte
 __device__ __forceinline__ uint32_t bytes_prefix_min(uint32_t x, uint32_t carry) {
-    x = __vminu4(x, (x << 8) | 0xFFu);
-    x = __vminu4(x, (x << 16) | 0xFFFFu);
-    return __vminu4(x, carry * 0x01010101u);
+    x = min7(x, (x << 8) | kEmpty);
+    x = min7(x, (x << 16) | (kEmpty4 >> 16));
+    return min7(x, carry * 0x01010101u);
 }
 
 // grid dims 0, 1, 2 (ND of them) of ns whole slabs staged in shared memory
@@ -539,7 +618,7 @@ __device__ __forceinline__ void slab_prefix(uint32_t* sw, uint32_t ns, uint32_t 
     const uint32_t words = ns * slab;
     for (uint32_t l = threadIdx.x; l < words / w0; l += blockDim.x) {  // dim 0: bytes of a line
         uint32_t* p = sw + (uint64_t)l * w0;
-        uint32_t carry = 0xFFu;
+        uint32_t carry = kEmpty;
         for (uint32_t a = 0; a < w0; ++a) {
             const uint32_t x = bytes_prefix_min(p[a], carry);
             p[a] = x;
@@ -550,9 +629,9 @@ __device__ __forceinline__ void slab_prefix(uint32_t* sw, uint32_t ns, uint32_t 
     if (ND >= 2) {  // dim 1: u32 columns, stride w0
         for (uint32_t l = threadIdx.x; l < ns * e2 * w0; l += blockDim.x) {
             uint32_t* p = sw + (uint64_t)(l / w0) * w0 * e1 + (l % w0);
-            uint32_t acc = ~0u;
+            uint32_t acc = kEmpty4;
             for (uint32_t a = 0; a < e1; ++a) {
-                acc = __vminu4(acc, p[a * w0]);
+                acc = min7(acc, p[a * w0]);
                 p[a * w0] = acc;
             }
         }
@@ -562,9 +641,9 @@ __device__ __forceinline__ void slab_prefix(uint32_t* sw, uint32_t ns, uint32_t 
         const uint32_t plane = w0 * e1;
         for (uint32_t l = threadIdx.x; l < ns * plane; l += blockDim.x) {
             uint32_t* p = sw + (uint64_t)(l / plane) * slab + (l % plane);
-            uint32_t acc = ~0u;
+            uint32_t acc = kEmpty4;
             for (uint32_t b = 0; b < e2; ++b) {
-                acc = __vminu4(acc, p[b * plane]);
+                acc = min7(acc, p[b * plane]);
                 p[b * plane] = acc;
             }
         }
@@ -626,7 +705,7 @@ k_mg_slabcol(uint32_t* __restrict__ M, uint32_t ncols, uint32_t w0, uint32_t e1,
 #pragma unroll
         for (int k = 0; k < kColPer; ++k) {
             const uint32_t i = threadIdx.x + k * kBlock;
-            pre[k] = i < slab ? base[i] : ~0u;
+            pre[k] = i < slab ? base[i] : kEmpty4;
         }
         for (uint32_t c3 = 0; c3 < e3; ++c3) {
 #pragma unroll
@@ -640,14 +719,14 @@ k_mg_slabcol(uint32_t* __restrict__ M, uint32_t ncols, uint32_t w0, uint32_t e1,
 #pragma unroll
                 for (int k = 0; k < kColPer; ++k) {
                     const uint32_t i = threadIdx.x + k * kBlock;
-                    pre[k] = i < slab ? nx[i] : ~0u;
+                    pre[k] = i < slab ? nx[i] : kEmpty4;
                 }
             }
             slab_prefix<3>(sw, 1, w0, e1, e2);
             uint32_t* o = base + (uint64_t)c3 * slab;
             for (uint32_t i = threadIdx.x; i < slab; i += blockDim.x) {
                 uint32_t x = sw[i];
-                if (c3) x = __vminu4(x, run[i]);
+                if (c3) x = min7(x, run[i]);
                 run[i] = x;
                 o[i] = x;
             }
@@ -672,16 +751,16 @@ k_mg_pair(uint32_t* __restrict__ M, uint64_t nwords, uint32_t ea, uint32_t eb, u
         uint32_t* base = M + hi * sa * plane + lo;
         uint32_t prev[EA];
 #pragma unroll
-        for (int x = 0; x < EA; ++x) prev[x] = ~0u;
+        for (int x = 0; x < EA; ++x) prev[x] = kEmpty4;
         for (uint32_t y = 0; y < eb; ++y) {
             uint32_t* p = base + (uint64_t)y * ea * sa;
             uint32_t v[EA];
 #pragma unroll
-            for (int x = 0; x < EA; ++x) v[x] = (uint32_t)x < ea ? p[(uint64_t)x * sa] : ~0u;
-            uint32_t run = ~0u;
+            for (int x = 0; x < EA; ++x) v[x] = (uint32_t)x < ea ? p[(uint64_t)x * sa] : kEmpty4;
+            uint32_t run = kEmpty4;
 #pragma unroll
             for (int x = 0; x < EA; ++x) {
-                run = __vminu4(run, __vminu4(v[x], prev[x]));
+                run = min7(run, min7(v[x], prev[x]));
                 prev[x] = run;
                 if ((uint32_t)x < ea) p[(uint64_t)x * sa] = run;
             }
@@ -704,17 +783,17 @@ k_mg_dim(uint32_t* __restrict__ M, uint64_t nwords, uint32_t e, uint64_t s,
         if (E > 0) {
             uint32_t v[E > 0 ? E : 1];
 #pragma unroll
-            for (int k = 0; k < E; ++k) v[k] = (uint32_t)k < e ? p[(uint64_t)k * s] : ~0u;
-            uint32_t acc = ~0u;
+            for (int k = 0; k < E; ++k) v[k] = (uint32_t)k < e ? p[(uint64_t)k * s] : kEmpty4;
+            uint32_t acc = kEmpty4;
 #pragma unroll
             for (int k = 0; k < E; ++k) {
-                acc = __vminu4(acc, v[k]);
+                acc = min7(acc, v[k]);
                 if ((uint32_t)k < e) p[(uint64_t)k * s] = acc;
             }
         } else {
-            uint32_t acc = ~0u;
+            uint32_t acc = kEmpty4;
             for (uint64_t k = 0; k < e; ++k) {
-                acc = __vminu4(acc, p[k * s]);
+                acc = min7(acc, p[k * s]);
                 p[k * s] = acc;
             }
         }
@@ -741,9 +820,14 @@ __global__ void k_mg_query(const CW* __restrict__ code, MinGeom geo, const uint8
             const CW w = code[t];
             const uint64_t r = mg_row(w, geo);
             const uint32_t c0 = (uint32_t)(w >> (8 * geo.m)) & 0xFFu;
-            bool hit = M[r] < c0;
-            for (int j = 0; j < geo.nd && !hit; ++j)
-                if ((uint32_t)(w >> (8 * geo.attr[j])) & 0xFFu) hit = M[r - geo.stride[j]] <= c0;
+            // every cell the test needs, loaded together (one round trip)
+            uint32_t lo = kEmpty;
+#pragma unroll
+            for (int j = 0; j < 7; ++j) {
+                if (j < geo.nd && ((uint32_t)(w >> (8 * geo.attr[j])) & 0xFFu))
+                    lo = min(lo, (uint32_t)M[r - geo.stride[j]]);
+            }
+            const bool hit = (uint32_t)M[r] < c0 || lo <= c0;
             if (hit) den[perm ? perm[t] : t] = geo.g;
             keep = !hit;
         }
@@ -799,6 +883,7 @@ static bool min_geometry(const std::vector<double>& amax, int d, int g, uint64_t
         e[j] = (uint32_t)k + 1;
         if (e[j] > e[m]) m = j;
     }
+    if (e[m] > 127) return false;  // the min'd codes must stay below the empty value 0x7F
     geo->nd = d - 1;
     geo->m = m;
     geo->g = g;
@@ -829,7 +914,7 @@ static int min_sweeps(Ctx& c, uint8_t* M, const MinGeom& geo, const unsigned lon
         return e && e[0] == '1';
     }();
     uint32_t* W = reinterpret_cast<uint32_t*>(M);
-    // (whole rows only: the 16-byte padding of the fill stays 0xFF)
+    // (whole rows only: the 16-byte padding of the fill stays empty)
     const uint64_t real_words = geo.stride[geo.nd - 1] * geo.ext[geo.nd - 1] / 4;
     int nl = 0;
     const uint32_t w0 = geo.ext[0] / 4;
@@ -1165,6 +1250,21 @@ bool gres_cells_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_ma
         }();
         const double* vals = d_skyv;
         const uint32_t* perm = nullptr;
+        static const bool nopriv = [] {  // SKYGPU_MG_NOPRIV=1: every step marks in HBM
+            const char* e = getenv("SKYGPU_MG_NOPRIV");
+            return e && e[0] == '1';
+        }();
+        uint32_t* stage = c.buf[B_MGSTAGE].as<uint32_t>((uint64_t)c.num_sms * 4 * kPrivCells / 4);
+        static bool priv_attr = false;
+        if (!priv_attr) {
+            SKY_CUDA(cudaFuncSetAttribute(k_mg_mark_priv<uint32_t>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)(kPrivCells * 4)));
+            SKY_CUDA(cudaFuncSetAttribute(k_mg_mark_priv<unsigned long long>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)(kPrivCells * 4)));
+            priv_attr = true;
+        }
         if (!nosort && na == S) {
             auto* k0 = c.buf[B_MGKEY0].as<unsigned long long>(S);
             auto* k1 = c.buf[B_MGKEY1].as<unsigned long long>(S);
@@ -1207,15 +1307,26 @@ bool gres_cells_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_ma
             for (int li = 0; li < sl.n; ++li) {
                 MinGeom geo;
                 min_geometry(amax, d, sl.g[li], 16ull << 30, &geo);
-                pdl_launch(k_mg_fill, grid_for(geo.bytes / 16, kBlock), kBlock, 0, c.stream,
-                           (uint4*)M, geo.bytes / 16, n_in);
                 pdl_launch(k_clear_slot_c, 1, 1, 0, c.stream, cnt[cur]);
+                const bool priv = !nopriv && geo.bytes <= kPrivCells;
+                const uint32_t nslots =
+                    (uint32_t)c.num_sms * (geo.bytes * 4 <= 48 * 1024 ? 4u : 1u);
                 const unsigned gs = grid_for(S, kBlock);
                 const unsigned gq = grid_for(na, kBlock);
                 int nl = 0;
                 auto run = [&](auto* cg) {
                     using CW = std::remove_const_t<std::remove_pointer_t<decltype(cg)>>;
-                    pdl_launch(k_mg_mark<CW>, gs, kBlock, 0, c.stream, cg, S, geo, M, n_in);
+                    if (priv) {
+                        pdl_launch(k_mg_mark_priv<CW>, nslots, kBlock, (size_t)geo.bytes * 4,
+                                   c.stream, cg, S, geo, stage, n_in);
+                        pdl_launch(k_mg_mark_reduce, grid_for(geo.bytes / 4, kBlock), kBlock, 0,
+                                   c.stream, (const uint32_t*)stage, nslots,
+                                   (uint32_t)(geo.bytes / 4), (uint32_t*)M, n_in);
+                    } else {
+                        pdl_launch(k_mg_fill, grid_for(geo.bytes / 16, kBlock), kBlock, 0,
+                                   c.stream, (uint4*)M, geo.bytes / 16, n_in);
+                        pdl_launch(k_mg_mark<CW>, gs, kBlock, 0, c.stream, cg, S, geo, M, n_in);
+                    }
                     nl = min_sweeps(c, M, geo, n_in);
                     pdl_launch(k_mg_query<CW>, gq, kBlock, 0, c.stream, cg, geo, (const uint8_t*)M,
                                in, na, n_in, d_den, perm, lists[cur], cnt[cur]);
