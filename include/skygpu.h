@@ -108,6 +108,8 @@ typedef struct skygpu_stats {
     uint64_t gres_kernel_launches;
     uint64_t sky_kernel_launches;
     uint64_t kernel_launches;      /* all of libskygpu's kernel launches in the call */
+    uint64_t sky_units;            /* rank-grid decide kernel: (comparator, 128-candidate item)
+                                      bitset tests — the unit of its shared-memory roofline */
 } skygpu_stats;
 
 /* library / device */

@@ -88,7 +88,7 @@ __global__ void k_init_slots(unsigned long long* slots, int mode) {
     const int i = threadIdx.x;
     if (i >= S_COUNT_) return;
     if (mode == 1) {  // test counters only
-        if (i == S_TESTS_SKY || i == S_TESTS_GRES) slots[i] = 0;
+        if (i == S_TESTS_SKY || i == S_TESTS_GRES || i == S_UNITS_SKY) slots[i] = 0;
         return;
     }
     if (mode == 2) {  // round counters only
@@ -100,7 +100,8 @@ __global__ void k_init_slots(unsigned long long* slots, int mode) {
         if (i == S_SMAX) slots[i] = 0;
         return;
     }
-    if (i == S_TESTS_SKY || i == S_TESTS_GRES || i == S_SPEC || i == S_IDSBAD) return;
+    if (i == S_TESTS_SKY || i == S_TESTS_GRES || i == S_UNITS_SKY || i == S_SPEC || i == S_IDSBAD)
+        return;
     unsigned long long v = 0;
     if (i == S_BAD || i == S_PAIR || i == S_GRIDBAD || i == S_SMIN) v = ~0ULL;
     if (i == S_MINGAP) v = 0x7FF0000000000000ULL;
@@ -225,7 +226,7 @@ void begin_stats(Ctx& c, skygpu_stats* st) {
 // final synchronisation), so end_stats needs no round trip of its own
 void fetch_test_counters(Ctx& c) {
     SKY_CUDA(cudaMemcpyAsync(c.h_slots + S_TESTS_SKY, c.d_slots + S_TESTS_SKY,
-                             2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c.stream));
+                             3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c.stream));
     c.counters_fetched = true;
 }
 
@@ -234,10 +235,11 @@ void end_stats(Ctx& c) {
         c.counters_fetched = false;  // recorded since then are left to complete
         SKY_CUDA(cudaStreamSynchronize(c.stream));
     } else {
-        read_slots(c, S_TESTS_SKY, 2);
+        read_slots(c, S_TESTS_SKY, 3);
     }
     c.st->skyline_tests = c.h_slots[S_TESTS_SKY];
     c.st->gres_tests = c.h_slots[S_TESTS_GRES];
+    c.st->sky_units = c.h_slots[S_UNITS_SKY];
     for (int i = 0; i < c.nspans; ++i) {
         float ms = 0;
         SKY_CUDA(cudaEventElapsedTime(&ms, c.ev[c.spans[i].a], c.ev[c.spans[i].a + 1]));

@@ -458,18 +458,22 @@ void sweeps(Ctx& c, W* R, const CellGeom& geo, bool fused, const unsigned long l
 // Min-grid form (the default for packed codes).  The bitset row above is,
 // after its in-word prefix-OR, a run of ones from the smallest attribute-0
 // code of any tuple whose other codes are <= the row's: the whole row is that
-// ONE number.  So the grid stores, per cell of the remaining d-1 attributes,
-//     M[r] = min { c_m(s) : row(s) <= r componentwise }   (0x7F: none)
-// one byte instead of a 32/64-bit word, and t (code c, row r) is dominated iff
-//     M[r] < c_m(t)   or   M[r - e_j] <= c_m(t)   for a grid attribute j, c_j >= 1
-// (the same two cases as the bitset query: a strictly smaller code on the
-// min'd attribute m in a row <= r, or a row strictly below r with a code <=).
-// The min'd attribute m is the one with the largest extent (smallest grid).
-// Byte grids are 4x smaller than u32 rows, so a step's grid is written once,
-// swept in two passes (d = 7) of SIMD byte minima (min7), and every
-// step below g ~ 22 of C5 stays resident in the 126 MB L2 across its passes.
-// Grid dim 0 (the fastest) is padded to a multiple of 4 bytes so that every
-// other dim's stride is a whole number of u32 words.
+// ONE number.  So the grid keeps ONE BYTE per cell r of the other d-1
+// attributes (m = the min'd attribute, the one of largest extent):
+//     P[r] = min { c_m(s) : row(s) <= r componentwise }
+//     M[r] = 2 P[r] + G[r],  G[r] = 0 iff P[r] is also attained by a row
+//                            strictly below r (0x7F: no tuple at all)
+// A skyline tuple t sits in its own cell r, so P[r] <= c_m(t), and t is
+// dominated iff P[r] < c_m(t) (a smaller code in a row <= r) or P[r] =
+// c_m(t) attained strictly below r:  M[r] <= 2 c_m(t).  ONE byte read per
+// query (the bitset form reads the row and one row below per attribute).
+// Sweeping keeps the encoding: along a dim, a predecessor contributes its
+// value with the low bit cleared (min(v, acc & ~1) — "attained below"), the
+// cell itself its own value; the mark writes 2 c_m + 1.  c_m <= 62 (extent
+// <= 63) keeps every value at most 125 < 0x7F.  Byte grids are 4x smaller
+// than u32 rows; every step below g ~ 22 of C5 stays resident in the 126 MB
+// L2 across its passes.  Grid dim 0 (the fastest) is padded to a multiple of
+// 4 bytes so that every other dim's stride is a whole number of u32 words.
 namespace {
 
 struct MinGeom {
@@ -482,12 +486,13 @@ struct MinGeom {
     uint64_t bytes;                // grid bytes (a multiple of 16)
 };
 
-// Cells hold 7-bit values (codes <= 126; 0x7F = empty), so a bytewise
+// Cells hold 7-bit values (<= 125; 0x7F = empty), so a bytewise
 // minimum is 3 instructions instead of __vminu4's emulated 7: t = a + 0x80 -
 // b per byte cannot carry or borrow across bytes, its top bit is a >= b,
 // PRMT replicates that bit over the byte, a LOP3 selects.
 constexpr uint32_t kEmpty = 0x7Fu;
 constexpr uint32_t kEmpty4 = 0x7F7F7F7Fu;
+constexpr uint32_t kPred4 = 0xFEFEFEFEu;  // a predecessor's value: its "own cell only" bit cleared
 
 __device__ __forceinline__ uint32_t min7(uint32_t a, uint32_t b) {
     const uint32_t t = a + 0x80808080u - b;
@@ -513,48 +518,30 @@ __global__ void k_mg_fill(uint4* __restrict__ p, uint64_t n16, const unsigned lo
         p[i] = f;
 }
 
-// every skyline tuple lowers its cell's byte to its code on attribute m.
-// Lanes of a warp that hit the same word combine first (match + byte
-// minima), then one CAS per word, optimistic about a fresh (0x7F) word.
+// every skyline tuple lowers its cell's byte to 2 c_m + 1 ("attained in
+// this cell"): one CAS, optimistic about a fresh (empty) word, retried with
+// the bytewise minimum when the word already holds marks
 template <class CW>
 __global__ void __launch_bounds__(kBlock)
 k_mg_mark(const CW* __restrict__ code, uint64_t S, MinGeom geo, uint8_t* __restrict__ M,
           const unsigned long long* live) {
     pdl_wait();
     if (step_dead(live)) return;
-    const uint32_t lane = threadIdx.x & 31;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t b = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) & ~31ULL; b < S; b += stride) {
-        const uint64_t i = b + lane;
-        uint32_t mine = kEmpty4;
-        uint64_t wi = ~0ULL;
-        if (i < S) {
-            const CW w = code[i];
-            const uint64_t r = mg_row(w, geo);
-            const uint32_t c0 = (uint32_t)(w >> (8 * geo.m)) & 0xFFu;
-            const uint32_t sh = 8u * (uint32_t)(r & 3u);
-            wi = r >> 2;
-            mine = (kEmpty4 & ~(0xFFu << sh)) | (c0 << sh);
-        }
-        const unsigned peers = __match_any_sync(0xffffffffu, wi);
-        uint32_t acc = mine;
-        if (__any_sync(0xffffffffu, __popc(peers) > 1)) {
-#pragma unroll 8
-            for (int k = 0; k < 32; ++k) {
-                const uint32_t v = __shfl_sync(0xffffffffu, mine, k);
-                if ((peers >> k) & 1u) acc = min7(acc, v);
-            }
-        }
-        if (i < S && (uint32_t)(__ffs(peers) - 1) == lane) {
-            uint32_t* word = reinterpret_cast<uint32_t*>(M) + wi;
-            uint32_t old = atomicCAS(word, kEmpty4, acc);
-            while (old != kEmpty4) {
-                const uint32_t nw = min7(old, acc);
-                if (nw == old) break;
-                const uint32_t prev = atomicCAS(word, old, nw);
-                if (prev == old) break;
-                old = prev;
-            }
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < S;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const CW w = code[i];
+        const uint64_t r = mg_row(w, geo);
+        const uint32_t c0 = (uint32_t)(w >> (8 * geo.m)) & 0xFFu;
+        const uint32_t sh = 8u * (uint32_t)(r & 3u);
+        const uint32_t mine = (kEmpty4 & ~(0xFFu << sh)) | ((2u * c0 + 1u) << sh);
+        uint32_t* word = reinterpret_cast<uint32_t*>(M) + (r >> 2);
+        uint32_t old = atomicCAS(word, kEmpty4, mine);
+        while (old != kEmpty4) {
+            const uint32_t nw = min7(old, mine);
+            if (nw == old) break;
+            const uint32_t prev = atomicCAS(word, old, nw);
+            if (prev == old) break;
+            old = prev;
         }
     }
 }
@@ -582,7 +569,8 @@ k_mg_mark_priv(const CW* __restrict__ code, uint64_t S, MinGeom geo, uint32_t* _
         const CW w = code[i];
         const uint32_t r = (uint32_t)mg_row(w, geo);
         const uint32_t c0 = (uint32_t)(w >> (8 * geo.m)) & 0xFFu;
-        if (cm[r] > c0) atomicMin(&cm[r], c0);
+        const uint32_t v = 2u * c0 + 1u;
+        if (cm[r] > v) atomicMin(&cm[r], v);
     }
     __syncthreads();
     uint32_t* out = stage + (uint64_t)blockIdx.x * (ncells / 4);
@@ -605,9 +593,9 @@ __global__ void k_mg_mark_reduce(const uint32_t* __restrict__ stage, uint32_t ns
 // prefix minimum along the 4 bytes of a word (byte k = lower address first),
 // then against the previous word's last byte
 __device__ __forceinline__ uint32_t bytes_prefix_min(uint32_t x, uint32_t carry) {
-    x = min7(x, (x << 8) | kEmpty);
-    x = min7(x, (x << 16) | (kEmpty4 >> 16));
-    return min7(x, carry * 0x01010101u);
+    x = min7(x, ((x << 8) | kEmpty) & kPred4);
+    x = min7(x, ((x << 16) | (kEmpty4 >> 16)) & kPred4);
+    return min7(x, (carry & 0xFEu) * 0x01010101u);
 }
 
 // grid dims 0, 1, 2 (ND of them) of ns whole slabs staged in shared memory
@@ -631,7 +619,7 @@ __device__ __forceinline__ void slab_prefix(uint32_t* sw, uint32_t ns, uint32_t 
             uint32_t* p = sw + (uint64_t)(l / w0) * w0 * e1 + (l % w0);
             uint32_t acc = kEmpty4;
             for (uint32_t a = 0; a < e1; ++a) {
-                acc = min7(acc, p[a * w0]);
+                acc = min7(p[a * w0], acc & kPred4);
                 p[a * w0] = acc;
             }
         }
@@ -643,7 +631,7 @@ __device__ __forceinline__ void slab_prefix(uint32_t* sw, uint32_t ns, uint32_t 
             uint32_t* p = sw + (uint64_t)(l / plane) * slab + (l % plane);
             uint32_t acc = kEmpty4;
             for (uint32_t b = 0; b < e2; ++b) {
-                acc = min7(acc, p[b * plane]);
+                acc = min7(p[b * plane], acc & kPred4);
                 p[b * plane] = acc;
             }
         }
@@ -726,7 +714,7 @@ k_mg_slabcol(uint32_t* __restrict__ M, uint32_t ncols, uint32_t w0, uint32_t e1,
             uint32_t* o = base + (uint64_t)c3 * slab;
             for (uint32_t i = threadIdx.x; i < slab; i += blockDim.x) {
                 uint32_t x = sw[i];
-                if (c3) x = min7(x, run[i]);
+                if (c3) x = min7(x, run[i] & kPred4);
                 run[i] = x;
                 o[i] = x;
             }
@@ -760,11 +748,72 @@ k_mg_pair(uint32_t* __restrict__ M, uint64_t nwords, uint32_t ea, uint32_t eb, u
             uint32_t run = kEmpty4;
 #pragma unroll
             for (int x = 0; x < EA; ++x) {
-                run = min7(run, min7(v[x], prev[x]));
+                run = min7(v[x], min7(run, prev[x]) & kPred4);
                 prev[x] = run;
                 if ((uint32_t)x < ea) p[(uint64_t)x * sa] = run;
             }
         }
+    }
+}
+
+// the same two dims staged through shared memory: a block takes a tile of
+// 32 consecutive u32 columns (128-byte lines) over the whole (ea x eb) plane,
+// all of it requested at once with cp.async (every load in flight), then
+// sweeps dim a and dim b in shared memory with every thread busy, and
+// writes the tile back — the register form above holds only ~16 warps per
+// SM (125 registers) and its loads wait row by row
+constexpr int kPT = 32;
+
+__device__ __forceinline__ void cp_async4(uint32_t* dst, const uint32_t* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                     static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+                 "l"(src)
+                 : "memory");
+}
+
+__global__ void __launch_bounds__(kBlock)
+k_mg_pair_smem(uint32_t* __restrict__ M, uint64_t nwords, uint32_t ea, uint32_t eb, uint64_t sa,
+               const unsigned long long* live) {
+    pdl_wait();
+    if (step_dead(live)) return;
+    extern __shared__ __align__(16) uint32_t tile[];  // [ea * eb][kPT]
+    const uint32_t plane = ea * eb;
+    const uint64_t nhi = nwords / (sa * plane);
+    const uint64_t tph = (sa + kPT - 1) / kPT;  // tiles per hi index
+    for (uint64_t t = blockIdx.x; t < nhi * tph; t += gridDim.x) {
+        const uint64_t hi = t / tph;
+        const uint32_t lo0 = (uint32_t)(t - hi * tph) * kPT;
+        const uint32_t ncol = (uint32_t)min((uint64_t)kPT, sa - lo0);
+        uint32_t* base = M + hi * sa * plane + lo0;
+        for (uint32_t i = threadIdx.x; i < plane * kPT; i += blockDim.x) {
+            const uint32_t e = i / kPT, col = i % kPT;
+            if (col < ncol) cp_async4(&tile[i], base + (uint64_t)e * sa + col);
+        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncthreads();
+        for (uint32_t l = threadIdx.x; l < eb * kPT; l += blockDim.x) {  // dim a
+            uint32_t* q = tile + (l / kPT) * ea * kPT + (l % kPT);
+            uint32_t acc = kEmpty4;
+            for (uint32_t x = 0; x < ea; ++x) {
+                acc = min7(q[x * kPT], acc & kPred4);
+                q[x * kPT] = acc;
+            }
+        }
+        __syncthreads();
+        for (uint32_t l = threadIdx.x; l < ea * kPT; l += blockDim.x) {  // dim b
+            uint32_t* q = tile + l;
+            uint32_t acc = kEmpty4;
+            for (uint32_t y = 0; y < eb; ++y) {
+                acc = min7(q[y * ea * kPT], acc & kPred4);
+                q[y * ea * kPT] = acc;
+            }
+        }
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < plane * kPT; i += blockDim.x) {
+            const uint32_t e = i / kPT, col = i % kPT;
+            if (col < ncol) base[(uint64_t)e * sa + col] = tile[i];
+        }
+        __syncthreads();
     }
 }
 
@@ -787,13 +836,13 @@ k_mg_dim(uint32_t* __restrict__ M, uint64_t nwords, uint32_t e, uint64_t s,
             uint32_t acc = kEmpty4;
 #pragma unroll
             for (int k = 0; k < E; ++k) {
-                acc = min7(acc, v[k]);
+                acc = min7(v[k], acc & kPred4);
                 if ((uint32_t)k < e) p[(uint64_t)k * s] = acc;
             }
         } else {
             uint32_t acc = kEmpty4;
             for (uint64_t k = 0; k < e; ++k) {
-                acc = min7(acc, p[k * s]);
+                acc = min7(p[k * s], acc & kPred4);
                 p[k * s] = acc;
             }
         }
@@ -820,14 +869,11 @@ __global__ void k_mg_query(const CW* __restrict__ code, MinGeom geo, const uint8
             const CW w = code[t];
             const uint64_t r = mg_row(w, geo);
             const uint32_t c0 = (uint32_t)(w >> (8 * geo.m)) & 0xFFu;
-            // every cell the test needs, loaded together (one round trip)
-            uint32_t lo = kEmpty;
-#pragma unroll
-            for (int j = 0; j < 7; ++j) {
-                if (j < geo.nd && ((uint32_t)(w >> (8 * geo.attr[j])) & 0xFFu))
-                    lo = min(lo, (uint32_t)M[r - geo.stride[j]]);
-            }
-            const bool hit = (uint32_t)M[r] < c0 || lo <= c0;
+            // one byte: P = M[r] >> 1 is the smallest c_m over rows <= r, and
+            // its low bit is 0 iff that minimum is also attained strictly
+            // below r; t (which is in cell r itself) is dominated iff
+            // P < c_m(t) or (P == c_m(t) and attained below): M[r] <= 2 c_m(t)
+            const bool hit = (uint32_t)M[r] <= 2u * c0;
             if (hit) den[perm ? perm[t] : t] = geo.g;
             keep = !hit;
         }
@@ -883,7 +929,7 @@ static bool min_geometry(const std::vector<double>& amax, int d, int g, uint64_t
         e[j] = (uint32_t)k + 1;
         if (e[j] > e[m]) m = j;
     }
-    if (e[m] > 127) return false;  // the min'd codes must stay below the empty value 0x7F
+    if (e[m] > 63) return false;  // 2 c_m + 1 must stay below the empty value 0x7F
     geo->nd = d - 1;
     geo->m = m;
     geo->g = g;
@@ -913,6 +959,11 @@ static int min_sweeps(Ctx& c, uint8_t* M, const MinGeom& geo, const unsigned lon
         const char* e = getenv("SKYGPU_MG_NOCOL");
         return e && e[0] == '1';
     }();
+    static const bool nosmem = [] {  // SKYGPU_MG_PAIRREG=1: the register pair kernel
+        const char* e = getenv("SKYGPU_MG_PAIRREG");
+        return e && e[0] == '1';
+    }();
+    constexpr size_t kPairSmemMax = 112 * 1024;
     uint32_t* W = reinterpret_cast<uint32_t*>(M);
     // (whole rows only: the 16-byte padding of the fill stays empty)
     const uint64_t real_words = geo.stride[geo.nd - 1] * geo.ext[geo.nd - 1] / 4;
@@ -933,6 +984,8 @@ static int min_sweeps(Ctx& c, uint8_t* M, const MinGeom& geo, const unsigned lon
         SKY_CUDA(cudaFuncSetAttribute(k_mg_slab<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSlabMax));
         SKY_CUDA(cudaFuncSetAttribute(k_mg_slab<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSlabMax));
         SKY_CUDA(cudaFuncSetAttribute(k_mg_slabcol, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSlabMax));
+        SKY_CUDA(cudaFuncSetAttribute(k_mg_pair_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)kPairSmemMax));
         attr_set = true;
     }
     const uint64_t nslabs = real_words / (slab / 4);
@@ -958,7 +1011,15 @@ static int min_sweeps(Ctx& c, uint8_t* M, const MinGeom& geo, const unsigned lon
     while (j < geo.nd) {
         const uint64_t sa = geo.stride[j] / 4;
         const uint32_t ea = geo.ext[j];
-        if (j + 1 < geo.nd && ea <= 32) {
+        if (j + 1 < geo.nd && !nosmem && (size_t)ea * geo.ext[j + 1] * kPT * 4 <= kPairSmemMax &&
+            sa >= (uint64_t)kPT) {
+            const uint32_t eb = geo.ext[j + 1];
+            const size_t smem = (size_t)ea * eb * kPT * 4;
+            const uint64_t tiles = real_words / (sa * ea * eb) * ((sa + kPT - 1) / kPT);
+            pdl_launch(k_mg_pair_smem, grid_for(tiles, 1, c.num_sms * 2), kBlock, smem, c.stream, W,
+                       real_words, ea, eb, sa, live);
+            j += 2;
+        } else if (j + 1 < geo.nd && ea <= 32) {
             const uint64_t lines = real_words / ((uint64_t)ea * geo.ext[j + 1]);
             const unsigned gp = grid_for(lines, kBlock);
             const uint32_t eb = geo.ext[j + 1];
@@ -1240,13 +1301,15 @@ bool gres_cells_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_ma
         const unsigned long long* n_in = nullptr;
         int cur = 0, nrun = 0;
         uint64_t swept = 0;
-        // locality order (every candidate asked: na == S with act the
-        // identity, the only way this engine is called): values permuted by
-        // the top step's row, candidates = sorted positions, den written
-        // through the permutation (SKYGPU_CELLS_NOSORT=1: input order)
+        // locality order (SKYGPU_CELLS_SORT=1; every candidate asked: na ==
+        // S with act the identity, the only way this engine is called):
+        // values permuted by the top step's row, candidates = sorted
+        // positions, den written through the permutation.  Off by default:
+        // with one-byte queries the sort and permutation cost more than the
+        // locality saves (C5: 1.1 ms against ~0.7 ms)
         static const bool nosort = [] {
-            const char* e = getenv("SKYGPU_CELLS_NOSORT");
-            return e && e[0] == '1';
+            const char* e = getenv("SKYGPU_CELLS_SORT");
+            return !(e && e[0] == '1');
         }();
         const double* vals = d_skyv;
         const uint32_t* perm = nullptr;

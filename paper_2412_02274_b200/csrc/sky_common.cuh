@@ -109,25 +109,26 @@ enum Slot {
     S_SEL = 0,         // DeviceSelect count
     S_TESTS_SKY = 1,   // dominance tests, skyline stage
     S_TESTS_GRES = 2,  // code tests, gres stage
-    S_MINGAP = 3,      // bits of the min positive gap (atomicMin)
-    S_MAXV = 4,        // bits of max |value| (atomicMax)
-    S_BAD = 5,         // first tuple index with a negative/NaN value (atomicMin; ~0 = none)
-    S_FLAG = 6,        // generic flag
-    S_PAIR = 7,        // check_skyline: min (a*S + b) (~0 = none)
-    S_SEL2 = 8,
-    S_GRIDBAD = 9,     // first flat index of a Grid value outside [0,1]
-    S_SMIN = 10,       // ord bits of the min / max tuple sum (skyline rounds)
-    S_SMAX = 11,
-    S_THR = 12,        // bits of the prefix threshold T (double)
-    S_C1 = 13,         // prefix size
-    S_C2 = 14,         // new skyline tuples of the round
-    S_C3 = 15,         // survivors of the round
-    S_GATE = 16,       // 1: the first round asks for the rank-grid engine (K5 skipped)
-    S_SPEC = 17,       // 1: the speculative gres launch did not apply (gres.cu), redo
-    S_IDSBAD = 18,     // 1: ids that arrived late were not strictly increasing, redo
-    S_LIVE0 = 19,      // cell engine: undecided candidates after a step (ping-pong)
-    S_LIVE1 = 20,
-    S_COUNT_ = 21
+    S_UNITS_SKY = 3,  // rank-grid K6: (comparator, item) bitset tests
+    S_MINGAP = 4,      // bits of the min positive gap (atomicMin)
+    S_MAXV = 5,        // bits of max |value| (atomicMax)
+    S_BAD = 6,         // first tuple index with a negative/NaN value (atomicMin; ~0 = none)
+    S_FLAG = 7,        // generic flag
+    S_PAIR = 8,        // check_skyline: min (a*S + b) (~0 = none)
+    S_SEL2 = 9,
+    S_GRIDBAD = 10,     // first flat index of a Grid value outside [0,1]
+    S_SMIN = 11,       // ord bits of the min / max tuple sum (skyline rounds)
+    S_SMAX = 12,
+    S_THR = 13,        // bits of the prefix threshold T (double)
+    S_C1 = 14,         // prefix size
+    S_C2 = 15,         // new skyline tuples of the round
+    S_C3 = 16,         // survivors of the round
+    S_GATE = 17,       // 1: the first round asks for the rank-grid engine (K5 skipped)
+    S_SPEC = 18,       // 1: the speculative gres launch did not apply (gres.cu), redo
+    S_IDSBAD = 19,     // 1: ids that arrived late were not strictly increasing, redo
+    S_LIVE0 = 20,      // cell engine: undecided candidates after a step (ping-pong)
+    S_LIVE1 = 21,
+    S_COUNT_ = 22
 };
 
 struct Ctx {

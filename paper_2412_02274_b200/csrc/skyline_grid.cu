@@ -620,7 +620,7 @@ k_grid_decide_tma(const double* __restrict__ rec, const int64_t* __restrict__ id
     for (int j = 2; j < D; ++j) wj[j] = wj[j - 1] * (uint32_t)k;
     uint32_t ps = 0, pphase = 0;  // producer ring position (warp 0)
     uint32_t cs = 0, cphase = 0;  // consumer ring position (warps 1..3)
-    unsigned long long cnt = 0;
+    unsigned long long cnt = 0, ucnt = 0;  // tests, (comparator, item) units
     for (;;) {
         if (threadIdx.x == 0) sm.item = atomicAdd(&ctr[1], 1u);
         __syncthreads();
@@ -761,9 +761,11 @@ k_grid_decide_tma(const double* __restrict__ rec, const int64_t* __restrict__ id
                 const volatile uint32_t* av = sm.alive;
                 uint32_t al[4] = {av[0], av[1], av[2], av[3]};
                 if ((al[0] | al[1] | al[2] | al[3]) != 0u) {
-                    if (cw == 0 && lane == 0)
+                    if (cw == 0 && lane == 0) {
                         cnt += (unsigned long long)sm.nreal[cs] *
                                (__popc(al[0]) + __popc(al[1]) + __popc(al[2]) + __popc(al[3]));
+                        ucnt += sm.nreal[cs];
+                    }
                     uint2* hb = sm.hits[cw];
                     for (uint32_t s0 = cw * 32; s0 < n; s0 += 32 * kTCons) {
                         const uint32_t s = s0 + lane;
@@ -851,6 +853,7 @@ k_grid_decide_tma(const double* __restrict__ rec, const int64_t* __restrict__ id
         }
     }
     add_count(tests, cnt);
+    add_count(tests + (S_UNITS_SKY - S_TESTS_SKY), ucnt);
 }
 
 template <int D, class F>

@@ -68,7 +68,7 @@ class Stats(C.Structure):
                [(n, C.c_double) for n in ("ms_total", "ms_h2d", "ms_skyline", "ms_gres", "ms_d2h",
                                            "ms_gres_kernel", "ms_sky_kernel")] + \
                [(n, C.c_uint64) for n in ("gres_kernel_launches", "sky_kernel_launches",
-                                           "kernel_launches")]
+                                           "kernel_launches", "sky_units")]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -1,6 +1,6 @@
 timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "cell_engine or min_grid" > gpurun_out/mg_tests.log 2>&1; echo "cell tests rc=$?"; tail -3 gpurun_out/mg_tests.log
 timeout 900 python -m pytest tests/test_gpu_variants.py -q -x -k "cell_engine_variants" > gpurun_out/mg_var.log 2>&1; echo "variants rc=$?"; tail -2 gpurun_out/mg_var.log
-for e in "" "SKYGPU_CELLS_NOSORT=1" "SKYGPU_MG_NOPRIV=1"; do
+for e in "" "SKYGPU_CELLS_SORT=1" "SKYGPU_MG_PAIRREG=1"; do
 env $e timeout 600 python bench.py --no-cpu-baseline --steps 10 > gpurun_out/mg_bench.log 2>&1; echo "bench [$e] rc=$?"; tail -1 gpurun_out/mg_bench.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], d['stage_ms'], d['e2e']['ms_per_step'])"
 done
 CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline"

@@ -70,14 +70,17 @@ print(bad)
 """
 
 
-@pytest.mark.parametrize("env", [{"SKYGPU_CELLS_BITSET": "1"}, {"SKYGPU_CELLS_NOSORT": "1"},
-                                 {"SKYGPU_MG_NOCOL": "1"}, {"SKYGPU_MG_NOPRIV": "1"}])
+@pytest.mark.parametrize("env", [{"SKYGPU_CELLS_BITSET": "1"}, {"SKYGPU_CELLS_SORT": "1"},
+                                 {"SKYGPU_MG_NOCOL": "1"}, {"SKYGPU_MG_NOPRIV": "1"},
+                                 {"SKYGPU_MG_PAIRREG": "1"}])
 def test_cell_engine_variants(env):
     """The HBM cell engine's alternatives against the pair engine's map:
     SKYGPU_CELLS_BITSET=1 the u32/u64 bitset-row form (the min-grid form is
-    the default), SKYGPU_CELLS_NOSORT=1 the min-grid over the input order (no
-    locality sort), SKYGPU_MG_NOCOL=1 the slab pass without the dim-3 running
-    minimum (one more sweep)."""
+    the default), SKYGPU_CELLS_SORT=1 the min-grid over a locality order (the
+    top step's rows), SKYGPU_MG_NOCOL=1 the slab pass without the dim-3 running
+    minimum (one more sweep), SKYGPU_MG_NOPRIV=1 every step marked in HBM (no
+    shared-memory privatised marks), SKYGPU_MG_PAIRREG=1 the register form of
+    the two-dim sweep."""
     e = dict(os.environ, SKYGPU_CELLS_SMEM="0", **env)
     out = subprocess.check_output([sys.executable, "-c", _BITSET, os.path.dirname(HERE)], env=e,
                                   text=True, timeout=900)
