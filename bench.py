@@ -418,6 +418,22 @@ def roofline(st, sky_ms, gres_ms, d, clk, workload="C2"):
                     "algorithmic_bytes_per_step": byts, "kernel_ms_per_step": ms,
                     "launches_per_step": st["gres_kernel_launches"],
                     "bytes_model": "per step: grid zeroed + read + written once, S*d*8 B read twice"}
+        if kind == "skyline" and st["sky_engine"] == 16 and st.get("sky_units"):
+            # rank-grid engine, TMA bitset decide kernel (skyline_grid.cu K6): one
+            # unit = one staged comparator tested against a 128-candidate item =
+            # D 16-byte candidate-bitset table reads; the shared-memory pipe
+            # (128 B/clk/SM) bounds it: peak = 148 * f * 128 / (16 D) units/s
+            units, ms, launches = st["sky_units"], sky_ms, st["sky_kernel_launches"]
+            peak = 148 * f * 128.0 / (16.0 * d)
+            achieved = units / (ms / 1e3) if ms > 0 else 0.0
+            return {"bound": "shared-memory pipe", "kernel": "k_grid_decide_tma",
+                    "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "G comparator-item tests/s",
+                    "frac": achieved / peak, "traffic": kernel_traffic(workload, "k_grid_decide"),
+                    "traffic_unit": "B/launch (ncu dram read+write)", "units_per_step": units,
+                    "tests_per_step": st["skyline_tests"], "kernel_ms_per_step": ms,
+                    "launches_per_step": launches, "bytes_smem_per_unit": 16 * d,
+                    "smem_bytes_per_clk_sm": 128, "f_clk_mhz": f / 1e6,
+                    "dominance_tests_per_s": st["skyline_tests"] / (ms / 1e3) / 1e9 if ms > 0 else 0.0}
         if kind == "skyline" and st["sky_engine"] == 16:  # rank-grid engine (skyline_grid.cu)
             tests, ms, launches = st["skyline_tests"], sky_ms, st["sky_kernel_launches"]
             i_test, l_pipe = 3, 64  # IADD3 + LOP3 + VIMNMX on the ALU pipe (+ IMAD.X, FMA pipe)

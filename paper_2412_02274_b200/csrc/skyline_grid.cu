@@ -80,7 +80,8 @@ template <int D>
 __global__ void __launch_bounds__(kGB)
 k_rank_codes(const double* __restrict__ v, const uint32_t* __restrict__ R, uint32_t r,
              const double* __restrict__ bounds, int k0, int k, GridWord<D>* __restrict__ code,
-             uint32_t* __restrict__ cell, uint32_t* __restrict__ count) {
+             uint32_t* __restrict__ cell, uint32_t* __restrict__ count,
+             uint32_t* __restrict__ iota) {
     pdl_wait();
     using W = GridWord<D>;
     __shared__ double sb[D * 128];
@@ -108,7 +109,8 @@ k_rank_codes(const double* __restrict__ v, const uint32_t* __restrict__ R, uint3
         const uint32_t cl = b0 + (uint32_t)k0 * row;
         code[i] = w;
         cell[i] = cl;
-        atomicAdd(&count[cl], 1u);
+        if (iota) iota[i] = i;
+        else atomicAdd(&count[cl], 1u);
     }
 }
 
@@ -126,6 +128,28 @@ __global__ void k_cell_scatter(const W* __restrict__ code, const uint32_t* __res
     }
 }
 
+// sorted-cell form of the bucketing (default): the cells sorted by a stable
+// radix sort (no per-tuple atomics on a 4M-entry histogram), then the
+// segment table from the run boundaries: seg[c] = first sorted position with
+// cell >= c, for every c in [0, ncells]
+__global__ void k_seg_bounds(const uint32_t* __restrict__ skey, uint32_t r, uint32_t ncells,
+                             uint32_t* __restrict__ seg) {
+    pdl_wait();
+    for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q <= r; q += gridDim.x * blockDim.x) {
+        const uint32_t hi = q < r ? skey[q] : ncells;
+        const uint32_t lo = q > 0 ? skey[q - 1] + 1 : 0;
+        for (uint32_t c = lo; c <= hi; ++c) seg[c] = q;
+    }
+}
+
+template <class W>
+__global__ void k_gather_codes(const uint32_t* __restrict__ sidx, uint32_t r,
+                               const W* __restrict__ code, W* __restrict__ scode) {
+    pdl_wait();
+    for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < r; q += gridDim.x * blockDim.x)
+        scode[q] = code[sidx[q]];
+}
+
 // each tuple's exact record in cell order: its D float64 values and its
 // sum key, (D + 1) doubles at rec[pos * (D + 1)] — the TMA decide kernel's
 // exact follow-up then reads one contiguous record per side instead of
@@ -135,10 +159,12 @@ template <int D>
 __global__ void k_gather_rec(const uint32_t* __restrict__ sidx, uint32_t r,
                              const double* __restrict__ v,
                              const unsigned long long* __restrict__ key,
-                             const uint32_t* __restrict__ R, double* __restrict__ rec) {
+                             const uint32_t* __restrict__ R, double* __restrict__ rec,
+                             const GridWord<D>* __restrict__ code, GridWord<D>* __restrict__ scode) {
     pdl_wait();
     for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < r; q += gridDim.x * blockDim.x) {
         const uint32_t i = sidx[q];
+        if (code) scode[q] = code[i];
         const uint64_t p = R ? R[i] : i;
         double x[D + 1];
 #pragma unroll
@@ -912,7 +938,14 @@ void sky_grid_decide(Ctx& c, const double* d_vals, int d, const unsigned long lo
     uint32_t* count = c.buf[B_GCNT].as<uint32_t>(cwords);
     uint32_t* seg = count + ncells + 1;
     unsigned* ctr = (unsigned*)(seg + ncells + 1);
-    SKY_CUDA(cudaMemsetAsync(count, 0, sizeof(uint32_t) * cwords, c.stream));
+    static const bool atomic_bucket = [] {  // see the bucketing below
+        const char* e = getenv("SKYGPU_GRID_ATOMIC");
+        return e && e[0] == '1';
+    }();
+    if (atomic_bucket)
+        SKY_CUDA(cudaMemsetAsync(count, 0, sizeof(uint32_t) * cwords, c.stream));
+    else  // (seg is written whole by k_seg_bounds; only the item counters)
+        SKY_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned) * 2, c.stream));
     pdl_launch(k_rank_bounds, d, 1024, 0, c.stream, d_vals, d, R, r, bounds);
     SKY_LAUNCH_CHECK();
     note_launch(c);
@@ -928,30 +961,58 @@ void sky_grid_decide(Ctx& c, const double* d_vals, int d, const unsigned long lo
         SKY_CUDA(cudaMemsetAsync(scode + r, 0x80, 16, c.stream));
         uint32_t* sidx = c.buf[B_GSIDX].as<uint32_t>(r);
         uint2* items = c.buf[B_GITEMS].as<uint2>(r / kItem + g.rows + 1);
-        pdl_launch(k_rank_codes<D>, grid_for(r, kGB, c.num_sms * 8), kGB, 0, c.stream,
-            d_vals, R, (uint32_t)r, bounds, g.k0, g.k, code, cell, count);
-        SKY_LAUNCH_CHECK();
-        size_t tmp = 0;
-        SKY_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, count, seg, (int)ncells + 1,
-                                               c.stream));
-        void* t = c.buf[B_CUB].get(tmp);
-        SKY_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, count, seg, (int)ncells + 1, c.stream));
-        SKY_CUDA(cudaMemsetAsync(count, 0, sizeof(uint32_t) * ncells, c.stream));  // cursors
+        // bucketing by cell: a stable radix sort of the cell ids (default),
+        // or a histogram + scan + atomic scatter (SKYGPU_GRID_ATOMIC=1)
         // K6: the TMA-staged bitset kernel (default) or the per-lane ALU
         // kernel (SKYGPU_GRID_KERNEL=alu, kept for A/B measurement)
         static const bool alu = [] {
             const char* e = getenv("SKYGPU_GRID_KERNEL");
             return e && e[0] == 'a';
         }();
-        double* rec = nullptr;
-        pdl_launch(k_cell_scatter<W>, grid_for(r, kGB), kGB, 0, c.stream, code, cell,
-                   (uint32_t)r, seg, count, scode, sidx);
-        if (!alu) {
-            rec = c.buf[B_GREC].as<double>(r * (D + 1));
-            pdl_launch(k_gather_rec<D>, grid_for(r, kGB), kGB, 0, c.stream, sidx, (uint32_t)r,
-                       d_vals, keys, R, rec);
+        double* rec = alu ? nullptr : c.buf[B_GREC].as<double>(r * (D + 1));
+        if (atomic_bucket) {
+            pdl_launch(k_rank_codes<D>, grid_for(r, kGB, c.num_sms * 8), kGB, 0, c.stream,
+                d_vals, R, (uint32_t)r, bounds, g.k0, g.k, code, cell, count, (uint32_t*)nullptr);
+            SKY_LAUNCH_CHECK();
+            size_t tmp = 0;
+            SKY_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, count, seg, (int)ncells + 1,
+                                                   c.stream));
+            void* t = c.buf[B_CUB].get(tmp);
+            SKY_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, count, seg, (int)ncells + 1, c.stream));
+            SKY_CUDA(cudaMemsetAsync(count, 0, sizeof(uint32_t) * ncells, c.stream));  // cursors
+            pdl_launch(k_cell_scatter<W>, grid_for(r, kGB), kGB, 0, c.stream, code, cell,
+                       (uint32_t)r, seg, count, scode, sidx);
+            if (rec)
+                pdl_launch(k_gather_rec<D>, grid_for(r, kGB), kGB, 0, c.stream, sidx, (uint32_t)r,
+                           d_vals, keys, R, rec, (const W*)nullptr, (W*)nullptr);
+            SKY_LAUNCH_CHECK();
+        } else {
+            uint32_t* iota = c.buf[B_GIOTA].as<uint32_t>(r);
+            uint32_t* skey = c.buf[B_GSKEY].as<uint32_t>(r);
+            pdl_launch(k_rank_codes<D>, grid_for(r, kGB, c.num_sms * 8), kGB, 0, c.stream,
+                d_vals, R, (uint32_t)r, bounds, g.k0, g.k, code, cell, count, iota);
+            SKY_LAUNCH_CHECK();
+            cub::DoubleBuffer<uint32_t> kb(cell, skey), vb(iota, sidx);
+            const int end_bit = std::max(1, 32 - __builtin_clz(ncells));
+            size_t tmp = 0;
+            SKY_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kb, vb, (int64_t)r, 0, end_bit,
+                                                     c.stream));
+            void* t = c.buf[B_CUB].get(tmp);
+            SKY_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, kb, vb, (int64_t)r, 0, end_bit,
+                                                     c.stream));
+            if (vb.Current() != sidx)
+                SKY_CUDA(cudaMemcpyAsync(sidx, vb.Current(), sizeof(uint32_t) * r,
+                                         cudaMemcpyDeviceToDevice, c.stream));
+            pdl_launch(k_seg_bounds, grid_for((uint64_t)r + 1, kGB), kGB, 0, c.stream,
+                       (const uint32_t*)kb.Current(), (uint32_t)r, ncells, seg);
+            if (rec)
+                pdl_launch(k_gather_rec<D>, grid_for(r, kGB), kGB, 0, c.stream, sidx, (uint32_t)r,
+                           d_vals, keys, R, rec, (const W*)code, scode);
+            else
+                pdl_launch(k_gather_codes<W>, grid_for(r, kGB), kGB, 0, c.stream, sidx,
+                           (uint32_t)r, (const W*)code, scode);
+            SKY_LAUNCH_CHECK();
         }
-        SKY_LAUNCH_CHECK();
         pdl_launch(k_row_items, grid_for(g.rows, kGB), kGB, 0, c.stream, seg, g.rows, g.k0, items,
                    ctr,
                                                                  shard_rank, shard_world);

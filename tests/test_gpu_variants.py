@@ -38,7 +38,8 @@ def _run(env, *extra):
                                  {"SKYGPU_NO_DEV_ROUND": "1"}, {"SKYGPU_OVERLAP": "0"},
                                  {"SKYGPU_PREFIX": "1500", "SKYGPU_SOLO": "4",
                                   "SKYGPU_DIR_PER_CELL": "32"},
-                                 {"SKYGPU_IDS_LATE": "0"}, {"SKYGPU_GRID_ROW": "128",
+                                 {"SKYGPU_IDS_LATE": "0"}, {"SKYGPU_GRID_ATOMIC": "1"},
+                                 {"SKYGPU_GRID_ROW": "128",
                                                             "SKYGPU_GRID_K0": "16"}])
 def test_env_variant_matches_goldens(env):
     r = _run(env)
@@ -72,14 +73,14 @@ print(bad)
 
 @pytest.mark.parametrize("env", [{"SKYGPU_CELLS_BITSET": "1"}, {"SKYGPU_CELLS_SORT": "1"},
                                  {"SKYGPU_MG_NOCOL": "1"}, {"SKYGPU_MG_NOPRIV": "1"},
-                                 {"SKYGPU_MG_PAIRREG": "1"}])
+                                 {"SKYGPU_MG_PAIRSMEM": "1"}])
 def test_cell_engine_variants(env):
     """The HBM cell engine's alternatives against the pair engine's map:
     SKYGPU_CELLS_BITSET=1 the u32/u64 bitset-row form (the min-grid form is
     the default), SKYGPU_CELLS_SORT=1 the min-grid over a locality order (the
     top step's rows), SKYGPU_MG_NOCOL=1 the slab pass without the dim-3 running
     minimum (one more sweep), SKYGPU_MG_NOPRIV=1 every step marked in HBM (no
-    shared-memory privatised marks), SKYGPU_MG_PAIRREG=1 the register form of
+    shared-memory privatised marks), SKYGPU_MG_PAIRSMEM=1 the shared-memory staged form of
     the two-dim sweep."""
     e = dict(os.environ, SKYGPU_CELLS_SMEM="0", **env)
     out = subprocess.check_output([sys.executable, "-c", _BITSET, os.path.dirname(HERE)], env=e,
