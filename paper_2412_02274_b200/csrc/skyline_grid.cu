@@ -49,11 +49,32 @@ constexpr uint32_t kItem = 32 * kCand;
 template <int D>
 using GridWord = typename std::conditional<(D <= 4), uint32_t, unsigned long long>::type;
 
+// Rank codes need only be MONOTONE in the value (s dominates t => every code
+// of s <= t's; every pass is confirmed exactly), so they are read from a
+// table: the value rounded to float (monotone), its bucket among 1024 equal
+// buckets spanning the attribute's central sample quantiles (monotone), and
+// T[j][bucket] = the number of quantiles falling in buckets <= it
+// (non-decreasing) — one shared-memory byte instead of a 7-step binary
+// search over float64 bounds.
+constexpr int kRankBuckets = 1024;
+
+struct RankTable {
+    float lo[8], scale[8];
+    uint8_t t[8][kRankBuckets];
+};
+
+__device__ __forceinline__ int rank_bucket(double x, float lo, float scale) {
+    float u = __fmul_rn(__fsub_rn(__double2float_rn(x), lo), scale);
+    u = fminf(fmaxf(u, 0.0f), (float)(kRankBuckets - 1));
+    return (int)u;
+}
+
 // bounds[j][b] (b < 127) = the sample of rank 32(b+1)-1 among 4096 strided
-// samples of attribute j over R (one CTA per attribute)
+// samples of attribute j over R (one CTA per attribute), and attribute j's
+// code table
 __global__ void __launch_bounds__(1024)
 k_rank_bounds(const double* __restrict__ v, int d, const uint32_t* __restrict__ R, uint64_t r,
-              double* __restrict__ bounds) {
+              double* __restrict__ bounds, RankTable* __restrict__ tab) {
     pdl_wait();
     using Sort = cub::BlockRadixSort<unsigned long long, 1024, 4>;
     __shared__ typename Sort::TempStorage tmp;
@@ -73,19 +94,48 @@ k_rank_bounds(const double* __restrict__ v, int d, const uint32_t* __restrict__ 
         if ((rank + 1) % 32 == 0 && rank < 4095)
             bounds[j * 128 + (rank + 1) / 32 - 1] = __longlong_as_double((long long)items[u]);
     }
+    __shared__ float fb[kBounds];
+    __shared__ int bk[kBounds];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const uint32_t rank = threadIdx.x * 4 + u;
+        if ((rank + 1) % 32 == 0 && rank < 4095)
+            fb[(rank + 1) / 32 - 1] = __double2float_rn(__longlong_as_double((long long)items[u]));
+    }
+    __syncthreads();
+    const float lo = fb[0], hi = fb[kBounds - 1];
+    const float scale = hi > lo ? __fdiv_rn((float)kRankBuckets, __fsub_rn(hi, lo)) : 0.0f;
+    if (threadIdx.x < kBounds) bk[threadIdx.x] = rank_bucket((double)fb[threadIdx.x], lo, scale);
+    __syncthreads();
+    for (int b = threadIdx.x; b < kRankBuckets; b += blockDim.x) {
+        int n = 0;
+        for (int q = 0; q < kBounds; ++q) n += bk[q] <= b;
+        tab->t[j][b] = (uint8_t)n;
+    }
+    if (threadIdx.x == 0) {
+        tab->lo[j] = lo;
+        tab->scale[j] = scale;
+    }
 }
 
 // rank codes, cell of every tuple of R (bin0 + k0 * row), cell histogram
 template <int D>
 __global__ void __launch_bounds__(kGB)
 k_rank_codes(const double* __restrict__ v, const uint32_t* __restrict__ R, uint32_t r,
-             const double* __restrict__ bounds, int k0, int k, GridWord<D>* __restrict__ code,
+             const RankTable* __restrict__ tab, int k0, int k, GridWord<D>* __restrict__ code,
              uint32_t* __restrict__ cell, uint32_t* __restrict__ count,
              uint32_t* __restrict__ iota) {
     pdl_wait();
     using W = GridWord<D>;
-    __shared__ double sb[D * 128];
-    for (int i = threadIdx.x; i < D * 128; i += blockDim.x) sb[i] = bounds[i];
+    __shared__ uint8_t st[D][kRankBuckets];
+    __shared__ float slo[D], ssc[D];
+    for (int i = threadIdx.x; i < D * kRankBuckets / 4; i += blockDim.x)
+        reinterpret_cast<uint32_t*>(&st[0][0])[i] =
+            reinterpret_cast<const uint32_t*>(&tab->t[0][0])[i];
+    if (threadIdx.x < D) {
+        slo[threadIdx.x] = tab->lo[threadIdx.x];
+        ssc[threadIdx.x] = tab->scale[threadIdx.x];
+    }
     __syncthreads();
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < r; i += gridDim.x * blockDim.x) {
         const uint64_t p = R ? R[i] : i;
@@ -94,10 +144,7 @@ k_rank_codes(const double* __restrict__ v, const uint32_t* __restrict__ R, uint3
 #pragma unroll
         for (int j = 0; j < D; ++j) {
             const double x = v[p * D + j];
-            int lo = 0;  // #bounds <= x (bounds sorted)
-#pragma unroll
-            for (int step = 64; step; step >>= 1)
-                if (lo + step <= kBounds && sb[j * 128 + lo + step - 1] <= x) lo += step;
+            const int lo = st[j][rank_bucket(x, slo[j], ssc[j])];
             w |= (W)lo << (8 * j);
             if (j == 0) {
                 b0 = (uint32_t)((lo * k0) >> 7);
@@ -933,20 +980,21 @@ void sky_grid_decide(Ctx& c, const double* d_vals, int d, const unsigned long lo
         SKY_CUDA(cudaMemsetAsync(keep, 0, r, c.stream));
     if (!g.k0) throw Error(SKYGPU_ERUNTIME, "sky_grid_decide: unsupported shape (internal)");
     const uint32_t ncells = g.ncells;
-    double* bounds = c.buf[B_PROJ].as<double>(8 * 128);
+    double* bounds = c.buf[B_PROJ].as<double>(8 * 128 + (sizeof(RankTable) + 7) / 8);
+    RankTable* rtab = reinterpret_cast<RankTable*>(bounds + 8 * 128);
     const uint64_t cwords = 2 * ((uint64_t)ncells + 1) + 2;
     uint32_t* count = c.buf[B_GCNT].as<uint32_t>(cwords);
     uint32_t* seg = count + ncells + 1;
     unsigned* ctr = (unsigned*)(seg + ncells + 1);
     static const bool atomic_bucket = [] {  // see the bucketing below
-        const char* e = getenv("SKYGPU_GRID_ATOMIC");
-        return e && e[0] == '1';
+        const char* e = getenv("SKYGPU_GRID_SORT");
+        return !(e && e[0] == '1');
     }();
     if (atomic_bucket)
         SKY_CUDA(cudaMemsetAsync(count, 0, sizeof(uint32_t) * cwords, c.stream));
     else  // (seg is written whole by k_seg_bounds; only the item counters)
         SKY_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned) * 2, c.stream));
-    pdl_launch(k_rank_bounds, d, 1024, 0, c.stream, d_vals, d, R, r, bounds);
+    pdl_launch(k_rank_bounds, d, 1024, 0, c.stream, d_vals, d, R, r, bounds, rtab);
     SKY_LAUNCH_CHECK();
     note_launch(c);
     trace_mark(c, "grid: bounds");
@@ -961,8 +1009,9 @@ void sky_grid_decide(Ctx& c, const double* d_vals, int d, const unsigned long lo
         SKY_CUDA(cudaMemsetAsync(scode + r, 0x80, 16, c.stream));
         uint32_t* sidx = c.buf[B_GSIDX].as<uint32_t>(r);
         uint2* items = c.buf[B_GITEMS].as<uint2>(r / kItem + g.rows + 1);
-        // bucketing by cell: a stable radix sort of the cell ids (default),
-        // or a histogram + scan + atomic scatter (SKYGPU_GRID_ATOMIC=1)
+        // bucketing by cell: a histogram + scan + atomic scatter (default),
+        // or a stable radix sort of the cell ids (SKYGPU_GRID_SORT=1:
+        // deterministic order inside a cell, measured 0.15 ms slower on C5)
         // K6: the TMA-staged bitset kernel (default) or the per-lane ALU
         // kernel (SKYGPU_GRID_KERNEL=alu, kept for A/B measurement)
         static const bool alu = [] {
@@ -972,7 +1021,8 @@ void sky_grid_decide(Ctx& c, const double* d_vals, int d, const unsigned long lo
         double* rec = alu ? nullptr : c.buf[B_GREC].as<double>(r * (D + 1));
         if (atomic_bucket) {
             pdl_launch(k_rank_codes<D>, grid_for(r, kGB, c.num_sms * 8), kGB, 0, c.stream,
-                d_vals, R, (uint32_t)r, bounds, g.k0, g.k, code, cell, count, (uint32_t*)nullptr);
+                d_vals, R, (uint32_t)r, (const RankTable*)rtab, g.k0, g.k, code, cell, count,
+                (uint32_t*)nullptr);
             SKY_LAUNCH_CHECK();
             size_t tmp = 0;
             SKY_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, count, seg, (int)ncells + 1,
@@ -990,7 +1040,7 @@ void sky_grid_decide(Ctx& c, const double* d_vals, int d, const unsigned long lo
             uint32_t* iota = c.buf[B_GIOTA].as<uint32_t>(r);
             uint32_t* skey = c.buf[B_GSKEY].as<uint32_t>(r);
             pdl_launch(k_rank_codes<D>, grid_for(r, kGB, c.num_sms * 8), kGB, 0, c.stream,
-                d_vals, R, (uint32_t)r, bounds, g.k0, g.k, code, cell, count, iota);
+                d_vals, R, (uint32_t)r, (const RankTable*)rtab, g.k0, g.k, code, cell, count, iota);
             SKY_LAUNCH_CHECK();
             cub::DoubleBuffer<uint32_t> kb(cell, skey), vb(iota, sidx);
             const int end_bit = std::max(1, 32 - __builtin_clz(ncells));

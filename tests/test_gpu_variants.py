@@ -38,7 +38,7 @@ def _run(env, *extra):
                                  {"SKYGPU_NO_DEV_ROUND": "1"}, {"SKYGPU_OVERLAP": "0"},
                                  {"SKYGPU_PREFIX": "1500", "SKYGPU_SOLO": "4",
                                   "SKYGPU_DIR_PER_CELL": "32"},
-                                 {"SKYGPU_IDS_LATE": "0"}, {"SKYGPU_GRID_ATOMIC": "1"},
+                                 {"SKYGPU_IDS_LATE": "0"}, {"SKYGPU_GRID_SORT": "1"},
                                  {"SKYGPU_GRID_ROW": "128",
                                                             "SKYGPU_GRID_K0": "16"}])
 def test_env_variant_matches_goldens(env):
