@@ -410,14 +410,16 @@ def roofline(st, sky_ms, gres_ms, d, clk, workload="C2"):
             byts = st["gres_cells"]
             achieved = byts / (ms / 1e3) if ms > 0 else 0.0
             peak = HBM_PEAK_GBS * 1e9
-            kern = "k_cells_or_dim"
-            tr = kernel_traffic(workload, kern)
-            return {"bound": "hbm", "kernel": "cells engine (k_cells_*)", "achieved": achieved / 1e9,
-                    "peak": peak / 1e9, "unit": "GB/s", "frac": achieved / peak,
-                    "traffic": tr, "traffic_unit": "B/launch of k_cells_or_dim (ncu dram read+write)",
+            tr = kernel_traffic(workload, "cells_engine_per_call")
+            return {"bound": "hbm", "kernel": "min-grid cell engine (k_mg_*, k_cells_codes)",
+                    "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "GB/s",
+                    "frac": achieved / peak, "traffic": tr,
+                    "traffic_unit": "B/call, all cell-engine kernels (ncu dram read+write, profiles/r02_launches_C5_v2.md)",
                     "algorithmic_bytes_per_step": byts, "kernel_ms_per_step": ms,
                     "launches_per_step": st["gres_kernel_launches"],
-                    "bytes_model": "per step: grid zeroed + read + written once, S*d*8 B read twice"}
+                    "bytes_model": "codes: S*d*8 B read + S*8 B per scanned step written; per step: the "
+                                   "byte grid written once, read + written once by an ideal fused "
+                                   "prefix minimum (3 x grid bytes), the S code words read twice"}
         if kind == "skyline" and st["sky_engine"] == 16 and st.get("sky_units"):
             # rank-grid engine, TMA bitset decide kernel (skyline_grid.cu K6): one
             # unit = one staged comparator tested against a 128-candidate item =
