@@ -723,137 +723,6 @@ k_mg_slabcol(uint32_t* __restrict__ M, uint32_t ncols, uint32_t w0, uint32_t e1,
     }
 }
 
-// ---- bucketed marks (default where they apply: grid dims >= 4, <= 16384
-// slabs).  The marks of a step are sorted into their slabs (slab = the cell's
-// dims >= 3; a counting sort per step: per-block shared-memory histograms, a
-// per-slab prefix over blocks, a scatter through shared-memory cursors) and
-// the slab-column pass builds each slab in shared memory from its bucket —
-// no grid fill, no scattered global read-modify-writes, and the first sweep
-// pass writes the grid without reading it.
-constexpr int kBuckBlock = 1024;
-constexpr uint32_t kMaxSlabs = 16384;
-
-template <class CW>
-__device__ __forceinline__ uint32_t mg_slab_of(CW w, const MinGeom& geo, const uint32_t* sdiv) {
-    uint32_t sl = 0;
-    for (int k = 3; k < geo.nd; ++k) sl += ((uint32_t)(w >> (8 * geo.attr[k])) & 0xFFu) * sdiv[k];
-    return sl;
-}
-
-// sdiv[k] = stride[k] / stride[3] (slab units), passed by value
-struct SlabDiv {
-    uint32_t v[kMaxCellDims];
-};
-
-template <class CW>
-__global__ void __launch_bounds__(kBuckBlock)
-k_mg_bhist(const CW* __restrict__ code, uint64_t S, MinGeom geo, SlabDiv sd, uint32_t nslab,
-           uint32_t* __restrict__ cnt, const unsigned long long* live) {
-    pdl_wait();
-    if (step_dead(live)) return;
-    extern __shared__ uint32_t h[];  // [nslab]
-    for (uint32_t i = threadIdx.x; i < nslab; i += blockDim.x) h[i] = 0;
-    __syncthreads();
-    const uint64_t per = (S + gridDim.x - 1) / gridDim.x;
-    const uint64_t lo = blockIdx.x * per, hi = min(S, lo + per);
-    for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x)
-        atomicAdd(&h[mg_slab_of(code[i], geo, sd.v)], 1u);
-    __syncthreads();
-    for (uint32_t i = threadIdx.x; i < nslab; i += blockDim.x)
-        cnt[(uint64_t)blockIdx.x * nslab + i] = h[i];
-}
-
-// cnt[b][s] -> exclusive prefix over blocks b (in place); tot[s] = the sum
-__global__ void k_mg_bprefix(uint32_t* __restrict__ cnt, uint32_t nblk, uint32_t nslab,
-                             uint32_t* __restrict__ tot, const unsigned long long* live) {
-    pdl_wait();
-    if (step_dead(live)) return;
-    for (uint32_t sl = blockIdx.x * blockDim.x + threadIdx.x; sl < nslab;
-         sl += gridDim.x * blockDim.x) {
-        uint32_t run = 0;
-        for (uint32_t b = 0; b < nblk; ++b) {
-            const uint32_t x = cnt[(uint64_t)b * nslab + sl];
-            cnt[(uint64_t)b * nslab + sl] = run;
-            run += x;
-        }
-        tot[sl] = run;
-    }
-}
-
-template <class CW>
-__global__ void __launch_bounds__(kBuckBlock)
-k_mg_bscatter(const CW* __restrict__ code, uint64_t S, MinGeom geo, SlabDiv sd, uint32_t nslab,
-              const uint32_t* __restrict__ pre, const uint32_t* __restrict__ base,
-              CW* __restrict__ out, const unsigned long long* live) {
-    pdl_wait();
-    if (step_dead(live)) return;
-    extern __shared__ uint32_t cur[];  // [nslab]
-    for (uint32_t i = threadIdx.x; i < nslab; i += blockDim.x)
-        cur[i] = base[i] + pre[(uint64_t)blockIdx.x * nslab + i];
-    __syncthreads();
-    const uint64_t per = (S + gridDim.x - 1) / gridDim.x;
-    const uint64_t lo = blockIdx.x * per, hi = min(S, lo + per);
-    for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-        const CW w = code[i];
-        out[atomicAdd(&cur[mg_slab_of(w, geo, sd.v)], 1u)] = w;
-    }
-}
-
-// the slab-column pass with the marks applied in shared memory: slab s of
-// column col is built empty, its bucket's codes [base[s], base[s+1]) lower
-// their bytes (shared-memory CAS), then dims 0..2 are swept and the running
-// minimum along dim 3 carried as in k_mg_slabcol; the grid is only written
-template <class CW>
-__global__ void __launch_bounds__(kBlock)
-k_mg_slabcol_marked(uint32_t* __restrict__ M, uint32_t ncols, uint32_t w0, uint32_t e1,
-                    uint32_t e2, uint32_t e3, MinGeom geo, const CW* __restrict__ buck,
-                    const uint32_t* __restrict__ base, const unsigned long long* live) {
-    pdl_wait();
-    if (step_dead(live)) return;
-    extern __shared__ __align__(16) uint32_t sw[];
-    const uint32_t slab = w0 * e1 * e2;
-    uint32_t* run = sw + slab;
-    const uint32_t s1 = (uint32_t)geo.stride[1], s2 = (uint32_t)geo.stride[2];
-    const uint32_t a0 = geo.attr[0], a1 = geo.attr[1], a2 = geo.attr[2], am = (uint32_t)geo.m;
-    for (uint32_t col = blockIdx.x; col < ncols; col += gridDim.x) {
-        uint32_t* outb = M + (uint64_t)col * e3 * slab;
-        for (uint32_t c3 = 0; c3 < e3; ++c3) {
-            for (uint32_t i = threadIdx.x; i < slab; i += blockDim.x) sw[i] = kEmpty4;
-            __syncthreads();
-            const uint32_t sl = col * e3 + c3;
-            const uint32_t b0 = base[sl], b1 = base[sl + 1];
-            uint8_t* sb = reinterpret_cast<uint8_t*>(sw);
-            for (uint32_t q = b0 + threadIdx.x; q < b1; q += blockDim.x) {
-                const CW w = buck[q];
-                const uint32_t off = ((uint32_t)(w >> (8 * a0)) & 0xFFu) +
-                                     ((uint32_t)(w >> (8 * a1)) & 0xFFu) * s1 +
-                                     ((uint32_t)(w >> (8 * a2)) & 0xFFu) * s2;
-                const uint32_t v = 2u * ((uint32_t)(w >> (8 * am)) & 0xFFu) + 1u;
-                if (sb[off] <= v) continue;
-                uint32_t* word = sw + (off >> 2);
-                const uint32_t sh = 8u * (off & 3u);
-                uint32_t old = *word;
-                while (((old >> sh) & 0xFFu) > v) {
-                    const uint32_t nw = (old & ~(0xFFu << sh)) | (v << sh);
-                    const uint32_t prev = atomicCAS(word, old, nw);
-                    if (prev == old) break;
-                    old = prev;
-                }
-            }
-            __syncthreads();
-            slab_prefix<3>(sw, 1, w0, e1, e2);
-            uint32_t* o = outb + (uint64_t)c3 * slab;
-            for (uint32_t i = threadIdx.x; i < slab; i += blockDim.x) {
-                uint32_t x = sw[i];
-                if (c3) x = min7(x, run[i] & kPred4);
-                run[i] = x;
-                o[i] = x;
-            }
-            __syncthreads();
-        }
-    }
-}
-
 // two grid dims a, b = a + 1 at once (word stride sa of dim a), one thread
 // per u32 column of the (ea x eb) plane: P = min(v, P[x-1][y], P[x][y-1])
 template <int EA>
@@ -1084,8 +953,7 @@ static bool min_geometry(const std::vector<double>& amax, int d, int g, uint64_t
 // (k_mg_slabcol; dims 0..2 in a slab pass when there is no dim 3 or the slab
 // is too large), the rest two at a time in registers (k_mg_pair) or one at a
 // time (k_mg_dim) — 2 passes for d = 7
-static int min_sweeps(Ctx& c, uint8_t* M, const MinGeom& geo, const unsigned long long* live,
-                      bool first_done = false) {
+static int min_sweeps(Ctx& c, uint8_t* M, const MinGeom& geo, const unsigned long long* live) {
     constexpr size_t kSlabMax = 48 * 1024;
     static const bool nocol = [] {
         const char* e = getenv("SKYGPU_MG_NOCOL");
@@ -1124,10 +992,7 @@ static int min_sweeps(Ctx& c, uint8_t* M, const MinGeom& geo, const unsigned lon
     }
     const uint64_t nslabs = real_words / (slab / 4);
     int j = sd;
-    if (first_done) {  // (dims 0..3 done by the bucketed slab-column pass)
-        j = 4;
-        --nl;
-    } else if (!nocol && sd == 3 && geo.nd >= 4 && slab / 4 <= (uint64_t)kColPer * kBlock) {
+    if (!nocol && sd == 3 && geo.nd >= 4 && slab / 4 <= (uint64_t)kColPer * kBlock) {
         const uint32_t e3 = geo.ext[3];
         const uint64_t ncols = nslabs / e3;
         pdl_launch(k_mg_slabcol, grid_for(ncols, 1, c.num_sms * 8), kBlock, (size_t)2 * slab,
@@ -1454,23 +1319,6 @@ bool gres_cells_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_ma
             const char* e = getenv("SKYGPU_MG_NOPRIV");
             return e && e[0] == '1';
         }();
-        static const bool nobuck = [] {  // SKYGPU_MG_NOBUCKET=1: fill + global CAS marks
-            const char* e = getenv("SKYGPU_MG_NOBUCKET");
-            return e && e[0] == '1';
-        }();
-        static bool buck_attr = false;
-        if (!buck_attr) {
-            SKY_CUDA(cudaFuncSetAttribute(k_mg_slabcol_marked<uint32_t>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 48 * 1024));
-            SKY_CUDA(cudaFuncSetAttribute(k_mg_slabcol_marked<unsigned long long>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 48 * 1024));
-            for (auto f : {(const void*)k_mg_bhist<uint32_t>, (const void*)k_mg_bhist<unsigned long long>,
-                           (const void*)k_mg_bscatter<uint32_t>,
-                           (const void*)k_mg_bscatter<unsigned long long>})
-                SKY_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              (int)(kMaxSlabs * 4)));
-            buck_attr = true;
-        }
         uint32_t* stage = c.buf[B_MGSTAGE].as<uint32_t>((uint64_t)c.num_sms * 4 * kPrivCells / 4);
         static bool priv_attr = false;
         if (!priv_attr) {
@@ -1533,56 +1381,18 @@ bool gres_cells_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_ma
                 int nl = 0;
                 auto run = [&](auto* cg) {
                     using CW = std::remove_const_t<std::remove_pointer_t<decltype(cg)>>;
-                    // bucketed marks: dims >= 4, the dims-0..2 slab within
-                    // the slab-column kernel's limits, <= kMaxSlabs slabs
-                    const uint64_t slab_b = (uint64_t)geo.ext[0] * geo.ext[1] * geo.ext[2];
-                    const uint64_t real_b = geo.stride[geo.nd - 1] * geo.ext[geo.nd - 1];
-                    const uint64_t nslab = geo.nd >= 4 ? real_b / slab_b : 0;
-                    const bool buck = !priv && !nobuck && geo.nd >= 4 && slab_b <= 24 * 1024 &&
-                                      slab_b / 4 <= (uint64_t)kColPer * kBlock &&
-                                      nslab <= kMaxSlabs;
                     if (priv) {
                         pdl_launch(k_mg_mark_priv<CW>, nslots, kBlock, (size_t)geo.bytes * 4,
                                    c.stream, cg, S, geo, stage, n_in);
                         pdl_launch(k_mg_mark_reduce, grid_for(geo.bytes / 4, kBlock), kBlock, 0,
                                    c.stream, (const uint32_t*)stage, nslots,
                                    (uint32_t)(geo.bytes / 4), (uint32_t*)M, n_in);
-                        nl = min_sweeps(c, M, geo, n_in);
-                    } else if (buck) {
-                        SlabDiv sdv{};
-                        for (int k = 3; k < geo.nd; ++k)
-                            sdv.v[k] = (uint32_t)(geo.stride[k] / geo.stride[3]);
-                        const uint32_t ns = (uint32_t)nslab, nblk = (uint32_t)c.num_sms;
-                        uint32_t* bcnt = c.buf[B_MGCNT].as<uint32_t>((uint64_t)nblk * kMaxSlabs +
-                                                                     2 * (kMaxSlabs + 1));
-                        uint32_t* tot = bcnt + (uint64_t)nblk * kMaxSlabs;
-                        uint32_t* base = tot + kMaxSlabs + 1;
-                        CW* bk = c.buf[B_MGBUCK].as<CW>(S);
-                        pdl_launch(k_mg_bhist<CW>, nblk, kBuckBlock, (size_t)ns * 4, c.stream, cg,
-                                   S, geo, sdv, ns, bcnt, n_in);
-                        pdl_launch(k_mg_bprefix, grid_for(ns, kBlock), kBlock, 0, c.stream, bcnt,
-                                   nblk, ns, tot, n_in);
-                        size_t tmp = 0;
-                        SKY_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, tot, base, (int)ns + 1,
-                                                               c.stream));
-                        void* tb = c.buf[B_CUB].get(tmp);
-                        SKY_CUDA(cub::DeviceScan::ExclusiveSum(tb, tmp, tot, base, (int)ns + 1,
-                                                               c.stream));
-                        pdl_launch(k_mg_bscatter<CW>, nblk, kBuckBlock, (size_t)ns * 4, c.stream,
-                                   cg, S, geo, sdv, ns, (const uint32_t*)bcnt,
-                                   (const uint32_t*)base, bk, n_in);
-                        const uint32_t e3 = geo.ext[3];
-                        pdl_launch(k_mg_slabcol_marked<CW>, grid_for(ns / e3, 1, c.num_sms * 8),
-                                   kBlock, (size_t)2 * slab_b, c.stream, (uint32_t*)M, ns / e3,
-                                   geo.ext[0] / 4, geo.ext[1], geo.ext[2], e3, geo, (const CW*)bk,
-                                   (const uint32_t*)base, n_in);
-                        nl = 5 + min_sweeps(c, M, geo, n_in, true);
                     } else {
                         pdl_launch(k_mg_fill, grid_for(geo.bytes / 16, kBlock), kBlock, 0,
                                    c.stream, (uint4*)M, geo.bytes / 16, n_in);
                         pdl_launch(k_mg_mark<CW>, gs, kBlock, 0, c.stream, cg, S, geo, M, n_in);
-                        nl = min_sweeps(c, M, geo, n_in);
                     }
+                    nl = min_sweeps(c, M, geo, n_in);
                     pdl_launch(k_mg_query<CW>, gq, kBlock, 0, c.stream, cg, geo, (const uint8_t*)M,
                                in, na, n_in, d_den, perm, lists[cur], cnt[cur]);
                 };

@@ -101,7 +101,7 @@ enum BufId {
     B_DEN, B_GTMP0, B_GTMP1, B_OUTPOS, B_PROJ, B_REPS, B_MISC, B_CELLS, B_CSUM,
     B_ORDER, B_AMAX, B_AQ, B_PQ, B_GCODE, B_GCELL, B_GSCODE, B_GSIDX, B_GITEMS, B_GCNT,
     B_ACC0, B_ACC1, B_ACC2, B_ACC3, B_ACC4, B_ACC5, B_ACC6, B_ACC7, B_ACC8, B_ACC9, B_ACC10,
-    B_ACC11, B_ACC12, B_ACC13, B_ACC14, B_ACC15, B_ACC16, B_SEED, B_AMAX2, B_IOTA, B_NORM, B_CSV, B_CSVVAL, B_CHIST, B_CCUR, B_GREC, B_CACT0, B_CACT1, B_MGKEY0, B_MGKEY1, B_MGIDX0, B_MGIDX1, B_MGVALS, B_MGSTAGE, B_GIOTA, B_GSKEY, B_MGCNT, B_MGBUCK, B_COUNT
+    B_ACC11, B_ACC12, B_ACC13, B_ACC14, B_ACC15, B_ACC16, B_SEED, B_AMAX2, B_IOTA, B_NORM, B_CSV, B_CSVVAL, B_CHIST, B_CCUR, B_GREC, B_CACT0, B_CACT1, B_MGKEY0, B_MGKEY1, B_MGIDX0, B_MGIDX1, B_MGVALS, B_MGSTAGE, B_GIOTA, B_GSKEY, B_COUNT
 };
 
 // Device-side scalar slots (one small allocation, read back through pinned memory).

@@ -660,6 +660,7 @@ struct alignas(16) DecideSmem {
     uint64_t full[kStages], empty[kStages];
     uint32_t alive[4];
     uint32_t item;
+    uint8_t lo4[4][8], hi4[4][8];         // each warp's candidate code range per attribute
     uint2 hits[kTCons][kHitCap];          // a consumer warp's code passes, tested in parallel
 };
 
@@ -719,6 +720,10 @@ k_grid_decide_tma(const double* __restrict__ rec, const int64_t* __restrict__ id
                 for (uint32_t r = lo + 1; r <= hi; ++r) {
                     const unsigned b = __ballot_sync(0xffffffffu, valid && x >= r);
                     if ((r & 31u) == lane) T[r * 4] = b;
+                }
+                if (lane == 0) {
+                    sm.lo4[warp][j] = (uint8_t)lo;
+                    sm.hi4[warp][j] = (uint8_t)hi;
                 }
             }
             if (lane == 0) sm.alive[warp] = vmask;
@@ -827,6 +832,18 @@ k_grid_decide_tma(const double* __restrict__ rec, const int64_t* __restrict__ id
         } else {
             // ================= consumers: test staged comparators
             const uint32_t cw = warp - 1;
+            // the item's code range per attribute: a comparator code <= lo
+            // passes every candidate on that attribute (the entry would be
+            // all-ones: no table read), one above hi passes none (no read,
+            // the comparator is out) — only codes inside (lo, hi] are looked
+            // up.  Comparators from rows strictly below the item's in an
+            // attribute's coarse bin never need that attribute's table.
+            uint32_t ilo[D], ihi[D];
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                ilo[j] = min(min(sm.lo4[0][j], sm.lo4[1][j]), min(sm.lo4[2][j], sm.lo4[3][j]));
+                ihi[j] = max(max(sm.hi4[0][j], sm.hi4[1][j]), max(sm.hi4[2][j], sm.hi4[3][j]));
+            }
             for (;;) {
                 mbar_wait(&sm.full[cs], cphase);
                 const uint32_t n = sm.nslot[cs];
@@ -845,15 +862,23 @@ k_grid_decide_tma(const double* __restrict__ rec, const int64_t* __restrict__ id
                         uint4 m = make_uint4(0u, 0u, 0u, 0u);
                         if (s < n) {
                             const W c = sm.ring[cs][s];
-                            m = make_uint4(al[0], al[1], al[2], al[3]);
+                            bool out = false;
 #pragma unroll
-                            for (int j = 0; j < D; ++j) {
-                                const uint4 e =
-                                    sm.tab[j * kTabR + ((uint32_t)(c >> (8 * j)) & 0xFFu)];
-                                m.x &= e.x;
-                                m.y &= e.y;
-                                m.z &= e.z;
-                                m.w &= e.w;
+                            for (int j = 0; j < D; ++j)
+                                out |= ((uint32_t)(c >> (8 * j)) & 0xFFu) > ihi[j];
+                            if (!out) {
+                                m = make_uint4(al[0], al[1], al[2], al[3]);
+#pragma unroll
+                                for (int j = 0; j < D; ++j) {
+                                    const uint32_t cj = (uint32_t)(c >> (8 * j)) & 0xFFu;
+                                    if (cj > ilo[j]) {
+                                        const uint4 e = sm.tab[j * kTabR + cj];
+                                        m.x &= e.x;
+                                        m.y &= e.y;
+                                        m.z &= e.z;
+                                        m.w &= e.w;
+                                    }
+                                }
                             }
                         }
                         const bool hit = (m.x | m.y | m.z | m.w) != 0u;

@@ -73,7 +73,7 @@ print(bad)
 
 @pytest.mark.parametrize("env", [{"SKYGPU_CELLS_BITSET": "1"}, {"SKYGPU_CELLS_SORT": "1"},
                                  {"SKYGPU_MG_NOCOL": "1"}, {"SKYGPU_MG_NOPRIV": "1"},
-                                 {"SKYGPU_MG_PAIRSMEM": "1"}, {"SKYGPU_MG_NOBUCKET": "1"}])
+                                 {"SKYGPU_MG_PAIRSMEM": "1"}])
 def test_cell_engine_variants(env):
     """The HBM cell engine's alternatives against the pair engine's map:
     SKYGPU_CELLS_BITSET=1 the u32/u64 bitset-row form (the min-grid form is
@@ -81,8 +81,7 @@ def test_cell_engine_variants(env):
     top step's rows), SKYGPU_MG_NOCOL=1 the slab pass without the dim-3 running
     minimum (one more sweep), SKYGPU_MG_NOPRIV=1 every step marked in HBM (no
     shared-memory privatised marks), SKYGPU_MG_PAIRSMEM=1 the shared-memory staged form of
-    the two-dim sweep, SKYGPU_MG_NOBUCKET=1 grid fill + scattered CAS marks
-    instead of the per-step slab buckets."""
+    the two-dim sweep."""
     e = dict(os.environ, SKYGPU_CELLS_SMEM="0", **env)
     out = subprocess.check_output([sys.executable, "-c", _BITSET, os.path.dirname(HERE)], env=e,
                                   text=True, timeout=900)
