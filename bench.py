@@ -229,6 +229,8 @@ def our_arm(args):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     shard_rank, shard_world = (rank, world) if strong else (0, 1)
     sky_flag = {"auto": skypar.SKY_AUTO, "rounds": skypar.SKY_ROUNDS, "grid": skypar.SKY_GRID}[args.sky_engine]
+    if args.local_prune:  # the plan's partitions as local-skyline pruning before the merge
+        sky_flag |= skypar.SKY_PARTS
 
     if strong and world > 1:
         # the library's own NCCL group (unique id shipped over
@@ -330,7 +332,9 @@ def our_arm(args):
                    "parallelism": f"{'one instance sharded: rank-grid rows, cell-engine steps (or gres tuples), libskygpu NCCL MAX all-reduces' if strong else 'independent instance'}"
                                   f" per GPU x{world}",
                    "gres_engine": {0: "auto", 1: "pairs", 2: "cells"}[args.engine],
-                   "skyline_engine": {8: "prefix rounds", 16: "rank grid"}.get(stats[-1]["sky_engine"], "?")},
+                   "skyline_engine": {8: "prefix rounds", 16: "rank grid"}.get(stats[-1]["sky_engine"], "?")
+                                     + (" after local-skyline pruning per partition" if args.local_prune else ""),
+                   "tuples_into_final": stats[-1]["tuples_into_final"]},
         "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms,
                 # (the spread of the host-timed steps: host noise shows here)
                 "ms_min": min(e2e_times), "ms_median": sorted(e2e_times)[len(e2e_times) // 2],
@@ -517,6 +521,8 @@ def main():
     ap.add_argument("--strategy", default=None, choices=["none", "grid", "angular", "sliced"],
                     help="override the workload's partitioning plan (both arms)")
     ap.add_argument("--partitions", type=int, default=None, help="override the target partitions")
+    ap.add_argument("--local-prune", action="store_true",
+                    help="the plan's partitions as local-skyline pruning before the merge")
     ap.add_argument("--cpu-repeat", type=int, default=0, help="0: 1 for C5, else 3")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -9,10 +9,13 @@
  *
  *   skygpu_parallel_skyline    <- skypar::parallel_skyline   include/skypar/parallel.hpp:46-47
  *   skygpu_grid_resistance     <- skypar::grid_resistance    include/skypar/gres.hpp:73-75
+ *   skygpu_skyline_bnl         <- skypar::skyline_bnl        include/skypar/core.hpp:78
  *   skygpu_snap_relation       <- skypar::snap_relation      include/skypar/gres.hpp:28
  *                                 (and snap_to_grid, gres.hpp:26 = a 1-tuple relation)
  *   skygpu_max_grid_intervals  <- skypar::max_grid_intervals include/skypar/gres.hpp:35
  *   skygpu_make_plan           <- skypar::make_plan          include/skypar/partition.hpp:43
+ *   skygpu_assign_partitions   <- skypar::assign_partitions  include/skypar/partition.hpp:90
+ *                                 (partition.cpp:183-213)
  *   skygpu_pipeline            <- the composition run_experiment performs
  *                                 (proj/src/harness.cpp:208 then :229-231)
  *   skygpu_sfs_accounting      <- the DominanceCounter totals inside
@@ -76,6 +79,9 @@ extern "C" {
 #define SKYGPU_SKY_ROUNDS 8u    /* force the prefix-round skyline engine */
 #define SKYGPU_SKY_GRID 16u     /* force the one-pass rank-grid skyline engine (d <= 8) */
 #define SKYGPU_NORMALIZE 32u    /* min-max normalise on the device first (harness.cpp:161-177) */
+#define SKYGPU_SKY_PARTS 64u    /* the plan's partitions as local-skyline pruning before the
+                                   merge (parallel.cpp:59-73 recast; partition.cu): the tuples
+                                   dominated inside their own partition are dropped first */
 
 /* mirrors skypar::PartitionPlan (partition.hpp:27-32) */
 typedef struct skygpu_plan {
@@ -133,6 +139,20 @@ int skygpu_host_buffer(uint64_t bytes, int slot, void** out, char* err, size_t e
 int skygpu_make_plan(int strategy, long long target_partitions, int dims, skygpu_plan* out,
                      char* err, size_t errlen);
 
+/* partition.hpp:90 assign_partitions (partition.cpp:183-213) on the device:
+ * out_pid[i] = the partition of tuple i under `plan` — grid cells
+ * (grid_cell + cell_partition_id, :85-109), hyperspherical slices
+ * (assign_angular, :139-174), or equal-count slices of the (attribute 0, id)
+ * order (assign_sliced, :176-181); 0 for SKYGPU_NONE.  Grid and sliced ids
+ * are the reference's bit for bit; angular ids use the device atan2 and may
+ * differ from glibc's only where an angle lies within an ulp of a slice
+ * boundary.  Errors: the reference's grid_cell text for a Grid value outside
+ * [0,1]; EINVAL for a plan whose ids would exceed its partition count.
+ * ids may be NULL (position order).  Host pointers. */
+int skygpu_assign_partitions(const double* vals, const int64_t* ids, uint64_t n, int d,
+                             const skygpu_plan* plan, int64_t* out_pid, char* err,
+                             size_t errlen);
+
 /* parallel.hpp:46-47 parallel_skyline.
  * out_pos[0..*out_n) receives the INPUT POSITIONS of the skyline tuples in the
  * reference's output order ((sum, id) ascending); out_pos must hold n entries.
@@ -142,6 +162,18 @@ int skygpu_parallel_skyline(const double* vals, const int64_t* ids, uint64_t n, 
                             const int64_t* rep_ids, uint64_t n_reps, int cores,
                             uint64_t* out_pos, uint64_t* out_n, skygpu_stats* stats, char* err,
                             size_t errlen);
+
+/* core.hpp:78 skyline_bnl (core.cpp:25-46): the tuples of (vals, ids) that no
+ * tuple dominates — the brute-force skyline's set (it differs from
+ * parallel_skyline's only where a tuple is dominated by one of EQUAL float64
+ * sum and larger id).  out_pos[0..*out_n) = their
+ * input positions in (sum, id) order (BNL's own window order is an artefact of
+ * its sequential swap-remove; the reference's callers compare sets,
+ * test_util.hpp:22-36).  out_pos sized n; ids may be NULL (positions).
+ * Host pointers. */
+int skygpu_skyline_bnl(const double* vals, const int64_t* ids, uint64_t n, int d,
+                       uint64_t* out_pos, uint64_t* out_n, skygpu_stats* stats, char* err,
+                       size_t errlen);
 
 /* gres.hpp:73-75 grid_resistance over a skyline of s tuples.
  * out_den[i] = resistance denominator of input tuple i (1 or g in [2, g_max]);

@@ -58,6 +58,8 @@ def lib():
         L.so_gres_cells.argtypes = [dp, u64, i32, i32, dp]
         L.so_gres_cells_steps.argtypes = [dp, u64, i32, dp, i32, dp]
         L.so_make_plan.argtypes = [i32, i64, i32, dp, dp]
+        L.so_assign_partitions.argtypes = [dp, dp, u64, i32, i32, i32, i64, dp]
+        L.so_assign_partitions.restype = i64
         _lib = L
     return _lib
 
@@ -179,6 +181,19 @@ def make_plan(strategy: str, target: int, dims: int):
     if rc:
         raise ValueError("make_plan: invalid argument")
     return int(sl[0]), int(pa[0])
+
+
+def assign_partitions(vals: np.ndarray, ids, strategy: str, slices: int, parts: int) -> np.ndarray:
+    """partition.cpp:183-213 restated (so_assign_partitions)."""
+    v = np.ascontiguousarray(vals, dtype=np.float64)
+    n, d = v.shape
+    i = None if ids is None else np.ascontiguousarray(ids, dtype=np.int64)
+    out = np.zeros(max(n, 1), dtype=np.int64)
+    rc = lib().so_assign_partitions(_p(v), None if i is None else _p(i), n, d,
+                                    STRATEGIES[strategy], slices, parts, _p(out))
+    if rc:
+        raise ValueError(f"grid_cell: value outside [0,1] at flat index {rc - 1}")
+    return out[:n]
 
 
 def refdrive_path(release: bool = True) -> str | None:

@@ -9,6 +9,8 @@
 //            print the results as one JSON object (sorted skyline ids, the
 //            skyline in output order, g_max, the denominators map, per-g rows).
 //   dump   : write the generated input as raw float64 (generator parity).
+//   pids   : the reference's assign_partitions on the generated input (golden
+//            partition ids for the device assign_partitions).
 //   csv    : parse --input with the reference's load_dataset_csv
 //            (harness.cpp:93-134) and print the relation (value bits in hex,
 //            ids) or the exception text — golden vectors for the device CSV
@@ -242,6 +244,26 @@ int run_golden(const Args& a) {
     return 0;
 }
 
+// pids: the reference's own assign_partitions (partition.cpp:183-213) on the
+// generated input — golden partition ids for the device assign_partitions
+int run_pids(const Args& a) {
+    Relation data = load_input(a);
+    PartitionPlan plan = make_plan(strategy_from_name(a.strategy), a.p, a.d);
+    std::printf("{\"n\":%zu,\"d\":%d,\"gen\":\"%s\",\"seed\":%llu,\"strategy\":\"%s\","
+                "\"p\":%lld,\"slices\":%d,\"partitions\":%lld,",
+                data.size(), a.d, a.input.empty() ? a.gen.c_str() : "file",
+                (unsigned long long)a.seed, a.strategy.c_str(), a.p, plan.slices, plan.partitions);
+    try {
+        const std::vector<long long> ids = assign_partitions(data, plan);
+        std::printf("\"pids\":[");
+        for (std::size_t i = 0; i < ids.size(); ++i) std::printf(i ? ",%lld" : "%lld", ids[i]);
+        std::printf("]}\n");
+    } catch (const std::exception& e) {
+        std::printf("\"pids_error\":\"%s\"}\n", e.what());
+    }
+    return 0;
+}
+
 int run_dump(const Args& a) {
     Relation data = load_input(a);
     std::ofstream out(a.out, std::ios::binary);
@@ -346,6 +368,7 @@ int main(int argc, char** argv) {
         if (a.mode == "golden") return run_golden(a);
         if (a.mode == "bench") return run_bench(a);
         if (a.mode == "dump") return run_dump(a);
+        if (a.mode == "pids") return run_pids(a);
         if (a.mode == "csv") return run_csv(a);
         throw std::runtime_error("unknown --mode " + a.mode);
     } catch (const std::exception& e) {

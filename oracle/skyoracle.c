@@ -458,3 +458,76 @@ int so_make_plan(int strategy, long long target, int dims, int* slices, long lon
     if (*parts > SO_MAX_PARTS) return -1;
     return 0;
 }
+
+/* ------------------------------------------------- assign_partitions --- */
+/* partition.cpp:183-213 with grid_cell + cell_partition_id (:85-109),
+ * to_hyperspherical + assign_angular (:139-174) and assign_sliced
+ * (:176-181; order by (attribute 0, id)).  Returns 0, or 1 + the first flat
+ * index of a Grid value outside [0,1] (grid_cell's throw, :91-94). */
+static const double* g_sl_v;
+static const int64_t* g_sl_ids;
+static int g_sl_d;
+static int cmp_sliced(const void* a, const void* b) {
+    const uint64_t x = *(const uint64_t*)a, y = *(const uint64_t*)b;
+    const double va = g_sl_v[x * g_sl_d], vb = g_sl_v[y * g_sl_d];
+    if (va != vb) return va < vb ? -1 : 1;
+    const int64_t ia = g_sl_ids ? g_sl_ids[x] : (int64_t)x, ib = g_sl_ids ? g_sl_ids[y] : (int64_t)y;
+    return ia < ib ? -1 : (ia > ib ? 1 : 0);
+}
+
+long long so_assign_partitions(const double* v, const int64_t* ids, uint64_t n, int d,
+                               int strategy, int slices, long long parts, int64_t* out) {
+    const double kPi = 3.14159265358979323846; /* partition.cpp:13 */
+    if (strategy == 0) {
+        for (uint64_t i = 0; i < n; ++i) out[i] = 0;
+        return 0;
+    }
+    if (strategy == 1) {
+        for (uint64_t i = 0; i < n; ++i) {
+            long long id = 0, w = 1;
+            for (int j = 0; j < d; ++j) {
+                const double x = v[i * d + j];
+                if (x < 0.0 || x > 1.0) return 1 + (long long)(i * d + j);
+                int idx = (int)(x * slices);
+                if (idx >= slices) idx = slices - 1;
+                id += (long long)idx * w;
+                w *= slices;
+            }
+            out[i] = id;
+        }
+        return 0;
+    }
+    if (strategy == 2) {
+        double tail[65];
+        for (uint64_t i = 0; i < n; ++i) {
+            const double* t = v + i * d;
+            int all_zero = 1;
+            for (int j = 0; j < d; ++j)
+                if (t[j] != 0.0) { all_zero = 0; break; }
+            if (all_zero) { out[i] = 0; continue; }
+            tail[d] = 0.0;
+            for (int j = d - 1; j >= 0; --j) tail[j] = tail[j + 1] + t[j] * t[j];
+            long long id = 0, w = 1;
+            for (int j = 0; j + 1 < d; ++j) {
+                const double ang = atan2(sqrt(tail[j + 1]), t[j]);
+                int idx = (int)((2.0 * ang / kPi) * slices);
+                if (idx >= slices) idx = slices - 1;
+                id += (long long)idx * w;
+                w *= slices;
+            }
+            out[i] = id;
+        }
+        return 0;
+    }
+    /* sliced */
+    uint64_t* order = (uint64_t*)malloc((n ? n : 1) * sizeof(uint64_t));
+    if (!order) return -1;
+    for (uint64_t i = 0; i < n; ++i) order[i] = i;
+    g_sl_v = v;
+    g_sl_ids = ids;
+    g_sl_d = d;
+    qsort(order, n, sizeof(uint64_t), cmp_sliced);
+    for (uint64_t r = 0; r < n; ++r) out[order[r]] = (long long)r * parts / (long long)n;
+    free(order);
+    return 0;
+}

@@ -26,6 +26,7 @@ NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompile
                      "-Xcompiler", "-ffp-contract=off", "-ccbin", HOST_CXX, "-I", INCLUDE,
                      "-I", CSRC, "--expt-relaxed-constexpr"]
 CU_SOURCES = ["skyline.cu", "skyline_grid.cu", "gres.cu", "cells.cu", "accounting.cu", "ingest.cu", "csv.cu",
+              "partition.cu",
               "abi.cu"]
 CXX_SOURCES = ["hostgen.cpp"]
 

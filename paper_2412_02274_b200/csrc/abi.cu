@@ -186,6 +186,23 @@ void validate_plan(const skygpu_plan* plan, int d) {
     (void)d;
 }
 
+// local-skyline pruning for one call: the pipeline flag SKYGPU_SKY_PARTS, or
+// SKYGPU_LOCAL_PRUNE=1 for every call of the process (the C++ drop-in's
+// parallel_skyline has no flags)
+bool local_prune_env() {
+    static const bool on = [] {
+        const char* e = getenv("SKYGPU_LOCAL_PRUNE");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
+struct LocalPruneScope {
+    Ctx& c;
+    LocalPruneScope(Ctx& cx, bool on) : c(cx) { c.local_prune = on || local_prune_env(); }
+    ~LocalPruneScope() { c.local_prune = false; }
+};
+
 template <class F>
 int guarded(char* err, size_t errlen, F&& f) {
     try {
@@ -308,6 +325,32 @@ namespace {
 __global__ void k_clear_slot(unsigned long long* slots, int i) {
     pdl_wait();
     slots[i] = 0;
+}
+
+// skyline_bnl's set (core.cpp:25-46) from the SFS engine's result K (in (sum,
+// id) order): BNL keeps exactly the tuples no tuple dominates, SFS those no
+// PREDECESSOR dominates.  They differ only for t in K dominated by a later
+// tuple of EQUAL float64 sum — and then by one inside K (the dominance-maximal
+// such tuple has no dominator of smaller or equal sum), which sits right
+// behind t in K's order.  keep[j] = 0 for those.
+__global__ void k_bnl_refine(const double* __restrict__ v, int d, const uint32_t* __restrict__ K,
+                             uint64_t S, uint8_t* __restrict__ keep) {
+    pdl_wait();
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < S;
+         j += (uint64_t)gridDim.x * blockDim.x) {
+        const double* t = v + (uint64_t)K[j] * d;
+        double st = 0.0;
+        for (int k = 0; k < d; ++k) st = __dadd_rn(st, t[k]);
+        bool dominated = false;
+        for (uint64_t q = j + 1; q < S && !dominated; ++q) {
+            const double* w = v + (uint64_t)K[q] * d;
+            double sw = 0.0;
+            for (int k = 0; k < d; ++k) sw = __dadd_rn(sw, w[k]);
+            if (!(sw == st)) break;  // sums ascend along K: the equal-sum run ended
+            dominated = dom_f64_dyn(w, t, d);
+        }
+        keep[j] = !dominated;
+    }
 }
 
 __global__ void k_widen(const uint32_t* __restrict__ a, uint64_t* __restrict__ b, uint64_t n) {
@@ -522,6 +565,53 @@ int skygpu_make_plan(int strategy, long long target, int dims, skygpu_plan* out,
     });
 }
 
+int skygpu_assign_partitions(const double* vals, const int64_t* ids, uint64_t n, int d,
+                             const skygpu_plan* plan, int64_t* out_pid, char* err,
+                             size_t errlen) {
+    return guarded(err, errlen, [&] {
+        if (!plan) invalid("assign_partitions: plan is required");
+        if (d < 1 || d > kMaxDims) invalid("assign_partitions: dims must be in [1, 32]");
+        validate_plan(plan, d);
+        const skygpu_plan pl = *plan;
+        if ((pl.strategy == SKYGPU_GRID || pl.strategy == SKYGPU_ANGULAR) && pl.slices < 1)
+            invalid(pl.strategy == SKYGPU_GRID ? "grid_cell: slices must be >= 1"
+                                               : "assign_angular: slices must be >= 1");
+        if (!plan_ids_in_range(pl, d) || pl.partitions > (1LL << 30))
+            invalid("assign_partitions: plan inconsistent with dims (partition ids would exceed "
+                    "the plan's partition count)");
+        if (n == 0) return;
+        if (n >= 0xFFFFFFFFull) invalid("assign_partitions: more than 2^32-1 tuples");
+        bool sorted = true;
+        for (uint64_t i = 0; ids && i + 1 < n && sorted; ++i) sorted = ids[i] < ids[i + 1];
+        Ctx& c = ctx();
+        double* dv = c.buf[B_IN_VALS].as<double>(n * d);
+        int64_t* di = c.buf[B_IN_IDS].as<int64_t>(n);
+        int32_t* pid = c.buf[B_PPID].as<int32_t>(n);
+        SKY_CUDA(cudaMemcpyAsync(dv, vals, n * d * sizeof(double), cudaMemcpyHostToDevice,
+                                 c.stream));
+        if (ids)
+            SKY_CUDA(cudaMemcpyAsync(di, ids, n * sizeof(int64_t), cudaMemcpyHostToDevice,
+                                     c.stream));
+        if (pl.strategy == SKYGPU_ANGULAR && d < 2) {
+            // to_hyperspherical throws for the first tuple that is not the origin
+            for (uint64_t i = 0; i < n; ++i)
+                if (vals[i] != 0.0) invalid("to_hyperspherical: needs at least 2 dimensions");
+        }
+        zero_slots(c);
+        assign_partitions_device(c, dv, ids ? di : nullptr, sorted, n, d, pl, pid);
+        std::vector<int32_t> h(n);
+        SKY_CUDA(cudaMemcpyAsync(h.data(), pid, n * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                                 c.stream));
+        read_slots(c, S_GRIDBAD, 1);
+        if (pl.strategy == SKYGPU_GRID && c.h_slots[S_GRIDBAD] != ~0ULL) {
+            const uint64_t flat = c.h_slots[S_GRIDBAD];
+            invalid("grid_cell: value " + std::to_string(vals[flat]) + " in attribute " +
+                    std::to_string(flat % d + 1) + " outside [0,1]; normalize the data first");
+        }
+        for (uint64_t i = 0; i < n; ++i) out_pid[i] = h[i];
+    });
+}
+
 int skygpu_parallel_skyline(const double* vals, const int64_t* ids, uint64_t n, int d,
                             const skygpu_plan* plan, const double* rep_vals,
                             const int64_t* rep_ids, uint64_t n_reps, int cores,
@@ -552,6 +642,7 @@ int skygpu_parallel_skyline(const double* vals, const int64_t* ids, uint64_t n, 
             SKY_CUDA(cudaMemcpyAsync(dr, rep_vals, n_reps * d * sizeof(double),
                                      cudaMemcpyHostToDevice, c.stream));
         }
+        LocalPruneScope lps(c, false);
         SkylineOut so = skyline_device(c, dv, di, n, d, pl, dr, n_reps);
         if (so.S)
             SKY_CUDA(cudaMemcpyAsync(out_pos, so.d_pos64, so.S * sizeof(uint64_t),
@@ -559,6 +650,56 @@ int skygpu_parallel_skyline(const double* vals, const int64_t* ids, uint64_t n, 
         all.stop(&c.st->ms_total);
         end_stats(c);  // final synchronisation
         *out_n = so.S;
+    });
+}
+
+int skygpu_skyline_bnl(const double* vals, const int64_t* ids, uint64_t n, int d,
+                       uint64_t* out_pos, uint64_t* out_n, skygpu_stats* stats, char* err,
+                       size_t errlen) {
+    return guarded(err, errlen, [&] {
+        if (d < 1 || d > kMaxDims) invalid("skyline_bnl: dims must be in [1, 32]");
+        Ctx& c = ctx();
+        begin_stats(c, stats);
+        *out_n = 0;
+        if (n == 0) {
+            end_stats(c);
+            return;
+        }
+        Timer all(c, 0);
+        double* dv = c.buf[B_IN_VALS].as<double>(n * d);
+        int64_t* di = c.buf[B_IN_IDS].as<int64_t>(n);
+        SKY_CUDA(cudaMemcpyAsync(dv, vals, n * d * sizeof(double), cudaMemcpyHostToDevice,
+                                 c.stream));
+        if (ids) {
+            SKY_CUDA(cudaMemcpyAsync(di, ids, n * sizeof(int64_t), cudaMemcpyHostToDevice,
+                                     c.stream));
+        } else {
+            pdl_launch(k_iota64, grid_for(n, 256), 256, 0, c.stream, di, n);
+            SKY_LAUNCH_CHECK();
+            note_launch(c);
+        }
+        const skygpu_plan none{SKYGPU_NONE, 1, 1, d};
+        LocalPruneScope lps(c, false);
+        SkylineOut so = skyline_device(c, dv, di, n, d, none, nullptr, 0);
+        std::vector<uint64_t> pos(so.S);
+        std::vector<uint8_t> keep(so.S);
+        if (so.S) {
+            uint8_t* dk = c.buf[B_PFLAGS].as<uint8_t>(so.S);
+            pdl_launch(k_bnl_refine, grid_for(so.S, 256), 256, 0, c.stream, (const double*)dv, d,
+                       (const uint32_t*)so.d_inpos, so.S, dk);
+            SKY_LAUNCH_CHECK();
+            note_launch(c);
+            SKY_CUDA(cudaMemcpyAsync(pos.data(), so.d_pos64, so.S * sizeof(uint64_t),
+                                     cudaMemcpyDeviceToHost, c.stream));
+            SKY_CUDA(cudaMemcpyAsync(keep.data(), dk, so.S, cudaMemcpyDeviceToHost, c.stream));
+        }
+        all.stop(&c.st->ms_total);
+        end_stats(c);  // final synchronisation
+        uint64_t m = 0;
+        for (uint64_t j = 0; j < so.S; ++j)
+            if (keep[j]) out_pos[m++] = pos[j];
+        *out_n = m;
+        c.st->skyline_size = m;
     });
 }
 
@@ -697,7 +838,9 @@ int skygpu_pipeline(const double* vals, const int64_t* ids, uint64_t n, int d,
         }();
         const bool streamed = !dev_in && overlap_env && !(flags & SKYGPU_NORMALIZE) &&
                               n * (uint64_t)(d + 1) * 8 >= stream_min &&
-                              d <= 8 && pl.strategy != SKYGPU_GRID && !(flags & SKYGPU_SKY_GRID);
+                              d <= 8 && pl.strategy != SKYGPU_GRID && !(flags & SKYGPU_SKY_GRID) &&
+                              !(flags & SKYGPU_SKY_PARTS) && !local_prune_env();
+        LocalPruneScope lps(c, (flags & SKYGPU_SKY_PARTS) != 0);
         // host ids travel behind the values and are only waited for at the
         // end of the skyline (speculating they are strictly increasing, the
         // usual row-order ids; otherwise the call re-runs once they are in)

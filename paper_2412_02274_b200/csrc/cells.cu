@@ -521,7 +521,7 @@ __global__ void k_mg_fill(uint4* __restrict__ p, uint64_t n16, const unsigned lo
 // every skyline tuple lowers its cell's byte to 2 c_m + 1 ("attained in
 // this cell"): one CAS, optimistic about a fresh (empty) word, retried with
 // the bytewise minimum when the word already holds marks
-template <class CW>
+template <class CW, bool LOADFIRST>
 __global__ void __launch_bounds__(kBlock)
 k_mg_mark(const CW* __restrict__ code, uint64_t S, MinGeom geo, uint8_t* __restrict__ M,
           const unsigned long long* live) {
@@ -535,7 +535,15 @@ k_mg_mark(const CW* __restrict__ code, uint64_t S, MinGeom geo, uint8_t* __restr
         const uint32_t sh = 8u * (uint32_t)(r & 3u);
         const uint32_t mine = (kEmpty4 & ~(0xFFu << sh)) | ((2u * c0 + 1u) << sh);
         uint32_t* word = reinterpret_cast<uint32_t*>(M) + (r >> 2);
-        uint32_t old = atomicCAS(word, kEmpty4, mine);
+        uint32_t old = kEmpty4;
+        if (LOADFIRST) {
+            // most tuples do not lower their cell (a cell's minimum changes
+            // ~ln k times over its k tuples): one L2 load settles them
+            old = __ldcg(word);
+            if (old == kEmpty4) old = atomicCAS(word, kEmpty4, mine);
+        } else {
+            old = atomicCAS(word, kEmpty4, mine);
+        }
         while (old != kEmpty4) {
             const uint32_t nw = min7(old, mine);
             if (nw == old) break;
@@ -1390,7 +1398,16 @@ bool gres_cells_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_ma
                     } else {
                         pdl_launch(k_mg_fill, grid_for(geo.bytes / 16, kBlock), kBlock, 0,
                                    c.stream, (uint4*)M, geo.bytes / 16, n_in);
-                        pdl_launch(k_mg_mark<CW>, gs, kBlock, 0, c.stream, cg, S, geo, M, n_in);
+                        static const bool load_first = [] {  // SKYGPU_MG_LOADFIRST=0: CAS first
+                            const char* e = getenv("SKYGPU_MG_LOADFIRST");
+                            return !(e && e[0] == '0');
+                        }();
+                        if (load_first)
+                            pdl_launch(k_mg_mark<CW, true>, gs, kBlock, 0, c.stream, cg, S, geo, M,
+                                       n_in);
+                        else
+                            pdl_launch(k_mg_mark<CW, false>, gs, kBlock, 0, c.stream, cg, S, geo, M,
+                                       n_in);
                     }
                     nl = min_sweeps(c, M, geo, n_in);
                     pdl_launch(k_mg_query<CW>, gq, kBlock, 0, c.stream, cg, geo, (const uint8_t*)M,

@@ -101,7 +101,9 @@ enum BufId {
     B_DEN, B_GTMP0, B_GTMP1, B_OUTPOS, B_PROJ, B_REPS, B_MISC, B_CELLS, B_CSUM,
     B_ORDER, B_AMAX, B_AQ, B_PQ, B_GCODE, B_GCELL, B_GSCODE, B_GSIDX, B_GITEMS, B_GCNT,
     B_ACC0, B_ACC1, B_ACC2, B_ACC3, B_ACC4, B_ACC5, B_ACC6, B_ACC7, B_ACC8, B_ACC9, B_ACC10,
-    B_ACC11, B_ACC12, B_ACC13, B_ACC14, B_ACC15, B_ACC16, B_SEED, B_AMAX2, B_IOTA, B_NORM, B_CSV, B_CSVVAL, B_CHIST, B_CCUR, B_GREC, B_CACT0, B_CACT1, B_MGKEY0, B_MGKEY1, B_MGIDX0, B_MGIDX1, B_MGVALS, B_MGSTAGE, B_GIOTA, B_GSKEY, B_COUNT
+    B_ACC11, B_ACC12, B_ACC13, B_ACC14, B_ACC15, B_ACC16, B_SEED, B_AMAX2, B_IOTA, B_NORM, B_CSV, B_CSVVAL, B_CHIST, B_CCUR, B_GREC, B_CACT0, B_CACT1, B_MGKEY0, B_MGKEY1, B_MGIDX0, B_MGIDX1, B_MGVALS, B_MGSTAGE, B_GIOTA, B_GSKEY,
+    B_PPID, B_PHIST, B_PTHR, B_PWPOS, B_PWV, B_PWKEY, B_PWTIE, B_PSK0, B_PSK1, B_PSV0, B_PSV1,
+    B_PFLAGS, B_COUNT
 };
 
 // Device-side scalar slots (one small allocation, read back through pinned memory).
@@ -185,6 +187,9 @@ struct Ctx {
     const int64_t* ids_host = nullptr;
     int64_t* ids_dev = nullptr;
     uint64_t ids_n = 0;
+    // SKYGPU_SKY_PARTS: local-skyline pruning per plan partition before the
+    // merge (partition.cu), set for the duration of one call
+    bool local_prune = false;
 };
 
 // record a labelled device timestamp when tracing is on
@@ -373,6 +378,22 @@ uint64_t select_representatives_device(Ctx& c, const double* d_vals, const int64
 int csv_parse_device(Ctx& c, const char* d_bytes, uint64_t len, int dims, uint64_t* rows,
                      double* d_vals, uint64_t vals_cap, uint64_t* err_line, int* err_col,
                      int* err_kind, int* internal);
+
+// partition.cu: assign_partitions (partition.cpp:183-213) on the device —
+// d_pid[i] = partition of tuple i in [0, plan.partitions); Grid values outside
+// [0,1] set slot S_GRIDBAD (first flat index).  ids_sorted: ids strictly
+// increasing in position order (sliced ties then follow positions).
+void assign_partitions_device(Ctx& c, const double* d_vals, const int64_t* d_ids, bool ids_sorted,
+                              uint64_t n, int d, const skygpu_plan& plan, int32_t* d_pid);
+// local-skyline pruning (partition.cu header): keep[i] = 0 for tuples dominated
+// by a preceding member of their partition's window skyline (and for tuples
+// outside `mask` when given); keys = K1's sum keys, tie_ids = ids or nullptr
+// (ties by position)
+bool local_prune_applies(const skygpu_plan& plan, int d);
+bool plan_ids_in_range(const skygpu_plan& plan, int d);
+uint64_t local_prune_device(Ctx& c, const double* d_vals, const unsigned long long* keys,
+                            const int64_t* tie_ids, uint64_t n, int d, const skygpu_plan& plan,
+                            const uint8_t* mask, uint8_t* keep, uint32_t* stats_parts);
 
 // float64 AoS -> SoA transpose on the device
 void aos_to_soa(Ctx& c, const double* d_aos, uint64_t n, int d, double* d_soa);

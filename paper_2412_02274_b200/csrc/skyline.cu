@@ -1611,8 +1611,11 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
     }();
     // the first round's threshold sampled from the values and its prefix
     // appended by K1 itself (no separate selection pass) — plain rounds only
+    // local-skyline pruning per plan partition before the merge (partition.cu)
+    const bool lprune = c.local_prune && local_prune_applies(plan, d) && n > 1 &&
+                        !(sky_engine & (kSkyAbortIfLarge | kSkyFirstPrefix));
     bool fused_first = !feed && sky_engine == 0 && !(plan.strategy == SKYGPU_GRID) &&
-                       n_reps == 0 && qpre && n > kCTACap && fused_sel_on;
+                       n_reps == 0 && qpre && n > kCTACap && fused_sel_on && !lprune;
     if (fused_first) {
         pdl_launch(k_sample_threshold, 1, 1024, 0, c.stream, (const unsigned long long*)nullptr,
                    (const uint32_t*)nullptr, n, kWant, c.d_slots, d_vals, d);
@@ -1651,7 +1654,8 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
         for (int k = 0; k < d && grid_cells <= (1u << 22); ++k) grid_cells *= (uint64_t)plan.slices;
         if (grid_cells > (1u << 22)) grid_cells = 0;  // too fine to tabulate: skip pruning
     }
-    if (grid_cells || n_reps > 0) {
+    uint64_t into_final = ~0ULL;  // survivors of the local pruning (the merge's input)
+    if (grid_cells || n_reps > 0 || lprune) {
         uint8_t* pre = c.buf[B_FLAGS].as<uint8_t>(n);
         if (grid_cells) {
             const int m = plan.slices;
@@ -1680,12 +1684,27 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
             SKY_LAUNCH_CHECK();
             note_launch(c);
         }
+        uint64_t into_parallel = 0;
+        if (lprune) {
+            if (grid_cells || n_reps > 0) {  // the tuples entering the partitions
+                select_flags<uint32_t>(c, nullptr, n, pre, Rbuf1, c.d_slots + S_C2);
+            }
+            uint8_t* lk = c.buf[B_PFLAGS].as<uint8_t>(n);
+            local_prune_device(c, d_vals, keys, tie_ids, n, d, plan,
+                               (grid_cells || n_reps > 0) ? pre : nullptr, lk, nullptr);
+            pre = lk;
+            trace_mark(c, "sky: local pruning");
+        }
         select_flags<uint32_t>(c, nullptr, n, pre, Rbuf0, c.d_slots + S_C3);
         read_slots(c, S_BAD, 11);  // S_BAD .. S_C3 (checks + survivors)
         R = Rbuf0;
         r = c.h_slots[S_C3];
+        into_parallel = lprune ? ((grid_cells || n_reps > 0) ? c.h_slots[S_C2] : n) : r;
+        if (lprune) into_final = r;
+        st.tuples_into_parallel = into_parallel;
+    } else {
+        st.tuples_into_parallel = r;
     }
-    st.tuples_into_parallel = r;
 
     uint64_t kc = 0;
     static const uint64_t kSeedWant = [] {  // the streamed head's seed prefix
@@ -2306,7 +2325,7 @@ SkylineOut skyline_device(Ctx& c, const double* d_vals, const int64_t* d_ids, ui
     }
     st.sfs_rounds = rounds;
     st.sky_engine = grid_used ? SKYGPU_SKY_GRID : SKYGPU_SKY_ROUNDS;
-    st.tuples_into_final = kc;
+    st.tuples_into_final = into_final != ~0ULL ? into_final : kc;
     st.ms_sky_kernel += kernel_ms;
     st.sky_kernel_launches += kernel_launches;
 

@@ -34,6 +34,7 @@ GRES_AUTO, GRES_PAIRS, GRES_CELLS = 0, 1, 2
 DEVICE_PTRS, CHECK_SKYLINE, SKIP_GRES = 1, 2, 4
 SKY_AUTO, SKY_ROUNDS, SKY_GRID = 0, 8, 16  # skyline engine flags
 NORMALIZE = 32  # pipeline flag: min-max normalise on the device first
+SKY_PARTS = 64  # pipeline flag: the plan's partitions as local-skyline pruning before the merge
 
 
 class SkyGpuError(RuntimeError):
@@ -102,6 +103,8 @@ def lib() -> C.CDLL:
         L.skygpu_set_device.argtypes = [i32, cp, sz]
         L.skygpu_set_stream.argtypes = [vp, cp, sz]
         L.skygpu_make_plan.argtypes = [i32, i64, i32, C.POINTER(_Plan), cp, sz]
+        L.skygpu_assign_partitions.argtypes = [vp, vp, u64, i32, C.POINTER(_Plan), vp, cp, sz]
+        L.skygpu_skyline_bnl.argtypes = [vp, vp, u64, i32, vp, vp, vp, cp, sz]
         L.skygpu_parallel_skyline.argtypes = [vp, vp, u64, i32, C.POINTER(_Plan), vp, vp, u64, i32,
                                               vp, vp, C.POINTER(Stats), cp, sz]
         L.skygpu_grid_resistance.argtypes = [vp, vp, u64, i32, C.POINTER(_Plan), u64, i32, i32, i32,
@@ -130,7 +133,7 @@ EXPORTED_SYMBOLS = ("skygpu_version", "skygpu_device_count", "skygpu_set_device"
                     "skygpu_set_collective", "skygpu_normalize", "skygpu_select_representatives",
                     "skygpu_read_csv", "skygpu_pipeline_csv", "skygpu_host_buffer",
                     "skygpu_nccl_unique_id", "skygpu_nccl_init", "skygpu_nccl_release",
-                    "skygpu_cells_step_plan")
+                    "skygpu_cells_step_plan", "skygpu_assign_partitions", "skygpu_skyline_bnl")
 
 
 def _check(rc: int, err: C.Array) -> None:
@@ -174,6 +177,18 @@ def make_plan(strategy, target_partitions: int, dims: int) -> PartitionPlan:
     return PartitionPlan(Strategy(out.strategy), out.slices, out.partitions, out.dims)
 
 
+def assign_partitions(values, plan: PartitionPlan, ids=None) -> np.ndarray:
+    """partition.hpp:90 (partition.cpp:183-213) on the device: the partition of
+    every tuple under ``plan`` (int64, one per tuple)."""
+    v, i = _relation(values, ids)
+    n, d = v.shape
+    out = np.zeros(max(n, 1), dtype=np.int64)
+    err = _errbuf()
+    _check(lib().skygpu_assign_partitions(_p(v), _p(i), n, d, C.byref(plan._c()), _p(out), err,
+                                          1024), err)
+    return out[:n]
+
+
 @dataclass
 class SkylineResult:
     positions: np.ndarray  # input positions, (sum, id) order
@@ -200,6 +215,21 @@ def parallel_skyline(values, ids=None, plan: PartitionPlan | None = None, reps=N
     _check(lib().skygpu_parallel_skyline(_p(v), _p(i), n, d, C.byref(plan._c()), _p(rv), _p(ri),
                                          rv.shape[0], int(cores), _p(out), _p(cnt), C.byref(st),
                                          err, 1024), err)
+    pos = out[: int(cnt[0])].astype(np.int64)
+    return SkylineResult(pos, i[pos], v[pos], st.as_dict())
+
+
+def skyline_bnl(values, ids=None) -> SkylineResult:
+    """core.hpp:78 skyline_bnl: the tuples no tuple dominates (a set; returned
+    in (sum, id) order)."""
+    v, i = _relation(values, ids)
+    n, d = v.shape
+    out = np.empty(max(n, 1), dtype=np.uint64)
+    cnt = np.zeros(1, dtype=np.uint64)
+    st = Stats()
+    err = _errbuf()
+    _check(lib().skygpu_skyline_bnl(_p(v), _p(i), n, d, _p(out), _p(cnt), C.byref(st), err, 1024),
+           err)
     pos = out[: int(cnt[0])].astype(np.int64)
     return SkylineResult(pos, i[pos], v[pos], st.as_dict())
 
@@ -268,10 +298,13 @@ class PipelineResult:
 def pipeline(values, ids=None, plan: PartitionPlan | None = None, cap: int | None = 25,
              engine: int = GRES_AUTO, shard_rank: int = 0, shard_world: int = 1,
              check_skyline: bool = False, skip_gres: bool = False,
-             sky_engine: int = SKY_AUTO, normalize: bool = False) -> PipelineResult:
+             sky_engine: int = SKY_AUTO, normalize: bool = False,
+             local_prune: bool = False) -> PipelineResult:
     """Skyline + grid resistance in one call (harness.cpp:208, :229-231).
     ``sky_engine`` forces the prefix-round (SKY_ROUNDS) or one-pass rank-grid
-    (SKY_GRID) skyline engine; the default picks by the first round's yield."""
+    (SKY_GRID) skyline engine; the default picks by the first round's yield.
+    ``local_prune`` runs the plan's partitions as local-skyline pruning before
+    the merge (SKY_PARTS, parallel.cpp:59-73 recast)."""
     v, i = _relation(values, ids)
     n, d = v.shape
     plan = plan or PartitionPlan(Strategy.NONE, 1, 1, d)
@@ -283,6 +316,7 @@ def pipeline(values, ids=None, plan: PartitionPlan | None = None, cap: int | Non
     err = _errbuf()
     flags = (CHECK_SKYLINE if check_skyline else 0) | (SKIP_GRES if skip_gres else 0) | int(sky_engine)
     flags |= NORMALIZE if normalize else 0
+    flags |= SKY_PARTS if local_prune else 0
     _check(lib().skygpu_pipeline(_p(v), _p(i), n, d, C.byref(plan._c()), 0 if cap is None else int(cap),
                                  int(engine), int(shard_rank), int(shard_world), flags, _p(pos), _p(den),
                                  _p(s), _p(gm), C.byref(st), err, 1024), err)

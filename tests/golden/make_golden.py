@@ -155,6 +155,27 @@ def main(which):
         # the C5 stream's 20k prefix (the reference arm's bench sample)
         gen_case("C5_prefix_20k_d7", "ant", 20000, 7, 1, strategy="angular", p=64, release=True,
                  cores=8)
+    if which in ("all", "pids"):
+        # the reference's own assign_partitions (partition.cpp:183-213) on
+        # seeded inputs: golden ids for the device assign_partitions and the
+        # oracle's restatement (one file, all cases)
+        cases = []
+        for gen, n, d, strat, p, seed in (
+                ("uni", 3000, 2, "grid", 16, 21), ("uni", 3000, 5, "grid", 64, 22),
+                ("ant", 3000, 7, "grid", 64, 23), ("lattice", 3000, 3, "grid", 64, 24),
+                ("uni", 3000, 2, "angular", 16, 31), ("ant", 3000, 3, "angular", 16, 32),
+                ("uni", 3000, 5, "angular", 64, 33), ("ant", 3000, 7, "angular", 64, 34),
+                ("lattice", 3000, 4, "angular", 81, 35),
+                ("uni", 3000, 3, "sliced", 16, 41), ("ant", 3000, 7, "sliced", 64, 42),
+                ("lattice", 3000, 2, "sliced", 7, 43), ("lattice", 3000, 5, "sliced", 100, 44),
+                ("uni", 2999, 4, "none", 1, 51)):
+            r = run(["--mode", "pids", "--gen", gen, "--n", n, "--d", d, "--seed", seed,
+                     "--strategy", strat, "--p", p])
+            cases.append(r)
+            print(f"pids {gen} n={n} d={d} {strat} p={p}: partitions={r['partitions']} "
+                  f"distinct={len(set(r.get('pids', [])))}", flush=True)
+        with gzip.open(os.path.join(HERE, "partition", "pids_cases.json.gz"), "wt") as f:
+            json.dump({"name": "pids_cases", "cases": cases}, f, separators=(",", ":"))
 
 
 if __name__ == "__main__":
