@@ -67,6 +67,19 @@ Ctx& ctx() {
 }
 
 void trace_mark(Ctx& c, const char* label) {
+    // SKYGPU_TRACE=2: synchronise and print every mark at once (localises a
+    // kernel that never returns; timings are meaningless in this mode)
+    static const bool sync_marks = [] {
+        const char* e = getenv("SKYGPU_TRACE");
+        return e && e[0] == '2';
+    }();
+    if (sync_marks) {
+        fprintf(stderr, "[skygpu mark] queued: %s\n", label);
+        fflush(stderr);
+        const cudaError_t e = cudaStreamSynchronize(c.stream);
+        fprintf(stderr, "[skygpu mark] done:   %s (%s)\n", label, cudaGetErrorString(e));
+        fflush(stderr);
+    }
     if (!c.trace || c.ntrace >= 96) return;
     c.tlabel[c.ntrace] = label;
     c.thost[c.ntrace] = std::chrono::duration<double, std::micro>(

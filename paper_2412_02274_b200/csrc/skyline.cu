@@ -983,7 +983,10 @@ k_sfs_intra_chunked(const double* __restrict__ Av, const unsigned long long* __r
             ++c;
         }
         const uint32_t i = c * kIntraChunk + 1 + (uint32_t)rem;
-        if (keep[i] == 0) continue;  // another chunk already found a dominator
+        // another chunk already found a dominator (keep[i] moves under other
+        // warps: the warp takes lane 0's reading, so no lane skips the votes
+        // below that the others wait at)
+        if (__shfl_sync(0xffffffffu, (unsigned)(keep[i] == 0), 0)) continue;
         const uint32_t j1 = min(i, (c + 1) * kIntraChunk);
         double t[D];
 #pragma unroll
@@ -1011,7 +1014,7 @@ k_sfs_intra_chunked(const double* __restrict__ Av, const unsigned long long* __r
                 dominated = true;
                 break;
             }
-            if (keep[i] == 0) break;
+            if (__shfl_sync(0xffffffffu, (unsigned)(keep[i] == 0), 0)) break;
         }
         if (dominated && lane == 0) keep[i] = 0;
     }

@@ -597,7 +597,7 @@ constexpr int kTCons = kTB / 32 - 1;
 constexpr int kStages = 4;
 constexpr int kStageCap = 256;    // codes per stage
 constexpr int kMaxPieces = 16;    // ranges per stage
-constexpr int kTabR = 129;        // table entries per attribute: codes 0..127, 128 = never
+constexpr int kTabEntries = 1280;  // table slots: >= 8 * 128 (d = 8 with whole-range codes, one copy)
 constexpr int kHitCap = 128;      // batched exact follow-ups per consumer warp
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -617,9 +617,12 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
                      smem_u32(bar))
                  : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, int tag = 0) {
     const uint32_t a = smem_u32(bar);
     uint32_t ok = 0;
+#ifdef SKYGPU_K6_WATCHDOG
+    unsigned long long spins = 0;
+#endif
     do {
         asm volatile(
             "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
@@ -627,6 +630,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
             : "=r"(ok)
             : "r"(a), "r"(parity)
             : "memory");
+#ifdef SKYGPU_K6_WATCHDOG  // debug build: name the wait that never completes
+        if (!ok && ++spins == (1ull << 24) && (threadIdx.x & 31) == 0) {
+            unsigned long long st;
+            asm volatile("ld.shared.b64 %0, [%1];" : "=l"(st) : "r"(a));
+            printf("[K6 watchdog] block %d warp %d site %d bar@%u parity %u state %llx\n",
+                   blockIdx.x, threadIdx.x >> 5, tag, a, parity, st);
+        }
+        if (!ok && spins == (1ull << 25)) __trap();
+#else
+        (void)tag;
+#endif
     } while (!ok);
 }
 // global -> shared bulk copy (16-byte aligned, size a multiple of 16),
@@ -650,9 +664,13 @@ __device__ __forceinline__ uint32_t div_rcp(uint32_t x, uint32_t b, float inv) {
 }
 
 template <int D>
-struct alignas(16) DecideSmem {
+struct alignas(128) DecideSmem {
     using W = GridWord<D>;
-    uint4 tab[D * kTabR];                 // candidate bitsets per (attribute, code)
+    // candidate bitsets per (attribute, code inside the item's code range),
+    // each entry in 2^cs adjacent copies: a lane reads copy (lane mod 2^cs), so
+    // with 8 copies the 8 lanes of a quarter-warp hit 8 different 16-byte bank
+    // groups whatever their codes — LDS.128 without bank conflicts
+    uint4 tab[kTabEntries];
     W ring[kStages][kStageCap];           // staged comparator codes
     uint32_t pslot[kStages][kMaxPieces];  // first slot of each staged range
     uint32_t ppos[kStages][kMaxPieces];   // its sorted position
@@ -665,13 +683,13 @@ struct alignas(16) DecideSmem {
 };
 
 template <int D>
-__global__ void __launch_bounds__(kTB, 8)
+__global__ void __launch_bounds__(kTB, 6)
 k_grid_decide_tma(const double* __restrict__ rec, const int64_t* __restrict__ ids,
                   const uint32_t* __restrict__ R,
                   const GridWord<D>* __restrict__ scode, const uint32_t* __restrict__ sidx,
                   const uint32_t* __restrict__ seg, const uint2* __restrict__ items,
                   unsigned* __restrict__ ctr, int k0, int k, uint8_t* __restrict__ keep,
-                  unsigned long long* __restrict__ tests) {
+                  unsigned long long* __restrict__ tests, int repl) {
     pdl_wait();
     using W = GridWord<D>;
     constexpr uint32_t kAlign = 16 / sizeof(W);  // codes per 16 bytes
@@ -693,7 +711,7 @@ k_grid_decide_tma(const double* __restrict__ rec, const int64_t* __restrict__ id
 #pragma unroll
     for (int j = 2; j < D; ++j) wj[j] = wj[j - 1] * (uint32_t)k;
     uint32_t ps = 0, pphase = 0;  // producer ring position (warp 0)
-    uint32_t cs = 0, cphase = 0;  // consumer ring position (warps 1..3)
+    uint32_t rs = 0, cphase = 0;  // consumer ring position (warps 1..3)
     unsigned long long cnt = 0, ucnt = 0;  // tests, (comparator, item) units
     for (;;) {
         if (threadIdx.x == 0) sm.item = atomicAdd(&ctr[1], 1u);
@@ -703,7 +721,13 @@ k_grid_decide_tma(const double* __restrict__ rec, const int64_t* __restrict__ id
         const uint2 item = items[it];
         const uint32_t own = item.x, first = item.y;
         const uint32_t end = min(seg[(own + 1) * k0], first + kItem);
-        // ---- candidate bitset tables: warp w builds word w of every entry
+        // ---- candidate bitset tables: warp w builds word w of every entry.
+        // Only codes inside the item's range (ilo, ihi] get an entry (a code
+        // <= ilo passes every candidate, one > ihi none); the entries of all
+        // attributes are packed back to back (toff) and replicated 2^cs times
+        // when they fit.
+        uint32_t ilo[D], ihi[D], tb[D];
+        uint32_t cs = 0;
         {
             const uint32_t q = first + threadIdx.x;
             const bool valid = q < end;
@@ -714,28 +738,58 @@ k_grid_decide_tma(const double* __restrict__ rec, const int64_t* __restrict__ id
                 const uint32_t x = (uint32_t)(cw >> (8 * j)) & 0xFFu;
                 const uint32_t lo = __reduce_min_sync(0xffffffffu, valid ? x : 255u);
                 const uint32_t hi = __reduce_max_sync(0xffffffffu, valid ? x : 0u);
-                uint32_t* T = reinterpret_cast<uint32_t*>(&sm.tab[j * kTabR]) + warp;
-                for (uint32_t r = lane; r < (uint32_t)kTabR; r += 32)
-                    if (r <= lo || r > hi) T[r * 4] = r <= lo ? vmask : 0u;
-                for (uint32_t r = lo + 1; r <= hi; ++r) {
-                    const unsigned b = __ballot_sync(0xffffffffu, valid && x >= r);
-                    if ((r & 31u) == lane) T[r * 4] = b;
-                }
                 if (lane == 0) {
                     sm.lo4[warp][j] = (uint8_t)lo;
                     sm.hi4[warp][j] = (uint8_t)hi;
                 }
             }
             if (lane == 0) sm.alive[warp] = vmask;
+            __syncthreads();
+            uint32_t tot = 0;
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                ilo[j] = min(min(sm.lo4[0][j], sm.lo4[1][j]), min(sm.lo4[2][j], sm.lo4[3][j]));
+                ihi[j] = max(max(sm.hi4[0][j], sm.hi4[1][j]), max(sm.hi4[2][j], sm.hi4[3][j]));
+                tb[j] = tot - ilo[j] - 1u;  // entry of code r: tb + r
+                tot += ihi[j] - ilo[j];
+            }
+            cs = repl == 0 ? 0u
+                 : tot * 8u <= (uint32_t)kTabEntries ? 3u
+                 : tot * 4u <= (uint32_t)kTabEntries ? 2u
+                 : tot * 2u <= (uint32_t)kTabEntries ? 1u : 0u;
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                const uint32_t x = (uint32_t)(cw >> (8 * j)) & 0xFFu;
+                uint32_t* T = reinterpret_cast<uint32_t*>(sm.tab) + warp;
+                for (uint32_t r = ilo[j] + 1; r <= ihi[j]; ++r) {
+                    const unsigned b = __ballot_sync(0xffffffffu, valid && x >= r);
+                    if ((r & 31u) == lane) T[((tb[j] + r) << cs) * 4u] = b;
+                }
+            }
+            if (cs) {
+                __syncthreads();
+                const uint32_t nc = (1u << cs) - 1u;
+                for (uint32_t e = threadIdx.x; e < tot * nc; e += kTB) {
+                    const uint32_t ent = e / nc, cpy = 1u + e - ent * nc;
+                    sm.tab[(ent << cs) + cpy] = sm.tab[ent << cs];
+                }
+            }
         }
         __syncthreads();
         if (warp == 0) {
             // ================= producer: walk the comparator ranges
             uint32_t used = 0, np = 0, nr = 0;
             bool open = false, stop = false;
+            // (the consumers clear alive bits concurrently: ONE lane reads
+            // and the warp takes its answer — lanes reading for themselves
+            // can disagree and diverge around the warp-level waits below)
             auto all_dead = [&]() {
-                const volatile uint32_t* a = sm.alive;
-                return (a[0] | a[1] | a[2] | a[3]) == 0u;
+                uint32_t x = 0;
+                if (lane == 0) {
+                    const volatile uint32_t* a = sm.alive;
+                    x = a[0] | a[1] | a[2] | a[3];
+                }
+                return __shfl_sync(0xffffffffu, x, 0) == 0u;
             };
             auto close = [&](bool fin) {
                 if (lane == 0) {
@@ -759,7 +813,7 @@ k_grid_decide_tma(const double* __restrict__ rec, const int64_t* __restrict__ id
                             stop = true;
                             break;
                         }
-                        mbar_wait(&sm.empty[ps], pphase ^ 1u);
+                        mbar_wait(&sm.empty[ps], pphase ^ 1u, 1);
                         used = np = nr = 0;
                         open = true;
                     }
@@ -825,43 +879,54 @@ k_grid_decide_tma(const double* __restrict__ rec, const int64_t* __restrict__ id
                 }
             }
             if (!open) {  // an empty stage carries the end marker
-                mbar_wait(&sm.empty[ps], pphase ^ 1u);
+                mbar_wait(&sm.empty[ps], pphase ^ 1u, 2);
                 used = np = nr = 0;
             }
             close(true);
         } else {
             // ================= consumers: test staged comparators
             const uint32_t cw = warp - 1;
-            // the item's code range per attribute: a comparator code <= lo
-            // passes every candidate on that attribute (the entry would be
-            // all-ones: no table read), one above hi passes none (no read,
-            // the comparator is out) — only codes inside (lo, hi] are looked
-            // up.  Comparators from rows strictly below the item's in an
+            // the item's code range per attribute (ilo, ihi above): a
+            // comparator code <= ilo passes every candidate on that attribute
+            // (no table read), one above ihi passes none (no read, the
+            // comparator is out) — only codes inside (ilo, ihi] are looked up.
+            // Comparators from rows strictly below the item's in an
             // attribute's coarse bin never need that attribute's table.
-            uint32_t ilo[D], ihi[D];
-#pragma unroll
-            for (int j = 0; j < D; ++j) {
-                ilo[j] = min(min(sm.lo4[0][j], sm.lo4[1][j]), min(sm.lo4[2][j], sm.lo4[3][j]));
-                ihi[j] = max(max(sm.hi4[0][j], sm.hi4[1][j]), max(sm.hi4[2][j], sm.hi4[3][j]));
-            }
+            const uint32_t lsel = lane & ((1u << cs) - 1u);
             for (;;) {
-                mbar_wait(&sm.full[cs], cphase);
-                const uint32_t n = sm.nslot[cs];
-                const bool fin = sm.last[cs] != 0u;
-                const volatile uint32_t* av = sm.alive;
-                uint32_t al[4] = {av[0], av[1], av[2], av[3]};
+                mbar_wait(&sm.full[rs], cphase, 3);
+                const uint32_t n = sm.nslot[rs];
+                const bool fin = sm.last[rs] != 0u;
+                // the alive masks change under the other consumer warps'
+                // atomicAnd while this warp's lanes leave the wait one by one:
+                // lane 0 reads them and broadcasts, so that the whole warp
+                // takes the same branch around the warp-level votes below
+                // (lanes reading for themselves could see "all dead" and
+                // "one alive" in the same stage and wait for each other at
+                // different warp barriers for ever)
+                uint32_t al[4] = {0u, 0u, 0u, 0u};
+                __syncwarp();
+                if (lane == 0) {
+                    const volatile uint32_t* av = sm.alive;
+                    al[0] = av[0];
+                    al[1] = av[1];
+                    al[2] = av[2];
+                    al[3] = av[3];
+                }
+#pragma unroll
+                for (int w = 0; w < 4; ++w) al[w] = __shfl_sync(0xffffffffu, al[w], 0);
                 if ((al[0] | al[1] | al[2] | al[3]) != 0u) {
                     if (cw == 0 && lane == 0) {
-                        cnt += (unsigned long long)sm.nreal[cs] *
+                        cnt += (unsigned long long)sm.nreal[rs] *
                                (__popc(al[0]) + __popc(al[1]) + __popc(al[2]) + __popc(al[3]));
-                        ucnt += sm.nreal[cs];
+                        ucnt += sm.nreal[rs];
                     }
                     uint2* hb = sm.hits[cw];
                     for (uint32_t s0 = cw * 32; s0 < n; s0 += 32 * kTCons) {
                         const uint32_t s = s0 + lane;
                         uint4 m = make_uint4(0u, 0u, 0u, 0u);
                         if (s < n) {
-                            const W c = sm.ring[cs][s];
+                            const W c = sm.ring[rs][s];
                             bool out = false;
 #pragma unroll
                             for (int j = 0; j < D; ++j)
@@ -872,7 +937,7 @@ k_grid_decide_tma(const double* __restrict__ rec, const int64_t* __restrict__ id
                                 for (int j = 0; j < D; ++j) {
                                     const uint32_t cj = (uint32_t)(c >> (8 * j)) & 0xFFu;
                                     if (cj > ilo[j]) {
-                                        const uint4 e = sm.tab[j * kTabR + cj];
+                                        const uint4 e = sm.tab[((tb[j] + cj) << cs) + lsel];
                                         m.x &= e.x;
                                         m.y &= e.y;
                                         m.z &= e.z;
@@ -889,9 +954,9 @@ k_grid_decide_tma(const double* __restrict__ rec, const int64_t* __restrict__ id
                         uint32_t qs = 0, nb = 0;
                         if (hit) {
                             uint32_t pi = 0;
-                            const uint32_t npc = sm.npiece[cs];
-                            while (pi + 1 < npc && sm.pslot[cs][pi + 1] <= s) ++pi;
-                            qs = sm.ppos[cs][pi] + (s - sm.pslot[cs][pi]);
+                            const uint32_t npc = sm.npiece[rs];
+                            while (pi + 1 < npc && sm.pslot[rs][pi + 1] <= s) ++pi;
+                            qs = sm.ppos[rs][pi] + (s - sm.pslot[rs][pi]);
                             nb = __popc(m.x) + __popc(m.y) + __popc(m.z) + __popc(m.w);
                         }
                         uint32_t incl = nb;
@@ -936,9 +1001,9 @@ k_grid_decide_tma(const double* __restrict__ rec, const int64_t* __restrict__ id
                     }
                 }
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&sm.empty[cs]);
-                if (++cs == kStages) {
-                    cs = 0;
+                if (lane == 0) mbar_arrive(&sm.empty[rs]);
+                if (++rs == kStages) {
+                    rs = 0;
                     cphase ^= 1u;
                 }
                 if (fin) break;
@@ -1043,6 +1108,12 @@ void sky_grid_decide(Ctx& c, const double* d_vals, int d, const unsigned long lo
             const char* e = getenv("SKYGPU_GRID_KERNEL");
             return e && e[0] == 'a';
         }();
+        // K6's candidate tables in up to 8 bank-staggered copies (default;
+        // SKYGPU_K6_REPL=0: one copy, for A/B measurement)
+        static const int k6_repl = [] {
+            const char* e = getenv("SKYGPU_K6_REPL");
+            return e && e[0] == '0' ? 0 : 1;
+        }();
         double* rec = alu ? nullptr : c.buf[B_GREC].as<double>(r * (D + 1));
         if (atomic_bucket) {
             pdl_launch(k_rank_codes<D>, grid_for(r, kGB, c.num_sms * 8), kGB, 0, c.stream,
@@ -1110,7 +1181,7 @@ void sky_grid_decide(Ctx& c, const double* d_vals, int d, const unsigned long lo
         else
             pdl_launch(k_grid_decide_tma<D>, c.num_sms * per_sm, kTB, 0, c.stream,
                 (const double*)rec, d_ids, R, scode, sidx, seg, items, ctr, g.k0, g.k, keep,
-                c.d_slots + S_TESTS_SKY);
+                c.d_slots + S_TESTS_SKY, k6_repl);
         SKY_LAUNCH_CHECK();
         SKY_CUDA(cudaEventRecord(c.ev[15], c.stream));
         note_launch(c);

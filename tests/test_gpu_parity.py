@@ -331,6 +331,26 @@ def test_grid_engine_ties_and_unsorted_ids():
         assert sorted(r2.positions.tolist()) == sorted(po.skyline_sfs(v2, np.array([0, 1]))[0].tolist())
 
 
+@pytest.mark.timeout(120)
+@pytest.mark.parametrize("gen,n,d", [("uni", 90000, 3), ("corr", 40000, 4), ("uni", 250000, 2),
+                                     ("uni", 120000, 5)])
+def test_grid_engine_items_that_die_at_once(gen, n, d):
+    """Dense dominance (tiny skylines): nearly every K6 item loses all of its
+    candidates within a stage or two, so the consumer warps' "everything dead"
+    early-outs and the producer's stop run constantly.  Round 2 found a
+    deadlock exactly there (lanes of one warp read the shared alive masks for
+    themselves, disagreed, and waited at different warp barriers:
+    profiles/r02_k6_deadlock_gdb.txt) — the masks are now read once per warp.
+    Repeated: the interleaving differs from run to run."""
+    v = sk.generate(gen, n, d, 11)
+    ids = 7 + 5 * np.arange(n, dtype=np.int64)
+    pos, _ = po.skyline_sfs(v, ids)
+    for _ in range(6):
+        res = sk.pipeline(v, ids, skip_gres=True, sky_engine=sk.SKY_GRID)
+        assert res.stats["sky_engine"] == sk.SKY_GRID
+        assert res.positions.tolist() == pos.tolist()
+
+
 @pytest.mark.parametrize("n", [200_000, 1_000_000])
 def test_grid_engine_auto_on_large_skyline(n):
     """C5-style data (skyline ~ input) switches to the rank grid after round 1;
