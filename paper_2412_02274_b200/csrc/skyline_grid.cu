@@ -597,7 +597,7 @@ constexpr int kTCons = kTB / 32 - 1;
 constexpr int kStages = 4;
 constexpr int kStageCap = 256;    // codes per stage
 constexpr int kMaxPieces = 16;    // ranges per stage
-constexpr int kTabEntries = 1280;  // table slots: >= 8 * 128 (d = 8 with whole-range codes, one copy)
+constexpr int kTabR = 129;        // table entries per attribute: codes 0..127, 128 = never
 constexpr int kHitCap = 128;      // batched exact follow-ups per consumer warp
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -617,7 +617,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
                      smem_u32(bar))
                  : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, int tag = 0) {
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, int site = 0) {
     const uint32_t a = smem_u32(bar);
     uint32_t ok = 0;
 #ifdef SKYGPU_K6_WATCHDOG
@@ -630,16 +630,16 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, int ta
             : "=r"(ok)
             : "r"(a), "r"(parity)
             : "memory");
-#ifdef SKYGPU_K6_WATCHDOG  // debug build: name the wait that never completes
+#ifdef SKYGPU_K6_WATCHDOG  // debug build: name the wait that never completes, then trap
         if (!ok && ++spins == (1ull << 24) && (threadIdx.x & 31) == 0) {
             unsigned long long st;
             asm volatile("ld.shared.b64 %0, [%1];" : "=l"(st) : "r"(a));
             printf("[K6 watchdog] block %d warp %d site %d bar@%u parity %u state %llx\n",
-                   blockIdx.x, threadIdx.x >> 5, tag, a, parity, st);
+                   blockIdx.x, threadIdx.x >> 5, site, a, parity, st);
         }
         if (!ok && spins == (1ull << 25)) __trap();
 #else
-        (void)tag;
+        (void)site;
 #endif
     } while (!ok);
 }
@@ -664,13 +664,9 @@ __device__ __forceinline__ uint32_t div_rcp(uint32_t x, uint32_t b, float inv) {
 }
 
 template <int D>
-struct alignas(128) DecideSmem {
+struct alignas(16) DecideSmem {
     using W = GridWord<D>;
-    // candidate bitsets per (attribute, code inside the item's code range),
-    // each entry in 2^cs adjacent copies: a lane reads copy (lane mod 2^cs), so
-    // with 8 copies the 8 lanes of a quarter-warp hit 8 different 16-byte bank
-    // groups whatever their codes — LDS.128 without bank conflicts
-    uint4 tab[kTabEntries];
+    uint4 tab[D * kTabR];                 // candidate bitsets per (attribute, code)
     W ring[kStages][kStageCap];           // staged comparator codes
     uint32_t pslot[kStages][kMaxPieces];  // first slot of each staged range
     uint32_t ppos[kStages][kMaxPieces];   // its sorted position
@@ -683,13 +679,13 @@ struct alignas(128) DecideSmem {
 };
 
 template <int D>
-__global__ void __launch_bounds__(kTB, 6)
+__global__ void __launch_bounds__(kTB, 8)
 k_grid_decide_tma(const double* __restrict__ rec, const int64_t* __restrict__ ids,
                   const uint32_t* __restrict__ R,
                   const GridWord<D>* __restrict__ scode, const uint32_t* __restrict__ sidx,
                   const uint32_t* __restrict__ seg, const uint2* __restrict__ items,
                   unsigned* __restrict__ ctr, int k0, int k, uint8_t* __restrict__ keep,
-                  unsigned long long* __restrict__ tests, int repl) {
+                  unsigned long long* __restrict__ tests) {
     pdl_wait();
     using W = GridWord<D>;
     constexpr uint32_t kAlign = 16 / sizeof(W);  // codes per 16 bytes
@@ -711,7 +707,7 @@ k_grid_decide_tma(const double* __restrict__ rec, const int64_t* __restrict__ id
 #pragma unroll
     for (int j = 2; j < D; ++j) wj[j] = wj[j - 1] * (uint32_t)k;
     uint32_t ps = 0, pphase = 0;  // producer ring position (warp 0)
-    uint32_t rs = 0, cphase = 0;  // consumer ring position (warps 1..3)
+    uint32_t cs = 0, cphase = 0;  // consumer ring position (warps 1..3)
     unsigned long long cnt = 0, ucnt = 0;  // tests, (comparator, item) units
     for (;;) {
         if (threadIdx.x == 0) sm.item = atomicAdd(&ctr[1], 1u);
@@ -721,13 +717,7 @@ k_grid_decide_tma(const double* __restrict__ rec, const int64_t* __restrict__ id
         const uint2 item = items[it];
         const uint32_t own = item.x, first = item.y;
         const uint32_t end = min(seg[(own + 1) * k0], first + kItem);
-        // ---- candidate bitset tables: warp w builds word w of every entry.
-        // Only codes inside the item's range (ilo, ihi] get an entry (a code
-        // <= ilo passes every candidate, one > ihi none); the entries of all
-        // attributes are packed back to back (toff) and replicated 2^cs times
-        // when they fit.
-        uint32_t ilo[D], ihi[D], tb[D];
-        uint32_t cs = 0;
+        // ---- candidate bitset tables: warp w builds word w of every entry
         {
             const uint32_t q = first + threadIdx.x;
             const bool valid = q < end;
@@ -738,42 +728,19 @@ k_grid_decide_tma(const double* __restrict__ rec, const int64_t* __restrict__ id
                 const uint32_t x = (uint32_t)(cw >> (8 * j)) & 0xFFu;
                 const uint32_t lo = __reduce_min_sync(0xffffffffu, valid ? x : 255u);
                 const uint32_t hi = __reduce_max_sync(0xffffffffu, valid ? x : 0u);
+                uint32_t* T = reinterpret_cast<uint32_t*>(&sm.tab[j * kTabR]) + warp;
+                for (uint32_t r = lane; r < (uint32_t)kTabR; r += 32)
+                    if (r <= lo || r > hi) T[r * 4] = r <= lo ? vmask : 0u;
+                for (uint32_t r = lo + 1; r <= hi; ++r) {
+                    const unsigned b = __ballot_sync(0xffffffffu, valid && x >= r);
+                    if ((r & 31u) == lane) T[r * 4] = b;
+                }
                 if (lane == 0) {
                     sm.lo4[warp][j] = (uint8_t)lo;
                     sm.hi4[warp][j] = (uint8_t)hi;
                 }
             }
             if (lane == 0) sm.alive[warp] = vmask;
-            __syncthreads();
-            uint32_t tot = 0;
-#pragma unroll
-            for (int j = 0; j < D; ++j) {
-                ilo[j] = min(min(sm.lo4[0][j], sm.lo4[1][j]), min(sm.lo4[2][j], sm.lo4[3][j]));
-                ihi[j] = max(max(sm.hi4[0][j], sm.hi4[1][j]), max(sm.hi4[2][j], sm.hi4[3][j]));
-                tb[j] = tot - ilo[j] - 1u;  // entry of code r: tb + r
-                tot += ihi[j] - ilo[j];
-            }
-            cs = repl == 0 ? 0u
-                 : tot * 8u <= (uint32_t)kTabEntries ? 3u
-                 : tot * 4u <= (uint32_t)kTabEntries ? 2u
-                 : tot * 2u <= (uint32_t)kTabEntries ? 1u : 0u;
-#pragma unroll
-            for (int j = 0; j < D; ++j) {
-                const uint32_t x = (uint32_t)(cw >> (8 * j)) & 0xFFu;
-                uint32_t* T = reinterpret_cast<uint32_t*>(sm.tab) + warp;
-                for (uint32_t r = ilo[j] + 1; r <= ihi[j]; ++r) {
-                    const unsigned b = __ballot_sync(0xffffffffu, valid && x >= r);
-                    if ((r & 31u) == lane) T[((tb[j] + r) << cs) * 4u] = b;
-                }
-            }
-            if (cs) {
-                __syncthreads();
-                const uint32_t nc = (1u << cs) - 1u;
-                for (uint32_t e = threadIdx.x; e < tot * nc; e += kTB) {
-                    const uint32_t ent = e / nc, cpy = 1u + e - ent * nc;
-                    sm.tab[(ent << cs) + cpy] = sm.tab[ent << cs];
-                }
-            }
         }
         __syncthreads();
         if (warp == 0) {
@@ -886,17 +853,22 @@ k_grid_decide_tma(const double* __restrict__ rec, const int64_t* __restrict__ id
         } else {
             // ================= consumers: test staged comparators
             const uint32_t cw = warp - 1;
-            // the item's code range per attribute (ilo, ihi above): a
-            // comparator code <= ilo passes every candidate on that attribute
-            // (no table read), one above ihi passes none (no read, the
-            // comparator is out) — only codes inside (ilo, ihi] are looked up.
-            // Comparators from rows strictly below the item's in an
+            // the item's code range per attribute: a comparator code <= lo
+            // passes every candidate on that attribute (the entry would be
+            // all-ones: no table read), one above hi passes none (no read,
+            // the comparator is out) — only codes inside (lo, hi] are looked
+            // up.  Comparators from rows strictly below the item's in an
             // attribute's coarse bin never need that attribute's table.
-            const uint32_t lsel = lane & ((1u << cs) - 1u);
+            uint32_t ilo[D], ihi[D];
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                ilo[j] = min(min(sm.lo4[0][j], sm.lo4[1][j]), min(sm.lo4[2][j], sm.lo4[3][j]));
+                ihi[j] = max(max(sm.hi4[0][j], sm.hi4[1][j]), max(sm.hi4[2][j], sm.hi4[3][j]));
+            }
             for (;;) {
-                mbar_wait(&sm.full[rs], cphase, 3);
-                const uint32_t n = sm.nslot[rs];
-                const bool fin = sm.last[rs] != 0u;
+                mbar_wait(&sm.full[cs], cphase, 3);
+                const uint32_t n = sm.nslot[cs];
+                const bool fin = sm.last[cs] != 0u;
                 // the alive masks change under the other consumer warps'
                 // atomicAnd while this warp's lanes leave the wait one by one:
                 // lane 0 reads them and broadcasts, so that the whole warp
@@ -917,16 +889,16 @@ k_grid_decide_tma(const double* __restrict__ rec, const int64_t* __restrict__ id
                 for (int w = 0; w < 4; ++w) al[w] = __shfl_sync(0xffffffffu, al[w], 0);
                 if ((al[0] | al[1] | al[2] | al[3]) != 0u) {
                     if (cw == 0 && lane == 0) {
-                        cnt += (unsigned long long)sm.nreal[rs] *
+                        cnt += (unsigned long long)sm.nreal[cs] *
                                (__popc(al[0]) + __popc(al[1]) + __popc(al[2]) + __popc(al[3]));
-                        ucnt += sm.nreal[rs];
+                        ucnt += sm.nreal[cs];
                     }
                     uint2* hb = sm.hits[cw];
                     for (uint32_t s0 = cw * 32; s0 < n; s0 += 32 * kTCons) {
                         const uint32_t s = s0 + lane;
                         uint4 m = make_uint4(0u, 0u, 0u, 0u);
                         if (s < n) {
-                            const W c = sm.ring[rs][s];
+                            const W c = sm.ring[cs][s];
                             bool out = false;
 #pragma unroll
                             for (int j = 0; j < D; ++j)
@@ -937,7 +909,7 @@ k_grid_decide_tma(const double* __restrict__ rec, const int64_t* __restrict__ id
                                 for (int j = 0; j < D; ++j) {
                                     const uint32_t cj = (uint32_t)(c >> (8 * j)) & 0xFFu;
                                     if (cj > ilo[j]) {
-                                        const uint4 e = sm.tab[((tb[j] + cj) << cs) + lsel];
+                                        const uint4 e = sm.tab[j * kTabR + cj];
                                         m.x &= e.x;
                                         m.y &= e.y;
                                         m.z &= e.z;
@@ -954,9 +926,9 @@ k_grid_decide_tma(const double* __restrict__ rec, const int64_t* __restrict__ id
                         uint32_t qs = 0, nb = 0;
                         if (hit) {
                             uint32_t pi = 0;
-                            const uint32_t npc = sm.npiece[rs];
-                            while (pi + 1 < npc && sm.pslot[rs][pi + 1] <= s) ++pi;
-                            qs = sm.ppos[rs][pi] + (s - sm.pslot[rs][pi]);
+                            const uint32_t npc = sm.npiece[cs];
+                            while (pi + 1 < npc && sm.pslot[cs][pi + 1] <= s) ++pi;
+                            qs = sm.ppos[cs][pi] + (s - sm.pslot[cs][pi]);
                             nb = __popc(m.x) + __popc(m.y) + __popc(m.z) + __popc(m.w);
                         }
                         uint32_t incl = nb;
@@ -1001,9 +973,9 @@ k_grid_decide_tma(const double* __restrict__ rec, const int64_t* __restrict__ id
                     }
                 }
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&sm.empty[rs]);
-                if (++rs == kStages) {
-                    rs = 0;
+                if (lane == 0) mbar_arrive(&sm.empty[cs]);
+                if (++cs == kStages) {
+                    cs = 0;
                     cphase ^= 1u;
                 }
                 if (fin) break;
@@ -1108,12 +1080,6 @@ void sky_grid_decide(Ctx& c, const double* d_vals, int d, const unsigned long lo
             const char* e = getenv("SKYGPU_GRID_KERNEL");
             return e && e[0] == 'a';
         }();
-        // K6's candidate tables in up to 8 bank-staggered copies (default;
-        // SKYGPU_K6_REPL=0: one copy, for A/B measurement)
-        static const int k6_repl = [] {
-            const char* e = getenv("SKYGPU_K6_REPL");
-            return e && e[0] == '0' ? 0 : 1;
-        }();
         double* rec = alu ? nullptr : c.buf[B_GREC].as<double>(r * (D + 1));
         if (atomic_bucket) {
             pdl_launch(k_rank_codes<D>, grid_for(r, kGB, c.num_sms * 8), kGB, 0, c.stream,
@@ -1181,7 +1147,7 @@ void sky_grid_decide(Ctx& c, const double* d_vals, int d, const unsigned long lo
         else
             pdl_launch(k_grid_decide_tma<D>, c.num_sms * per_sm, kTB, 0, c.stream,
                 (const double*)rec, d_ids, R, scode, sidx, seg, items, ctr, g.k0, g.k, keep,
-                c.d_slots + S_TESTS_SKY, k6_repl);
+                c.d_slots + S_TESTS_SKY);
         SKY_LAUNCH_CHECK();
         SKY_CUDA(cudaEventRecord(c.ev[15], c.stream));
         note_launch(c);
