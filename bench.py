@@ -439,7 +439,13 @@ def roofline(st, sky_ms, gres_ms, d, clk, workload="C2"):
                     "tests_per_step": st["skyline_tests"], "kernel_ms_per_step": ms,
                     "launches_per_step": launches, "bytes_smem_per_unit": 16 * d,
                     "smem_bytes_per_clk_sm": 128, "f_clk_mhz": f / 1e6,
-                    "dominance_tests_per_s": st["skyline_tests"] / (ms / 1e3) / 1e9 if ms > 0 else 0.0}
+                    "dominance_tests_per_s": st["skyline_tests"] / (ms / 1e3) / 1e9 if ms > 0 else 0.0,
+                    # the (live candidate, comparator) decisions against what a
+                    # per-pair SWAR kernel could do at best (3 ALU ops per test
+                    # on the 64-lane ALU pipe, the round-1 k_grid_decide model)
+                    "compare_roofline_equiv": {
+                        "peak_gtests_s": 148 * f * 64 / 3.0 / 1e9,
+                        "frac": (st["skyline_tests"] / (ms / 1e3)) / (148 * f * 64 / 3.0) if ms > 0 else 0.0}}
         if kind == "skyline" and st["sky_engine"] == 16:  # rank-grid engine (skyline_grid.cu)
             tests, ms, launches = st["skyline_tests"], sky_ms, st["sky_kernel_launches"]
             i_test, l_pipe = 3, 64  # IADD3 + LOP3 + VIMNMX on the ALU pipe (+ IMAD.X, FMA pipe)

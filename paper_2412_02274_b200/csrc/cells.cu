@@ -1398,9 +1398,11 @@ bool gres_cells_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_ma
                     } else {
                         pdl_launch(k_mg_fill, grid_for(geo.bytes / 16, kBlock), kBlock, 0,
                                    c.stream, (uint4*)M, geo.bytes / 16, n_in);
-                        static const bool load_first = [] {  // SKYGPU_MG_LOADFIRST=0: CAS first
+                        // SKYGPU_MG_LOADFIRST=1: an L2 load before the CAS (measured
+                        // on C5: gres 6.54 ms against 6.40 ms CAS-first — off)
+                        static const bool load_first = [] {
                             const char* e = getenv("SKYGPU_MG_LOADFIRST");
-                            return !(e && e[0] == '0');
+                            return e && e[0] == '1';
                         }();
                         if (load_first)
                             pdl_launch(k_mg_mark<CW, true>, gs, kBlock, 0, c.stream, cg, S, geo, M,
