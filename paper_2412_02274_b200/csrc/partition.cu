@@ -316,15 +316,31 @@ k_local_filter(const double* __restrict__ v, uint64_t n, int d,
                const int32_t* __restrict__ pid, const uint8_t* __restrict__ mask,
                const double* __restrict__ wv, const unsigned long long* __restrict__ wkey,
                const long long* __restrict__ wtie, const uint32_t* __restrict__ wcnt,
-               uint8_t* __restrict__ keep, unsigned long long* __restrict__ tests) {
+               uint8_t* __restrict__ keep, unsigned long long* __restrict__ tests,
+               uint32_t sample, unsigned long long* __restrict__ slots) {
     pdl_wait();
     const int dd = D > 0 ? D : d;
     constexpr int DA = D > 0 ? D : kMaxDims;
     unsigned long long ntest = 0;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-         i += (uint64_t)gridDim.x * blockDim.x) {
+    // sample > 0: the probe pass — every sample-th tuple, counted in
+    // S_LPS_N / S_LPS_HIT, keep untouched.  sample == 0: the full pass; when
+    // the probe saw the windows dominate under a quarter of its tuples (a
+    // skyline-heavy relation: C5 loses 3 % of its tuples to 64 partitions'
+    // windows for 37 ms of scans) nothing is pruned here and the merge engine
+    // decides everything — pruning any subset is valid.
+    const uint64_t step = sample ? sample : 1;
+    const uint64_t cnt = (n + step - 1) / step;
+    const bool idle = !sample && slots[S_LPS_HIT] * 4 < slots[S_LPS_N];
+    unsigned long long nprobe = 0, nhit = 0;
+    for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < cnt;
+         q += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t i = q * step;
         if (mask && !mask[i]) {
-            keep[i] = 0;
+            if (!sample) keep[i] = 0;
+            continue;
+        }
+        if (idle) {
+            keep[i] = 1;
             continue;
         }
         const uint32_t p = (uint32_t)pid[i];
@@ -353,9 +369,18 @@ k_local_filter(const double* __restrict__ v, uint64_t n, int d,
                 break;
             }
         }
-        keep[i] = !dom;
+        if (sample) {
+            ++nprobe;
+            nhit += dom;
+        } else {
+            keep[i] = !dom;
+        }
     }
     add_count(tests, ntest);
+    if (sample) {
+        add_count(slots + S_LPS_N, nprobe);
+        add_count(slots + S_LPS_HIT, nhit);
+    }
 }
 
 template <class KT>
@@ -506,10 +531,28 @@ uint64_t local_prune_device(Ctx& c, const double* d_vals, const unsigned long lo
                    (const uint32_t*)cur, (const uint32_t*)wpos, wv, wkey, wtie, wcnt,
                    c.d_slots + S_TESTS_SKY);
         SKY_LAUNCH_CHECK();
+        // probe (every probe-th tuple, ~8k of them), then the full pass gated
+        // on the probe's yield (SKYGPU_LOCAL_PROBE=0: always the full pass)
+        static const bool probe_on = [] {
+            const char* e = getenv("SKYGPU_LOCAL_PROBE");
+            return !(e && e[0] == '0');
+        }();
+        const uint32_t probe = probe_on && n >= (1u << 18) ? (uint32_t)(n >> 13) : 0u;
+        SKY_CUDA(cudaMemsetAsync(c.d_slots + S_LPS_N, 0, 2 * sizeof(unsigned long long),
+                                 c.stream));
+        if (probe) {
+            pdl_launch(k_local_filter<D>, grid_for((n + probe - 1) / probe, kPBlock), kPBlock, 0,
+                       c.stream, d_vals, n, d, keys, tie_ids, (const int32_t*)pid, mask,
+                       (const double*)wv, (const unsigned long long*)wkey,
+                       (const long long*)wtie, (const uint32_t*)wcnt, keep,
+                       c.d_slots + S_TESTS_SKY, probe, c.d_slots);
+            SKY_LAUNCH_CHECK();
+            note_launch(c);
+        }
         pdl_launch(k_local_filter<D>, gb, kPBlock, 0, c.stream, d_vals, n, d, keys, tie_ids,
                    (const int32_t*)pid, mask, (const double*)wv,
                    (const unsigned long long*)wkey, (const long long*)wtie,
-                   (const uint32_t*)wcnt, keep, c.d_slots + S_TESTS_SKY);
+                   (const uint32_t*)wcnt, keep, c.d_slots + S_TESTS_SKY, 0u, c.d_slots);
         SKY_LAUNCH_CHECK();
     });
     note_launch(c, 2);

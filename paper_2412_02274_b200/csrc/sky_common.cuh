@@ -130,7 +130,9 @@ enum Slot {
     S_IDSBAD = 19,     // 1: ids that arrived late were not strictly increasing, redo
     S_LIVE0 = 20,      // cell engine: undecided candidates after a step (ping-pong)
     S_LIVE1 = 21,
-    S_COUNT_ = 22
+    S_LPS_N = 22,      // local pruning: sampled tuples / those the windows dominate
+    S_LPS_HIT = 23,
+    S_COUNT_ = 24
 };
 
 struct Ctx {
