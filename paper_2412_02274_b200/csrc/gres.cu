@@ -268,11 +268,12 @@ k_gres_pairs_tiled(const W* __restrict__ codes, uint32_t S, int G, int g_max,
 #pragma unroll
         for (int c = 0; c < kCandPerWarp; ++c) {
             if (((valid >> c) & 1) && best[c] < g) best[c] = max(best[c], vden[t[c]]);
-            // (den moves under other blocks' atomicMax: the warp takes lane
-            // 0's reading, so that every lane leaves the scan loops together)
-            best[c] = __shfl_sync(0xffffffffu, best[c], 0);
             if (best[c] < g) alive |= 1u << c;
         }
+        // (den moves under other blocks' atomicMax, so lanes may have read
+        // different values: the warp takes lane 0's alive mask — every lane
+        // must leave the scan loops and their warp votes together)
+        alive = __shfl_sync(0xffffffffu, alive, 0);
         if (!__syncthreads_or(alive != 0)) break;
         const W* cg = codes + (uint64_t)gi * S;
         W tc[kCandPerWarp], tg[kCandPerWarp];
@@ -355,8 +356,6 @@ k_gres_pairs_resident(const W* __restrict__ codes, uint32_t S, int G, int g_max,
         const uint32_t idx = blockIdx.x * kResCand + warp * kCandPerWarp + c;
         t[c] = idx < na ? act[idx] : 0;
         best[c] = idx < na ? vden[t[c]] : 0x7fffffff;
-        // (den moves under other blocks' atomicMax: one reading per warp)
-        best[c] = __shfl_sync(0xffffffffu, best[c], 0);
     }
     unsigned long long cnt = 0;
     for (int gi = 0; gi < G; ++gi) {
@@ -365,6 +364,10 @@ k_gres_pairs_resident(const W* __restrict__ codes, uint32_t S, int G, int g_max,
 #pragma unroll
         for (int c = 0; c < kCandPerWarp; ++c)
             if (best[c] < g) alive |= 1u << c;
+        // (den moves under other blocks' atomicMax, so lanes may have read
+        // different values: the warp takes lane 0's alive mask — every lane
+        // must leave the scan loop and its ballots together)
+        alive = __shfl_sync(0xffffffffu, alive, 0);
         if (!alive) break;
         W tc[kCandPerWarp], tg[kCandPerWarp];
         int nb[kCandPerWarp];
@@ -373,7 +376,6 @@ k_gres_pairs_resident(const W* __restrict__ codes, uint32_t S, int G, int g_max,
             tc[c] = cand[gi * kResCand + warp * kCandPerWarp + c];
             tg[c] = tc[c] | H;
             nb[c] = ((alive >> c) & 1) ? vden[t[c]] : best[c];  // consumed after the scan
-            nb[c] = __shfl_sync(0xffffffffu, nb[c], 0);
         }
         const W* cg = comp + (size_t)gi * rl;
         // branch-free inner loop: every lane tests its comparator against all
