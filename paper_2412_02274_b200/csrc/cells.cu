@@ -1398,12 +1398,18 @@ bool gres_cells_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_ma
                     } else {
                         pdl_launch(k_mg_fill, grid_for(geo.bytes / 16, kBlock), kBlock, 0,
                                    c.stream, (uint4*)M, geo.bytes / 16, n_in);
-                        // SKYGPU_MG_LOADFIRST=1: an L2 load before the CAS (measured
-                        // on C5: gres 6.54 ms against 6.40 ms CAS-first — off)
-                        static const bool load_first = [] {
-                            const char* e = getenv("SKYGPU_MG_LOADFIRST");
-                            return e && e[0] == '1';
+                        // an L2 load before the CAS for the small grids (up to
+                        // SKYGPU_MG_LOADFIRST_MB, default 4 MB: many tuples per
+                        // cell, most of them lower nothing — the load spares the
+                        // serialised same-address atomics); CAS first for the
+                        // large ones, where the load would be a second DRAM trip
+                        // (C5 gres: always 6.54 ms, never 6.41 ms, <= 4 MB 6.27 ms)
+                        static const uint64_t lf_bytes = [] {
+                            const char* e = getenv("SKYGPU_MG_LOADFIRST_MB");
+                            const double mb = e ? atof(e) : 4.0;
+                            return (uint64_t)(mb * 1048576.0);
                         }();
+                        const bool load_first = geo.bytes <= lf_bytes;
                         if (load_first)
                             pdl_launch(k_mg_mark<CW, true>, gs, kBlock, 0, c.stream, cg, S, geo, M,
                                        n_in);
