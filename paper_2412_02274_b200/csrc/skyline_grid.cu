@@ -583,7 +583,7 @@ k_grid_decide(const double* __restrict__ v, const unsigned long long* __restrict
 //    instead of 128 SWAR tests.
 //  * TMA bulk staging.  Warp 0 of the CTA is a producer: it walks the same
 //    comparator ranges (own chunk, own row, then every row <= the item's
-//    row) and streams them with cp.async.bulk into a 4-stage shared-memory
+//    row) and streams them with cp.async.bulk into a 3-stage (3 x 384 codes) shared-memory
 //    ring (mbarrier complete_tx); warps 1..3 consume stages.  Ranges are
 //    copied at 16-byte granularity, so up to one code on either side of a
 //    range is an extra comparator — harmless: the predecessor rule may test
@@ -594,11 +594,28 @@ k_grid_decide(const double* __restrict__ v, const unsigned long long* __restrict
 // ---------------------------------------------------------------------------
 constexpr int kTB = 128;          // threads: warp 0 producer, warps 1..3 consumers
 constexpr int kTCons = kTB / 32 - 1;
-constexpr int kStages = 4;
-constexpr int kStageCap = 256;    // codes per stage
-constexpr int kMaxPieces = 16;    // ranges per stage
+// (compile-time knobs: scripts/build_k6_variant.sh NAME -DSKY_K6_...=.. builds a
+// variant beside the in-tree library for same-box timing, scripts/gpu_k6_variants.sh.
+// Measured on C5, 8 CTAs/SM each: 4 x 256 codes 5.89 ms, 3 x 384 5.51 ms, 2 x 576
+// 5.53 ms, 4 x 288 5.64 ms, 6 x 192 5.95 ms, 4 x 320 (7 CTAs/SM) 6.19 ms — long
+// stages matter more than many; 384 = 4 full rounds of the 3 consumer warps.)
+#ifndef SKY_K6_STAGES
+#define SKY_K6_STAGES 3
+#endif
+#ifndef SKY_K6_STAGE_CAP
+#define SKY_K6_STAGE_CAP 384
+#endif
+#ifndef SKY_K6_MAX_PIECES
+#define SKY_K6_MAX_PIECES 24
+#endif
+constexpr int kStages = SKY_K6_STAGES;
+constexpr int kStageCap = SKY_K6_STAGE_CAP;    // codes per stage
+constexpr int kMaxPieces = SKY_K6_MAX_PIECES;  // ranges per stage
 constexpr int kTabR = 129;        // table entries per attribute: codes 0..127, 128 = never
-constexpr int kHitCap = 128;      // batched exact follow-ups per consumer warp
+#ifndef SKY_K6_HIT_CAP
+#define SKY_K6_HIT_CAP 128
+#endif
+constexpr int kHitCap = SKY_K6_HIT_CAP;  // batched exact follow-ups per consumer warp
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
