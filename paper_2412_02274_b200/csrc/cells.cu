@@ -598,6 +598,45 @@ __global__ void k_mg_mark_reduce(const uint32_t* __restrict__ stage, uint32_t ns
     }
 }
 
+// mid-size grids: marks into a u32-per-cell copy with the native one-way
+// atomicMin (RED.MIN: no value returns, no CAS retry loop under contention),
+// then packed to the byte grid.  The copy is 4 x the grid: only worth it while
+// it stays in L2.
+__global__ void k_mg_fill32(uint4* __restrict__ p, uint64_t n16, const unsigned long long* live) {
+    pdl_wait();
+    if (step_dead(live)) return;
+    const uint4 f = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n16;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        p[i] = f;
+}
+
+template <class CW>
+__global__ void __launch_bounds__(kBlock)
+k_mg_mark32(const CW* __restrict__ code, uint64_t S, MinGeom geo, uint32_t* __restrict__ G,
+            const unsigned long long* live) {
+    pdl_wait();
+    if (step_dead(live)) return;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < S;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const CW w = code[i];
+        const uint64_t r = mg_row(w, geo);
+        const uint32_t c0 = (uint32_t)(w >> (8 * geo.m)) & 0xFFu;
+        atomicMin(&G[r], 2u * c0 + 1u);
+    }
+}
+
+__global__ void k_mg_pack(const uint4* __restrict__ G, uint64_t nwords, uint32_t* __restrict__ M,
+                          const unsigned long long* live) {
+    pdl_wait();
+    if (step_dead(live)) return;
+    for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < nwords;
+         q += (uint64_t)gridDim.x * blockDim.x) {
+        const uint4 g = G[q];
+        M[q] = g.x | (g.y << 8) | (g.z << 16) | (g.w << 24);
+    }
+}
+
 // prefix minimum along the 4 bytes of a word (byte k = lower address first),
 // then against the previous word's last byte
 __device__ __forceinline__ uint32_t bytes_prefix_min(uint32_t x, uint32_t carry) {
@@ -1364,6 +1403,20 @@ bool gres_cells_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_ma
             in = nullptr;  // the identity over sorted positions
             swept += S * (uint64_t)d * 8 * 2 + S * 24;
         }
+        // marks through a u32 copy of the grid while the copy stays small (see
+        // k_mg_mark32; SKYGPU_MG_RED_MB = the copy's size limit, 0 = never;
+        // C5 gres: never 6.26 ms, 16 MB 6.16, 64 MB 6.09, 128 MB 6.14, 256 MB
+        // 6.53, always 7.61).  (B_MGVALS holds the permuted values of the
+        // locality order otherwise)
+        static const uint64_t red_bytes = [] {
+            const char* e = getenv("SKYGPU_MG_RED_MB");
+            const double mb = e ? atof(e) : 64.0;
+            return (uint64_t)(mb * 1048576.0);
+        }();
+        uint32_t* G32 = nullptr;
+        if (red_bytes && vals == d_skyv)
+            G32 = static_cast<uint32_t*>(
+                c.buf[B_MGVALS].get(std::min<uint64_t>(red_bytes, top.bytes * 4)));
         for (size_t s0 = 0; s0 < steps.size(); s0 += chunk) {
             StepList sl;
             sl.n = (int)std::min<uint64_t>(chunk, steps.size() - s0);
@@ -1386,7 +1439,7 @@ bool gres_cells_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_ma
                     (uint32_t)c.num_sms * (geo.bytes * 4 <= 48 * 1024 ? 4u : 1u);
                 const unsigned gs = grid_for(S, kBlock);
                 const unsigned gq = grid_for(na, kBlock);
-                int nl = 0;
+                int nl = 0, nl_extra = 0;
                 auto run = [&](auto* cg) {
                     using CW = std::remove_const_t<std::remove_pointer_t<decltype(cg)>>;
                     if (priv) {
@@ -1395,6 +1448,14 @@ bool gres_cells_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_ma
                         pdl_launch(k_mg_mark_reduce, grid_for(geo.bytes / 4, kBlock), kBlock, 0,
                                    c.stream, (const uint32_t*)stage, nslots,
                                    (uint32_t)(geo.bytes / 4), (uint32_t*)M, n_in);
+                    } else if (G32 && geo.bytes * 4 <= red_bytes) {
+                        uint32_t* G = G32;
+                        pdl_launch(k_mg_fill32, grid_for(geo.bytes / 4, kBlock), kBlock, 0,
+                                   c.stream, (uint4*)G, geo.bytes / 4, n_in);
+                        pdl_launch(k_mg_mark32<CW>, gs, kBlock, 0, c.stream, cg, S, geo, G, n_in);
+                        pdl_launch(k_mg_pack, grid_for(geo.bytes / 4, kBlock), kBlock, 0, c.stream,
+                                   (const uint4*)G, geo.bytes / 4, (uint32_t*)M, n_in);
+                        ++nl_extra;
                     } else {
                         pdl_launch(k_mg_fill, grid_for(geo.bytes / 16, kBlock), kBlock, 0,
                                    c.stream, (uint4*)M, geo.bytes / 16, n_in);
@@ -1426,7 +1487,7 @@ bool gres_cells_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_ma
                 else
                     run((const unsigned long long*)codes + (uint64_t)li * S);
                 SKY_LAUNCH_CHECK();
-                note_launch(c, 4 + nl);
+                note_launch(c, 4 + nl + nl_extra);
                 // algorithmic bytes of the step: the grid filled, read and
                 // written once by an ideal fused prefix minimum, plus the
                 // mark and query reads of the S code words
