@@ -197,8 +197,9 @@ __global__ void k_gather_codes(const uint32_t* __restrict__ sidx, uint32_t r,
         scode[q] = code[sidx[q]];
 }
 
-// each tuple's exact record in cell order: its D float64 values and its
-// sum key, (D + 1) doubles at rec[pos * (D + 1)] — the TMA decide kernel's
+// each tuple's exact record in cell order: its D float64 values at
+// rec[pos * (D + 1)] (stride D + 1 doubles: 64-byte records for D = 7; the
+// sum key is recomputed by exact_rec when it matters) — the TMA decide kernel's
 // exact follow-up then reads one contiguous record per side instead of
 // chasing sidx -> R -> values and keys.  Gathered (writes coalesced, the
 // 64-byte reads random) after the scatter.
@@ -213,13 +214,12 @@ __global__ void k_gather_rec(const uint32_t* __restrict__ sidx, uint32_t r,
         const uint32_t i = sidx[q];
         if (code) scode[q] = code[i];
         const uint64_t p = R ? R[i] : i;
-        double x[D + 1];
+        double x[D];
 #pragma unroll
         for (int j = 0; j < D; ++j) x[j] = v[p * D + j];
-        x[D] = __longlong_as_double((long long)key[p]);
-        double* o = rec + (uint64_t)q * (D + 1);
+        double* o = rec + (uint64_t)q * (D + 1);  // (slot D unused: 64-byte records for D = 7)
 #pragma unroll
-        for (int j = 0; j <= D; ++j) o[j] = x[j];
+        for (int j = 0; j < D; ++j) o[j] = x[j];
     }
 }
 
@@ -314,15 +314,25 @@ __device__ __forceinline__ bool exact_rec(const double* __restrict__ rec,
                                           uint32_t qt) {
     const double* a = rec + (uint64_t)qs * (D + 1);
     const double* b = rec + (uint64_t)qt * (D + 1);
-    double s[D + 1], t[D + 1];
+    double s[D], t[D];
 #pragma unroll
-    for (int j = 0; j <= D; ++j) {
+    for (int j = 0; j < D; ++j) {
         s[j] = a[j];
         t[j] = b[j];
     }
     if (!dom_f64<D>(s, t)) return false;
-    const unsigned long long ks = (unsigned long long)__double_as_longlong(s[D]);
-    const unsigned long long kt = (unsigned long long)__double_as_longlong(t[D]);
+    // the (sum, id) precedence only matters when the float64 sums tie
+    // (dominance implies sum(s) <= sum(t)): the sums are recomputed here, for
+    // the few confirmed dominances, exactly as K1 computes the keys
+    // (left-to-right __dadd_rn from 0.0, ord_bits) — the records carry no key,
+    // which spares the gather a random 8-byte read per tuple
+    double ss = 0.0, st = 0.0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+        ss = __dadd_rn(ss, s[j]);
+        st = __dadd_rn(st, t[j]);
+    }
+    const unsigned long long ks = ord_bits(ss), kt = ord_bits(st);
     if (ks != kt) return ks < kt;  // dominance implies ks <= kt
     const uint32_t is = sidx[qs], it = sidx[qt];
     const uint64_t ps = R ? R[is] : is, pt = R ? R[it] : it;
