@@ -76,7 +76,8 @@ print(bad)
                                  {"SKYGPU_MG_PAIRSMEM": "1"}, {"SKYGPU_MG_LOADFIRST_MB": "100000"},
                                  {"SKYGPU_MG_NOPRIV": "1", "SKYGPU_MG_LOADFIRST_MB": "0"},
                                  {"SKYGPU_MG_RED_MB": "0"}, {"SKYGPU_MG_RED_MB": "100000"},
-                                 {"SKYGPU_MG_RED_MB": "100000", "SKYGPU_MG_NOPRIV": "1"}])
+                                 {"SKYGPU_MG_RED_MB": "100000", "SKYGPU_MG_NOPRIV": "1"},
+                                 {"SKYGPU_MG_PRIV_CELLS": "40960", "SKYGPU_MG_RED_MB": "0"}])
 def test_cell_engine_variants(env):
     """The HBM cell engine's alternatives against the pair engine's map:
     SKYGPU_CELLS_BITSET=1 the u32/u64 bitset-row form (the min-grid form is
