@@ -509,8 +509,12 @@ __device__ __forceinline__ uint64_t mg_row(CW w, const MinGeom& geo) {
     return r;
 }
 
-__global__ void k_mg_fill(uint4* __restrict__ p, uint64_t n16, const unsigned long long* live) {
+// (`clear`: the step's undecided counter, zeroed here — before the step's
+// query appends to it — instead of by a one-thread launch of its own)
+__global__ void k_mg_fill(uint4* __restrict__ p, uint64_t n16, const unsigned long long* live,
+                          unsigned long long* clear) {
     pdl_wait();
+    if (clear && blockIdx.x == 0 && threadIdx.x == 0) *clear = 0;
     if (step_dead(live)) return;
     const uint4 f = make_uint4(kEmpty4, kEmpty4, kEmpty4, kEmpty4);
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n16;
@@ -564,8 +568,9 @@ constexpr uint32_t kPrivCells = 40960;
 template <class CW>
 __global__ void __launch_bounds__(kBlock)
 k_mg_mark_priv(const CW* __restrict__ code, uint64_t S, MinGeom geo, uint32_t* __restrict__ stage,
-               const unsigned long long* live) {
+               const unsigned long long* live, unsigned long long* clear) {
     pdl_wait();
+    if (clear && blockIdx.x == 0 && threadIdx.x == 0) *clear = 0;
     if (step_dead(live)) return;
     extern __shared__ uint32_t cm[];
     const uint32_t ncells = (uint32_t)geo.bytes;
@@ -602,8 +607,10 @@ __global__ void k_mg_mark_reduce(const uint32_t* __restrict__ stage, uint32_t ns
 // atomicMin (RED.MIN: no value returns, no CAS retry loop under contention),
 // then packed to the byte grid.  The copy is 4 x the grid: only worth it while
 // it stays in L2.
-__global__ void k_mg_fill32(uint4* __restrict__ p, uint64_t n16, const unsigned long long* live) {
+__global__ void k_mg_fill32(uint4* __restrict__ p, uint64_t n16, const unsigned long long* live,
+                            unsigned long long* clear) {
     pdl_wait();
+    if (clear && blockIdx.x == 0 && threadIdx.x == 0) *clear = 0;
     if (step_dead(live)) return;
     const uint4 f = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n16;
@@ -1433,7 +1440,6 @@ bool gres_cells_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_ma
             for (int li = 0; li < sl.n; ++li) {
                 MinGeom geo;
                 min_geometry(amax, d, sl.g[li], 16ull << 30, &geo);
-                pdl_launch(k_clear_slot_c, 1, 1, 0, c.stream, cnt[cur]);
                 // (SKYGPU_MG_PRIV_CELLS: the privatised range, at most kPrivCells;
                 // the u32 RED marks take over above it.  C5 gres: 40960 cells
                 // 6.09 ms, 20000 (g <= 4) 6.03, 2000 6.20, none 6.78)
@@ -1452,21 +1458,21 @@ bool gres_cells_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_ma
                     using CW = std::remove_const_t<std::remove_pointer_t<decltype(cg)>>;
                     if (priv) {
                         pdl_launch(k_mg_mark_priv<CW>, nslots, kBlock, (size_t)geo.bytes * 4,
-                                   c.stream, cg, S, geo, stage, n_in);
+                                   c.stream, cg, S, geo, stage, n_in, cnt[cur]);
                         pdl_launch(k_mg_mark_reduce, grid_for(geo.bytes / 4, kBlock), kBlock, 0,
                                    c.stream, (const uint32_t*)stage, nslots,
                                    (uint32_t)(geo.bytes / 4), (uint32_t*)M, n_in);
                     } else if (G32 && geo.bytes * 4 <= red_bytes) {
                         uint32_t* G = G32;
                         pdl_launch(k_mg_fill32, grid_for(geo.bytes / 4, kBlock), kBlock, 0,
-                                   c.stream, (uint4*)G, geo.bytes / 4, n_in);
+                                   c.stream, (uint4*)G, geo.bytes / 4, n_in, cnt[cur]);
                         pdl_launch(k_mg_mark32<CW>, gs, kBlock, 0, c.stream, cg, S, geo, G, n_in);
                         pdl_launch(k_mg_pack, grid_for(geo.bytes / 4, kBlock), kBlock, 0, c.stream,
                                    (const uint4*)G, geo.bytes / 4, (uint32_t*)M, n_in);
                         ++nl_extra;
                     } else {
                         pdl_launch(k_mg_fill, grid_for(geo.bytes / 16, kBlock), kBlock, 0,
-                                   c.stream, (uint4*)M, geo.bytes / 16, n_in);
+                                   c.stream, (uint4*)M, geo.bytes / 16, n_in, cnt[cur]);
                         // an L2 load before the CAS for the small grids (up to
                         // SKYGPU_MG_LOADFIRST_MB, default 4 MB: many tuples per
                         // cell, most of them lower nothing — the load spares the
@@ -1495,7 +1501,7 @@ bool gres_cells_device(Ctx& c, const double* d_skyv, uint64_t S, int d, int g_ma
                 else
                     run((const unsigned long long*)codes + (uint64_t)li * S);
                 SKY_LAUNCH_CHECK();
-                note_launch(c, 4 + nl + nl_extra);
+                note_launch(c, 3 + nl + nl_extra);
                 // algorithmic bytes of the step: the grid filled, read and
                 // written once by an ideal fused prefix minimum, plus the
                 // mark and query reads of the S code words
