@@ -39,6 +39,7 @@ def _run(env, *extra):
                                  {"SKYGPU_PREFIX": "1500", "SKYGPU_SOLO": "4",
                                   "SKYGPU_DIR_PER_CELL": "32"},
                                  {"SKYGPU_IDS_LATE": "0"}, {"SKYGPU_GRID_SORT": "1"},
+                                 {"SKYGPU_GRID_RECSCATTER": "0"},
                                  {"SKYGPU_GRID_ROW": "128",
                                                             "SKYGPU_GRID_K0": "16"}])
 def test_env_variant_matches_goldens(env):
