@@ -1081,8 +1081,14 @@ static int min_sweeps(Ctx& c, uint8_t* M, const MinGeom& geo, const unsigned lon
             const uint32_t eb = geo.ext[j + 1];
             if (ea <= 8)
                 pdl_launch(k_mg_pair<8>, gp, kBlock, 0, c.stream, W, real_words, ea, eb, sa, live);
+            else if (ea <= 12)
+                pdl_launch(k_mg_pair<12>, gp, kBlock, 0, c.stream, W, real_words, ea, eb, sa, live);
             else if (ea <= 16)
                 pdl_launch(k_mg_pair<16>, gp, kBlock, 0, c.stream, W, real_words, ea, eb, sa, live);
+            else if (ea <= 20)
+                pdl_launch(k_mg_pair<20>, gp, kBlock, 0, c.stream, W, real_words, ea, eb, sa, live);
+            else if (ea <= 26)  // (cap 25: extents up to 26)
+                pdl_launch(k_mg_pair<26>, gp, kBlock, 0, c.stream, W, real_words, ea, eb, sa, live);
             else
                 pdl_launch(k_mg_pair<32>, gp, kBlock, 0, c.stream, W, real_words, ea, eb, sa, live);
             j += 2;
