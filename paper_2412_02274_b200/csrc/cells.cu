@@ -733,6 +733,7 @@ k_mg_slab(uint32_t* __restrict__ M, uint64_t nwords, uint32_t w0, uint32_t e1, u
 // the current one is swept.
 constexpr int kColPer = 20;  // slab words per thread (slab <= 5120 words)
 
+template <int PER>  // slab words per thread (PER * kBlock >= slab words)
 __global__ void __launch_bounds__(kBlock)
 k_mg_slabcol(uint32_t* __restrict__ M, uint32_t ncols, uint32_t w0, uint32_t e1, uint32_t e2,
              uint32_t e3, const unsigned long long* live) {
@@ -743,15 +744,15 @@ k_mg_slabcol(uint32_t* __restrict__ M, uint32_t ncols, uint32_t w0, uint32_t e1,
     uint32_t* run = sw + slab;
     for (uint32_t col = blockIdx.x; col < ncols; col += gridDim.x) {
         uint32_t* base = M + (uint64_t)col * e3 * slab;
-        uint32_t pre[kColPer];
+        uint32_t pre[PER];
 #pragma unroll
-        for (int k = 0; k < kColPer; ++k) {
+        for (int k = 0; k < PER; ++k) {
             const uint32_t i = threadIdx.x + k * kBlock;
             pre[k] = i < slab ? base[i] : kEmpty4;
         }
         for (uint32_t c3 = 0; c3 < e3; ++c3) {
 #pragma unroll
-            for (int k = 0; k < kColPer; ++k) {
+            for (int k = 0; k < PER; ++k) {
                 const uint32_t i = threadIdx.x + k * kBlock;
                 if (i < slab) sw[i] = pre[k];
             }
@@ -759,7 +760,7 @@ k_mg_slabcol(uint32_t* __restrict__ M, uint32_t ncols, uint32_t w0, uint32_t e1,
             if (c3 + 1 < e3) {
                 const uint32_t* nx = base + (uint64_t)(c3 + 1) * slab;
 #pragma unroll
-                for (int k = 0; k < kColPer; ++k) {
+                for (int k = 0; k < PER; ++k) {
                     const uint32_t i = threadIdx.x + k * kBlock;
                     pre[k] = i < slab ? nx[i] : kEmpty4;
                 }
@@ -1039,7 +1040,11 @@ static int min_sweeps(Ctx& c, uint8_t* M, const MinGeom& geo, const unsigned lon
         SKY_CUDA(cudaFuncSetAttribute(k_mg_slab<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSlabMax));
         SKY_CUDA(cudaFuncSetAttribute(k_mg_slab<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSlabMax));
         SKY_CUDA(cudaFuncSetAttribute(k_mg_slab<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSlabMax));
-        SKY_CUDA(cudaFuncSetAttribute(k_mg_slabcol, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSlabMax));
+        SKY_CUDA(cudaFuncSetAttribute(k_mg_slabcol<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSlabMax));
+        SKY_CUDA(cudaFuncSetAttribute(k_mg_slabcol<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSlabMax));
+        SKY_CUDA(cudaFuncSetAttribute(k_mg_slabcol<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSlabMax));
+        SKY_CUDA(cudaFuncSetAttribute(k_mg_slabcol<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSlabMax));
+        SKY_CUDA(cudaFuncSetAttribute(k_mg_slabcol<kColPer>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSlabMax));
         SKY_CUDA(cudaFuncSetAttribute(k_mg_pair_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)kPairSmemMax));
         attr_set = true;
@@ -1049,8 +1054,23 @@ static int min_sweeps(Ctx& c, uint8_t* M, const MinGeom& geo, const unsigned lon
     if (!nocol && sd == 3 && geo.nd >= 4 && slab / 4 <= (uint64_t)kColPer * kBlock) {
         const uint32_t e3 = geo.ext[3];
         const uint64_t ncols = nslabs / e3;
-        pdl_launch(k_mg_slabcol, grid_for(ncols, 1, c.num_sms * 8), kBlock, (size_t)2 * slab,
-                   c.stream, W, (uint32_t)ncols, w0, e1, e2, e3, live);
+        const uint64_t per = (slab / 4 + kBlock - 1) / kBlock;  // words per thread
+        const unsigned gc = grid_for(ncols, 1, c.num_sms * 8);
+        if (per <= 4)
+            pdl_launch(k_mg_slabcol<4>, gc, kBlock, (size_t)2 * slab, c.stream, W, (uint32_t)ncols,
+                       w0, e1, e2, e3, live);
+        else if (per <= 8)
+            pdl_launch(k_mg_slabcol<8>, gc, kBlock, (size_t)2 * slab, c.stream, W, (uint32_t)ncols,
+                       w0, e1, e2, e3, live);
+        else if (per <= 12)
+            pdl_launch(k_mg_slabcol<12>, gc, kBlock, (size_t)2 * slab, c.stream, W,
+                       (uint32_t)ncols, w0, e1, e2, e3, live);
+        else if (per <= 16)
+            pdl_launch(k_mg_slabcol<16>, gc, kBlock, (size_t)2 * slab, c.stream, W,
+                       (uint32_t)ncols, w0, e1, e2, e3, live);
+        else
+            pdl_launch(k_mg_slabcol<kColPer>, gc, kBlock, (size_t)2 * slab, c.stream, W,
+                       (uint32_t)ncols, w0, e1, e2, e3, live);
         j = 4;
     } else {
         const uint32_t spb = (uint32_t)std::max<uint64_t>(1, (kSlabMax / 2) / slab);
