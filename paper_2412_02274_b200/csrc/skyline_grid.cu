@@ -747,6 +747,7 @@ struct alignas(16) DecideSmem {
     uint32_t alive[4];
     uint32_t item;
     uint8_t lo4[4][8], hi4[4][8];         // each warp's candidate code range per attribute
+    uint8_t binlo[132];                   // first code of coarse bin b (b <= k), 128 beyond
     uint2 hits[kTCons][kHitCap];          // a consumer warp's code passes, tested in parallel
 };
 
@@ -771,6 +772,9 @@ k_grid_decide_tma(const double* __restrict__ rec, const int64_t* __restrict__ id
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
+    // first code of every coarse bin: bin(c) = (c * k) >> 7 (k_rank_codes)
+    for (uint32_t b = threadIdx.x; b < 132; b += blockDim.x)
+        sm.binlo[b] = (uint8_t)min(128u, (b * 128u + (uint32_t)k - 1u) / (uint32_t)k);
     __syncthreads();
     const uint32_t nitems = ctr[0];
     uint32_t wj[D];
@@ -795,13 +799,25 @@ k_grid_decide_tma(const double* __restrict__ rec, const int64_t* __restrict__ id
             const bool valid = q < end;
             const W cw = valid ? scode[q] : (W)0;
             const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+            // the item's candidates share one row: on attributes 1.. their codes
+            // lie in ONE coarse bin, and only entries inside the item's code
+            // range are ever read (the consumers' predicates) — so a warp fills
+            // its word for that bin's codes only (attribute 0, whose fine bins
+            // an item spans, and grids of < 4 bins keep the whole range)
+            const W c0w = scode[first];
 #pragma unroll
             for (int j = 0; j < D; ++j) {
                 const uint32_t x = (uint32_t)(cw >> (8 * j)) & 0xFFu;
                 const uint32_t lo = __reduce_min_sync(0xffffffffu, valid ? x : 255u);
                 const uint32_t hi = __reduce_max_sync(0xffffffffu, valid ? x : 0u);
                 uint32_t* T = reinterpret_cast<uint32_t*>(&sm.tab[j * kTabR]) + warp;
-                for (uint32_t r = lane; r < (uint32_t)kTabR; r += 32)
+                uint32_t flo = 0, fhi = (uint32_t)kTabR - 1u;
+                if (j >= 1 && k >= 4) {
+                    const uint32_t b = ((((uint32_t)(c0w >> (8 * j)) & 0xFFu)) * (uint32_t)k) >> 7;
+                    flo = sm.binlo[b];
+                    fhi = sm.binlo[b + 1];
+                }
+                for (uint32_t r = flo + lane; r <= fhi; r += 32)
                     if (r <= lo || r > hi) T[r * 4] = r <= lo ? vmask : 0u;
                 for (uint32_t r = lo + 1; r <= hi; ++r) {
                     const unsigned b = __ballot_sync(0xffffffffu, valid && x >= r);
