@@ -418,7 +418,7 @@ def roofline(st, sky_ms, gres_ms, d, clk, workload="C2"):
             return {"bound": "hbm", "kernel": "min-grid cell engine (k_mg_*, k_cells_codes)",
                     "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "GB/s",
                     "frac": achieved / peak, "traffic": tr,
-                    "traffic_unit": "B/call, all cell-engine kernels (ncu dram read+write, profiles/r02_launches_C5_v5.md)",
+                    "traffic_unit": "B/call, all cell-engine kernels (ncu dram read+write, profiles/r02_launches_C5_v6.md)",
                     "algorithmic_bytes_per_step": byts, "kernel_ms_per_step": ms,
                     "launches_per_step": st["gres_kernel_launches"],
                     "bytes_model": "codes: S*d*8 B read + S*8 B per scanned step written; per step: the "
